@@ -1,0 +1,185 @@
+/*
+ * hsseig_b200 — C ABI of the B200 (sm_100a) divide-and-conquer merge step.
+ *
+ * Drop-in for the merge-path functions of the reference package `hsseig`
+ * (arXiv 1510.04591 reference, pkg/src/hsseig).  Every entry point takes
+ * DEVICE pointers owned by the caller (PyTorch tensors in the Python host
+ * layer), plain integer sizes and a cudaStream_t passed as `void *`.
+ * Nothing here allocates or frees caller memory.  All arrays are float64,
+ * C-contiguous (row-major) unless a leading dimension says otherwise.
+ *
+ * Calls are asynchronous on `stream`.  The return value reports argument
+ * and launch errors only; numerical failures the reference raises as
+ * exceptions are written to a caller-provided device status block and read
+ * by the host once the stream is synchronised (see hsseig_status).
+ */
+#ifndef HSSEIG_B200_H
+#define HSSEIG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return / status codes */
+#define HSSEIG_OK 0
+#define HSSEIG_ERR_ARG 1          /* ValueError */
+#define HSSEIG_ERR_BRACKET 2      /* SecularConvergenceError, secular.py:25,172-179 */
+#define HSSEIG_ERR_RADICAND 3     /* WeightRecomputationError, secular.py:29,226-230 */
+#define HSSEIG_ERR_CUDA 4
+
+/*
+ * Device status block written by the kernels (int64 x 8):
+ *   [0] total secular iterations     [1] first root with gamma<=0 (or k)
+ *   [2] first root with mu<=0 (or k) [3] first bad Loewner radicand (or k)
+ *   [4] HSS saturated-ID count       [5] max ID rank used (r_used)
+ *   [6], [7] reserved
+ */
+typedef struct hsseig_status {
+  int64_t v[8];
+} hsseig_status;
+
+/* Library identification (build check). */
+const char *hsseig_version(void);
+int hsseig_status_init(hsseig_status *status_dev, int64_t k, void *stream);
+
+/*
+ * (a1) All k secular roots with gap pairs.
+ * Replaces secular_all (pkg/src/hsseig/_kernels.pyx:178-234) behind
+ * solve_secular (pkg/src/hsseig/secular.py:159-180).
+ * d: k strictly ascending poles; z: k nonzero weights; rho > 0.
+ * lam/gamma/mu: k outputs; iters: k per-root iteration counts (int32).
+ * work: >= 2*k + 64 doubles of device scratch.
+ * status[0] += total iterations; status[1]/[2] = first bracket loss.
+ */
+int hsseig_secular(const double *d, const double *z, int64_t k, double rho, double *lam,
+                   double *gamma, double *mu, int32_t *iters, double *work,
+                   hsseig_status *status, void *stream);
+
+/*
+ * (a3) Virtual-pole extension dnext[j] = d[j+1], dnext[k-1] = d[k-1]+gamma+mu
+ * (pkg/src/hsseig/secular.py:195-199).  Needed by every Cauchy entry.
+ */
+int hsseig_dnext(const double *d, const double *gamma, const double *mu, int64_t k,
+                 double *dnext, void *stream);
+
+/*
+ * (a4) Loewner recomputation of the weights.
+ * Replaces recompute_weights (pkg/src/hsseig/secular.py:206-236).
+ * status[3] = first index with a non-positive / non-finite radicand.
+ */
+int hsseig_loewner(const double *d, const double *dnext, const double *gamma,
+                   const double *mu, const double *z, int64_t k, double rho, double *zhat,
+                   hsseig_status *status, void *stream);
+
+/*
+ * (a5) Column normalizers v_j = 1/||zhat ./ (d - lam_j)||.
+ * Replaces column_normalizers (pkg/src/hsseig/secular.py:239-250).
+ */
+int hsseig_normalizers(const double *d, const double *dnext, const double *gamma,
+                       const double *mu, const double *zhat, int64_t k, double *v,
+                       void *stream);
+
+/* Generators of the Cauchy-like matrix (pkg/src/hsseig/cauchy.py:15-38); device pointers. */
+typedef struct hsseig_gen {
+  const double *d, *dnext, *gamma, *mu, *zhat, *v;
+  int64_t k;
+} hsseig_gen;
+
+/*
+ * (a6) Dense block C[rows, cols] -> out (nr x nc, leading dim ldo).
+ * Replaces CauchyEvecMatrix.block (pkg/src/hsseig/cauchy.py:48-56).
+ * rows/cols: int64 device index arrays.
+ */
+int hsseig_cauchy_block(const hsseig_gen *gen, const int64_t *rows, int64_t nr,
+                        const int64_t *cols, int64_t nc, double *out, int64_t ldo,
+                        void *stream);
+
+/*
+ * (a7) Randomized sampling Y = C @ Omega and Z = C^T @ Omega with C generated
+ * tile by tile in shared memory and contracted on FP64 DMMA.
+ * Replaces CauchyEvecMatrix.multiply / transpose_multiply (cauchy.py:70-100).
+ * Omega: k x w (ld = ldom).  Y, Z: k x w (ld = ldy).
+ * work: hsseig_sample_work_doubles(k, w) doubles (split-K partials).
+ */
+int64_t hsseig_sample_work_doubles(int64_t k, int64_t w);
+int hsseig_cauchy_sample(const hsseig_gen *gen, const double *omega, int64_t ldom, int64_t w,
+                         double *Y, double *Z, int64_t ldy, double *work, void *stream);
+
+/*
+ * HSS tree (pkg/src/hsseig/hss.py:151-214): nodes in the reference's postorder
+ * numbering over a power-of-two leaf count.  Topology arrays are filled by the
+ * host (hsseig_tree_layout); numeric slots by hsseig_hss_build_rand.
+ * Slot layout (all row-major, leading dimension `ws`):
+ *   U, V : n_nodes slots of pmax x ws (p rows used, rank columns used)
+ *   B    : n_nodes slots of ws x ws   (rU(node) x rV(sibling))
+ *   D    : n_leaves slots of mmax x mmax (leading dimension mmax)
+ *   rsel, csel, rloc, cloc : n_nodes x ws int32
+ */
+typedef struct hsseig_tree {
+  int32_t k, n_leaves, depth, n_nodes, w, ws, pmax, mmax;
+  /* device topology, indexed by postorder node id */
+  const int32_t *lo, *hi, *left, *right;
+  const int32_t *level_nodes; /* node ids ordered by (level, position), level 1..depth */
+  const int32_t *level_off;   /* host-side copy is level_off_h */
+  int32_t level_off_h[33];    /* offsets into level_nodes for levels 0..depth (+1) */
+  int32_t root;
+  /* device numeric slots */
+  int32_t *rU, *rV, *rsel, *csel, *rloc, *cloc, *flags;
+  double *U, *V, *B, *D, *rres, *cres;
+  /* construction scratch (device) */
+  double *M;      /* 2 * n_leaves * pmax * ws : matrices handed to the ID */
+  double *psel;   /* n_nodes * ws * ws : selected rows of Phi */
+  double *tsel;   /* n_nodes * ws * ws : selected rows of Theta */
+  double *ycomp;  /* n_nodes * ws * ws : V^T Omega compressions */
+  double *zcomp;  /* n_nodes * ws * ws : U^T Omega compressions */
+} hsseig_tree;
+
+/* bytes of device memory hsseig_tree_layout carves for one tree */
+int64_t hsseig_tree_bytes(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax);
+/*
+ * Fill `tree` with pointers carved from `dev_mem` (hsseig_tree_bytes) and copy the
+ * topology for leaf boundaries `bounds_h` (host, n_leaves+1 ints) to the device.
+ */
+int hsseig_tree_layout(hsseig_tree *tree, const int32_t *bounds_h, int32_t n_leaves, int32_t w,
+                       void *dev_mem, void *stream);
+
+/*
+ * (a10, a11) Randomized HSS construction, Algorithm 2 (pkg/src/hsseig/hss.py:217-306):
+ * leaf D / Phi / Theta formation, batched column-pivoted-QR interpolative
+ * decompositions (dgeqp3 + dtrtrs semantics, hss.py:120-148) level by level,
+ * skeleton B blocks regenerated from the generators.
+ * Y, Z: sampled blocks (ld = ldy); omega (ld = ldom); w = r + p.
+ * status[4] = saturated-ID count (tree flagged), status[5] = r_used.
+ */
+int hsseig_hss_build_rand(const hsseig_gen *gen, const double *omega, int64_t ldom,
+                          const double *Y, const double *Z, int64_t ldy, double id_tol,
+                          hsseig_tree *tree, hsseig_status *status, void *stream);
+
+/*
+ * (a12) Structured product out = X @ H (Algorithm 3; pkg/src/hsseig/hss.py:309-361).
+ * X: P x k (ld = ldx), out: P x k (ld = ldo), row-major.
+ * work: hsseig_matmul_work_doubles(P, tree) doubles.
+ */
+int64_t hsseig_matmul_work_doubles(int64_t P, const hsseig_tree *tree);
+int hsseig_hss_matmul_right(const double *X, int64_t ldx, int64_t P, const hsseig_tree *tree,
+                            double *out, int64_t ldo, double *work, void *stream);
+
+/*
+ * (a14) Dense update out = Qb @ C with C generated on the fly (fallback path).
+ * Replaces update_vectors_dense(Qblock, C.to_dense()) (pkg/src/hsseig/dc.py:132-138).
+ */
+int hsseig_dense_update(const double *Qb, int64_t ldq, int64_t P, const hsseig_gen *gen,
+                        double *out, int64_t ldo, void *stream);
+
+/* Plain batched helper used by tests/bench: out = A @ B (P x K)(K x N), FP64 DMMA. */
+int hsseig_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                int64_t ldc, int64_t M, int64_t N, int64_t K, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HSSEIG_B200_H */

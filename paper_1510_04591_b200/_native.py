@@ -1,0 +1,125 @@
+"""ctypes binding of libhsseig_b200.so (the C ABI declared in include/hsseig_b200.h).
+
+There is no CPU fallback: importing the compute entry points without the built
+library, or calling them without a CUDA device, raises immediately.
+"""
+import ctypes
+import os
+
+import torch
+
+from . import build as _build
+
+_LIB = None
+
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+
+HSSEIG_OK = 0
+HSSEIG_ERR_ARG = 1
+HSSEIG_ERR_BRACKET = 2
+HSSEIG_ERR_RADICAND = 3
+HSSEIG_ERR_CUDA = 4
+
+
+class Gen(ctypes.Structure):
+    """hsseig_gen"""
+    _fields_ = [("d", c_vp), ("dnext", c_vp), ("gamma", c_vp), ("mu", c_vp), ("zhat", c_vp),
+                ("v", c_vp), ("k", c_i64)]
+
+
+class Tree(ctypes.Structure):
+    """hsseig_tree"""
+    _fields_ = [("k", c_i32), ("n_leaves", c_i32), ("depth", c_i32), ("n_nodes", c_i32),
+                ("w", c_i32), ("ws", c_i32), ("pmax", c_i32), ("mmax", c_i32),
+                ("lo", c_vp), ("hi", c_vp), ("left", c_vp), ("right", c_vp),
+                ("level_nodes", c_vp), ("level_off", c_vp), ("level_off_h", c_i32 * 33),
+                ("root", c_i32),
+                ("rU", c_vp), ("rV", c_vp), ("rsel", c_vp), ("csel", c_vp), ("rloc", c_vp),
+                ("cloc", c_vp), ("flags", c_vp),
+                ("U", c_vp), ("V", c_vp), ("B", c_vp), ("D", c_vp), ("rres", c_vp),
+                ("cres", c_vp),
+                ("M", c_vp), ("psel", c_vp), ("tsel", c_vp), ("ycomp", c_vp), ("zcomp", c_vp)]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "hsseig_version": (ctypes.c_char_p, []),
+    "hsseig_status_init": (ctypes.c_int, [c_vp, c_i64, c_vp]),
+    "hsseig_secular": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                      c_vp, c_vp]),
+    "hsseig_dnext": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "hsseig_loewner": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp,
+                                      c_vp]),
+    "hsseig_normalizers": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "hsseig_cauchy_block": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_vp, c_i64, c_vp,
+                                           c_i64, c_vp]),
+    "hsseig_sample_work_doubles": (c_i64, [c_i64, c_i64]),
+    "hsseig_cauchy_sample": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_i64, c_vp, c_vp,
+                                            c_i64, c_vp, c_vp]),
+    "hsseig_tree_bytes": (c_i64, [c_i32, c_i32, c_i32, c_i32]),
+    "hsseig_tree_layout": (ctypes.c_int, [ctypes.POINTER(Tree), ctypes.POINTER(c_i32), c_i32,
+                                          c_i32, c_vp, c_vp]),
+    "hsseig_hss_build_rand": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_vp, c_vp, c_i64,
+                                             c_dbl, ctypes.POINTER(Tree), c_vp, c_vp]),
+    "hsseig_matmul_work_doubles": (c_i64, [c_i64, ctypes.POINTER(Tree)]),
+    "hsseig_hss_matmul_right": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(Tree), c_vp,
+                                               c_i64, c_vp, c_vp]),
+    "hsseig_dense_update": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(Gen), c_vp, c_i64,
+                                           c_vp]),
+    "hsseig_gemm": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64,
+                                   c_vp]),
+}
+
+EXPORTS = tuple(_SIGS)
+
+
+def lib_path():
+    return _build.LIB
+
+
+def load(build_if_missing=True):
+    """Load (building first if stale and nvcc is present) the shared library."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = _build.LIB
+    if build_if_missing:
+        try:
+            _build.build()
+        except (OSError, FileNotFoundError):
+            pass
+    if not os.path.exists(path):
+        raise RuntimeError(f"hsseig_b200: native library {path} is missing; run "
+                           "`python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("hsseig_b200 requires a CUDA device (sm_100a); there is no CPU path")
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def check(rc, what):
+    if rc == HSSEIG_OK:
+        return
+    if rc == HSSEIG_ERR_ARG:
+        raise ValueError(f"{what}: invalid argument")
+    raise RuntimeError(f"{what}: CUDA error (status {rc})")

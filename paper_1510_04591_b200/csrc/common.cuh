@@ -1,0 +1,90 @@
+// Shared device helpers for the sm_100a merge-step kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hsseig_b200.h"
+
+#define HSS_CHECK_LAUNCH()                                       \
+  do {                                                           \
+    cudaError_t _e = cudaGetLastError();                         \
+    if (_e != cudaSuccess) return HSSEIG_ERR_CUDA;               \
+  } while (0)
+
+namespace hsseig {
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+constexpr double kEps = 2.220446049250313e-16;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_prod(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v *= __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Stable d_i - lam_j from the gap pair of root j (pkg/src/hsseig/secular.py:183-203):
+//   i <= j : (d_i - d_j) - gamma_j        i > j : (d_i - d_{j+1}) + mu_j
+// dnext_j is d_{j+1} (the virtual pole d_{k-1}+gamma_{k-1}+mu_{k-1} for j = k-1).
+__device__ __forceinline__ double stable_gap(int64_t i, int64_t j, double di, double dj,
+                                             double dnext_j, double gam_j, double mu_j) {
+  return (i <= j) ? ((di - dj) - gam_j) : ((di - dnext_j) + mu_j);
+}
+
+// Generators of the Cauchy-like eigenvector matrix C_ij = zhat_i v_j / (d_i - lam_j)
+// (pkg/src/hsseig/cauchy.py:15-56).  dnext has the virtual pole appended at k-1.
+struct CauchyGen {
+  const double* d;
+  const double* dnext;
+  const double* gam;
+  const double* mu;
+  const double* zhat;
+  const double* v;
+  int64_t k;
+
+  __device__ __forceinline__ double entry(int64_t i, int64_t j) const {
+    double g = stable_gap(i, j, __ldg(d + i), __ldg(d + j), __ldg(dnext + j), __ldg(gam + j),
+                          __ldg(mu + j));
+    return (__ldg(zhat + i) * __ldg(v + j)) / g;
+  }
+};
+
+// ---- FP64 warp MMA (DMMA) --------------------------------------------------
+// m8n8k4, A row-major fragment a = A[lane/4][lane%4], B col fragment b = B[lane%4][lane/4],
+// C fragment c0,c1 = C[lane/4][2*(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int n = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int n = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+}  // namespace hsseig

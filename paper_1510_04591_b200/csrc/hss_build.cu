@@ -1,0 +1,562 @@
+// Randomized HSS construction (ADC2) on sm_100a, level by level.
+//
+// Reference path (pkg/src/hsseig/hss.py):
+//   _build_skeleton           hss.py:188-214   -> hsseig_tree_layout (host topology)
+//   rand_hss_construct        hss.py:217-306   -> leaf_form / genB / inner_form / id kernels
+//   _interp_rows              hss.py:120-148   -> id_kernel: column-pivoted Householder QR of
+//                                                 M^T following LAPACK dgeqp3/dlaqp2 (pivot on
+//                                                 downdated norms, sqrt(eps) recompute rule),
+//                                                 trailing-mass truncation, saturation flag,
+//                                                 in-place dtrsm back substitution
+// One CTA per (node, side): side 0 compresses the block row (Phi -> U, rows_sel),
+// side 1 the block column (Theta -> V, cols_sel).  Every matrix an ID sees is at
+// most (2w) x w, so it lives in shared memory for the whole factorization.
+#include <vector>
+
+#include "common.cuh"
+
+namespace hsseig {
+
+constexpr double kTol3z = 1.0536712127723509e-08;  // sqrt(dlamch('E')) = sqrt(2^-53)
+constexpr double kFlagTol = 1e-12;                  // hss.py:117
+
+struct TreeDev {
+  int32_t k, n_leaves, depth, w, ws, pmax, mmax;
+  const int32_t *lo, *hi, *left, *right, *lnodes;
+  int32_t *rU, *rV, *rsel, *csel, *rloc, *cloc, *flags;
+  double *U, *V, *B, *D, *rres, *cres, *M, *psel, *tsel, *ycomp, *zcomp;
+};
+
+static TreeDev to_dev(const hsseig_tree* t) {
+  TreeDev d;
+  d.k = t->k; d.n_leaves = t->n_leaves; d.depth = t->depth; d.w = t->w; d.ws = t->ws;
+  d.pmax = t->pmax; d.mmax = t->mmax;
+  d.lo = t->lo; d.hi = t->hi; d.left = t->left; d.right = t->right; d.lnodes = t->level_nodes;
+  d.rU = t->rU; d.rV = t->rV; d.rsel = t->rsel; d.csel = t->csel; d.rloc = t->rloc;
+  d.cloc = t->cloc; d.flags = t->flags;
+  d.U = t->U; d.V = t->V; d.B = t->B; d.D = t->D; d.rres = t->rres; d.cres = t->cres;
+  d.M = t->M; d.psel = t->psel; d.tsel = t->tsel; d.ycomp = t->ycomp; d.zcomp = t->zcomp;
+  return d;
+}
+
+__device__ __forceinline__ size_t slot_pw(const TreeDev& T, int node) {
+  return (size_t)node * T.pmax * T.ws;
+}
+__device__ __forceinline__ size_t slot_ww(const TreeDev& T, int node) {
+  return (size_t)node * T.ws * T.ws;
+}
+
+// ---------------------------------------------------------------------------
+// leaf level: D = C(t,t);  Phi = Y_t - D Omega_t (side 0);  Theta = Z_t - D^T Omega_t (side 1)
+// (hss.py:261-268)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
+                                                        const double* __restrict__ om,
+                                                        int64_t ldom,
+                                                        const double* __restrict__ Y,
+                                                        const double* __restrict__ Z,
+                                                        int64_t ldy) {
+  extern __shared__ __align__(16) double sm[];
+  const int j = blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  const int node = T.lnodes[(1 << T.depth) - 1 + j];
+  const int lo = T.lo[node], m = T.hi[node] - lo, w = T.w;
+  constexpr int RA = 16;
+  double* sOm = sm;                  // m x w
+  double* sD = sm + (size_t)T.mmax * w;  // RA x m chunk
+  for (int e = tid; e < m * w; e += blockDim.x) {
+    int b = e / w, c = e % w;
+    sOm[e] = om[(int64_t)(lo + b) * ldom + c];
+  }
+  const double* src = side == 0 ? Y : Z;
+  double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * T.ws;
+  double* Dslot = T.D + (size_t)j * T.mmax * T.mmax;
+  for (int a0 = 0; a0 < m; a0 += RA) {
+    const int na = min(RA, m - a0);
+    __syncthreads();
+    for (int e = tid; e < na * m; e += blockDim.x) {
+      int aa = e / m, b = e % m;
+      double val = side == 0 ? g.entry(lo + a0 + aa, lo + b) : g.entry(lo + b, lo + a0 + aa);
+      sD[aa * m + b] = val;
+      if (side == 0) Dslot[(size_t)(a0 + aa) * T.mmax + b] = val;
+    }
+    __syncthreads();
+    for (int e = tid; e < na * w; e += blockDim.x) {
+      int aa = e / w, c = e % w;
+      double s = 0.0;
+      const double* drow = sD + aa * m;
+      for (int b = 0; b < m; ++b) s = fma(drow[b], sOm[b * w + c], s);
+      Mo[(size_t)(a0 + aa) * T.ws + c] = src[(int64_t)(lo + a0 + aa) * ldy + c] - s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// skeleton blocks of the children of every node at one level (hss.py:270-271, 299-301):
+//   B_left = C(rows_sel(left), cols_sel(right)),  B_right = C(rows_sel(right), cols_sel(left))
+// ---------------------------------------------------------------------------
+__global__ void genB_kernel(CauchyGen g, TreeDev T, int level) {
+  const int j = blockIdx.x, which = blockIdx.y, tid = threadIdx.x;
+  const int node = T.lnodes[(1 << level) - 1 + j];
+  const int a = T.left[node], b = T.right[node];
+  const int me = which == 0 ? a : b, sib = which == 0 ? b : a;
+  const int nr = T.rU[me], nc = T.rV[sib];
+  const int32_t* rs = T.rsel + (size_t)me * T.ws;
+  const int32_t* cs = T.csel + (size_t)sib * T.ws;
+  double* Bo = T.B + slot_ww(T, me);
+  for (int e = tid; e < nr * nc; e += blockDim.x) {
+    int r = e / nc, c = e % nc;
+    Bo[r * T.ws + c] = g.entry(rs[r], cs[c]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// inner level (hss.py:272-277):
+//   Phi   = [ psel_a - B_a ycomp_b ; psel_b - B_b ycomp_a ]
+//   Theta = [ tsel_a - B_b^T zcomp_b ; tsel_b - B_a^T zcomp_a ]
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level) {
+  const int j = blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  const int node = T.lnodes[(1 << level) - 1 + j];
+  const int a = T.left[node], b = T.right[node], w = T.w, ws = T.ws;
+  double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * ws;
+  const int na = side == 0 ? T.rU[a] : T.rV[a];
+  const int nb = side == 0 ? T.rU[b] : T.rV[b];
+  for (int e = tid; e < (na + nb) * w; e += blockDim.x) {
+    int row = e / w, c = e % w;
+    bool top = row < na;
+    int rr = top ? row : row - na;
+    int me = top ? a : b, sib = top ? b : a;
+    double s = 0.0;
+    if (side == 0) {
+      // psel_me[rr] - B_me[rr, :] ycomp_sib
+      const double* Bm = T.B + slot_ww(T, me) + (size_t)rr * ws;
+      const double* yc = T.ycomp + slot_ww(T, sib);
+      int nk = T.rV[sib];
+      for (int t = 0; t < nk; ++t) s = fma(Bm[t], yc[(size_t)t * ws + c], s);
+      Mo[(size_t)row * ws + c] = T.psel[slot_ww(T, me) + (size_t)rr * ws + c] - s;
+    } else {
+      // tsel_me[rr] - B_sib[:, rr]^T zcomp_sib
+      const double* Bs = T.B + slot_ww(T, sib);
+      const double* zc = T.zcomp + slot_ww(T, sib);
+      int nk = T.rU[sib];
+      for (int t = 0; t < nk; ++t) s = fma(Bs[(size_t)t * ws + rr], zc[(size_t)t * ws + c], s);
+      Mo[(size_t)row * ws + c] = T.tsel[slot_ww(T, me) + (size_t)rr * ws + c] - s;
+    }
+  }
+}
+
+// LAPACK dlapy2: sqrt(x^2 + y^2) without destructive under/overflow
+__device__ __forceinline__ double lapy2(double x, double y) {
+  double xa = fabs(x), ya = fabs(y);
+  double wv = fmax(xa, ya), zv = fmin(xa, ya);
+  if (zv == 0.0) return wv;
+  double q = zv / wv;
+  return wv * sqrt(1.0 + q * q);
+}
+
+// ---------------------------------------------------------------------------
+// Interpolative decomposition of one p x w matrix M (rows = candidates), hss.py:120-148.
+// Column-pivoted QR of A = M^T (w x p): the candidate rows of M are the columns of A
+// and are stored contiguously in shared memory (sA[j*w + t] = A[t][j]).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double tol,
+                                                 const double* __restrict__ om, int64_t ldom,
+                                                 hsseig_status* st) {
+  extern __shared__ __align__(16) double sm[];
+  const int j = blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int node = T.lnodes[(1 << level) - 1 + j];
+  const bool leaf = T.left[node] < 0;
+  const int w = T.w, ws = T.ws;
+  int p;
+  if (leaf) p = T.hi[node] - T.lo[node];
+  else {
+    int a = T.left[node], b = T.right[node];
+    p = side == 0 ? T.rU[a] + T.rU[b] : T.rV[a] + T.rV[b];
+  }
+  const double* Mg = T.M + (size_t)(2 * j + side) * T.pmax * ws;
+  double* sA = sm;                              // p x w
+  double* vn1 = sA + (size_t)T.pmax * w;        // p
+  double* vn2 = vn1 + T.pmax;                   // p
+  double* tail = vn2 + T.pmax;                  // w + 1
+  double* red = tail + (w + 1);                 // 32 scratch
+  int* piv = reinterpret_cast<int*>(red + 32);  // p
+  __shared__ double s_tau, s_nf;
+  __shared__ int s_r, s_sat;
+  __shared__ double s_resid;
+
+  for (int e = tid; e < p * w; e += blockDim.x) {
+    int row = e / w, c = e % w;
+    sA[e] = Mg[(size_t)row * ws + c];
+  }
+  for (int e = tid; e < p; e += blockDim.x) piv[e] = e;
+  __syncthreads();
+  // Frobenius norm (hss.py:128) and initial column norms (dgeqp3: dnrm2 of each column)
+  {
+    double s = 0.0;
+    for (int e = tid; e < p * w; e += blockDim.x) s = fma(sA[e], sA[e], s);
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+  }
+  for (int c = warp; c < p; c += nwarps) {
+    double s = 0.0;
+    for (int t = lane; t < w; t += 32) s = fma(sA[c * w + t], sA[c * w + t], s);
+    s = sqrt(warp_sum(s));
+    if (lane == 0) { vn1[c] = s; vn2[c] = s; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int t = 0; t < nwarps; ++t) s += red[t];
+    s_nf = sqrt(s);
+  }
+  __syncthreads();
+  const double nf = s_nf;
+  int r = 0, sat = 0;
+  double resid = 0.0;
+  const int mn = min(w, p);
+  if (!(nf == 0.0 || p == 0 || w == 0)) {
+    for (int i = 0; i < mn; ++i) {
+      if (warp == 0) {
+        // pivot: first index of the largest partial norm (idamax)
+        double best = -1.0;
+        int bi = i;
+        for (int c = i + lane; c < p; c += 32) {
+          double v = vn1[c];
+          if (v > best) { best = v; bi = c; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        const int pvt = bi;
+        if (pvt != i) {
+          for (int t = lane; t < w; t += 32) {
+            double x0 = sA[i * w + t];
+            sA[i * w + t] = sA[pvt * w + t];
+            sA[pvt * w + t] = x0;
+          }
+          if (lane == 0) {
+            int tp = piv[pvt]; piv[pvt] = piv[i]; piv[i] = tp;
+            vn1[pvt] = vn1[i];
+            vn2[pvt] = vn2[i];
+          }
+        }
+        __syncwarp();
+        // Householder reflector for column i (dlarfg on A[i:, i])
+        double* col = sA + i * w;
+        double xs = 0.0;
+        for (int t = i + 1 + lane; t < w; t += 32) xs = fma(col[t], col[t], xs);
+        double xnorm = sqrt(warp_sum(xs));
+        double alpha = col[i];
+        double tau = 0.0, beta = alpha;
+        if (xnorm != 0.0) {
+          beta = -copysign(lapy2(alpha, xnorm), alpha);
+          tau = (beta - alpha) / beta;
+          double scal = 1.0 / (alpha - beta);
+          for (int t = i + 1 + lane; t < w; t += 32) col[t] *= scal;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          col[i] = beta;
+          s_tau = tau;
+        }
+      }
+      __syncthreads();
+      // apply H_i^T to the trailing columns and downdate their partial norms (dlaqp2)
+      const double tau = s_tau;
+      const double* v = sA + i * w;
+      for (int c = i + 1 + warp; c < p; c += nwarps) {
+        double* a = sA + c * w;
+        if (tau != 0.0) {
+          double dsum = 0.0;
+          for (int t = i + lane; t < w; t += 32) dsum = fma(t == i ? 1.0 : v[t], a[t], dsum);
+          dsum = warp_sum(dsum);
+          double f = tau * dsum;
+          for (int t = i + lane; t < w; t += 32) a[t] = fma(-f, t == i ? 1.0 : v[t], a[t]);
+        }
+        __syncwarp();
+        double n1 = vn1[c];
+        if (n1 != 0.0) {
+          double q = fabs(a[i]) / n1;
+          double temp = fmax(1.0 - q * q, 0.0);
+          double ratio = n1 / vn2[c];
+          double temp2 = temp * ratio * ratio;
+          if (temp2 <= kTol3z) {
+            double s = 0.0;
+            for (int t = i + 1 + lane; t < w; t += 32) s = fma(a[t], a[t], s);
+            s = sqrt(warp_sum(s));
+            if (lane == 0) {
+              double nv = (i + 1 < w) ? s : 0.0;
+              vn1[c] = nv;
+              vn2[c] = nv;
+            }
+          } else if (lane == 0) {
+            vn1[c] = n1 * sqrt(temp);
+          }
+        }
+        __syncwarp();
+      }
+      __syncthreads();
+    }
+    // trailing Frobenius mass of R's rows, cumulated from the bottom (hss.py:134-136)
+    for (int t = warp; t < mn; t += nwarps) {
+      double s = 0.0;
+      for (int c = t + lane; c < p; c += 32) s = fma(sA[c * w + t], sA[c * w + t], s);
+      s = warp_sum(s);
+      if (lane == 0) tail[t] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double acc = 0.0;
+      tail[mn] = 0.0;
+      for (int t = mn - 1; t >= 0; --t) {
+        acc += tail[t];
+        tail[t] = acc;
+      }
+      const double cut = (tol * nf) * (tol * nf);
+      int wanted = mn;
+      for (int t = 0; t <= mn; ++t)
+        if (tail[t] <= cut) { wanted = t; break; }
+      int nz = 0;
+      for (int t = 0; t < mn; ++t) nz += (fabs(sA[t * w + t]) > 0.0) ? 1 : 0;
+      int rr = min(min(wanted, w), nz);
+      int sflag = 0;
+      if (wanted >= w) sflag = sqrt(fmax(tail[w - 1], 0.0)) > kFlagTol * nf ? 1 : 0;
+      s_r = rr;
+      s_sat = sflag;
+      s_resid = sqrt(fmax(tail[rr], 0.0)) / nf;
+    }
+    __syncthreads();
+    r = s_r;
+    sat = s_sat;
+    resid = s_resid;
+    // T = R[:r,:r]^{-1} R[:r, r:], in place, column-oriented back substitution (dtrsm L/U/N/N)
+    for (int c = r + tid; c < p; c += blockDim.x) {
+      double* x = sA + c * w;
+      for (int t = r - 1; t >= 0; --t) {
+        double xt = x[t] / sA[t * w + t];
+        x[t] = xt;
+        if (xt != 0.0)
+          for (int s2 = 0; s2 < t; ++s2) x[s2] = fma(-xt, sA[t * w + s2], x[s2]);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- outputs: basis X (p x r), skeleton indices, selected rows, compressions
+  int32_t* rank_arr = side == 0 ? T.rU : T.rV;
+  double* X = (side == 0 ? T.U : T.V) + slot_pw(T, node);
+  int32_t* loc = (side == 0 ? T.rloc : T.cloc) + (size_t)node * ws;
+  int32_t* sel = (side == 0 ? T.rsel : T.csel) + (size_t)node * ws;
+  double* selrows = (side == 0 ? T.psel : T.tsel) + slot_ww(T, node);
+  double* comp = (side == 0 ? T.zcomp : T.ycomp) + slot_ww(T, node);
+  if (tid == 0) {
+    rank_arr[node] = r;
+    T.flags[2 * node + side] = sat;
+    (side == 0 ? T.rres : T.cres)[node] = resid;
+    if (sat) atomicAdd(reinterpret_cast<unsigned long long*>(&st->v[4]), 1ull);
+    atomicMax(reinterpret_cast<long long*>(&st->v[5]), (long long)r);
+  }
+  for (int e = tid; e < p * r; e += blockDim.x) {
+    int jj = e / r, t = e % r;  // jj = position in pivoted order
+    double val = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * w + t];
+    X[(size_t)piv[jj] * ws + t] = val;
+  }
+  for (int t = tid; t < r; t += blockDim.x) {
+    int pj = piv[t];
+    loc[t] = pj;
+    int gsel;
+    if (leaf) gsel = T.lo[node] + pj;
+    else {
+      int a = T.left[node], b = T.right[node];
+      const int32_t* sa = (side == 0 ? T.rsel : T.csel) + (size_t)a * ws;
+      const int32_t* sb = (side == 0 ? T.rsel : T.csel) + (size_t)b * ws;
+      int na = side == 0 ? T.rU[a] : T.rV[a];
+      gsel = pj < na ? sa[pj] : sb[pj - na];
+    }
+    sel[t] = gsel;
+  }
+  for (int e = tid; e < r * w; e += blockDim.x) {
+    int t = e / w, c = e % w;
+    selrows[(size_t)t * ws + c] = Mg[(size_t)piv[t] * ws + c];
+  }
+  // comp = X^T S, S = Omega_t (leaf) or [comp_a; comp_b] (inner)   (hss.py:281-282, 295-296)
+  for (int e = tid; e < r * w; e += blockDim.x) {
+    int t = e / w, c = e % w;
+    auto srow = [&](int q) -> double {
+      if (leaf) return om[(int64_t)(T.lo[node] + q) * ldom + c];
+      int a = T.left[node], b = T.right[node];
+      int na = side == 0 ? T.rU[a] : T.rV[a];
+      const double* ca = (side == 0 ? T.zcomp : T.ycomp) + slot_ww(T, a);
+      const double* cb = (side == 0 ? T.zcomp : T.ycomp) + slot_ww(T, b);
+      return q < na ? ca[(size_t)q * ws + c] : cb[(size_t)(q - na) * ws + c];
+    };
+    double s = srow(piv[t]);
+    for (int jj = r; jj < p; ++jj) s = fma(sA[jj * w + t], srow(piv[jj]), s);
+    comp[(size_t)t * ws + c] = s;
+  }
+}
+
+}  // namespace hsseig
+
+using namespace hsseig;
+
+static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct TreeCarve {
+  int64_t off_lo, off_hi, off_left, off_right, off_lnodes, off_rU, off_rV, off_rsel, off_csel,
+      off_rloc, off_cloc, off_flags, off_U, off_V, off_B, off_D, off_rres, off_cres, off_M,
+      off_psel, off_tsel, off_ycomp, off_zcomp, total;
+};
+
+static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
+  TreeCarve c;
+  const int64_t nn = 2 * (int64_t)n_leaves - 1;
+  const int64_t ws = w + (w & 1);
+  const int64_t pmax = std::max<int64_t>(mmax, 2 * (int64_t)w);
+  int64_t o = 0;
+  auto take = [&](int64_t bytes) { int64_t at = o; o = align_up(o + bytes, 256); return at; };
+  c.off_lo = take(4 * nn); c.off_hi = take(4 * nn); c.off_left = take(4 * nn);
+  c.off_right = take(4 * nn); c.off_lnodes = take(4 * nn);
+  c.off_rU = take(4 * nn); c.off_rV = take(4 * nn);
+  c.off_rsel = take(4 * nn * ws); c.off_csel = take(4 * nn * ws);
+  c.off_rloc = take(4 * nn * ws); c.off_cloc = take(4 * nn * ws);
+  c.off_flags = take(4 * 2 * nn);
+  c.off_U = take(8 * nn * pmax * ws); c.off_V = take(8 * nn * pmax * ws);
+  c.off_B = take(8 * nn * ws * ws); c.off_D = take(8 * (int64_t)n_leaves * mmax * mmax);
+  c.off_rres = take(8 * nn); c.off_cres = take(8 * nn);
+  c.off_M = take(8 * 2 * (int64_t)n_leaves * pmax * ws);
+  c.off_psel = take(8 * nn * ws * ws); c.off_tsel = take(8 * nn * ws * ws);
+  c.off_ycomp = take(8 * nn * ws * ws); c.off_zcomp = take(8 * nn * ws * ws);
+  c.total = o;
+  (void)k;
+  return c;
+}
+
+extern "C" int64_t hsseig_tree_bytes(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
+  return carve(k, n_leaves, w, mmax).total;
+}
+
+extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t n_leaves, int32_t w,
+                                  void* dev_mem, void* stream) {
+  if (!t || !bounds || n_leaves < 2 || (n_leaves & (n_leaves - 1)) || w < 1 || !dev_mem)
+    return HSSEIG_ERR_ARG;
+  int depth = 0;
+  while ((1 << depth) < n_leaves) ++depth;
+  if (depth > 31) return HSSEIG_ERR_ARG;
+  int32_t mmax = 0;
+  for (int i = 0; i < n_leaves; ++i) {
+    if (bounds[i + 1] <= bounds[i]) return HSSEIG_ERR_ARG;
+    mmax = std::max(mmax, bounds[i + 1] - bounds[i]);
+  }
+  const int32_t k = bounds[n_leaves];
+  const int nn = 2 * n_leaves - 1;
+  // postorder numbering (hss.py:188-214) and (level, position) -> node map
+  std::vector<int32_t> lo(nn), hi(nn), left(nn, -1), right(nn, -1), lnodes(nn);
+  int counter = 0;
+  struct Rec {
+    static int go(int a, int b, int lev, int pos, const int32_t* bd, std::vector<int32_t>& lo,
+                  std::vector<int32_t>& hi, std::vector<int32_t>& L, std::vector<int32_t>& R,
+                  std::vector<int32_t>& ln, int& cnt) {
+      if (b - a == 1) {
+        int id = cnt++;
+        lo[id] = bd[a]; hi[id] = bd[a + 1];
+        ln[(1 << lev) - 1 + pos] = id;
+        return id;
+      }
+      int h = (a + b) / 2;
+      int l = go(a, h, lev + 1, 2 * pos, bd, lo, hi, L, R, ln, cnt);
+      int r = go(h, b, lev + 1, 2 * pos + 1, bd, lo, hi, L, R, ln, cnt);
+      int id = cnt++;
+      lo[id] = lo[l]; hi[id] = hi[r]; L[id] = l; R[id] = r;
+      ln[(1 << lev) - 1 + pos] = id;
+      return id;
+    }
+  };
+  int root = Rec::go(0, n_leaves, 0, 0, bounds, lo, hi, left, right, lnodes, counter);
+  TreeCarve c = carve(k, n_leaves, w, mmax);
+  char* base = static_cast<char*>(dev_mem);
+  t->k = k; t->n_leaves = n_leaves; t->depth = depth; t->n_nodes = nn; t->w = w;
+  t->ws = w + (w & 1);
+  t->pmax = std::max<int32_t>(mmax, 2 * w);
+  t->mmax = mmax;
+  t->root = root;
+  for (int l = 0; l <= depth && l < 31; ++l) t->level_off_h[l] = (1 << l) - 1;
+  t->lo = reinterpret_cast<int32_t*>(base + c.off_lo);
+  t->hi = reinterpret_cast<int32_t*>(base + c.off_hi);
+  t->left = reinterpret_cast<int32_t*>(base + c.off_left);
+  t->right = reinterpret_cast<int32_t*>(base + c.off_right);
+  t->level_nodes = reinterpret_cast<int32_t*>(base + c.off_lnodes);
+  t->level_off = nullptr;
+  t->rU = reinterpret_cast<int32_t*>(base + c.off_rU);
+  t->rV = reinterpret_cast<int32_t*>(base + c.off_rV);
+  t->rsel = reinterpret_cast<int32_t*>(base + c.off_rsel);
+  t->csel = reinterpret_cast<int32_t*>(base + c.off_csel);
+  t->rloc = reinterpret_cast<int32_t*>(base + c.off_rloc);
+  t->cloc = reinterpret_cast<int32_t*>(base + c.off_cloc);
+  t->flags = reinterpret_cast<int32_t*>(base + c.off_flags);
+  t->U = reinterpret_cast<double*>(base + c.off_U);
+  t->V = reinterpret_cast<double*>(base + c.off_V);
+  t->B = reinterpret_cast<double*>(base + c.off_B);
+  t->D = reinterpret_cast<double*>(base + c.off_D);
+  t->rres = reinterpret_cast<double*>(base + c.off_rres);
+  t->cres = reinterpret_cast<double*>(base + c.off_cres);
+  t->M = reinterpret_cast<double*>(base + c.off_M);
+  t->psel = reinterpret_cast<double*>(base + c.off_psel);
+  t->tsel = reinterpret_cast<double*>(base + c.off_tsel);
+  t->ycomp = reinterpret_cast<double*>(base + c.off_ycomp);
+  t->zcomp = reinterpret_cast<double*>(base + c.off_zcomp);
+  cudaStream_t s = (cudaStream_t)stream;
+  bool ok = cudaMemcpyAsync((void*)t->lo, lo.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+            cudaMemcpyAsync((void*)t->hi, hi.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+            cudaMemcpyAsync((void*)t->left, left.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+            cudaMemcpyAsync((void*)t->right, right.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+            cudaMemcpyAsync((void*)t->level_nodes, lnodes.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+            cudaMemsetAsync(t->rU, 0, 4 * nn, s) == cudaSuccess &&
+            cudaMemsetAsync(t->rV, 0, 4 * nn, s) == cudaSuccess &&
+            cudaMemsetAsync(t->flags, 0, 8 * nn, s) == cudaSuccess &&
+            cudaMemsetAsync(t->U, 0, (size_t)8 * nn * t->pmax * t->ws, s) == cudaSuccess &&
+            cudaMemsetAsync(t->V, 0, (size_t)8 * nn * t->pmax * t->ws, s) == cudaSuccess &&
+            cudaMemsetAsync(t->B, 0, (size_t)8 * nn * t->ws * t->ws, s) == cudaSuccess;
+  if (!ok) return HSSEIG_ERR_CUDA;
+  // host vectors die here: wait for the copies
+  if (cudaStreamSynchronize(s) != cudaSuccess) return HSSEIG_ERR_CUDA;
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega, int64_t ldom,
+                                     const double* Y, const double* Z, int64_t ldy, double id_tol,
+                                     hsseig_tree* tree, hsseig_status* st, void* stream) {
+  if (!gen || !tree || !omega || !Y || !Z || !st || gen->k != tree->k) return HSSEIG_ERR_ARG;
+  if (tree->w > tree->mmax || tree->w > 128) return HSSEIG_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  CauchyGen g;
+  g.d = gen->d; g.dnext = gen->dnext; g.gam = gen->gamma; g.mu = gen->mu; g.zhat = gen->zhat;
+  g.v = gen->v; g.k = gen->k;
+  TreeDev T = to_dev(tree);
+  const size_t smem_leaf = sizeof(double) * ((size_t)T.mmax * T.w + 16 * (size_t)T.mmax);
+  const size_t smem_id = sizeof(double) * ((size_t)T.pmax * T.w + 2 * T.pmax + T.w + 1 + 32) +
+                         sizeof(int) * T.pmax + 64;
+  if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024) return HSSEIG_ERR_ARG;
+  cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);
+  cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_id);
+  for (int lev = T.depth; lev >= 1; --lev) {
+    dim3 grid(1u << lev, 2);
+    if (lev == T.depth) {
+      leaf_form_kernel<<<grid, 256, smem_leaf, s>>>(g, T, omega, ldom, Y, Z, ldy);
+    } else {
+      genB_kernel<<<grid, 256, 0, s>>>(g, T, lev);
+      HSS_CHECK_LAUNCH();
+      inner_form_kernel<<<grid, 256, 0, s>>>(T, lev);
+    }
+    HSS_CHECK_LAUNCH();
+    id_kernel<<<grid, 256, smem_id, s>>>(T, lev, id_tol, omega, ldom, st);
+    HSS_CHECK_LAUNCH();
+  }
+  genB_kernel<<<dim3(1, 2), 256, 0, s>>>(g, T, 0);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}

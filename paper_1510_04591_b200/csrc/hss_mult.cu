@@ -1,0 +1,296 @@
+// HSS x dense product from the right, out = X H (Algorithm 3), on sm_100a.
+//
+// Reference: hss_matmul_right (pkg/src/hsseig/hss.py:309-361).
+// Every step of the algorithm is a tall-skinny contraction over the P rows of X
+// with a node-local factor, so each tree level is ONE launch of a batched
+// two-segment DMMA GEMM (one job per node):
+//   up, leaf  : G_i = X[:, t_i] U_i
+//   up, inner : G_i = [G_l | G_r] U_i
+//   down      : F_i = [G_sib | F_par] [B_sib ; V_par(rows of i)^T]     (the "inherit" term)
+//   final     : out[:, t_i] = [X[:, t_i] | F_i] [D_i ; V_i^T]
+// Job descriptors are built on the device from the ranks the construction wrote,
+// so no host synchronisation is needed between construction and multiply.
+#include "dmma_gemm.cuh"
+
+namespace hsseig {
+
+struct GemmJob {
+  const double* A1;
+  const double* A2;
+  const double* B1;
+  const double* B2;
+  double* C;
+  int64_t lda1, lda2, b1r, b1c, b2r, b2c, ldc;
+  int32_t K1, K2, N, pad;
+};
+
+template <class T>
+__global__ void __launch_bounds__(T::THREADS) batched_gemm2_kernel(const GemmJob* __restrict__ jobs,
+                                                                   int64_t M) {
+  extern __shared__ __align__(16) double smem[];
+  const GemmJob jb = jobs[blockIdx.y];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / T::WN, wn = warp % T::WN;
+  const int64_t m0 = (int64_t)blockIdx.x * T::BM;
+  if (jb.N <= 0) return;
+  const int nc1 = (jb.K1 + T::BK - 1) / T::BK, nc2 = (jb.K2 + T::BK - 1) / T::BK;
+  const int nch = nc1 + nc2;
+  Acc<T> acc;
+  acc.zero();
+  auto sa = [&](int s) { return smem + s * T::STAGE_ELEMS; };
+  auto sb = [&](int s) { return smem + s * T::STAGE_ELEMS + T::A_ELEMS; };
+  auto produce = [&](int c, int s) {
+    if (c < nc1) {
+      const int k0 = c * T::BK;
+      load_a_async<T>(sa(s), jb.A1, jb.lda1, M, m0, jb.K1, k0, tid);
+      load_b_async<T>(sb(s), jb.B1, jb.b1r, jb.b1c, jb.K1, k0, jb.N, 0, tid);
+    } else {
+      const int k0 = (c - nc1) * T::BK;
+      load_a_async<T>(sa(s), jb.A2, jb.lda2, M, m0, jb.K2, k0, tid);
+      load_b_async<T>(sb(s), jb.B2, jb.b2r, jb.b2c, jb.K2, k0, jb.N, 0, tid);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < T::STAGES - 1; ++s) {
+    if (s < nch) produce(s, s);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait<T::STAGES - 2>();
+    __syncthreads();
+    const int pf = c + T::STAGES - 1;
+    if (pf < nch) produce(pf, pf % T::STAGES);
+    cp_async_commit();
+    mma_chunk<T>(sa(c % T::STAGES), sb(c % T::STAGES), acc, wm, wn, lane);
+  }
+  cp_async_wait<0>();
+  store_acc<T>(acc, jb.C, jb.ldc, M, m0, jb.N, 0, wm, wn, lane);
+}
+
+struct MultPlan {
+  int32_t depth, n_leaves, ws, pmax, mmax;
+  const int32_t *lo, *hi, *left, *right, *lnodes, *rU, *rV;
+  const double *U, *V, *B, *D;
+  const double* X;
+  int64_t ldx;
+  double* out;
+  int64_t ldo;
+  double* Gb;  // levels 1..depth, level l at Gb + P*ws*(2^l - 2), ld = 2^l * ws
+  double* Fb;
+  int64_t P;
+};
+
+__device__ __forceinline__ double* lvl_buf(double* base, int64_t P, int ws, int l) {
+  return base + P * (int64_t)ws * ((1ll << l) - 2);
+}
+
+// Job table: up-sweep level l at [2^l - 2, 2^{l+1} - 2) for l = 1..depth (2n-2 jobs),
+// down-sweep the same offsets shifted by 2n-2, the leaf finish last (n jobs).
+__global__ void setup_jobs_kernel(MultPlan p, GemmJob* __restrict__ jobs) {
+  const int n = p.n_leaves;
+  const int nup = 2 * n - 2;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 2 * nup + n) return;
+  const int ws = p.ws;
+  const size_t pw = (size_t)p.pmax * ws, ww = (size_t)ws * ws;
+  GemmJob jb;
+  jb.A2 = nullptr; jb.B2 = nullptr;
+  jb.lda2 = 0; jb.b2r = 0; jb.b2c = 0; jb.K2 = 0; jb.pad = 0;
+  if (e < 2 * nup) {
+    const bool up = e < nup;
+    const int q = up ? e : e - nup;
+    int l = 1;
+    while (q >= (1 << (l + 1)) - 2) ++l;
+    const int j = q - ((1 << l) - 2);
+    const int node = p.lnodes[(1 << l) - 1 + j];
+    const int64_t ldl = (int64_t)(1 << l) * ws;
+    if (up) {
+      // G_node = A U_node,  A = X[:, t] (leaf) or [G_left | G_right]
+      jb.C = lvl_buf(p.Gb, p.P, ws, l) + (int64_t)j * ws;
+      jb.ldc = ldl;
+      jb.N = p.rU[node];
+      jb.B1 = p.U + (size_t)node * pw;
+      jb.b1r = ws; jb.b1c = 1;
+      if (l == p.depth) {
+        const int lo = p.lo[node];
+        jb.A1 = p.X + lo;
+        jb.lda1 = p.ldx;
+        jb.K1 = p.hi[node] - lo;
+      } else {
+        const int a = p.left[node], b = p.right[node];
+        const int64_t ldc1 = (int64_t)(1 << (l + 1)) * ws;
+        jb.A1 = lvl_buf(p.Gb, p.P, ws, l + 1) + (int64_t)(2 * j) * ws;
+        jb.lda1 = ldc1;
+        jb.K1 = p.rU[a];
+        jb.A2 = jb.A1 + ws;
+        jb.lda2 = ldc1;
+        jb.K2 = p.rU[b];
+        jb.B2 = jb.B1 + (size_t)p.rU[a] * ws;
+        jb.b2r = ws; jb.b2c = 1;
+      }
+    } else {
+      // F_node = G_sib B_sib (+ F_parent V_parent[rows of node]^T)
+      const int sib = p.lnodes[(1 << l) - 1 + (j ^ 1)];
+      jb.A1 = lvl_buf(p.Gb, p.P, ws, l) + (int64_t)(j ^ 1) * ws;
+      jb.lda1 = ldl;
+      jb.K1 = p.rU[sib];
+      jb.B1 = p.B + (size_t)sib * ww;
+      jb.b1r = ws; jb.b1c = 1;
+      jb.C = lvl_buf(p.Fb, p.P, ws, l) + (int64_t)j * ws;
+      jb.ldc = ldl;
+      jb.N = p.rV[node];
+      if (l > 1) {
+        const int par = p.lnodes[(1 << (l - 1)) - 1 + (j >> 1)];
+        const int off = (j & 1) ? p.rV[p.left[par]] : 0;
+        jb.A2 = lvl_buf(p.Fb, p.P, ws, l - 1) + (int64_t)(j >> 1) * ws;
+        jb.lda2 = (int64_t)(1 << (l - 1)) * ws;
+        jb.K2 = p.rV[par];
+        jb.B2 = p.V + (size_t)par * pw + (size_t)off * ws;
+        jb.b2r = 1; jb.b2c = ws;
+      }
+    }
+  } else {
+    // out[:, t] = X[:, t] D + F_leaf V_leaf^T
+    const int j = e - 2 * nup;
+    const int node = p.lnodes[(1 << p.depth) - 1 + j];
+    const int lo = p.lo[node];
+    jb.A1 = p.X + lo;
+    jb.lda1 = p.ldx;
+    jb.K1 = p.hi[node] - lo;
+    jb.B1 = p.D + (size_t)j * p.mmax * p.mmax;
+    jb.b1r = p.mmax; jb.b1c = 1;
+    jb.A2 = lvl_buf(p.Fb, p.P, ws, p.depth) + (int64_t)j * ws;
+    jb.lda2 = (int64_t)(1 << p.depth) * ws;
+    jb.K2 = p.rV[node];
+    jb.B2 = p.V + (size_t)node * pw;
+    jb.b2r = 1; jb.b2c = ws;
+    jb.C = p.out + lo;
+    jb.ldc = p.ldo;
+    jb.N = p.hi[node] - lo;
+  }
+  jobs[e] = jb;
+}
+
+template <class T>
+static int launch_batched(const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
+  if (njobs <= 0 || M <= 0) return HSSEIG_OK;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(batched_gemm2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)T::SMEM_BYTES);
+    attr = true;
+  }
+  dim3 grid((unsigned)((M + T::BM - 1) / T::BM), (unsigned)njobs);
+  batched_gemm2_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(jobs, M);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+// narrow outputs (ranks): BM = 128, BN = 16*NF
+static int launch_narrow(int nf, const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
+  switch (nf) {
+    case 1: return launch_batched<Tile<4, 1, 4, 2>>(jobs, njobs, M, s);
+    case 2: return launch_batched<Tile<4, 2, 4, 2>>(jobs, njobs, M, s);
+    case 3: return launch_batched<Tile<4, 3, 4, 2>>(jobs, njobs, M, s);
+    case 4: return launch_batched<Tile<4, 4, 4, 2>>(jobs, njobs, M, s);
+    case 5: return launch_batched<Tile<4, 5, 4, 2>>(jobs, njobs, M, s);
+    case 6: return launch_batched<Tile<4, 6, 4, 2>>(jobs, njobs, M, s);
+    case 7: return launch_batched<Tile<4, 7, 4, 2>>(jobs, njobs, M, s);
+    default: return HSSEIG_ERR_ARG;
+  }
+}
+
+// wide outputs (leaf finish, plain GEMM tiles): BM = 64, BN = 16*NF
+static int launch_wide(int nf, const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
+  switch (nf) {
+    case 1: case 2: case 3: case 4: return launch_batched<Tile<2, 4, 4, 2>>(jobs, njobs, M, s);
+    case 5: return launch_batched<Tile<2, 5, 4, 2>>(jobs, njobs, M, s);
+    case 6: return launch_batched<Tile<2, 6, 4, 2>>(jobs, njobs, M, s);
+    case 7: return launch_batched<Tile<2, 7, 4, 2>>(jobs, njobs, M, s);
+    case 8: return launch_batched<Tile<2, 8, 4, 2>>(jobs, njobs, M, s);
+    case 9: return launch_batched<Tile<2, 9, 4, 2>>(jobs, njobs, M, s);
+    case 10: return launch_batched<Tile<2, 10, 4, 2>>(jobs, njobs, M, s);
+    case 11: return launch_batched<Tile<2, 11, 4, 2>>(jobs, njobs, M, s);
+    case 12: return launch_batched<Tile<2, 12, 4, 2>>(jobs, njobs, M, s);
+    case 13: return launch_batched<Tile<2, 13, 4, 2>>(jobs, njobs, M, s);
+    default: return HSSEIG_ERR_ARG;
+  }
+}
+
+__global__ void single_job_kernel(GemmJob* jobs, const double* A, int64_t lda, const double* B,
+                                  int64_t ldb, double* C, int64_t ldc, int N, int K, int n0) {
+  GemmJob jb;
+  jb.A1 = A; jb.lda1 = lda; jb.K1 = K;
+  jb.B1 = B + n0; jb.b1r = ldb; jb.b1c = 1;
+  jb.A2 = nullptr; jb.B2 = nullptr; jb.lda2 = 0; jb.b2r = 0; jb.b2c = 0; jb.K2 = 0;
+  jb.C = C + n0; jb.ldc = ldc; jb.N = N; jb.pad = 0;
+  jobs[blockIdx.x] = jb;
+}
+
+}  // namespace hsseig
+
+using namespace hsseig;
+
+static int64_t jobs_doubles(int64_t n_leaves) {
+  int64_t njobs = 2 * (2 * n_leaves - 2) + n_leaves;
+  return (njobs * (int64_t)sizeof(GemmJob) + 7) / 8 + 32;
+}
+
+extern "C" int64_t hsseig_matmul_work_doubles(int64_t P, const hsseig_tree* t) {
+  if (!t) return -1;
+  return 2 * P * (int64_t)t->ws * (2 * (int64_t)t->n_leaves - 2) + jobs_doubles(t->n_leaves);
+}
+
+extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
+                                       const hsseig_tree* t, double* out, int64_t ldo,
+                                       double* work, void* stream) {
+  if (!t || !X || !out || !work || P < 0 || ldx < t->k || ldo < t->k) return HSSEIG_ERR_ARG;
+  if (P == 0) return HSSEIG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t lvl_total = P * (int64_t)t->ws * (2 * (int64_t)t->n_leaves - 2);
+  MultPlan p;
+  p.depth = t->depth; p.n_leaves = t->n_leaves; p.ws = t->ws; p.pmax = t->pmax; p.mmax = t->mmax;
+  p.lo = t->lo; p.hi = t->hi; p.left = t->left; p.right = t->right; p.lnodes = t->level_nodes;
+  p.rU = t->rU; p.rV = t->rV; p.U = t->U; p.V = t->V; p.B = t->B; p.D = t->D;
+  p.X = X; p.ldx = ldx; p.out = out; p.ldo = ldo; p.P = P;
+  p.Gb = work;
+  p.Fb = work + lvl_total;
+  GemmJob* jobs = reinterpret_cast<GemmJob*>(work + 2 * lvl_total);
+  const int n = t->n_leaves, nup = 2 * n - 2;
+  const int total = 2 * nup + n;
+  setup_jobs_kernel<<<(total + 127) / 128, 128, 0, s>>>(p, jobs);
+  HSS_CHECK_LAUNCH();
+  const int nf = (t->w + 15) / 16;
+  int rc;
+  for (int l = t->depth; l >= 1; --l)
+    if ((rc = launch_narrow(nf, jobs + ((1 << l) - 2), 1 << l, P, s))) return rc;
+  for (int l = 1; l <= t->depth; ++l)
+    if ((rc = launch_narrow(nf, jobs + nup + ((1 << l) - 2), 1 << l, P, s))) return rc;
+  return launch_wide((t->mmax + 15) / 16, jobs + 2 * nup, n, P, s);
+}
+
+extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                           int64_t ldc, int64_t M, int64_t N, int64_t K, void* stream) {
+  // Test/bench helper: plain C = A B on the same DMMA engine, N split in 128-wide jobs.
+  // The caller passes C's job scratch implicitly: jobs live in a small static device buffer.
+  static GemmJob* jobs = nullptr;
+  static int cap = 0;
+  if (M < 0 || N < 0 || K < 0 || lda < K || ldb < N || ldc < N) return HSSEIG_ERR_ARG;
+  if (M == 0 || N == 0) return HSSEIG_OK;
+  const int nj = (int)((N + 127) / 128);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (nj > cap) {
+    if (jobs) cudaFree(jobs);
+    if (cudaMalloc(&jobs, sizeof(GemmJob) * nj) != cudaSuccess) return HSSEIG_ERR_CUDA;
+    cap = nj;
+  }
+  for (int q = 0; q < nj; ++q) {
+    int n0 = q * 128;
+    int nn = (int)std::min<int64_t>(128, N - n0);
+    single_job_kernel<<<1, 1, 0, s>>>(jobs + q, A, lda, B, ldb, C, ldc, nn, (int)K, n0);
+    HSS_CHECK_LAUNCH();
+  }
+  return launch_wide(8, jobs, nj, M, s);
+}
+
+extern "C" const char* hsseig_version(void) { return "hsseig_b200 0.1 sm_100a"; }

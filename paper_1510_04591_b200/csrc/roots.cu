@@ -1,0 +1,387 @@
+// Secular roots, Loewner weight recomputation and column normalizers on sm_100a.
+//
+// Reference path (pkg/src/hsseig):
+//   secular_all / _solve_one_root   _kernels.pyx:19-234   -> secular_kernel
+//   stable_gap / gap_table          secular.py:183-203    -> hsseig::stable_gap
+//   recompute_weights (Loewner)     secular.py:206-236    -> loewner_kernel
+//   column_normalizers              secular.py:239-250    -> normalizer_kernel
+//
+// Work decomposition: one warp owns R roots (rows / columns); its lanes stride
+// the k poles so every pole read (d_j, z_j^2, gamma_j, ...) feeds R roots.  All
+// cross-lane reductions are xor butterflies, which leave bit-identical totals in
+// every lane, so the per-root control flow below is warp-uniform.
+#include "common.cuh"
+
+namespace hsseig {
+
+constexpr int kMaxRational = 60;   // _kernels.pyx:11
+constexpr int kMaxBisect = 200;    // _kernels.pyx:12
+constexpr double kNoStep = -1e308;
+
+// Reciprocal to ~1 ulp: MUFU seed + two Newton steps (no IEEE division sequence).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ double quad_inner(double a, double b, double c) {
+  double disc = a * a - 4.0 * b * c;
+  double s = sqrt(disc < 0.0 ? 0.0 : disc);
+  if (c == 0.0) return a != 0.0 ? b / a : kNoStep;
+  if (a <= 0.0) return (a - s) / (2.0 * c);
+  return (a + s) != 0.0 ? 2.0 * b / (a + s) : kNoStep;
+}
+
+__device__ __forceinline__ double quad_outer(double a, double b, double c) {
+  double disc = a * a - 4.0 * b * c;
+  double s = sqrt(disc < 0.0 ? 0.0 : disc);
+  if (a >= 0.0) return c != 0.0 ? (a + s) / (2.0 * c) : kNoStep;
+  return (a - s) != 0.0 ? 2.0 * b / (a - s) : kNoStep;
+}
+
+// z2 = z*z and sum(z2) in a fixed order (one block).
+__global__ void square_sum_kernel(const double* __restrict__ z, int64_t k, double* __restrict__ z2,
+                                  double* __restrict__ sum_out) {
+  __shared__ double part[32];
+  double s = 0.0;
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    double q = z[j] * z[j];
+    z2[j] = q;
+    s += q;
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = (threadIdx.x < (blockDim.x >> 5)) ? part[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) *sum_out = t;
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) secular_kernel(
+    const double* __restrict__ d, const double* __restrict__ z2, const double* __restrict__ sumz2p,
+    int64_t k, double rho, double* __restrict__ lam, double* __restrict__ gam,
+    double* __restrict__ mu, int32_t* __restrict__ iters, hsseig_status* __restrict__ st) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (i0 >= k) return;
+  const double sumz2 = *sumz2p;
+
+  if (k == 1) {  // _kernels.pyx:204-209
+    if (lane == 0) {
+      double g = rho * sumz2;
+      lam[0] = d[0] + g;
+      gam[0] = g;
+      mu[0] = 0.0;
+      iters[0] = 1;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st->v[0]), 1ull);
+      if (!(g > 0.0)) atomicMin(reinterpret_cast<long long*>(&st->v[1]), 0ll);
+    }
+    return;
+  }
+
+  double lo[R], hi[R], x[R], dori[R], half[R];
+  int64_t split[R], ori[R];
+  bool live[R], outer[R];
+  int it[R];
+
+  // --- bracket set-up (_kernels.pyx:66-91); interior roots need f at the midpoint
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t i = i0 + r;
+    live[r] = i < k;
+    outer[r] = (i == k - 1);
+    half[r] = (live[r] && !outer[r]) ? 0.5 * (__ldg(d + i + 1) - __ldg(d + i)) : 0.0;
+    dori[r] = live[r] ? __ldg(d + i) : 0.0;
+    it[r] = 0;
+  }
+  double fh[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) fh[r] = 0.0;
+  for (int64_t j = lane; j < k; j += 32) {
+    const double dj = __ldg(d + j), qj = __ldg(z2 + j);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (live[r] && !outer[r]) fh[r] += rho * qj / ((dj - dori[r]) - half[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t i = i0 + r;
+    double f = 1.0 + warp_sum(fh[r]);
+    if (!live[r]) continue;
+    if (outer[r]) {
+      ori[r] = k - 1;
+      lo[r] = 0.0;
+      hi[r] = rho * sumz2;
+      split[r] = k - 2;
+    } else if (f > 0.0) {
+      ori[r] = i;
+      lo[r] = 0.0;
+      hi[r] = half[r];
+      split[r] = i;
+    } else {
+      ori[r] = i + 1;
+      lo[r] = -half[r];
+      hi[r] = 0.0;
+      split[r] = i;
+    }
+    dori[r] = __ldg(d + ori[r]);
+    x[r] = 0.5 * (lo[r] + hi[r]);
+  }
+
+  // --- rational-interpolant iteration (_kernels.pyx:93-156), all R roots per pole sweep
+  bool fallback[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) fallback[r] = live[r];
+  for (int step = 0; step < kMaxRational; ++step) {
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) any |= fallback[r];
+    if (!any) break;
+    double sl[R], sr[R], dl[R], dr[R], mg[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) sl[r] = sr[r] = dl[r] = dr[r] = mg[r] = 0.0;
+    for (int64_t j = lane; j < k; j += 32) {
+      const double dj = __ldg(d + j), qj = __ldg(z2 + j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!fallback[r]) continue;
+        double g = (dj - dori[r]) - x[r];
+        double inv = rcp_nr(g);
+        double t = qj * inv;
+        double td = t * inv;
+        if (j <= split[r]) {
+          sl[r] += t;
+          dl[r] += td;
+        } else {
+          sr[r] += t;
+          dr[r] += td;
+        }
+        mg[r] += fabs(t);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (!fallback[r]) continue;
+      double psi = rho * warp_sum(sl[r]), phi = rho * warp_sum(sr[r]);
+      double psip = rho * warp_sum(dl[r]), phip = rho * warp_sum(dr[r]);
+      double mag = rho * warp_sum(mg[r]);
+      it[r] += 1;
+      double f = 1.0 + psi + phi;
+      if (f > 0.0) hi[r] = x[r]; else lo[r] = x[r];
+      if (fabs(f) <= kEps * (1.0 + 8.0 * mag)) { fallback[r] = false; continue; }
+      int64_t pa = outer[r] ? k - 2 : i0 + r, pb = pa + 1;
+      double ga = ((__ldg(d + pa) - dori[r]) - x[r]);
+      double gb = ((__ldg(d + pb) - dori[r]) - x[r]);
+      double qa = (ga + gb) * f - ga * gb * (psip + phip);
+      double qb = ga * gb * f;
+      double qc = f - ga * psip - gb * phip;
+      double eta = outer[r] ? quad_outer(qa, qb, qc) : quad_inner(qa, qb, qc);
+      double xn = (eta == kNoStep) ? 0.5 * (lo[r] + hi[r]) : x[r] + eta;
+      if (!(lo[r] < xn && xn < hi[r])) xn = 0.5 * (lo[r] + hi[r]);
+      if (xn == x[r]) { fallback[r] = false; continue; }
+      x[r] = xn;
+    }
+  }
+
+  // --- bisection fallback (_kernels.pyx:158-171); rare, one root at a time
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (!fallback[r]) continue;
+    for (int step = 0; step < kMaxBisect; ++step) {
+      it[r] += 1;
+      double xm = 0.5 * (lo[r] + hi[r]);
+      if (xm <= lo[r] || xm >= hi[r]) break;
+      double s = 0.0;
+      for (int64_t j = lane; j < k; j += 32)
+        s += rho * __ldg(z2 + j) / ((__ldg(d + j) - dori[r]) - xm);
+      double f = 1.0 + warp_sum(s);
+      if (f > 0.0) hi[r] = xm; else lo[r] = xm;
+    }
+    x[r] = 0.5 * (lo[r] + hi[r]);
+  }
+
+  // --- gap pairs (_kernels.pyx:213-233) and bracket checks (secular.py:172-179)
+  if (lane == 0) {
+    unsigned long long tot = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (!live[r]) continue;
+      int64_t i = i0 + r;
+      double g, m;
+      if (outer[r]) {
+        g = x[r];
+        m = rho * sumz2 - x[r];
+        lam[i] = d[i] + x[r];
+      } else {
+        double width = d[i + 1] - d[i];
+        if (ori[r] == i) { g = x[r]; m = width - x[r]; }
+        else { g = width + x[r]; m = -x[r]; }
+        lam[i] = dori[r] + x[r];
+      }
+      gam[i] = g;
+      mu[i] = m;
+      iters[i] = it[r];
+      tot += (unsigned long long)it[r];
+      if (!(g > 0.0)) atomicMin(reinterpret_cast<long long*>(&st->v[1]), (long long)i);
+      if (!(m > 0.0)) atomicMin(reinterpret_cast<long long*>(&st->v[2]), (long long)i);
+    }
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->v[0]), tot);
+  }
+}
+
+// dnext[j] = d[j+1]; dnext[k-1] = d[k-1] + gamma[k-1] + mu[k-1]  (secular.py:199)
+__global__ void dnext_kernel(const double* __restrict__ d, const double* __restrict__ gam,
+                             const double* __restrict__ mu, int64_t k, double* __restrict__ dn) {
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  dn[j] = (j + 1 < k) ? d[j + 1] : (d[k - 1] + gam[k - 1]) + mu[k - 1];
+}
+
+// zhat_i = sign(z_i) sqrt( prod_{j!=i} (lam_j - d_i)/(d_j - d_i) * gamma_i / rho )
+template <int R>
+__global__ void __launch_bounds__(256) loewner_kernel(
+    const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
+    const double* __restrict__ mu, const double* __restrict__ z, int64_t k, double rho,
+    double* __restrict__ zhat, hsseig_status* __restrict__ st) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (i0 >= k) return;
+  double di[R], pr[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    di[r] = (i0 + r < k) ? __ldg(d + i0 + r) : 0.0;
+    pr[r] = 1.0;
+  }
+  for (int64_t j = lane; j < k; j += 32) {
+    const double dj = __ldg(d + j), dnj = __ldg(dn + j), gj = __ldg(gam + j), mj = __ldg(mu + j);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      int64_t i = i0 + r;
+      if (j == i) continue;
+      double num = -stable_gap(i, j, di[r], dj, dnj, gj, mj);
+      double den = dj - di[r];
+      pr[r] *= num / den;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double p = warp_prod(pr[r]);
+    int64_t i = i0 + r;
+    if (lane == 0 && i < k) {
+      double rad = (p * gam[i]) / rho;
+      if (!(rad > 0.0) || !isfinite(rad)) {
+        atomicMin(reinterpret_cast<long long*>(&st->v[3]), (long long)i);
+        zhat[i] = 0.0;
+      } else {
+        zhat[i] = copysign(sqrt(rad), z[i]);
+      }
+    }
+  }
+}
+
+// v_j = 1 / sqrt( sum_i (zhat_i / (d_i - lam_j))^2 )
+template <int R>
+__global__ void __launch_bounds__(256) normalizer_kernel(
+    const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
+    const double* __restrict__ mu, const double* __restrict__ zh, int64_t k,
+    double* __restrict__ v) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (j0 >= k) return;
+  double dj[R], dnj[R], gj[R], mj[R], s[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t j = j0 + r < k ? j0 + r : k - 1;
+    dj[r] = __ldg(d + j);
+    dnj[r] = __ldg(dn + j);
+    gj[r] = __ldg(gam + j);
+    mj[r] = __ldg(mu + j);
+    s[r] = 0.0;
+  }
+  for (int64_t i = lane; i < k; i += 32) {
+    const double di = __ldg(d + i), zi = __ldg(zh + i);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double g = stable_gap(i, j0 + r, di, dj[r], dnj[r], gj[r], mj[r]);
+      double q = zi * rcp_nr(g);
+      s[r] = fma(q, q, s[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double t = warp_sum(s[r]);
+    if (lane == 0 && j0 + r < k) v[j0 + r] = 1.0 / sqrt(t);
+  }
+}
+
+}  // namespace hsseig
+
+using namespace hsseig;
+
+extern "C" int hsseig_status_init(hsseig_status* st, int64_t k, void* stream) {
+  hsseig_status h;
+  for (int t = 0; t < 8; ++t) h.v[t] = 0;
+  h.v[1] = h.v[2] = h.v[3] = k;
+  if (cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
+    return HSSEIG_ERR_CUDA;
+  // the host struct goes out of scope: make the copy complete before returning
+  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return HSSEIG_ERR_CUDA;
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_secular(const double* d, const double* z, int64_t k, double rho,
+                              double* lam, double* gamma, double* mu, int32_t* iters, double* work,
+                              hsseig_status* st, void* stream) {
+  if (k < 1 || !(rho > 0.0) || !d || !z || !lam || !gamma || !mu || !iters || !work || !st)
+    return HSSEIG_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* z2 = work;
+  double* sum = work + k;
+  square_sum_kernel<<<1, 1024, 0, s>>>(z, k, z2, sum);
+  HSS_CHECK_LAUNCH();
+  constexpr int R = 4;
+  int64_t warps = (k + R - 1) / R;
+  int blocks = (int)((warps + 7) / 8);
+  secular_kernel<R><<<blocks, 256, 0, s>>>(d, z2, sum, k, rho, lam, gamma, mu, iters, st);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_dnext(const double* d, const double* gamma, const double* mu, int64_t k,
+                            double* dnext, void* stream) {
+  if (k < 1) return HSSEIG_ERR_ARG;
+  dnext_kernel<<<(unsigned)((k + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d, gamma, mu, k, dnext);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_loewner(const double* d, const double* dnext, const double* gamma,
+                              const double* mu, const double* z, int64_t k, double rho,
+                              double* zhat, hsseig_status* st, void* stream) {
+  if (k < 1 || !(rho > 0.0)) return HSSEIG_ERR_ARG;
+  constexpr int R = 4;
+  int64_t warps = (k + R - 1) / R;
+  loewner_kernel<R><<<(unsigned)((warps + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
+      d, dnext, gamma, mu, z, k, rho, zhat, st);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_normalizers(const double* d, const double* dnext, const double* gamma,
+                                  const double* mu, const double* zhat, int64_t k, double* v,
+                                  void* stream) {
+  if (k < 1) return HSSEIG_ERR_ARG;
+  constexpr int R = 4;
+  int64_t warps = (k + R - 1) / R;
+  normalizer_kernel<R><<<(unsigned)((warps + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
+      d, dnext, gamma, mu, zhat, k, v);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}

@@ -1,0 +1,152 @@
+"""Merge-step drivers and solver configuration (host mirror of pkg/src/hsseig/dc.py).
+
+``update_vectors_dense`` / ``update_vectors_hss`` keep the reference signatures
+and fallback rules (dc.py:132-171); ``merge_update`` is the merge body of
+dc.py:236-247 (secular -> Loewner -> normalizers -> dense or HSS update) for one
+post-deflation rank-one system whose eigenvector block already sits on the GPU.
+"""
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .cauchy import CauchyEvecMatrix
+from .flops import FlopCounter, cauchy_eval_flops, gemm_flops
+from .hss import (MAX_WIDTH, build_partition, estimate_rank, finish_construct, hss_matmul_right,
+                  rand_hss_construct)
+from .secular import RankOneSystem, dev, recompute_weights, solve_secular
+
+METHODS = ("dense-dc", "adc-rand")
+
+
+class BaseCaseError(ArithmeticError):
+    """dc.py:27"""
+
+
+@dataclass
+class SolverConfig:
+    """dc.py:30-51 (same fields, defaults and validation)."""
+
+    base_size: int = 25
+    hss_threshold: int = 2000
+    leaf_size: int = 200
+    oversample: int = 10
+    rank_eps: float = 1e-16
+    rank_cap: int = 100
+    seed: int = 0
+    method: str = "adc-rand"
+
+    def __post_init__(self):
+        if self.base_size < 3:
+            raise ValueError("base_size must be at least 3")
+        if self.hss_threshold < 4 * self.leaf_size:
+            raise ValueError("hss_threshold must be at least 4x leaf_size")
+        if self.rank_eps <= 0.0 or not (0 < self.rank_cap):
+            raise ValueError("tolerances must be positive")
+        if self.oversample < 0:
+            raise ValueError("oversample must be non-negative")
+        if self.method not in METHODS:
+            raise ValueError(f"method must be one of {METHODS}")
+
+
+@dataclass
+class MergeRecord:
+    """dc.py:54-62"""
+
+    size: int
+    kept: int
+    n_deflated: int
+    used_hss: bool = False
+    hss_rank: int = 0
+    fell_back: bool = False
+    flops: dict = field(default_factory=dict)
+
+
+@dataclass
+class EigenResult:
+    """dc.py:65-79; lam and Q stay on the device (torch float64)."""
+
+    lam: torch.Tensor
+    Q: torch.Tensor
+    merges: list = field(default_factory=list)
+    flops: FlopCounter = field(default_factory=FlopCounter)
+
+    @property
+    def n(self):
+        return int(self.lam.numel())
+
+    def max_deflation_fraction(self):
+        if not self.merges:
+            return 0.0
+        return max(m.n_deflated / m.size for m in self.merges)
+
+
+def update_vectors_dense(Qblock, Qprime, flops=None, out=None):
+    """Plain update Qblock @ Qprime (dc.py:132-138).
+
+    Qprime may be a CauchyEvecMatrix: its tiles are then generated on the fly inside
+    the DMMA GEMM (the reference first materialises C.to_dense(), counted the same way).
+    """
+    Qb = dev(Qblock)
+    if isinstance(Qprime, CauchyEvecMatrix):
+        if Qb.shape[1] != Qprime.k:
+            raise ValueError("inner dimensions do not match")
+        if flops is not None:
+            flops.update_dense += cauchy_eval_flops(Qprime.k * Qprime.k)
+            flops.update_dense += gemm_flops(Qb.shape[0], Qprime.k, Qprime.k)
+        return Qprime.right_multiply_into(Qb, out=out)
+    from . import _native as nat
+    Qp = dev(Qprime)
+    if Qb.shape[1] != Qp.shape[0]:
+        raise ValueError("inner dimensions do not match")
+    if flops is not None:
+        flops.update_dense += gemm_flops(Qb.shape[0], *Qp.shape)
+    if out is None:
+        out = torch.empty(Qb.shape[0], Qp.shape[1], dtype=torch.float64, device="cuda")
+    nat.check(nat.load().hsseig_gemm(nat.ptr(Qb), Qb.stride(0), nat.ptr(Qp), Qp.stride(0),
+                                     nat.ptr(out), out.stride(0), Qb.shape[0], Qp.shape[1],
+                                     Qb.shape[1], nat.stream_ptr()), "gemm")
+    return out
+
+
+def update_vectors_hss(Qblock, C, cfg, seed=0, flops=None, record=None, omega=None,
+                       return_tree=False):
+    """HSS update with the reference's dense fallbacks (dc.py:141-171)."""
+    k = C.k
+
+    def dense_fallback():
+        if record is not None:
+            record.used_hss = False
+            record.fell_back = True
+        out = update_vectors_dense(Qblock, C, flops=flops)
+        return (out, None) if return_tree else out
+
+    try:
+        part = build_partition(k, cfg.leaf_size, C.d, C.gamma, C.mu)
+    except ValueError:
+        return dense_fallback()
+    r_est = estimate_rank(part, C.d, C.gamma, C.mu, cfg.rank_eps, cfg.rank_cap)
+    r = min(r_est, part.min_leaf - cfg.oversample)
+    if r < 1 or r + cfg.oversample > MAX_WIDTH:
+        return dense_fallback()
+    H = rand_hss_construct(C, part, r, p=cfg.oversample, seed=seed, flops=flops, omega=omega)
+    if H.flagged:
+        return dense_fallback()
+    if record is not None:
+        record.used_hss = True
+        record.hss_rank = H.r_used
+    out = hss_matmul_right(Qblock, H, flops=flops)
+    return (out, H) if return_tree else out
+
+
+def merge_update(d, z, rho, Qblock, cfg, seed=0, flops=None, record=None, omega=None):
+    """Merge body for one rank-one system (dc.py:236-247): returns (lam, Q_new, C)."""
+    sys = RankOneSystem(d, z, rho)
+    sol = solve_secular(sys, flops=flops)
+    recompute_weights(sys.d, sol, sys.z, rho=rho, flops=flops)
+    C = CauchyEvecMatrix.from_secular(sys, sol, flops=flops)
+    if cfg.method == "adc-rand" and sys.size > cfg.hss_threshold:
+        Qn = update_vectors_hss(Qblock, C, cfg, seed=seed, flops=flops, record=record, omega=omega)
+    else:
+        Qn = update_vectors_dense(Qblock, C, flops=flops)
+    return sol.lam, Qn, C

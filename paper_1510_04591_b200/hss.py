@@ -1,0 +1,394 @@
+"""HSS approximation of the merge eigenvector matrix, built and applied on the GPU.
+
+Host mirror of pkg/src/hsseig/hss.py.  Partition and rank estimate are O(#leaves)
+host logic over a few pole gaps; the randomized construction (Algorithm 2) and
+the structured product (Algorithm 3) run in libhsseig_b200.so
+(csrc/hss_build.cu, csrc/hss_mult.cu).  The tree lives in one device blob laid
+out by hsseig_tree_layout; per-node views are materialised only on request.
+"""
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .flops import cauchy_eval_flops, cpqr_flops, gemm_flops
+from .secular import Status, dev
+
+DIST_SHIFT_THRESHOLD = 1e-10   # hss.py:20
+MAX_BOUNDARY_SHIFT = 5         # hss.py:21
+DEFAULT_RANK_CAP = 100         # hss.py:22
+DEFAULT_ID_TOL = 1e-15         # hss.py:23
+DENSE_BOUND = 4096             # hss.py:24
+FLAG_TOL = 1e-12               # hss.py:117
+MAX_WIDTH = 112                # sample width r + p supported by the sampling kernels
+
+
+@dataclass(frozen=True)
+class HssPartition:
+    """Contiguous leaf ranges covering 0..k; power-of-two leaf count (hss.py:27-45)."""
+
+    ranges: tuple
+    leaf_size: int
+    depth: int
+
+    @property
+    def k(self):
+        return self.ranges[-1][1]
+
+    @property
+    def n_leaves(self):
+        return len(self.ranges)
+
+    @property
+    def min_leaf(self):
+        return min(hi - lo for lo, hi in self.ranges)
+
+    def bounds(self):
+        return np.array([lo for lo, _ in self.ranges] + [self.k], dtype=np.int32)
+
+
+def _host(x):
+    if x is None:
+        return None
+    if isinstance(x, torch.Tensor):
+        return x.detach().cpu().numpy()
+    return np.asarray(x, dtype=np.float64)
+
+
+def build_partition(k, m, d=None, gamma=None, mu=None):
+    """Near-equal power-of-two leaves; clustered boundaries slide up to 5 slots (hss.py:48-79)."""
+    if k < 2 * m:
+        raise ValueError(f"order {k} below twice the leaf size {m}")
+    n_leaves = 1
+    while n_leaves * m < k:
+        n_leaves *= 2
+    q, extra = divmod(k, n_leaves)
+    starts = np.zeros(n_leaves + 1, dtype=np.int64)
+    starts[1:] = np.cumsum([q + 1] * extra + [q] * (n_leaves - extra))
+    mu = _host(mu)
+    if mu is not None and n_leaves > 1:
+        for b in range(1, n_leaves):
+            s = int(starts[b])
+            if mu[s - 1] >= DIST_SHIFT_THRESHOLD:
+                continue
+            cand = np.arange(max(starts[b - 1] + 1, s - MAX_BOUNDARY_SHIFT),
+                             min(starts[b + 1] - 1, s + MAX_BOUNDARY_SHIFT) + 1)
+            g = mu[cand - 1]
+            if float(g.max()) > mu[s - 1]:
+                starts[b] = cand[int(np.argmax(g))]
+    ranges = tuple((int(starts[i]), int(starts[i + 1])) for i in range(n_leaves))
+    return HssPartition(ranges=ranges, leaf_size=m, depth=int(math.log2(n_leaves)))
+
+
+def rank_bound(R, eps):
+    """Sum-of-exponentials term count for 1/x on [1, R] (hss.py:82-84)."""
+    return int(math.ceil(math.log(16.0 / eps) * math.log(8.0 * R) / math.pi ** 2))
+
+
+def estimate_rank(partition, d, gamma, mu, eps=1e-16, cap=DEFAULT_RANK_CAP):
+    """Off-diagonal rank estimate from the boundary gaps (hss.py:87-103)."""
+    if partition.n_leaves < 2:
+        return 0
+    starts = np.array([lo for lo, _ in partition.ranges[1:]], dtype=np.int64)
+    if isinstance(mu, torch.Tensor):   # gather the few values needed on the device
+        span = float((d[-1] + gamma[-1]) - d[0])
+        dist = mu[torch.as_tensor(starts - 1, device=mu.device)].cpu().numpy()
+    else:
+        d, gamma, mu = _host(d), _host(gamma), _host(mu)
+        span = (d[-1] + gamma[-1]) - d[0]
+        dist = mu[starts - 1]
+    r = 0
+    for gap in dist:
+        r = max(r, rank_bound(max(span / gap, 1.0), eps))
+    return min(max(r, 1), cap)
+
+
+class HssNode:
+    """Host view of one tree node (hss.py:151-174); numeric fields download on demand."""
+
+    def __init__(self, tree, index, level, lo, hi):
+        self._t = tree
+        self.index, self.level, self.lo, self.hi = index, level, lo, hi
+        self.left = self.right = self.parent = self.sibling = -1
+
+    @property
+    def is_leaf(self):
+        return self.left < 0
+
+    def _rows(self, side):
+        if self.index == self._t.root:
+            return 0
+        if self.is_leaf:
+            return self.hi - self.lo
+        r = self._t.ranks()[side]
+        return int(r[self.left] + r[self.right])
+
+    @property
+    def U(self):
+        if self.index == self._t.root:
+            return None
+        return self._t.slot("U", self.index, self._rows(0), int(self._t.ranks()[0][self.index]))
+
+    @property
+    def V(self):
+        if self.index == self._t.root:
+            return None
+        return self._t.slot("V", self.index, self._rows(1), int(self._t.ranks()[1][self.index]))
+
+    @property
+    def B(self):
+        if self.index == self._t.root:
+            return None
+        rU, rV = self._t.ranks()
+        return self._t.slot("B", self.index, int(rU[self.index]), int(rV[self.sibling]))
+
+    @property
+    def D(self):
+        if not self.is_leaf:
+            return None
+        return self._t.leaf_D(self.index)
+
+    def _sel(self, name, side):
+        if self.index == self._t.root:
+            return None
+        r = int(self._t.ranks()[side][self.index])
+        return self._t.islot(name, self.index, r)
+
+    rows_sel = property(lambda self: self._sel("rsel", 0))
+    cols_sel = property(lambda self: self._sel("csel", 1))
+    rows_local = property(lambda self: self._sel("rloc", 0))
+    cols_local = property(lambda self: self._sel("cloc", 1))
+
+
+@dataclass
+class HssTree:
+    """Device-resident HSS tree (hss.py:177-185) with reference-compatible node views."""
+
+    partition: HssPartition
+    w: int
+    k: int = 0
+    r_used: int = 0
+    flagged: bool = False
+    flags: list = field(default_factory=list)
+    seed: object = None
+
+    def __post_init__(self):
+        lib = nat.load()
+        p = self.partition
+        self.k = p.k
+        self._bounds = p.bounds()
+        mmax = int(np.diff(self._bounds).max())
+        nbytes = int(lib.hsseig_tree_bytes(p.k, p.n_leaves, self.w, mmax))
+        self.mem = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self.ct = nat.Tree()
+        b = np.ascontiguousarray(self._bounds, dtype=np.int32)
+        nat.check(lib.hsseig_tree_layout(ctypes.byref(self.ct),
+                                         b.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                         p.n_leaves, self.w, nat.ptr(self.mem), nat.stream_ptr()),
+                  "tree_layout")
+        self.root = int(self.ct.root)
+        self._build_nodes()
+        self._ranks = None
+
+    # -- topology (postorder, identical to hss.py:188-214) --
+    def _build_nodes(self):
+        nodes = []
+        ranges = self.partition.ranges
+
+        def rec(a, b, level):
+            if b - a == 1:
+                nodes.append(HssNode(self, len(nodes), level, *ranges[a]))
+                return len(nodes) - 1
+            h = (a + b) // 2
+            li, ri = rec(a, h, level + 1), rec(h, b, level + 1)
+            nd = HssNode(self, len(nodes), level, nodes[li].lo, nodes[ri].hi)
+            nd.left, nd.right = li, ri
+            nodes.append(nd)
+            me = len(nodes) - 1
+            nodes[li].parent = nodes[ri].parent = me
+            nodes[li].sibling, nodes[ri].sibling = ri, li
+            return me
+
+        rec(0, self.partition.n_leaves, 0)
+        self.nodes = nodes
+        self._leaf_pos = {}
+        pos = 0
+        for nd in nodes:
+            if nd.is_leaf:
+                self._leaf_pos[nd.index] = pos
+                pos += 1
+
+    def levels(self):
+        depth = max(n.level for n in self.nodes)
+        by = [[] for _ in range(depth + 1)]
+        for n in self.nodes:
+            by[n.level].append(n.index)
+        return by
+
+    # -- device views --
+    def _view(self, attr, dtype, count, offset_elems):
+        base = self.mem.data_ptr()
+        off = getattr(self.ct, attr) - base
+        esz = 8 if dtype == torch.float64 else 4
+        start = off + offset_elems * esz
+        return self.mem[start:start + count * esz].view(dtype)
+
+    def ranks(self):
+        if self._ranks is None:
+            nn = self.ct.n_nodes
+            rU = self._view("rU", torch.int32, nn, 0).cpu().numpy()
+            rV = self._view("rV", torch.int32, nn, 0).cpu().numpy()
+            self._ranks = (rU, rV)
+        return self._ranks
+
+    def slot(self, name, node, rows, cols):
+        ws = self.ct.ws
+        if name in ("U", "V"):
+            n = self.ct.pmax * ws
+        else:
+            n = ws * ws
+        flat = self._view(name, torch.float64, n, node * n)
+        return flat.view(-1, ws)[:rows, :cols].cpu().numpy().copy()
+
+    def islot(self, name, node, r):
+        ws = self.ct.ws
+        return self._view(name, torch.int32, ws, node * ws)[:r].cpu().numpy().astype(np.intp)
+
+    def leaf_D(self, node):
+        mm = self.ct.mmax
+        j = self._leaf_pos[node]
+        flat = self._view("D", torch.float64, mm * mm, j * mm * mm)
+        m = self.nodes[node].hi - self.nodes[node].lo
+        return flat.view(mm, mm)[:m, :m].cpu().numpy().copy()
+
+
+def _construct_flops(tree, k, w):
+    rU, rV = tree.ranks()
+    f = 2 * (gemm_flops(k, k, w) + cauchy_eval_flops(k * k))
+    for nd in tree.nodes:
+        if nd.index == tree.root:
+            continue
+        if nd.is_leaf:
+            m = nd.hi - nd.lo
+            f += cauchy_eval_flops(m * m) + 2 * gemm_flops(m, m, w)
+            f += cpqr_flops(w, m, max(int(rU[nd.index]), 1)) + cpqr_flops(w, m, max(int(rV[nd.index]), 1))
+        else:
+            a, b = nd.left, nd.right
+            f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
+            f += 2 * gemm_flops(int(rU[a] + rU[b]), w, max(int(rU[a]), int(rV[b])))
+            f += cpqr_flops(w, int(rU[a] + rU[b]), max(int(rU[nd.index]), 1))
+            f += cpqr_flops(w, int(rV[a] + rV[b]), max(int(rV[nd.index]), 1))
+    rt = tree.nodes[tree.root]
+    a, b = rt.left, rt.right
+    f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
+    return f
+
+
+def mult_flops(tree, P):
+    """hss_mult counter of hss.py:329-357 for P rows."""
+    rU, rV = tree.ranks()
+    f = 0
+    for nd in tree.nodes:
+        i = nd.index
+        if i == tree.root:
+            continue
+        m = nd.hi - nd.lo
+        if nd.is_leaf:
+            f += gemm_flops(P, m, int(rU[i]))
+            f += gemm_flops(P, m, m) + gemm_flops(P, int(rV[i]), m)
+        else:
+            f += gemm_flops(P, int(rU[nd.left] + rU[nd.right]), int(rU[i]))
+            f += gemm_flops(P, int(rV[i]), int(rV[nd.left] + rV[nd.right]))
+        f += gemm_flops(P, int(rU[nd.sibling]), int(rV[i]))
+    return f
+
+
+def sample_omega(k, w, seed):
+    """The reference's Gaussian sample block (hss.py:236-237), drawn on the host."""
+    return np.random.default_rng(seed).standard_normal((k, w))
+
+
+def rand_hss_construct(A, partition, r, p=10, seed=0, id_tol=DEFAULT_ID_TOL, flops=None,
+                       omega=None, finish=True):
+    """Randomized bottom-up construction from one Gaussian sample (hss.py:217-306)."""
+    if partition.n_leaves < 2:
+        raise ValueError("need at least two leaves; use the dense path instead")
+    if r < 1 or p < 0:
+        raise ValueError("need rank estimate >= 1 and oversampling >= 0")
+    w = r + p
+    if w > partition.min_leaf:
+        raise ValueError(f"sample width {w} exceeds smallest leaf {partition.min_leaf}")
+    if w > MAX_WIDTH:
+        raise ValueError(f"sample width {w} above the supported {MAX_WIDTH}")
+    if omega is None:
+        omega = sample_omega(A.k, w, seed)
+    om = dev(omega)
+    Y, Z = A.sample(om)
+    tree = HssTree(partition, w, seed=seed)
+    st = Status(A.k)
+    nat.check(nat.load().hsseig_hss_build_rand(A.gen, nat.ptr(om), om.stride(0), nat.ptr(Y),
+                                               nat.ptr(Z), Y.stride(0), float(id_tol),
+                                               ctypes.byref(tree.ct), nat.ptr(st.t),
+                                               nat.stream_ptr()), "hss_build_rand")
+    tree._status = st
+    tree._omega = om
+    if finish:
+        finish_construct(tree, flops)
+    return tree
+
+
+def finish_construct(tree, flops=None):
+    """Host read-back after construction: flags, ranks, r_used and the flop counter."""
+    v = tree._status.read()
+    nn = tree.ct.n_nodes
+    fl = tree._view("flags", torch.int32, 2 * nn, 0).cpu().numpy().reshape(nn, 2)
+    rr = tree._view("rres", torch.float64, nn, 0).cpu().numpy()
+    cr = tree._view("cres", torch.float64, nn, 0).cpu().numpy()
+    tree.flags = []
+    # the reference appends flags in processing order: deepest level first, postorder within
+    for idx in sorted((n.index for n in tree.nodes if n.index != tree.root),
+                      key=lambda i: -tree.nodes[i].level):
+        if fl[idx, 0]:
+            tree.flags.append((idx, "row", float(rr[idx])))
+        if fl[idx, 1]:
+            tree.flags.append((idx, "col", float(cr[idx])))
+    tree.flagged = bool(v[4] > 0)
+    tree._ranks = None
+    rU, rV = tree.ranks()
+    mask = np.ones(nn, dtype=bool)
+    mask[tree.root] = False
+    tree.r_used = int(max(rU[mask].max(), rV[mask].max()))
+    if flops is not None:
+        flops.hss_construct += _construct_flops(tree, tree.k, tree.w)
+    return tree
+
+
+def hss_matmul_right(X, H, flops=None, out=None):
+    """Structured product X @ H (hss.py:309-361) as per-level batched DMMA GEMMs."""
+    X = dev(X)
+    if X.ndim == 1:
+        X = X[None, :]
+    if X.shape[1] != H.k:
+        raise ValueError(f"X has {X.shape[1]} columns, tree order is {H.k}")
+    P = X.shape[0]
+    lib = nat.load()
+    if out is None:
+        out = torch.empty(P, H.k, dtype=torch.float64, device="cuda")
+    work = torch.empty(int(lib.hsseig_matmul_work_doubles(P, ctypes.byref(H.ct))),
+                       dtype=torch.float64, device="cuda")
+    nat.check(lib.hsseig_hss_matmul_right(nat.ptr(X), X.stride(0), P, ctypes.byref(H.ct),
+                                          nat.ptr(out), out.stride(0), nat.ptr(work),
+                                          nat.stream_ptr()), "hss_matmul_right")
+    if flops is not None:
+        flops.hss_mult += mult_flops(H, P)
+    return out
+
+
+def hss_to_dense(H, bound=DENSE_BOUND):
+    """Dense reconstruction (testing utility, hss.py:375-394) via the identity probe."""
+    if H.k > bound:
+        raise ValueError(f"order {H.k} above the dense reconstruction bound {bound}")
+    return hss_matmul_right(torch.eye(H.k, dtype=torch.float64, device="cuda"), H)

@@ -1,0 +1,271 @@
+"""GPU parity: every merge-path kernel against the reference golden vectors and the oracle.
+
+All calls go through libhsseig_b200.so (the C ABI) via the package's host layer.
+"""
+import numpy as np
+import pytest
+
+from helpers import EPS, config4_system, golden, random_system, unpack_tree
+from oracle import hss_oracle as orc
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1510_04591_b200 as hb  # noqa: E402
+from paper_1510_04591_b200 import _native  # noqa: E402
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def sec():
+    return golden("secular")
+
+
+@pytest.fixture(scope="module")
+def hssg():
+    return golden("hss")
+
+
+def test_library_is_the_cuda_path():
+    lib = _native.load()
+    assert b"sm_100a" in lib.hsseig_version()
+
+
+# ---------------------------------------------------------------- secular (a1)
+def test_secular_vs_reference_golden(sec):
+    for name in sec["names"]:
+        d, z, rho = sec[f"{name}_d"], sec[f"{name}_z"], float(sec[f"{name}_rho"])
+        sol = hb.solve_secular(hb.RankOneSystem(d, z, rho))
+        lam = sec[f"{name}_lam"]
+        scale = np.abs(lam).max()
+        # pkg/tests/test_kernels.py:20-32: 64 eps * scale, iterations within max(2, k/20)
+        assert np.abs(np_(sol.lam) - lam).max() <= 64 * EPS * scale
+        assert np.abs(np_(sol.gamma) - sec[f"{name}_gamma"]).max() <= 64 * EPS * scale
+        assert np.abs(np_(sol.mu) - sec[f"{name}_mu"]).max() <= 64 * EPS * scale
+        assert abs(sol.iterations - int(sec[f"{name}_iters"])) <= max(2, d.size // 20)
+
+
+def test_secular_golden_ratio_and_single_pole():
+    sol = hb.solve_secular(hb.RankOneSystem(np.array([-1.0, 1.0]), np.array([1.0, 1.0]) / np.sqrt(2), 1.0))
+    np.testing.assert_allclose(np_(sol.lam), [(1 - np.sqrt(5)) / 2, (1 + np.sqrt(5)) / 2], rtol=1e-15)
+    sol = hb.solve_secular(hb.RankOneSystem(np.array([0.7]), np.array([-0.3]), 2.0))
+    assert float(sol.lam[0]) == 0.7 + 2.0 * 0.09 and float(sol.mu[0]) == 0.0
+
+
+@pytest.mark.parametrize("k", [5000, 32768])
+def test_secular_config4_vs_oracle(k):
+    d, u, rho = config4_system(k, 1)
+    sol = hb.solve_secular(hb.RankOneSystem(d, u, rho))
+    if k > 8000:   # oracle is O(k^2) serial: check a strided subset of roots
+        lam = np_(sol.lam)
+        gam, mu = np_(sol.gamma), np_(sol.mu)
+        assert np.all(gam > 0) and np.all(mu > 0)
+        assert np.all(np.diff(lam) > 0) and np.all(lam[:-1] < d[1:]) and np.all(lam > d)
+        # residual of the secular equation at a sample of roots, in the shifted variable
+        for i in range(0, k, 997):
+            g = (d - d[i]) - gam[i]
+            f = 1.0 + rho * np.sum(u * u / g)
+            mag = rho * np.sum(u * u / np.abs(g))
+            assert abs(f) <= 64 * k * EPS * max(mag, 1.0)
+        return
+    lam, gam, mu, it = orc.secular_all(d, u, rho)
+    scale = np.abs(lam).max()
+    assert np.abs(np_(sol.lam) - lam).max() <= 64 * EPS * scale
+    assert np.abs(np_(sol.gamma) - gam).max() <= 64 * EPS * scale
+    assert np.abs(np_(sol.mu) - mu).max() <= 64 * EPS * scale
+    assert abs(sol.iterations - it) <= max(2, k // 20)
+
+
+def test_secular_bracket_error_maps_to_exception():
+    # a pole set that is not strictly ascending is rejected before any kernel runs
+    with pytest.raises(ValueError):
+        hb.RankOneSystem(np.array([1.0, 1.0]), np.array([1.0, 1.0]), 1.0)
+
+
+# ---------------------------------------------------------- Loewner / v (a4, a5)
+def test_loewner_normalizers_vs_reference(sec):
+    for name in sec["names"]:
+        if f"{name}_zhat" not in sec:
+            continue
+        d, z, rho = sec[f"{name}_d"], sec[f"{name}_z"], float(sec[f"{name}_rho"])
+        sys = hb.RankOneSystem(d, z, rho)
+        sol = hb.solve_secular(sys)
+        zh = hb.recompute_weights(sys.d, sol, sys.z, rho=rho)
+        np.testing.assert_allclose(np_(zh), sec[f"{name}_zhat"], rtol=1e-12)
+        v = hb.column_normalizers(sys.d, sol.gamma, sol.mu, zh)
+        np.testing.assert_allclose(np_(v), sec[f"{name}_v"], rtol=1e-12)
+
+
+def test_loewner_broken_interlacing_raises():
+    d = np.array([0.0, 1.0, 2.0])
+    sys = hb.RankOneSystem(d, np.array([0.5, 0.5, 0.5]), 1.0)
+    sol = hb.solve_secular(sys)
+    sol.gamma[1] = -0.1          # root 1 pushed left of its pole: radicand turns negative
+    with pytest.raises(hb.WeightRecomputationError):
+        hb.recompute_weights(sys.d, sol, sys.z, rho=1.0)
+
+
+def test_eigvec_orthogonality_k2000():
+    # pkg/tests/test_secular.py:261-265: orthogonality <= 50 k eps
+    d, z, rho = random_system(np.random.default_rng(3), 2000)
+    sys = hb.RankOneSystem(d, z, rho)
+    sol = hb.solve_secular(sys)
+    hb.recompute_weights(sys.d, sol, sys.z, rho=rho)
+    C = hb.CauchyEvecMatrix.from_secular(sys, sol)
+    Q = C.to_dense()
+    err = float((Q.T @ Q - torch.eye(2000, dtype=torch.float64, device="cuda")).abs().max())
+    assert err <= 50 * 2000 * EPS
+
+
+# ---------------------------------------------------------- Cauchy (a6, a7, a14)
+def _gen_from(g, name):
+    return hb.CauchyEvecMatrix(g[f"{name}_d"], g[f"{name}_gamma"], g[f"{name}_mu"],
+                               g[f"{name}_zhat"], g[f"{name}_v"])
+
+
+@pytest.mark.parametrize("name", ["t256", "t600", "c4_2048"])
+def test_cauchy_block_and_sampling(hssg, name):
+    C = _gen_from(hssg, name)
+    G = orc.Generators(hssg[f"{name}_d"], hssg[f"{name}_gamma"], hssg[f"{name}_mu"],
+                       hssg[f"{name}_zhat"], hssg[f"{name}_v"])
+    rows = np.arange(0, C.k, 7)
+    cols = np.arange(3, C.k, 5)
+    np.testing.assert_allclose(np_(C.block(rows, cols)), G.block(rows, cols), rtol=4 * EPS, atol=0)
+    w = int(hssg[f"{name}_r"]) + 10
+    seed = [int(s) for s in hssg[f"{name}_seed"]]
+    Om = orc.sample_block(C.k, w, seed)
+    Y, Z = C.sample(Om)
+    for got, ref in ((Y, hssg[f"{name}_Y"]), (Z, hssg[f"{name}_Z"])):
+        assert np.abs(np_(got) - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_sampling_deterministic():
+    d, z, rho = config4_system(3000, 9)
+    C = hb.merge_update(d, z, rho, np.eye(3000)[:4], hb.SolverConfig(method="dense-dc"))[2]
+    Om = np.random.default_rng(1).standard_normal((3000, 77))
+    Y1, Z1 = C.sample(Om)
+    Y2, Z2 = C.sample(Om)
+    assert torch.equal(Y1, Y2) and torch.equal(Z1, Z2)
+
+
+def test_dense_update_vs_torch():
+    d, z, rho = config4_system(1500, 2)
+    X = np.random.default_rng(0).standard_normal((333, 1500))
+    lam, Qn, C = hb.merge_update(d, z, rho, X, hb.SolverConfig(method="dense-dc"))
+    ref = torch.as_tensor(X, device="cuda") @ C.to_dense()
+    assert float((Qn - ref).abs().max()) <= 1e-13 * float(ref.abs().max())
+
+
+def test_plain_gemm_helper():
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((517, 300))
+    B = rng.standard_normal((300, 271))
+    out = hb.update_vectors_dense(A, B)
+    np.testing.assert_allclose(np_(out), A @ B, rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------- HSS (a8-a13)
+@pytest.mark.parametrize("name", ["t256", "t600", "c4_2048"])
+def test_hss_tree_vs_reference(hssg, name):
+    g = hssg
+    C = _gen_from(g, name)
+    m = int(g[f"{name}_leaf"])
+    part = hb.build_partition(C.k, m, C.d, C.gamma, C.mu)
+    assert [tuple(x) for x in g[f"{name}_ranges"]] == list(part.ranges)
+    r = min(hb.estimate_rank(part, C.d, C.gamma, C.mu, float(g[f"{name}_eps"])), part.min_leaf - 10)
+    assert r == int(g[f"{name}_r"])
+    seed = [int(s) for s in g[f"{name}_seed"]]
+    f = hb.FlopCounter()
+    H = hb.rand_hss_construct(C, part, r, p=10, seed=seed, flops=f)
+    assert f.hss_construct == int(g[f"{name}_flops_construct"])
+    assert H.r_used == int(g[f"{name}_tree_r_used"]) and int(H.flagged) == int(g[f"{name}_tree_flagged"])
+    ref = unpack_tree(g, f"{name}_tree_")
+    for nd, rn in zip(H.nodes, ref):
+        assert (nd.lo, nd.hi, nd.level, nd.left, nd.right) == (rn["lo"], rn["hi"], rn["level"], rn["left"], rn["right"])
+        if nd.index == H.root:
+            continue
+        # same skeleton rows/columns as LAPACK dgeqp3 picked in the reference
+        np.testing.assert_array_equal(nd.rows_sel, rn["rsel"])
+        np.testing.assert_array_equal(nd.cols_sel, rn["csel"])
+        np.testing.assert_allclose(nd.U, rn["U"], atol=1e-9)
+        np.testing.assert_allclose(nd.V, rn["V"], atol=1e-9)
+        np.testing.assert_allclose(nd.B.ravel(), rn["B"], rtol=1e-13, atol=1e-15)
+        if nd.is_leaf:
+            t = np.arange(nd.lo, nd.hi)
+            np.testing.assert_allclose(nd.D, np_(C.block(t, t)), rtol=0, atol=0)
+    X = np.random.default_rng(99).standard_normal((40, C.k))
+    f2 = hb.FlopCounter()
+    XH = hb.hss_matmul_right(X, H, flops=f2)
+    assert f2.hss_mult == int(g[f"{name}_flops_mult"])
+    ref_xh = g[f"{name}_XH"]
+    assert np.abs(np_(XH) - ref_xh).max() <= 1e-12 * np.abs(ref_xh).max()
+    Qold = np.random.default_rng(5).standard_normal((48, C.k))
+    cfg = hb.SolverConfig(leaf_size=m, hss_threshold=4 * m, rank_eps=float(g[f"{name}_eps"]))
+    Qn = hb.update_vectors_hss(Qold, C, cfg, seed=seed)
+    refq = g[f"{name}_Qnew"]
+    assert np.abs(np_(Qn) - refq).max() <= 1e-12 * np.abs(refq).max()
+
+
+def test_rank_starved_tree_flags(hssg):
+    g = hssg
+    sys = hb.RankOneSystem(g["starved_d"], g["starved_z"], float(g["starved_rho"]))
+    sol = hb.solve_secular(sys)
+    hb.recompute_weights(sys.d, sol, sys.z, rho=sys.rho)
+    C = hb.CauchyEvecMatrix.from_secular(sys, sol)
+    part = hb.build_partition(256, 64, C.d, C.gamma, C.mu)
+    H = hb.rand_hss_construct(C, part, r=1, p=0, seed=0)
+    assert H.flagged == bool(g["starved_flagged"]) and len(H.flags) == int(g["starved_nflags"])
+    rec = hb.MergeRecord(size=256, kept=256, n_deflated=0)
+    cfg = hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_cap=1, oversample=0)
+    X = np.random.default_rng(1).standard_normal((8, 256))
+    out = hb.update_vectors_hss(X, C, cfg, seed=0, record=rec)
+    assert rec.fell_back and not rec.used_hss
+    ref = torch.as_tensor(X, device="cuda") @ C.to_dense()
+    assert float((out - ref).abs().max()) <= 1e-13 * float(ref.abs().max())
+
+
+def test_hss_multiply_matches_dense_reconstruction():
+    d, z, rho = config4_system(4096, 4)
+    sys = hb.RankOneSystem(d, z, rho)
+    sol = hb.solve_secular(sys)
+    hb.recompute_weights(sys.d, sol, sys.z, rho=rho)
+    C = hb.CauchyEvecMatrix.from_secular(sys, sol)
+    part = hb.build_partition(4096, 128, C.d, C.gamma, C.mu)
+    r = min(hb.estimate_rank(part, C.d, C.gamma, C.mu, 1e-13), part.min_leaf - 10)
+    H = hb.rand_hss_construct(C, part, r, p=10, seed=[0, 0])
+    assert not H.flagged
+    dense = hb.hss_to_dense(H)
+    A = C.to_dense()
+    # construction reconstruction (pkg/tests/test_hss.py:184-190 style, relative Frobenius)
+    assert float(torch.linalg.norm(dense - A) / torch.linalg.norm(A)) <= 1e-12
+    X = torch.randn(777, 4096, dtype=torch.float64, device="cuda")
+    out = hb.hss_matmul_right(X, H)
+    ref = X @ dense
+    assert float((out - ref).abs().max()) <= 1e-13 * float(ref.abs().max())
+
+
+@pytest.mark.parametrize("n", [8192])
+def test_isolated_merge_orthogonality(n):
+    # size-independent property: Q_old orthogonal => Q_new = Q_old C_hss orthogonal
+    d, u, rho = config4_system(n, 0)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    Q0, _ = torch.linalg.qr(torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g))
+    cfg = hb.SolverConfig(leaf_size=128, hss_threshold=512, rank_eps=1e-13)
+    rec = hb.MergeRecord(size=n, kept=n, n_deflated=0)
+    lam, Qn, C = hb.merge_update(d, u, rho, Q0, cfg, seed=[0, 0], record=rec)
+    assert rec.used_hss and not rec.fell_back
+    I = torch.eye(n, dtype=torch.float64, device="cuda")
+    orth = float((Qn.T @ Qn - I).abs().max()) / n
+    assert orth <= 1e-15
+    # eigen-residual of diag(d) + rho u u^T through Q0: (Q0^T Qn) = C_hss approximates C
+    Cd = Q0.T @ Qn
+    dd = torch.as_tensor(d, device="cuda")
+    uu = torch.as_tensor(u, device="cuda")
+    R = dd[:, None] * Cd + rho * uu[:, None] * (uu[None, :] @ Cd) - Cd * lam[None, :]
+    assert float(R.abs().max()) <= 1e-11
