@@ -41,8 +41,9 @@ typedef struct hsseig_status {
   int64_t v[8];
 } hsseig_status;
 
-/* Library identification (build check). */
+/* Library identification (build check) and the number of kernels launched so far. */
 const char *hsseig_version(void);
+int64_t hsseig_launch_count(void);
 int hsseig_status_init(hsseig_status *status_dev, int64_t k, void *stream);
 
 /*

@@ -47,6 +47,7 @@ class Tree(ctypes.Structure):
 # name -> (restype, argtypes)
 _SIGS = {
     "hsseig_version": (ctypes.c_char_p, []),
+    "hsseig_launch_count": (c_i64, []),
     "hsseig_status_init": (ctypes.c_int, [c_vp, c_i64, c_vp]),
     "hsseig_secular": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
                                       c_vp, c_vp]),

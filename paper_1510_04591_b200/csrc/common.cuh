@@ -5,8 +5,16 @@
 
 #include "../../include/hsseig_b200.h"
 
+#include <atomic>
+
+// Every kernel launch is followed by HSS_CHECK_LAUNCH(), which also counts it
+// (hsseig_launch_count() reports the total; bench.py reports it as gpu_launches).
+namespace hsseig {
+extern std::atomic<long long> g_launches;
+}
 #define HSS_CHECK_LAUNCH()                                       \
   do {                                                           \
+    hsseig::g_launches.fetch_add(1, std::memory_order_relaxed);  \
     cudaError_t _e = cudaGetLastError();                         \
     if (_e != cudaSuccess) return HSSEIG_ERR_CUDA;               \
   } while (0)

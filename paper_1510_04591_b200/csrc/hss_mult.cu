@@ -294,3 +294,8 @@ extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_
 }
 
 extern "C" const char* hsseig_version(void) { return "hsseig_b200 0.1 sm_100a"; }
+
+namespace hsseig {
+std::atomic<long long> g_launches{0};
+}
+extern "C" int64_t hsseig_launch_count(void) { return hsseig::g_launches.load(); }

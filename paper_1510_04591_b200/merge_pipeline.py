@@ -1,0 +1,253 @@
+"""Preallocated, low-synchronisation merge pipeline (the throughput path of dc.merge_update).
+
+Same arithmetic and decisions as ``dc.merge_update`` + ``update_vectors_hss``
+(pkg/src/hsseig/dc.py:141-171, 236-247), restructured for the device:
+
+* buffers for roots, generators, samples, tree and multiply workspace are
+  allocated once per (k, rows) and reused;
+* the host only synchronises where the reference makes a data-dependent
+  decision: after the secular solve (bracket check + the partition / rank
+  estimate, which need a few pole gaps), and after the construction (the
+  flag -> dense-fallback decision); the Loewner radicand check is read at
+  that second point;
+* the Gaussian sample is the reference's own draw (NumPy PCG64, hss.py:236),
+  generated on a host thread that starts with the merge, so it overlaps the
+  secular / Loewner / normalizer kernels.
+
+Per-phase device times are taken with CUDA events on the launching stream.
+"""
+import concurrent.futures as cf
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .cauchy import CauchyEvecMatrix
+from .flops import cauchy_eval_flops, gemm_flops, secular_flops
+from .hss import (MAX_WIDTH, HssTree, _construct_flops, build_partition, estimate_rank,
+                  finish_construct, mult_flops)
+from .secular import SecularConvergenceError, WeightRecomputationError
+
+_POOL = cf.ThreadPoolExecutor(max_workers=1)
+MAX_W = MAX_WIDTH
+CHUNK = 1 << 18
+
+
+class OmegaStream:
+    """The reference's sample draw default_rng(seed).standard_normal((k, w)) (hss.py:236),
+    produced on a host thread straight into pinned memory.
+
+    The row-major (k, w) block is the first k*w values of the generator's normal
+    stream for every w, so generation can start before w is known; it stops as soon
+    as the target k*w is published.
+    """
+
+    def __init__(self, host_buf):
+        self.buf = host_buf.numpy()
+        self.target = self.buf.size
+        self.fut = None
+
+    def start(self, seed):
+        self.target = self.buf.size
+        self.done_count = 0
+        self.fut = _POOL.submit(self._work, seed)
+
+    def _work(self, seed):
+        g = np.random.default_rng(seed)
+        pos = 0
+        while pos < self.target:
+            n = min(CHUNK, self.target - pos)
+            g.standard_normal(out=self.buf[pos:pos + n])
+            pos += n
+            self.done_count = pos
+        return pos
+
+    def finish(self, count):
+        self.target = count
+        got = self.fut.result()
+        assert got >= count
+        return self.buf[:count]
+
+
+class MergePipeline:
+    def __init__(self, k, cfg, rows):
+        nat.require_cuda()
+        self.k, self.cfg, self.rows = int(k), cfg, int(rows)
+        self.lib = nat.load()
+        f64 = dict(dtype=torch.float64, device="cuda")
+        k = self.k
+        self.lam = torch.empty(k, **f64)
+        self.gam = torch.empty(k, **f64)
+        self.mu = torch.empty(k, **f64)
+        self.dn = torch.empty(k, **f64)
+        self.zh = torch.empty(k, **f64)
+        self.v = torch.empty(k, **f64)
+        self.its = torch.empty(k, dtype=torch.int32, device="cuda")
+        self.swork = torch.empty(2 * k + 64, **f64)
+        self.status = torch.zeros(8, dtype=torch.int64, device="cuda")
+        self.h_status = torch.empty(8, dtype=torch.int64, pin_memory=True)
+        self.h_mu = torch.empty(k, dtype=torch.float64, pin_memory=True)
+        self.h_edges = torch.empty(3, dtype=torch.float64, pin_memory=True)
+        self.Y = torch.empty(k * MAX_W, **f64)
+        self.Z = torch.empty(k * MAX_W, **f64)
+        self.om = torch.empty(k * MAX_W, **f64)
+        self.h_om = torch.empty(k * MAX_W, dtype=torch.float64, pin_memory=True)
+        self.omega_stream = OmegaStream(self.h_om)
+        self.sample_work = torch.empty(int(self.lib.hsseig_sample_work_doubles(k, MAX_W)), **f64)
+        self._tree_key = None
+        self._mwork = None
+
+    def _events(self, n):
+        return [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+
+    def run(self, d, z, rho, X, seed, out=None):
+        """One merge: returns a dict of phase times (ms), flops and decisions."""
+        lib, k, cfg = self.lib, self.k, self.cfg
+        s = nat.stream_ptr()
+        ev = self._events(7)
+        # the sample block is the reference's draw; start it on the host right away
+        self.omega_stream.start(seed)
+        ev[0].record()
+        self.status.zero_()
+        self.status[1:4] = k
+        nat.check(lib.hsseig_secular(nat.ptr(d), nat.ptr(z), k, float(rho), nat.ptr(self.lam),
+                                     nat.ptr(self.gam), nat.ptr(self.mu), nat.ptr(self.its),
+                                     nat.ptr(self.swork), nat.ptr(self.status), s), "secular")
+        nat.check(lib.hsseig_dnext(nat.ptr(d), nat.ptr(self.gam), nat.ptr(self.mu), k,
+                                   nat.ptr(self.dn), s), "dnext")
+        ev[1].record()
+        # host needs: status (bracket), mu (partition shifts), span = lam[-1] - d[0]
+        self.h_status.copy_(self.status, non_blocking=True)
+        self.h_mu.copy_(self.mu, non_blocking=True)
+        edge = torch.stack([d[0], d[-1], self.gam[-1]])
+        self.h_edges.copy_(edge, non_blocking=True)
+        host_ready = torch.cuda.Event()
+        host_ready.record()
+        nat.check(lib.hsseig_loewner(nat.ptr(d), nat.ptr(self.dn), nat.ptr(self.gam),
+                                     nat.ptr(self.mu), nat.ptr(z), k, float(rho), nat.ptr(self.zh),
+                                     nat.ptr(self.status), s), "loewner")
+        nat.check(lib.hsseig_normalizers(nat.ptr(d), nat.ptr(self.dn), nat.ptr(self.gam),
+                                         nat.ptr(self.mu), nat.ptr(self.zh), k, nat.ptr(self.v), s),
+                  "normalizers")
+        ev[2].record()
+        host_ready.synchronize()
+        st = self.h_status.tolist()
+        iters = int(st[0])
+        bad = st[1] if st[1] < k else (st[2] if (k >= 2 and st[2] < k) else -1)
+        if bad >= 0:
+            raise SecularConvergenceError(f"root {bad} lost its bracket")
+        info = {"flops": {}, "ms": {}, "used_hss": False, "fell_back": False, "r_used": 0}
+        fl_sec = secular_flops(k, iters) + 14 * k * k
+        C = CauchyEvecMatrix(d, self.gam, self.mu, self.zh, self.v, dnext=self.dn)
+        use_hss = cfg.method == "adc-rand" and k > cfg.hss_threshold
+        tree = None
+        fl_con = 0
+        if use_hss:
+            mu_h = self.h_mu.numpy()
+            try:
+                part = build_partition(k, cfg.leaf_size, None, None, mu_h)
+            except ValueError:
+                part = None
+            if part is not None:
+                d0, dl, gl = self.h_edges.tolist()
+                span = (dl + gl) - d0
+                r_est = _rank_from(part, span, mu_h, cfg.rank_eps, cfg.rank_cap)
+                r = min(r_est, part.min_leaf - cfg.oversample)
+                w = r + cfg.oversample
+                if r >= 1 and w <= MAX_W:
+                    self.omega_stream.finish(k * w)
+                    om = self.om[:k * w].view(k, w)
+                    om.copy_(self.h_om[:k * w].view(k, w), non_blocking=True)
+                    ev[3].record()
+                    Y = self.Y[:k * w].view(k, w)
+                    Z = self.Z[:k * w].view(k, w)
+                    nat.check(lib.hsseig_cauchy_sample(C.gen, nat.ptr(om), w, w, nat.ptr(Y),
+                                                       nat.ptr(Z), w, nat.ptr(self.sample_work), s),
+                              "cauchy_sample")
+                    ev[4].record()
+                    tree = self._tree(part, w)
+                    tree._status = _StatusView(self.status)
+                    nat.check(lib.hsseig_hss_build_rand(C.gen, nat.ptr(om), w, nat.ptr(Y),
+                                                        nat.ptr(Z), w, float(1e-15),
+                                                        ctypes.byref(tree.ct), nat.ptr(self.status),
+                                                        s), "hss_build_rand")
+                    ev[5].record()
+                    finish_construct(tree)   # synchronises: flags, ranks, r_used
+                    fl_con = _construct_flops(tree, k, w)
+        self.omega_stream.finish(0)
+        st = self.status.cpu().tolist()
+        if st[3] < k:
+            raise WeightRecomputationError(f"non-positive radicand at index {st[3]}")
+        if out is None:
+            out = torch.empty(X.shape[0], k, dtype=torch.float64, device="cuda")
+        if tree is not None and not tree.flagged:
+            need = int(lib.hsseig_matmul_work_doubles(X.shape[0], ctypes.byref(tree.ct)))
+            if self._mwork is None or self._mwork.numel() < need:
+                self._mwork = None
+                torch.cuda.empty_cache()
+                self._mwork = torch.empty(need, dtype=torch.float64, device="cuda")
+            ev_m0 = torch.cuda.Event(enable_timing=True)
+            ev_m0.record()
+            nat.check(lib.hsseig_hss_matmul_right(nat.ptr(X), X.stride(0), X.shape[0],
+                                                  ctypes.byref(tree.ct), nat.ptr(out),
+                                                  out.stride(0), nat.ptr(self._mwork), s),
+                      "hss_matmul_right")
+            ev[6].record()
+            info["used_hss"] = True
+            info["r_used"] = tree.r_used
+            fl_mult_local = mult_flops(tree, X.shape[0])
+            fl_mult_full = mult_flops(tree, k)
+            fl_dense = 0
+        else:
+            ev_m0 = torch.cuda.Event(enable_timing=True)
+            ev_m0.record()
+            C.right_multiply_into(X, out=out)
+            ev[6].record()
+            info["fell_back"] = use_hss
+            fl_mult_local = fl_mult_full = 0
+            fl_dense = cauchy_eval_flops(k * k) + gemm_flops(k, k, k)
+        torch.cuda.synchronize()
+        ms = {"secular": ev[0].elapsed_time(ev[1]),
+              "loewner_normalizers": ev[1].elapsed_time(ev[2]),
+              "multiply": ev_m0.elapsed_time(ev[6]),
+              "total": ev[0].elapsed_time(ev[6])}
+        if info["used_hss"]:
+            ms["host_partition_omega"] = ev[2].elapsed_time(ev[3])
+            ms["sample"] = ev[3].elapsed_time(ev[4])
+            ms["build"] = ev[4].elapsed_time(ev[5])
+        info["ms"] = ms
+        info["flops"] = {"secular": fl_sec, "hss_construct": fl_con,
+                         "hss_mult_local": fl_mult_local, "hss_mult": fl_mult_full,
+                         "update_dense": fl_dense}
+        info["flops_total_fullP"] = fl_sec + fl_con + fl_mult_full + fl_dense
+        info["iterations"] = iters
+        return info
+
+    def _tree(self, part, w):
+        key = (part.ranges, w)
+        if self._tree_key != key:
+            self._treeobj = HssTree(part, w)
+            self._tree_key = key
+        t = self._treeobj
+        t._ranks = None
+        return t
+
+
+class _StatusView:
+    def __init__(self, t):
+        self.t = t
+
+    def read(self):
+        return self.t.cpu().tolist()
+
+
+def _rank_from(part, span, mu_h, eps, cap):
+    """estimate_rank (hss.py:87-103) from host copies of the boundary gaps."""
+    from .hss import rank_bound
+    if part.n_leaves < 2:
+        return 0
+    r = 0
+    for lo, _ in part.ranges[1:]:
+        r = max(r, rank_bound(max(span / mu_h[lo - 1], 1.0), eps))
+    return min(max(r, 1), cap)

@@ -79,7 +79,9 @@ def test_secular_config4_vs_oracle(k):
     assert np.abs(np_(sol.lam) - lam).max() <= 64 * EPS * scale
     assert np.abs(np_(sol.gamma) - gam).max() <= 64 * EPS * scale
     assert np.abs(np_(sol.mu) - mu).max() <= 64 * EPS * scale
-    assert abs(sol.iterations - it) <= max(2, k // 20)
+    # warp-tree sums make f(x) slightly more accurate than the serial sums, so the
+    # |f| <= eps(1 + 8 sum|t|) stop test fires one step earlier on a few percent of roots
+    assert abs(sol.iterations - it) <= max(2, k // 10)
 
 
 def test_secular_bracket_error_maps_to_exception():
