@@ -115,8 +115,9 @@ int hsseig_cauchy_sample(const hsseig_gen *gen, const double *omega, int64_t ldo
  * host (hsseig_tree_layout); numeric slots by hsseig_hss_build_rand.
  * Slot layout (all row-major, leading dimension `ws`):
  *   U, V : n_nodes slots of pmax x ws (p rows used, rank columns used)
+ *   Vt   : n_nodes slots of ws x pmax (V transposed, rank rows used)
  *   B    : n_nodes slots of ws x ws   (rU(node) x rV(sibling))
- *   D    : n_leaves slots of mmax x mmax (leading dimension mmax)
+ *   D    : n_leaves slots of dld x dld (leading dimension dld = mmax rounded up to even)
  *   rsel, csel, rloc, cloc : n_nodes x ws int32
  */
 typedef struct hsseig_tree {
@@ -129,7 +130,8 @@ typedef struct hsseig_tree {
   int32_t root;
   /* device numeric slots */
   int32_t *rU, *rV, *rsel, *csel, *rloc, *cloc, *flags;
-  double *U, *V, *B, *D, *rres, *cres;
+  double *U, *V, *Vt, *B, *D, *rres, *cres;
+  int32_t dld;
   /* construction scratch (device) */
   double *M;      /* 2 * n_leaves * pmax * ws : matrices handed to the ID */
   double *psel;   /* n_nodes * ws * ws : selected rows of Phi */

@@ -39,8 +39,8 @@ class Tree(ctypes.Structure):
                 ("root", c_i32),
                 ("rU", c_vp), ("rV", c_vp), ("rsel", c_vp), ("csel", c_vp), ("rloc", c_vp),
                 ("cloc", c_vp), ("flags", c_vp),
-                ("U", c_vp), ("V", c_vp), ("B", c_vp), ("D", c_vp), ("rres", c_vp),
-                ("cres", c_vp),
+                ("U", c_vp), ("V", c_vp), ("Vt", c_vp), ("B", c_vp), ("D", c_vp), ("rres", c_vp),
+                ("cres", c_vp), ("dld", c_i32),
                 ("M", c_vp), ("psel", c_vp), ("tsel", c_vp), ("ycomp", c_vp), ("zcomp", c_vp)]
 
 

@@ -57,6 +57,68 @@ __device__ __forceinline__ void mma_chunk(const double* __restrict__ sA,
   }
 }
 
+// Partial chunk: only the first kv (multiple of 4, <= BK) k-columns are live, and only the
+// first jmax n-fragments of this warp carry output columns (both warp-uniform).
+template <class T>
+__device__ __forceinline__ void mma_chunk_part(const double* __restrict__ sA,
+                                               const double* __restrict__ sB, Acc<T>& acc, int wm,
+                                               int wn, int lane, int kv, int jmax) {
+  const int gr = lane >> 2, gc = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < T::BK; kk += 4) {
+    if (kk >= kv) break;
+    double a[T::MF], b[T::NF];
+#pragma unroll
+    for (int i = 0; i < T::MF; ++i) a[i] = sA[(wm * T::MF * 8 + i * 8 + gr) * T::SA + kk + gc];
+#pragma unroll
+    for (int j = 0; j < T::NF; ++j) b[j] = sB[(kk + gc) * T::SB + wn * T::NF * 8 + j * 8 + gr];
+#pragma unroll
+    for (int j = 0; j < T::NF; ++j) {
+      if (j >= jmax) break;
+#pragma unroll
+      for (int i = 0; i < T::MF; ++i) dmma_8x8x4(acc.c[i][j][0], acc.c[i][j][1], a[i], b[j]);
+    }
+  }
+}
+
+// 16-byte async copies (pairs of doubles); the tail pair of a row copies 8 bytes and
+// zero-fills the rest.  Requires 16-byte aligned rows (checked by the caller).
+template <class T>
+__device__ __forceinline__ void load_a_async16(double* sA, const double* __restrict__ A,
+                                               int64_t lda, int64_t M, int64_t m0, int K, int k0,
+                                               int tid) {
+  constexpr int PR = T::BK / 2;
+  constexpr int N = T::BM * PR;
+#pragma unroll
+  for (int e = tid; e < N; e += T::THREADS) {
+    const int r = e / PR, c = (e % PR) * 2;
+    const int64_t gr = m0 + r;
+    const int gc = k0 + c;
+    const int nvalid = (gr < M) ? max(0, min(2, K - gc)) : 0;
+    const double* src = nvalid ? (A + gr * lda + gc) : A;
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sA + r * T::SA + c));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(src),
+                 "r"(nvalid * 8));
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void load_b_async16(double* sB, const double* __restrict__ B,
+                                               int64_t ldb, int K, int k0, int N, int tid) {
+  constexpr int PR = (T::BN + 1) / 2;
+  constexpr int NE = T::BK * PR;
+#pragma unroll 2
+  for (int e = tid; e < NE; e += T::THREADS) {
+    const int r = e / PR, c = (e % PR) * 2;
+    const int gk = k0 + r;
+    const int nvalid = (gk < K) ? max(0, min(2, N - c)) : 0;
+    const double* src = nvalid ? (B + (int64_t)gk * ldb + c) : B;
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sB + r * T::SB + c));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(src),
+                 "r"(nvalid * 8));
+  }
+}
+
 // Async copy of an A chunk: rows [m0, m0+BM) x cols [k0, k0+BK) of row-major A (ld),
 // zero-filled outside [0,M) x [0,K).
 template <class T>

@@ -24,7 +24,8 @@ struct TreeDev {
   int32_t k, n_leaves, depth, w, ws, pmax, mmax;
   const int32_t *lo, *hi, *left, *right, *lnodes;
   int32_t *rU, *rV, *rsel, *csel, *rloc, *cloc, *flags;
-  double *U, *V, *B, *D, *rres, *cres, *M, *psel, *tsel, *ycomp, *zcomp;
+  double *U, *V, *Vt, *B, *D, *rres, *cres, *M, *psel, *tsel, *ycomp, *zcomp;
+  int32_t dld;
 };
 
 static TreeDev to_dev(const hsseig_tree* t) {
@@ -34,7 +35,7 @@ static TreeDev to_dev(const hsseig_tree* t) {
   d.lo = t->lo; d.hi = t->hi; d.left = t->left; d.right = t->right; d.lnodes = t->level_nodes;
   d.rU = t->rU; d.rV = t->rV; d.rsel = t->rsel; d.csel = t->csel; d.rloc = t->rloc;
   d.cloc = t->cloc; d.flags = t->flags;
-  d.U = t->U; d.V = t->V; d.B = t->B; d.D = t->D; d.rres = t->rres; d.cres = t->cres;
+  d.U = t->U; d.V = t->V; d.Vt = t->Vt; d.dld = t->dld; d.B = t->B; d.D = t->D; d.rres = t->rres; d.cres = t->cres;
   d.M = t->M; d.psel = t->psel; d.tsel = t->tsel; d.ycomp = t->ycomp; d.zcomp = t->zcomp;
   return d;
 }
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
   }
   const double* src = side == 0 ? Y : Z;
   double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * T.ws;
-  double* Dslot = T.D + (size_t)j * T.mmax * T.mmax;
+  double* Dslot = T.D + (size_t)j * T.dld * T.dld;
   for (int a0 = 0; a0 < m; a0 += RA) {
     const int na = min(RA, m - a0);
     __syncthreads();
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
       int aa = e / m, b = e % m;
       double val = side == 0 ? g.entry(lo + a0 + aa, lo + b) : g.entry(lo + b, lo + a0 + aa);
       sD[aa * m + b] = val;
-      if (side == 0) Dslot[(size_t)(a0 + aa) * T.mmax + b] = val;
+      if (side == 0) Dslot[(size_t)(a0 + aa) * T.dld + b] = val;
     }
     __syncthreads();
     for (int e = tid; e < na * w; e += blockDim.x) {
@@ -156,18 +157,22 @@ __device__ __forceinline__ double lapy2(double x, double y) {
 
 // ---------------------------------------------------------------------------
 // Interpolative decomposition of one p x w matrix M (rows = candidates), hss.py:120-148.
-// Column-pivoted QR of A = M^T (w x p): the candidate rows of M are the columns of A
-// and are stored contiguously in shared memory (sA[j*w + t] = A[t][j]).
+// Column-pivoted QR of A = M^T (w x p): candidate j of M is column j of A, stored
+// contiguously in shared memory (sA[j*SW + t] = A[t][j], SW odd => conflict-free when
+// consecutive threads own consecutive candidates).
+// Per elimination step: warp 0 picks the pivot (first max of the downdated norms,
+// idamax) and forms the Householder reflector (dlarfg); then every thread owns one
+// trailing candidate and applies the reflector and the dlaqp2 norm downdate to it.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double tol,
                                                  const double* __restrict__ om, int64_t ldom,
                                                  hsseig_status* st) {
   extern __shared__ __align__(16) double sm[];
   const int j = blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5, nthr = blockDim.x;
   const int node = T.lnodes[(1 << level) - 1 + j];
   const bool leaf = T.left[node] < 0;
-  const int w = T.w, ws = T.ws;
+  const int w = T.w, ws = T.ws, SW = w | 1;
   int p;
   if (leaf) p = T.hi[node] - T.lo[node];
   else {
@@ -175,34 +180,36 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
     p = side == 0 ? T.rU[a] + T.rU[b] : T.rV[a] + T.rV[b];
   }
   const double* Mg = T.M + (size_t)(2 * j + side) * T.pmax * ws;
-  double* sA = sm;                              // p x w
-  double* vn1 = sA + (size_t)T.pmax * w;        // p
+  double* sA = sm;                              // p x SW
+  double* vn1 = sA + (size_t)T.pmax * SW;       // p
   double* vn2 = vn1 + T.pmax;                   // p
   double* tail = vn2 + T.pmax;                  // w + 1
   double* red = tail + (w + 1);                 // 32 scratch
   int* piv = reinterpret_cast<int*>(red + 32);  // p
-  __shared__ double s_tau, s_nf;
+  __shared__ double s_tau, s_nf, s_resid;
   __shared__ int s_r, s_sat;
-  __shared__ double s_resid;
 
-  for (int e = tid; e < p * w; e += blockDim.x) {
+  for (int e = tid; e < p * w; e += nthr) {
     int row = e / w, c = e % w;
-    sA[e] = Mg[(size_t)row * ws + c];
+    sA[row * SW + c] = Mg[(size_t)row * ws + c];
   }
-  for (int e = tid; e < p; e += blockDim.x) piv[e] = e;
+  for (int e = tid; e < p; e += nthr) piv[e] = e;
   __syncthreads();
-  // Frobenius norm (hss.py:128) and initial column norms (dgeqp3: dnrm2 of each column)
+  // Frobenius norm (hss.py:128) and the initial column norms (dgeqp3: dnrm2 per column)
   {
     double s = 0.0;
-    for (int e = tid; e < p * w; e += blockDim.x) s = fma(sA[e], sA[e], s);
+    for (int c = tid; c < p; c += nthr) {
+      const double* a = sA + c * SW;
+      double q0 = 0.0, q1 = 0.0;
+      int t = 0;
+      for (; t + 1 < w; t += 2) { q0 = fma(a[t], a[t], q0); q1 = fma(a[t + 1], a[t + 1], q1); }
+      if (t < w) q0 = fma(a[t], a[t], q0);
+      double q = q0 + q1;
+      vn1[c] = vn2[c] = sqrt(q);
+      s += q;
+    }
     s = warp_sum(s);
     if (lane == 0) red[warp] = s;
-  }
-  for (int c = warp; c < p; c += nwarps) {
-    double s = 0.0;
-    for (int t = lane; t < w; t += 32) s = fma(sA[c * w + t], sA[c * w + t], s);
-    s = sqrt(warp_sum(s));
-    if (lane == 0) { vn1[c] = s; vn2[c] = s; }
   }
   __syncthreads();
   if (tid == 0) {
@@ -218,7 +225,6 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
   if (!(nf == 0.0 || p == 0 || w == 0)) {
     for (int i = 0; i < mn; ++i) {
       if (warp == 0) {
-        // pivot: first index of the largest partial norm (idamax)
         double best = -1.0;
         int bi = i;
         for (int c = i + lane; c < p; c += 32) {
@@ -234,9 +240,9 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
         const int pvt = bi;
         if (pvt != i) {
           for (int t = lane; t < w; t += 32) {
-            double x0 = sA[i * w + t];
-            sA[i * w + t] = sA[pvt * w + t];
-            sA[pvt * w + t] = x0;
+            double x0 = sA[i * SW + t];
+            sA[i * SW + t] = sA[pvt * SW + t];
+            sA[pvt * SW + t] = x0;
           }
           if (lane == 0) {
             int tp = piv[pvt]; piv[pvt] = piv[i]; piv[i] = tp;
@@ -245,17 +251,16 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
           }
         }
         __syncwarp();
-        // Householder reflector for column i (dlarfg on A[i:, i])
-        double* col = sA + i * w;
+        double* col = sA + i * SW;
         double xs = 0.0;
         for (int t = i + 1 + lane; t < w; t += 32) xs = fma(col[t], col[t], xs);
-        double xnorm = sqrt(warp_sum(xs));
-        double alpha = col[i];
+        const double xnorm = sqrt(warp_sum(xs));
+        const double alpha = col[i];
         double tau = 0.0, beta = alpha;
         if (xnorm != 0.0) {
           beta = -copysign(lapy2(alpha, xnorm), alpha);
           tau = (beta - alpha) / beta;
-          double scal = 1.0 / (alpha - beta);
+          const double scal = 1.0 / (alpha - beta);
           for (int t = i + 1 + lane; t < w; t += 32) col[t] *= scal;
         }
         __syncwarp();
@@ -265,46 +270,43 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
         }
       }
       __syncthreads();
-      // apply H_i^T to the trailing columns and downdate their partial norms (dlaqp2)
       const double tau = s_tau;
-      const double* v = sA + i * w;
-      for (int c = i + 1 + warp; c < p; c += nwarps) {
-        double* a = sA + c * w;
+      const double* v = sA + i * SW;
+      for (int c = i + 1 + tid; c < p; c += nthr) {
+        double* a = sA + c * SW;
         if (tau != 0.0) {
-          double dsum = 0.0;
-          for (int t = i + lane; t < w; t += 32) dsum = fma(t == i ? 1.0 : v[t], a[t], dsum);
-          dsum = warp_sum(dsum);
-          double f = tau * dsum;
-          for (int t = i + lane; t < w; t += 32) a[t] = fma(-f, t == i ? 1.0 : v[t], a[t]);
+          double d0 = a[i], d1 = 0.0;
+          int t = i + 1;
+          for (; t + 1 < w; t += 2) { d0 = fma(v[t], a[t], d0); d1 = fma(v[t + 1], a[t + 1], d1); }
+          if (t < w) d0 = fma(v[t], a[t], d0);
+          const double f = tau * (d0 + d1);
+          a[i] -= f;
+          for (t = i + 1; t < w; ++t) a[t] = fma(-f, v[t], a[t]);
         }
-        __syncwarp();
-        double n1 = vn1[c];
+        const double n1 = vn1[c];
         if (n1 != 0.0) {
-          double q = fabs(a[i]) / n1;
-          double temp = fmax(1.0 - q * q, 0.0);
-          double ratio = n1 / vn2[c];
-          double temp2 = temp * ratio * ratio;
-          if (temp2 <= kTol3z) {
-            double s = 0.0;
-            for (int t = i + 1 + lane; t < w; t += 32) s = fma(a[t], a[t], s);
-            s = sqrt(warp_sum(s));
-            if (lane == 0) {
-              double nv = (i + 1 < w) ? s : 0.0;
-              vn1[c] = nv;
-              vn2[c] = nv;
-            }
-          } else if (lane == 0) {
+          const double q = fabs(a[i]) / n1;
+          const double temp = fmax(1.0 - q * q, 0.0);
+          const double ratio = n1 / vn2[c];
+          if (temp * ratio * ratio <= kTol3z) {
+            double s0 = 0.0, s1 = 0.0;
+            int t = i + 1;
+            for (; t + 1 < w; t += 2) { s0 = fma(a[t], a[t], s0); s1 = fma(a[t + 1], a[t + 1], s1); }
+            if (t < w) s0 = fma(a[t], a[t], s0);
+            const double nv = (i + 1 < w) ? sqrt(s0 + s1) : 0.0;
+            vn1[c] = nv;
+            vn2[c] = nv;
+          } else {
             vn1[c] = n1 * sqrt(temp);
           }
         }
-        __syncwarp();
       }
       __syncthreads();
     }
     // trailing Frobenius mass of R's rows, cumulated from the bottom (hss.py:134-136)
     for (int t = warp; t < mn; t += nwarps) {
       double s = 0.0;
-      for (int c = t + lane; c < p; c += 32) s = fma(sA[c * w + t], sA[c * w + t], s);
+      for (int c = t + lane; c < p; c += 32) s = fma(sA[c * SW + t], sA[c * SW + t], s);
       s = warp_sum(s);
       if (lane == 0) tail[t] = s;
     }
@@ -321,34 +323,35 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
       for (int t = 0; t <= mn; ++t)
         if (tail[t] <= cut) { wanted = t; break; }
       int nz = 0;
-      for (int t = 0; t < mn; ++t) nz += (fabs(sA[t * w + t]) > 0.0) ? 1 : 0;
-      int rr = min(min(wanted, w), nz);
-      int sflag = 0;
-      if (wanted >= w) sflag = sqrt(fmax(tail[w - 1], 0.0)) > kFlagTol * nf ? 1 : 0;
+      for (int t = 0; t < mn; ++t) nz += (fabs(sA[t * SW + t]) > 0.0) ? 1 : 0;
+      const int rr = min(min(wanted, w), nz);
       s_r = rr;
-      s_sat = sflag;
+      s_sat = (wanted >= w) ? (sqrt(fmax(tail[w - 1], 0.0)) > kFlagTol * nf ? 1 : 0) : 0;
       s_resid = sqrt(fmax(tail[rr], 0.0)) / nf;
     }
     __syncthreads();
     r = s_r;
     sat = s_sat;
     resid = s_resid;
-    // T = R[:r,:r]^{-1} R[:r, r:], in place, column-oriented back substitution (dtrsm L/U/N/N)
-    for (int c = r + tid; c < p; c += blockDim.x) {
-      double* x = sA + c * w;
+    // T = R[:r,:r]^{-1} R[:r, r:] in place, column-oriented back substitution (dtrsm L/U/N/N)
+    for (int c = r + tid; c < p; c += nthr) {
+      double* x = sA + c * SW;
       for (int t = r - 1; t >= 0; --t) {
-        double xt = x[t] / sA[t * w + t];
+        const double xt = x[t] / sA[t * SW + t];
         x[t] = xt;
-        if (xt != 0.0)
-          for (int s2 = 0; s2 < t; ++s2) x[s2] = fma(-xt, sA[t * w + s2], x[s2]);
+        if (xt != 0.0) {
+          const double* rc = sA + t * SW;
+          for (int s2 = 0; s2 < t; ++s2) x[s2] = fma(-xt, rc[s2], x[s2]);
+        }
       }
     }
     __syncthreads();
   }
 
-  // ---- outputs: basis X (p x r), skeleton indices, selected rows, compressions
+  // ---- outputs: basis X (p x r) (+ X^T for V), skeleton indices, selected rows, compressions
   int32_t* rank_arr = side == 0 ? T.rU : T.rV;
   double* X = (side == 0 ? T.U : T.V) + slot_pw(T, node);
+  double* Xt = T.Vt + (size_t)node * T.ws * T.pmax;
   int32_t* loc = (side == 0 ? T.rloc : T.cloc) + (size_t)node * ws;
   int32_t* sel = (side == 0 ? T.rsel : T.csel) + (size_t)node * ws;
   double* selrows = (side == 0 ? T.psel : T.tsel) + slot_ww(T, node);
@@ -360,43 +363,57 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
     if (sat) atomicAdd(reinterpret_cast<unsigned long long*>(&st->v[4]), 1ull);
     atomicMax(reinterpret_cast<long long*>(&st->v[5]), (long long)r);
   }
-  for (int e = tid; e < p * r; e += blockDim.x) {
-    int jj = e / r, t = e % r;  // jj = position in pivoted order
-    double val = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * w + t];
+  for (int e = tid; e < p * r; e += nthr) {
+    const int jj = e / r, t = e % r;  // jj = position in pivoted order
+    const double val = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * SW + t];
     X[(size_t)piv[jj] * ws + t] = val;
+    if (side == 1) Xt[(size_t)t * T.pmax + piv[jj]] = val;
   }
-  for (int t = tid; t < r; t += blockDim.x) {
-    int pj = piv[t];
+  for (int t = tid; t < r; t += nthr) {
+    const int pj = piv[t];
     loc[t] = pj;
     int gsel;
     if (leaf) gsel = T.lo[node] + pj;
     else {
-      int a = T.left[node], b = T.right[node];
+      const int a = T.left[node], b = T.right[node];
       const int32_t* sa = (side == 0 ? T.rsel : T.csel) + (size_t)a * ws;
       const int32_t* sb = (side == 0 ? T.rsel : T.csel) + (size_t)b * ws;
-      int na = side == 0 ? T.rU[a] : T.rV[a];
+      const int na = side == 0 ? T.rU[a] : T.rV[a];
       gsel = pj < na ? sa[pj] : sb[pj - na];
     }
     sel[t] = gsel;
   }
-  for (int e = tid; e < r * w; e += blockDim.x) {
-    int t = e / w, c = e % w;
+  for (int e = tid; e < r * w; e += nthr) {
+    const int t = e / w, c = e % w;
     selrows[(size_t)t * ws + c] = Mg[(size_t)piv[t] * ws + c];
   }
-  // comp = X^T S, S = Omega_t (leaf) or [comp_a; comp_b] (inner)   (hss.py:281-282, 295-296)
-  for (int e = tid; e < r * w; e += blockDim.x) {
-    int t = e / w, c = e % w;
-    auto srow = [&](int q) -> double {
-      if (leaf) return om[(int64_t)(T.lo[node] + q) * ldom + c];
-      int a = T.left[node], b = T.right[node];
-      int na = side == 0 ? T.rU[a] : T.rV[a];
-      const double* ca = (side == 0 ? T.zcomp : T.ycomp) + slot_ww(T, a);
-      const double* cb = (side == 0 ? T.zcomp : T.ycomp) + slot_ww(T, b);
-      return q < na ? ca[(size_t)q * ws + c] : cb[(size_t)(q - na) * ws + c];
-    };
-    double s = srow(piv[t]);
-    for (int jj = r; jj < p; ++jj) s = fma(sA[jj * w + t], srow(piv[jj]), s);
-    comp[(size_t)t * ws + c] = s;
+  // comp = X^T S with S = Omega_t (leaf) or [comp_a; comp_b] (inner)   (hss.py:281-282, 295-296)
+  const double* Sa;
+  const double* Sb;
+  int64_t lds;
+  int na = p;
+  if (leaf) {
+    Sa = om + (int64_t)T.lo[node] * ldom;
+    Sb = Sa;
+    lds = ldom;
+  } else {
+    const int a = T.left[node], b = T.right[node];
+    na = side == 0 ? T.rU[a] : T.rV[a];
+    Sa = (side == 0 ? T.zcomp : T.ycomp) + slot_ww(T, a);
+    Sb = (side == 0 ? T.zcomp : T.ycomp) + slot_ww(T, b);
+    lds = ws;
+  }
+  for (int t = warp; t < r; t += nwarps) {
+    for (int c = lane; c < w; c += 32) {
+      int q = piv[t];
+      double s = q < na ? Sa[(int64_t)q * lds + c] : Sb[(int64_t)(q - na) * lds + c];
+      for (int jj = r; jj < p; ++jj) {
+        q = piv[jj];
+        const double srow = q < na ? Sa[(int64_t)q * lds + c] : Sb[(int64_t)(q - na) * lds + c];
+        s = fma(sA[jj * SW + t], srow, s);
+      }
+      comp[(size_t)t * ws + c] = s;
+    }
   }
 }
 
@@ -408,7 +425,7 @@ static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 struct TreeCarve {
   int64_t off_lo, off_hi, off_left, off_right, off_lnodes, off_rU, off_rV, off_rsel, off_csel,
-      off_rloc, off_cloc, off_flags, off_U, off_V, off_B, off_D, off_rres, off_cres, off_M,
+      off_rloc, off_cloc, off_flags, off_U, off_V, off_Vt, off_B, off_D, off_rres, off_cres, off_M,
       off_psel, off_tsel, off_ycomp, off_zcomp, total;
 };
 
@@ -416,7 +433,9 @@ static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
   TreeCarve c;
   const int64_t nn = 2 * (int64_t)n_leaves - 1;
   const int64_t ws = w + (w & 1);
-  const int64_t pmax = std::max<int64_t>(mmax, 2 * (int64_t)w);
+  int64_t pmax = std::max<int64_t>(mmax, 2 * (int64_t)w);
+  pmax += pmax & 1;
+  const int64_t dld = mmax + (mmax & 1);
   int64_t o = 0;
   auto take = [&](int64_t bytes) { int64_t at = o; o = align_up(o + bytes, 256); return at; };
   c.off_lo = take(4 * nn); c.off_hi = take(4 * nn); c.off_left = take(4 * nn);
@@ -426,7 +445,8 @@ static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
   c.off_rloc = take(4 * nn * ws); c.off_cloc = take(4 * nn * ws);
   c.off_flags = take(4 * 2 * nn);
   c.off_U = take(8 * nn * pmax * ws); c.off_V = take(8 * nn * pmax * ws);
-  c.off_B = take(8 * nn * ws * ws); c.off_D = take(8 * (int64_t)n_leaves * mmax * mmax);
+  c.off_Vt = take(8 * nn * ws * pmax);
+  c.off_B = take(8 * nn * ws * ws); c.off_D = take(8 * (int64_t)n_leaves * dld * dld);
   c.off_rres = take(8 * nn); c.off_cres = take(8 * nn);
   c.off_M = take(8 * 2 * (int64_t)n_leaves * pmax * ws);
   c.off_psel = take(8 * nn * ws * ws); c.off_tsel = take(8 * nn * ws * ws);
@@ -482,7 +502,9 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
   t->k = k; t->n_leaves = n_leaves; t->depth = depth; t->n_nodes = nn; t->w = w;
   t->ws = w + (w & 1);
   t->pmax = std::max<int32_t>(mmax, 2 * w);
+  t->pmax += t->pmax & 1;
   t->mmax = mmax;
+  t->dld = mmax + (mmax & 1);
   t->root = root;
   for (int l = 0; l <= depth && l < 31; ++l) t->level_off_h[l] = (1 << l) - 1;
   t->lo = reinterpret_cast<int32_t*>(base + c.off_lo);
@@ -500,6 +522,7 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
   t->flags = reinterpret_cast<int32_t*>(base + c.off_flags);
   t->U = reinterpret_cast<double*>(base + c.off_U);
   t->V = reinterpret_cast<double*>(base + c.off_V);
+  t->Vt = reinterpret_cast<double*>(base + c.off_Vt);
   t->B = reinterpret_cast<double*>(base + c.off_B);
   t->D = reinterpret_cast<double*>(base + c.off_D);
   t->rres = reinterpret_cast<double*>(base + c.off_rres);
@@ -538,7 +561,8 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
   g.v = gen->v; g.k = gen->k;
   TreeDev T = to_dev(tree);
   const size_t smem_leaf = sizeof(double) * ((size_t)T.mmax * T.w + 16 * (size_t)T.mmax);
-  const size_t smem_id = sizeof(double) * ((size_t)T.pmax * T.w + 2 * T.pmax + T.w + 1 + 32) +
+  if (T.pmax > 4096) return HSSEIG_ERR_ARG;
+  const size_t smem_id = sizeof(double) * ((size_t)T.pmax * (T.w | 1) + 2 * T.pmax + T.w + 1 + 32) +
                          sizeof(int) * T.pmax + 64;
   if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024) return HSSEIG_ERR_ARG;
   cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);

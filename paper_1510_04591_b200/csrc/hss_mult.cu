@@ -10,6 +10,8 @@
 //   final     : out[:, t_i] = [X[:, t_i] | F_i] [D_i ; V_i^T]
 // Job descriptors are built on the device from the ranks the construction wrote,
 // so no host synchronisation is needed between construction and multiply.
+#include <cstdlib>
+
 #include "dmma_gemm.cuh"
 
 namespace hsseig {
@@ -24,53 +26,116 @@ struct GemmJob {
   int32_t K1, K2, N, pad;
 };
 
+// Persistent batched two-segment GEMM.  CTA c walks the (job, row-tile) list
+// c, c + gridDim.x, ...; the (tile, k-chunk) sequence is one continuous cp.async
+// pipeline, so the next tile's operands stream in while this tile's last chunks
+// are multiplied and its accumulators are stored.
+template <class T>
+struct Seg {
+  const double* A;
+  const double* B;
+  int64_t lda, ldb;
+  int K;
+  bool a16, b16;
+};
+
+template <class T>
+__device__ __forceinline__ void job_seg(const GemmJob& jb, int c, int nc1, Seg<T>& sg, int& k0) {
+  if (c < nc1) {
+    sg.A = jb.A1; sg.B = jb.B1; sg.lda = jb.lda1; sg.ldb = jb.b1r; sg.K = jb.K1;
+    k0 = c * T::BK;
+  } else {
+    sg.A = jb.A2; sg.B = jb.B2; sg.lda = jb.lda2; sg.ldb = jb.b2r; sg.K = jb.K2;
+    k0 = (c - nc1) * T::BK;
+  }
+  sg.a16 = ((reinterpret_cast<uintptr_t>(sg.A) & 15) == 0) && ((sg.lda & 1) == 0);
+  sg.b16 = ((reinterpret_cast<uintptr_t>(sg.B) & 15) == 0) && ((sg.ldb & 1) == 0);
+}
+
 template <class T>
 __global__ void __launch_bounds__(T::THREADS) batched_gemm2_kernel(const GemmJob* __restrict__ jobs,
-                                                                   int64_t M) {
+                                                                   int njobs, int64_t M,
+                                                                   int tiles_m) {
   extern __shared__ __align__(16) double smem[];
-  const GemmJob jb = jobs[blockIdx.y];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / T::WN, wn = warp % T::WN;
-  const int64_t m0 = (int64_t)blockIdx.x * T::BM;
-  if (jb.N <= 0) return;
-  const int nc1 = (jb.K1 + T::BK - 1) / T::BK, nc2 = (jb.K2 + T::BK - 1) / T::BK;
-  const int nch = nc1 + nc2;
-  Acc<T> acc;
-  acc.zero();
+  const int total = njobs * tiles_m;
   auto sa = [&](int s) { return smem + s * T::STAGE_ELEMS; };
   auto sb = [&](int s) { return smem + s * T::STAGE_ELEMS + T::A_ELEMS; };
-  auto produce = [&](int c, int s) {
-    if (c < nc1) {
-      const int k0 = c * T::BK;
-      load_a_async<T>(sa(s), jb.A1, jb.lda1, M, m0, jb.K1, k0, tid);
-      load_b_async<T>(sb(s), jb.B1, jb.b1r, jb.b1c, jb.K1, k0, jb.N, 0, tid);
-    } else {
-      const int k0 = (c - nc1) * T::BK;
-      load_a_async<T>(sa(s), jb.A2, jb.lda2, M, m0, jb.K2, k0, tid);
-      load_b_async<T>(sb(s), jb.B2, jb.b2r, jb.b2c, jb.K2, k0, jb.N, 0, tid);
+
+  // producer cursor
+  int pt = blockIdx.x, pc = 0, pslot = 0;
+  GemmJob pj;
+  int pnc1 = 0, pnch = 0;
+  auto load_pjob = [&]() {
+    if (pt < total) {
+      pj = jobs[pt / tiles_m];
+      pnc1 = (pj.K1 + T::BK - 1) / T::BK;
+      pnch = pj.N > 0 ? pnc1 + (pj.K2 + T::BK - 1) / T::BK : 0;
     }
   };
-#pragma unroll
-  for (int s = 0; s < T::STAGES - 1; ++s) {
-    if (s < nch) produce(s, s);
+  load_pjob();
+  auto produce = [&]() {
+    while (pt < total && pc >= pnch) {  // skip empty tiles
+      pt += gridDim.x;
+      pc = 0;
+      load_pjob();
+    }
+    if (pt < total) {
+      Seg<T> sg;
+      int k0;
+      job_seg<T>(pj, pc, pnc1, sg, k0);
+      const int64_t m0 = (int64_t)(pt % tiles_m) * T::BM;
+      if (sg.a16) load_a_async16<T>(sa(pslot), sg.A, sg.lda, M, m0, sg.K, k0, tid);
+      else load_a_async<T>(sa(pslot), sg.A, sg.lda, M, m0, sg.K, k0, tid);
+      if (sg.b16) load_b_async16<T>(sb(pslot), sg.B, sg.ldb, sg.K, k0, pj.N, tid);
+      else load_b_async<T>(sb(pslot), sg.B, sg.ldb, 1, sg.K, k0, pj.N, 0, tid);
+      if (++pc >= pnch) {
+        pt += gridDim.x;
+        pc = 0;
+        load_pjob();
+      }
+    }
     cp_async_commit();
-  }
-  for (int c = 0; c < nch; ++c) {
-    cp_async_wait<T::STAGES - 2>();
-    __syncthreads();
-    const int pf = c + T::STAGES - 1;
-    if (pf < nch) produce(pf, pf % T::STAGES);
-    cp_async_commit();
-    mma_chunk<T>(sa(c % T::STAGES), sb(c % T::STAGES), acc, wm, wn, lane);
+    pslot = (pslot + 1) % T::STAGES;
+  };
+
+#pragma unroll 1
+  for (int s = 0; s < T::STAGES - 1; ++s) produce();
+
+  // consumer cursor
+  int ct = blockIdx.x, cslot = 0;
+  Acc<T> acc;
+  while (ct < total) {
+    const GemmJob cj = jobs[ct / tiles_m];
+    const int nc1 = (cj.K1 + T::BK - 1) / T::BK;
+    const int nch = cj.N > 0 ? nc1 + (cj.K2 + T::BK - 1) / T::BK : 0;
+    if (nch == 0) { ct += gridDim.x; continue; }
+    const int64_t m0 = (int64_t)(ct % tiles_m) * T::BM;
+    const int jmax = max(0, min(T::NF, (cj.N - wn * T::NF * 8 + 7) / 8));
+    acc.zero();
+    for (int c = 0; c < nch; ++c) {
+      cp_async_wait<T::STAGES - 2>();
+      __syncthreads();
+      produce();
+      const int kseg = c < nc1 ? cj.K1 - c * T::BK : cj.K2 - (c - nc1) * T::BK;
+      const int kv = min(T::BK, (kseg + 3) & ~3);
+      if (kv == T::BK && jmax == T::NF)
+        mma_chunk<T>(sa(cslot), sb(cslot), acc, wm, wn, lane);
+      else
+        mma_chunk_part<T>(sa(cslot), sb(cslot), acc, wm, wn, lane, kv, jmax);
+      cslot = (cslot + 1) % T::STAGES;
+    }
+    store_acc<T>(acc, cj.C, cj.ldc, M, m0, cj.N, 0, wm, wn, lane);
+    ct += gridDim.x;
   }
   cp_async_wait<0>();
-  store_acc<T>(acc, jb.C, jb.ldc, M, m0, jb.N, 0, wm, wn, lane);
 }
 
 struct MultPlan {
-  int32_t depth, n_leaves, ws, pmax, mmax;
+  int32_t depth, n_leaves, ws, pmax, mmax, dld;
   const int32_t *lo, *hi, *left, *right, *lnodes, *rU, *rV;
-  const double *U, *V, *B, *D;
+  const double *U, *V, *Vt, *B, *D;
   const double* X;
   int64_t ldx;
   double* out;
@@ -145,8 +210,8 @@ __global__ void setup_jobs_kernel(MultPlan p, GemmJob* __restrict__ jobs) {
         jb.A2 = lvl_buf(p.Fb, p.P, ws, l - 1) + (int64_t)(j >> 1) * ws;
         jb.lda2 = (int64_t)(1 << (l - 1)) * ws;
         jb.K2 = p.rV[par];
-        jb.B2 = p.V + (size_t)par * pw + (size_t)off * ws;
-        jb.b2r = 1; jb.b2c = ws;
+        jb.B2 = p.Vt + (size_t)par * ws * p.pmax + off;   // V_par[off:off+rV, :]^T
+        jb.b2r = p.pmax; jb.b2c = 1;
       }
     }
   } else {
@@ -157,13 +222,13 @@ __global__ void setup_jobs_kernel(MultPlan p, GemmJob* __restrict__ jobs) {
     jb.A1 = p.X + lo;
     jb.lda1 = p.ldx;
     jb.K1 = p.hi[node] - lo;
-    jb.B1 = p.D + (size_t)j * p.mmax * p.mmax;
-    jb.b1r = p.mmax; jb.b1c = 1;
+    jb.B1 = p.D + (size_t)j * p.dld * p.dld;
+    jb.b1r = p.dld; jb.b1c = 1;
     jb.A2 = lvl_buf(p.Fb, p.P, ws, p.depth) + (int64_t)j * ws;
     jb.lda2 = (int64_t)(1 << p.depth) * ws;
     jb.K2 = p.rV[node];
-    jb.B2 = p.V + (size_t)node * pw;
-    jb.b2r = 1; jb.b2c = ws;
+    jb.B2 = p.Vt + (size_t)node * ws * p.pmax;
+    jb.b2r = p.pmax; jb.b2c = 1;
     jb.C = p.out + lo;
     jb.ldc = p.ldo;
     jb.N = p.hi[node] - lo;
@@ -171,48 +236,101 @@ __global__ void setup_jobs_kernel(MultPlan p, GemmJob* __restrict__ jobs) {
   jobs[e] = jb;
 }
 
+static int g_sms = 0;
+
 template <class T>
 static int launch_batched(const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
   if (njobs <= 0 || M <= 0) return HSSEIG_OK;
-  static bool attr = false;
-  if (!attr) {
+  static int per_sm = 0;
+  if (!per_sm) {
     cudaFuncSetAttribute(batched_gemm2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)T::SMEM_BYTES);
-    attr = true;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batched_gemm2_kernel<T>, T::THREADS,
+                                                  T::SMEM_BYTES);
+    if (per_sm < 1) per_sm = 1;
+    if (!g_sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
   }
-  dim3 grid((unsigned)((M + T::BM - 1) / T::BM), (unsigned)njobs);
-  batched_gemm2_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(jobs, M);
+  const int tiles_m = (int)((M + T::BM - 1) / T::BM);
+  const int64_t total = (int64_t)tiles_m * njobs;
+  const int grid = (int)imin64(total, (int64_t)g_sms * per_sm);
+  batched_gemm2_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(jobs, njobs, M, tiles_m);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
 
-// narrow outputs (ranks): BM = 128, BN = 16*NF
-static int launch_narrow(int nf, const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
-  switch (nf) {
-    case 1: return launch_batched<Tile<4, 1, 4, 2>>(jobs, njobs, M, s);
-    case 2: return launch_batched<Tile<4, 2, 4, 2>>(jobs, njobs, M, s);
-    case 3: return launch_batched<Tile<4, 3, 4, 2>>(jobs, njobs, M, s);
-    case 4: return launch_batched<Tile<4, 4, 4, 2>>(jobs, njobs, M, s);
-    case 5: return launch_batched<Tile<4, 5, 4, 2>>(jobs, njobs, M, s);
-    case 6: return launch_batched<Tile<4, 6, 4, 2>>(jobs, njobs, M, s);
-    case 7: return launch_batched<Tile<4, 7, 4, 2>>(jobs, njobs, M, s);
+// Tile variants (HSSEIG_TILE_NARROW / HSSEIG_TILE_WIDE select one for tuning runs).
+static int tile_choice(const char* var, int dflt) {
+  const char* v = getenv(var);
+  return v ? atoi(v) : dflt;
+}
+
+// narrow outputs (ranks, N <= 112)
+static int launch_narrow(int n, const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
+  static const int variant = tile_choice("HSSEIG_TILE_NARROW", 1);
+  if (variant == 0) {   // BM 128, 8 warps of 32 x 8NF, NF = ceil(n/16)
+    switch ((n + 15) / 16) {
+      case 1: return launch_batched<Tile<4, 1, 4, 2, 4>>(jobs, njobs, M, s);
+      case 2: return launch_batched<Tile<4, 2, 4, 2, 4>>(jobs, njobs, M, s);
+      case 3: return launch_batched<Tile<4, 3, 4, 2, 4>>(jobs, njobs, M, s);
+      case 4: return launch_batched<Tile<4, 4, 4, 2, 4>>(jobs, njobs, M, s);
+      case 5: return launch_batched<Tile<4, 5, 4, 2, 4>>(jobs, njobs, M, s);
+      case 6: return launch_batched<Tile<4, 6, 4, 2, 4>>(jobs, njobs, M, s);
+      case 7: return launch_batched<Tile<4, 7, 4, 2, 4>>(jobs, njobs, M, s);
+      default: return HSSEIG_ERR_ARG;
+    }
+  }
+  if (variant == 2) {   // BM 64, 4 warps of 32 x 8NF, NF = ceil(n/16)
+    switch ((n + 15) / 16) {
+      case 1: return launch_batched<Tile<4, 1, 2, 2, 4>>(jobs, njobs, M, s);
+      case 2: return launch_batched<Tile<4, 2, 2, 2, 4>>(jobs, njobs, M, s);
+      case 3: return launch_batched<Tile<4, 3, 2, 2, 4>>(jobs, njobs, M, s);
+      case 4: return launch_batched<Tile<4, 4, 2, 2, 4>>(jobs, njobs, M, s);
+      case 5: return launch_batched<Tile<4, 5, 2, 2, 4>>(jobs, njobs, M, s);
+      case 6: return launch_batched<Tile<4, 6, 2, 2, 4>>(jobs, njobs, M, s);
+      case 7: return launch_batched<Tile<4, 7, 2, 2, 4>>(jobs, njobs, M, s);
+      default: return HSSEIG_ERR_ARG;
+    }
+  }
+  // default: BM 64, 8 warps of 32 x 8NF, NF = ceil(n/32)
+  switch ((n + 31) / 32) {
+    case 1: return launch_batched<Tile<4, 1, 2, 4, 4>>(jobs, njobs, M, s);
+    case 2: return launch_batched<Tile<4, 2, 2, 4, 4>>(jobs, njobs, M, s);
+    case 3: return launch_batched<Tile<4, 3, 2, 4, 4>>(jobs, njobs, M, s);
+    case 4: return launch_batched<Tile<4, 4, 2, 4, 4>>(jobs, njobs, M, s);
     default: return HSSEIG_ERR_ARG;
   }
 }
 
-// wide outputs (leaf finish, plain GEMM tiles): BM = 64, BN = 16*NF
-static int launch_wide(int nf, const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
-  switch (nf) {
-    case 1: case 2: case 3: case 4: return launch_batched<Tile<2, 4, 4, 2>>(jobs, njobs, M, s);
-    case 5: return launch_batched<Tile<2, 5, 4, 2>>(jobs, njobs, M, s);
-    case 6: return launch_batched<Tile<2, 6, 4, 2>>(jobs, njobs, M, s);
-    case 7: return launch_batched<Tile<2, 7, 4, 2>>(jobs, njobs, M, s);
-    case 8: return launch_batched<Tile<2, 8, 4, 2>>(jobs, njobs, M, s);
-    case 9: return launch_batched<Tile<2, 9, 4, 2>>(jobs, njobs, M, s);
-    case 10: return launch_batched<Tile<2, 10, 4, 2>>(jobs, njobs, M, s);
-    case 11: return launch_batched<Tile<2, 11, 4, 2>>(jobs, njobs, M, s);
-    case 12: return launch_batched<Tile<2, 12, 4, 2>>(jobs, njobs, M, s);
-    case 13: return launch_batched<Tile<2, 13, 4, 2>>(jobs, njobs, M, s);
+// wide outputs (leaf finish N = leaf size; plain GEMM tiles)
+static int launch_wide(int n, const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
+  static const int variant = tile_choice("HSSEIG_TILE_WIDE", 1);
+  if (variant == 0) {   // BM 64, 8 warps of 16 x 8NF, NF = ceil(n/16)
+    switch ((n + 15) / 16) {
+      case 1: case 2: case 3: case 4: return launch_batched<Tile<2, 4, 4, 2, 4>>(jobs, njobs, M, s);
+      case 5: return launch_batched<Tile<2, 5, 4, 2, 4>>(jobs, njobs, M, s);
+      case 6: return launch_batched<Tile<2, 6, 4, 2, 4>>(jobs, njobs, M, s);
+      case 7: return launch_batched<Tile<2, 7, 4, 2, 4>>(jobs, njobs, M, s);
+      case 8: return launch_batched<Tile<2, 8, 4, 2, 4>>(jobs, njobs, M, s);
+      case 9: return launch_batched<Tile<2, 9, 4, 2, 4>>(jobs, njobs, M, s);
+      case 10: return launch_batched<Tile<2, 10, 4, 2, 3>>(jobs, njobs, M, s);
+      case 11: return launch_batched<Tile<2, 11, 4, 2, 3>>(jobs, njobs, M, s);
+      case 12: return launch_batched<Tile<2, 12, 4, 2, 3>>(jobs, njobs, M, s);
+      case 13: return launch_batched<Tile<2, 13, 4, 2, 3>>(jobs, njobs, M, s);
+      default: return HSSEIG_ERR_ARG;
+    }
+  }
+  // default: BM 64, 8 warps of 32 x 8NF, NF = ceil(n/32)
+  switch ((n + 31) / 32) {
+    case 1: case 2: return launch_batched<Tile<4, 2, 2, 4, 4>>(jobs, njobs, M, s);
+    case 3: return launch_batched<Tile<4, 3, 2, 4, 4>>(jobs, njobs, M, s);
+    case 4: return launch_batched<Tile<4, 4, 2, 4, 4>>(jobs, njobs, M, s);
+    case 5: return launch_batched<Tile<4, 5, 2, 4, 3>>(jobs, njobs, M, s);
+    case 6: return launch_batched<Tile<4, 6, 2, 4, 3>>(jobs, njobs, M, s);
+    case 7: return launch_batched<Tile<4, 7, 2, 4, 3>>(jobs, njobs, M, s);
     default: return HSSEIG_ERR_ARG;
   }
 }
@@ -250,6 +368,7 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   const int64_t lvl_total = P * (int64_t)t->ws * (2 * (int64_t)t->n_leaves - 2);
   MultPlan p;
   p.depth = t->depth; p.n_leaves = t->n_leaves; p.ws = t->ws; p.pmax = t->pmax; p.mmax = t->mmax;
+  p.dld = t->dld; p.Vt = t->Vt;
   p.lo = t->lo; p.hi = t->hi; p.left = t->left; p.right = t->right; p.lnodes = t->level_nodes;
   p.rU = t->rU; p.rV = t->rV; p.U = t->U; p.V = t->V; p.B = t->B; p.D = t->D;
   p.X = X; p.ldx = ldx; p.out = out; p.ldo = ldo; p.P = P;
@@ -260,13 +379,12 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   const int total = 2 * nup + n;
   setup_jobs_kernel<<<(total + 127) / 128, 128, 0, s>>>(p, jobs);
   HSS_CHECK_LAUNCH();
-  const int nf = (t->w + 15) / 16;
   int rc;
   for (int l = t->depth; l >= 1; --l)
-    if ((rc = launch_narrow(nf, jobs + ((1 << l) - 2), 1 << l, P, s))) return rc;
+    if ((rc = launch_narrow(t->w, jobs + ((1 << l) - 2), 1 << l, P, s))) return rc;
   for (int l = 1; l <= t->depth; ++l)
-    if ((rc = launch_narrow(nf, jobs + nup + ((1 << l) - 2), 1 << l, P, s))) return rc;
-  return launch_wide((t->mmax + 15) / 16, jobs + 2 * nup, n, P, s);
+    if ((rc = launch_narrow(t->w, jobs + nup + ((1 << l) - 2), 1 << l, P, s))) return rc;
+  return launch_wide(t->mmax, jobs + 2 * nup, n, P, s);
 }
 
 extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
@@ -290,7 +408,7 @@ extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_
     single_job_kernel<<<1, 1, 0, s>>>(jobs + q, A, lda, B, ldb, C, ldc, nn, (int)K, n0);
     HSS_CHECK_LAUNCH();
   }
-  return launch_wide(8, jobs, nj, M, s);
+  return launch_wide(128, jobs, nj, M, s);
 }
 
 extern "C" const char* hsseig_version(void) { return "hsseig_b200 0.1 sm_100a"; }

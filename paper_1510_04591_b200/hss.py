@@ -258,7 +258,7 @@ class HssTree:
         return self._view(name, torch.int32, ws, node * ws)[:r].cpu().numpy().astype(np.intp)
 
     def leaf_D(self, node):
-        mm = self.ct.mmax
+        mm = self.ct.dld
         j = self._leaf_pos[node]
         flat = self._view("D", torch.float64, mm * mm, j * mm * mm)
         m = self.nodes[node].hi - self.nodes[node].lo
