@@ -177,6 +177,20 @@ int hsseig_hss_matmul_right(const double *X, int64_t ldx, int64_t P, const hssei
 int hsseig_dense_update(const double *Qb, int64_t ldq, int64_t P, const hsseig_gen *gen,
                         double *out, int64_t ldo, void *stream);
 
+/*
+ * The reference's Gaussian sample draw on the device, bit-identical to
+ * numpy.random.Generator(PCG64(state, inc)).standard_normal(n) (hss.py:236-237).
+ * hsseig_set_normal_tables loads NumPy's ziggurat tables (ki, wi, fi; 256 each, host
+ * pointers) once.  state/inc: the PCG64 128-bit state and increment as hi/lo words
+ * (Generator.bit_generator.state).  work: hsseig_normals_work_bytes(n) bytes.
+ * *fail_dev (int32, device) is set non-zero if the rejection chain could not be
+ * resolved; the caller then draws on the host instead.
+ */
+int hsseig_set_normal_tables(const uint64_t *ki, const double *wi, const double *fi);
+int64_t hsseig_normals_work_bytes(int64_t n);
+int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                         int64_t n, double *out, void *work, int32_t *fail_dev, void *stream);
+
 /* Plain batched helper used by tests/bench: out = A @ B (P x K)(K x N), FP64 DMMA. */
 int hsseig_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *stream);

@@ -71,6 +71,12 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
   const double* src = side == 0 ? Y : Z;
   double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * T.ws;
   double* Dslot = T.D + (size_t)j * T.dld * T.dld;
+  if (side == 0) {
+    for (int e = tid; e < T.dld * T.dld; e += blockDim.x) {
+      const int a = e / T.dld, b = e % T.dld;
+      if (a >= m || b >= m) Dslot[e] = 0.0;
+    }
+  }
   for (int a0 = 0; a0 < m; a0 += RA) {
     const int na = min(RA, m - a0);
     __syncthreads();
@@ -104,9 +110,10 @@ __global__ void genB_kernel(CauchyGen g, TreeDev T, int level) {
   const int32_t* rs = T.rsel + (size_t)me * T.ws;
   const int32_t* cs = T.csel + (size_t)sib * T.ws;
   double* Bo = T.B + slot_ww(T, me);
-  for (int e = tid; e < nr * nc; e += blockDim.x) {
-    int r = e / nc, c = e % nc;
-    Bo[r * T.ws + c] = g.entry(rs[r], cs[c]);
+  // the whole ws x ws slot is written: zero padding makes K-tail chunks of the multiply exact
+  for (int e = tid; e < T.ws * T.ws; e += blockDim.x) {
+    int r = e / T.ws, c = e % T.ws;
+    Bo[e] = (r < nr && c < nc) ? g.entry(rs[r], cs[c]) : 0.0;
   }
 }
 
@@ -363,11 +370,14 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
     if (sat) atomicAdd(reinterpret_cast<unsigned long long*>(&st->v[4]), 1ull);
     atomicMax(reinterpret_cast<long long*>(&st->v[5]), (long long)r);
   }
-  for (int e = tid; e < p * r; e += nthr) {
-    const int jj = e / r, t = e % r;  // jj = position in pivoted order
-    const double val = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * SW + t];
-    X[(size_t)piv[jj] * ws + t] = val;
-    if (side == 1) Xt[(size_t)t * T.pmax + piv[jj]] = val;
+  // full slots (zero padding beyond p rows / r columns keeps the multiply's K tails exact)
+  for (int e = tid; e < T.pmax * ws; e += nthr) {
+    const int jj = e / ws, t = e % ws;  // jj = position in pivoted order
+    double val = 0.0;
+    if (jj < p && t < r) val = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * SW + t];
+    const int row = jj < p ? piv[jj] : jj;
+    X[(size_t)row * ws + t] = val;
+    if (side == 1) Xt[(size_t)t * T.pmax + row] = val;
   }
   for (int t = tid; t < r; t += nthr) {
     const int pj = piv[t];
@@ -432,7 +442,7 @@ struct TreeCarve {
 static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
   TreeCarve c;
   const int64_t nn = 2 * (int64_t)n_leaves - 1;
-  const int64_t ws = w + (w & 1);
+  const int64_t ws = (w + 15) / 16 * 16;
   int64_t pmax = std::max<int64_t>(mmax, 2 * (int64_t)w);
   pmax += pmax & 1;
   const int64_t dld = mmax + (mmax & 1);
@@ -500,7 +510,7 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
   TreeCarve c = carve(k, n_leaves, w, mmax);
   char* base = static_cast<char*>(dev_mem);
   t->k = k; t->n_leaves = n_leaves; t->depth = depth; t->n_nodes = nn; t->w = w;
-  t->ws = w + (w & 1);
+  t->ws = (w + 15) / 16 * 16;
   t->pmax = std::max<int32_t>(mmax, 2 * w);
   t->pmax += t->pmax & 1;
   t->mmax = mmax;

@@ -3,141 +3,214 @@
 // Reference: hss_matmul_right (pkg/src/hsseig/hss.py:309-361).
 // Every step of the algorithm is a tall-skinny contraction over the P rows of X
 // with a node-local factor, so each tree level is ONE launch of a batched
-// two-segment DMMA GEMM (one job per node):
+// two-segment FP64 GEMM (one job per node):
 //   up, leaf  : G_i = X[:, t_i] U_i
 //   up, inner : G_i = [G_l | G_r] U_i
 //   down      : F_i = [G_sib | F_par] [B_sib ; V_par(rows of i)^T]     (the "inherit" term)
 //   final     : out[:, t_i] = [X[:, t_i] | F_i] [D_i ; V_i^T]
-// Job descriptors are built on the device from the ranks the construction wrote,
-// so no host synchronisation is needed between construction and multiply.
+//
+// Kernel shape (Blackwell): persistent CTAs, one TMA producer warp and WM x WN DMMA
+// consumer warps.  Operand tiles move by cp.async.bulk.tensor (TMA) into a STAGES-deep
+// shared-memory ring guarded by full/empty mbarriers, so no block-wide barrier sits in
+// the main loop; FP64 has no tcgen05 kind on sm_100a, so the contraction runs on the
+// warp-level DMMA.8x8x4 tensor sub-pipe.  Boxes are 4 columns wider than the tile
+// so the dense TMA rows land with a stride of 4 (mod 16) doubles, which keeps every
+// fragment load bank-conflict free without a swizzle.
+//
+// Exactness of K tails: factor slots are stored zero-padded to the 16-aligned slot
+// width and G/F slots get zeros beyond their rank (store width SW), so a chunk that
+// runs past a segment's K multiplies finite values by zeros.
+//
+// Job descriptors are built on the device from the ranks the construction wrote, so
+// no host synchronisation is needed between construction and multiply.
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
+#include <cstring>
 
 #include "dmma_gemm.cuh"
 
 namespace hsseig {
 
-struct GemmJob {
-  const double* A1;
-  const double* A2;
-  const double* B1;
-  const double* B2;
+constexpr int kMaps = 8;  // roles: 0 X, 1 G_l, 2 G_{l+1}, 3 F_{l-1} (or F_depth), 4 U, 5 B, 6 Vt, 7 D
+
+struct MapSet {
+  CUtensorMap m[kMaps];
+};
+
+struct TJob {
+  int32_t am[2], acol[2];            // A map role and column offset per segment (rows = tile)
+  int32_t bm[2], brow[2], bcol[2];   // B map role, row and column offset per segment
+  int32_t K[2], N, SW;               // segment depths, output width, store width (zero fill)
   double* C;
-  int64_t lda1, lda2, b1r, b1c, b2r, b2c, ldc;
-  int32_t K1, K2, N, pad;
+  int64_t ldc;
 };
 
-// Persistent batched two-segment GEMM.  CTA c walks the (job, row-tile) list
-// c, c + gridDim.x, ...; the (tile, k-chunk) sequence is one continuous cp.async
-// pipeline, so the next tile's operands stream in while this tile's last chunks
-// are multiplied and its accumulators are stored.
-template <class T>
-struct Seg {
-  const double* A;
-  const double* B;
-  int64_t lda, ldb;
-  int K;
-  bool a16, b16;
+template <int MF_, int NF_, int WM_, int WN_, int STAGES_>
+struct TTile {
+  static constexpr int MF = MF_, NF = NF_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr int BM = WM * MF * 8;
+  static constexpr int BN = WN * NF * 8;
+  static constexpr int BK = 16;
+  static constexpr int SA = BK + 4;             // A box width (doubles) = smem row stride
+  static constexpr int SB = ((BN + 15) / 16) * 16 + 4;
+  static constexpr int CONSUMERS = WM * WN;
+  static constexpr int THREADS = (CONSUMERS + 1) * 32;
+  static constexpr int A_BYTES = BM * SA * 8;
+  static constexpr int B_BYTES = BK * SB * 8;
+  static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + 127) / 128) * 128;
+  static constexpr size_t SMEM_BYTES = (size_t)STAGE_BYTES * STAGES + 2 * STAGES * 8 + 128;
 };
 
-template <class T>
-__device__ __forceinline__ void job_seg(const GemmJob& jb, int c, int nc1, Seg<T>& sg, int& k0) {
-  if (c < nc1) {
-    sg.A = jb.A1; sg.B = jb.B1; sg.lda = jb.lda1; sg.ldb = jb.b1r; sg.K = jb.K1;
-    k0 = c * T::BK;
-  } else {
-    sg.A = jb.A2; sg.B = jb.B2; sg.lda = jb.lda2; sg.ldb = jb.b2r; sg.K = jb.K2;
-    k0 = (c - nc1) * T::BK;
-  }
-  sg.a16 = ((reinterpret_cast<uintptr_t>(sg.A) & 15) == 0) && ((sg.lda & 1) == 0);
-  sg.b16 = ((reinterpret_cast<uintptr_t>(sg.B) & 15) == 0) && ((sg.ldb & 1) == 0);
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 
 template <class T>
-__global__ void __launch_bounds__(T::THREADS) batched_gemm2_kernel(const GemmJob* __restrict__ jobs,
-                                                                   int njobs, int64_t M,
-                                                                   int tiles_m) {
-  extern __shared__ __align__(16) double smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / T::WN, wn = warp % T::WN;
-  const int total = njobs * tiles_m;
-  auto sa = [&](int s) { return smem + s * T::STAGE_ELEMS; };
-  auto sb = [&](int s) { return smem + s * T::STAGE_ELEMS + T::A_ELEMS; };
+__device__ __forceinline__ void tmma_chunk(const double* __restrict__ sA, const double* __restrict__ sB,
+                                           double (&c)[T::MF][T::NF][2], int wm, int wn, int lane,
+                                           int kv, int jmax) {
+  const int gr = lane >> 2, gc = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < T::BK; kk += 4) {
+    if (kk >= kv) break;
+    double a[T::MF], b[T::NF];
+#pragma unroll
+    for (int i = 0; i < T::MF; ++i) a[i] = sA[(wm * T::MF * 8 + i * 8 + gr) * T::SA + kk + gc];
+#pragma unroll
+    for (int j = 0; j < T::NF; ++j) b[j] = sB[(kk + gc) * T::SB + wn * T::NF * 8 + j * 8 + gr];
+#pragma unroll
+    for (int j = 0; j < T::NF; ++j) {
+      if (j >= jmax) break;
+#pragma unroll
+      for (int i = 0; i < T::MF; ++i) dmma_8x8x4(c[i][j][0], c[i][j][1], a[i], b[j]);
+    }
+  }
+}
 
-  // producer cursor
-  int pt = blockIdx.x, pc = 0, pslot = 0;
-  GemmJob pj;
-  int pnc1 = 0, pnch = 0;
-  auto load_pjob = [&]() {
-    if (pt < total) {
-      pj = jobs[pt / tiles_m];
-      pnc1 = (pj.K1 + T::BK - 1) / T::BK;
-      pnch = pj.N > 0 ? pnc1 + (pj.K2 + T::BK - 1) / T::BK : 0;
+template <class T>
+__global__ void __launch_bounds__(T::THREADS, 1)
+    tma_gemm_kernel(const __grid_constant__ MapSet maps, const TJob* __restrict__ jobs, int njobs,
+                    int64_t M, int tiles_m) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 127) & ~(uintptr_t)127);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)T::STAGE_BYTES * T::STAGES);
+  uint64_t* empty = full + T::STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int total = njobs * tiles_m;
+  if (tid == 0) {
+    for (int s = 0; s < T::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], T::CONSUMERS);
     }
-  };
-  load_pjob();
-  auto produce = [&]() {
-    while (pt < total && pc >= pnch) {  // skip empty tiles
-      pt += gridDim.x;
-      pc = 0;
-      load_pjob();
-    }
-    if (pt < total) {
-      Seg<T> sg;
-      int k0;
-      job_seg<T>(pj, pc, pnc1, sg, k0);
-      const int64_t m0 = (int64_t)(pt % tiles_m) * T::BM;
-      if (sg.a16) load_a_async16<T>(sa(pslot), sg.A, sg.lda, M, m0, sg.K, k0, tid);
-      else load_a_async<T>(sa(pslot), sg.A, sg.lda, M, m0, sg.K, k0, tid);
-      if (sg.b16) load_b_async16<T>(sb(pslot), sg.B, sg.ldb, sg.K, k0, pj.N, tid);
-      else load_b_async<T>(sb(pslot), sg.B, sg.ldb, 1, sg.K, k0, pj.N, 0, tid);
-      if (++pc >= pnch) {
-        pt += gridDim.x;
-        pc = 0;
-        load_pjob();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == T::CONSUMERS) {
+    // ---------------- TMA producer (one lane) ----------------
+    if (lane == 0) {
+      uint32_t q = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const TJob jb = jobs[t / tiles_m];
+        if (jb.N <= 0) continue;
+        const int m0 = (t % tiles_m) * T::BM;
+        for (int sg = 0; sg < 2; ++sg) {
+          const int nc = (jb.K[sg] + T::BK - 1) / T::BK;
+          for (int c = 0; c < nc; ++c, ++q) {
+            const int slot = q % T::STAGES;
+            mbar_wait(&empty[slot], ((q / T::STAGES) & 1) ^ 1);
+            mbar_expect_tx(&full[slot], T::A_BYTES + T::B_BYTES);
+            unsigned char* st = sm + (size_t)slot * T::STAGE_BYTES;
+            tma_load_2d(st, &maps.m[jb.am[sg]], jb.acol[sg] + c * T::BK, m0, &full[slot]);
+            tma_load_2d(st + T::A_BYTES, &maps.m[jb.bm[sg]], jb.bcol[sg], jb.brow[sg] + c * T::BK,
+                        &full[slot]);
+          }
+        }
       }
     }
-    cp_async_commit();
-    pslot = (pslot + 1) % T::STAGES;
-  };
-
-#pragma unroll 1
-  for (int s = 0; s < T::STAGES - 1; ++s) produce();
-
-  // consumer cursor
-  int ct = blockIdx.x, cslot = 0;
-  Acc<T> acc;
-  while (ct < total) {
-    const GemmJob cj = jobs[ct / tiles_m];
-    const int nc1 = (cj.K1 + T::BK - 1) / T::BK;
-    const int nch = cj.N > 0 ? nc1 + (cj.K2 + T::BK - 1) / T::BK : 0;
-    if (nch == 0) { ct += gridDim.x; continue; }
-    const int64_t m0 = (int64_t)(ct % tiles_m) * T::BM;
-    const int jmax = max(0, min(T::NF, (cj.N - wn * T::NF * 8 + 7) / 8));
-    acc.zero();
-    for (int c = 0; c < nch; ++c) {
-      cp_async_wait<T::STAGES - 2>();
-      __syncthreads();
-      produce();
-      const int kseg = c < nc1 ? cj.K1 - c * T::BK : cj.K2 - (c - nc1) * T::BK;
-      const int kv = min(T::BK, (kseg + 3) & ~3);
-      if (kv == T::BK && jmax == T::NF)
-        mma_chunk<T>(sa(cslot), sb(cslot), acc, wm, wn, lane);
-      else
-        mma_chunk_part<T>(sa(cslot), sb(cslot), acc, wm, wn, lane, kv, jmax);
-      cslot = (cslot + 1) % T::STAGES;
-    }
-    store_acc<T>(acc, cj.C, cj.ldc, M, m0, cj.N, 0, wm, wn, lane);
-    ct += gridDim.x;
+    return;
   }
-  cp_async_wait<0>();
+
+  // ---------------- DMMA consumers ----------------
+  const int wm = warp / T::WN, wn = warp % T::WN;
+  const int gr = lane >> 2, gc = lane & 3;
+  uint32_t q = 0;
+  double acc[T::MF][T::NF][2];
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const TJob jb = jobs[t / tiles_m];
+    if (jb.N <= 0) continue;
+    const int64_t m0 = (int64_t)(t % tiles_m) * T::BM;
+    const int jmax = max(0, min(T::NF, (jb.N - wn * T::NF * 8 + 7) / 8));
+#pragma unroll
+    for (int i = 0; i < T::MF; ++i)
+#pragma unroll
+      for (int j = 0; j < T::NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int sg = 0; sg < 2; ++sg) {
+      const int K = jb.K[sg];
+      const int nc = (K + T::BK - 1) / T::BK;
+      for (int c = 0; c < nc; ++c, ++q) {
+        const int slot = q % T::STAGES;
+        mbar_wait(&full[slot], (q / T::STAGES) & 1);
+        const double* sA = reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES);
+        const double* sB =
+            reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES);
+        const int kv = min(T::BK, ((K - c * T::BK) + 3) & ~3);
+        tmma_chunk<T>(sA, sB, acc, wm, wn, lane, kv, jmax);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+      }
+    }
+    // epilogue: accumulators for columns < N, zeros in [N, SW)
+#pragma unroll
+    for (int i = 0; i < T::MF; ++i) {
+      const int64_t row = m0 + wm * T::MF * 8 + i * 8 + gr;
+      if (row >= M) continue;
+      double* crow = jb.C + row * jb.ldc;
+#pragma unroll
+      for (int j = 0; j < T::NF; ++j) {
+        const int col = wn * T::NF * 8 + j * 8 + 2 * gc;
+        if (col < jb.SW) crow[col] = col < jb.N ? acc[i][j][0] : 0.0;
+        if (col + 1 < jb.SW) crow[col + 1] = col + 1 < jb.N ? acc[i][j][1] : 0.0;
+      }
+    }
+  }
 }
 
 struct MultPlan {
-  int32_t depth, n_leaves, ws, pmax, mmax, dld;
+  int32_t depth, n_leaves, ws, pmax, dld;
   const int32_t *lo, *hi, *left, *right, *lnodes, *rU, *rV;
-  const double *U, *V, *Vt, *B, *D;
-  const double* X;
-  int64_t ldx;
   double* out;
   int64_t ldo;
   double* Gb;  // levels 1..depth, level l at Gb + P*ws*(2^l - 2), ld = 2^l * ws
@@ -145,22 +218,23 @@ struct MultPlan {
   int64_t P;
 };
 
-__device__ __forceinline__ double* lvl_buf(double* base, int64_t P, int ws, int l) {
-  return base + P * (int64_t)ws * ((1ll << l) - 2);
+__host__ __device__ __forceinline__ int64_t lvl_off(int64_t P, int ws, int l) {
+  return P * (int64_t)ws * ((1ll << l) - 2);
 }
 
 // Job table: up-sweep level l at [2^l - 2, 2^{l+1} - 2) for l = 1..depth (2n-2 jobs),
 // down-sweep the same offsets shifted by 2n-2, the leaf finish last (n jobs).
-__global__ void setup_jobs_kernel(MultPlan p, GemmJob* __restrict__ jobs) {
+__global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs) {
   const int n = p.n_leaves;
   const int nup = 2 * n - 2;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= 2 * nup + n) return;
   const int ws = p.ws;
-  const size_t pw = (size_t)p.pmax * ws, ww = (size_t)ws * ws;
-  GemmJob jb;
-  jb.A2 = nullptr; jb.B2 = nullptr;
-  jb.lda2 = 0; jb.b2r = 0; jb.b2c = 0; jb.K2 = 0; jb.pad = 0;
+  TJob jb;
+  jb.am[0] = jb.am[1] = 0;
+  jb.bm[0] = jb.bm[1] = 4;
+  jb.acol[0] = jb.acol[1] = jb.brow[0] = jb.brow[1] = jb.bcol[0] = jb.bcol[1] = 0;
+  jb.K[0] = jb.K[1] = 0;
   if (e < 2 * nup) {
     const bool up = e < nup;
     const int q = up ? e : e - nup;
@@ -168,84 +242,94 @@ __global__ void setup_jobs_kernel(MultPlan p, GemmJob* __restrict__ jobs) {
     while (q >= (1 << (l + 1)) - 2) ++l;
     const int j = q - ((1 << l) - 2);
     const int node = p.lnodes[(1 << l) - 1 + j];
-    const int64_t ldl = (int64_t)(1 << l) * ws;
+    jb.ldc = (int64_t)(1 << l) * ws;
+    jb.SW = ws;
     if (up) {
-      // G_node = A U_node,  A = X[:, t] (leaf) or [G_left | G_right]
-      jb.C = lvl_buf(p.Gb, p.P, ws, l) + (int64_t)j * ws;
-      jb.ldc = ldl;
+      jb.C = p.Gb + lvl_off(p.P, ws, l) + (int64_t)j * ws;
       jb.N = p.rU[node];
-      jb.B1 = p.U + (size_t)node * pw;
-      jb.b1r = ws; jb.b1c = 1;
       if (l == p.depth) {
-        const int lo = p.lo[node];
-        jb.A1 = p.X + lo;
-        jb.lda1 = p.ldx;
-        jb.K1 = p.hi[node] - lo;
+        jb.am[0] = 0; jb.acol[0] = p.lo[node]; jb.K[0] = p.hi[node] - p.lo[node];
+        jb.bm[0] = 4; jb.brow[0] = node * p.pmax;
       } else {
         const int a = p.left[node], b = p.right[node];
-        const int64_t ldc1 = (int64_t)(1 << (l + 1)) * ws;
-        jb.A1 = lvl_buf(p.Gb, p.P, ws, l + 1) + (int64_t)(2 * j) * ws;
-        jb.lda1 = ldc1;
-        jb.K1 = p.rU[a];
-        jb.A2 = jb.A1 + ws;
-        jb.lda2 = ldc1;
-        jb.K2 = p.rU[b];
-        jb.B2 = jb.B1 + (size_t)p.rU[a] * ws;
-        jb.b2r = ws; jb.b2c = 1;
+        jb.am[0] = 2; jb.acol[0] = 2 * j * ws; jb.K[0] = p.rU[a];
+        jb.bm[0] = 4; jb.brow[0] = node * p.pmax;
+        jb.am[1] = 2; jb.acol[1] = (2 * j + 1) * ws; jb.K[1] = p.rU[b];
+        jb.bm[1] = 4; jb.brow[1] = node * p.pmax + p.rU[a];
       }
     } else {
-      // F_node = G_sib B_sib (+ F_parent V_parent[rows of node]^T)
       const int sib = p.lnodes[(1 << l) - 1 + (j ^ 1)];
-      jb.A1 = lvl_buf(p.Gb, p.P, ws, l) + (int64_t)(j ^ 1) * ws;
-      jb.lda1 = ldl;
-      jb.K1 = p.rU[sib];
-      jb.B1 = p.B + (size_t)sib * ww;
-      jb.b1r = ws; jb.b1c = 1;
-      jb.C = lvl_buf(p.Fb, p.P, ws, l) + (int64_t)j * ws;
-      jb.ldc = ldl;
+      jb.C = p.Fb + lvl_off(p.P, ws, l) + (int64_t)j * ws;
       jb.N = p.rV[node];
+      jb.am[0] = 1; jb.acol[0] = (j ^ 1) * ws; jb.K[0] = p.rU[sib];
+      jb.bm[0] = 5; jb.brow[0] = sib * ws;
       if (l > 1) {
         const int par = p.lnodes[(1 << (l - 1)) - 1 + (j >> 1)];
-        const int off = (j & 1) ? p.rV[p.left[par]] : 0;
-        jb.A2 = lvl_buf(p.Fb, p.P, ws, l - 1) + (int64_t)(j >> 1) * ws;
-        jb.lda2 = (int64_t)(1 << (l - 1)) * ws;
-        jb.K2 = p.rV[par];
-        jb.B2 = p.Vt + (size_t)par * ws * p.pmax + off;   // V_par[off:off+rV, :]^T
-        jb.b2r = p.pmax; jb.b2c = 1;
+        jb.am[1] = 3; jb.acol[1] = (j >> 1) * ws; jb.K[1] = p.rV[par];
+        jb.bm[1] = 6; jb.brow[1] = par * ws; jb.bcol[1] = (j & 1) ? p.rV[p.left[par]] : 0;
       }
     }
   } else {
-    // out[:, t] = X[:, t] D + F_leaf V_leaf^T
     const int j = e - 2 * nup;
     const int node = p.lnodes[(1 << p.depth) - 1 + j];
     const int lo = p.lo[node];
-    jb.A1 = p.X + lo;
-    jb.lda1 = p.ldx;
-    jb.K1 = p.hi[node] - lo;
-    jb.B1 = p.D + (size_t)j * p.dld * p.dld;
-    jb.b1r = p.dld; jb.b1c = 1;
-    jb.A2 = lvl_buf(p.Fb, p.P, ws, p.depth) + (int64_t)j * ws;
-    jb.lda2 = (int64_t)(1 << p.depth) * ws;
-    jb.K2 = p.rV[node];
-    jb.B2 = p.Vt + (size_t)node * ws * p.pmax;
-    jb.b2r = p.pmax; jb.b2c = 1;
     jb.C = p.out + lo;
     jb.ldc = p.ldo;
-    jb.N = p.hi[node] - lo;
+    jb.N = jb.SW = p.hi[node] - lo;
+    jb.am[0] = 0; jb.acol[0] = lo; jb.K[0] = p.hi[node] - lo;
+    jb.bm[0] = 7; jb.brow[0] = j * p.dld;
+    jb.am[1] = 3; jb.acol[1] = j * ws; jb.K[1] = p.rV[node];
+    jb.bm[1] = 6; jb.brow[1] = node * ws;
   }
   jobs[e] = jb;
 }
 
+// ---------------------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Row-major (rows x cols, leading dimension ld) float64 matrix, box of box_rows x box_cols.
+static bool make_map(CUtensorMap* m, const double* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                     uint32_t box_cols, uint32_t box_rows) {
+  memset(m, 0, sizeof(*m));
+  if (!base) return true;   // role unused by this launch
+  auto fn = encode_fn();
+  if (!fn || rows == 0 || cols == 0) return false;
+  cuuint64_t gdim[2] = {cols, rows};
+  cuuint64_t gstride[1] = {ld * 8};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Raw operand descriptions (rows, cols, ld) for the 8 roles of one launch.
+struct Operand {
+  const double* base;
+  uint64_t rows, cols, ld;
+};
+
 static int g_sms = 0;
 
 template <class T>
-static int launch_batched(const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
+static int launch_tma(const Operand (&ops)[kMaps], const TJob* jobs, int njobs, int64_t M,
+                      cudaStream_t s) {
   if (njobs <= 0 || M <= 0) return HSSEIG_OK;
   static int per_sm = 0;
   if (!per_sm) {
-    cudaFuncSetAttribute(batched_gemm2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tma_gemm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)T::SMEM_BYTES);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, batched_gemm2_kernel<T>, T::THREADS,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tma_gemm_kernel<T>, T::THREADS,
                                                   T::SMEM_BYTES);
     if (per_sm < 1) per_sm = 1;
     if (!g_sms) {
@@ -254,95 +338,90 @@ static int launch_batched(const GemmJob* jobs, int njobs, int64_t M, cudaStream_
       cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     }
   }
+  MapSet maps;
+  for (int r = 0; r < kMaps; ++r) {
+    const bool is_a = r < 4;
+    const uint32_t bc = is_a ? T::SA : T::SB;
+    const uint32_t br = is_a ? T::BM : T::BK;
+    if (!make_map(&maps.m[r], ops[r].base, ops[r].rows, ops[r].cols, ops[r].ld, bc, br))
+      return HSSEIG_ERR_ARG;
+  }
   const int tiles_m = (int)((M + T::BM - 1) / T::BM);
   const int64_t total = (int64_t)tiles_m * njobs;
   const int grid = (int)imin64(total, (int64_t)g_sms * per_sm);
-  batched_gemm2_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(jobs, njobs, M, tiles_m);
+  tma_gemm_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(maps, jobs, njobs, M, tiles_m);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
 
-// Tile variants (HSSEIG_TILE_NARROW / HSSEIG_TILE_WIDE select one for tuning runs).
 static int tile_choice(const char* var, int dflt) {
   const char* v = getenv(var);
   return v ? atoi(v) : dflt;
 }
 
 // narrow outputs (ranks, N <= 112)
-static int launch_narrow(int n, const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
+static int launch_narrow(int n, const Operand (&ops)[kMaps], const TJob* jobs, int njobs, int64_t M,
+                         cudaStream_t s) {
   static const int variant = tile_choice("HSSEIG_TILE_NARROW", 1);
-  if (variant == 0) {   // BM 128, 8 warps of 32 x 8NF, NF = ceil(n/16)
+  if (variant == 0) {   // BM 128: 8 consumer warps of 32 x 8NF, NF = ceil(n/16)
     switch ((n + 15) / 16) {
-      case 1: return launch_batched<Tile<4, 1, 4, 2, 4>>(jobs, njobs, M, s);
-      case 2: return launch_batched<Tile<4, 2, 4, 2, 4>>(jobs, njobs, M, s);
-      case 3: return launch_batched<Tile<4, 3, 4, 2, 4>>(jobs, njobs, M, s);
-      case 4: return launch_batched<Tile<4, 4, 4, 2, 4>>(jobs, njobs, M, s);
-      case 5: return launch_batched<Tile<4, 5, 4, 2, 4>>(jobs, njobs, M, s);
-      case 6: return launch_batched<Tile<4, 6, 4, 2, 4>>(jobs, njobs, M, s);
-      case 7: return launch_batched<Tile<4, 7, 4, 2, 4>>(jobs, njobs, M, s);
+      case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 4, 2, 5>>(ops, jobs, njobs, M, s);
+      case 5: return launch_tma<TTile<4, 5, 4, 2, 5>>(ops, jobs, njobs, M, s);
+      case 6: return launch_tma<TTile<4, 6, 4, 2, 5>>(ops, jobs, njobs, M, s);
+      case 7: return launch_tma<TTile<4, 7, 4, 2, 5>>(ops, jobs, njobs, M, s);
       default: return HSSEIG_ERR_ARG;
     }
   }
-  if (variant == 2) {   // BM 64, 4 warps of 32 x 8NF, NF = ceil(n/16)
-    switch ((n + 15) / 16) {
-      case 1: return launch_batched<Tile<4, 1, 2, 2, 4>>(jobs, njobs, M, s);
-      case 2: return launch_batched<Tile<4, 2, 2, 2, 4>>(jobs, njobs, M, s);
-      case 3: return launch_batched<Tile<4, 3, 2, 2, 4>>(jobs, njobs, M, s);
-      case 4: return launch_batched<Tile<4, 4, 2, 2, 4>>(jobs, njobs, M, s);
-      case 5: return launch_batched<Tile<4, 5, 2, 2, 4>>(jobs, njobs, M, s);
-      case 6: return launch_batched<Tile<4, 6, 2, 2, 4>>(jobs, njobs, M, s);
-      case 7: return launch_batched<Tile<4, 7, 2, 2, 4>>(jobs, njobs, M, s);
-      default: return HSSEIG_ERR_ARG;
-    }
-  }
-  // default: BM 64, 8 warps of 32 x 8NF, NF = ceil(n/32)
+  // default: BM 64: 8 consumer warps of 32 x 8NF, NF = ceil(n/32)
   switch ((n + 31) / 32) {
-    case 1: return launch_batched<Tile<4, 1, 2, 4, 4>>(jobs, njobs, M, s);
-    case 2: return launch_batched<Tile<4, 2, 2, 4, 4>>(jobs, njobs, M, s);
-    case 3: return launch_batched<Tile<4, 3, 2, 4, 4>>(jobs, njobs, M, s);
-    case 4: return launch_batched<Tile<4, 4, 2, 4, 4>>(jobs, njobs, M, s);
+    case 1: case 2: return launch_tma<TTile<4, 2, 2, 4, 8>>(ops, jobs, njobs, M, s);
+    case 3: return launch_tma<TTile<4, 3, 2, 4, 8>>(ops, jobs, njobs, M, s);
+    case 4: return launch_tma<TTile<4, 4, 2, 4, 6>>(ops, jobs, njobs, M, s);
     default: return HSSEIG_ERR_ARG;
   }
 }
 
-// wide outputs (leaf finish N = leaf size; plain GEMM tiles)
-static int launch_wide(int n, const GemmJob* jobs, int njobs, int64_t M, cudaStream_t s) {
+// wide outputs (leaf finish N = leaf size; plain GEMM tiles), N <= 224
+static int launch_wide(int n, const Operand (&ops)[kMaps], const TJob* jobs, int njobs, int64_t M,
+                       cudaStream_t s) {
   static const int variant = tile_choice("HSSEIG_TILE_WIDE", 1);
-  if (variant == 0) {   // BM 64, 8 warps of 16 x 8NF, NF = ceil(n/16)
+  if (variant == 0) {   // BM 64: 8 consumer warps of 16 x 8NF, NF = ceil(n/16)
     switch ((n + 15) / 16) {
-      case 1: case 2: case 3: case 4: return launch_batched<Tile<2, 4, 4, 2, 4>>(jobs, njobs, M, s);
-      case 5: return launch_batched<Tile<2, 5, 4, 2, 4>>(jobs, njobs, M, s);
-      case 6: return launch_batched<Tile<2, 6, 4, 2, 4>>(jobs, njobs, M, s);
-      case 7: return launch_batched<Tile<2, 7, 4, 2, 4>>(jobs, njobs, M, s);
-      case 8: return launch_batched<Tile<2, 8, 4, 2, 4>>(jobs, njobs, M, s);
-      case 9: return launch_batched<Tile<2, 9, 4, 2, 4>>(jobs, njobs, M, s);
-      case 10: return launch_batched<Tile<2, 10, 4, 2, 3>>(jobs, njobs, M, s);
-      case 11: return launch_batched<Tile<2, 11, 4, 2, 3>>(jobs, njobs, M, s);
-      case 12: return launch_batched<Tile<2, 12, 4, 2, 3>>(jobs, njobs, M, s);
-      case 13: return launch_batched<Tile<2, 13, 4, 2, 3>>(jobs, njobs, M, s);
+      case 1: case 2: case 3: case 4: case 5: case 6:
+        return launch_tma<TTile<2, 6, 4, 2, 6>>(ops, jobs, njobs, M, s);
+      case 7: return launch_tma<TTile<2, 7, 4, 2, 6>>(ops, jobs, njobs, M, s);
+      case 8: return launch_tma<TTile<2, 8, 4, 2, 6>>(ops, jobs, njobs, M, s);
+      case 9: return launch_tma<TTile<2, 9, 4, 2, 6>>(ops, jobs, njobs, M, s);
+      case 10: return launch_tma<TTile<2, 10, 4, 2, 5>>(ops, jobs, njobs, M, s);
+      case 11: return launch_tma<TTile<2, 11, 4, 2, 5>>(ops, jobs, njobs, M, s);
+      case 12: return launch_tma<TTile<2, 12, 4, 2, 5>>(ops, jobs, njobs, M, s);
+      case 13: return launch_tma<TTile<2, 13, 4, 2, 5>>(ops, jobs, njobs, M, s);
+      case 14: return launch_tma<TTile<2, 14, 4, 2, 5>>(ops, jobs, njobs, M, s);
       default: return HSSEIG_ERR_ARG;
     }
   }
-  // default: BM 64, 8 warps of 32 x 8NF, NF = ceil(n/32)
+  // default: BM 64: 8 consumer warps of 32 x 8NF, NF = ceil(n/32)
   switch ((n + 31) / 32) {
-    case 1: case 2: return launch_batched<Tile<4, 2, 2, 4, 4>>(jobs, njobs, M, s);
-    case 3: return launch_batched<Tile<4, 3, 2, 4, 4>>(jobs, njobs, M, s);
-    case 4: return launch_batched<Tile<4, 4, 2, 4, 4>>(jobs, njobs, M, s);
-    case 5: return launch_batched<Tile<4, 5, 2, 4, 3>>(jobs, njobs, M, s);
-    case 6: return launch_batched<Tile<4, 6, 2, 4, 3>>(jobs, njobs, M, s);
-    case 7: return launch_batched<Tile<4, 7, 2, 4, 3>>(jobs, njobs, M, s);
+    case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 2, 4, 6>>(ops, jobs, njobs, M, s);
+    case 5: return launch_tma<TTile<4, 5, 2, 4, 6>>(ops, jobs, njobs, M, s);
+    case 6: return launch_tma<TTile<4, 6, 2, 4, 5>>(ops, jobs, njobs, M, s);
+    case 7: return launch_tma<TTile<4, 7, 2, 4, 5>>(ops, jobs, njobs, M, s);
     default: return HSSEIG_ERR_ARG;
   }
 }
 
-__global__ void single_job_kernel(GemmJob* jobs, const double* A, int64_t lda, const double* B,
-                                  int64_t ldb, double* C, int64_t ldc, int N, int K, int n0) {
-  GemmJob jb;
-  jb.A1 = A; jb.lda1 = lda; jb.K1 = K;
-  jb.B1 = B + n0; jb.b1r = ldb; jb.b1c = 1;
-  jb.A2 = nullptr; jb.B2 = nullptr; jb.lda2 = 0; jb.b2r = 0; jb.b2c = 0; jb.K2 = 0;
-  jb.C = C + n0; jb.ldc = ldc; jb.N = N; jb.pad = 0;
-  jobs[blockIdx.x] = jb;
+__global__ void plain_jobs_kernel(TJob* jobs, int nj, double* C, int64_t ldc, int N, int K) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nj) return;
+  TJob jb;
+  jb.am[0] = 0; jb.am[1] = 0; jb.acol[0] = 0; jb.acol[1] = 0;
+  jb.bm[0] = 4; jb.bm[1] = 4; jb.brow[0] = 0; jb.brow[1] = 0; jb.bcol[0] = q * 128; jb.bcol[1] = 0;
+  jb.K[0] = K; jb.K[1] = 0;
+  jb.N = min(128, N - q * 128);
+  jb.SW = jb.N;
+  jb.C = C + q * 128;
+  jb.ldc = ldc;
+  jobs[q] = jb;
 }
 
 }  // namespace hsseig
@@ -350,8 +429,8 @@ __global__ void single_job_kernel(GemmJob* jobs, const double* A, int64_t lda, c
 using namespace hsseig;
 
 static int64_t jobs_doubles(int64_t n_leaves) {
-  int64_t njobs = 2 * (2 * n_leaves - 2) + n_leaves;
-  return (njobs * (int64_t)sizeof(GemmJob) + 7) / 8 + 32;
+  const int64_t njobs = 2 * (2 * n_leaves - 2) + n_leaves;
+  return (njobs * (int64_t)sizeof(TJob) + 7) / 8 + 32;
 }
 
 extern "C" int64_t hsseig_matmul_work_doubles(int64_t P, const hsseig_tree* t) {
@@ -364,54 +443,73 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
                                        double* work, void* stream) {
   if (!t || !X || !out || !work || P < 0 || ldx < t->k || ldo < t->k) return HSSEIG_ERR_ARG;
   if (P == 0) return HSSEIG_OK;
+  if ((reinterpret_cast<uintptr_t>(X) & 15) || (ldx & 1) || (reinterpret_cast<uintptr_t>(work) & 15))
+    return HSSEIG_ERR_ARG;   // TMA needs 16-byte aligned rows
+  if (P > 0x7fffffff) return HSSEIG_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t lvl_total = P * (int64_t)t->ws * (2 * (int64_t)t->n_leaves - 2);
+  const int ws = t->ws, n = t->n_leaves, nn = t->n_nodes, nup = 2 * n - 2;
+  const int64_t lvl_total = P * (int64_t)ws * (2 * (int64_t)n - 2);
   MultPlan p;
-  p.depth = t->depth; p.n_leaves = t->n_leaves; p.ws = t->ws; p.pmax = t->pmax; p.mmax = t->mmax;
-  p.dld = t->dld; p.Vt = t->Vt;
+  p.depth = t->depth; p.n_leaves = n; p.ws = ws; p.pmax = t->pmax; p.dld = t->dld;
   p.lo = t->lo; p.hi = t->hi; p.left = t->left; p.right = t->right; p.lnodes = t->level_nodes;
-  p.rU = t->rU; p.rV = t->rV; p.U = t->U; p.V = t->V; p.B = t->B; p.D = t->D;
-  p.X = X; p.ldx = ldx; p.out = out; p.ldo = ldo; p.P = P;
+  p.rU = t->rU; p.rV = t->rV;
+  p.out = out; p.ldo = ldo; p.P = P;
   p.Gb = work;
   p.Fb = work + lvl_total;
-  GemmJob* jobs = reinterpret_cast<GemmJob*>(work + 2 * lvl_total);
-  const int n = t->n_leaves, nup = 2 * n - 2;
-  const int total = 2 * nup + n;
-  setup_jobs_kernel<<<(total + 127) / 128, 128, 0, s>>>(p, jobs);
+  TJob* jobs = reinterpret_cast<TJob*>(work + 2 * lvl_total);
+  setup_jobs_kernel<<<(2 * nup + n + 127) / 128, 128, 0, s>>>(p, jobs);
   HSS_CHECK_LAUNCH();
+  auto lvl = [&](double* base, int l) -> Operand {
+    if (l < 1 || l > t->depth) return Operand{nullptr, 0, 0, 0};
+    const uint64_t cols = (uint64_t)(1u << l) * ws;
+    return Operand{base + lvl_off(P, ws, l), (uint64_t)P, cols, cols};
+  };
+  const Operand none{nullptr, 0, 0, 0};
+  const Operand Xop{X, (uint64_t)P, (uint64_t)t->k, (uint64_t)ldx};
+  const Operand Uop{t->U, (uint64_t)nn * t->pmax, (uint64_t)ws, (uint64_t)ws};
+  const Operand Bop{t->B, (uint64_t)nn * ws, (uint64_t)ws, (uint64_t)ws};
+  const Operand Vtop{t->Vt, (uint64_t)nn * ws, (uint64_t)t->pmax, (uint64_t)t->pmax};
+  const Operand Dop{t->D, (uint64_t)n * t->dld, (uint64_t)t->dld, (uint64_t)t->dld};
   int rc;
-  for (int l = t->depth; l >= 1; --l)
-    if ((rc = launch_narrow(t->w, jobs + ((1 << l) - 2), 1 << l, P, s))) return rc;
-  for (int l = 1; l <= t->depth; ++l)
-    if ((rc = launch_narrow(t->w, jobs + nup + ((1 << l) - 2), 1 << l, P, s))) return rc;
-  return launch_wide(t->mmax, jobs + 2 * nup, n, P, s);
+  for (int l = t->depth; l >= 1; --l) {
+    const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), lvl(p.Gb, l + 1), none, Uop, Bop, Vtop, Dop};
+    if ((rc = launch_narrow(t->w, ops, jobs + ((1 << l) - 2), 1 << l, P, s))) return rc;
+  }
+  for (int l = 1; l <= t->depth; ++l) {
+    const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), none, lvl(p.Fb, l - 1), Uop, Bop, Vtop, Dop};
+    if ((rc = launch_narrow(t->w, ops, jobs + nup + ((1 << l) - 2), 1 << l, P, s))) return rc;
+  }
+  const Operand ops[kMaps] = {Xop, none, none, lvl(p.Fb, t->depth), Uop, Bop, Vtop, Dop};
+  return launch_wide(t->mmax, ops, jobs + 2 * nup, n, P, s);
 }
 
 extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                            int64_t ldc, int64_t M, int64_t N, int64_t K, void* stream) {
-  // Test/bench helper: plain C = A B on the same DMMA engine, N split in 128-wide jobs.
-  // The caller passes C's job scratch implicitly: jobs live in a small static device buffer.
-  static GemmJob* jobs = nullptr;
+  // Test/bench helper: plain C = A B on the same TMA/DMMA engine, N split in 128-wide jobs.
+  static TJob* jobs = nullptr;
   static int cap = 0;
   if (M < 0 || N < 0 || K < 0 || lda < K || ldb < N || ldc < N) return HSSEIG_ERR_ARG;
   if (M == 0 || N == 0) return HSSEIG_OK;
+  if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) || (lda & 1) ||
+      (ldb & 1) || K == 0)
+    return HSSEIG_ERR_ARG;
   const int nj = (int)((N + 127) / 128);
   cudaStream_t s = (cudaStream_t)stream;
   if (nj > cap) {
     if (jobs) cudaFree(jobs);
-    if (cudaMalloc(&jobs, sizeof(GemmJob) * nj) != cudaSuccess) return HSSEIG_ERR_CUDA;
+    if (cudaMalloc(&jobs, sizeof(TJob) * nj) != cudaSuccess) return HSSEIG_ERR_CUDA;
     cap = nj;
   }
-  for (int q = 0; q < nj; ++q) {
-    int n0 = q * 128;
-    int nn = (int)std::min<int64_t>(128, N - n0);
-    single_job_kernel<<<1, 1, 0, s>>>(jobs + q, A, lda, B, ldb, C, ldc, nn, (int)K, n0);
-    HSS_CHECK_LAUNCH();
-  }
-  return launch_wide(128, jobs, nj, M, s);
+  plain_jobs_kernel<<<(nj + 127) / 128, 128, 0, s>>>(jobs, nj, C, ldc, (int)N, (int)K);
+  HSS_CHECK_LAUNCH();
+  // the maps carry the exact extents, so TMA zero-fills the K / N tails
+  const Operand none{nullptr, 0, 0, 0};
+  const Operand ops[kMaps] = {Operand{A, (uint64_t)M, (uint64_t)K, (uint64_t)lda}, none, none, none,
+                              Operand{B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb}, none, none, none};
+  return launch_wide(128, ops, jobs, nj, M, s);
 }
 
-extern "C" const char* hsseig_version(void) { return "hsseig_b200 0.1 sm_100a"; }
+extern "C" const char* hsseig_version(void) { return "hsseig_b200 0.2 sm_100a"; }
 
 namespace hsseig {
 std::atomic<long long> g_launches{0};

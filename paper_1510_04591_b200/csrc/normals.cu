@@ -1,0 +1,252 @@
+// The reference's Gaussian sample block on the device, bit-for-bit.
+//
+// rand_hss_construct draws Omega = default_rng(seed).standard_normal((k, w))
+// (pkg/src/hsseig/hss.py:236-237): NumPy's PCG64 (XSL-RR 128/64) bit stream fed
+// through its 256-layer ziggurat for the normal distribution (NumPy
+// random/src/distributions: random_standard_normal; third-party, not vendored).
+// The generator is sequential and the ziggurat rejects a variable number of
+// draws, so the device version works in three passes over the raw stream:
+//   1. raw     : every thread jumps the LCG to its segment (O(log n) advance) and
+//                writes its 64-bit outputs;
+//   2. walk    : every segment parses the rejection chain from the first E entry
+//                offsets it can be entered at and records exit position and count;
+//   3. resolve : one block fixes the true entry offset of each segment (chains
+//                from nearby offsets merge within a few draws, so the look-back
+//                is short) and prefix-sums the counts;
+//   4. emit    : every segment re-walks from its true entry and writes its normals
+//                at their global index.
+// The ziggurat tables are NumPy's own (ki/wi/fi), loaded once by the host from the
+// installed NumPy and checked against NumPy output before use.
+#include "common.cuh"
+
+namespace hsseig {
+
+typedef unsigned __int128 u128;
+
+constexpr int kSeg = 256;      // raw draws per segment
+constexpr int kEntries = 4;    // entry offsets tried per segment
+constexpr double kZigR = 3.6541528853610088;
+constexpr double kZigInvR = 0.27366123732975828;
+
+__device__ uint64_t g_ki[256];
+__device__ double g_wi[256];
+__device__ double g_fi[256];
+static bool g_tables_loaded = false;
+
+__device__ __forceinline__ u128 mk128(uint64_t hi, uint64_t lo) { return ((u128)hi << 64) | lo; }
+
+__device__ __forceinline__ uint64_t xsl_rr(u128 s) {
+  const uint64_t x = (uint64_t)(s >> 64) ^ (uint64_t)s;
+  const unsigned rot = (unsigned)(s >> 122);
+  return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+// state after `delta` LCG steps (PCG's O(log delta) jump)
+__device__ u128 lcg_advance(u128 state, u128 delta, u128 mult, u128 plus) {
+  u128 acc_mult = 1, acc_plus = 0;
+  while (delta > 0) {
+    if (delta & 1) {
+      acc_mult *= mult;
+      acc_plus = acc_plus * mult + plus;
+    }
+    plus = (mult + 1) * plus;
+    mult *= mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+__global__ void raw_kernel(uint64_t sh, uint64_t sl, uint64_t ih, uint64_t il, int64_t L,
+                           uint64_t* __restrict__ U) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t p0 = t * kSeg;
+  if (p0 >= L) return;
+  const u128 mult = mk128(2549297995355413924ull, 4865540595714422341ull);
+  const u128 inc = mk128(ih, il);
+  u128 s = lcg_advance(mk128(sh, sl), (u128)p0, mult, inc);
+  const int64_t pe = p0 + kSeg < L ? p0 + kSeg : L;
+  for (int64_t p = p0; p < pe; ++p) {
+    s = s * mult + inc;
+    U[p] = xsl_rr(s);
+  }
+}
+
+__device__ __forceinline__ double unit(uint64_t r) { return (double)(r >> 11) * (1.0 / 9007199254740992.0); }
+
+// Parse one normal starting at draw p; returns the next start, writes the value.
+// Draws beyond L count as failure (returns L).
+__device__ __forceinline__ int64_t one_normal(const uint64_t* __restrict__ U, int64_t p, int64_t L,
+                                              double* val) {
+  for (;;) {
+    if (p >= L) return L;
+    uint64_t r = U[p];
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffull;
+    double x = (double)rabs * g_wi[idx];
+    if (sign) x = -x;
+    if (rabs < g_ki[idx]) { *val = x; return p + 1; }
+    if (idx == 0) {
+      int64_t q = p + 1;
+      for (;;) {
+        if (q + 1 >= L) return L;
+        const double xx = -kZigInvR * log1p(-unit(U[q]));
+        const double yy = -log1p(-unit(U[q + 1]));
+        q += 2;
+        if (yy + yy > xx * xx) {
+          *val = ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
+          return q;
+        }
+      }
+    }
+    if (p + 1 >= L) return L;
+    if ((g_fi[idx - 1] - g_fi[idx]) * unit(U[p + 1]) + g_fi[idx] < exp(-0.5 * x * x)) {
+      *val = x;
+      return p + 2;
+    }
+    p += 2;  // wedge rejection: the same normal restarts on the next draws
+  }
+}
+
+// exit position and start count of the chain entering segment t at offset e
+__global__ void walk_kernel(const uint64_t* __restrict__ U, int64_t L, int nseg,
+                            int64_t* __restrict__ exitpos, int32_t* __restrict__ count) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nseg) return;
+  const int64_t a = (int64_t)t * kSeg, b = a + kSeg;
+  for (int e = 0; e < kEntries; ++e) {
+    int64_t p = a + e;
+    int c = 0;
+    double v;
+    while (p < b) {
+      p = one_normal(U, p, L, &v);
+      ++c;
+    }
+    exitpos[t * kEntries + e] = p;
+    count[t * kEntries + e] = c;
+  }
+}
+
+// one block: true entry offset of every segment, then an exclusive scan of the counts
+__global__ void resolve_kernel(const int64_t* __restrict__ exitpos, const int32_t* __restrict__ count,
+                               int nseg, int64_t n, int32_t* __restrict__ entry,
+                               int64_t* __restrict__ base, int32_t* __restrict__ fail) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (nseg + nt - 1) / nt;
+  const int s0 = tid * per, s1 = min(nseg, s0 + per);
+  // entry of segment t: from the previous segment's exit; a segment whose exit does not
+  // depend on its entry ("merged") makes the next entry known without looking further back
+  for (int t = s0; t < s1; ++t) {
+    // nearest earlier segment q0 whose exit does not depend on its entry
+    int q0 = t - 1;
+    while (q0 >= 0) {
+      const int64_t* x = exitpos + (int64_t)q0 * kEntries;
+      bool merged = true;
+      for (int q = 1; q < kEntries; ++q) merged &= (x[q] == x[0]);
+      if (merged) break;
+      --q0;
+    }
+    int eq, q;
+    if (q0 >= 0) {
+      eq = (int)(exitpos[(int64_t)q0 * kEntries] - (int64_t)(q0 + 1) * kSeg);
+      q = q0 + 1;
+    } else {
+      eq = 0;
+      q = 0;
+    }
+    for (; q < t; ++q) {
+      if (eq < 0 || eq >= kEntries) { *fail = 1; eq = 0; }
+      eq = (int)(exitpos[(int64_t)q * kEntries + eq] - (int64_t)(q + 1) * kSeg);
+    }
+    if (eq < 0 || eq >= kEntries) { *fail = 1; eq = 0; }
+    entry[t] = eq;
+  }
+  __syncthreads();
+  int64_t s = 0;
+  for (int t = s0; t < s1; ++t) s += count[(int64_t)t * kEntries + entry[t]];
+  part[tid] = s;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t acc = 0;
+    for (int q = 0; q < nt; ++q) {
+      const int64_t v = part[q];
+      part[q] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  int64_t acc = part[tid];
+  for (int t = s0; t < s1; ++t) {
+    base[t] = acc;
+    acc += count[(int64_t)t * kEntries + entry[t]];
+  }
+  if (tid == nt - 1) {
+    base[nseg] = acc;
+    if (acc < n) *fail = 2;   // raw stream too short (never at the sizes the margin covers)
+  }
+}
+
+__global__ void emit_kernel(const uint64_t* __restrict__ U, int64_t L, int nseg,
+                            const int32_t* __restrict__ entry, const int64_t* __restrict__ base,
+                            int64_t n, double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nseg) return;
+  const int64_t a = (int64_t)t * kSeg, b = a + kSeg;
+  int64_t p = a + entry[t], i = base[t];
+  while (p < b && i < n) {
+    double v;
+    p = one_normal(U, p, L, &v);
+    out[i++] = v;
+  }
+}
+
+}  // namespace hsseig
+
+using namespace hsseig;
+
+static int64_t raw_len(int64_t n) { return ((n + n / 16 + 4096 + kSeg - 1) / kSeg) * kSeg; }
+
+extern "C" int hsseig_set_normal_tables(const uint64_t* ki, const double* wi, const double* fi) {
+  if (!ki || !wi || !fi) return HSSEIG_ERR_ARG;
+  if (cudaMemcpyToSymbol(g_ki, ki, sizeof(uint64_t) * 256) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_wi, wi, sizeof(double) * 256) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_fi, fi, sizeof(double) * 256) != cudaSuccess)
+    return HSSEIG_ERR_CUDA;
+  g_tables_loaded = true;
+  return HSSEIG_OK;
+}
+
+extern "C" int64_t hsseig_normals_work_bytes(int64_t n) {
+  const int64_t L = raw_len(n);
+  const int64_t nseg = L / kSeg;
+  return 8 * L + nseg * kEntries * (8 + 4) + nseg * 4 + (nseg + 1) * 8 + 1024;
+}
+
+extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                                    uint64_t inc_lo, int64_t n, double* out, void* work,
+                                    int32_t* fail_dev, void* stream) {
+  if (!g_tables_loaded) return HSSEIG_ERR_ARG;
+  if (n < 0 || !out || !work || !fail_dev) return HSSEIG_ERR_ARG;
+  if (n == 0) return HSSEIG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t L = raw_len(n);
+  const int nseg = (int)(L / kSeg);
+  char* w = static_cast<char*>(work);
+  uint64_t* U = reinterpret_cast<uint64_t*>(w);
+  int64_t* exitpos = reinterpret_cast<int64_t*>(w + 8 * L);
+  int32_t* count = reinterpret_cast<int32_t*>(exitpos + (int64_t)nseg * kEntries);
+  int32_t* entry = count + (int64_t)nseg * kEntries;
+  int64_t* base = reinterpret_cast<int64_t*>(
+      (reinterpret_cast<uintptr_t>(entry + nseg) + 7) & ~(uintptr_t)7);
+  raw_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(state_hi, state_lo, inc_hi, inc_lo, L, U);
+  HSS_CHECK_LAUNCH();
+  walk_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(U, L, nseg, exitpos, count);
+  HSS_CHECK_LAUNCH();
+  resolve_kernel<<<1, 1024, 0, s>>>(exitpos, count, nseg, n, entry, base, fail_dev);
+  HSS_CHECK_LAUNCH();
+  emit_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(U, L, nseg, entry, base, n, out);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}

@@ -103,6 +103,11 @@ def update_vectors_dense(Qblock, Qprime, flops=None, out=None):
         flops.update_dense += gemm_flops(Qb.shape[0], *Qp.shape)
     if out is None:
         out = torch.empty(Qb.shape[0], Qp.shape[1], dtype=torch.float64, device="cuda")
+    # the TMA engine wants 16-byte aligned rows (even leading dimensions)
+    if Qb.stride(0) % 2:
+        Qb = torch.nn.functional.pad(Qb, (0, 1))[:, :Qb.shape[1]]
+    if Qp.stride(0) % 2:
+        Qp = torch.nn.functional.pad(Qp, (0, 1))[:, :Qp.shape[1]]
     nat.check(nat.load().hsseig_gemm(nat.ptr(Qb), Qb.stride(0), nat.ptr(Qp), Qp.stride(0),
                                      nat.ptr(out), out.stride(0), Qb.shape[0], Qp.shape[1],
                                      Qb.shape[1], nat.stream_ptr()), "gemm")
