@@ -34,7 +34,7 @@ namespace hsseig {
 
 constexpr int kMaps = 8;  // roles: 0 X, 1 G_l, 2 G_{l+1}, 3 F_{l-1} (or F_depth), 4 U, 5 B, 6 Vt, 7 D
 
-struct MapSet {
+struct alignas(128) MapSet {
   CUtensorMap m[kMaps];
 };
 
@@ -120,7 +120,7 @@ __device__ __forceinline__ void tmma_chunk(const double* __restrict__ sA, const 
 
 template <class T>
 __global__ void __launch_bounds__(T::THREADS, 1)
-    tma_gemm_kernel(const __grid_constant__ MapSet maps, const TJob* __restrict__ jobs, int njobs,
+    tma_gemm_kernel(const MapSet* __restrict__ maps, const TJob* __restrict__ jobs, int njobs,
                     int64_t M, int tiles_m) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>(
@@ -153,8 +153,8 @@ __global__ void __launch_bounds__(T::THREADS, 1)
             mbar_wait(&empty[slot], ((q / T::STAGES) & 1) ^ 1);
             mbar_expect_tx(&full[slot], T::A_BYTES + T::B_BYTES);
             unsigned char* st = sm + (size_t)slot * T::STAGE_BYTES;
-            tma_load_2d(st, &maps.m[jb.am[sg]], jb.acol[sg] + c * T::BK, m0, &full[slot]);
-            tma_load_2d(st + T::A_BYTES, &maps.m[jb.bm[sg]], jb.bcol[sg], jb.brow[sg] + c * T::BK,
+            tma_load_2d(st, &maps->m[jb.am[sg]], jb.acol[sg] + c * T::BK, m0, &full[slot]);
+            tma_load_2d(st + T::A_BYTES, &maps->m[jb.bm[sg]], jb.bcol[sg], jb.brow[sg] + c * T::BK,
                         &full[slot]);
           }
         }
@@ -321,9 +321,11 @@ struct Operand {
 
 static int g_sms = 0;
 
+// Tensor maps live in device memory (one MapSet per launch, filled by an ordered H2D copy
+// on the launch stream) so the kernel can pick a map by role at run time.
 template <class T>
-static int launch_tma(const Operand (&ops)[kMaps], const TJob* jobs, int njobs, int64_t M,
-                      cudaStream_t s) {
+static int launch_tma(const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jobs, int njobs,
+                      int64_t M, cudaStream_t s) {
   if (njobs <= 0 || M <= 0) return HSSEIG_OK;
   static int per_sm = 0;
   if (!per_sm) {
@@ -346,10 +348,12 @@ static int launch_tma(const Operand (&ops)[kMaps], const TJob* jobs, int njobs, 
     if (!make_map(&maps.m[r], ops[r].base, ops[r].rows, ops[r].cols, ops[r].ld, bc, br))
       return HSSEIG_ERR_ARG;
   }
+  if (cudaMemcpyAsync(dmaps, &maps, sizeof(MapSet), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return HSSEIG_ERR_CUDA;
   const int tiles_m = (int)((M + T::BM - 1) / T::BM);
   const int64_t total = (int64_t)tiles_m * njobs;
   const int grid = (int)imin64(total, (int64_t)g_sms * per_sm);
-  tma_gemm_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(maps, jobs, njobs, M, tiles_m);
+  tma_gemm_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(dmaps, jobs, njobs, M, tiles_m);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
@@ -360,52 +364,52 @@ static int tile_choice(const char* var, int dflt) {
 }
 
 // narrow outputs (ranks, N <= 112)
-static int launch_narrow(int n, const Operand (&ops)[kMaps], const TJob* jobs, int njobs, int64_t M,
-                         cudaStream_t s) {
+static int launch_narrow(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJob* jobs, int njobs,
+                         int64_t M, cudaStream_t s) {
   static const int variant = tile_choice("HSSEIG_TILE_NARROW", 1);
   if (variant == 0) {   // BM 128: 8 consumer warps of 32 x 8NF, NF = ceil(n/16)
     switch ((n + 15) / 16) {
-      case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 4, 2, 5>>(ops, jobs, njobs, M, s);
-      case 5: return launch_tma<TTile<4, 5, 4, 2, 5>>(ops, jobs, njobs, M, s);
-      case 6: return launch_tma<TTile<4, 6, 4, 2, 5>>(ops, jobs, njobs, M, s);
-      case 7: return launch_tma<TTile<4, 7, 4, 2, 5>>(ops, jobs, njobs, M, s);
+      case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
+      case 5: return launch_tma<TTile<4, 5, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
+      case 6: return launch_tma<TTile<4, 6, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
+      case 7: return launch_tma<TTile<4, 7, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
       default: return HSSEIG_ERR_ARG;
     }
   }
   // default: BM 64: 8 consumer warps of 32 x 8NF, NF = ceil(n/32)
   switch ((n + 31) / 32) {
-    case 1: case 2: return launch_tma<TTile<4, 2, 2, 4, 8>>(ops, jobs, njobs, M, s);
-    case 3: return launch_tma<TTile<4, 3, 2, 4, 8>>(ops, jobs, njobs, M, s);
-    case 4: return launch_tma<TTile<4, 4, 2, 4, 6>>(ops, jobs, njobs, M, s);
+    case 1: case 2: return launch_tma<TTile<4, 2, 2, 4, 8>>(ops, dm, jobs, njobs, M, s);
+    case 3: return launch_tma<TTile<4, 3, 2, 4, 8>>(ops, dm, jobs, njobs, M, s);
+    case 4: return launch_tma<TTile<4, 4, 2, 4, 6>>(ops, dm, jobs, njobs, M, s);
     default: return HSSEIG_ERR_ARG;
   }
 }
 
 // wide outputs (leaf finish N = leaf size; plain GEMM tiles), N <= 224
-static int launch_wide(int n, const Operand (&ops)[kMaps], const TJob* jobs, int njobs, int64_t M,
-                       cudaStream_t s) {
+static int launch_wide(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJob* jobs, int njobs,
+                       int64_t M, cudaStream_t s) {
   static const int variant = tile_choice("HSSEIG_TILE_WIDE", 1);
   if (variant == 0) {   // BM 64: 8 consumer warps of 16 x 8NF, NF = ceil(n/16)
     switch ((n + 15) / 16) {
       case 1: case 2: case 3: case 4: case 5: case 6:
-        return launch_tma<TTile<2, 6, 4, 2, 6>>(ops, jobs, njobs, M, s);
-      case 7: return launch_tma<TTile<2, 7, 4, 2, 6>>(ops, jobs, njobs, M, s);
-      case 8: return launch_tma<TTile<2, 8, 4, 2, 6>>(ops, jobs, njobs, M, s);
-      case 9: return launch_tma<TTile<2, 9, 4, 2, 6>>(ops, jobs, njobs, M, s);
-      case 10: return launch_tma<TTile<2, 10, 4, 2, 5>>(ops, jobs, njobs, M, s);
-      case 11: return launch_tma<TTile<2, 11, 4, 2, 5>>(ops, jobs, njobs, M, s);
-      case 12: return launch_tma<TTile<2, 12, 4, 2, 5>>(ops, jobs, njobs, M, s);
-      case 13: return launch_tma<TTile<2, 13, 4, 2, 5>>(ops, jobs, njobs, M, s);
-      case 14: return launch_tma<TTile<2, 14, 4, 2, 5>>(ops, jobs, njobs, M, s);
+        return launch_tma<TTile<2, 6, 4, 2, 6>>(ops, dm, jobs, njobs, M, s);
+      case 7: return launch_tma<TTile<2, 7, 4, 2, 6>>(ops, dm, jobs, njobs, M, s);
+      case 8: return launch_tma<TTile<2, 8, 4, 2, 6>>(ops, dm, jobs, njobs, M, s);
+      case 9: return launch_tma<TTile<2, 9, 4, 2, 6>>(ops, dm, jobs, njobs, M, s);
+      case 10: return launch_tma<TTile<2, 10, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
+      case 11: return launch_tma<TTile<2, 11, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
+      case 12: return launch_tma<TTile<2, 12, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
+      case 13: return launch_tma<TTile<2, 13, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
+      case 14: return launch_tma<TTile<2, 14, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
       default: return HSSEIG_ERR_ARG;
     }
   }
   // default: BM 64: 8 consumer warps of 32 x 8NF, NF = ceil(n/32)
   switch ((n + 31) / 32) {
-    case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 2, 4, 6>>(ops, jobs, njobs, M, s);
-    case 5: return launch_tma<TTile<4, 5, 2, 4, 6>>(ops, jobs, njobs, M, s);
-    case 6: return launch_tma<TTile<4, 6, 2, 4, 5>>(ops, jobs, njobs, M, s);
-    case 7: return launch_tma<TTile<4, 7, 2, 4, 5>>(ops, jobs, njobs, M, s);
+    case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 2, 4, 6>>(ops, dm, jobs, njobs, M, s);
+    case 5: return launch_tma<TTile<4, 5, 2, 4, 6>>(ops, dm, jobs, njobs, M, s);
+    case 6: return launch_tma<TTile<4, 6, 2, 4, 5>>(ops, dm, jobs, njobs, M, s);
+    case 7: return launch_tma<TTile<4, 7, 2, 4, 5>>(ops, dm, jobs, njobs, M, s);
     default: return HSSEIG_ERR_ARG;
   }
 }
@@ -430,7 +434,7 @@ using namespace hsseig;
 
 static int64_t jobs_doubles(int64_t n_leaves) {
   const int64_t njobs = 2 * (2 * n_leaves - 2) + n_leaves;
-  return (njobs * (int64_t)sizeof(TJob) + 7) / 8 + 32;
+  return (njobs * (int64_t)sizeof(TJob) + 7) / 8 + 32 + 66 * (int64_t)sizeof(MapSet) / 8 + 32;
 }
 
 extern "C" int64_t hsseig_matmul_work_doubles(int64_t P, const hsseig_tree* t) {
@@ -457,6 +461,10 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   p.Gb = work;
   p.Fb = work + lvl_total;
   TJob* jobs = reinterpret_cast<TJob*>(work + 2 * lvl_total);
+  const int njob_total = 2 * nup + n;
+  MapSet* dmaps = reinterpret_cast<MapSet*>(
+      (reinterpret_cast<uintptr_t>(jobs + njob_total) + 255) & ~(uintptr_t)255);
+  if (t->depth > 31) return HSSEIG_ERR_ARG;
   setup_jobs_kernel<<<(2 * nup + n + 127) / 128, 128, 0, s>>>(p, jobs);
   HSS_CHECK_LAUNCH();
   auto lvl = [&](double* base, int l) -> Operand {
@@ -473,20 +481,24 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   int rc;
   for (int l = t->depth; l >= 1; --l) {
     const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), lvl(p.Gb, l + 1), none, Uop, Bop, Vtop, Dop};
-    if ((rc = launch_narrow(t->w, ops, jobs + ((1 << l) - 2), 1 << l, P, s))) return rc;
+    if ((rc = launch_narrow(t->w, ops, dmaps + (t->depth - l), jobs + ((1 << l) - 2), 1 << l, P, s)))
+      return rc;
   }
   for (int l = 1; l <= t->depth; ++l) {
     const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), none, lvl(p.Fb, l - 1), Uop, Bop, Vtop, Dop};
-    if ((rc = launch_narrow(t->w, ops, jobs + nup + ((1 << l) - 2), 1 << l, P, s))) return rc;
+    if ((rc = launch_narrow(t->w, ops, dmaps + t->depth + l - 1, jobs + nup + ((1 << l) - 2), 1 << l,
+                            P, s)))
+      return rc;
   }
   const Operand ops[kMaps] = {Xop, none, none, lvl(p.Fb, t->depth), Uop, Bop, Vtop, Dop};
-  return launch_wide(t->mmax, ops, jobs + 2 * nup, n, P, s);
+  return launch_wide(t->mmax, ops, dmaps + 2 * t->depth, jobs + 2 * nup, n, P, s);
 }
 
 extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                            int64_t ldc, int64_t M, int64_t N, int64_t K, void* stream) {
   // Test/bench helper: plain C = A B on the same TMA/DMMA engine, N split in 128-wide jobs.
   static TJob* jobs = nullptr;
+  static MapSet* dmaps = nullptr;
   static int cap = 0;
   if (M < 0 || N < 0 || K < 0 || lda < K || ldb < N || ldc < N) return HSSEIG_ERR_ARG;
   if (M == 0 || N == 0) return HSSEIG_OK;
@@ -500,13 +512,16 @@ extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_
     if (cudaMalloc(&jobs, sizeof(TJob) * nj) != cudaSuccess) return HSSEIG_ERR_CUDA;
     cap = nj;
   }
+  if (!dmaps) {
+    if (cudaMalloc(&dmaps, sizeof(MapSet)) != cudaSuccess) return HSSEIG_ERR_CUDA;
+  }
   plain_jobs_kernel<<<(nj + 127) / 128, 128, 0, s>>>(jobs, nj, C, ldc, (int)N, (int)K);
   HSS_CHECK_LAUNCH();
   // the maps carry the exact extents, so TMA zero-fills the K / N tails
   const Operand none{nullptr, 0, 0, 0};
   const Operand ops[kMaps] = {Operand{A, (uint64_t)M, (uint64_t)K, (uint64_t)lda}, none, none, none,
                               Operand{B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb}, none, none, none};
-  return launch_wide(128, ops, jobs, nj, M, s);
+  return launch_wide(128, ops, dmaps, jobs, nj, M, s);
 }
 
 extern "C" const char* hsseig_version(void) { return "hsseig_b200 0.2 sm_100a"; }

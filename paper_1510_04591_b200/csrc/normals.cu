@@ -24,7 +24,7 @@ namespace hsseig {
 typedef unsigned __int128 u128;
 
 constexpr int kSeg = 256;      // raw draws per segment
-constexpr int kEntries = 4;    // entry offsets tried per segment
+constexpr int kEntries = 16;   // entry offsets tried per segment
 constexpr double kZigR = 3.6541528853610088;
 constexpr double kZigInvR = 0.27366123732975828;
 
@@ -109,22 +109,49 @@ __device__ __forceinline__ int64_t one_normal(const uint64_t* __restrict__ U, in
   }
 }
 
-// exit position and start count of the chain entering segment t at offset e
+// exit position and start count of the chain entering segment t at offset e.  The chain
+// from offset 0 is walked in full and its starts kept in a 256-bit map; the chains from
+// the other offsets stop as soon as they land on one of those starts (they coincide
+// from there on), so each extra entry costs only a few parses.
 __global__ void walk_kernel(const uint64_t* __restrict__ U, int64_t L, int nseg,
                             int64_t* __restrict__ exitpos, int32_t* __restrict__ count) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nseg) return;
   const int64_t a = (int64_t)t * kSeg, b = a + kSeg;
-  for (int e = 0; e < kEntries; ++e) {
-    int64_t p = a + e;
+  uint32_t bits[kSeg / 32];
+#pragma unroll
+  for (int q = 0; q < kSeg / 32; ++q) bits[q] = 0u;
+  int64_t p = a;
+  int c0 = 0;
+  double v;
+  while (p < b) {
+    const int r = (int)(p - a);
+    bits[r >> 5] |= 1u << (r & 31);
+    p = one_normal(U, p, L, &v);
+    ++c0;
+  }
+  const int64_t x0 = p;
+  exitpos[(int64_t)t * kEntries] = x0;
+  count[(int64_t)t * kEntries] = c0;
+  for (int e = 1; e < kEntries; ++e) {
+    p = a + e;
     int c = 0;
-    double v;
+    bool merged = false;
     while (p < b) {
+      const int r = (int)(p - a);
+      if ((bits[r >> 5] >> (r & 31)) & 1u) {
+        // chain-0 starts at positions >= r
+        int rest = __popc(bits[r >> 5] >> (r & 31));
+        for (int q = (r >> 5) + 1; q < kSeg / 32; ++q) rest += __popc(bits[q]);
+        c += rest;
+        merged = true;
+        break;
+      }
       p = one_normal(U, p, L, &v);
       ++c;
     }
-    exitpos[t * kEntries + e] = p;
-    count[t * kEntries + e] = c;
+    exitpos[(int64_t)t * kEntries + e] = merged ? x0 : p;
+    count[(int64_t)t * kEntries + e] = c;
   }
 }
 

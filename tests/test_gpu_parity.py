@@ -286,3 +286,13 @@ def test_isolated_merge_orthogonality(n):
     uu = torch.as_tensor(u, device="cuda")
     R = dd[:, None] * Cd + rho * uu[:, None] * (uu[None, :] @ Cd) - Cd * lam[None, :]
     assert float(R.abs().max()) <= 1e-11
+
+
+# ------------------------------------------------------- sample draw (hss.py:236)
+@pytest.mark.parametrize("seed,k,w", [([0, 0], 32768, 84), ([3, 17], 5000, 37), ([1, 2], 100, 7)])
+def test_device_sample_draw_is_numpy_bit_exact(seed, k, w):
+    from paper_1510_04591_b200 import sample_rng
+    assert sample_rng.available(), "NumPy ziggurat tables not found / device draw mismatch"
+    got = sample_rng.normals(seed, k * w).cpu().numpy()
+    ref = np.random.default_rng(seed).standard_normal((k, w)).ravel()
+    np.testing.assert_array_equal(got, ref)
