@@ -102,7 +102,7 @@ int hsseig_cauchy_block(const hsseig_gen *gen, const int64_t *rows, int64_t nr,
  * (a7) Randomized sampling Y = C @ Omega and Z = C^T @ Omega with C generated
  * tile by tile in shared memory and contracted on FP64 DMMA.
  * Replaces CauchyEvecMatrix.multiply / transpose_multiply (cauchy.py:70-100).
- * Omega: k x w (ld = ldom).  Y, Z: k x w (ld = ldy).
+ * Omega: k x w (ld = ldom, even; 16-byte aligned rows for TMA).  Y, Z: k x w (ld = ldy).
  * work: hsseig_sample_work_doubles(k, w) doubles (split-K partials).
  */
 int64_t hsseig_sample_work_doubles(int64_t k, int64_t w);
@@ -182,14 +182,17 @@ int hsseig_dense_update(const double *Qb, int64_t ldq, int64_t P, const hsseig_g
  * numpy.random.Generator(PCG64(state, inc)).standard_normal(n) (hss.py:236-237).
  * hsseig_set_normal_tables loads NumPy's ziggurat tables (ki, wi, fi; 256 each, host
  * pointers) once.  state/inc: the PCG64 128-bit state and increment as hi/lo words
- * (Generator.bit_generator.state).  work: hsseig_normals_work_bytes(n) bytes.
+ * (Generator.bit_generator.state).  Value i goes to out[(i / w) * ldo + i % w], i.e. the
+ * row-major (n / w) x w block standard_normal((n / w, w)) with leading dimension ldo.
+ * work: hsseig_normals_work_bytes(n) bytes.
  * *fail_dev (int32, device) is set non-zero if the rejection chain could not be
  * resolved; the caller then draws on the host instead.
  */
 int hsseig_set_normal_tables(const uint64_t *ki, const double *wi, const double *fi);
 int64_t hsseig_normals_work_bytes(int64_t n);
 int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
-                         int64_t n, double *out, void *work, int32_t *fail_dev, void *stream);
+                         int64_t n, int64_t w, int64_t ldo, double *out, void *work,
+                         int32_t *fail_dev, void *stream);
 
 /* Plain batched helper used by tests/bench: out = A @ B (P x K)(K x N), FP64 DMMA. */
 int hsseig_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,

@@ -10,7 +10,7 @@ from . import _native as nat
 from .flops import cauchy_eval_flops, gemm_flops
 from .secular import column_normalizers, dev, stable_gap
 
-MAX_SAMPLE_WIDTH = 112
+MAX_SAMPLE_WIDTH = 128
 
 
 class CauchyEvecMatrix:
@@ -85,6 +85,10 @@ class CauchyEvecMatrix:
             Y, Z = torch.cat([p[0] for p in parts], 1), torch.cat([p[1] for p in parts], 1)
         else:
             lib = nat.load()
+            if omega.stride(0) % 2 or omega.data_ptr() % 16:   # TMA wants 16-byte aligned rows
+                padded = torch.zeros(self.k, w + (w % 2), dtype=torch.float64, device="cuda")
+                padded[:, :w] = omega
+                omega = padded
             Y = torch.empty(self.k, w, dtype=torch.float64, device="cuda")
             Z = torch.empty_like(Y)
             work = torch.empty(int(lib.hsseig_sample_work_doubles(self.k, w)), dtype=torch.float64,

@@ -11,7 +11,7 @@
 // blockIdx.y; partial tiles go to a workspace and are summed in a fixed order so
 // the result is deterministic run to run (the reference's determinism-in-seed
 // contract, pkg/tests/test_hss.py:192-200).
-#include "dmma_gemm.cuh"
+#include "tma.cuh"
 
 namespace hsseig {
 
@@ -24,56 +24,135 @@ __global__ void cauchy_block_kernel(CauchyGen g, const int64_t* __restrict__ row
   out[a * ldo + b] = g.entry(rows[a], cols[b]);
 }
 
+// Sampling, warp-specialised: GEN generator warps evaluate the BM x BK tile of C (or C^T)
+// on the FP64 pipe straight into a shared-memory ring and one of them arms the TMA copy
+// of the matching Omega rows; WM x WN consumer warps contract on the DMMA tensor
+// sub-pipe.  The two pipes overlap, and full/empty mbarriers replace block barriers.
+// Work items are (row tile, K split) pairs walked persistently; partial tiles go to
+// part[split] and are reduced in a fixed order (deterministic).
+constexpr int kGenWarps = 4;
+
 template <class T, bool TRANS>
-__global__ void __launch_bounds__(T::THREADS) sample_kernel(CauchyGen g,
-                                                            const double* __restrict__ om,
-                                                            int64_t ldom, int w,
-                                                            double* __restrict__ part,
-                                                            int64_t ldp, int64_t kchunk) {
-  extern __shared__ __align__(16) double smem[];
+__global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
+    sample_ws_kernel(CauchyGen g, const MapSet* __restrict__ omap, int w, double* __restrict__ part,
+                     int64_t ldp, int kchunk, int nsplit, int tiles) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 127) & ~(uintptr_t)127);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)T::STAGE_BYTES * T::STAGES);
+  uint64_t* empty = full + T::STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / T::WN, wn = warp % T::WN;
   const int64_t k = g.k;
-  const int64_t m0 = (int64_t)blockIdx.x * T::BM;
-  const int64_t kbeg = (int64_t)blockIdx.y * kchunk;
-  const int64_t kend = min(k, kbeg + kchunk);
-  const int nch = (int)((kend - kbeg + T::BK - 1) / T::BK);
-  Acc<T> acc;
-  acc.zero();
-
-  auto stage_a = [&](int s) { return smem + s * T::STAGE_ELEMS; };
-  auto stage_b = [&](int s) { return smem + s * T::STAGE_ELEMS + T::A_ELEMS; };
-  auto produce = [&](int c, int s) {
-    const int64_t k0 = kbeg + (int64_t)c * T::BK;
-    // Omega rows [k0, k0+BK) (async)
-    load_b_async<T>(stage_b(s), om + k0 * ldom, ldom, 1, (int)imin64(T::BK, kend - k0), 0, w,
-                    0, tid);
-    cp_async_commit();
-    // C tile (computed): A[r][c] = C[m0+r][k0+c]  or  C[k0+c][m0+r] for C^T
-    double* sA = stage_a(s);
-    for (int e = tid; e < T::BM * T::BK; e += T::THREADS) {
-      int r = e / T::BK, cc = e % T::BK;
-      int64_t row = m0 + r, col = k0 + cc;
-      double val = 0.0;
-      if (row < k && col < kend) val = TRANS ? g.entry(col, row) : g.entry(row, col);
-      sA[r * T::SA + cc] = val;
+  const int items = tiles * nsplit;
+  if (tid == 0) {
+    for (int s = 0; s < T::STAGES; ++s) {
+      mbar_init(&full[s], kGenWarps + 1);
+      mbar_init(&empty[s], T::CONSUMERS);
     }
-  };
-
-  produce(0, 0);
-  for (int c = 0; c < nch; ++c) {
-    const int s = c & 1;
-    if (c + 1 < nch) {
-      produce(c + 1, s ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    mma_chunk<T>(stage_a(s), stage_b(s), acc, wm, wn, lane);
-    __syncthreads();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  store_acc<T>(acc, part + (int64_t)blockIdx.y * k * ldp, ldp, k, m0, w, 0, wm, wn, lane);
+  __syncthreads();
+
+  if (warp >= T::CONSUMERS) {
+    // ---------------- generators ----------------
+    constexpr int GT = kGenWarps * 32;
+    constexpr int PER = T::BM * T::BK / GT;       // entries per thread per chunk
+    constexpr int CPR = T::BK / PER;              // threads per tile row
+    const int gt = tid - T::CONSUMERS * 32;
+    const int r = gt / CPR, c0 = (gt % CPR) * PER;
+    uint32_t q = 0;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+      const int tile = it % tiles, split = it / tiles;
+      const int64_t m0 = (int64_t)tile * T::BM;
+      const int64_t kbeg = (int64_t)split * kchunk;
+      const int64_t kend = imin64(k, kbeg + kchunk);
+      const int nch = (int)((kend - kbeg + T::BK - 1) / T::BK);
+      // fixed index of this thread's tile row: i (rows of C) or j (columns of C, TRANS)
+      const int64_t fix = m0 + r;
+      const bool fix_ok = fix < k;
+      double fd = 0.0, fz = 0.0, fdn = 0.0, fg = 0.0, fm = 0.0, fv = 0.0;
+      if (fix_ok) {
+        fd = __ldg(g.d + fix);
+        if (TRANS) {
+          fdn = __ldg(g.dnext + fix); fg = __ldg(g.gam + fix); fm = __ldg(g.mu + fix);
+          fv = __ldg(g.v + fix);
+        } else {
+          fz = __ldg(g.zhat + fix);
+        }
+      }
+      for (int c = 0; c < nch; ++c, ++q) {
+        const int slot = q % T::STAGES;
+        mbar_wait(&empty[slot], ((q / T::STAGES) & 1) ^ 1);
+        const int64_t k0 = kbeg + (int64_t)c * T::BK;
+        double* sA = reinterpret_cast<double*>(sm + (size_t)slot * T::STAGE_BYTES);
+#pragma unroll
+        for (int e = 0; e < PER; ++e) {
+          const int64_t var = k0 + c0 + e;   // the index running along K
+          double val = 0.0;
+          if (fix_ok && var < kend) {
+            if (TRANS) {   // C[var][fix]
+              const double di = __ldg(g.d + var);
+              const double gap = stable_gap(var, fix, di, fd, fdn, fg, fm);
+              val = (__ldg(g.zhat + var) * fv) / gap;
+            } else {       // C[fix][var]
+              const double gap = stable_gap(fix, var, fd, __ldg(g.d + var), __ldg(g.dnext + var),
+                                            __ldg(g.gam + var), __ldg(g.mu + var));
+              val = (fz * __ldg(g.v + var)) / gap;
+            }
+          }
+          sA[r * T::SA + c0 + e] = val;
+        }
+        if (warp == T::CONSUMERS && lane == 0) {
+          mbar_expect_tx(&full[slot], T::B_BYTES);
+          tma_load_2d(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES, &omap->m[0], 0, (int)k0,
+                      &full[slot]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[slot]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- DMMA consumers ----------------
+  const int wm = warp / T::WN, wn = warp % T::WN;
+  const int gr = lane >> 2, gc = lane & 3;
+  const int jmax = max(0, min(T::NF, (w - wn * T::NF * 8 + 7) / 8));
+  uint32_t q = 0;
+  double acc[T::MF][T::NF][2];
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int tile = it % tiles, split = it / tiles;
+    const int64_t m0 = (int64_t)tile * T::BM;
+    const int64_t kbeg = (int64_t)split * kchunk;
+    const int64_t kend = imin64(k, kbeg + kchunk);
+    const int nch = (int)((kend - kbeg + T::BK - 1) / T::BK);
+#pragma unroll
+    for (int i = 0; i < T::MF; ++i)
+#pragma unroll
+      for (int j = 0; j < T::NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int c = 0; c < nch; ++c, ++q) {
+      const int slot = q % T::STAGES;
+      mbar_wait(&full[slot], (q / T::STAGES) & 1);
+      const double* sA = reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES);
+      const double* sB =
+          reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES);
+      tmma_chunk<T>(sA, sB, acc, wm, wn, lane, T::BK, jmax);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    double* P = part + (int64_t)split * k * ldp;
+#pragma unroll
+    for (int i = 0; i < T::MF; ++i) {
+      const int64_t row = m0 + wm * T::MF * 8 + i * 8 + gr;
+      if (row >= k) continue;
+#pragma unroll
+      for (int j = 0; j < T::NF; ++j) {
+        const int col = wn * T::NF * 8 + j * 8 + 2 * gc;
+        if (col < w) P[row * ldp + col] = acc[i][j][0];
+        if (col + 1 < w) P[row * ldp + col + 1] = acc[i][j][1];
+      }
+    }
+  }
 }
 
 // out[row][col] = sum_s part[s][row][col], s ascending (fixed order)
@@ -133,31 +212,52 @@ __global__ void __launch_bounds__(T::THREADS) dense_update_kernel(const double* 
   store_acc<T>(acc, out + n0, ldo, P, m0, (int)imin64(T::BN, k - n0), 0, wm, wn, lane);
 }
 
+static void sample_split(int64_t k, int64_t bm, int64_t* nsplit, int64_t* kchunk) {
+  const int64_t tiles = (k + bm - 1) / bm;
+  int64_t ns = (148 * 6 + tiles - 1) / tiles;     // enough items to keep every SM busy
+  ns = imax64(1, imin64(ns, (k + 511) / 512));
+  int64_t kc = (k + ns - 1) / ns;
+  kc = (kc + 15) / 16 * 16;
+  *nsplit = (k + kc - 1) / kc;
+  *kchunk = kc;
+}
+
 template <class T>
 static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int w, double* Y,
                          double* Z, int64_t ldy, double* work, cudaStream_t s) {
   const int64_t k = g.k;
   const int64_t tiles = (k + T::BM - 1) / T::BM;
   const int64_t ldp = ((w + 1) / 2) * 2;
-  // split K so that each of the two passes fills ~8 CTAs per SM
-  int64_t nsplit = (148 * 8 + tiles - 1) / tiles;
-  nsplit = imax64(1, imin64(nsplit, (k + 255) / 256));
-  int64_t kchunk = (k + nsplit - 1) / nsplit;
-  kchunk = ((kchunk + T::BK - 1) / T::BK) * T::BK;
-  nsplit = (k + kchunk - 1) / kchunk;
-  const size_t smem = sizeof(double) * T::STAGE_ELEMS * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sample_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(sample_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  int64_t nsplit, kchunk;
+  sample_split(k, T::BM, &nsplit, &kchunk);
+  constexpr int threads = (T::CONSUMERS + kGenWarps) * 32;
+  static int per_sm = 0, sms = 0;
+  if (!per_sm) {
+    cudaFuncSetAttribute(sample_ws_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_BYTES);
+    cudaFuncSetAttribute(sample_ws_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)T::SMEM_BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sample_ws_kernel<T, false>, threads, T::SMEM_BYTES);
+    if (per_sm < 1) per_sm = 1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  dim3 grid((unsigned)tiles, (unsigned)nsplit);
   double* pY = work;
   double* pZ = work + nsplit * k * ldp;
-  sample_kernel<T, false><<<grid, T::THREADS, smem, s>>>(g, om, ldom, w, pY, ldp, kchunk);
+  MapSet* dmap = reinterpret_cast<MapSet*>(
+      (reinterpret_cast<uintptr_t>(work + 2 * nsplit * k * ldp) + 255) & ~(uintptr_t)255);
+  MapSet maps;
+  for (int r = 1; r < kMaps; ++r) make_map(&maps.m[r], nullptr, 0, 0, 0, 0, 0);
+  if (!make_map(&maps.m[0], om, (uint64_t)k, (uint64_t)w, (uint64_t)ldom, T::SB, T::BK))
+    return HSSEIG_ERR_ARG;
+  if (cudaMemcpyAsync(dmap, &maps, sizeof(MapSet), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return HSSEIG_ERR_CUDA;
+  const int64_t items = tiles * nsplit;
+  const int grid = (int)imin64(items, (int64_t)sms * per_sm);
+  sample_ws_kernel<T, false><<<grid, threads, T::SMEM_BYTES, s>>>(g, dmap, w, pY, ldp, (int)kchunk,
+                                                                (int)nsplit, (int)tiles);
   HSS_CHECK_LAUNCH();
-  sample_kernel<T, true><<<grid, T::THREADS, smem, s>>>(g, om, ldom, w, pZ, ldp, kchunk);
+  sample_ws_kernel<T, true><<<grid, threads, T::SMEM_BYTES, s>>>(g, dmap, w, pZ, ldp, (int)kchunk,
+                                                               (int)nsplit, (int)tiles);
   HSS_CHECK_LAUNCH();
   unsigned rb = (unsigned)((k * w + 255) / 256);
   splitk_reduce_kernel<<<rb, 256, 0, s>>>(pY, (int)nsplit, k, w, ldp, Y, ldy);
@@ -196,31 +296,24 @@ extern "C" int hsseig_cauchy_block(const hsseig_gen* gen, const int64_t* rows, i
 }
 
 extern "C" int64_t hsseig_sample_work_doubles(int64_t k, int64_t w) {
-  // upper bound: nsplit <= 148*8 / tiles + 1 with tiles = ceil(k/128); two passes
-  int64_t tiles = (k + 127) / 128;
-  int64_t nsplit = (148 * 8 + tiles - 1) / tiles;
-  nsplit = nsplit < 1 ? 1 : nsplit;
-  int64_t cap = (k + 255) / 256;
-  if (nsplit > cap) nsplit = cap;
-  if (nsplit < 1) nsplit = 1;
-  int64_t ldp = ((w + 1) / 2) * 2;
-  return 2 * (nsplit + 1) * k * ldp;
+  int64_t nsplit, kchunk;
+  sample_split(k, 64, &nsplit, &kchunk);
+  const int64_t ldp = ((w + 1) / 2) * 2;
+  return 2 * nsplit * k * ldp + (int64_t)(sizeof(MapSet) + 512) / 8;
 }
 
 extern "C" int hsseig_cauchy_sample(const hsseig_gen* gen, const double* omega, int64_t ldom,
                                     int64_t w, double* Y, double* Z, int64_t ldy, double* work,
                                     void* stream) {
-  if (!gen || w < 1 || w > 112 || ldom < w || ldy < w) return HSSEIG_ERR_ARG;
+  if (!gen || w < 1 || w > 128 || ldom < w || ldy < w) return HSSEIG_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(omega) & 15) || (ldom & 1)) return HSSEIG_ERR_ARG;  // TMA rows
   CauchyGen g = to_gen(gen);
   cudaStream_t s = (cudaStream_t)stream;
-  switch ((w + 15) / 16) {
-    case 1: return launch_sample<Tile<4, 1, 4, 2, 2>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-    case 2: return launch_sample<Tile<4, 2, 4, 2, 2>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-    case 3: return launch_sample<Tile<4, 3, 4, 2, 2>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-    case 4: return launch_sample<Tile<4, 4, 4, 2, 2>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-    case 5: return launch_sample<Tile<4, 5, 4, 2, 2>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-    case 6: return launch_sample<Tile<4, 6, 4, 2, 2>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-    default: return launch_sample<Tile<4, 7, 4, 2, 2>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
+  switch ((w + 31) / 32) {   // BM 64: 8 DMMA warps of 32 x 8NF + 4 generator warps
+    case 1: return launch_sample<TTile<4, 1, 2, 4, 8>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
+    case 2: return launch_sample<TTile<4, 2, 2, 4, 8>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
+    case 3: return launch_sample<TTile<4, 3, 2, 4, 8>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
+    default: return launch_sample<TTile<4, 4, 2, 4, 6>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
   }
 }
 

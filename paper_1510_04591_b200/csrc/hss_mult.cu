@@ -23,20 +23,14 @@
 //
 // Job descriptors are built on the device from the ranks the construction wrote, so
 // no host synchronisation is needed between construction and multiply.
-#include <cudaTypedefs.h>
-
 #include <cstdlib>
 #include <cstring>
 
-#include "dmma_gemm.cuh"
+#include "tma.cuh"
 
 namespace hsseig {
 
-constexpr int kMaps = 8;  // roles: 0 X, 1 G_l, 2 G_{l+1}, 3 F_{l-1} (or F_depth), 4 U, 5 B, 6 Vt, 7 D
-
-struct alignas(128) MapSet {
-  CUtensorMap m[kMaps];
-};
+// tensor-map roles: 0 X, 1 G_l, 2 G_{l+1}, 3 F_{l-1} (or F_depth), 4 U, 5 B, 6 Vt, 7 D
 
 struct TJob {
   int32_t am[2], acol[2];            // A map role and column offset per segment (rows = tile)
@@ -45,78 +39,6 @@ struct TJob {
   double* C;
   int64_t ldc;
 };
-
-template <int MF_, int NF_, int WM_, int WN_, int STAGES_>
-struct TTile {
-  static constexpr int MF = MF_, NF = NF_, WM = WM_, WN = WN_, STAGES = STAGES_;
-  static constexpr int BM = WM * MF * 8;
-  static constexpr int BN = WN * NF * 8;
-  static constexpr int BK = 16;
-  static constexpr int SA = BK + 4;             // A box width (doubles) = smem row stride
-  static constexpr int SB = ((BN + 15) / 16) * 16 + 4;
-  static constexpr int CONSUMERS = WM * WN;
-  static constexpr int THREADS = (CONSUMERS + 1) * 32;
-  static constexpr int A_BYTES = BM * SA * 8;
-  static constexpr int B_BYTES = BK * SB * 8;
-  static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + 127) / 128) * 128;
-  static constexpr size_t SMEM_BYTES = (size_t)STAGE_BYTES * STAGES + 2 * STAGES * 8 + 128;
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-      "@!P bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <class T>
-__device__ __forceinline__ void tmma_chunk(const double* __restrict__ sA, const double* __restrict__ sB,
-                                           double (&c)[T::MF][T::NF][2], int wm, int wn, int lane,
-                                           int kv, int jmax) {
-  const int gr = lane >> 2, gc = lane & 3;
-#pragma unroll
-  for (int kk = 0; kk < T::BK; kk += 4) {
-    if (kk >= kv) break;
-    double a[T::MF], b[T::NF];
-#pragma unroll
-    for (int i = 0; i < T::MF; ++i) a[i] = sA[(wm * T::MF * 8 + i * 8 + gr) * T::SA + kk + gc];
-#pragma unroll
-    for (int j = 0; j < T::NF; ++j) b[j] = sB[(kk + gc) * T::SB + wn * T::NF * 8 + j * 8 + gr];
-#pragma unroll
-    for (int j = 0; j < T::NF; ++j) {
-      if (j >= jmax) break;
-#pragma unroll
-      for (int i = 0; i < T::MF; ++i) dmma_8x8x4(c[i][j][0], c[i][j][1], a[i], b[j]);
-    }
-  }
-}
 
 template <class T>
 __global__ void __launch_bounds__(T::THREADS, 1)
@@ -285,34 +207,6 @@ __global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs) {
 }
 
 // ---------------------------------------------------------------------------- host side
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult qr;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
-        qr == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// Row-major (rows x cols, leading dimension ld) float64 matrix, box of box_rows x box_cols.
-static bool make_map(CUtensorMap* m, const double* base, uint64_t rows, uint64_t cols, uint64_t ld,
-                     uint32_t box_cols, uint32_t box_rows) {
-  memset(m, 0, sizeof(*m));
-  if (!base) return true;   // role unused by this launch
-  auto fn = encode_fn();
-  if (!fn || rows == 0 || cols == 0) return false;
-  cuuint64_t gdim[2] = {cols, rows};
-  cuuint64_t gstride[1] = {ld * 8};
-  cuuint32_t box[2] = {box_cols, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 // Raw operand descriptions (rows, cols, ld) for the 8 roles of one launch.
 struct Operand {
   const double* base;

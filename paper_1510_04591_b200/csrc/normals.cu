@@ -217,7 +217,7 @@ __global__ void resolve_kernel(const int64_t* __restrict__ exitpos, const int32_
 
 __global__ void emit_kernel(const uint64_t* __restrict__ U, int64_t L, int nseg,
                             const int32_t* __restrict__ entry, const int64_t* __restrict__ base,
-                            int64_t n, double* __restrict__ out) {
+                            int64_t n, int64_t w, int64_t ldo, double* __restrict__ out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nseg) return;
   const int64_t a = (int64_t)t * kSeg, b = a + kSeg;
@@ -225,7 +225,8 @@ __global__ void emit_kernel(const uint64_t* __restrict__ U, int64_t L, int nseg,
   while (p < b && i < n) {
     double v;
     p = one_normal(U, p, L, &v);
-    out[i++] = v;
+    out[(i / w) * ldo + (i % w)] = v;   // row-major (n / w) x w block with leading dimension ldo
+    ++i;
   }
 }
 
@@ -252,10 +253,10 @@ extern "C" int64_t hsseig_normals_work_bytes(int64_t n) {
 }
 
 extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
-                                    uint64_t inc_lo, int64_t n, double* out, void* work,
-                                    int32_t* fail_dev, void* stream) {
+                                    uint64_t inc_lo, int64_t n, int64_t w, int64_t ldo, double* out,
+                                    void* work, int32_t* fail_dev, void* stream) {
   if (!g_tables_loaded) return HSSEIG_ERR_ARG;
-  if (n < 0 || !out || !work || !fail_dev) return HSSEIG_ERR_ARG;
+  if (n < 0 || w < 1 || ldo < w || !out || !work || !fail_dev) return HSSEIG_ERR_ARG;
   if (n == 0) return HSSEIG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t L = raw_len(n);
@@ -273,7 +274,7 @@ extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64
   HSS_CHECK_LAUNCH();
   resolve_kernel<<<1, 1024, 0, s>>>(exitpos, count, nseg, n, entry, base, fail_dev);
   HSS_CHECK_LAUNCH();
-  emit_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(U, L, nseg, entry, base, n, out);
+  emit_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(U, L, nseg, entry, base, n, w, ldo, out);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }

@@ -79,13 +79,19 @@ class NormalStream:
                                 dtype=torch.uint8, device="cuda")
         self.fail = torch.zeros(1, dtype=torch.int32, device="cuda")
 
-    def draw(self, seed, n, out, state=None):
-        """Enqueue the first n normals of default_rng(seed) into out (device float64)."""
+    def draw(self, seed, n, out, w=None, ld=None, state=None):
+        """Enqueue the first n normals of default_rng(seed) into out (device float64).
+
+        With w / ld the values land as the row-major (n / w) x w block with leading
+        dimension ld, i.e. standard_normal((n // w, w)) in a padded layout.
+        """
         if n > self.nmax:
             raise ValueError("draw longer than the stream buffers")
+        w = int(w or max(n, 1))
+        ld = int(ld or w)
         sh, sl, ih, il = state if state is not None else pcg_state(seed)
         self.fail.zero_()
-        nat.check(self.lib.hsseig_pcg64_normals(sh, sl, ih, il, int(n), nat.ptr(out),
+        nat.check(self.lib.hsseig_pcg64_normals(sh, sl, ih, il, int(n), w, ld, nat.ptr(out),
                                                 nat.ptr(self.work), nat.ptr(self.fail),
                                                 nat.stream_ptr()), "pcg64_normals")
         return out
