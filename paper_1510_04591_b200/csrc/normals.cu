@@ -261,9 +261,9 @@ extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t L = raw_len(n);
   const int nseg = (int)(L / kSeg);
-  char* w = static_cast<char*>(work);
-  uint64_t* U = reinterpret_cast<uint64_t*>(w);
-  int64_t* exitpos = reinterpret_cast<int64_t*>(w + 8 * L);
+  char* wk = static_cast<char*>(work);
+  uint64_t* U = reinterpret_cast<uint64_t*>(wk);
+  int64_t* exitpos = reinterpret_cast<int64_t*>(wk + 8 * L);
   int32_t* count = reinterpret_cast<int32_t*>(exitpos + (int64_t)nseg * kEntries);
   int32_t* entry = count + (int64_t)nseg * kEntries;
   int64_t* base = reinterpret_cast<int64_t*>(
