@@ -114,10 +114,12 @@ int hsseig_cauchy_sample(const hsseig_gen *gen, const double *omega, int64_t ldo
  * numbering over a power-of-two leaf count.  Topology arrays are filled by the
  * host (hsseig_tree_layout); numeric slots by hsseig_hss_build_rand.
  * Slot layout (all row-major, leading dimension `ws`):
- *   U, V : n_nodes slots of pmax x ws (p rows used, rank columns used)
- *   Vt   : n_nodes slots of ws x pmax (V transposed, rank rows used)
+ *   U, V : n_nodes slots of pmax x ws; candidate row q at slot row q + 1 (row 0 is zero)
+ *   Vt   : n_nodes slots of ws x pmax (V transposed; an inner node's right-child
+ *          candidates start at the next even column)
  *   B    : n_nodes slots of ws x ws   (rU(node) x rV(sibling))
- *   D    : n_leaves slots of dld x dld (leading dimension dld = mmax rounded up to even)
+ *   D    : n_leaves slots of (dld + 2) x dld, D[a][b] at row a + 1 (dld = mmax rounded to even)
+ *   ws   : w rounded up to a multiple of 16; every slot is zero outside its data
  *   rsel, csel, rloc, cloc : n_nodes x ws int32
  */
 typedef struct hsseig_tree {

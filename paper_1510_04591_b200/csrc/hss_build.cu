@@ -70,11 +70,12 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
   }
   const double* src = side == 0 ? Y : Z;
   double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * T.ws;
-  double* Dslot = T.D + (size_t)j * T.dld * T.dld;
+  // D slot: (dld + 2) x dld, row 0 and rows/cols past m are zero, D[a][b] at row a + 1
+  double* Dslot = T.D + (size_t)j * (T.dld + 2) * T.dld;
   if (side == 0) {
-    for (int e = tid; e < T.dld * T.dld; e += blockDim.x) {
-      const int a = e / T.dld, b = e % T.dld;
-      if (a >= m || b >= m) Dslot[e] = 0.0;
+    for (int e = tid; e < (T.dld + 2) * T.dld; e += blockDim.x) {
+      const int a = e / T.dld - 1, b = e % T.dld;
+      if (a < 0 || a >= m || b >= m) Dslot[e] = 0.0;
     }
   }
   for (int a0 = 0; a0 < m; a0 += RA) {
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
       int aa = e / m, b = e % m;
       double val = side == 0 ? g.entry(lo + a0 + aa, lo + b) : g.entry(lo + b, lo + a0 + aa);
       sD[aa * m + b] = val;
-      if (side == 0) Dslot[(size_t)(a0 + aa) * T.dld + b] = val;
+      if (side == 0) Dslot[(size_t)(a0 + aa + 1) * T.dld + b] = val;
     }
     __syncthreads();
     for (int e = tid; e < na * w; e += blockDim.x) {
@@ -370,14 +371,28 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
     if (sat) atomicAdd(reinterpret_cast<unsigned long long*>(&st->v[4]), 1ull);
     atomicMax(reinterpret_cast<long long*>(&st->v[5]), (long long)r);
   }
-  // full slots (zero padding beyond p rows / r columns keeps the multiply's K tails exact)
-  for (int e = tid; e < T.pmax * ws; e += nthr) {
+  // Full slots: zero padding beyond p rows / r columns keeps the multiply's K tails exact.
+  // U/V: candidate row q at slot row q + 1 (row 0 stays zero, so a TMA box may start one
+  // row early when its A operand starts at an odd column).  V^T: candidate q at column q,
+  // except that an inner node's right-child candidates start at an even column (TMA box
+  // starts must be 16-byte aligned).
+  int na_v = p;
+  if (!leaf) na_v = side == 0 ? T.rU[T.left[node]] : T.rV[T.left[node]];
+  const int rshift = (!leaf && (na_v & 1)) ? 1 : 0;
+  for (int e = tid; e < (T.pmax - 1) * ws; e += nthr) {
     const int jj = e / ws, t = e % ws;  // jj = position in pivoted order
     double val = 0.0;
     if (jj < p && t < r) val = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * SW + t];
-    const int row = jj < p ? piv[jj] : jj;
-    X[(size_t)row * ws + t] = val;
-    if (side == 1) Xt[(size_t)t * T.pmax + row] = val;
+    const int q = jj < p ? piv[jj] : jj;   // candidate row
+    X[(size_t)(q + 1) * ws + t] = val;
+    if (side == 1) {
+      const int col = q < na_v ? q : q + rshift;
+      if (col < T.pmax) Xt[(size_t)t * T.pmax + col] = val;
+    }
+  }
+  for (int t = tid; t < ws; t += nthr) {
+    X[t] = 0.0;
+    if (side == 1 && rshift) Xt[(size_t)t * T.pmax + na_v] = 0.0;
   }
   for (int t = tid; t < r; t += nthr) {
     const int pj = piv[t];
@@ -444,7 +459,7 @@ static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
   const int64_t nn = 2 * (int64_t)n_leaves - 1;
   const int64_t ws = (w + 15) / 16 * 16;
   int64_t pmax = std::max<int64_t>(mmax, 2 * (int64_t)w);
-  pmax += pmax & 1;
+  pmax += (pmax & 1) + 2;
   const int64_t dld = mmax + (mmax & 1);
   int64_t o = 0;
   auto take = [&](int64_t bytes) { int64_t at = o; o = align_up(o + bytes, 256); return at; };
@@ -456,7 +471,7 @@ static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
   c.off_flags = take(4 * 2 * nn);
   c.off_U = take(8 * nn * pmax * ws); c.off_V = take(8 * nn * pmax * ws);
   c.off_Vt = take(8 * nn * ws * pmax);
-  c.off_B = take(8 * nn * ws * ws); c.off_D = take(8 * (int64_t)n_leaves * dld * dld);
+  c.off_B = take(8 * nn * ws * ws); c.off_D = take(8 * (int64_t)n_leaves * (dld + 2) * dld);
   c.off_rres = take(8 * nn); c.off_cres = take(8 * nn);
   c.off_M = take(8 * 2 * (int64_t)n_leaves * pmax * ws);
   c.off_psel = take(8 * nn * ws * ws); c.off_tsel = take(8 * nn * ws * ws);
@@ -512,7 +527,7 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
   t->k = k; t->n_leaves = n_leaves; t->depth = depth; t->n_nodes = nn; t->w = w;
   t->ws = (w + 15) / 16 * 16;
   t->pmax = std::max<int32_t>(mmax, 2 * w);
-  t->pmax += t->pmax & 1;
+  t->pmax += (t->pmax & 1) + 2;
   t->mmax = mmax;
   t->dld = mmax + (mmax & 1);
   t->root = root;

@@ -170,14 +170,17 @@ __global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs) {
       jb.C = p.Gb + lvl_off(p.P, ws, l) + (int64_t)j * ws;
       jb.N = p.rU[node];
       if (l == p.depth) {
-        jb.am[0] = 0; jb.acol[0] = p.lo[node]; jb.K[0] = p.hi[node] - p.lo[node];
-        jb.bm[0] = 4; jb.brow[0] = node * p.pmax;
+        // TMA boxes must start on a 16-byte column: an odd leaf start begins one column
+        // early against the zero row that precedes every U slot
+        const int lo = p.lo[node], sh = lo & 1;
+        jb.am[0] = 0; jb.acol[0] = lo - sh; jb.K[0] = p.hi[node] - lo + sh;
+        jb.bm[0] = 4; jb.brow[0] = node * p.pmax + 1 - sh;
       } else {
         const int a = p.left[node], b = p.right[node];
         jb.am[0] = 2; jb.acol[0] = 2 * j * ws; jb.K[0] = p.rU[a];
-        jb.bm[0] = 4; jb.brow[0] = node * p.pmax;
+        jb.bm[0] = 4; jb.brow[0] = node * p.pmax + 1;
         jb.am[1] = 2; jb.acol[1] = (2 * j + 1) * ws; jb.K[1] = p.rU[b];
-        jb.bm[1] = 4; jb.brow[1] = node * p.pmax + p.rU[a];
+        jb.bm[1] = 4; jb.brow[1] = node * p.pmax + 1 + p.rU[a];
       }
     } else {
       const int sib = p.lnodes[(1 << l) - 1 + (j ^ 1)];
@@ -188,18 +191,19 @@ __global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs) {
       if (l > 1) {
         const int par = p.lnodes[(1 << (l - 1)) - 1 + (j >> 1)];
         jb.am[1] = 3; jb.acol[1] = (j >> 1) * ws; jb.K[1] = p.rV[par];
-        jb.bm[1] = 6; jb.brow[1] = par * ws; jb.bcol[1] = (j & 1) ? p.rV[p.left[par]] : 0;
+        const int nl = p.rV[p.left[par]];
+        jb.bm[1] = 6; jb.brow[1] = par * ws; jb.bcol[1] = (j & 1) ? nl + (nl & 1) : 0;
       }
     }
   } else {
     const int j = e - 2 * nup;
     const int node = p.lnodes[(1 << p.depth) - 1 + j];
-    const int lo = p.lo[node];
+    const int lo = p.lo[node], sh = lo & 1;
     jb.C = p.out + lo;
     jb.ldc = p.ldo;
     jb.N = jb.SW = p.hi[node] - lo;
-    jb.am[0] = 0; jb.acol[0] = lo; jb.K[0] = p.hi[node] - lo;
-    jb.bm[0] = 7; jb.brow[0] = j * p.dld;
+    jb.am[0] = 0; jb.acol[0] = lo - sh; jb.K[0] = p.hi[node] - lo + sh;
+    jb.bm[0] = 7; jb.brow[0] = j * (p.dld + 2) + 1 - sh;
     jb.am[1] = 3; jb.acol[1] = j * ws; jb.K[1] = p.rV[node];
     jb.bm[1] = 6; jb.brow[1] = node * ws;
   }
@@ -371,7 +375,7 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   const Operand Uop{t->U, (uint64_t)nn * t->pmax, (uint64_t)ws, (uint64_t)ws};
   const Operand Bop{t->B, (uint64_t)nn * ws, (uint64_t)ws, (uint64_t)ws};
   const Operand Vtop{t->Vt, (uint64_t)nn * ws, (uint64_t)t->pmax, (uint64_t)t->pmax};
-  const Operand Dop{t->D, (uint64_t)n * t->dld, (uint64_t)t->dld, (uint64_t)t->dld};
+  const Operand Dop{t->D, (uint64_t)n * (t->dld + 2), (uint64_t)t->dld, (uint64_t)t->dld};
   int rc;
   for (int l = t->depth; l >= 1; --l) {
     const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), lvl(p.Gb, l + 1), none, Uop, Bop, Vtop, Dop};

@@ -246,10 +246,11 @@ class HssTree:
 
     def slot(self, name, node, rows, cols):
         ws = self.ct.ws
-        if name in ("U", "V"):
+        if name in ("U", "V"):   # candidate rows start at slot row 1 (row 0 is zero padding)
             n = self.ct.pmax * ws
-        else:
-            n = ws * ws
+            flat = self._view(name, torch.float64, n, node * n)
+            return flat.view(-1, ws)[1:rows + 1, :cols].cpu().numpy().copy()
+        n = ws * ws
         flat = self._view(name, torch.float64, n, node * n)
         return flat.view(-1, ws)[:rows, :cols].cpu().numpy().copy()
 
@@ -260,9 +261,10 @@ class HssTree:
     def leaf_D(self, node):
         mm = self.ct.dld
         j = self._leaf_pos[node]
-        flat = self._view("D", torch.float64, mm * mm, j * mm * mm)
+        n = (mm + 2) * mm
+        flat = self._view("D", torch.float64, n, j * n)
         m = self.nodes[node].hi - self.nodes[node].lo
-        return flat.view(mm, mm)[:m, :m].cpu().numpy().copy()
+        return flat.view(mm + 2, mm)[1:m + 1, :m].cpu().numpy().copy()
 
 
 def _construct_flops(tree, k, w):

@@ -5,14 +5,14 @@ Same arithmetic and decisions as ``dc.merge_update`` + ``update_vectors_hss``
 
 * buffers for roots, generators, samples, tree and multiply workspace are
   allocated once per (k, rows) and reused;
-* the host only synchronises where the reference makes a data-dependent
-  decision: after the secular solve (bracket check + the partition / rank
-  estimate, which need a few pole gaps), and after the construction (the
-  flag -> dense-fallback decision); the Loewner radicand check is read at
-  that second point;
-* the Gaussian sample is the reference's own draw (NumPy PCG64, hss.py:236),
-  generated on a host thread that starts with the merge, so it overlaps the
-  secular / Loewner / normalizer kernels.
+* the host synchronises only where the reference makes a data-dependent
+  decision: after the secular solve (bracket check, partition and rank
+  estimate, which need the pole gaps) and after the construction (the
+  flag -> dense-fallback decision, where the Loewner radicand check is read too);
+* the Gaussian sample is the reference's own draw default_rng([seed, merge_id])
+  (hss.py:236), generated on the device bit-for-bit (sample_rng); if NumPy's
+  ziggurat tables cannot be loaded the same draw is made on a host thread that
+  starts with the merge.
 
 Per-phase device times are taken with CUDA events on the launching stream.
 """
@@ -23,10 +23,11 @@ import numpy as np
 import torch
 
 from . import _native as nat
+from . import sample_rng
 from .cauchy import CauchyEvecMatrix
 from .flops import cauchy_eval_flops, gemm_flops, secular_flops
-from .hss import (MAX_WIDTH, HssTree, _construct_flops, build_partition, estimate_rank,
-                  finish_construct, mult_flops)
+from .hss import (MAX_WIDTH, HssTree, _construct_flops, build_partition, finish_construct,
+                  mult_flops, rank_bound)
 from .secular import SecularConvergenceError, WeightRecomputationError
 
 _POOL = cf.ThreadPoolExecutor(max_workers=1)
@@ -34,23 +35,25 @@ MAX_W = MAX_WIDTH
 CHUNK = 1 << 18
 
 
-class OmegaStream:
-    """The reference's sample draw default_rng(seed).standard_normal((k, w)) (hss.py:236),
-    produced on a host thread straight into pinned memory.
+def _ceil16(x):
+    return (x + 15) // 16 * 16
 
-    The row-major (k, w) block is the first k*w values of the generator's normal
-    stream for every w, so generation can start before w is known; it stops as soon
-    as the target k*w is published.
+
+class HostOmega:
+    """Host fallback for the sample draw, produced on a thread into pinned memory.
+
+    The row-major (k, w) block is the first k*w values of the generator's normal stream
+    for every w, so generation starts before w is known and stops at the published k*w.
     """
 
-    def __init__(self, host_buf):
-        self.buf = host_buf.numpy()
-        self.target = self.buf.size
+    def __init__(self, n):
+        self.buf = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        self.np = self.buf.numpy()
+        self.target = n
         self.fut = None
 
     def start(self, seed):
-        self.target = self.buf.size
-        self.done_count = 0
+        self.target = self.np.size
         self.fut = _POOL.submit(self._work, seed)
 
     def _work(self, seed):
@@ -58,20 +61,19 @@ class OmegaStream:
         pos = 0
         while pos < self.target:
             n = min(CHUNK, self.target - pos)
-            g.standard_normal(out=self.buf[pos:pos + n])
+            g.standard_normal(out=self.np[pos:pos + n])
             pos += n
-            self.done_count = pos
         return pos
 
     def finish(self, count):
         self.target = count
-        got = self.fut.result()
+        got = self.fut.result() if self.fut is not None else 0
         assert got >= count
         return self.buf[:count]
 
 
 class MergePipeline:
-    def __init__(self, k, cfg, rows):
+    def __init__(self, k, cfg, rows, device_rng=True):
         nat.require_cuda()
         self.k, self.cfg, self.rows = int(k), cfg, int(rows)
         self.lib = nat.load()
@@ -89,12 +91,16 @@ class MergePipeline:
         self.h_status = torch.empty(8, dtype=torch.int64, pin_memory=True)
         self.h_mu = torch.empty(k, dtype=torch.float64, pin_memory=True)
         self.h_edges = torch.empty(3, dtype=torch.float64, pin_memory=True)
-        self.Y = torch.empty(k * MAX_W, **f64)
-        self.Z = torch.empty(k * MAX_W, **f64)
-        self.om = torch.empty(k * MAX_W, **f64)
-        self.h_om = torch.empty(k * MAX_W, dtype=torch.float64, pin_memory=True)
-        self.omega_stream = OmegaStream(self.h_om)
+        wmax = _ceil16(MAX_W)
+        self.Y = torch.empty(k * wmax, **f64)
+        self.Z = torch.empty(k * wmax, **f64)
+        self.om = torch.empty(k * wmax, **f64)
         self.sample_work = torch.empty(int(self.lib.hsseig_sample_work_doubles(k, MAX_W)), **f64)
+        self.device_rng = bool(device_rng) and sample_rng.available()
+        if self.device_rng:
+            self.normals = sample_rng.NormalStream(k * MAX_W)
+        else:
+            self.host_omega = HostOmega(k * MAX_W)
         self._tree_key = None
         self._mwork = None
 
@@ -106,8 +112,10 @@ class MergePipeline:
         lib, k, cfg = self.lib, self.k, self.cfg
         s = nat.stream_ptr()
         ev = self._events(7)
-        # the sample block is the reference's draw; start it on the host right away
-        self.omega_stream.start(seed)
+        if self.device_rng:
+            pcg = sample_rng.pcg_state(seed)
+        else:
+            self.host_omega.start(seed)
         ev[0].record()
         self.status.zero_()
         self.status[1:4] = k
@@ -120,8 +128,7 @@ class MergePipeline:
         # host needs: status (bracket), mu (partition shifts), span = lam[-1] - d[0]
         self.h_status.copy_(self.status, non_blocking=True)
         self.h_mu.copy_(self.mu, non_blocking=True)
-        edge = torch.stack([d[0], d[-1], self.gam[-1]])
-        self.h_edges.copy_(edge, non_blocking=True)
+        self.h_edges.copy_(torch.stack([d[0], d[-1], self.gam[-1]]), non_blocking=True)
         host_ready = torch.cuda.Event()
         host_ready.record()
         nat.check(lib.hsseig_loewner(nat.ptr(d), nat.ptr(self.dn), nat.ptr(self.gam),
@@ -137,7 +144,8 @@ class MergePipeline:
         bad = st[1] if st[1] < k else (st[2] if (k >= 2 and st[2] < k) else -1)
         if bad >= 0:
             raise SecularConvergenceError(f"root {bad} lost its bracket")
-        info = {"flops": {}, "ms": {}, "used_hss": False, "fell_back": False, "r_used": 0}
+        info = {"flops": {}, "ms": {}, "used_hss": False, "fell_back": False, "r_used": 0,
+                "device_rng": self.device_rng}
         fl_sec = secular_flops(k, iters) + 14 * k * k
         C = CauchyEvecMatrix(d, self.gam, self.mu, self.zh, self.v, dnext=self.dn)
         use_hss = cfg.method == "adc-rand" and k > cfg.hss_threshold
@@ -156,38 +164,45 @@ class MergePipeline:
                 r = min(r_est, part.min_leaf - cfg.oversample)
                 w = r + cfg.oversample
                 if r >= 1 and w <= MAX_W:
-                    self.omega_stream.finish(k * w)
-                    om = self.om[:k * w].view(k, w)
-                    om.copy_(self.h_om[:k * w].view(k, w), non_blocking=True)
+                    ws = _ceil16(w)
+                    om = self.om[:k * ws].view(k, ws)
+                    if self.device_rng:
+                        self.normals.draw(seed, k * w, om, w=w, ld=ws, state=pcg)
+                    else:
+                        hv = self.host_omega.finish(k * w)
+                        om[:, :w].copy_(hv.view(k, w), non_blocking=True)
                     ev[3].record()
-                    Y = self.Y[:k * w].view(k, w)
-                    Z = self.Z[:k * w].view(k, w)
-                    nat.check(lib.hsseig_cauchy_sample(C.gen, nat.ptr(om), w, w, nat.ptr(Y),
-                                                       nat.ptr(Z), w, nat.ptr(self.sample_work), s),
+                    Y = self.Y[:k * ws].view(k, ws)
+                    Z = self.Z[:k * ws].view(k, ws)
+                    nat.check(lib.hsseig_cauchy_sample(C.gen, nat.ptr(om), ws, w, nat.ptr(Y),
+                                                       nat.ptr(Z), ws, nat.ptr(self.sample_work), s),
                               "cauchy_sample")
                     ev[4].record()
                     tree = self._tree(part, w)
                     tree._status = _StatusView(self.status)
-                    nat.check(lib.hsseig_hss_build_rand(C.gen, nat.ptr(om), w, nat.ptr(Y),
-                                                        nat.ptr(Z), w, float(1e-15),
+                    nat.check(lib.hsseig_hss_build_rand(C.gen, nat.ptr(om), ws, nat.ptr(Y),
+                                                        nat.ptr(Z), ws, float(1e-15),
                                                         ctypes.byref(tree.ct), nat.ptr(self.status),
                                                         s), "hss_build_rand")
                     ev[5].record()
                     finish_construct(tree)   # synchronises: flags, ranks, r_used
+                    if self.device_rng and self.normals.failed():
+                        raise RuntimeError("device sample draw could not resolve its rejection chain")
                     fl_con = _construct_flops(tree, k, w)
-        self.omega_stream.finish(0)
+        if not self.device_rng:
+            self.host_omega.finish(0)
         st = self.status.cpu().tolist()
         if st[3] < k:
             raise WeightRecomputationError(f"non-positive radicand at index {st[3]}")
         if out is None:
             out = torch.empty(X.shape[0], k, dtype=torch.float64, device="cuda")
+        ev_m0 = torch.cuda.Event(enable_timing=True)
         if tree is not None and not tree.flagged:
             need = int(lib.hsseig_matmul_work_doubles(X.shape[0], ctypes.byref(tree.ct)))
             if self._mwork is None or self._mwork.numel() < need:
                 self._mwork = None
                 torch.cuda.empty_cache()
                 self._mwork = torch.empty(need, dtype=torch.float64, device="cuda")
-            ev_m0 = torch.cuda.Event(enable_timing=True)
             ev_m0.record()
             nat.check(lib.hsseig_hss_matmul_right(nat.ptr(X), X.stride(0), X.shape[0],
                                                   ctypes.byref(tree.ct), nat.ptr(out),
@@ -200,7 +215,6 @@ class MergePipeline:
             fl_mult_full = mult_flops(tree, k)
             fl_dense = 0
         else:
-            ev_m0 = torch.cuda.Event(enable_timing=True)
             ev_m0.record()
             C.right_multiply_into(X, out=out)
             ev[6].record()
@@ -244,7 +258,6 @@ class _StatusView:
 
 def _rank_from(part, span, mu_h, eps, cap):
     """estimate_rank (hss.py:87-103) from host copies of the boundary gaps."""
-    from .hss import rank_bound
     if part.n_leaves < 2:
         return 0
     r = 0

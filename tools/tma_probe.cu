@@ -22,7 +22,7 @@ __global__ void probe(const MapSet* maps, int c0, int c1, int bc, int br, double
   for (int e = threadIdx.x; e < bc * br; e += blockDim.x) out[e] = s[e];
 }
 
-int main() {
+int main(int argc, char** argv) {
   const int rows = 40, cols = 256, ld = 256;
   std::vector<double> h(rows * ld);
   for (int i = 0; i < rows * ld; ++i) h[i] = i;
@@ -33,7 +33,10 @@ int main() {
   MapSet* dm;
   cudaMalloc(&dm, sizeof(MapSet));
   struct Case { int bc, br, c0, c1, variant; };
-  Case cases[] = {{20, 16, 0, 0, 0}, {20, 16, 0, 0, 1}, {20, 64, 3, 0, 1}, {100, 16, 5, 30, 1}, {20, 64, 250, 10, 1}};
+  Case all[] = {{20, 16, 0, 0, 1}, {20, 64, 0, 0, 1}, {20, 16, 3, 0, 1}, {20, 16, 2, 0, 1},
+                 {20, 16, 4, 0, 1}, {20, 32, 2, 5, 1}, {100, 16, 6, 30, 1}, {20, 16, 250, 10, 1}};
+  int which = argc > 1 ? atoi(argv[1]) : 0;
+  Case cases[1] = {all[which]};
   for (auto& cs : cases) {
     MapSet ms;
     memset(&ms, 0, sizeof(ms));
