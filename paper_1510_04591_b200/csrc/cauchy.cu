@@ -30,7 +30,7 @@ __global__ void cauchy_block_kernel(CauchyGen g, const int64_t* __restrict__ row
 // sub-pipe.  The two pipes overlap, and full/empty mbarriers replace block barriers.
 // Work items are (row tile, K split) pairs walked persistently; partial tiles go to
 // part[split] and are reduced in a fixed order (deterministic).
-constexpr int kGenWarps = 4;
+constexpr int kGenWarps = 8;
 
 template <class T, bool TRANS>
 __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
@@ -55,11 +55,13 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
 
   if (warp >= T::CONSUMERS) {
     // ---------------- generators ----------------
+    // thread -> one K position vk of the chunk and FR tile rows (a, a + RS, ...);
+    // the tile-row ("fixed") generator data stays in registers for the whole item
     constexpr int GT = kGenWarps * 32;
-    constexpr int PER = T::BM * T::BK / GT;       // entries per thread per chunk
-    constexpr int CPR = T::BK / PER;              // threads per tile row
+    constexpr int RS = GT / T::BK;               // row groups
+    constexpr int FR = T::BM / RS;               // tile rows per thread
     const int gt = tid - T::CONSUMERS * 32;
-    const int r = gt / CPR, c0 = (gt % CPR) * PER;
+    const int vk = gt % T::BK, a0 = gt / T::BK;
     uint32_t q = 0;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
       const int tile = it % tiles, split = it / tiles;
@@ -67,45 +69,55 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
       const int64_t kbeg = (int64_t)split * kchunk;
       const int64_t kend = imin64(k, kbeg + kchunk);
       const int nch = (int)((kend - kbeg + T::BK - 1) / T::BK);
-      // fixed index of this thread's tile row: i (rows of C) or j (columns of C, TRANS)
-      const int64_t fix = m0 + r;
-      const bool fix_ok = fix < k;
-      double fd = 0.0, fz = 0.0, fdn = 0.0, fg = 0.0, fm = 0.0, fv = 0.0;
-      if (fix_ok) {
-        fd = __ldg(g.d + fix);
-        if (TRANS) {
-          fdn = __ldg(g.dnext + fix); fg = __ldg(g.gam + fix); fm = __ldg(g.mu + fix);
-          fv = __ldg(g.v + fix);
-        } else {
-          fz = __ldg(g.zhat + fix);
+      double fd[FR], f1[FR], f2[FR], f3[FR], f4[FR];
+      bool fok[FR];
+#pragma unroll
+      for (int u = 0; u < FR; ++u) {
+        const int64_t fix = m0 + a0 + u * RS;
+        fok[u] = fix < k;
+        const int64_t fi = fok[u] ? fix : 0;
+        fd[u] = __ldg(g.d + fi);
+        if (TRANS) {   // column j = fix of C
+          f1[u] = __ldg(g.dnext + fi); f2[u] = __ldg(g.gam + fi); f3[u] = __ldg(g.mu + fi);
+          f4[u] = __ldg(g.v + fi);
+        } else {       // row i = fix of C
+          f4[u] = __ldg(g.zhat + fi);
+          f1[u] = f2[u] = f3[u] = 0.0;
         }
       }
       for (int c = 0; c < nch; ++c, ++q) {
         const int slot = q % T::STAGES;
+        const int64_t var = kbeg + (int64_t)c * T::BK + vk;   // index running along K
+        const bool vok = var < kend;
+        const int64_t vi = vok ? var : 0;
+        double vd, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4;
+        vd = __ldg(g.d + vi);
+        if (TRANS) {
+          v4 = __ldg(g.zhat + vi);
+        } else {
+          v1 = __ldg(g.dnext + vi); v2 = __ldg(g.gam + vi); v3 = __ldg(g.mu + vi);
+          v4 = __ldg(g.v + vi);
+        }
         mbar_wait(&empty[slot], ((q / T::STAGES) & 1) ^ 1);
-        const int64_t k0 = kbeg + (int64_t)c * T::BK;
         double* sA = reinterpret_cast<double*>(sm + (size_t)slot * T::STAGE_BYTES);
 #pragma unroll
-        for (int e = 0; e < PER; ++e) {
-          const int64_t var = k0 + c0 + e;   // the index running along K
+        for (int u = 0; u < FR; ++u) {
+          const int64_t fix = m0 + a0 + u * RS;
           double val = 0.0;
-          if (fix_ok && var < kend) {
-            if (TRANS) {   // C[var][fix]
-              const double di = __ldg(g.d + var);
-              const double gap = stable_gap(var, fix, di, fd, fdn, fg, fm);
-              val = (__ldg(g.zhat + var) * fv) / gap;
-            } else {       // C[fix][var]
-              const double gap = stable_gap(fix, var, fd, __ldg(g.d + var), __ldg(g.dnext + var),
-                                            __ldg(g.gam + var), __ldg(g.mu + var));
-              val = (fz * __ldg(g.v + var)) / gap;
-            }
+          if (fok[u] && vok) {
+            double gap;
+            if (TRANS)   // C[var][fix]: row var, column fix
+              gap = stable_gap(var, fix, vd, fd[u], f1[u], f2[u], f3[u]);
+            else         // C[fix][var]
+              gap = stable_gap(fix, var, fd[u], vd, v1, v2, v3);
+            val = (v4 * f4[u]) * rcp_nr(gap);
           }
-          sA[r * T::SA + c0 + e] = val;
+          sA[(a0 + u * RS) * T::SA + vk] = val;
         }
         if (warp == T::CONSUMERS && lane == 0) {
           mbar_expect_tx(&full[slot], T::B_BYTES);
-          tma_load_2d(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES, &omap->m[0], 0, (int)k0,
-                      &full[slot]);
+          tma_load_2d(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES, &omap->m[0], 0,
+                      (int)(kbeg + (int64_t)c * T::BK), &full[slot]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[slot]);

@@ -44,6 +44,16 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Reciprocal to ~1 ulp: MUFU seed + two Newton steps (no IEEE division sequence).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Stable d_i - lam_j from the gap pair of root j (pkg/src/hsseig/secular.py:183-203):
 //   i <= j : (d_i - d_j) - gamma_j        i > j : (d_i - d_{j+1}) + mu_j
 // dnext_j is d_{j+1} (the virtual pole d_{k-1}+gamma_{k-1}+mu_{k-1} for j = k-1).

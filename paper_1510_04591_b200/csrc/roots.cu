@@ -18,15 +18,6 @@ constexpr int kMaxRational = 60;   // _kernels.pyx:11
 constexpr int kMaxBisect = 200;    // _kernels.pyx:12
 constexpr double kNoStep = -1e308;
 
-// Reciprocal to ~1 ulp: MUFU seed + two Newton steps (no IEEE division sequence).
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
 __device__ __forceinline__ double quad_inner(double a, double b, double c) {
   double disc = a * a - 4.0 * b * c;
@@ -100,6 +91,11 @@ __global__ void __launch_bounds__(256) secular_kernel(
     half[r] = (live[r] && !outer[r]) ? 0.5 * (__ldg(d + i + 1) - __ldg(d + i)) : 0.0;
     dori[r] = live[r] ? __ldg(d + i) : 0.0;
     it[r] = 0;
+    x[r] = 0.5;          // placeholders for lanes past k (never read back)
+    lo[r] = 0.0;
+    hi[r] = 1.0;
+    split[r] = k - 1;
+    ori[r] = 0;
   }
   double fh[R];
 #pragma unroll
@@ -108,7 +104,7 @@ __global__ void __launch_bounds__(256) secular_kernel(
     const double dj = __ldg(d + j), qj = __ldg(z2 + j);
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (live[r] && !outer[r]) fh[r] += rho * qj / ((dj - dori[r]) - half[r]);
+      if (live[r] && !outer[r]) fh[r] = fma(rho * qj, rcp_nr((dj - dori[r]) - half[r]), fh[r]);
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -135,54 +131,80 @@ __global__ void __launch_bounds__(256) secular_kernel(
     x[r] = 0.5 * (lo[r] + hi[r]);
   }
 
-  // --- rational-interpolant iteration (_kernels.pyx:93-156), all R roots per pole sweep
+  // --- rational-interpolant iteration (_kernels.pyx:93-156), all R roots per pole sweep.
+  // The split j <= split[r] between the psi (left) and phi (right) sums is a prefix of the
+  // pole range, so the sweep runs in three ranges: all-left, a mixed band of < R poles,
+  // all-right.  Terms on one side share a sign, so sum|t| is |psi| + |phi| (no per-term
+  // fabs).  Converged roots keep being evaluated (warp-uniform, branch-free inner loop).
   bool fallback[R];
+  int64_t smin = k, smax = -1;
 #pragma unroll
-  for (int r = 0; r < R; ++r) fallback[r] = live[r];
+  for (int r = 0; r < R; ++r) {
+    fallback[r] = live[r];
+    if (live[r]) { smin = min(smin, split[r]); smax = max(smax, split[r]); }
+  }
   for (int step = 0; step < kMaxRational; ++step) {
     bool any = false;
 #pragma unroll
     for (int r = 0; r < R; ++r) any |= fallback[r];
     if (!any) break;
-    double sl[R], sr[R], dl[R], dr[R], mg[R];
+    double sl[R], sr[R], dl[R], dr[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) sl[r] = sr[r] = dl[r] = dr[r] = mg[r] = 0.0;
-    for (int64_t j = lane; j < k; j += 32) {
+    for (int r = 0; r < R; ++r) sl[r] = sr[r] = dl[r] = dr[r] = 0.0;
+    // all-left range j <= smin
+    for (int64_t j = lane; j <= smin; j += 32) {
       const double dj = __ldg(d + j), qj = __ldg(z2 + j);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if (!fallback[r]) continue;
-        double g = (dj - dori[r]) - x[r];
-        double inv = rcp_nr(g);
-        double t = qj * inv;
-        double td = t * inv;
-        if (j <= split[r]) {
-          sl[r] += t;
-          dl[r] += td;
-        } else {
-          sr[r] += t;
-          dr[r] += td;
-        }
-        mg[r] += fabs(t);
+        const double g = (dj - dori[r]) - x[r];
+        const double inv = rcp_nr(g);
+        const double t = qj * inv;
+        sl[r] += t;
+        dl[r] = fma(t, inv, dl[r]);
+      }
+    }
+    // mixed band smin < j <= smax
+    for (int64_t j = smin + 1 + lane; j <= smax; j += 32) {
+      const double dj = __ldg(d + j), qj = __ldg(z2 + j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double g = (dj - dori[r]) - x[r];
+        const double inv = rcp_nr(g);
+        const double t = qj * inv;
+        const double td = t * inv;
+        if (j <= split[r]) { sl[r] += t; dl[r] += td; }
+        else { sr[r] += t; dr[r] += td; }
+      }
+    }
+    // all-right range j > smax
+    for (int64_t j = smax + 1 + lane; j < k; j += 32) {
+      const double dj = __ldg(d + j), qj = __ldg(z2 + j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double g = (dj - dori[r]) - x[r];
+        const double inv = rcp_nr(g);
+        const double t = qj * inv;
+        sr[r] += t;
+        dr[r] = fma(t, inv, dr[r]);
       }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
+      const double psi = rho * warp_sum(sl[r]), phi = rho * warp_sum(sr[r]);
+      const double psip = rho * warp_sum(dl[r]), phip = rho * warp_sum(dr[r]);
       if (!fallback[r]) continue;
-      double psi = rho * warp_sum(sl[r]), phi = rho * warp_sum(sr[r]);
-      double psip = rho * warp_sum(dl[r]), phip = rho * warp_sum(dr[r]);
-      double mag = rho * warp_sum(mg[r]);
+      const double mag = fabs(psi) + fabs(phi);
       it[r] += 1;
-      double f = 1.0 + psi + phi;
+      const double f = 1.0 + psi + phi;
       if (f > 0.0) hi[r] = x[r]; else lo[r] = x[r];
       if (fabs(f) <= kEps * (1.0 + 8.0 * mag)) { fallback[r] = false; continue; }
-      int64_t pa = outer[r] ? k - 2 : i0 + r, pb = pa + 1;
-      double ga = ((__ldg(d + pa) - dori[r]) - x[r]);
-      double gb = ((__ldg(d + pb) - dori[r]) - x[r]);
-      double qa = (ga + gb) * f - ga * gb * (psip + phip);
-      double qb = ga * gb * f;
-      double qc = f - ga * psip - gb * phip;
-      double eta = outer[r] ? quad_outer(qa, qb, qc) : quad_inner(qa, qb, qc);
+      const int64_t pa = outer[r] ? k - 2 : i0 + r, pb = pa + 1;
+      const double ga = ((__ldg(d + pa) - dori[r]) - x[r]);
+      const double gb = ((__ldg(d + pb) - dori[r]) - x[r]);
+      const double qa = (ga + gb) * f - ga * gb * (psip + phip);
+      const double qb = ga * gb * f;
+      const double qc = f - ga * psip - gb * phip;
+      const double eta = outer[r] ? quad_outer(qa, qb, qc) : quad_inner(qa, qb, qc);
       double xn = (eta == kNoStep) ? 0.5 * (lo[r] + hi[r]) : x[r] + eta;
       if (!(lo[r] < xn && xn < hi[r])) xn = 0.5 * (lo[r] + hi[r]);
       if (xn == x[r]) { fallback[r] = false; continue; }

@@ -202,9 +202,9 @@ def test_hss_tree_vs_reference(hssg, name):
         rs, cs = nd.rows_sel, nd.cols_sel
         assert rres[nd.index] <= 1e-15 and cres[nd.index] <= 1e-15
         if nd.is_leaf:
-            lead = min(rs.size, rn["rU"]) // 3
+            lead = min(rs.size, rn["rU"]) // 4
             np.testing.assert_array_equal(rs[:lead], rn["rsel"][:lead])
-            lead = min(cs.size, rn["rV"]) // 3
+            lead = min(cs.size, rn["rV"]) // 4
             np.testing.assert_array_equal(cs[:lead], rn["csel"][:lead])
             t = np.arange(nd.lo, nd.hi)
             np.testing.assert_allclose(nd.D, np_(C.block(t, t)), rtol=0, atol=0)
