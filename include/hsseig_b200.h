@@ -189,12 +189,16 @@ int hsseig_dense_update(const double *Qb, int64_t ldq, int64_t P, const hsseig_g
  * work: hsseig_normals_work_bytes(n) bytes.
  * *fail_dev (int32, device) is set non-zero if the rejection chain could not be
  * resolved; the caller then draws on the host instead.
+ * tails (device int64, 1 + 3*tail_cap; may be NULL): tails[0] = count, then per normal
+ * taken from the ziggurat tail (about 1 in 4000) its output offset, the raw 64-bit draw
+ * fed to log1p and the sign bit.  NumPy evaluates those with the C library's log1p; the
+ * host re-evaluates them (value = +-(r - log1p(-u) / r)) so the block is bit-identical.
  */
 int hsseig_set_normal_tables(const uint64_t *ki, const double *wi, const double *fi);
 int64_t hsseig_normals_work_bytes(int64_t n);
 int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                          int64_t n, int64_t w, int64_t ldo, double *out, void *work,
-                         int32_t *fail_dev, void *stream);
+                         int32_t *fail_dev, int64_t *tails, int64_t tail_cap, void *stream);
 
 /* Plain batched helper used by tests/bench: out = A @ B (P x K)(K x N), FP64 DMMA. */
 int hsseig_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,

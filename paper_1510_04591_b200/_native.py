@@ -74,7 +74,7 @@ _SIGS = {
     "hsseig_normals_work_bytes": (c_i64, [c_i64]),
     "hsseig_pcg64_normals": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp,
-                                            c_vp]),
+                                            c_vp, c_i64, c_vp]),
     "hsseig_gemm": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64,
                                    c_vp]),
 }

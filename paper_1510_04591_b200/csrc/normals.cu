@@ -75,8 +75,12 @@ __device__ __forceinline__ double unit(uint64_t r) { return (double)(r >> 11) * 
 
 // Parse one normal starting at draw p; returns the next start, writes the value.
 // Draws beyond L count as failure (returns L).
+// *tail_u receives the raw draw behind the tail-branch log1p (0 otherwise): NumPy evaluates
+// that value with the C library's log1p, whose last bit the device log1p does not always
+// reproduce, so the host re-evaluates those few values (about 1 in 4000 normals).
 __device__ __forceinline__ int64_t one_normal(const uint64_t* __restrict__ U, int64_t p, int64_t L,
-                                              double* val) {
+                                              double* val, uint64_t* tail_u = nullptr,
+                                              int* tail_sign = nullptr) {
   for (;;) {
     if (p >= L) return L;
     uint64_t r = U[p];
@@ -96,6 +100,10 @@ __device__ __forceinline__ int64_t one_normal(const uint64_t* __restrict__ U, in
         q += 2;
         if (yy + yy > xx * xx) {
           *val = ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
+          if (tail_u) {
+            *tail_u = U[q - 2];
+            *tail_sign = (int)((rabs >> 8) & 1);
+          }
           return q;
         }
       }
@@ -217,15 +225,35 @@ __global__ void resolve_kernel(const int64_t* __restrict__ exitpos, const int32_
 
 __global__ void emit_kernel(const uint64_t* __restrict__ U, int64_t L, int nseg,
                             const int32_t* __restrict__ entry, const int64_t* __restrict__ base,
-                            int64_t n, int64_t w, int64_t ldo, double* __restrict__ out) {
+                            int64_t n, int64_t w, int64_t ldo, double* __restrict__ out,
+                            int64_t* __restrict__ tails, int64_t tail_cap,
+                            int32_t* __restrict__ fail) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nseg) return;
   const int64_t a = (int64_t)t * kSeg, b = a + kSeg;
   int64_t p = a + entry[t], i = base[t];
   while (p < b && i < n) {
     double v;
-    p = one_normal(U, p, L, &v);
-    out[(i / w) * ldo + (i % w)] = v;   // row-major (n / w) x w block with leading dimension ldo
+    uint64_t tu = 0;
+    int tsg = 0;
+    bool tail = false;
+    {
+      uint64_t tmp = ~0ull;
+      p = one_normal(U, p, L, &v, &tmp, &tsg);
+      if (tmp != ~0ull) { tail = true; tu = tmp; }
+    }
+    const int64_t o = (i / w) * ldo + (i % w);   // row-major (n / w) x w, leading dimension ldo
+    out[o] = v;
+    if (tail && tails) {
+      const unsigned long long slot = atomicAdd(reinterpret_cast<unsigned long long*>(tails), 1ull);
+      if ((int64_t)slot < tail_cap) {
+        tails[1 + 3 * slot] = o;
+        tails[2 + 3 * slot] = (int64_t)tu;
+        tails[3 + 3 * slot] = tsg;
+      } else {
+        *fail = 3;
+      }
+    }
     ++i;
   }
 }
@@ -254,7 +282,8 @@ extern "C" int64_t hsseig_normals_work_bytes(int64_t n) {
 
 extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
                                     uint64_t inc_lo, int64_t n, int64_t w, int64_t ldo, double* out,
-                                    void* work, int32_t* fail_dev, void* stream) {
+                                    void* work, int32_t* fail_dev, int64_t* tails,
+                                    int64_t tail_cap, void* stream) {
   if (!g_tables_loaded) return HSSEIG_ERR_ARG;
   if (n < 0 || w < 1 || ldo < w || !out || !work || !fail_dev) return HSSEIG_ERR_ARG;
   if (n == 0) return HSSEIG_OK;
@@ -274,7 +303,9 @@ extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64
   HSS_CHECK_LAUNCH();
   resolve_kernel<<<1, 1024, 0, s>>>(exitpos, count, nseg, n, entry, base, fail_dev);
   HSS_CHECK_LAUNCH();
-  emit_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(U, L, nseg, entry, base, n, w, ldo, out);
+  if (tails && cudaMemsetAsync(tails, 0, sizeof(int64_t), s) != cudaSuccess) return HSSEIG_ERR_CUDA;
+  emit_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(U, L, nseg, entry, base, n, w, ldo, out, tails,
+                                                 tail_cap, fail_dev);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }

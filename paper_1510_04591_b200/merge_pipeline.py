@@ -95,6 +95,7 @@ class MergePipeline:
         self.Y = torch.empty(k * wmax, **f64)
         self.Z = torch.empty(k * wmax, **f64)
         self.om = torch.empty(k * wmax, **f64)
+        self.om_flat = torch.empty(k * MAX_W, **f64)
         self.sample_work = torch.empty(int(self.lib.hsseig_sample_work_doubles(k, MAX_W)), **f64)
         self.device_rng = bool(device_rng) and sample_rng.available()
         if self.device_rng:
@@ -112,11 +113,13 @@ class MergePipeline:
         lib, k, cfg = self.lib, self.k, self.cfg
         s = nat.stream_ptr()
         ev = self._events(7)
+        ev[0].record()
         if self.device_rng:
-            pcg = sample_rng.pcg_state(seed)
+            # the whole k x MAX_W prefix of the sample stream (the (k, w) block is its first
+            # k*w values for every w), drawn before w is known; tail records read back later
+            self.normals.draw(seed, k * MAX_W, self.om_flat)
         else:
             self.host_omega.start(seed)
-        ev[0].record()
         self.status.zero_()
         self.status[1:4] = k
         nat.check(lib.hsseig_secular(nat.ptr(d), nat.ptr(z), k, float(rho), nat.ptr(self.lam),
@@ -167,7 +170,12 @@ class MergePipeline:
                     ws = _ceil16(w)
                     om = self.om[:k * ws].view(k, ws)
                     if self.device_rng:
-                        self.normals.draw(seed, k * w, om, w=w, ld=ws, state=pcg)
+                        try:
+                            self.normals.fixup()
+                            om[:, :w].copy_(self.om_flat[:k * w].view(k, w))
+                        except RuntimeError:   # unresolved rejection chain: the host draw
+                            hv = np.random.default_rng(seed).standard_normal((k, w))
+                            om[:, :w].copy_(torch.as_tensor(hv, device="cuda"))
                     else:
                         hv = self.host_omega.finish(k * w)
                         om[:, :w].copy_(hv.view(k, w), non_blocking=True)
@@ -186,8 +194,6 @@ class MergePipeline:
                                                         s), "hss_build_rand")
                     ev[5].record()
                     finish_construct(tree)   # synchronises: flags, ranks, r_used
-                    if self.device_rng and self.normals.failed():
-                        raise RuntimeError("device sample draw could not resolve its rejection chain")
                     fl_con = _construct_flops(tree, k, w)
         if not self.device_rng:
             self.host_omega.finish(0)

@@ -9,6 +9,7 @@ callers draw on the host with NumPy (the reference's own call).
 """
 import ctypes
 import glob
+import math
 import os
 
 import numpy as np
@@ -17,6 +18,9 @@ import torch
 from . import _native as nat
 
 _STATE = {"ok": None}
+ZIG_R = 3.6541528853610088        # NumPy ziggurat_nor_r
+ZIG_INV_R = 0.27366123732975828    # NumPy ziggurat_nor_inv_r
+TAIL_CAP = 1 << 16
 _KI0 = 0x000EF33D8025EF6A     # first entry of NumPy's ki_double table (ziggurat, 256 layers)
 
 
@@ -78,6 +82,10 @@ class NormalStream:
         self.work = torch.empty(int(self.lib.hsseig_normals_work_bytes(self.nmax)),
                                 dtype=torch.uint8, device="cuda")
         self.fail = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.tails = torch.zeros(1 + 3 * TAIL_CAP, dtype=torch.int64, device="cuda")
+        self.h_tails = torch.empty(1 + 3 * TAIL_CAP, dtype=torch.int64, pin_memory=True)
+        self.h_fail = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        self._ev = None
 
     def draw(self, seed, n, out, w=None, ld=None, state=None):
         """Enqueue the first n normals of default_rng(seed) into out (device float64).
@@ -93,11 +101,39 @@ class NormalStream:
         self.fail.zero_()
         nat.check(self.lib.hsseig_pcg64_normals(sh, sl, ih, il, int(n), w, ld, nat.ptr(out),
                                                 nat.ptr(self.work), nat.ptr(self.fail),
-                                                nat.stream_ptr()), "pcg64_normals")
+                                                nat.ptr(self.tails), TAIL_CAP, nat.stream_ptr()),
+                  "pcg64_normals")
+        # the tail records and the failure flag come back asynchronously; fixup() applies them
+        self.h_tails.copy_(self.tails, non_blocking=True)
+        self.h_fail.copy_(self.fail, non_blocking=True)
+        self._ev = torch.cuda.Event()
+        self._ev.record()
+        self._out = out
         return out
 
+    def fixup(self):
+        """Re-evaluate the ziggurat-tail values with the C library's log1p (as NumPy does).
+
+        Waits for the draw's record read-back (not for the whole stream)."""
+        self._ev.synchronize()
+        if int(self.h_fail[0]):
+            raise RuntimeError("device normal stream could not resolve the rejection chain")
+        cnt = int(self.h_tails[0])
+        if cnt == 0:
+            return 0
+        rec = self.h_tails[1:1 + 3 * cnt].numpy().reshape(cnt, 3)
+        vals = np.empty(cnt)
+        for t in range(cnt):
+            u = (int(rec[t, 1]) & 0xFFFFFFFFFFFFFFFF) >> 11
+            xx = -ZIG_INV_R * math.log1p(-(u * (1.0 / 9007199254740992.0)))
+            vals[t] = -(ZIG_R + xx) if rec[t, 2] else ZIG_R + xx
+        idx = torch.as_tensor(rec[:, 0].copy()).to("cuda", non_blocking=False)
+        self._out.view(-1)[idx] = torch.as_tensor(vals).to("cuda")
+        return cnt
+
     def failed(self):
-        return bool(self.fail.item())
+        self._ev.synchronize()
+        return bool(int(self.h_fail[0]))
 
 
 def normals(seed, n):
@@ -105,6 +141,5 @@ def normals(seed, n):
     out = torch.empty(int(n), dtype=torch.float64, device="cuda")
     ns = NormalStream(n)
     ns.draw(seed, n, out)
-    if ns.failed():
-        raise RuntimeError("device normal stream could not resolve the rejection chain")
+    ns.fixup()
     return out
