@@ -134,6 +134,12 @@ def finish_secular(sol, k, flops=None):
     return sol
 
 
+def finish_secular_status_only(sol):
+    """Iteration total without the bracket check (the raw kernel contract of secular_all)."""
+    sol.iterations = int(sol._status.read()[0])
+    return sol
+
+
 def stable_gap(i, j, d, gamma, mu):
     """d[i] - lam[j] without cancellation (secular.py:183-192)."""
     if i <= j:

@@ -296,3 +296,14 @@ def test_device_sample_draw_is_numpy_bit_exact(seed, k, w):
     got = sample_rng.normals(seed, k * w).cpu().numpy()
     ref = np.random.default_rng(seed).standard_normal((k, w)).ravel()
     np.testing.assert_array_equal(got, ref)
+
+
+def test_plugin_secular_all_contract(sec):
+    # the reference's kernel seam: NumPy in / NumPy out (pkg/src/hsseig/_kernels.pyx:178-234)
+    from paper_1510_04591_b200 import plugin
+    name = "rand600"
+    d, z, rho = sec[f"{name}_d"], sec[f"{name}_z"], float(sec[f"{name}_rho"])
+    lam, gam, mu, it = plugin.secular_all(d, z, rho)
+    assert isinstance(lam, np.ndarray) and lam.dtype == np.float64 and isinstance(it, int)
+    scale = np.abs(sec[f"{name}_lam"]).max()
+    assert np.abs(lam - sec[f"{name}_lam"]).max() <= 64 * EPS * scale
