@@ -58,6 +58,10 @@ int hsseig_status_init(hsseig_status *status_dev, int64_t k, void *stream);
 int hsseig_secular(const double *d, const double *z, int64_t k, double rho, double *lam,
                    double *gamma, double *mu, int32_t *iters, double *work,
                    hsseig_status *status, void *stream);
+/* Roots [ibeg, iend) only (multi-GPU index shard); outputs hold iend - ibeg entries. */
+int hsseig_secular_part(const double *d, const double *z, int64_t k, double rho, int64_t ibeg,
+                        int64_t iend, double *lam, double *gamma, double *mu, int32_t *iters,
+                        double *work, hsseig_status *status, void *stream);
 
 /*
  * (a3) Virtual-pole extension dnext[j] = d[j+1], dnext[k-1] = d[k-1]+gamma+mu
@@ -74,6 +78,10 @@ int hsseig_dnext(const double *d, const double *gamma, const double *mu, int64_t
 int hsseig_loewner(const double *d, const double *dnext, const double *gamma,
                    const double *mu, const double *z, int64_t k, double rho, double *zhat,
                    hsseig_status *status, void *stream);
+/* Weights [ibeg, iend) only; zhat holds iend - ibeg entries. */
+int hsseig_loewner_part(const double *d, const double *dnext, const double *gamma,
+                        const double *mu, const double *z, int64_t k, double rho, int64_t ibeg,
+                        int64_t iend, double *zhat, hsseig_status *status, void *stream);
 
 /*
  * (a5) Column normalizers v_j = 1/||zhat ./ (d - lam_j)||.
@@ -82,6 +90,10 @@ int hsseig_loewner(const double *d, const double *dnext, const double *gamma,
 int hsseig_normalizers(const double *d, const double *dnext, const double *gamma,
                        const double *mu, const double *zhat, int64_t k, double *v,
                        void *stream);
+/* Normalizers of columns [jbeg, jend) only; v holds jend - jbeg entries. */
+int hsseig_normalizers_part(const double *d, const double *dnext, const double *gamma,
+                            const double *mu, const double *zhat, int64_t k, int64_t jbeg,
+                            int64_t jend, double *v, void *stream);
 
 /* Generators of the Cauchy-like matrix (pkg/src/hsseig/cauchy.py:15-38); device pointers. */
 typedef struct hsseig_gen {
@@ -108,6 +120,10 @@ int hsseig_cauchy_block(const hsseig_gen *gen, const int64_t *rows, int64_t nr,
 int64_t hsseig_sample_work_doubles(int64_t k, int64_t w);
 int hsseig_cauchy_sample(const hsseig_gen *gen, const double *omega, int64_t ldom, int64_t w,
                          double *Y, double *Z, int64_t ldy, double *work, void *stream);
+/* Rows [row0, row1) of Y and of Z (multi-GPU shard); Y, Z hold row1 - row0 rows. */
+int hsseig_cauchy_sample_part(const hsseig_gen *gen, const double *omega, int64_t ldom, int64_t w,
+                              int64_t row0, int64_t row1, double *Y, double *Z, int64_t ldy,
+                              double *work, void *stream);
 
 /*
  * HSS tree (pkg/src/hsseig/hss.py:151-214): nodes in the reference's postorder

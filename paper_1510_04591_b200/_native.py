@@ -51,6 +51,14 @@ _SIGS = {
     "hsseig_status_init": (ctypes.c_int, [c_vp, c_i64, c_vp]),
     "hsseig_secular": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
                                       c_vp, c_vp]),
+    "hsseig_secular_part": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_i64, c_i64, c_vp, c_vp,
+                                           c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "hsseig_loewner_part": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_i64,
+                                           c_i64, c_vp, c_vp, c_vp]),
+    "hsseig_normalizers_part": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64,
+                                               c_vp, c_vp]),
+    "hsseig_cauchy_sample_part": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_i64, c_i64,
+                                                 c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "hsseig_dnext": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "hsseig_loewner": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp,
                                       c_vp]),

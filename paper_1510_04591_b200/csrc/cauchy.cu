@@ -35,7 +35,8 @@ constexpr int kGenWarps = 8;
 template <class T, bool TRANS>
 __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
     sample_ws_kernel(CauchyGen g, const MapSet* __restrict__ omap, int w, double* __restrict__ part,
-                     int64_t ldp, int kchunk, int nsplit, int tiles) {
+                     int64_t ldp, int kchunk, int nsplit, int tiles, int64_t row0, int64_t row1) {
+  // output rows [row0, row1) of Y (or Z); part rows are indexed from row0
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smraw) + 127) & ~(uintptr_t)127);
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
     uint32_t q = 0;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
       const int tile = it % tiles, split = it / tiles;
-      const int64_t m0 = (int64_t)tile * T::BM;
+      const int64_t m0 = row0 + (int64_t)tile * T::BM;
       const int64_t kbeg = (int64_t)split * kchunk;
       const int64_t kend = imin64(k, kbeg + kchunk);
       const int nch = (int)((kend - kbeg + T::BK - 1) / T::BK);
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
 #pragma unroll
       for (int u = 0; u < FR; ++u) {
         const int64_t fix = m0 + a0 + u * RS;
-        fok[u] = fix < k;
+        fok[u] = fix < row1;
         const int64_t fi = fok[u] ? fix : 0;
         fd[u] = __ldg(g.d + fi);
         if (TRANS) {   // column j = fix of C
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
   double acc[T::MF][T::NF][2];
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
     const int tile = it % tiles, split = it / tiles;
-    const int64_t m0 = (int64_t)tile * T::BM;
+    const int64_t m0 = (int64_t)tile * T::BM;   // relative to row0
     const int64_t kbeg = (int64_t)split * kchunk;
     const int64_t kend = imin64(k, kbeg + kchunk);
     const int nch = (int)((kend - kbeg + T::BK - 1) / T::BK);
@@ -152,11 +153,12 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
-    double* P = part + (int64_t)split * k * ldp;
+    const int64_t nrows = row1 - row0;
+    double* P = part + (int64_t)split * nrows * ldp;
 #pragma unroll
     for (int i = 0; i < T::MF; ++i) {
       const int64_t row = m0 + wm * T::MF * 8 + i * 8 + gr;
-      if (row >= k) continue;
+      if (row >= nrows) continue;
 #pragma unroll
       for (int j = 0; j < T::NF; ++j) {
         const int col = wn * T::NF * 8 + j * 8 + 2 * gc;
@@ -224,8 +226,8 @@ __global__ void __launch_bounds__(T::THREADS) dense_update_kernel(const double* 
   store_acc<T>(acc, out + n0, ldo, P, m0, (int)imin64(T::BN, k - n0), 0, wm, wn, lane);
 }
 
-static void sample_split(int64_t k, int64_t bm, int64_t* nsplit, int64_t* kchunk) {
-  const int64_t tiles = (k + bm - 1) / bm;
+static void sample_split(int64_t k, int64_t nrows, int64_t bm, int64_t* nsplit, int64_t* kchunk) {
+  const int64_t tiles = (nrows + bm - 1) / bm;
   int64_t ns = (148 * 6 + tiles - 1) / tiles;     // enough items to keep every SM busy
   ns = imax64(1, imin64(ns, (k + 511) / 512));
   int64_t kc = (k + ns - 1) / ns;
@@ -235,13 +237,15 @@ static void sample_split(int64_t k, int64_t bm, int64_t* nsplit, int64_t* kchunk
 }
 
 template <class T>
-static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int w, double* Y,
-                         double* Z, int64_t ldy, double* work, cudaStream_t s) {
+static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int w, int64_t row0,
+                         int64_t row1, double* Y, double* Z, int64_t ldy, double* work,
+                         cudaStream_t s) {
   const int64_t k = g.k;
-  const int64_t tiles = (k + T::BM - 1) / T::BM;
+  const int64_t nrows = row1 - row0;
+  const int64_t tiles = (nrows + T::BM - 1) / T::BM;
   const int64_t ldp = ((w + 1) / 2) * 2;
   int64_t nsplit, kchunk;
-  sample_split(k, T::BM, &nsplit, &kchunk);
+  sample_split(k, nrows, T::BM, &nsplit, &kchunk);
   constexpr int threads = (T::CONSUMERS + kGenWarps) * 32;
   static int per_sm = 0, sms = 0;
   if (!per_sm) {
@@ -254,9 +258,9 @@ static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   double* pY = work;
-  double* pZ = work + nsplit * k * ldp;
+  double* pZ = work + nsplit * nrows * ldp;
   MapSet* dmap = reinterpret_cast<MapSet*>(
-      (reinterpret_cast<uintptr_t>(work + 2 * nsplit * k * ldp) + 255) & ~(uintptr_t)255);
+      (reinterpret_cast<uintptr_t>(work + 2 * nsplit * nrows * ldp) + 255) & ~(uintptr_t)255);
   MapSet maps;
   for (int r = 1; r < kMaps; ++r) make_map(&maps.m[r], nullptr, 0, 0, 0, 0, 0);
   if (!make_map(&maps.m[0], om, (uint64_t)k, (uint64_t)w, (uint64_t)ldom, T::SB, T::BK))
@@ -266,15 +270,15 @@ static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int
   const int64_t items = tiles * nsplit;
   const int grid = (int)imin64(items, (int64_t)sms * per_sm);
   sample_ws_kernel<T, false><<<grid, threads, T::SMEM_BYTES, s>>>(g, dmap, w, pY, ldp, (int)kchunk,
-                                                                (int)nsplit, (int)tiles);
+                                                                (int)nsplit, (int)tiles, row0, row1);
   HSS_CHECK_LAUNCH();
   sample_ws_kernel<T, true><<<grid, threads, T::SMEM_BYTES, s>>>(g, dmap, w, pZ, ldp, (int)kchunk,
-                                                               (int)nsplit, (int)tiles);
+                                                               (int)nsplit, (int)tiles, row0, row1);
   HSS_CHECK_LAUNCH();
-  unsigned rb = (unsigned)((k * w + 255) / 256);
-  splitk_reduce_kernel<<<rb, 256, 0, s>>>(pY, (int)nsplit, k, w, ldp, Y, ldy);
+  unsigned rb = (unsigned)((nrows * w + 255) / 256);
+  splitk_reduce_kernel<<<rb, 256, 0, s>>>(pY, (int)nsplit, nrows, w, ldp, Y, ldy);
   HSS_CHECK_LAUNCH();
-  splitk_reduce_kernel<<<rb, 256, 0, s>>>(pZ, (int)nsplit, k, w, ldp, Z, ldy);
+  splitk_reduce_kernel<<<rb, 256, 0, s>>>(pZ, (int)nsplit, nrows, w, ldp, Z, ldy);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
@@ -308,25 +312,40 @@ extern "C" int hsseig_cauchy_block(const hsseig_gen* gen, const int64_t* rows, i
 }
 
 extern "C" int64_t hsseig_sample_work_doubles(int64_t k, int64_t w) {
-  int64_t nsplit, kchunk;
-  sample_split(k, 64, &nsplit, &kchunk);
+  // covers every row range: nsplit * nrows is maximal for the full range
+  int64_t worst = 0;
+  for (int64_t nrows = k; nrows >= 1; nrows = nrows / 2) {
+    int64_t nsplit, kchunk;
+    sample_split(k, nrows, 64, &nsplit, &kchunk);
+    worst = imax64(worst, nsplit * nrows);
+    if (nrows == 1) break;
+  }
   const int64_t ldp = ((w + 1) / 2) * 2;
-  return 2 * nsplit * k * ldp + (int64_t)(sizeof(MapSet) + 512) / 8;
+  return 2 * (worst + 64) * ldp + (int64_t)(sizeof(MapSet) + 512) / 8;
+}
+
+extern "C" int hsseig_cauchy_sample_part(const hsseig_gen* gen, const double* omega, int64_t ldom,
+                                         int64_t w, int64_t row0, int64_t row1, double* Y, double* Z,
+                                         int64_t ldy, double* work, void* stream) {
+  if (!gen || w < 1 || w > 128 || ldom < w || ldy < w || row0 < 0 || row1 > gen->k || row0 > row1)
+    return HSSEIG_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(omega) & 15) || (ldom & 1)) return HSSEIG_ERR_ARG;  // TMA rows
+  if (row0 == row1) return HSSEIG_OK;
+  CauchyGen g = to_gen(gen);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch ((w + 31) / 32) {   // BM 64: 8 DMMA warps of 32 x 8NF + 8 generator warps
+    case 1: return launch_sample<TTile<4, 1, 2, 4, 8>>(g, omega, ldom, (int)w, row0, row1, Y, Z, ldy, work, s);
+    case 2: return launch_sample<TTile<4, 2, 2, 4, 8>>(g, omega, ldom, (int)w, row0, row1, Y, Z, ldy, work, s);
+    case 3: return launch_sample<TTile<4, 3, 2, 4, 8>>(g, omega, ldom, (int)w, row0, row1, Y, Z, ldy, work, s);
+    default: return launch_sample<TTile<4, 4, 2, 4, 6>>(g, omega, ldom, (int)w, row0, row1, Y, Z, ldy, work, s);
+  }
 }
 
 extern "C" int hsseig_cauchy_sample(const hsseig_gen* gen, const double* omega, int64_t ldom,
                                     int64_t w, double* Y, double* Z, int64_t ldy, double* work,
                                     void* stream) {
-  if (!gen || w < 1 || w > 128 || ldom < w || ldy < w) return HSSEIG_ERR_ARG;
-  if ((reinterpret_cast<uintptr_t>(omega) & 15) || (ldom & 1)) return HSSEIG_ERR_ARG;  // TMA rows
-  CauchyGen g = to_gen(gen);
-  cudaStream_t s = (cudaStream_t)stream;
-  switch ((w + 31) / 32) {   // BM 64: 8 DMMA warps of 32 x 8NF + 4 generator warps
-    case 1: return launch_sample<TTile<4, 1, 2, 4, 8>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-    case 2: return launch_sample<TTile<4, 2, 2, 4, 8>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-    case 3: return launch_sample<TTile<4, 3, 2, 4, 8>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-    default: return launch_sample<TTile<4, 4, 2, 4, 6>>(g, omega, ldom, (int)w, Y, Z, ldy, work, s);
-  }
+  if (!gen) return HSSEIG_ERR_ARG;
+  return hsseig_cauchy_sample_part(gen, omega, ldom, w, 0, gen->k, Y, Z, ldy, work, stream);
 }
 
 extern "C" int hsseig_dense_update(const double* Qb, int64_t ldq, int64_t P, const hsseig_gen* gen,

@@ -57,11 +57,13 @@ __global__ void square_sum_kernel(const double* __restrict__ z, int64_t k, doubl
 template <int R>
 __global__ void __launch_bounds__(256) secular_kernel(
     const double* __restrict__ d, const double* __restrict__ z2, const double* __restrict__ sumz2p,
-    int64_t k, double rho, double* __restrict__ lam, double* __restrict__ gam,
-    double* __restrict__ mu, int32_t* __restrict__ iters, hsseig_status* __restrict__ st) {
+    int64_t k, double rho, int64_t ibeg, int64_t iend, double* __restrict__ lam,
+    double* __restrict__ gam, double* __restrict__ mu, int32_t* __restrict__ iters,
+    hsseig_status* __restrict__ st) {
+  // roots [ibeg, iend) of the k; outputs are written at index i - ibeg
   const int lane = threadIdx.x & 31;
-  const int64_t i0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
-  if (i0 >= k) return;
+  const int64_t i0 = ibeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (i0 >= iend) return;
   const double sumz2 = *sumz2p;
 
   if (k == 1) {  // _kernels.pyx:204-209
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(256) secular_kernel(
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     int64_t i = i0 + r;
-    live[r] = i < k;
+    live[r] = i < iend;
     outer[r] = (i == k - 1);
     half[r] = (live[r] && !outer[r]) ? 0.5 * (__ldg(d + i + 1) - __ldg(d + i)) : 0.0;
     dori[r] = live[r] ? __ldg(d + i) : 0.0;
@@ -236,20 +238,21 @@ __global__ void __launch_bounds__(256) secular_kernel(
     for (int r = 0; r < R; ++r) {
       if (!live[r]) continue;
       int64_t i = i0 + r;
+      const int64_t o = i - ibeg;
       double g, m;
       if (outer[r]) {
         g = x[r];
         m = rho * sumz2 - x[r];
-        lam[i] = d[i] + x[r];
+        lam[o] = d[i] + x[r];
       } else {
         double width = d[i + 1] - d[i];
         if (ori[r] == i) { g = x[r]; m = width - x[r]; }
         else { g = width + x[r]; m = -x[r]; }
-        lam[i] = dori[r] + x[r];
+        lam[o] = dori[r] + x[r];
       }
-      gam[i] = g;
-      mu[i] = m;
-      iters[i] = it[r];
+      gam[o] = g;
+      mu[o] = m;
+      iters[o] = it[r];
       tot += (unsigned long long)it[r];
       if (!(g > 0.0)) atomicMin(reinterpret_cast<long long*>(&st->v[1]), (long long)i);
       if (!(m > 0.0)) atomicMin(reinterpret_cast<long long*>(&st->v[2]), (long long)i);
@@ -271,14 +274,14 @@ template <int R>
 __global__ void __launch_bounds__(256) loewner_kernel(
     const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
     const double* __restrict__ mu, const double* __restrict__ z, int64_t k, double rho,
-    double* __restrict__ zhat, hsseig_status* __restrict__ st) {
+    int64_t ibeg, int64_t iend, double* __restrict__ zhat, hsseig_status* __restrict__ st) {
   const int lane = threadIdx.x & 31;
-  const int64_t i0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
-  if (i0 >= k) return;
+  const int64_t i0 = ibeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (i0 >= iend) return;
   double di[R], pr[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    di[r] = (i0 + r < k) ? __ldg(d + i0 + r) : 0.0;
+    di[r] = (i0 + r < iend) ? __ldg(d + i0 + r) : 0.0;
     pr[r] = 1.0;
   }
   for (int64_t j = lane; j < k; j += 32) {
@@ -296,13 +299,13 @@ __global__ void __launch_bounds__(256) loewner_kernel(
   for (int r = 0; r < R; ++r) {
     double p = warp_prod(pr[r]);
     int64_t i = i0 + r;
-    if (lane == 0 && i < k) {
+    if (lane == 0 && i < iend) {
       double rad = (p * gam[i]) / rho;
       if (!(rad > 0.0) || !isfinite(rad)) {
         atomicMin(reinterpret_cast<long long*>(&st->v[3]), (long long)i);
-        zhat[i] = 0.0;
+        zhat[i - ibeg] = 0.0;
       } else {
-        zhat[i] = copysign(sqrt(rad), z[i]);
+        zhat[i - ibeg] = copysign(sqrt(rad), z[i]);
       }
     }
   }
@@ -312,15 +315,15 @@ __global__ void __launch_bounds__(256) loewner_kernel(
 template <int R>
 __global__ void __launch_bounds__(256) normalizer_kernel(
     const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
-    const double* __restrict__ mu, const double* __restrict__ zh, int64_t k,
-    double* __restrict__ v) {
+    const double* __restrict__ mu, const double* __restrict__ zh, int64_t k, int64_t jbeg,
+    int64_t jend, double* __restrict__ v) {
   const int lane = threadIdx.x & 31;
-  const int64_t j0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
-  if (j0 >= k) return;
+  const int64_t j0 = jbeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (j0 >= jend) return;
   double dj[R], dnj[R], gj[R], mj[R], s[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    int64_t j = j0 + r < k ? j0 + r : k - 1;
+    int64_t j = j0 + r < jend ? j0 + r : jend - 1;
     dj[r] = __ldg(d + j);
     dnj[r] = __ldg(dn + j);
     gj[r] = __ldg(gam + j);
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(256) normalizer_kernel(
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     double t = warp_sum(s[r]);
-    if (lane == 0 && j0 + r < k) v[j0 + r] = 1.0 / sqrt(t);
+    if (lane == 0 && j0 + r < jend) v[j0 + r - jbeg] = 1.0 / sqrt(t);
   }
 }
 
@@ -358,22 +361,31 @@ extern "C" int hsseig_status_init(hsseig_status* st, int64_t k, void* stream) {
   return HSSEIG_OK;
 }
 
-extern "C" int hsseig_secular(const double* d, const double* z, int64_t k, double rho,
-                              double* lam, double* gamma, double* mu, int32_t* iters, double* work,
-                              hsseig_status* st, void* stream) {
-  if (k < 1 || !(rho > 0.0) || !d || !z || !lam || !gamma || !mu || !iters || !work || !st)
+extern "C" int hsseig_secular_part(const double* d, const double* z, int64_t k, double rho,
+                                   int64_t ibeg, int64_t iend, double* lam, double* gamma,
+                                   double* mu, int32_t* iters, double* work, hsseig_status* st,
+                                   void* stream) {
+  if (k < 1 || !(rho > 0.0) || !d || !z || !lam || !gamma || !mu || !iters || !work || !st ||
+      ibeg < 0 || iend > k || ibeg > iend)
     return HSSEIG_ERR_ARG;
+  if (ibeg == iend) return HSSEIG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   double* z2 = work;
   double* sum = work + k;
   square_sum_kernel<<<1, 1024, 0, s>>>(z, k, z2, sum);
   HSS_CHECK_LAUNCH();
   constexpr int R = 4;
-  int64_t warps = (k + R - 1) / R;
-  int blocks = (int)((warps + 7) / 8);
-  secular_kernel<R><<<blocks, 256, 0, s>>>(d, z2, sum, k, rho, lam, gamma, mu, iters, st);
+  const int64_t warps = (iend - ibeg + R - 1) / R;
+  const int blocks = (int)((warps + 7) / 8);
+  secular_kernel<R><<<blocks, 256, 0, s>>>(d, z2, sum, k, rho, ibeg, iend, lam, gamma, mu, iters, st);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
+}
+
+extern "C" int hsseig_secular(const double* d, const double* z, int64_t k, double rho,
+                              double* lam, double* gamma, double* mu, int32_t* iters, double* work,
+                              hsseig_status* st, void* stream) {
+  return hsseig_secular_part(d, z, k, rho, 0, k, lam, gamma, mu, iters, work, st, stream);
 }
 
 extern "C" int hsseig_dnext(const double* d, const double* gamma, const double* mu, int64_t k,
@@ -384,14 +396,35 @@ extern "C" int hsseig_dnext(const double* d, const double* gamma, const double* 
   return HSSEIG_OK;
 }
 
+extern "C" int hsseig_loewner_part(const double* d, const double* dnext, const double* gamma,
+                                   const double* mu, const double* z, int64_t k, double rho,
+                                   int64_t ibeg, int64_t iend, double* zhat, hsseig_status* st,
+                                   void* stream) {
+  if (k < 1 || !(rho > 0.0) || ibeg < 0 || iend > k || ibeg > iend) return HSSEIG_ERR_ARG;
+  if (ibeg == iend) return HSSEIG_OK;
+  constexpr int R = 4;
+  const int64_t warps = (iend - ibeg + R - 1) / R;
+  loewner_kernel<R><<<(unsigned)((warps + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
+      d, dnext, gamma, mu, z, k, rho, ibeg, iend, zhat, st);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
 extern "C" int hsseig_loewner(const double* d, const double* dnext, const double* gamma,
                               const double* mu, const double* z, int64_t k, double rho,
                               double* zhat, hsseig_status* st, void* stream) {
-  if (k < 1 || !(rho > 0.0)) return HSSEIG_ERR_ARG;
+  return hsseig_loewner_part(d, dnext, gamma, mu, z, k, rho, 0, k, zhat, st, stream);
+}
+
+extern "C" int hsseig_normalizers_part(const double* d, const double* dnext, const double* gamma,
+                                       const double* mu, const double* zhat, int64_t k,
+                                       int64_t jbeg, int64_t jend, double* v, void* stream) {
+  if (k < 1 || jbeg < 0 || jend > k || jbeg > jend) return HSSEIG_ERR_ARG;
+  if (jbeg == jend) return HSSEIG_OK;
   constexpr int R = 4;
-  int64_t warps = (k + R - 1) / R;
-  loewner_kernel<R><<<(unsigned)((warps + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
-      d, dnext, gamma, mu, z, k, rho, zhat, st);
+  const int64_t warps = (jend - jbeg + R - 1) / R;
+  normalizer_kernel<R><<<(unsigned)((warps + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
+      d, dnext, gamma, mu, zhat, k, jbeg, jend, v);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
@@ -399,11 +432,5 @@ extern "C" int hsseig_loewner(const double* d, const double* dnext, const double
 extern "C" int hsseig_normalizers(const double* d, const double* dnext, const double* gamma,
                                   const double* mu, const double* zhat, int64_t k, double* v,
                                   void* stream) {
-  if (k < 1) return HSSEIG_ERR_ARG;
-  constexpr int R = 4;
-  int64_t warps = (k + R - 1) / R;
-  normalizer_kernel<R><<<(unsigned)((warps + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
-      d, dnext, gamma, mu, zhat, k, v);
-  HSS_CHECK_LAUNCH();
-  return HSSEIG_OK;
+  return hsseig_normalizers_part(d, dnext, gamma, mu, zhat, k, 0, k, v, stream);
 }
