@@ -1,0 +1,243 @@
+"""Multi-GPU merge: row-block sharding of Q_old with index-sharded roots.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  For one merge:
+
+* roots, Loewner weights and column normalizers are sharded by index
+  (rank r owns [r*c, (r+1)*c), c = ceil(k / world)); lam/gamma/mu, zhat and v are
+  all-gathered (3k + 2k doubles);
+* the sample products are sharded by rows: rank r computes rows of Y = C Omega and of
+  Z = C^T Omega in its index range; Y and Z are all-gathered (2 k ws doubles);
+* partition, rank estimate, the sample draw and the HSS construction are replicated
+  (every rank holds the whole tree: D and B are regenerated from the generators,
+  never sent);
+* the multiply Q_new = Q_old H is row-local: Q_old never moves.
+
+The driver is written against a small ``ops`` interface so the same sharding /
+gathering logic runs on the GPU (``GpuOps``: libhsseig_b200.so through the C ABI) and,
+in the CPU test-suite, with gloo and a NumPy stand-in.
+"""
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .flops import secular_flops
+from .hss import build_partition, rank_bound
+from .secular import SecularConvergenceError, WeightRecomputationError
+
+
+def shard_range(k, rank, world):
+    """Index shard [lo, hi) of rank in a padded even split (chunk = ceil(k / world))."""
+    c = -(-k // world)
+    lo = min(k, rank * c)
+    return lo, min(k, lo + c), c
+
+
+def gather_rows(local, chunk, k, group=None):
+    """All-gather equal-size row chunks (padded to `chunk` rows) and trim to k rows."""
+    world = dist.get_world_size(group)
+    if local.shape[0] < chunk:
+        pad = torch.zeros((chunk - local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
+                          device=local.device)
+        local = torch.cat([local, pad])
+    parts = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(parts, local.contiguous(), group=group)
+    return torch.cat(parts)[:k]
+
+
+def rank_from(part, span, mu_h, eps, cap):
+    """estimate_rank (hss.py:87-103) from host copies of the boundary gaps."""
+    if part.n_leaves < 2:
+        return 0
+    r = 0
+    for lo, _ in part.ranges[1:]:
+        r = max(r, rank_bound(max(span / mu_h[lo - 1], 1.0), eps))
+    return min(max(r, 1), cap)
+
+
+class ShardedMerge:
+    """One merge over the ranks of `group`; each rank holds rows of Q_old."""
+
+    def __init__(self, k, cfg, ops, group=None):
+        self.k, self.cfg, self.ops, self.group = int(k), cfg, ops, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def run(self, d, z, rho, X, seed):
+        k, cfg, ops = self.k, self.cfg, self.ops
+        lo, hi, c = shard_range(k, self.rank, self.world)
+        info = {"used_hss": False, "fell_back": False, "r_used": 0}
+        # roots of this rank's index shard, then the full arrays on every rank
+        lam_l, gam_l, mu_l, st_l = ops.secular_part(d, z, rho, lo, hi)
+        full = gather_rows(torch.stack([lam_l, gam_l, mu_l], 1), c, k, self.group)
+        lam, gam, mu = full[:, 0].contiguous(), full[:, 1].contiguous(), full[:, 2].contiguous()
+        st = gather_rows(st_l.view(1, -1), 1, self.world, self.group)   # world x 3
+        iters = int(st[:, 0].sum())
+        bad_g = int(st[:, 1].min())
+        bad_m = int(st[:, 2].min())
+        bad = bad_g if bad_g < k else (bad_m if (k >= 2 and bad_m < k) else -1)
+        if bad >= 0:
+            raise SecularConvergenceError(f"root {bad} lost its bracket")
+        dn = ops.dnext(d, gam, mu)
+        zh_l, rad_l = ops.loewner_part(d, dn, gam, mu, z, rho, lo, hi)
+        zh = gather_rows(zh_l, c, k, self.group).contiguous()
+        rad = gather_rows(rad_l.view(1, -1), 1, self.world, self.group)
+        if int(rad.min()) < k:
+            raise WeightRecomputationError(f"non-positive radicand at index {int(rad.min())}")
+        v_l = ops.normalizers_part(d, dn, gam, mu, zh, lo, hi)
+        v = gather_rows(v_l, c, k, self.group).contiguous()
+        info["iterations"] = iters
+        info["flops_secular"] = secular_flops(k, iters) + 14 * k * k
+        gen = ops.generators(d, dn, gam, mu, zh, v)
+        tree = None
+        if cfg.method == "adc-rand" and k > cfg.hss_threshold:
+            mu_h = mu.cpu().numpy()
+            try:
+                part = build_partition(k, cfg.leaf_size, None, None, mu_h)
+            except ValueError:
+                part = None
+            if part is not None:
+                span = float((d[-1] + gam[-1]) - d[0])
+                r = min(rank_from(part, span, mu_h, cfg.rank_eps, cfg.rank_cap),
+                        part.min_leaf - cfg.oversample)
+                w = r + cfg.oversample
+                if r >= 1 and w <= ops.max_width:
+                    om = ops.omega(seed, k, w)
+                    Y_l, Z_l = ops.sample_part(gen, om, w, lo, hi)
+                    Y = gather_rows(Y_l, c, k, self.group)
+                    Z = gather_rows(Z_l, c, k, self.group)
+                    tree = ops.build(gen, part, w, om, Y, Z)
+        if tree is not None and not ops.flagged(tree):
+            info["used_hss"] = True
+            info["r_used"] = ops.r_used(tree)
+            out = ops.multiply(X, tree)
+        else:
+            info["fell_back"] = tree is not None
+            out = ops.dense(X, gen)
+        info["tree"] = tree
+        return lam, out, info
+
+
+class GpuOps:
+    """Device implementation of the ShardedMerge ops through libhsseig_b200.so."""
+
+    def __init__(self, k):
+        from . import _native as nat
+        from . import sample_rng
+        from .hss import MAX_WIDTH
+        self.nat, self.lib, self.k = nat, nat.load(), int(k)
+        self.max_width = MAX_WIDTH
+        f64 = dict(dtype=torch.float64, device="cuda")
+        self.swork = torch.empty(2 * self.k + 64, **f64)
+        self.status = torch.zeros(8, dtype=torch.int64, device="cuda")
+        self.sample_work = torch.empty(int(self.lib.hsseig_sample_work_doubles(self.k, MAX_WIDTH)), **f64)
+        self.rng = sample_rng.NormalStream(self.k * MAX_WIDTH) if sample_rng.available() else None
+        self._trees = {}
+        self._mwork = None
+
+    def _s(self):
+        return self.nat.stream_ptr()
+
+    def secular_part(self, d, z, rho, lo, hi):
+        nat, n = self.nat, hi - lo
+        lam = torch.empty(n, dtype=torch.float64, device="cuda")
+        gam, mu = torch.empty_like(lam), torch.empty_like(lam)
+        its = torch.empty(n, dtype=torch.int32, device="cuda")
+        self.status.zero_()
+        self.status[1:4] = self.k
+        nat.check(self.lib.hsseig_secular_part(nat.ptr(d), nat.ptr(z), self.k, float(rho), lo, hi,
+                                               nat.ptr(lam), nat.ptr(gam), nat.ptr(mu), nat.ptr(its),
+                                               nat.ptr(self.swork), nat.ptr(self.status), self._s()),
+                  "secular_part")
+        return lam, gam, mu, self.status[:3].clone()
+
+    def dnext(self, d, gam, mu):
+        nat = self.nat
+        dn = torch.empty_like(d)
+        nat.check(self.lib.hsseig_dnext(nat.ptr(d), nat.ptr(gam), nat.ptr(mu), self.k, nat.ptr(dn),
+                                        self._s()), "dnext")
+        return dn
+
+    def loewner_part(self, d, dn, gam, mu, z, rho, lo, hi):
+        nat = self.nat
+        zh = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+        self.status[3] = self.k
+        nat.check(self.lib.hsseig_loewner_part(nat.ptr(d), nat.ptr(dn), nat.ptr(gam), nat.ptr(mu),
+                                               nat.ptr(z), self.k, float(rho), lo, hi, nat.ptr(zh),
+                                               nat.ptr(self.status), self._s()), "loewner_part")
+        return zh, self.status[3:4].clone()
+
+    def normalizers_part(self, d, dn, gam, mu, zh, lo, hi):
+        nat = self.nat
+        v = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+        nat.check(self.lib.hsseig_normalizers_part(nat.ptr(d), nat.ptr(dn), nat.ptr(gam), nat.ptr(mu),
+                                                   nat.ptr(zh), self.k, lo, hi, nat.ptr(v),
+                                                   self._s()), "normalizers_part")
+        return v
+
+    def generators(self, d, dn, gam, mu, zh, v):
+        from .cauchy import CauchyEvecMatrix
+        return CauchyEvecMatrix(d, gam, mu, zh, v, dnext=dn)
+
+    def omega(self, seed, k, w):
+        ws = (w + 15) // 16 * 16
+        om = torch.zeros(k, ws, dtype=torch.float64, device="cuda")
+        if self.rng is not None:
+            flat = torch.empty(k * w, dtype=torch.float64, device="cuda")
+            self.rng.draw(seed, k * w, flat)
+            self.rng.fixup()
+            om[:, :w] = flat.view(k, w)
+        else:
+            om[:, :w] = torch.as_tensor(np.random.default_rng(seed).standard_normal((k, w)),
+                                        device="cuda")
+        return om
+
+    def sample_part(self, gen, om, w, lo, hi):
+        nat = self.nat
+        ws = om.shape[1]
+        Y = torch.empty(hi - lo, ws, dtype=torch.float64, device="cuda")
+        Z = torch.empty_like(Y)
+        nat.check(self.lib.hsseig_cauchy_sample_part(gen.gen, nat.ptr(om), ws, w, lo, hi, nat.ptr(Y),
+                                                     nat.ptr(Z), ws, nat.ptr(self.sample_work),
+                                                     self._s()), "cauchy_sample_part")
+        return Y, Z
+
+    def build(self, gen, part, w, om, Y, Z):
+        from .hss import HssTree, finish_construct
+        from .secular import Status
+        nat = self.nat
+        key = (part.ranges, w)
+        if key not in self._trees:
+            self._trees = {key: HssTree(part, w)}
+        tree = self._trees[key]
+        tree._ranks = None
+        st = Status(self.k)
+        nat.check(self.lib.hsseig_hss_build_rand(gen.gen, nat.ptr(om), om.shape[1], nat.ptr(Y),
+                                                 nat.ptr(Z), Y.shape[1], 1e-15, ctypes.byref(tree.ct),
+                                                 nat.ptr(st.t), self._s()), "hss_build_rand")
+        tree._status = st
+        finish_construct(tree)
+        return tree
+
+    def flagged(self, tree):
+        return tree.flagged
+
+    def r_used(self, tree):
+        return tree.r_used
+
+    def multiply(self, X, tree):
+        nat = self.nat
+        out = torch.empty(X.shape[0], self.k, dtype=torch.float64, device="cuda")
+        need = int(self.lib.hsseig_matmul_work_doubles(X.shape[0], ctypes.byref(tree.ct)))
+        if self._mwork is None or self._mwork.numel() < need:
+            self._mwork = None
+            self._mwork = torch.empty(need, dtype=torch.float64, device="cuda")
+        nat.check(self.lib.hsseig_hss_matmul_right(nat.ptr(X), X.stride(0), X.shape[0],
+                                                   ctypes.byref(tree.ct), nat.ptr(out), out.stride(0),
+                                                   nat.ptr(self._mwork), self._s()), "hss_matmul_right")
+        return out
+
+    def dense(self, X, gen):
+        return gen.right_multiply_into(X)
+

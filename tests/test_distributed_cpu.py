@@ -1,0 +1,123 @@
+"""World-size-2 gloo test of the multi-GPU merge driver's host logic (sharding, padding,
+all-gathers, replicated construction, row-local multiply) with a NumPy stand-in for the
+device ops (the oracle).  The GPU path runs the same driver with GpuOps."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from helpers import config4_system
+from oracle import hss_oracle as orc
+
+
+class NumpyOps:
+    """Oracle-backed ops: each 'part' is the full oracle result sliced to the shard."""
+    max_width = 112
+
+    def __init__(self, k):
+        self.k = k
+
+    def secular_part(self, d, z, rho, lo, hi):
+        lam, gam, mu, _, per = orc.secular_all(d.numpy(), z.numpy(), rho, per_root=True)
+        sl = slice(lo, hi)
+        bad_g = lo + int(np.flatnonzero(gam[sl] <= 0)[0]) if np.any(gam[sl] <= 0) else self.k
+        bad_m = lo + int(np.flatnonzero(mu[sl] <= 0)[0]) if np.any(mu[sl] <= 0) else self.k
+        st = torch.tensor([int(per[sl].sum()), bad_g, bad_m], dtype=torch.int64)
+        return (torch.as_tensor(lam[sl]), torch.as_tensor(gam[sl]), torch.as_tensor(mu[sl]), st)
+
+    def dnext(self, d, gam, mu):
+        return torch.cat([d[1:], (d[-1:] + gam[-1:]) + mu[-1:]])
+
+    def loewner_part(self, d, dn, gam, mu, z, rho, lo, hi):
+        zh = orc.loewner(d.numpy(), gam.numpy(), mu.numpy(), z.numpy(), rho)
+        return torch.as_tensor(zh[lo:hi]), torch.tensor([self.k], dtype=torch.int64)
+
+    def normalizers_part(self, d, dn, gam, mu, zh, lo, hi):
+        v = orc.normalizers(d.numpy(), gam.numpy(), mu.numpy(), zh.numpy())
+        return torch.as_tensor(v[lo:hi])
+
+    def generators(self, d, dn, gam, mu, zh, v):
+        return orc.Generators(d.numpy(), gam.numpy(), mu.numpy(), zh.numpy(), v.numpy())
+
+    def omega(self, seed, k, w):
+        return torch.as_tensor(orc.sample_block(k, w, seed))
+
+    def sample_part(self, G, om, w, lo, hi):
+        return (torch.as_tensor(G.times(om.numpy())[lo:hi]),
+                torch.as_tensor(G.t_times(om.numpy())[lo:hi]))
+
+    def build(self, G, part, w, om, Y, Z):
+        # the gathered samples must be the full products
+        assert np.allclose(Y.numpy(), G.times(om.numpy()), rtol=0, atol=1e-13)
+        assert np.allclose(Z.numpy(), G.t_times(om.numpy()), rtol=0, atol=1e-13)
+        return orc.rand_construct(G, list(part.ranges), w - 10, 10, Omega=om.numpy())
+
+    def flagged(self, T):
+        return T.flagged
+
+    def r_used(self, T):
+        return T.r_used
+
+    def multiply(self, X, T):
+        return torch.as_tensor(orc.hss_apply_right(X.numpy(), T))
+
+    def dense(self, X, G):
+        return torch.as_tensor(orc.update_dense(X.numpy(), G))
+
+
+def _worker(rank, world, port, k, P, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1510_04591_b200 import SolverConfig
+    from paper_1510_04591_b200.distributed import ShardedMerge
+    d, u, rho = config4_system(k, 3)
+    X = np.random.default_rng(7).standard_normal((P, k))
+    r0, r1 = rank * P // world, (rank + 1) * P // world
+    cfg = SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13)
+    sm = ShardedMerge(k, cfg, NumpyOps(k))
+    lam, out, info = sm.run(torch.as_tensor(d), torch.as_tensor(u), rho, torch.as_tensor(X[r0:r1]),
+                            seed=[0, 0])
+    parts = [torch.empty(((r + 1) * P // world - r * P // world, k), dtype=torch.float64)
+             for r in range(world)]
+    if out.shape[0] < parts[rank].shape[0]:
+        raise AssertionError("bad local shape")
+    dist.all_gather(parts, out.contiguous()) if len({p.shape for p in parts}) == 1 else None
+    if rank == 0:
+        np.savez(out_path, lam=lam.numpy(), out=torch.cat(parts).numpy(),
+                 used=info["used_hss"], r=info["r_used"])
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("k,P", [(600, 40)])
+def test_sharded_merge_world2_matches_single_process(tmp_path, k, P):
+    out_path = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(2, _free_port(), k, P, out_path), nprocs=2, join=True)
+    res = np.load(out_path)
+    d, u, rho = config4_system(k, 3)
+    X = np.random.default_rng(7).standard_normal((P, k))
+    G, lam, _ = orc.generators_from_roots(d, u, rho)
+    ref = orc.update_hss(X, G, 64, 10, 1e-13, 100, [0, 0])
+    assert bool(res["used"])
+    np.testing.assert_array_equal(res["lam"], lam)
+    np.testing.assert_allclose(res["out"], ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+
+
+def test_shard_ranges_cover_exactly():
+    from paper_1510_04591_b200.distributed import shard_range
+    for k in (1, 7, 600, 32768):
+        for world in (1, 2, 3, 8):
+            got = [shard_range(k, r, world)[:2] for r in range(world)]
+            assert got[0][0] == 0 and got[-1][1] == k
+            assert all(a[1] == b[0] for a, b in zip(got, got[1:]))

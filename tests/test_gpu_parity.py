@@ -307,3 +307,32 @@ def test_plugin_secular_all_contract(sec):
     assert isinstance(lam, np.ndarray) and lam.dtype == np.float64 and isinstance(it, int)
     scale = np.abs(sec[f"{name}_lam"]).max()
     assert np.abs(lam - sec[f"{name}_lam"]).max() <= 64 * EPS * scale
+
+
+def test_sharded_merge_driver_single_rank_nccl():
+    # the multi-GPU driver (index-sharded roots/weights/samples, replicated tree,
+    # row-local multiply) on a one-rank NCCL group against the single-GPU pipeline
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1510_04591_b200.distributed import GpuOps, ShardedMerge
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n = 4096
+        d, u, rho = config4_system(n, 5)
+        X = torch.randn(300, n, dtype=torch.float64, device="cuda")
+        cfg = hb.SolverConfig(leaf_size=128, hss_threshold=512, rank_eps=1e-13)
+        sm = ShardedMerge(n, cfg, GpuOps(n))
+        dd, uu = torch.as_tensor(d, device="cuda"), torch.as_tensor(u, device="cuda")
+        lam, out, info = sm.run(dd, uu, rho, X, seed=[0, 0])
+        assert info["used_hss"]
+        lam2, ref, _ = hb.merge_update(d, u, rho, X, cfg, seed=[0, 0])
+        assert torch.equal(lam, lam2)
+        assert float((out - ref).abs().max()) <= 1e-14 * float(ref.abs().max())
+    finally:
+        dist.destroy_process_group()
