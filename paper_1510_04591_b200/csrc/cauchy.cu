@@ -86,19 +86,27 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
           f1[u] = f2[u] = f3[u] = 0.0;
         }
       }
+      // K-running generator data of the next chunk is loaded one chunk ahead
+      auto load_var = [&](int cc, double& od, double& o1, double& o2, double& o3, double& o4) {
+        const int64_t vv = kbeg + (int64_t)cc * T::BK + vk;
+        const int64_t vi = vv < kend ? vv : 0;
+        od = __ldg(g.d + vi);
+        if (TRANS) {
+          o4 = __ldg(g.zhat + vi);
+          o1 = o2 = o3 = 0.0;
+        } else {
+          o1 = __ldg(g.dnext + vi); o2 = __ldg(g.gam + vi); o3 = __ldg(g.mu + vi);
+          o4 = __ldg(g.v + vi);
+        }
+      };
+      double nd = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0, n4 = 0.0;
+      if (nch > 0) load_var(0, nd, n1, n2, n3, n4);
       for (int c = 0; c < nch; ++c, ++q) {
         const int slot = q % T::STAGES;
         const int64_t var = kbeg + (int64_t)c * T::BK + vk;   // index running along K
         const bool vok = var < kend;
-        const int64_t vi = vok ? var : 0;
-        double vd, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4;
-        vd = __ldg(g.d + vi);
-        if (TRANS) {
-          v4 = __ldg(g.zhat + vi);
-        } else {
-          v1 = __ldg(g.dnext + vi); v2 = __ldg(g.gam + vi); v3 = __ldg(g.mu + vi);
-          v4 = __ldg(g.v + vi);
-        }
+        const double vd = nd, v1 = n1, v2 = n2, v3 = n3, v4 = n4;
+        if (c + 1 < nch) load_var(c + 1, nd, n1, n2, n3, n4);
         mbar_wait(&empty[slot], ((q / T::STAGES) & 1) ^ 1);
         double* sA = reinterpret_cast<double*>(sm + (size_t)slot * T::STAGE_BYTES);
 #pragma unroll

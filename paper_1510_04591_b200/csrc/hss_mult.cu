@@ -41,7 +41,7 @@ struct TJob {
 };
 
 template <class T>
-__global__ void __launch_bounds__(T::THREADS, 1)
+__global__ void __launch_bounds__(T::THREADS, T::MINB)
     tma_gemm_kernel(const MapSet* __restrict__ maps, const TJob* __restrict__ jobs, int njobs,
                     int64_t M, int tiles_m) {
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -265,6 +265,14 @@ static int tile_choice(const char* var, int dflt) {
 static int launch_narrow(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJob* jobs, int njobs,
                          int64_t M, cudaStream_t s) {
   static const int variant = tile_choice("HSSEIG_TILE_NARROW", 1);
+  if (variant == 2) {   // BM 64, 4-stage ring: two CTAs per SM
+    switch ((n + 31) / 32) {
+      case 1: case 2: return launch_tma<TTile<4, 2, 2, 4, 4>>(ops, dm, jobs, njobs, M, s);
+      case 3: return launch_tma<TTile<4, 3, 2, 4, 4>>(ops, dm, jobs, njobs, M, s);
+      case 4: return launch_tma<TTile<4, 4, 2, 4, 3>>(ops, dm, jobs, njobs, M, s);
+      default: return HSSEIG_ERR_ARG;
+    }
+  }
   if (variant == 0) {   // BM 128: 8 consumer warps of 32 x 8NF, NF = ceil(n/16)
     switch ((n + 15) / 16) {
       case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
@@ -287,6 +295,15 @@ static int launch_narrow(int n, const Operand (&ops)[kMaps], MapSet* dm, const T
 static int launch_wide(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJob* jobs, int njobs,
                        int64_t M, cudaStream_t s) {
   static const int variant = tile_choice("HSSEIG_TILE_WIDE", 1);
+  if (variant == 2) {   // BM 64, short ring: two CTAs per SM
+    switch ((n + 31) / 32) {
+      case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 2, 4, 4>>(ops, dm, jobs, njobs, M, s);
+      case 5: return launch_tma<TTile<4, 5, 2, 4, 3>>(ops, dm, jobs, njobs, M, s);
+      case 6: return launch_tma<TTile<4, 6, 2, 4, 3>>(ops, dm, jobs, njobs, M, s);
+      case 7: return launch_tma<TTile<4, 7, 2, 4, 2>>(ops, dm, jobs, njobs, M, s);
+      default: return HSSEIG_ERR_ARG;
+    }
+  }
   if (variant == 0) {   // BM 64: 8 consumer warps of 16 x 8NF, NF = ceil(n/16)
     switch ((n + 15) / 16) {
       case 1: case 2: case 3: case 4: case 5: case 6:

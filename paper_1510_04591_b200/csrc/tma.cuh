@@ -28,6 +28,8 @@ struct TTile {
   static constexpr int B_BYTES = BK * SB * 8;
   static constexpr int STAGE_BYTES = ((A_BYTES + B_BYTES + 127) / 128) * 128;
   static constexpr size_t SMEM_BYTES = (size_t)STAGE_BYTES * STAGES + 2 * STAGES * 8 + 128;
+  // two CTAs per SM when the ring is small enough (more warps to hide DMMA latency)
+  static constexpr int MINB = SMEM_BYTES <= 112 * 1024 ? 2 : 1;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
