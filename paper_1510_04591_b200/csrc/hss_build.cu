@@ -174,7 +174,7 @@ __device__ __forceinline__ double lapy2(double x, double y) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double tol,
                                                  const double* __restrict__ om, int64_t ldom,
-                                                 hsseig_status* st) {
+                                                 hsseig_status* st, int fused_form) {
   extern __shared__ __align__(16) double sm[];
   const int j = blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5, nthr = blockDim.x;
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
     int a = T.left[node], b = T.right[node];
     p = side == 0 ? T.rU[a] + T.rU[b] : T.rV[a] + T.rV[b];
   }
-  const double* Mg = T.M + (size_t)(2 * j + side) * T.pmax * ws;
+  double* Mg = T.M + (size_t)(2 * j + side) * T.pmax * ws;
   double* sA = sm;                              // p x SW
   double* vn1 = sA + (size_t)T.pmax * SW;       // p
   double* vn2 = vn1 + T.pmax;                   // p
@@ -197,9 +197,57 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
   __shared__ double s_tau, s_nf, s_resid;
   __shared__ int s_r, s_sat;
 
-  for (int e = tid; e < p * w; e += nthr) {
-    int row = e / w, c = e % w;
-    sA[row * SW + c] = Mg[(size_t)row * ws + c];
+  if (fused_form && !leaf) {
+    // inner level formation (hss.py:272-277) straight into shared memory:
+    //   Phi   = [ psel_a - B_a ycomp_b ; psel_b - B_b ycomp_a ]
+    //   Theta = [ tsel_a - B_b^T zcomp_b ; tsel_b - B_a^T zcomp_a ]
+    // the sibling compression is staged in smem; M also goes to global for the
+    // selected-row output below
+    double* sC = reinterpret_cast<double*>(piv + T.pmax + 2);
+    sC = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sC) + 15) & ~(uintptr_t)15);
+    const int a = T.left[node], b = T.right[node];
+    const int na = side == 0 ? T.rU[a] : T.rV[a];
+    for (int half = 0; half < 2; ++half) {
+      const int me = half == 0 ? a : b, sib = half == 0 ? b : a;
+      const int nrow = half == 0 ? na : p - na, off = half == 0 ? 0 : na;
+      const int nk = side == 0 ? T.rV[sib] : T.rU[sib];
+      const double* comp = (side == 0 ? T.ycomp : T.zcomp) + slot_ww(T, sib);
+      const double* sel = (side == 0 ? T.psel : T.tsel) + slot_ww(T, me);
+      const double* Bb = T.B + slot_ww(T, side == 0 ? me : sib);
+      __syncthreads();
+      for (int e = tid; e < nk * w; e += nthr) {
+        const int t = e / w, c = e % w;
+        sC[e] = comp[(size_t)t * ws + c];
+      }
+      __syncthreads();
+      for (int e = tid; e < nrow * w; e += nthr) {
+        const int row = e / w, c = e % w;
+        double s0 = 0.0, s1 = 0.0;
+        int t = 0;
+        if (side == 0) {
+          const double* br = Bb + (size_t)row * ws;
+          for (; t + 1 < nk; t += 2) {
+            s0 = fma(__ldg(br + t), sC[t * w + c], s0);
+            s1 = fma(__ldg(br + t + 1), sC[(t + 1) * w + c], s1);
+          }
+          if (t < nk) s0 = fma(__ldg(br + t), sC[t * w + c], s0);
+        } else {
+          for (; t + 1 < nk; t += 2) {
+            s0 = fma(__ldg(Bb + (size_t)t * ws + row), sC[t * w + c], s0);
+            s1 = fma(__ldg(Bb + (size_t)(t + 1) * ws + row), sC[(t + 1) * w + c], s1);
+          }
+          if (t < nk) s0 = fma(__ldg(Bb + (size_t)t * ws + row), sC[t * w + c], s0);
+        }
+        const double val = sel[(size_t)row * ws + c] - (s0 + s1);
+        sA[(off + row) * SW + c] = val;
+        Mg[(size_t)(off + row) * ws + c] = val;
+      }
+    }
+  } else {
+    for (int e = tid; e < p * w; e += nthr) {
+      int row = e / w, c = e % w;
+      sA[row * SW + c] = Mg[(size_t)row * ws + c];
+    }
   }
   for (int e = tid; e < p; e += nthr) piv[e] = e;
   __syncthreads();
@@ -283,12 +331,18 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
       for (int c = i + 1 + tid; c < p; c += nthr) {
         double* a = sA + c * SW;
         if (tau != 0.0) {
-          double d0 = a[i], d1 = 0.0;
+          double d0 = a[i], d1 = 0.0, d2 = 0.0, d3 = 0.0;
           int t = i + 1;
-          for (; t + 1 < w; t += 2) { d0 = fma(v[t], a[t], d0); d1 = fma(v[t + 1], a[t + 1], d1); }
-          if (t < w) d0 = fma(v[t], a[t], d0);
-          const double f = tau * (d0 + d1);
+          for (; t + 3 < w; t += 4) {
+            d0 = fma(v[t], a[t], d0);
+            d1 = fma(v[t + 1], a[t + 1], d1);
+            d2 = fma(v[t + 2], a[t + 2], d2);
+            d3 = fma(v[t + 3], a[t + 3], d3);
+          }
+          for (; t < w; ++t) d0 = fma(v[t], a[t], d0);
+          const double f = tau * ((d0 + d1) + (d2 + d3));
           a[i] -= f;
+#pragma unroll 4
           for (t = i + 1; t < w; ++t) a[t] = fma(-f, v[t], a[t]);
         }
         const double n1 = vn1[c];
@@ -589,20 +643,27 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
   if (T.pmax > 4096) return HSSEIG_ERR_ARG;
   const size_t smem_id = sizeof(double) * ((size_t)T.pmax * (T.w | 1) + 2 * T.pmax + T.w + 1 + 32) +
                          sizeof(int) * T.pmax + 64;
+  // fused inner formation needs room for one sibling compression (w x w)
+  const size_t smem_fused = smem_id + sizeof(double) * ((size_t)T.w * T.w + 4);
+  const int fused = smem_fused <= 227 * 1024 ? 1 : 0;
   if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024) return HSSEIG_ERR_ARG;
   cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);
-  cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_id);
+  cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(fused ? smem_fused : smem_id));
   for (int lev = T.depth; lev >= 1; --lev) {
     dim3 grid(1u << lev, 2);
     if (lev == T.depth) {
       leaf_form_kernel<<<grid, 256, smem_leaf, s>>>(g, T, omega, ldom, Y, Z, ldy);
     } else {
       genB_kernel<<<grid, 256, 0, s>>>(g, T, lev);
-      HSS_CHECK_LAUNCH();
-      inner_form_kernel<<<grid, 256, 0, s>>>(T, lev);
+      if (!fused) {
+        HSS_CHECK_LAUNCH();
+        inner_form_kernel<<<grid, 256, 0, s>>>(T, lev);
+      }
     }
     HSS_CHECK_LAUNCH();
-    id_kernel<<<grid, 256, smem_id, s>>>(T, lev, id_tol, omega, ldom, st);
+    id_kernel<<<grid, 256, fused ? smem_fused : smem_id, s>>>(T, lev, id_tol, omega, ldom, st,
+                                                             lev == T.depth ? 0 : fused);
     HSS_CHECK_LAUNCH();
   }
   genB_kernel<<<dim3(1, 2), 256, 0, s>>>(g, T, 0);
