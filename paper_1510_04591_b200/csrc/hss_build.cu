@@ -11,6 +11,7 @@
 // One CTA per (node, side): side 0 compresses the block row (Phi -> U, rows_sel),
 // side 1 the block column (Theta -> V, cols_sel).  Every matrix an ID sees is at
 // most (2w) x w, so it lives in shared memory for the whole factorization.
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -645,7 +646,8 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
                          sizeof(int) * T.pmax + 64;
   // fused inner formation needs room for one sibling compression (w x w)
   const size_t smem_fused = smem_id + sizeof(double) * ((size_t)T.w * T.w + 4);
-  const int fused = smem_fused <= 227 * 1024 ? 1 : 0;
+  static const int fuse_pref = getenv("HSSEIG_FUSED_FORM") ? atoi(getenv("HSSEIG_FUSED_FORM")) : 1;
+  const int fused = (fuse_pref && smem_fused <= 227 * 1024) ? 1 : 0;
   if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024) return HSSEIG_ERR_ARG;
   cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);
   cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -662,8 +664,9 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
       }
     }
     HSS_CHECK_LAUNCH();
-    id_kernel<<<grid, 256, fused ? smem_fused : smem_id, s>>>(T, lev, id_tol, omega, ldom, st,
-                                                             lev == T.depth ? 0 : fused);
+    const int fuse_here = lev == T.depth ? 0 : fused;
+    id_kernel<<<grid, 256, fuse_here ? smem_fused : smem_id, s>>>(T, lev, id_tol, omega, ldom, st,
+                                                                 fuse_here);
     HSS_CHECK_LAUNCH();
   }
   genB_kernel<<<dim3(1, 2), 256, 0, s>>>(g, T, 0);
