@@ -125,32 +125,53 @@ __global__ void genB_kernel(CauchyGen g, TreeDev T, int level) {
 //   Theta = [ tsel_a - B_b^T zcomp_b ; tsel_b - B_a^T zcomp_a ]
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level) {
-  const int j = blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  // one CTA per (node, side, half): rows [off, off + nrow) of Phi (side 0) or Theta (side 1).
+  // B block and sibling compression are staged in shared memory; every thread carries 4
+  // independent output columns so the contraction is not latency bound.
+  extern __shared__ __align__(16) double fs[];
+  const int j = blockIdx.x, side = blockIdx.y, half = blockIdx.z, tid = threadIdx.x;
   const int node = T.lnodes[(1 << level) - 1 + j];
   const int a = T.left[node], b = T.right[node], w = T.w, ws = T.ws;
-  double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * ws;
+  const int me = half == 0 ? a : b, sib = half == 0 ? b : a;
   const int na = side == 0 ? T.rU[a] : T.rV[a];
-  const int nb = side == 0 ? T.rU[b] : T.rV[b];
-  for (int e = tid; e < (na + nb) * w; e += blockDim.x) {
-    int row = e / w, c = e % w;
-    bool top = row < na;
-    int rr = top ? row : row - na;
-    int me = top ? a : b, sib = top ? b : a;
-    double s = 0.0;
-    if (side == 0) {
-      // psel_me[rr] - B_me[rr, :] ycomp_sib
-      const double* Bm = T.B + slot_ww(T, me) + (size_t)rr * ws;
-      const double* yc = T.ycomp + slot_ww(T, sib);
-      int nk = T.rV[sib];
-      for (int t = 0; t < nk; ++t) s = fma(Bm[t], yc[(size_t)t * ws + c], s);
-      Mo[(size_t)row * ws + c] = T.psel[slot_ww(T, me) + (size_t)rr * ws + c] - s;
-    } else {
-      // tsel_me[rr] - B_sib[:, rr]^T zcomp_sib
-      const double* Bs = T.B + slot_ww(T, sib);
-      const double* zc = T.zcomp + slot_ww(T, sib);
-      int nk = T.rU[sib];
-      for (int t = 0; t < nk; ++t) s = fma(Bs[(size_t)t * ws + rr], zc[(size_t)t * ws + c], s);
-      Mo[(size_t)row * ws + c] = T.tsel[slot_ww(T, me) + (size_t)rr * ws + c] - s;
+  const int nrow = side == 0 ? T.rU[me] : T.rV[me];
+  const int off = half == 0 ? 0 : na;
+  const int nk = side == 0 ? T.rV[sib] : T.rU[sib];
+  double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * ws;
+  const double* comp = (side == 0 ? T.ycomp : T.zcomp) + slot_ww(T, sib);
+  const double* sel = (side == 0 ? T.psel : T.tsel) + slot_ww(T, me);
+  const double* Bb = T.B + slot_ww(T, side == 0 ? me : sib);
+  const int SK = nk | 1;                 // odd stride for the B tile rows
+  double* sBt = fs;                      // nrow x nk  (B_me, or B_sib^T)
+  double* sCm = fs + (size_t)w * SK;     // nk x w
+  for (int e = tid; e < nrow * nk; e += blockDim.x) {
+    const int r = e / nk, t = e % nk;
+    sBt[r * SK + t] = side == 0 ? Bb[(size_t)r * ws + t] : Bb[(size_t)t * ws + r];
+  }
+  for (int e = tid; e < nk * w; e += blockDim.x) {
+    const int t = e / w, c = e % w;
+    sCm[e] = comp[(size_t)t * ws + c];
+  }
+  __syncthreads();
+  const int cq = (w + 3) / 4;            // columns per quarter
+  for (int e = tid; e < nrow * cq; e += blockDim.x) {
+    const int r = e / cq, c0 = e % cq;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* br = sBt + r * SK;
+#pragma unroll 2
+    for (int t = 0; t < nk; ++t) {
+      const double bv = br[t];
+      const double* cr = sCm + t * w;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + q * cq;
+        if (c < w) acc[q] = fma(bv, cr[c], acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + q * cq;
+      if (c < w) Mo[(size_t)(off + r) * ws + c] = sel[(size_t)r * ws + c] - acc[q];
     }
   }
 }
@@ -646,7 +667,9 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
                          sizeof(int) * T.pmax + 64;
   // fused inner formation needs room for one sibling compression (w x w)
   const size_t smem_fused = smem_id + sizeof(double) * ((size_t)T.w * T.w + 4);
-  static const int fuse_pref = getenv("HSSEIG_FUSED_FORM") ? atoi(getenv("HSSEIG_FUSED_FORM")) : 1;
+  static const int fuse_pref = getenv("HSSEIG_FUSED_FORM") ? atoi(getenv("HSSEIG_FUSED_FORM")) : 0;
+  const size_t smem_form = sizeof(double) * ((size_t)T.w * ((T.w | 1) + T.w) + 8);
+  cudaFuncSetAttribute(inner_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_form);
   const int fused = (fuse_pref && smem_fused <= 227 * 1024) ? 1 : 0;
   if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024) return HSSEIG_ERR_ARG;
   cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);
@@ -660,7 +683,7 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
       genB_kernel<<<grid, 256, 0, s>>>(g, T, lev);
       if (!fused) {
         HSS_CHECK_LAUNCH();
-        inner_form_kernel<<<grid, 256, 0, s>>>(T, lev);
+        inner_form_kernel<<<dim3(1u << lev, 2, 2), 256, smem_form, s>>>(T, lev);
       }
     }
     HSS_CHECK_LAUNCH();
