@@ -504,16 +504,48 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
     Sb = (side == 0 ? T.zcomp : T.ycomp) + slot_ww(T, b);
     lds = ws;
   }
-  for (int t = warp; t < r; t += nwarps) {
-    for (int c = lane; c < w; c += 32) {
-      int q = piv[t];
-      double s = q < na ? Sa[(int64_t)q * lds + c] : Sb[(int64_t)(q - na) * lds + c];
-      for (int jj = r; jj < p; ++jj) {
-        q = piv[jj];
-        const double srow = q < na ? Sa[(int64_t)q * lds + c] : Sb[(int64_t)(q - na) * lds + c];
-        s = fma(sA[jj * SW + t], srow, s);
+  // warp -> groups of 4 output rows t, lane -> up to 4 columns c; each S row is loaded
+  // once per group and feeds 16 independent FMA chains
+  auto srow_ptr = [&](int q) -> const double* {
+    return q < na ? Sa + (int64_t)q * lds : Sb + (int64_t)(q - na) * lds;
+  };
+  for (int t0 = warp * 4; t0 < r; t0 += nwarps * 4) {
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u;
+      const double* sr = srow_ptr(t < r ? piv[t] : piv[0]);
+#pragma unroll
+      for (int cq = 0; cq < 4; ++cq) {
+        const int c = lane + 32 * cq;
+        acc[u][cq] = (t < r && c < w) ? sr[c] : 0.0;
       }
-      comp[(size_t)t * ws + c] = s;
+    }
+#pragma unroll 2
+    for (int jj = r; jj < p; ++jj) {
+      const double* sr = srow_ptr(piv[jj]);
+      double sv[4];
+#pragma unroll
+      for (int cq = 0; cq < 4; ++cq) {
+        const int c = lane + 32 * cq;
+        sv[cq] = c < w ? sr[c] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double coef = (t0 + u < r) ? sA[jj * SW + t0 + u] : 0.0;
+#pragma unroll
+        for (int cq = 0; cq < 4; ++cq) acc[u][cq] = fma(coef, sv[cq], acc[u][cq]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = t0 + u;
+      if (t >= r) continue;
+#pragma unroll
+      for (int cq = 0; cq < 4; ++cq) {
+        const int c = lane + 32 * cq;
+        if (c < w) comp[(size_t)t * ws + c] = acc[u][cq];
+      }
     }
   }
 }
