@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
     //   Theta = [ tsel_a - B_b^T zcomp_b ; tsel_b - B_a^T zcomp_a ]
     // the sibling compression is staged in smem; M also goes to global for the
     // selected-row output below
-    double* sC = reinterpret_cast<double*>(piv + T.pmax + 2);
+    double* sC = reinterpret_cast<double*>(piv + 2 * T.pmax + 2);
     sC = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sC) + 15) & ~(uintptr_t)15);
     const int a = T.left[node], b = T.right[node];
     const int na = side == 0 ? T.rU[a] : T.rV[a];
@@ -452,23 +452,26 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
   // row early when its A operand starts at an odd column).  V^T: candidate q at column q,
   // except that an inner node's right-child candidates start at an even column (TMA box
   // starts must be 16-byte aligned).
+  // The slots were zeroed by hsseig_hss_build_rand; only the data region is written.
   int na_v = p;
   if (!leaf) na_v = side == 0 ? T.rU[T.left[node]] : T.rV[T.left[node]];
   const int rshift = (!leaf && (na_v & 1)) ? 1 : 0;
-  for (int e = tid; e < (T.pmax - 1) * ws; e += nthr) {
-    const int jj = e / ws, t = e % ws;  // jj = position in pivoted order
-    double val = 0.0;
-    if (jj < p && t < r) val = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * SW + t];
-    const int q = jj < p ? piv[jj] : jj;   // candidate row
+  int* ipiv = piv + T.pmax;            // candidate -> pivoted position
+  for (int e = tid; e < p; e += nthr) ipiv[piv[e]] = e;
+  __syncthreads();
+  for (int e = tid; e < p * r; e += nthr) {   // X[q][t], t fastest (coalesced rows)
+    const int q = e / r, t = e % r;
+    const int jj = ipiv[q];
+    const double val = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * SW + t];
     X[(size_t)(q + 1) * ws + t] = val;
-    if (side == 1) {
-      const int col = q < na_v ? q : q + rshift;
-      if (col < T.pmax) Xt[(size_t)t * T.pmax + col] = val;
-    }
   }
-  for (int t = tid; t < ws; t += nthr) {
-    X[t] = 0.0;
-    if (side == 1 && rshift) Xt[(size_t)t * T.pmax + na_v] = 0.0;
+  if (side == 1) {
+    for (int e = tid; e < r * p; e += nthr) {   // X^T[t][col(q)], q fastest (coalesced rows)
+      const int t = e / p, q = e % p;
+      const int jj = ipiv[q];
+      const double val = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * SW + t];
+      Xt[(size_t)t * T.pmax + (q < na_v ? q : q + rshift)] = val;
+    }
   }
   for (int t = tid; t < r; t += nthr) {
     const int pj = piv[t];
@@ -696,7 +699,7 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
   const size_t smem_leaf = sizeof(double) * ((size_t)T.mmax * T.w + 16 * (size_t)T.mmax);
   if (T.pmax > 4096) return HSSEIG_ERR_ARG;
   const size_t smem_id = sizeof(double) * ((size_t)T.pmax * (T.w | 1) + 2 * T.pmax + T.w + 1 + 32) +
-                         sizeof(int) * T.pmax + 64;
+                         sizeof(int) * 2 * T.pmax + 64;
   // fused inner formation needs room for one sibling compression (w x w)
   const size_t smem_fused = smem_id + sizeof(double) * ((size_t)T.w * T.w + 4);
   static const int fuse_pref = getenv("HSSEIG_FUSED_FORM") ? atoi(getenv("HSSEIG_FUSED_FORM")) : 0;
@@ -707,6 +710,12 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
   cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);
   cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(fused ? smem_fused : smem_id));
+  // zero the factor slots once; the ID kernels then write only their data regions
+  const size_t nn = (size_t)(2 * T.n_leaves - 1);
+  if (cudaMemsetAsync(T.U, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess ||
+      cudaMemsetAsync(T.V, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess ||
+      cudaMemsetAsync(T.Vt, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess)
+    return HSSEIG_ERR_CUDA;
   for (int lev = T.depth; lev >= 1; --lev) {
     dim3 grid(1u << lev, 2);
     if (lev == T.depth) {
