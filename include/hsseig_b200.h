@@ -216,6 +216,40 @@ int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, 
                          int64_t n, int64_t w, int64_t ldo, double *out, void *work,
                          int32_t *fail_dev, int64_t *tails, int64_t tail_cap, void *stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Divide-and-conquer glue (the caller around the merge: SURVEY.md §8 f1-f2).
+ * --------------------------------------------------------------------------------------- */
+/*
+ * Base case for every leaf of the recursion at once: implicit QL with Wilkinson shift
+ * (tql2, pkg/src/hsseig/_kernels.pyx:352-411) followed by the ascending stable sort of
+ * dc.py:118-129.  Matrix m has order off[m+1]-off[m] <= 32, diagonal a[off[m]..] and
+ * off-diagonal b[off[m]-m..] (n-1 entries); lam[off[m]..] receives its eigenvalues and
+ * Q[qoff[m]..] its n x n row-major eigenvectors.  status[m] = 1 + l if eigenvalue l
+ * stalls after max_iter sweeps (BaseCaseError), else untouched.
+ */
+int hsseig_tql2_batched(const double *a, const double *b, const int64_t *off, int64_t nmat,
+                        int max_iter, double *lam, double *Q, const int64_t *qoff,
+                        int32_t *status, void *stream);
+/*
+ * Host deflation of the merged system (pkg/src/hsseig/secular.py:91-156): returns k;
+ * d_out/z_out/perm hold the kept system then the deflated poles; rotations (ri, rj, rc,
+ * rs) in input indices, n_rot of them.  Host pointers.
+ */
+int64_t hsseig_deflate(const double *d, const double *z, int64_t n, double rho, double *d_out,
+                       double *z_out, int64_t *perm, int64_t *ri, int64_t *rj, double *rc,
+                       double *rs, int64_t *n_rot, double *tol_out);
+/* W[:, c] = blockdiag(Q1, Q2)[:, src[c]] (dc.py:222-224, 241, 255). */
+int hsseig_assemble_merge(const double *Q1, int64_t n1, const double *Q2, int64_t n2,
+                          const int64_t *src, double *W, int64_t ldw, void *stream);
+/* Deflation rotations on column pairs of W, in order (dc.py:225-230). */
+int hsseig_apply_rotations(double *W, int64_t ldw, int64_t rows, const int64_t *ca,
+                           const int64_t *cb, const double *c, const double *s, int64_t nrot,
+                           void *stream);
+/* out[:, c] = src[c] < k ? A[:, src[c]] : B[:, src[c]] (final eigenvalue order, dc.py:253-257). */
+int hsseig_gather_columns(const double *A, int64_t lda, const double *B, int64_t ldb, int64_t k,
+                          const int64_t *src, int64_t ncol, int64_t rows, double *out,
+                          int64_t ldo, void *stream);
+
 /* Plain batched helper used by tests/bench: out = A @ B (P x K)(K x N), FP64 DMMA. */
 int hsseig_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *stream);

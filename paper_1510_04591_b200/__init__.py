@@ -11,6 +11,7 @@ from .hss import (HssPartition, HssTree, build_partition, estimate_rank, hss_mat
                   hss_to_dense, rand_hss_construct, rank_bound)
 from .matgen import (FAMILIES, SymTridiagonal, gen_clement, gen_config5, gen_hermite, gen_kac,
                      gen_laguerre, gen_legendre, gen_toeplitz, gen_uniform, isolated_merge_system)
+from .solver import adc_solve
 from .secular import (RankOneSystem, SecularConvergenceError, SecularSolution,
                       WeightRecomputationError, column_normalizers, recompute_weights,
                       solve_secular)

@@ -83,6 +83,15 @@ _SIGS = {
     "hsseig_pcg64_normals": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp,
                                             c_vp, c_i64, c_vp]),
+    "hsseig_tql2_batched": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, ctypes.c_int, c_vp, c_vp, c_vp,
+                                           c_vp, c_vp]),
+    "hsseig_deflate": (c_i64, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                               c_vp, c_vp]),
+    "hsseig_assemble_merge": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
+    "hsseig_apply_rotations": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
+                                              c_vp]),
+    "hsseig_gather_columns": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64,
+                                             c_vp, c_i64, c_vp]),
     "hsseig_gemm": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64,
                                    c_vp]),
 }

@@ -1,0 +1,259 @@
+// Divide-and-conquer glue around the merge path:
+//   * batched base-case QL on the leaves of the recursion     (_kernels.pyx:352-411, dc.py:118-129)
+//   * host deflation of the merged rank-one system            (secular.py:91-156)
+//   * device assembly of blockdiag(Q1, Q2) permuted to [kept | deflated], the deflation
+//     Givens rotations, and the final eigenvalue-order column gather (dc.py:215-257)
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <vector>
+
+#include "common.cuh"
+
+namespace hsseig {
+
+// ---------------------------------------------------------------------------
+// batched implicit QL with Wilkinson shift, one warp per tridiagonal (n <= 32);
+// lane r owns row r of the rotation accumulator.  Scalar recurrences run redundantly
+// in every lane on shared d/e (identical values), rounding kept IEEE (no FMA
+// contraction) like the reference's C loop.
+// ---------------------------------------------------------------------------
+constexpr int kQLMax = 32;
+
+__global__ void tql2_batched_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                    const int64_t* __restrict__ off, int64_t nmat, int max_iter,
+                                    double* __restrict__ lam, double* __restrict__ Q,
+                                    const int64_t* __restrict__ qoff, int32_t* __restrict__ status) {
+  __shared__ double sd[4][kQLMax], se[4][kQLMax + 1], sz[4][kQLMax][kQLMax + 1];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m = (int64_t)blockIdx.x * 4 + wl;
+  if (m >= nmat) return;
+  const int64_t o = off[m];
+  const int n = (int)(off[m + 1] - o);
+  double* d = sd[wl];
+  double* e = se[wl];
+  double(*Z)[kQLMax + 1] = sz[wl];
+  if (lane < n) {
+    d[lane] = a[o + lane];
+    e[lane] = (lane + 1 < n) ? b[o - m + lane] : 0.0;   // b has n-1 entries per matrix
+    for (int c = 0; c < n; ++c) Z[lane][c] = (lane == c) ? 1.0 : 0.0;
+  }
+  __syncwarp();
+  int fail = 0;
+  if (n > 1) {
+    for (int l = 0; l < n && !fail; ++l) {
+      int it = 0;
+      for (;;) {
+        int mm = l;
+        for (; mm < n - 1; ++mm) {
+          const double dd = __dadd_rn(fabs(d[mm]), fabs(d[mm + 1]));
+          if (fabs(e[mm]) <= __dmul_rn(kEps, dd)) break;
+        }
+        if (mm == l) break;
+        if (++it > max_iter) { fail = 1 + l; break; }
+        double g = __ddiv_rn(__dsub_rn(d[l + 1], d[l]), __dmul_rn(2.0, e[l]));
+        double r = hypot(g, 1.0);
+        g = __dadd_rn(__dsub_rn(d[mm], d[l]), __ddiv_rn(e[l], __dadd_rn(g, copysign(r, g))));
+        double s = 1.0, c = 1.0, p = 0.0;
+        bool clean = true;
+        for (int i = mm - 1; i >= l; --i) {
+          const double f = __dmul_rn(s, e[i]);
+          const double bb = __dmul_rn(c, e[i]);
+          r = hypot(f, g);
+          __syncwarp();
+          if (lane == 0) e[i + 1] = r;
+          __syncwarp();
+          if (r == 0.0) {
+            if (lane == 0) {
+              d[i + 1] = __dsub_rn(d[i + 1], p);
+              e[mm] = 0.0;
+            }
+            __syncwarp();
+            clean = false;
+            break;
+          }
+          s = __ddiv_rn(f, r);
+          c = __ddiv_rn(g, r);
+          g = __dsub_rn(d[i + 1], p);
+          r = __dadd_rn(__dmul_rn(__dsub_rn(d[i], g), s), __dmul_rn(__dmul_rn(2.0, c), bb));
+          p = __dmul_rn(s, r);
+          __syncwarp();
+          if (lane == 0) d[i + 1] = __dadd_rn(g, p);
+          g = __dsub_rn(__dmul_rn(c, r), bb);
+          if (lane < n) {
+            const double zi = Z[lane][i], zi1 = Z[lane][i + 1];
+            Z[lane][i + 1] = __dadd_rn(__dmul_rn(s, zi), __dmul_rn(c, zi1));
+            Z[lane][i] = __dsub_rn(__dmul_rn(c, zi), __dmul_rn(s, zi1));
+          }
+          __syncwarp();
+        }
+        if (clean) {
+          __syncwarp();
+          if (lane == 0) {
+            d[l] = __dsub_rn(d[l], p);
+            e[l] = g;
+            e[mm] = 0.0;
+          }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  __syncwarp();
+  // ascending order, stable (np.argsort kind="stable", dc.py:127)
+  if (lane < n) {
+    const double v = d[lane];
+    int pos = 0;
+    for (int j = 0; j < n; ++j) pos += (d[j] < v) || (d[j] == v && j < lane);
+    lam[o + pos] = v;
+    double* q = Q + qoff[m];
+    for (int row = 0; row < n; ++row) q[(int64_t)row * n + pos] = Z[row][lane];
+  }
+  if (lane == 0 && fail) status[m] = fail;
+}
+
+// W[:, c] = blockdiag(Q1, Q2)[:, src[c]] for c < n, W row-major (ldw)
+__global__ void assemble_kernel(const double* __restrict__ Q1, int64_t n1, const double* __restrict__ Q2,
+                                int64_t n2, const int64_t* __restrict__ src, double* __restrict__ W,
+                                int64_t ldw) {
+  const int64_t n = n1 + n2;
+  const int64_t row = blockIdx.y;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sc = src[c];
+    double v = 0.0;
+    if (row < n1) { if (sc < n1) v = Q1[row * n1 + sc]; }
+    else if (sc >= n1) v = Q2[(row - n1) * n2 + (sc - n1)];
+    W[row * ldw + c] = v;
+  }
+}
+
+// deflation Givens rotations on column pairs, in order, every row independently
+// (dc.py:225-230: col_a = c*a + s*b, col_b = -s*a + c*b, no FMA contraction)
+__global__ void rotate_kernel(double* __restrict__ W, int64_t ldw, int64_t rows,
+                              const int64_t* __restrict__ ca, const int64_t* __restrict__ cb,
+                              const double* __restrict__ cs, const double* __restrict__ sn,
+                              int64_t nrot) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  double* w = W + row * ldw;
+  for (int64_t t = 0; t < nrot; ++t) {
+    const int64_t ia = ca[t], ib = cb[t];
+    const double c = cs[t], s = sn[t];
+    const double x = w[ia], y = w[ib];
+    w[ia] = __dadd_rn(__dmul_rn(c, x), __dmul_rn(s, y));
+    w[ib] = __dadd_rn(__dmul_rn(-s, x), __dmul_rn(c, y));
+  }
+}
+
+// out[:, c] = (src[c] < k ? A[:, src[c]] : B[:, src[c]])  (final eigenvalue order)
+__global__ void gather2_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                               int64_t ldb, int64_t k, const int64_t* __restrict__ src, int64_t ncol,
+                               double* __restrict__ out, int64_t ldo) {
+  const int64_t row = blockIdx.y;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncol;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sc = src[c];
+    out[row * ldo + c] = sc < k ? A[row * lda + sc] : B[row * ldb + sc];
+  }
+}
+
+}  // namespace hsseig
+
+using namespace hsseig;
+
+extern "C" int hsseig_tql2_batched(const double* a, const double* b, const int64_t* off,
+                                   int64_t nmat, int max_iter, double* lam, double* Q,
+                                   const int64_t* qoff, int32_t* status, void* stream) {
+  if (nmat < 0 || !a || !off || !lam || !Q || !qoff || !status) return HSSEIG_ERR_ARG;
+  if (nmat == 0) return HSSEIG_OK;
+  tql2_batched_kernel<<<(unsigned)((nmat + 3) / 4), 128, 0, (cudaStream_t)stream>>>(
+      a, b, off, nmat, max_iter, lam, Q, qoff, status);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_assemble_merge(const double* Q1, int64_t n1, const double* Q2, int64_t n2,
+                                     const int64_t* src, double* W, int64_t ldw, void* stream) {
+  const int64_t n = n1 + n2;
+  if (n <= 0 || ldw < n || n > 0x7fffffff) return HSSEIG_ERR_ARG;
+  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n);
+  assemble_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(Q1, n1, Q2, n2, src, W, ldw);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_apply_rotations(double* W, int64_t ldw, int64_t rows, const int64_t* ca,
+                                      const int64_t* cb, const double* c, const double* s,
+                                      int64_t nrot, void* stream) {
+  if (rows < 0 || nrot < 0) return HSSEIG_ERR_ARG;
+  if (nrot == 0 || rows == 0) return HSSEIG_OK;
+  rotate_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, (cudaStream_t)stream>>>(W, ldw, rows, ca,
+                                                                                  cb, c, s, nrot);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_gather_columns(const double* A, int64_t lda, const double* B, int64_t ldb,
+                                     int64_t k, const int64_t* src, int64_t ncol, int64_t rows,
+                                     double* out, int64_t ldo, void* stream) {
+  if (rows < 0 || ncol < 0 || rows > 0x7fffffff) return HSSEIG_ERR_ARG;
+  if (rows == 0 || ncol == 0) return HSSEIG_OK;
+  dim3 grid((unsigned)std::min<int64_t>((ncol + 255) / 256, 64), (unsigned)rows);
+  gather2_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, B, ldb, k, src, ncol, out, ldo);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+/*
+ * Host deflation (secular.py:91-156), restated: negligible weights deflate at their pole,
+ * pole pairs closer than tol are merged by a Givens rotation that zeroes one weight.
+ * Inputs d, z (n), rho.  Outputs: d_out/z_out with the kept system first (k entries,
+ * sorted poles) followed by the deflated poles (ascending); perm[n] = sorted-input index
+ * of each output slot; rotations (ri, rj, rc, rs; n_rot <= n) in sorted-input indices.
+ * Returns k.
+ */
+extern "C" int64_t hsseig_deflate(const double* d, const double* z, int64_t n, double rho,
+                                  double* d_out, double* z_out, int64_t* perm, int64_t* ri,
+                                  int64_t* rj, double* rc, double* rs, int64_t* n_rot,
+                                  double* tol_out) {
+  if (n < 1) return -1;
+  double dmax = 0.0, zz = 0.0;
+  for (int64_t t = 0; t < n; ++t) {
+    dmax = std::max(dmax, std::fabs(d[t]));
+    zz += z[t] * z[t];
+  }
+  const double tol = 8.0 * kEps * std::max(dmax, rho * zz);
+  std::vector<int64_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return d[x] < d[y]; });
+  std::vector<double> ds(n), zs(n);
+  for (int64_t t = 0; t < n; ++t) { ds[t] = d[order[t]]; zs[t] = z[order[t]]; }
+  std::vector<char> keep(n, 1);
+  int64_t surv = -1, nr = 0;
+  for (int64_t t = 0; t < n; ++t) {
+    if (rho * std::fabs(zs[t]) <= tol) { keep[t] = 0; continue; }
+    if (surv >= 0 && ds[t] - ds[surv] <= tol) {
+      const double h = std::hypot(zs[surv], zs[t]);
+      const double c = zs[surv] / h, s = zs[t] / h;
+      zs[surv] = h;
+      zs[t] = 0.0;
+      const double dp = ds[surv], dt = ds[t];
+      ds[surv] = c * c * dp + s * s * dt;
+      ds[t] = s * s * dp + c * c * dt;
+      ri[nr] = order[surv]; rj[nr] = order[t]; rc[nr] = c; rs[nr] = s; ++nr;
+      keep[t] = 0;
+    } else {
+      surv = t;
+    }
+  }
+  std::vector<int64_t> kept, defl;
+  for (int64_t t = 0; t < n; ++t) (keep[t] ? kept : defl).push_back(t);
+  std::stable_sort(defl.begin(), defl.end(), [&](int64_t x, int64_t y) { return ds[x] < ds[y]; });
+  int64_t q = 0;
+  for (int64_t t : kept) { d_out[q] = ds[t]; z_out[q] = zs[t]; perm[q] = order[t]; ++q; }
+  for (int64_t t : defl) { d_out[q] = ds[t]; z_out[q] = zs[t]; perm[q] = order[t]; ++q; }
+  *n_rot = nr;
+  if (tol_out) *tol_out = tol;
+  return (int64_t)kept.size();
+}

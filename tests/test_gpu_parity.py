@@ -5,7 +5,7 @@ All calls go through libhsseig_b200.so (the C ABI) via the package's host layer.
 import numpy as np
 import pytest
 
-from helpers import EPS, config4_system, golden, random_system, unpack_tree
+from helpers import EPS, align_columns, config4_system, golden, random_system, unpack_tree
 from oracle import hss_oracle as orc
 
 torch = pytest.importorskip("torch")
@@ -336,3 +336,53 @@ def test_sharded_merge_driver_single_rank_nccl():
         assert float((out - ref).abs().max()) <= 1e-14 * float(ref.abs().max())
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------- full DC solve (dc.py:174-257)
+@pytest.mark.parametrize("fam", ["toeplitz", "kac", "uniform", "cfg5"])
+@pytest.mark.parametrize("method", ["adc-rand", "dense-dc"])
+def test_adc_solve_vs_reference(fam, method):
+    g = golden("adc")
+    a, b = g[f"{fam}_a"], g[f"{fam}_b"]
+    T = hb.SymTridiagonal(a, b)
+    cfg = hb.SolverConfig(leaf_size=32, hss_threshold=128, rank_eps=1e-13, method=method)
+    res = hb.adc_solve(T, cfg)
+    tag = f"{fam}_{method}"
+    nrm = T.norm_max()
+    assert np.abs(res.lam - g[f"{tag}_lam"]).max() <= 1e-12 * nrm
+    ref_m = g[f"{tag}_merges"]
+    got = np.array([[m.size, m.kept, m.n_deflated, int(m.used_hss), m.hss_rank, int(m.fell_back)]
+                    for m in res.merges], dtype=np.int64)
+    # merge sizes, deflation counts and the HSS / fallback decisions are the reference's
+    np.testing.assert_array_equal(got[:, [0, 1, 2, 3, 5]], ref_m[:, [0, 1, 2, 3, 5]])
+    Q = res.Q
+    n = T.n
+    orth = float((Q.T @ Q - torch.eye(n, dtype=torch.float64, device="cuda")).abs().max()) / n
+    A = torch.as_tensor(T.to_dense(), device="cuda")
+    lam = torch.as_tensor(res.lam, device="cuda")
+    bwd = float((A - (Q * lam) @ Q.T).abs().max()) / (nrm * n)
+    assert orth <= 10 * max(float(g[f"{tag}_orth"]), EPS)
+    assert bwd <= 10 * max(float(g[f"{tag}_bwd"]), EPS)
+    if fam in ("toeplitz", "kac"):
+        Qs = np_(Q)[:, ::8]
+        ref = g[f"{tag}_Qcols"]
+        assert np.abs(align_columns(Qs, ref) - ref).max() <= 1e-10
+
+
+def test_adc_solve_toeplitz_closed_form():
+    # pkg/tests/test_dc.py:249-257 / acceptance 8: 2 + 2 cos(j pi / (N+1)), HSS used
+    n = 2000
+    T = hb.gen_toeplitz(n)
+    cfg = hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13)
+    res = hb.adc_solve(T, cfg)
+    ref = np.sort(2 + 2 * np.cos(np.arange(1, n + 1) * np.pi / (n + 1)))
+    assert np.abs(res.lam - ref).max() <= 1e-12 * 4
+    assert any(m.used_hss for m in res.merges)
+
+
+def test_adc_solve_kac_closed_form():
+    n = 1024
+    T = hb.gen_kac(n)
+    res = hb.adc_solve(T, hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13))
+    ref = -(n - 1) + 2.0 * np.arange(n)
+    assert np.abs(res.lam - ref).max() <= 1e-12 * T.norm_max()
