@@ -8,7 +8,7 @@ import torch
 
 from . import _native as nat
 from .flops import cauchy_eval_flops, gemm_flops
-from .secular import column_normalizers, dev, stable_gap
+from .secular import column_normalizers, dev, dev_rows, stable_gap
 
 MAX_SAMPLE_WIDTH = 128
 
@@ -125,7 +125,7 @@ class CauchyEvecMatrix:
 
     def right_multiply_into(self, Qblock, out=None):
         """out = Qblock @ C with C generated on the fly (dense update, dc.py:132-138)."""
-        Q = dev(Qblock)
+        Q = dev_rows(Qblock)
         if Q.shape[1] != self.k:
             raise ValueError("inner dimensions do not match")
         if out is None:

@@ -14,7 +14,7 @@ from .cauchy import CauchyEvecMatrix
 from .flops import FlopCounter, cauchy_eval_flops, gemm_flops
 from .hss import (MAX_WIDTH, build_partition, estimate_rank, finish_construct, hss_matmul_right,
                   rand_hss_construct)
-from .secular import RankOneSystem, dev, recompute_weights, solve_secular
+from .secular import RankOneSystem, dev, dev_rows, recompute_weights, solve_secular
 
 METHODS = ("dense-dc", "adc-rand")
 
@@ -87,7 +87,7 @@ def update_vectors_dense(Qblock, Qprime, flops=None, out=None):
     Qprime may be a CauchyEvecMatrix: its tiles are then generated on the fly inside
     the DMMA GEMM (the reference first materialises C.to_dense(), counted the same way).
     """
-    Qb = dev(Qblock)
+    Qb = dev_rows(Qblock)
     if isinstance(Qprime, CauchyEvecMatrix):
         if Qb.shape[1] != Qprime.k:
             raise ValueError("inner dimensions do not match")

@@ -15,7 +15,7 @@ import torch
 
 from . import _native as nat
 from .flops import cauchy_eval_flops, cpqr_flops, gemm_flops
-from .secular import Status, dev
+from .secular import Status, dev, dev_rows
 
 DIST_SHIFT_THRESHOLD = 1e-10   # hss.py:20
 MAX_BOUNDARY_SHIFT = 5         # hss.py:21
@@ -370,11 +370,15 @@ def finish_construct(tree, flops=None):
 
 def hss_matmul_right(X, H, flops=None, out=None):
     """Structured product X @ H (hss.py:309-361) as per-level batched DMMA GEMMs."""
-    X = dev(X)
+    X = dev_rows(X)
     if X.ndim == 1:
         X = X[None, :]
     if X.shape[1] != H.k:
         raise ValueError(f"X has {X.shape[1]} columns, tree order is {H.k}")
+    if X.stride(0) % 2 or X.data_ptr() % 16:   # TMA reads X with 16-byte aligned rows
+        Xp = torch.empty(X.shape[0], X.shape[1] + 1, dtype=torch.float64, device="cuda")
+        Xp[:, :X.shape[1]] = X
+        X = Xp[:, :X.shape[1]]
     P = X.shape[0]
     lib = nat.load()
     if out is None:

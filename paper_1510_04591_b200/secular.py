@@ -23,6 +23,14 @@ class WeightRecomputationError(ArithmeticError):
     """secular.py:29"""
 
 
+def dev_rows(x):
+    """Row-major float64 device matrix; a CUDA view with unit column stride is kept as is."""
+    if (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.ndim == 2
+            and x.stride(1) == 1):
+        return x
+    return dev(x)
+
+
 def dev(x, dtype=torch.float64):
     """Device float64 contiguous tensor view/copy of x (numpy or torch)."""
     if isinstance(x, torch.Tensor):
