@@ -44,6 +44,8 @@ typedef struct hsseig_status {
 /* Library identification (build check) and the number of kernels launched so far. */
 const char *hsseig_version(void);
 int64_t hsseig_launch_count(void);
+/* Where the last HSSEIG_ERR_ARG of this thread came from ("invalid argument (file:line)"). */
+const char *hsseig_last_error(void);
 int hsseig_status_init(hsseig_status *status_dev, int64_t k, void *stream);
 
 /*

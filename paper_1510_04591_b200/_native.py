@@ -48,6 +48,7 @@ class Tree(ctypes.Structure):
 _SIGS = {
     "hsseig_version": (ctypes.c_char_p, []),
     "hsseig_launch_count": (c_i64, []),
+    "hsseig_last_error": (ctypes.c_char_p, []),
     "hsseig_status_init": (ctypes.c_int, [c_vp, c_i64, c_vp]),
     "hsseig_secular": (ctypes.c_int, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
                                       c_vp, c_vp]),
@@ -144,5 +145,6 @@ def check(rc, what):
     if rc == HSSEIG_OK:
         return
     if rc == HSSEIG_ERR_ARG:
-        raise ValueError(f"{what}: invalid argument")
+        detail = _LIB.hsseig_last_error().decode() if _LIB is not None else "invalid argument"
+        raise ValueError(f"{what}: {detail}")
     raise RuntimeError(f"{what}: CUDA error (status {rc})")

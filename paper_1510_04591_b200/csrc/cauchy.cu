@@ -272,7 +272,7 @@ static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int
   MapSet maps;
   for (int r = 1; r < kMaps; ++r) make_map(&maps.m[r], nullptr, 0, 0, 0, 0, 0);
   if (!make_map(&maps.m[0], om, (uint64_t)k, (uint64_t)w, (uint64_t)ldom, T::SB, T::BK))
-    return HSSEIG_ERR_ARG;
+    HSS_ARG_FAIL();
   if (cudaMemcpyAsync(dmap, &maps, sizeof(MapSet), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return HSSEIG_ERR_CUDA;
   const int64_t items = tiles * nsplit;
@@ -310,7 +310,7 @@ static CauchyGen to_gen(const hsseig_gen* g) {
 extern "C" int hsseig_cauchy_block(const hsseig_gen* gen, const int64_t* rows, int64_t nr,
                                    const int64_t* cols, int64_t nc, double* out, int64_t ldo,
                                    void* stream) {
-  if (!gen || nr < 0 || nc < 0 || ldo < nc) return HSSEIG_ERR_ARG;
+  if (!gen || nr < 0 || nc < 0 || ldo < nc) HSS_ARG_FAIL();
   if (nr == 0 || nc == 0) return HSSEIG_OK;
   int64_t n = nr * nc;
   cauchy_block_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
@@ -336,8 +336,8 @@ extern "C" int hsseig_cauchy_sample_part(const hsseig_gen* gen, const double* om
                                          int64_t w, int64_t row0, int64_t row1, double* Y, double* Z,
                                          int64_t ldy, double* work, void* stream) {
   if (!gen || w < 1 || w > 128 || ldom < w || ldy < w || row0 < 0 || row1 > gen->k || row0 > row1)
-    return HSSEIG_ERR_ARG;
-  if ((reinterpret_cast<uintptr_t>(omega) & 15) || (ldom & 1)) return HSSEIG_ERR_ARG;  // TMA rows
+    HSS_ARG_FAIL();
+  if ((reinterpret_cast<uintptr_t>(omega) & 15) || (ldom & 1)) HSS_ARG_FAIL();  // TMA rows
   if (row0 == row1) return HSSEIG_OK;
   CauchyGen g = to_gen(gen);
   cudaStream_t s = (cudaStream_t)stream;
@@ -352,13 +352,13 @@ extern "C" int hsseig_cauchy_sample_part(const hsseig_gen* gen, const double* om
 extern "C" int hsseig_cauchy_sample(const hsseig_gen* gen, const double* omega, int64_t ldom,
                                     int64_t w, double* Y, double* Z, int64_t ldy, double* work,
                                     void* stream) {
-  if (!gen) return HSSEIG_ERR_ARG;
+  if (!gen) HSS_ARG_FAIL();
   return hsseig_cauchy_sample_part(gen, omega, ldom, w, 0, gen->k, Y, Z, ldy, work, stream);
 }
 
 extern "C" int hsseig_dense_update(const double* Qb, int64_t ldq, int64_t P, const hsseig_gen* gen,
                                    double* out, int64_t ldo, void* stream) {
-  if (!gen || P < 0 || ldq < gen->k || ldo < gen->k) return HSSEIG_ERR_ARG;
+  if (!gen || P < 0 || ldq < gen->k || ldo < gen->k) HSS_ARG_FAIL();
   if (P == 0) return HSSEIG_OK;
   using T = Tile<4, 8, 4, 2, 2>;
   const size_t smem = sizeof(double) * T::STAGE_ELEMS * 2;

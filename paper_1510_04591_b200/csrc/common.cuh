@@ -12,6 +12,16 @@
 namespace hsseig {
 extern std::atomic<long long> g_launches;
 }
+namespace hsseig {
+void set_arg_error(const char* file, int line);
+}
+// argument / configuration failure: remember where (hsseig_last_error) and return code 1
+#define HSS_ARG_FAIL()                               \
+  do {                                               \
+    hsseig::set_arg_error(__FILE__, __LINE__);       \
+    return HSSEIG_ERR_ARG;                           \
+  } while (0)
+
 #define HSS_CHECK_LAUNCH()                                       \
   do {                                                           \
     hsseig::g_launches.fetch_add(1, std::memory_order_relaxed);  \

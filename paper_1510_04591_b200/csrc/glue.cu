@@ -165,7 +165,7 @@ using namespace hsseig;
 extern "C" int hsseig_tql2_batched(const double* a, const double* b, const int64_t* off,
                                    int64_t nmat, int max_iter, double* lam, double* Q,
                                    const int64_t* qoff, int32_t* status, void* stream) {
-  if (nmat < 0 || !a || !off || !lam || !Q || !qoff || !status) return HSSEIG_ERR_ARG;
+  if (nmat < 0 || !a || !off || !lam || !Q || !qoff || !status) HSS_ARG_FAIL();
   if (nmat == 0) return HSSEIG_OK;
   tql2_batched_kernel<<<(unsigned)((nmat + 3) / 4), 128, 0, (cudaStream_t)stream>>>(
       a, b, off, nmat, max_iter, lam, Q, qoff, status);
@@ -176,7 +176,7 @@ extern "C" int hsseig_tql2_batched(const double* a, const double* b, const int64
 extern "C" int hsseig_assemble_merge(const double* Q1, int64_t n1, const double* Q2, int64_t n2,
                                      const int64_t* src, double* W, int64_t ldw, void* stream) {
   const int64_t n = n1 + n2;
-  if (n <= 0 || ldw < n || n > 0x7fffffff) return HSSEIG_ERR_ARG;
+  if (n <= 0 || ldw < n || n > 0x7fffffff) HSS_ARG_FAIL();
   dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n);
   assemble_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(Q1, n1, Q2, n2, src, W, ldw);
   HSS_CHECK_LAUNCH();
@@ -186,7 +186,7 @@ extern "C" int hsseig_assemble_merge(const double* Q1, int64_t n1, const double*
 extern "C" int hsseig_apply_rotations(double* W, int64_t ldw, int64_t rows, const int64_t* ca,
                                       const int64_t* cb, const double* c, const double* s,
                                       int64_t nrot, void* stream) {
-  if (rows < 0 || nrot < 0) return HSSEIG_ERR_ARG;
+  if (rows < 0 || nrot < 0) HSS_ARG_FAIL();
   if (nrot == 0 || rows == 0) return HSSEIG_OK;
   rotate_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, (cudaStream_t)stream>>>(W, ldw, rows, ca,
                                                                                   cb, c, s, nrot);
@@ -197,7 +197,7 @@ extern "C" int hsseig_apply_rotations(double* W, int64_t ldw, int64_t rows, cons
 extern "C" int hsseig_gather_columns(const double* A, int64_t lda, const double* B, int64_t ldb,
                                      int64_t k, const int64_t* src, int64_t ncol, int64_t rows,
                                      double* out, int64_t ldo, void* stream) {
-  if (rows < 0 || ncol < 0 || rows > 0x7fffffff) return HSSEIG_ERR_ARG;
+  if (rows < 0 || ncol < 0 || rows > 0x7fffffff) HSS_ARG_FAIL();
   if (rows == 0 || ncol == 0) return HSSEIG_OK;
   dim3 grid((unsigned)std::min<int64_t>((ncol + 255) / 256, 64), (unsigned)rows);
   gather2_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, B, ldb, k, src, ncol, out, ldo);

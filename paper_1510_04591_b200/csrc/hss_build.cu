@@ -599,13 +599,13 @@ extern "C" int64_t hsseig_tree_bytes(int32_t k, int32_t n_leaves, int32_t w, int
 extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t n_leaves, int32_t w,
                                   void* dev_mem, void* stream) {
   if (!t || !bounds || n_leaves < 2 || (n_leaves & (n_leaves - 1)) || w < 1 || !dev_mem)
-    return HSSEIG_ERR_ARG;
+    HSS_ARG_FAIL();
   int depth = 0;
   while ((1 << depth) < n_leaves) ++depth;
-  if (depth > 31) return HSSEIG_ERR_ARG;
+  if (depth > 31) HSS_ARG_FAIL();
   int32_t mmax = 0;
   for (int i = 0; i < n_leaves; ++i) {
-    if (bounds[i + 1] <= bounds[i]) return HSSEIG_ERR_ARG;
+    if (bounds[i + 1] <= bounds[i]) HSS_ARG_FAIL();
     mmax = std::max(mmax, bounds[i + 1] - bounds[i]);
   }
   const int32_t k = bounds[n_leaves];
@@ -689,15 +689,15 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
 extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega, int64_t ldom,
                                      const double* Y, const double* Z, int64_t ldy, double id_tol,
                                      hsseig_tree* tree, hsseig_status* st, void* stream) {
-  if (!gen || !tree || !omega || !Y || !Z || !st || gen->k != tree->k) return HSSEIG_ERR_ARG;
-  if (tree->w > tree->mmax || tree->w > 128) return HSSEIG_ERR_ARG;
+  if (!gen || !tree || !omega || !Y || !Z || !st || gen->k != tree->k) HSS_ARG_FAIL();
+  if (tree->w > tree->mmax || tree->w > 128) HSS_ARG_FAIL();
   cudaStream_t s = (cudaStream_t)stream;
   CauchyGen g;
   g.d = gen->d; g.dnext = gen->dnext; g.gam = gen->gamma; g.mu = gen->mu; g.zhat = gen->zhat;
   g.v = gen->v; g.k = gen->k;
   TreeDev T = to_dev(tree);
   const size_t smem_leaf = sizeof(double) * ((size_t)T.mmax * T.w + 16 * (size_t)T.mmax);
-  if (T.pmax > 4096) return HSSEIG_ERR_ARG;
+  if (T.pmax > 4096) HSS_ARG_FAIL();
   const size_t smem_id = sizeof(double) * ((size_t)T.pmax * (T.w | 1) + 2 * T.pmax + T.w + 1 + 32) +
                          sizeof(int) * 2 * T.pmax + 64;
   // fused inner formation needs room for one sibling compression (w x w)
@@ -706,7 +706,7 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
   const size_t smem_form = sizeof(double) * ((size_t)T.w * ((T.w | 1) + T.w) + 8);
   cudaFuncSetAttribute(inner_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_form);
   const int fused = (fuse_pref && smem_fused <= 227 * 1024) ? 1 : 0;
-  if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024) return HSSEIG_ERR_ARG;
+  if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024) HSS_ARG_FAIL();
   cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);
   cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(fused ? smem_fused : smem_id));

@@ -23,6 +23,7 @@
 //
 // Job descriptors are built on the device from the ranks the construction wrote, so
 // no host synchronisation is needed between construction and multiply.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -244,7 +245,7 @@ static int launch_tma(const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jo
     const uint32_t bc = is_a ? T::SA : T::SB;
     const uint32_t br = is_a ? T::BM : T::BK;
     if (!make_map(&maps.m[r], ops[r].base, ops[r].rows, ops[r].cols, ops[r].ld, bc, br))
-      return HSSEIG_ERR_ARG;
+      HSS_ARG_FAIL();
   }
   if (cudaMemcpyAsync(dmaps, &maps, sizeof(MapSet), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return HSSEIG_ERR_CUDA;
@@ -270,7 +271,7 @@ static int launch_narrow(int n, const Operand (&ops)[kMaps], MapSet* dm, const T
       case 1: case 2: return launch_tma<TTile<4, 2, 2, 4, 4>>(ops, dm, jobs, njobs, M, s);
       case 3: return launch_tma<TTile<4, 3, 2, 4, 4>>(ops, dm, jobs, njobs, M, s);
       case 4: return launch_tma<TTile<4, 4, 2, 4, 3>>(ops, dm, jobs, njobs, M, s);
-      default: return HSSEIG_ERR_ARG;
+      default: HSS_ARG_FAIL();
     }
   }
   if (variant == 0) {   // BM 128: 8 consumer warps of 32 x 8NF, NF = ceil(n/16)
@@ -279,7 +280,7 @@ static int launch_narrow(int n, const Operand (&ops)[kMaps], MapSet* dm, const T
       case 5: return launch_tma<TTile<4, 5, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
       case 6: return launch_tma<TTile<4, 6, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
       case 7: return launch_tma<TTile<4, 7, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      default: return HSSEIG_ERR_ARG;
+      default: HSS_ARG_FAIL();
     }
   }
   // default: BM 64: 8 consumer warps of 32 x 8NF, NF = ceil(n/32)
@@ -287,7 +288,7 @@ static int launch_narrow(int n, const Operand (&ops)[kMaps], MapSet* dm, const T
     case 1: case 2: return launch_tma<TTile<4, 2, 2, 4, 8>>(ops, dm, jobs, njobs, M, s);
     case 3: return launch_tma<TTile<4, 3, 2, 4, 8>>(ops, dm, jobs, njobs, M, s);
     case 4: return launch_tma<TTile<4, 4, 2, 4, 6>>(ops, dm, jobs, njobs, M, s);
-    default: return HSSEIG_ERR_ARG;
+    default: HSS_ARG_FAIL();
   }
 }
 
@@ -301,7 +302,7 @@ static int launch_wide(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJo
       case 5: return launch_tma<TTile<4, 5, 2, 4, 3>>(ops, dm, jobs, njobs, M, s);
       case 6: return launch_tma<TTile<4, 6, 2, 4, 3>>(ops, dm, jobs, njobs, M, s);
       case 7: return launch_tma<TTile<4, 7, 2, 4, 2>>(ops, dm, jobs, njobs, M, s);
-      default: return HSSEIG_ERR_ARG;
+      default: HSS_ARG_FAIL();
     }
   }
   if (variant == 0) {   // BM 64: 8 consumer warps of 16 x 8NF, NF = ceil(n/16)
@@ -316,7 +317,7 @@ static int launch_wide(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJo
       case 12: return launch_tma<TTile<2, 12, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
       case 13: return launch_tma<TTile<2, 13, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
       case 14: return launch_tma<TTile<2, 14, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      default: return HSSEIG_ERR_ARG;
+      default: HSS_ARG_FAIL();
     }
   }
   // default: BM 64: 8 consumer warps of 32 x 8NF, NF = ceil(n/32)
@@ -325,7 +326,7 @@ static int launch_wide(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJo
     case 5: return launch_tma<TTile<4, 5, 2, 4, 6>>(ops, dm, jobs, njobs, M, s);
     case 6: return launch_tma<TTile<4, 6, 2, 4, 5>>(ops, dm, jobs, njobs, M, s);
     case 7: return launch_tma<TTile<4, 7, 2, 4, 5>>(ops, dm, jobs, njobs, M, s);
-    default: return HSSEIG_ERR_ARG;
+    default: HSS_ARG_FAIL();
   }
 }
 
@@ -360,11 +361,11 @@ extern "C" int64_t hsseig_matmul_work_doubles(int64_t P, const hsseig_tree* t) {
 extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
                                        const hsseig_tree* t, double* out, int64_t ldo,
                                        double* work, void* stream) {
-  if (!t || !X || !out || !work || P < 0 || ldx < t->k || ldo < t->k) return HSSEIG_ERR_ARG;
+  if (!t || !X || !out || !work || P < 0 || ldx < t->k || ldo < t->k) HSS_ARG_FAIL();
   if (P == 0) return HSSEIG_OK;
   if ((reinterpret_cast<uintptr_t>(X) & 15) || (ldx & 1) || (reinterpret_cast<uintptr_t>(work) & 15))
-    return HSSEIG_ERR_ARG;   // TMA needs 16-byte aligned rows
-  if (P > 0x7fffffff) return HSSEIG_ERR_ARG;
+    HSS_ARG_FAIL();   // TMA needs 16-byte aligned rows
+  if (P > 0x7fffffff) HSS_ARG_FAIL();
   cudaStream_t s = (cudaStream_t)stream;
   const int ws = t->ws, n = t->n_leaves, nn = t->n_nodes, nup = 2 * n - 2;
   const int64_t lvl_total = P * (int64_t)ws * (2 * (int64_t)n - 2);
@@ -379,7 +380,7 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   const int njob_total = 2 * nup + n;
   MapSet* dmaps = reinterpret_cast<MapSet*>(
       (reinterpret_cast<uintptr_t>(jobs + njob_total) + 255) & ~(uintptr_t)255);
-  if (t->depth > 31) return HSSEIG_ERR_ARG;
+  if (t->depth > 31) HSS_ARG_FAIL();
   setup_jobs_kernel<<<(2 * nup + n + 127) / 128, 128, 0, s>>>(p, jobs);
   HSS_CHECK_LAUNCH();
   auto lvl = [&](double* base, int l) -> Operand {
@@ -415,11 +416,11 @@ extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_
   static TJob* jobs = nullptr;
   static MapSet* dmaps = nullptr;
   static int cap = 0;
-  if (M < 0 || N < 0 || K < 0 || lda < K || ldb < N || ldc < N) return HSSEIG_ERR_ARG;
+  if (M < 0 || N < 0 || K < 0 || lda < K || ldb < N || ldc < N) HSS_ARG_FAIL();
   if (M == 0 || N == 0) return HSSEIG_OK;
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) || (lda & 1) ||
       (ldb & 1) || K == 0)
-    return HSSEIG_ERR_ARG;
+    HSS_ARG_FAIL();
   const int nj = (int)((N + 127) / 128);
   cudaStream_t s = (cudaStream_t)stream;
   if (nj > cap) {
@@ -443,5 +444,11 @@ extern "C" const char* hsseig_version(void) { return "hsseig_b200 0.2 sm_100a"; 
 
 namespace hsseig {
 std::atomic<long long> g_launches{0};
+static thread_local char g_err[256] = "";
+void set_arg_error(const char* file, int line) {
+  const char* base = strrchr(file, '/');
+  snprintf(g_err, sizeof(g_err), "invalid argument (%s:%d)", base ? base + 1 : file, line);
 }
+}
+extern "C" const char* hsseig_last_error(void) { return hsseig::g_err; }
 extern "C" int64_t hsseig_launch_count(void) { return hsseig::g_launches.load(); }

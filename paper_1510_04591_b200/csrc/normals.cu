@@ -265,7 +265,7 @@ using namespace hsseig;
 static int64_t raw_len(int64_t n) { return ((n + n / 16 + 4096 + kSeg - 1) / kSeg) * kSeg; }
 
 extern "C" int hsseig_set_normal_tables(const uint64_t* ki, const double* wi, const double* fi) {
-  if (!ki || !wi || !fi) return HSSEIG_ERR_ARG;
+  if (!ki || !wi || !fi) HSS_ARG_FAIL();
   if (cudaMemcpyToSymbol(g_ki, ki, sizeof(uint64_t) * 256) != cudaSuccess ||
       cudaMemcpyToSymbol(g_wi, wi, sizeof(double) * 256) != cudaSuccess ||
       cudaMemcpyToSymbol(g_fi, fi, sizeof(double) * 256) != cudaSuccess)
@@ -284,8 +284,8 @@ extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64
                                     uint64_t inc_lo, int64_t n, int64_t w, int64_t ldo, double* out,
                                     void* work, int32_t* fail_dev, int64_t* tails,
                                     int64_t tail_cap, void* stream) {
-  if (!g_tables_loaded) return HSSEIG_ERR_ARG;
-  if (n < 0 || w < 1 || ldo < w || !out || !work || !fail_dev) return HSSEIG_ERR_ARG;
+  if (!g_tables_loaded) HSS_ARG_FAIL();
+  if (n < 0 || w < 1 || ldo < w || !out || !work || !fail_dev) HSS_ARG_FAIL();
   if (n == 0) return HSSEIG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t L = raw_len(n);

@@ -367,7 +367,7 @@ extern "C" int hsseig_secular_part(const double* d, const double* z, int64_t k, 
                                    void* stream) {
   if (k < 1 || !(rho > 0.0) || !d || !z || !lam || !gamma || !mu || !iters || !work || !st ||
       ibeg < 0 || iend > k || ibeg > iend)
-    return HSSEIG_ERR_ARG;
+    HSS_ARG_FAIL();
   if (ibeg == iend) return HSSEIG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   double* z2 = work;
@@ -390,7 +390,7 @@ extern "C" int hsseig_secular(const double* d, const double* z, int64_t k, doubl
 
 extern "C" int hsseig_dnext(const double* d, const double* gamma, const double* mu, int64_t k,
                             double* dnext, void* stream) {
-  if (k < 1) return HSSEIG_ERR_ARG;
+  if (k < 1) HSS_ARG_FAIL();
   dnext_kernel<<<(unsigned)((k + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d, gamma, mu, k, dnext);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
@@ -400,7 +400,7 @@ extern "C" int hsseig_loewner_part(const double* d, const double* dnext, const d
                                    const double* mu, const double* z, int64_t k, double rho,
                                    int64_t ibeg, int64_t iend, double* zhat, hsseig_status* st,
                                    void* stream) {
-  if (k < 1 || !(rho > 0.0) || ibeg < 0 || iend > k || ibeg > iend) return HSSEIG_ERR_ARG;
+  if (k < 1 || !(rho > 0.0) || ibeg < 0 || iend > k || ibeg > iend) HSS_ARG_FAIL();
   if (ibeg == iend) return HSSEIG_OK;
   constexpr int R = 4;
   const int64_t warps = (iend - ibeg + R - 1) / R;
@@ -419,7 +419,7 @@ extern "C" int hsseig_loewner(const double* d, const double* dnext, const double
 extern "C" int hsseig_normalizers_part(const double* d, const double* dnext, const double* gamma,
                                        const double* mu, const double* zhat, int64_t k,
                                        int64_t jbeg, int64_t jend, double* v, void* stream) {
-  if (k < 1 || jbeg < 0 || jend > k || jbeg > jend) return HSSEIG_ERR_ARG;
+  if (k < 1 || jbeg < 0 || jend > k || jbeg > jend) HSS_ARG_FAIL();
   if (jbeg == jend) return HSSEIG_OK;
   constexpr int R = 4;
   const int64_t warps = (jend - jbeg + R - 1) / R;
