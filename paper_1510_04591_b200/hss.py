@@ -376,7 +376,7 @@ def hss_matmul_right(X, H, flops=None, out=None):
     if X.shape[1] != H.k:
         raise ValueError(f"X has {X.shape[1]} columns, tree order is {H.k}")
     if X.stride(0) % 2 or X.data_ptr() % 16:   # TMA reads X with 16-byte aligned rows
-        Xp = torch.empty(X.shape[0], X.shape[1] + 1, dtype=torch.float64, device="cuda")
+        Xp = torch.empty(X.shape[0], X.shape[1] + (X.shape[1] & 1), dtype=torch.float64, device="cuda")
         Xp[:, :X.shape[1]] = X
         X = Xp[:, :X.shape[1]]
     P = X.shape[0]
