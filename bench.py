@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--n", type=int, default=N_MERGE)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-eigh", action="store_true")
     return ap.parse_args()
 
 
@@ -181,6 +182,59 @@ def measure_dgemm_peak(torch):
     e1.record()
     torch.cuda.synchronize()
     return 2 * n ** 3 / (e0.elapsed_time(e1) / 4 * 1e-3) / 1e12
+
+
+def eigh_lines():
+    """Full tridiagonal eigendecompositions (BASELINE configs 1-3) on the GPU: wall-s + accuracy.
+
+    CPU reference wall-s for the same configs (survey container, 8 cores) is in BASELINE.md:
+    1.32 s / 22.05 s / 124.5 s.
+    """
+    import torch
+
+    import paper_1510_04591_b200 as hb
+    out = {}
+    cases = [
+        ("cfg1_uniform_N2000", hb.gen_uniform(2000, 0),
+         hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13), None),
+        ("cfg2_toeplitz_N10000_adc2", hb.gen_toeplitz(10000),
+         hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13),
+         np.sort(2 + 2 * np.cos(np.arange(1, 10001) * np.pi / 10001))),
+        ("cfg3_kac_N20000", hb.gen_kac(20000), hb.SolverConfig(rank_eps=1e-13),
+         -(20000 - 1) + 2.0 * np.arange(20000)),
+    ]
+    for name, T, cfg, exact in cases:
+        hb.adc_solve(T, cfg)   # warm-up (allocator, tree buffers)
+        best = None
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = hb.adc_solve(T, cfg)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        n = T.n
+        Q = res.Q
+        a = torch.as_tensor(T.a, device="cuda")
+        b = torch.as_tensor(T.b, device="cuda")
+        TQ = a[:, None] * Q
+        TQ[:-1] += b[:, None] * Q[1:]
+        TQ[1:] += b[:, None] * Q[:-1]
+        resid = float((TQ - Q * torch.as_tensor(res.lam, device="cuda")[None, :]).abs().max())
+        del TQ
+        G = Q.T @ Q
+        G.diagonal().sub_(1.0)
+        orth = float(G.abs().max()) / n
+        del G
+        rec = {"wall_s": best, "merges": len(res.merges),
+               "hss_merges": int(sum(m.used_hss for m in res.merges)),
+               "orthogonality": orth, "residual": resid / (n * T.norm_max())}
+        if exact is not None:
+            rec["eig_err_over_normT"] = float(np.abs(res.lam - exact).max()) / T.norm_max()
+        out[name] = rec
+        del res, Q
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_ours(args):
@@ -340,6 +394,8 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clocks,
         }
+        if world == 1 and not args.no_eigh:
+            line["eigh"] = eigh_lines()
         if not args.no_cpu and world == 1:
             tf, dt, fl, thr = cpu_merge_flops_per_s(CPU_SAMPLE_N)
             line["cpu_baseline"] = {
