@@ -350,11 +350,16 @@ def run_ours(args):
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(nst):
-            Xd.copy_(hQ, non_blocking=True)
             dd = hd.to("cuda", non_blocking=True)
             du = hu.to("cuda", non_blocking=True)
-            step(Xd, out, dd, du)
-            hOut.copy_(out, non_blocking=True)
+            if world == 1:
+                # public streaming API: Q_old rows land in chunks while the factors are built,
+                # Q_new rows go back while later chunks are multiplied
+                pipe.run(dd, du, rho, Xd, seed=[SEED, 0], out=out, host_io=(hQ, hOut))
+            else:
+                Xd.copy_(hQ, non_blocking=True)
+                step(Xd, out, dd, du)
+                hOut.copy_(out, non_blocking=True)
         f1.record()
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1) / nst

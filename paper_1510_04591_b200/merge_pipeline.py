@@ -108,12 +108,33 @@ class MergePipeline:
     def _events(self, n):
         return [torch.cuda.Event(enable_timing=True) for _ in range(n)]
 
-    def run(self, d, z, rho, X, seed, out=None):
-        """One merge: returns a dict of phase times (ms), flops and decisions."""
+    def run(self, d, z, rho, X, seed, out=None, host_io=None, chunks=8):
+        """One merge: returns a dict of phase times (ms), flops and decisions.
+
+        host_io=(X_host, out_host): Q_old is streamed from pinned host memory into X in
+        row chunks while the roots / sample / tree are computed, each chunk is multiplied
+        as soon as it has landed and its rows of Q_new are copied back to out_host while
+        the next chunk is multiplied (copy engines overlap the DMMA work).
+        """
         lib, k, cfg = self.lib, self.k, self.cfg
         s = nat.stream_ptr()
         ev = self._events(7)
         ev[0].record()
+        P = X.shape[0]
+        bounds = None
+        if host_io is not None:
+            Xh, Oh = host_io
+            if not hasattr(self, "_h2d"):
+                self._h2d, self._d2h = torch.cuda.Stream(), torch.cuda.Stream()
+            bounds = [(P * i // chunks, P * (i + 1) // chunks) for i in range(chunks)]
+            ev_in = []
+            self._h2d.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(self._h2d):
+                for r0, r1 in bounds:
+                    X[r0:r1].copy_(Xh[r0:r1], non_blocking=True)
+                    e = torch.cuda.Event()
+                    e.record(self._h2d)
+                    ev_in.append(e)
         if self.device_rng:
             # the whole k x MAX_W prefix of the sample stream (the (k, w) block is its first
             # k*w values for every w), drawn before w is known; tail records read back later
@@ -204,16 +225,31 @@ class MergePipeline:
             out = torch.empty(X.shape[0], k, dtype=torch.float64, device="cuda")
         ev_m0 = torch.cuda.Event(enable_timing=True)
         if tree is not None and not tree.flagged:
-            need = int(lib.hsseig_matmul_work_doubles(X.shape[0], ctypes.byref(tree.ct)))
+            rows_max = P if bounds is None else max(r1 - r0 for r0, r1 in bounds)
+            need = int(lib.hsseig_matmul_work_doubles(rows_max, ctypes.byref(tree.ct)))
             if self._mwork is None or self._mwork.numel() < need:
                 self._mwork = None
                 torch.cuda.empty_cache()
                 self._mwork = torch.empty(need, dtype=torch.float64, device="cuda")
             ev_m0.record()
-            nat.check(lib.hsseig_hss_matmul_right(nat.ptr(X), X.stride(0), X.shape[0],
-                                                  ctypes.byref(tree.ct), nat.ptr(out),
-                                                  out.stride(0), nat.ptr(self._mwork), s),
-                      "hss_matmul_right")
+            if bounds is None:
+                nat.check(lib.hsseig_hss_matmul_right(nat.ptr(X), X.stride(0), X.shape[0],
+                                                      ctypes.byref(tree.ct), nat.ptr(out),
+                                                      out.stride(0), nat.ptr(self._mwork), s),
+                          "hss_matmul_right")
+            else:
+                cur = torch.cuda.current_stream()
+                for (r0, r1), e in zip(bounds, ev_in):
+                    cur.wait_event(e)
+                    nat.check(lib.hsseig_hss_matmul_right(nat.ptr(X[r0:r1]), X.stride(0), r1 - r0,
+                                                          ctypes.byref(tree.ct), nat.ptr(out[r0:r1]),
+                                                          out.stride(0), nat.ptr(self._mwork), s),
+                              "hss_matmul_right")
+                    done = torch.cuda.Event()
+                    done.record(cur)
+                    self._d2h.wait_event(done)
+                    with torch.cuda.stream(self._d2h):
+                        Oh[r0:r1].copy_(out[r0:r1], non_blocking=True)
             ev[6].record()
             info["used_hss"] = True
             info["r_used"] = tree.r_used
@@ -221,12 +257,21 @@ class MergePipeline:
             fl_mult_full = mult_flops(tree, k)
             fl_dense = 0
         else:
+            if bounds is not None:
+                for e in ev_in:
+                    torch.cuda.current_stream().wait_event(e)
             ev_m0.record()
             C.right_multiply_into(X, out=out)
             ev[6].record()
+            if bounds is not None:
+                self._d2h.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(self._d2h):
+                    Oh.copy_(out, non_blocking=True)
             info["fell_back"] = use_hss
             fl_mult_local = fl_mult_full = 0
             fl_dense = cauchy_eval_flops(k * k) + gemm_flops(k, k, k)
+        if bounds is not None:
+            torch.cuda.current_stream().wait_stream(self._d2h)
         torch.cuda.synchronize()
         ms = {"secular": ev[0].elapsed_time(ev[1]),
               "loewner_normalizers": ev[1].elapsed_time(ev[2]),

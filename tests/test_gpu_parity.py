@@ -386,3 +386,22 @@ def test_adc_solve_kac_closed_form():
     res = hb.adc_solve(T, hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13))
     ref = -(n - 1) + 2.0 * np.arange(n)
     assert np.abs(res.lam - ref).max() <= 1e-12 * T.norm_max()
+
+
+def test_pipeline_streamed_host_io_matches_device_run():
+    from paper_1510_04591_b200.merge_pipeline import MergePipeline
+    n = 4096
+    d, u, rho = config4_system(n, 8)
+    cfg = hb.SolverConfig(leaf_size=128, hss_threshold=512, rank_eps=1e-13)
+    pipe = MergePipeline(n, cfg, rows=1000)
+    X = torch.randn(1000, n, dtype=torch.float64, device="cuda")
+    dd, uu = torch.as_tensor(d, device="cuda"), torch.as_tensor(u, device="cuda")
+    out = torch.empty_like(X)
+    pipe.run(dd, uu, rho, X, seed=[0, 0], out=out)
+    Xh = X.cpu().pin_memory()
+    Oh = torch.empty_like(Xh).pin_memory()
+    Xd = torch.empty_like(X)
+    out2 = torch.empty_like(X)
+    info = pipe.run(dd, uu, rho, Xd, seed=[0, 0], out=out2, host_io=(Xh, Oh), chunks=3)
+    assert info["used_hss"]
+    assert torch.equal(Oh, out.cpu())
