@@ -180,6 +180,16 @@ int hsseig_tree_layout(hsseig_tree *tree, const int32_t *bounds_h, int32_t n_lea
 int hsseig_hss_build_rand(const hsseig_gen *gen, const double *omega, int64_t ldom,
                           const double *Y, const double *Z, int64_t ldy, double id_tol,
                           hsseig_tree *tree, hsseig_status *status, void *stream);
+/*
+ * Multi-GPU form: levels lev_from (deepest) .. lev_to only, and at every level only the
+ * node positions of part `part` of `nparts` (power of two): each rank builds its own
+ * subtrees below level log2(nparts); after the node slots are all-gathered the upper
+ * levels are built (nparts = 1) on every rank.  lev_to = 0 also forms the root blocks.
+ */
+int hsseig_hss_build_rand_levels(const hsseig_gen *gen, const double *omega, int64_t ldom,
+                                 const double *Y, const double *Z, int64_t ldy, double id_tol,
+                                 hsseig_tree *tree, hsseig_status *status, int lev_from,
+                                 int lev_to, int part, int nparts, void *stream);
 
 /*
  * (a12) Structured product out = X @ H (Algorithm 3; pkg/src/hsseig/hss.py:309-361).

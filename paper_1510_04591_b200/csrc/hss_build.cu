@@ -57,9 +57,9 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
                                                         int64_t ldom,
                                                         const double* __restrict__ Y,
                                                         const double* __restrict__ Z,
-                                                        int64_t ldy) {
+                                                        int64_t ldy, int j0) {
   extern __shared__ __align__(16) double sm[];
-  const int j = blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  const int j = j0 + blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
   const int node = T.lnodes[(1 << T.depth) - 1 + j];
   const int lo = T.lo[node], m = T.hi[node] - lo, w = T.w;
   constexpr int RA = 16;
@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
 // skeleton blocks of the children of every node at one level (hss.py:270-271, 299-301):
 //   B_left = C(rows_sel(left), cols_sel(right)),  B_right = C(rows_sel(right), cols_sel(left))
 // ---------------------------------------------------------------------------
-__global__ void genB_kernel(CauchyGen g, TreeDev T, int level) {
-  const int j = blockIdx.x, which = blockIdx.y, tid = threadIdx.x;
+__global__ void genB_kernel(CauchyGen g, TreeDev T, int level, int j0) {
+  const int j = j0 + blockIdx.x, which = blockIdx.y, tid = threadIdx.x;
   const int node = T.lnodes[(1 << level) - 1 + j];
   const int a = T.left[node], b = T.right[node];
   const int me = which == 0 ? a : b, sib = which == 0 ? b : a;
@@ -124,12 +124,12 @@ __global__ void genB_kernel(CauchyGen g, TreeDev T, int level) {
 //   Phi   = [ psel_a - B_a ycomp_b ; psel_b - B_b ycomp_a ]
 //   Theta = [ tsel_a - B_b^T zcomp_b ; tsel_b - B_a^T zcomp_a ]
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level) {
+__global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level, int j0) {
   // one CTA per (node, side, half): rows [off, off + nrow) of Phi (side 0) or Theta (side 1).
   // B block and sibling compression are staged in shared memory; every thread carries 4
   // independent output columns so the contraction is not latency bound.
   extern __shared__ __align__(16) double fs[];
-  const int j = blockIdx.x, side = blockIdx.y, half = blockIdx.z, tid = threadIdx.x;
+  const int j = j0 + blockIdx.x, side = blockIdx.y, half = blockIdx.z, tid = threadIdx.x;
   const int node = T.lnodes[(1 << level) - 1 + j];
   const int a = T.left[node], b = T.right[node], w = T.w, ws = T.ws;
   const int me = half == 0 ? a : b, sib = half == 0 ? b : a;
@@ -196,9 +196,9 @@ __device__ __forceinline__ double lapy2(double x, double y) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double tol,
                                                  const double* __restrict__ om, int64_t ldom,
-                                                 hsseig_status* st, int fused_form) {
+                                                 hsseig_status* st, int j0) {
   extern __shared__ __align__(16) double sm[];
-  const int j = blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  const int j = j0 + blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5, nthr = blockDim.x;
   const int node = T.lnodes[(1 << level) - 1 + j];
   const bool leaf = T.left[node] < 0;
@@ -219,53 +219,7 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
   __shared__ double s_tau, s_nf, s_resid;
   __shared__ int s_r, s_sat;
 
-  if (fused_form && !leaf) {
-    // inner level formation (hss.py:272-277) straight into shared memory:
-    //   Phi   = [ psel_a - B_a ycomp_b ; psel_b - B_b ycomp_a ]
-    //   Theta = [ tsel_a - B_b^T zcomp_b ; tsel_b - B_a^T zcomp_a ]
-    // the sibling compression is staged in smem; M also goes to global for the
-    // selected-row output below
-    double* sC = reinterpret_cast<double*>(piv + 2 * T.pmax + 2);
-    sC = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sC) + 15) & ~(uintptr_t)15);
-    const int a = T.left[node], b = T.right[node];
-    const int na = side == 0 ? T.rU[a] : T.rV[a];
-    for (int half = 0; half < 2; ++half) {
-      const int me = half == 0 ? a : b, sib = half == 0 ? b : a;
-      const int nrow = half == 0 ? na : p - na, off = half == 0 ? 0 : na;
-      const int nk = side == 0 ? T.rV[sib] : T.rU[sib];
-      const double* comp = (side == 0 ? T.ycomp : T.zcomp) + slot_ww(T, sib);
-      const double* sel = (side == 0 ? T.psel : T.tsel) + slot_ww(T, me);
-      const double* Bb = T.B + slot_ww(T, side == 0 ? me : sib);
-      __syncthreads();
-      for (int e = tid; e < nk * w; e += nthr) {
-        const int t = e / w, c = e % w;
-        sC[e] = comp[(size_t)t * ws + c];
-      }
-      __syncthreads();
-      for (int e = tid; e < nrow * w; e += nthr) {
-        const int row = e / w, c = e % w;
-        double s0 = 0.0, s1 = 0.0;
-        int t = 0;
-        if (side == 0) {
-          const double* br = Bb + (size_t)row * ws;
-          for (; t + 1 < nk; t += 2) {
-            s0 = fma(__ldg(br + t), sC[t * w + c], s0);
-            s1 = fma(__ldg(br + t + 1), sC[(t + 1) * w + c], s1);
-          }
-          if (t < nk) s0 = fma(__ldg(br + t), sC[t * w + c], s0);
-        } else {
-          for (; t + 1 < nk; t += 2) {
-            s0 = fma(__ldg(Bb + (size_t)t * ws + row), sC[t * w + c], s0);
-            s1 = fma(__ldg(Bb + (size_t)(t + 1) * ws + row), sC[(t + 1) * w + c], s1);
-          }
-          if (t < nk) s0 = fma(__ldg(Bb + (size_t)t * ws + row), sC[t * w + c], s0);
-        }
-        const double val = sel[(size_t)row * ws + c] - (s0 + s1);
-        sA[(off + row) * SW + c] = val;
-        Mg[(size_t)(off + row) * ws + c] = val;
-      }
-    }
-  } else {
+  {
     for (int e = tid; e < p * w; e += nthr) {
       int row = e / w, c = e % w;
       sA[row * SW + c] = Mg[(size_t)row * ws + c];
@@ -686,12 +640,17 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
   return HSSEIG_OK;
 }
 
-extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega, int64_t ldom,
-                                     const double* Y, const double* Z, int64_t ldy, double id_tol,
-                                     hsseig_tree* tree, hsseig_status* st, void* stream) {
+// Levels lev_from (deepest) .. lev_to of the construction, restricted at every level to
+// the node positions of part `part` of `nparts` (positions are split evenly, so a part is
+// the subtree set under level log2(nparts)); the root's skeleton blocks when lev_to == 0.
+static int build_levels(const hsseig_gen* gen, const double* omega, int64_t ldom, const double* Y,
+                        const double* Z, int64_t ldy, double id_tol, hsseig_tree* tree,
+                        hsseig_status* st, int lev_from, int lev_to, int part, int nparts,
+                        cudaStream_t s) {
   if (!gen || !tree || !omega || !Y || !Z || !st || gen->k != tree->k) HSS_ARG_FAIL();
   if (tree->w > tree->mmax || tree->w > 128) HSS_ARG_FAIL();
-  cudaStream_t s = (cudaStream_t)stream;
+  if (nparts < 1 || (nparts & (nparts - 1)) || part < 0 || part >= nparts) HSS_ARG_FAIL();
+  if (lev_from > tree->depth || lev_to < 0 || lev_to > lev_from + 1) HSS_ARG_FAIL();
   CauchyGen g;
   g.d = gen->d; g.dnext = gen->dnext; g.gam = gen->gamma; g.mu = gen->mu; g.zhat = gen->zhat;
   g.v = gen->v; g.k = gen->k;
@@ -700,40 +659,55 @@ extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega,
   if (T.pmax > 4096) HSS_ARG_FAIL();
   const size_t smem_id = sizeof(double) * ((size_t)T.pmax * (T.w | 1) + 2 * T.pmax + T.w + 1 + 32) +
                          sizeof(int) * 2 * T.pmax + 64;
-  // fused inner formation needs room for one sibling compression (w x w)
-  const size_t smem_fused = smem_id + sizeof(double) * ((size_t)T.w * T.w + 4);
-  static const int fuse_pref = getenv("HSSEIG_FUSED_FORM") ? atoi(getenv("HSSEIG_FUSED_FORM")) : 0;
   const size_t smem_form = sizeof(double) * ((size_t)T.w * ((T.w | 1) + T.w) + 8);
+  if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024 || smem_form > 227 * 1024) HSS_ARG_FAIL();
   cudaFuncSetAttribute(inner_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_form);
-  const int fused = (fuse_pref && smem_fused <= 227 * 1024) ? 1 : 0;
-  if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024) HSS_ARG_FAIL();
   cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);
-  cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(fused ? smem_fused : smem_id));
-  // zero the factor slots once; the ID kernels then write only their data regions
-  const size_t nn = (size_t)(2 * T.n_leaves - 1);
-  if (cudaMemsetAsync(T.U, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess ||
-      cudaMemsetAsync(T.V, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess ||
-      cudaMemsetAsync(T.Vt, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess)
-    return HSSEIG_ERR_CUDA;
-  for (int lev = T.depth; lev >= 1; --lev) {
-    dim3 grid(1u << lev, 2);
+  cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_id);
+  if (lev_from == T.depth) {
+    // zero the factor slots once; the ID kernels then write only their data regions
+    const size_t nn = (size_t)(2 * T.n_leaves - 1);
+    if (cudaMemsetAsync(T.U, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess ||
+        cudaMemsetAsync(T.V, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess ||
+        cudaMemsetAsync(T.Vt, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess)
+      return HSSEIG_ERR_CUDA;
+  }
+  for (int lev = lev_from; lev >= lev_to && lev >= 1; --lev) {
+    const int npos = 1 << lev;
+    if (npos % nparts) HSS_ARG_FAIL();
+    const int cnt = npos / nparts, j0 = part * cnt;
+    dim3 grid(cnt, 2);
     if (lev == T.depth) {
-      leaf_form_kernel<<<grid, 256, smem_leaf, s>>>(g, T, omega, ldom, Y, Z, ldy);
+      leaf_form_kernel<<<grid, 256, smem_leaf, s>>>(g, T, omega, ldom, Y, Z, ldy, j0);
     } else {
-      genB_kernel<<<grid, 256, 0, s>>>(g, T, lev);
-      if (!fused) {
-        HSS_CHECK_LAUNCH();
-        inner_form_kernel<<<dim3(1u << lev, 2, 2), 256, smem_form, s>>>(T, lev);
-      }
+      genB_kernel<<<grid, 256, 0, s>>>(g, T, lev, j0);
+      HSS_CHECK_LAUNCH();
+      inner_form_kernel<<<dim3(cnt, 2, 2), 256, smem_form, s>>>(T, lev, j0);
     }
     HSS_CHECK_LAUNCH();
-    const int fuse_here = lev == T.depth ? 0 : fused;
-    id_kernel<<<grid, 256, fuse_here ? smem_fused : smem_id, s>>>(T, lev, id_tol, omega, ldom, st,
-                                                                 fuse_here);
+    id_kernel<<<grid, 256, smem_id, s>>>(T, lev, id_tol, omega, ldom, st, j0);
     HSS_CHECK_LAUNCH();
   }
-  genB_kernel<<<dim3(1, 2), 256, 0, s>>>(g, T, 0);
-  HSS_CHECK_LAUNCH();
+  if (lev_to == 0) {
+    genB_kernel<<<dim3(1, 2), 256, 0, s>>>(g, T, 0, 0);
+    HSS_CHECK_LAUNCH();
+  }
   return HSSEIG_OK;
+}
+
+extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega, int64_t ldom,
+                                     const double* Y, const double* Z, int64_t ldy, double id_tol,
+                                     hsseig_tree* tree, hsseig_status* st, void* stream) {
+  if (!tree) HSS_ARG_FAIL();
+  return build_levels(gen, omega, ldom, Y, Z, ldy, id_tol, tree, st, tree->depth, 0, 0, 1,
+                      (cudaStream_t)stream);
+}
+
+extern "C" int hsseig_hss_build_rand_levels(const hsseig_gen* gen, const double* omega,
+                                            int64_t ldom, const double* Y, const double* Z,
+                                            int64_t ldy, double id_tol, hsseig_tree* tree,
+                                            hsseig_status* st, int lev_from, int lev_to, int part,
+                                            int nparts, void* stream) {
+  return build_levels(gen, omega, ldom, Y, Z, ldy, id_tol, tree, st, lev_from, lev_to, part,
+                      nparts, (cudaStream_t)stream);
 }
