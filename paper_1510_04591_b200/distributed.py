@@ -107,7 +107,7 @@ class ShardedMerge:
                     Y_l, Z_l = ops.sample_part(gen, om, w, lo, hi)
                     Y = gather_rows(Y_l, c, k, self.group)
                     Z = gather_rows(Z_l, c, k, self.group)
-                    tree = ops.build(gen, part, w, om, Y, Z)
+                    tree = ops.build(gen, part, w, om, Y, Z, self.group)
         if tree is not None and not ops.flagged(tree):
             info["used_hss"] = True
             info["r_used"] = ops.r_used(tree)
@@ -117,6 +117,52 @@ class ShardedMerge:
             out = ops.dense(X, gen)
         info["tree"] = tree
         return lam, out, info
+
+
+def subtree_layout(depth, s_lev):
+    """Postorder node-id ranges and leaf ranges of the 2^s_lev subtrees rooted at level s_lev."""
+    size = (1 << (depth - s_lev + 1)) - 1
+    blocks, leaves = [], []
+
+    def rec(level, pos, first):
+        # first = postorder id of the first node of the subtree rooted at (level, pos)
+        if level == s_lev:
+            blocks.append((first, first + size))
+            nl = 1 << (depth - s_lev)
+            leaves.append((pos * nl, (pos + 1) * nl))
+            return first + size
+        nxt = rec(level + 1, 2 * pos, first)
+        nxt = rec(level + 1, 2 * pos + 1, nxt)
+        return nxt + 1
+
+    rec(0, 0, 0)
+    return blocks, leaves
+
+
+def gather_subtrees(tree, s_lev, group=None):
+    """All-gather the node slots each rank built for its subtree (contiguous postorder
+    blocks; D by leaf) so every rank holds the full tree below level s_lev."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    ct = tree.ct
+    depth, ws, pmax, dld = ct.depth, ct.ws, ct.pmax, ct.dld
+    blocks, leaves = subtree_layout(depth, s_lev)
+    per_node = {"rU": 4, "rV": 4, "flags": 8, "rres": 8, "cres": 8, "rsel": 4 * ws, "csel": 4 * ws,
+                "rloc": 4 * ws, "cloc": 4 * ws, "U": 8 * pmax * ws, "V": 8 * pmax * ws,
+                "Vt": 8 * ws * pmax, "B": 8 * ws * ws, "psel": 8 * ws * ws, "tsel": 8 * ws * ws,
+                "ycomp": 8 * ws * ws, "zcomp": 8 * ws * ws}
+    base = tree.mem.data_ptr()
+    regions = [(name, nb, blocks) for name, nb in per_node.items()]
+    regions.append(("D", 8 * (dld + 2) * dld, leaves))
+    for name, nb, rng in regions:
+        off = getattr(ct, name) - base
+        lo, hi = rng[rank]
+        mine = tree.mem[off + lo * nb: off + hi * nb]
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine.contiguous(), group=group)
+        for r, (a, b) in enumerate(rng):
+            if r != rank:
+                tree.mem[off + a * nb: off + b * nb].copy_(parts[r])
 
 
 class GpuOps:
@@ -203,7 +249,9 @@ class GpuOps:
                                                      self._s()), "cauchy_sample_part")
         return Y, Z
 
-    def build(self, gen, part, w, om, Y, Z):
+    def build(self, gen, part, w, om, Y, Z, group=None):
+        """Construction; with several ranks each builds its subtrees below level log2(world),
+        the subtree slots are all-gathered and the upper levels are built on every rank."""
         from .hss import HssTree, finish_construct
         from .secular import Status
         nat = self.nat
@@ -213,9 +261,20 @@ class GpuOps:
         tree = self._trees[key]
         tree._ranks = None
         st = Status(self.k)
-        nat.check(self.lib.hsseig_hss_build_rand(gen.gen, nat.ptr(om), om.shape[1], nat.ptr(Y),
-                                                 nat.ptr(Z), Y.shape[1], 1e-15, ctypes.byref(tree.ct),
-                                                 nat.ptr(st.t), self._s()), "hss_build_rand")
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        args = (gen.gen, nat.ptr(om), om.shape[1], nat.ptr(Y), nat.ptr(Z), Y.shape[1], 1e-15,
+                ctypes.byref(tree.ct), nat.ptr(st.t))
+        depth = tree.ct.depth
+        if world > 1 and (1 << depth) >= world and (world & (world - 1)) == 0:
+            s_lev = world.bit_length() - 1
+            nat.check(self.lib.hsseig_hss_build_rand_levels(*args, depth, s_lev, rank, world,
+                                                            self._s()), "build_levels")
+            gather_subtrees(tree, s_lev, group)
+            nat.check(self.lib.hsseig_hss_build_rand_levels(*args, s_lev - 1, 0, 0, 1, self._s()),
+                      "build_levels")
+        else:
+            nat.check(self.lib.hsseig_hss_build_rand(*args, self._s()), "hss_build_rand")
         tree._status = st
         finish_construct(tree)
         return tree

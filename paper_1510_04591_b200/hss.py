@@ -357,7 +357,7 @@ def finish_construct(tree, flops=None):
             tree.flags.append((idx, "row", float(rr[idx])))
         if fl[idx, 1]:
             tree.flags.append((idx, "col", float(cr[idx])))
-    tree.flagged = bool(v[4] > 0)
+    tree.flagged = bool(fl.any())        # per-node saturation flags (also right after a gather)
     tree._ranks = None
     rU, rV = tree.ranks()
     mask = np.ones(nn, dtype=bool)

@@ -50,7 +50,7 @@ class NumpyOps:
         return (torch.as_tensor(G.times(om.numpy())[lo:hi]),
                 torch.as_tensor(G.t_times(om.numpy())[lo:hi]))
 
-    def build(self, G, part, w, om, Y, Z):
+    def build(self, G, part, w, om, Y, Z, group=None):
         # the gathered samples must be the full products
         assert np.allclose(Y.numpy(), G.times(om.numpy()), rtol=0, atol=1e-13)
         assert np.allclose(Z.numpy(), G.t_times(om.numpy()), rtol=0, atol=1e-13)
@@ -121,3 +121,19 @@ def test_shard_ranges_cover_exactly():
             got = [shard_range(k, r, world)[:2] for r in range(world)]
             assert got[0][0] == 0 and got[-1][1] == k
             assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
+
+
+def test_subtree_layout_matches_postorder():
+    from paper_1510_04591_b200.distributed import subtree_layout
+    from oracle.hss_oracle import postorder_nodes
+    for depth in (1, 2, 3, 5):
+        ranges = [(i, i + 1) for i in range(1 << depth)]
+        nodes, root = postorder_nodes(ranges)
+        for s_lev in range(0, depth + 1):
+            blocks, leaves = subtree_layout(depth, s_lev)
+            assert len(blocks) == 1 << s_lev
+            for (a, b), (la, lb) in zip(blocks, leaves):
+                sub = nodes[b - 1]          # subtree root is last in its postorder block
+                assert sub.level == s_lev
+                assert all(sub.lo <= nodes[i].lo and nodes[i].hi <= sub.hi for i in range(a, b))
+                assert (sub.lo, sub.hi) == (la, lb)

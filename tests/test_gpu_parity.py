@@ -405,3 +405,40 @@ def test_pipeline_streamed_host_io_matches_device_run():
     info = pipe.run(dd, uu, rho, Xd, seed=[0, 0], out=out2, host_io=(Xh, Oh), chunks=3)
     assert info["used_hss"]
     assert torch.equal(Oh, out.cpu())
+
+
+@pytest.mark.parametrize("nparts", [2, 4])
+def test_partitioned_construction_equals_single_build(nparts):
+    # the multi-GPU construction: every part builds its subtrees below level log2(nparts),
+    # then the upper levels; run all parts on one device and compare with the single build
+    import ctypes
+    from paper_1510_04591_b200.hss import HssTree, finish_construct, sample_omega
+    from paper_1510_04591_b200.secular import Status
+    n = 4096
+    d, u, rho = config4_system(n, 6)
+    sys_ = hb.RankOneSystem(d, u, rho)
+    sol = hb.solve_secular(sys_)
+    hb.recompute_weights(sys_.d, sol, sys_.z, rho=rho)
+    C = hb.CauchyEvecMatrix.from_secular(sys_, sol)
+    part = hb.build_partition(n, 128, C.d, C.gamma, C.mu)
+    r = min(hb.estimate_rank(part, C.d, C.gamma, C.mu, 1e-13), part.min_leaf - 10)
+    H1 = hb.rand_hss_construct(C, part, r, p=10, seed=[0, 0])
+    w = r + 10
+    om = torch.as_tensor(sample_omega(n, w, [0, 0]), device="cuda")
+    Y, Z = C.sample(om)
+    H2 = HssTree(part, w)
+    st = Status(n)
+    lib = _native.load()
+    args = (C.gen, _native.ptr(om), om.stride(0), _native.ptr(Y), _native.ptr(Z), Y.stride(0),
+            1e-15, ctypes.byref(H2.ct), _native.ptr(st.t))
+    s_lev = nparts.bit_length() - 1
+    for p_ in range(nparts):
+        _native.check(lib.hsseig_hss_build_rand_levels(*args, H2.ct.depth, s_lev, p_, nparts,
+                                                       _native.stream_ptr()), "levels")
+    _native.check(lib.hsseig_hss_build_rand_levels(*args, s_lev - 1, 0, 0, 1, _native.stream_ptr()),
+                  "levels")
+    H2._status = st
+    finish_construct(H2)
+    assert (H1.ranks()[0] == H2.ranks()[0]).all() and (H1.ranks()[1] == H2.ranks()[1]).all()
+    X = torch.randn(200, n, dtype=torch.float64, device="cuda")
+    assert torch.equal(hb.hss_matmul_right(X, H1), hb.hss_matmul_right(X, H2))
