@@ -180,6 +180,9 @@ int hsseig_tree_layout(hsseig_tree *tree, const int32_t *bounds_h, int32_t n_lea
 int hsseig_hss_build_rand(const hsseig_gen *gen, const double *omega, int64_t ldom,
                           const double *Y, const double *Z, int64_t ldy, double id_tol,
                           hsseig_tree *tree, hsseig_status *status, void *stream);
+/* Zero the tree's factor slots (done by hsseig_hss_build_rand; call once before the
+ * per-level form below). */
+int hsseig_tree_clear(hsseig_tree *tree, void *stream);
 /*
  * Multi-GPU form: levels lev_from (deepest) .. lev_to only, and at every level only the
  * node positions of part `part` of `nparts` (power of two): each rank builds its own

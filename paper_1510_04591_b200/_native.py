@@ -74,6 +74,7 @@ _SIGS = {
                                           c_i32, c_vp, c_vp]),
     "hsseig_hss_build_rand": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_vp, c_vp, c_i64,
                                              c_dbl, ctypes.POINTER(Tree), c_vp, c_vp]),
+    "hsseig_tree_clear": (ctypes.c_int, [ctypes.POINTER(Tree), c_vp]),
     "hsseig_hss_build_rand_levels": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_vp, c_vp,
                                                     c_i64, c_dbl, ctypes.POINTER(Tree), c_vp,
                                                     ctypes.c_int, ctypes.c_int, ctypes.c_int,

@@ -664,14 +664,6 @@ static int build_levels(const hsseig_gen* gen, const double* omega, int64_t ldom
   cudaFuncSetAttribute(inner_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_form);
   cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);
   cudaFuncSetAttribute(id_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_id);
-  if (lev_from == T.depth) {
-    // zero the factor slots once; the ID kernels then write only their data regions
-    const size_t nn = (size_t)(2 * T.n_leaves - 1);
-    if (cudaMemsetAsync(T.U, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess ||
-        cudaMemsetAsync(T.V, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess ||
-        cudaMemsetAsync(T.Vt, 0, 8 * nn * T.pmax * T.ws, s) != cudaSuccess)
-      return HSSEIG_ERR_CUDA;
-  }
   for (int lev = lev_from; lev >= lev_to && lev >= 1; --lev) {
     const int npos = 1 << lev;
     if (npos % nparts) HSS_ARG_FAIL();
@@ -695,10 +687,24 @@ static int build_levels(const hsseig_gen* gen, const double* omega, int64_t ldom
   return HSSEIG_OK;
 }
 
+extern "C" int hsseig_tree_clear(hsseig_tree* tree, void* stream) {
+  // zero the factor slots; the ID kernels then write only their data regions
+  if (!tree) HSS_ARG_FAIL();
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t nn = (size_t)tree->n_nodes;
+  if (cudaMemsetAsync(tree->U, 0, 8 * nn * tree->pmax * tree->ws, s) != cudaSuccess ||
+      cudaMemsetAsync(tree->V, 0, 8 * nn * tree->pmax * tree->ws, s) != cudaSuccess ||
+      cudaMemsetAsync(tree->Vt, 0, 8 * nn * tree->pmax * tree->ws, s) != cudaSuccess)
+    return HSSEIG_ERR_CUDA;
+  return HSSEIG_OK;
+}
+
 extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega, int64_t ldom,
                                      const double* Y, const double* Z, int64_t ldy, double id_tol,
                                      hsseig_tree* tree, hsseig_status* st, void* stream) {
   if (!tree) HSS_ARG_FAIL();
+  const int rc = hsseig_tree_clear(tree, stream);
+  if (rc) return rc;
   return build_levels(gen, omega, ldom, Y, Z, ldy, id_tol, tree, st, tree->depth, 0, 0, 1,
                       (cudaStream_t)stream);
 }

@@ -268,6 +268,7 @@ class GpuOps:
         depth = tree.ct.depth
         if world > 1 and (1 << depth) >= world and (world & (world - 1)) == 0:
             s_lev = world.bit_length() - 1
+            nat.check(self.lib.hsseig_tree_clear(ctypes.byref(tree.ct), self._s()), "tree_clear")
             nat.check(self.lib.hsseig_hss_build_rand_levels(*args, depth, s_lev, rank, world,
                                                             self._s()), "build_levels")
             gather_subtrees(tree, s_lev, group)

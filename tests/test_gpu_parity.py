@@ -432,6 +432,7 @@ def test_partitioned_construction_equals_single_build(nparts):
     args = (C.gen, _native.ptr(om), om.stride(0), _native.ptr(Y), _native.ptr(Z), Y.stride(0),
             1e-15, ctypes.byref(H2.ct), _native.ptr(st.t))
     s_lev = nparts.bit_length() - 1
+    _native.check(lib.hsseig_tree_clear(ctypes.byref(H2.ct), _native.stream_ptr()), "clear")
     for p_ in range(nparts):
         _native.check(lib.hsseig_hss_build_rand_levels(*args, H2.ct.depth, s_lev, p_, nparts,
                                                        _native.stream_ptr()), "levels")
