@@ -10,6 +10,8 @@
 // the k poles so every pole read (d_j, z_j^2, gamma_j, ...) feeds R roots.  All
 // cross-lane reductions are xor butterflies, which leave bit-identical totals in
 // every lane, so the per-root control flow below is warp-uniform.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hsseig {
@@ -54,8 +56,8 @@ __global__ void square_sum_kernel(const double* __restrict__ z, int64_t k, doubl
   }
 }
 
-template <int R>
-__global__ void __launch_bounds__(256) secular_kernel(
+template <int R, int MINB>
+__global__ void __launch_bounds__(256, MINB) secular_kernel(
     const double* __restrict__ d, const double* __restrict__ z2, const double* __restrict__ sumz2p,
     int64_t k, double rho, int64_t ibeg, int64_t iend, double* __restrict__ lam,
     double* __restrict__ gam, double* __restrict__ mu, int32_t* __restrict__ iters,
@@ -374,10 +376,19 @@ extern "C" int hsseig_secular_part(const double* d, const double* z, int64_t k, 
   double* sum = work + k;
   square_sum_kernel<<<1, 1024, 0, s>>>(z, k, z2, sum);
   HSS_CHECK_LAUNCH();
-  constexpr int R = 4;
-  const int64_t warps = (iend - ibeg + R - 1) / R;
-  const int blocks = (int)((warps + 7) / 8);
-  secular_kernel<R><<<blocks, 256, 0, s>>>(d, z2, sum, k, rho, ibeg, iend, lam, gamma, mu, iters, st);
+  static const int variant = getenv("HSSEIG_SEC_VARIANT") ? atoi(getenv("HSSEIG_SEC_VARIANT")) : 0;
+  auto launch = [&](auto kern, int R) {
+    const int64_t warps = (iend - ibeg + R - 1) / R;
+    const int blocks = (int)((warps + 7) / 8);
+    kern<<<blocks, 256, 0, s>>>(d, z2, sum, k, rho, ibeg, iend, lam, gamma, mu, iters, st);
+  };
+  switch (variant) {
+    case 1: launch(secular_kernel<4, 3>, 4); break;
+    case 2: launch(secular_kernel<2, 4>, 2); break;
+    case 3: launch(secular_kernel<8, 1>, 8); break;
+    case 4: launch(secular_kernel<2, 2>, 2); break;
+    default: launch(secular_kernel<4, 2>, 4); break;
+  }
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
