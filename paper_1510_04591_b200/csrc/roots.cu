@@ -387,6 +387,10 @@ extern "C" int hsseig_secular_part(const double* d, const double* z, int64_t k, 
     case 2: launch(secular_kernel<2, 4>, 2); break;
     case 3: launch(secular_kernel<8, 1>, 8); break;
     case 4: launch(secular_kernel<2, 2>, 2); break;
+    case 5: launch(secular_kernel<2, 3>, 2); break;
+    case 6: launch(secular_kernel<1, 4>, 1); break;
+    case 7: launch(secular_kernel<1, 6>, 1); break;
+    case 8: launch(secular_kernel<3, 3>, 3); break;
     default: launch(secular_kernel<4, 2>, 4); break;
   }
   HSS_CHECK_LAUNCH();
