@@ -137,8 +137,15 @@ class MergePipeline:
                     ev_in.append(e)
         if self.device_rng:
             # the whole k x MAX_W prefix of the sample stream (the (k, w) block is its first
-            # k*w values for every w), drawn before w is known; tail records read back later
-            self.normals.draw(seed, k * MAX_W, self.om_flat)
+            # k*w values for every w), drawn before w is known on a side stream that
+            # overlaps the root solve; tail records read back later
+            if not hasattr(self, "_rng_stream"):
+                self._rng_stream = torch.cuda.Stream()
+            self._rng_stream.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(self._rng_stream):
+                self.normals.draw(seed, k * MAX_W, self.om_flat)
+                self._rng_done = torch.cuda.Event()
+                self._rng_done.record(self._rng_stream)
         else:
             self.host_omega.start(seed)
         self.status.zero_()
@@ -192,6 +199,7 @@ class MergePipeline:
                     om = self.om[:k * ws].view(k, ws)
                     if self.device_rng:
                         try:
+                            torch.cuda.current_stream().wait_event(self._rng_done)
                             self.normals.fixup()
                             om[:, :w].copy_(self.om_flat[:k * w].view(k, w))
                         except RuntimeError:   # unresolved rejection chain: the host draw
