@@ -38,8 +38,9 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
                      int64_t ldp, int kchunk, int nsplit, int tiles, int64_t row0, int64_t row1) {
   // output rows [row0, row1) of Y (or Z); part rows are indexed from row0
   extern __shared__ __align__(128) unsigned char smraw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smraw) + 127) & ~(uintptr_t)127);
+  // 128-byte aligned ring; pointer arithmetic on the __shared__ array keeps the shared
+  // address space (fragment loads compile to LDS, not generic LD)
+  unsigned char* sm = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)T::STAGE_BYTES * T::STAGES);
   uint64_t* empty = full + T::STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -138,7 +139,6 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
   // ---------------- DMMA consumers ----------------
   const int wm = warp / T::WN, wn = warp % T::WN;
   const int gr = lane >> 2, gc = lane & 3;
-  const int jmax = max(0, min(T::NF, (w - wn * T::NF * 8 + 7) / 8));
   uint32_t q = 0;
   double acc[T::MF][T::NF][2];
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
       const double* sA = reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES);
       const double* sB =
           reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES);
-      tmma_chunk<T>(sA, sB, acc, wm, wn, lane, T::BK, jmax);
+      tmma_chunk<T>(sA, sB, acc, wm, wn, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
     }

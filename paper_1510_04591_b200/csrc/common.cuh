@@ -36,6 +36,9 @@ __host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { retur
 
 constexpr double kEps = 2.220446049250313e-16;
 
+// rows of a leaf's D slot: a zero row, the m data rows, zero rows to a whole 16-deep chunk
+__host__ __device__ __forceinline__ int hsseig_drows(int mmax) { return (mmax + 1 + 15) / 16 * 16 + 2; }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -71,10 +71,11 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
   }
   const double* src = side == 0 ? Y : Z;
   double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * T.ws;
-  // D slot: (dld + 2) x dld, row 0 and rows/cols past m are zero, D[a][b] at row a + 1
-  double* Dslot = T.D + (size_t)j * (T.dld + 2) * T.dld;
+  // D slot: drows x dld, row 0 and rows/cols past m are zero, D[a][b] at row a + 1
+  const int drows = hsseig_drows(T.mmax);
+  double* Dslot = T.D + (size_t)j * drows * T.dld;
   if (side == 0) {
-    for (int e = tid; e < (T.dld + 2) * T.dld; e += blockDim.x) {
+    for (int e = tid; e < drows * T.dld; e += blockDim.x) {
       const int a = e / T.dld - 1, b = e % T.dld;
       if (a < 0 || a >= m || b >= m) Dslot[e] = 0.0;
     }
@@ -523,7 +524,8 @@ static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
   TreeCarve c;
   const int64_t nn = 2 * (int64_t)n_leaves - 1;
   const int64_t ws = (w + 15) / 16 * 16;
-  int64_t pmax = std::max<int64_t>(mmax, 2 * (int64_t)w);
+  // slots hold zero rows past their data far enough for whole 16-deep K chunks
+  int64_t pmax = std::max<int64_t>((mmax + 1 + 15) / 16 * 16, 2 * (int64_t)w);
   pmax += (pmax & 1) + 2;
   const int64_t dld = mmax + (mmax & 1);
   int64_t o = 0;
@@ -536,7 +538,7 @@ static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
   c.off_flags = take(4 * 2 * nn);
   c.off_U = take(8 * nn * pmax * ws); c.off_V = take(8 * nn * pmax * ws);
   c.off_Vt = take(8 * nn * ws * pmax);
-  c.off_B = take(8 * nn * ws * ws); c.off_D = take(8 * (int64_t)n_leaves * (dld + 2) * dld);
+  c.off_B = take(8 * nn * ws * ws); c.off_D = take(8 * (int64_t)n_leaves * hsseig_drows(mmax) * dld);
   c.off_rres = take(8 * nn); c.off_cres = take(8 * nn);
   c.off_M = take(8 * 2 * (int64_t)n_leaves * pmax * ws);
   c.off_psel = take(8 * nn * ws * ws); c.off_tsel = take(8 * nn * ws * ws);
@@ -591,7 +593,7 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
   char* base = static_cast<char*>(dev_mem);
   t->k = k; t->n_leaves = n_leaves; t->depth = depth; t->n_nodes = nn; t->w = w;
   t->ws = (w + 15) / 16 * 16;
-  t->pmax = std::max<int32_t>(mmax, 2 * w);
+  t->pmax = std::max<int32_t>((mmax + 1 + 15) / 16 * 16, 2 * w);
   t->pmax += (t->pmax & 1) + 2;
   t->mmax = mmax;
   t->dld = mmax + (mmax & 1);

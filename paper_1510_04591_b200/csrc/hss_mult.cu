@@ -46,8 +46,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
     tma_gemm_kernel(const MapSet* __restrict__ maps, const TJob* __restrict__ jobs, int njobs,
                     int64_t M, int tiles_m) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smraw) + 127) & ~(uintptr_t)127);
+  // 128-byte aligned ring; pointer arithmetic on the __shared__ array keeps the shared
+  // address space (fragment loads compile to LDS, not generic LD)
+  unsigned char* sm = smraw + ((128u - (smem_u32(smraw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)T::STAGE_BYTES * T::STAGES);
   uint64_t* empty = full + T::STAGES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -95,7 +96,6 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
     const TJob jb = jobs[t / tiles_m];
     if (jb.N <= 0) continue;
     const int64_t m0 = (int64_t)(t % tiles_m) * T::BM;
-    const int jmax = max(0, min(T::NF, (jb.N - wn * T::NF * 8 + 7) / 8));
 #pragma unroll
     for (int i = 0; i < T::MF; ++i)
 #pragma unroll
@@ -109,8 +109,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const double* sA = reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES);
         const double* sB =
             reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES);
-        const int kv = min(T::BK, ((K - c * T::BK) + 3) & ~3);
-        tmma_chunk<T>(sA, sB, acc, wm, wn, lane, kv, jmax);
+        tmma_chunk<T>(sA, sB, acc, wm, wn, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[slot]);
       }
@@ -132,7 +131,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 }
 
 struct MultPlan {
-  int32_t depth, n_leaves, ws, pmax, dld;
+  int32_t depth, n_leaves, ws, pmax, dld, mmax;
   const int32_t *lo, *hi, *left, *right, *lnodes, *rU, *rV;
   double* out;
   int64_t ldo;
@@ -204,7 +203,7 @@ __global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs) {
     jb.ldc = p.ldo;
     jb.N = jb.SW = p.hi[node] - lo;
     jb.am[0] = 0; jb.acol[0] = lo - sh; jb.K[0] = p.hi[node] - lo + sh;
-    jb.bm[0] = 7; jb.brow[0] = j * (p.dld + 2) + 1 - sh;
+    jb.bm[0] = 7; jb.brow[0] = j * hsseig_drows(p.mmax) + 1 - sh;
     jb.am[1] = 3; jb.acol[1] = j * ws; jb.K[1] = p.rV[node];
     jb.bm[1] = 6; jb.brow[1] = node * ws;
   }
@@ -371,6 +370,7 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   const int64_t lvl_total = P * (int64_t)ws * (2 * (int64_t)n - 2);
   MultPlan p;
   p.depth = t->depth; p.n_leaves = n; p.ws = ws; p.pmax = t->pmax; p.dld = t->dld;
+  p.mmax = t->mmax;
   p.lo = t->lo; p.hi = t->hi; p.left = t->left; p.right = t->right; p.lnodes = t->level_nodes;
   p.rU = t->rU; p.rV = t->rV;
   p.out = out; p.ldo = ldo; p.P = P;
@@ -393,7 +393,7 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   const Operand Uop{t->U, (uint64_t)nn * t->pmax, (uint64_t)ws, (uint64_t)ws};
   const Operand Bop{t->B, (uint64_t)nn * ws, (uint64_t)ws, (uint64_t)ws};
   const Operand Vtop{t->Vt, (uint64_t)nn * ws, (uint64_t)t->pmax, (uint64_t)t->pmax};
-  const Operand Dop{t->D, (uint64_t)n * (t->dld + 2), (uint64_t)t->dld, (uint64_t)t->dld};
+  const Operand Dop{t->D, (uint64_t)n * hsseig_drows(t->mmax), (uint64_t)t->dld, (uint64_t)t->dld};
   int rc;
   for (int l = t->depth; l >= 1; --l) {
     const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), lvl(p.Gb, l + 1), none, Uop, Bop, Vtop, Dop};

@@ -66,25 +66,26 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// One full BK chunk, branch-free: K tails and padded output columns are exact because the
+// operands beyond K are zero-padded (factor slots, TMA out-of-bounds fill) and the output
+// columns beyond N are never stored as accumulator values.
 template <class T>
 __device__ __forceinline__ void tmma_chunk(const double* __restrict__ sA, const double* __restrict__ sB,
-                                           double (&c)[T::MF][T::NF][2], int wm, int wn, int lane,
-                                           int kv, int jmax) {
+                                           double (&c)[T::MF][T::NF][2], int wm, int wn, int lane) {
   const int gr = lane >> 2, gc = lane & 3;
+  const double* a0 = sA + (wm * T::MF * 8 + gr) * T::SA + gc;
+  const double* b0 = sB + gc * T::SB + wn * T::NF * 8 + gr;
 #pragma unroll
   for (int kk = 0; kk < T::BK; kk += 4) {
-    if (kk >= kv) break;
     double a[T::MF], b[T::NF];
 #pragma unroll
-    for (int i = 0; i < T::MF; ++i) a[i] = sA[(wm * T::MF * 8 + i * 8 + gr) * T::SA + kk + gc];
+    for (int i = 0; i < T::MF; ++i) a[i] = a0[i * 8 * T::SA + kk];
 #pragma unroll
-    for (int j = 0; j < T::NF; ++j) b[j] = sB[(kk + gc) * T::SB + wn * T::NF * 8 + j * 8 + gr];
+    for (int j = 0; j < T::NF; ++j) b[j] = b0[kk * T::SB + j * 8];
 #pragma unroll
-    for (int j = 0; j < T::NF; ++j) {
-      if (j >= jmax) break;
+    for (int j = 0; j < T::NF; ++j)
 #pragma unroll
       for (int i = 0; i < T::MF; ++i) dmma_8x8x4(c[i][j][0], c[i][j][1], a[i], b[j]);
-    }
   }
 }
 

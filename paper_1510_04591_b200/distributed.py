@@ -153,7 +153,8 @@ def gather_subtrees(tree, s_lev, group=None):
                 "ycomp": 8 * ws * ws, "zcomp": 8 * ws * ws}
     base = tree.mem.data_ptr()
     regions = [(name, nb, blocks) for name, nb in per_node.items()]
-    regions.append(("D", 8 * (dld + 2) * dld, leaves))
+    drows = (ct.mmax + 1 + 15) // 16 * 16 + 2
+    regions.append(("D", 8 * drows * dld, leaves))
     for name, nb, rng in regions:
         off = getattr(ct, name) - base
         lo, hi = rng[rank]

@@ -260,11 +260,12 @@ class HssTree:
 
     def leaf_D(self, node):
         mm = self.ct.dld
+        drows = (self.ct.mmax + 1 + 15) // 16 * 16 + 2
         j = self._leaf_pos[node]
-        n = (mm + 2) * mm
+        n = drows * mm
         flat = self._view("D", torch.float64, n, j * n)
         m = self.nodes[node].hi - self.nodes[node].lo
-        return flat.view(mm + 2, mm)[1:m + 1, :m].cpu().numpy().copy()
+        return flat.view(drows, mm)[1:m + 1, :m].cpu().numpy().copy()
 
 
 def _construct_flops(tree, k, w):
