@@ -48,7 +48,7 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
   const int items = tiles * nsplit;
   if (tid == 0) {
     for (int s = 0; s < T::STAGES; ++s) {
-      mbar_init(&full[s], kGenWarps + 1);
+      mbar_init(&full[s], kGenWarps * 32 + 1);   // every generator thread + the TMA arm
       mbar_init(&empty[s], T::CONSUMERS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -129,8 +129,8 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
           tma_load_2d(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES, &omap->m[0], 0,
                       (int)(kbeg + (int64_t)c * T::BK), &full[slot]);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[slot]);
+        // each generator thread releases its own tile writes (mbarrier.arrive is .release)
+        mbar_arrive(&full[slot]);
       }
     }
     return;
