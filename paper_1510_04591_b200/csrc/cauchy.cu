@@ -64,6 +64,7 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
     constexpr int FR = T::BM / RS;               // tile rows per thread
     const int gt = tid - T::CONSUMERS * 32;
     const int vk = gt % T::BK, a0 = gt / T::BK;
+    if (warp == T::CONSUMERS && lane == 0) tmap_acquire(&omap->m[0]);
     uint32_t q = 0;
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
       const int tile = it % tiles, split = it / tiles;
@@ -158,8 +159,7 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
       const double* sB =
           reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES);
       tmma_chunk<T>(sA, sB, acc, wm, wn, lane);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
+      stage_release(&empty[slot], lane);
     }
     const int64_t nrows = row1 - row0;
     double* P = part + (int64_t)split * nrows * ldp;

@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
   if (warp == T::CONSUMERS) {
     // ---------------- TMA producer (one lane) ----------------
     if (lane == 0) {
+      for (int r = 0; r < kMaps; ++r) tmap_acquire(&maps->m[r]);
       uint32_t q = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const TJob jb = jobs[t / tiles_m];
@@ -110,8 +111,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const double* sB =
             reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES);
         tmma_chunk<T>(sA, sB, acc, wm, wn, lane);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
+        stage_release(&empty[slot], lane);
       }
     }
     // epilogue: accumulators for columns < N, zeros in [N, SW)

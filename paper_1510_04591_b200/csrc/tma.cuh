@@ -57,6 +57,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Consumer release of one ring stage.  The stage's next TMA fill (async proxy) must not
+// overtake this warp's fragment reads (generic proxy): ptxas does not make the mbarrier
+// arrive wait for outstanding LDS, so the reads are fenced into the async proxy first.
+__device__ __forceinline__ void stage_release(uint64_t* b, int lane) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) mbar_arrive(b);
+}
+// Tensor maps live in device memory and are rewritten (H2D copy) between launches at the
+// same address; the TMA unit may serve a stale cached descriptor unless the issuing thread
+// acquires the generic-proxy writes into the tensormap proxy first.
+__device__ __forceinline__ void tmap_acquire(const CUtensorMap* map) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(
+                   reinterpret_cast<uint64_t>(map))
+               : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
   asm volatile(
