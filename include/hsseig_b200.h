@@ -158,6 +158,9 @@ typedef struct hsseig_tree {
   double *tsel;   /* n_nodes * ws * ws : selected rows of Theta */
   double *ycomp;  /* n_nodes * ws * ws : V^T Omega compressions */
   double *zcomp;  /* n_nodes * ws * ws : U^T Omega compressions */
+  /* host-side upper bound on the node ranks, set by the caller after reading the ranks
+     back (0 = unknown, w is used); sizes the multiply's output tiles to the ranks */
+  int32_t rmax;
 } hsseig_tree;
 
 /* bytes of device memory hsseig_tree_layout carves for one tree */

@@ -41,7 +41,7 @@ class Tree(ctypes.Structure):
                 ("cloc", c_vp), ("flags", c_vp),
                 ("U", c_vp), ("V", c_vp), ("Vt", c_vp), ("B", c_vp), ("D", c_vp), ("rres", c_vp),
                 ("cres", c_vp), ("dld", c_i32),
-                ("M", c_vp), ("psel", c_vp), ("tsel", c_vp), ("ycomp", c_vp), ("zcomp", c_vp)]
+                ("M", c_vp), ("psel", c_vp), ("tsel", c_vp), ("ycomp", c_vp), ("zcomp", c_vp), ("rmax", c_i32)]
 
 
 # name -> (restype, argtypes)

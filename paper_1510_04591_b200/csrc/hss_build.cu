@@ -598,6 +598,7 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
   t->mmax = mmax;
   t->dld = mmax + (mmax & 1);
   t->root = root;
+  t->rmax = 0;
   for (int l = 0; l <= depth && l < 31; ++l) t->level_off_h[l] = (1 << l) - 1;
   t->lo = reinterpret_cast<int32_t*>(base + c.off_lo);
   t->hi = reinterpret_cast<int32_t*>(base + c.off_hi);

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
         const double* sA = reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES);
         const double* sB =
             reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES);
-        tmma_chunk<T>(sA, sB, acc, wm, wn, lane);
+        tmma_chunk<T>(sA, sB, acc, wm, wn, lane, min(T::BK, (K - c * T::BK + 3) & ~3));
         stage_release(&empty[slot], lane);
       }
     }
@@ -261,10 +261,36 @@ static int tile_choice(const char* var, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
+// Rank-width tiles: 8 consumer warps stacked along M (BM = 128), one warp spans the whole
+// output width in NF 8-column fragments, so N is padded to a multiple of 8 only.
+constexpr int narrow_stages(int nf) {
+  return (200 * 1024) / (128 * 20 * 8 + 16 * (((nf * 8 + 15) / 16) * 16 + 4) * 8) < 8
+             ? (200 * 1024) / (128 * 20 * 8 + 16 * (((nf * 8 + 15) / 16) * 16 + 4) * 8)
+             : 8;
+}
+template <int NF>
+using RankTile = TTile<2, NF, 8, 1, narrow_stages(NF)>;
+
 // narrow outputs (ranks, N <= 112)
 static int launch_narrow(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJob* jobs, int njobs,
                          int64_t M, cudaStream_t s) {
-  static const int variant = tile_choice("HSSEIG_TILE_NARROW", 1);
+  static const int variant = tile_choice("HSSEIG_TILE_NARROW", 3);
+  if (variant == 3) {
+    switch ((n + 7) / 8) {
+      case 1: case 2: case 3: case 4: return launch_tma<RankTile<4>>(ops, dm, jobs, njobs, M, s);
+      case 5: return launch_tma<RankTile<5>>(ops, dm, jobs, njobs, M, s);
+      case 6: return launch_tma<RankTile<6>>(ops, dm, jobs, njobs, M, s);
+      case 7: return launch_tma<RankTile<7>>(ops, dm, jobs, njobs, M, s);
+      case 8: return launch_tma<RankTile<8>>(ops, dm, jobs, njobs, M, s);
+      case 9: return launch_tma<RankTile<9>>(ops, dm, jobs, njobs, M, s);
+      case 10: return launch_tma<RankTile<10>>(ops, dm, jobs, njobs, M, s);
+      case 11: return launch_tma<RankTile<11>>(ops, dm, jobs, njobs, M, s);
+      case 12: return launch_tma<RankTile<12>>(ops, dm, jobs, njobs, M, s);
+      case 13: return launch_tma<RankTile<13>>(ops, dm, jobs, njobs, M, s);
+      case 14: return launch_tma<RankTile<14>>(ops, dm, jobs, njobs, M, s);
+      default: HSS_ARG_FAIL();
+    }
+  }
   if (variant == 2) {   // BM 64, 4-stage ring: two CTAs per SM
     switch ((n + 31) / 32) {
       case 1: case 2: return launch_tma<TTile<4, 2, 2, 4, 4>>(ops, dm, jobs, njobs, M, s);
@@ -395,14 +421,16 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   const Operand Vtop{t->Vt, (uint64_t)nn * ws, (uint64_t)t->pmax, (uint64_t)t->pmax};
   const Operand Dop{t->D, (uint64_t)n * hsseig_drows(t->mmax), (uint64_t)t->dld, (uint64_t)t->dld};
   int rc;
+  // output tiles cover the ranks (host bound rmax when the caller supplied it)
+  const int nr = (t->rmax > 0 && t->rmax < t->w) ? t->rmax : t->w;
   for (int l = t->depth; l >= 1; --l) {
     const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), lvl(p.Gb, l + 1), none, Uop, Bop, Vtop, Dop};
-    if ((rc = launch_narrow(t->w, ops, dmaps + (t->depth - l), jobs + ((1 << l) - 2), 1 << l, P, s)))
+    if ((rc = launch_narrow(nr, ops, dmaps + (t->depth - l), jobs + ((1 << l) - 2), 1 << l, P, s)))
       return rc;
   }
   for (int l = 1; l <= t->depth; ++l) {
     const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), none, lvl(p.Fb, l - 1), Uop, Bop, Vtop, Dop};
-    if ((rc = launch_narrow(t->w, ops, dmaps + t->depth + l - 1, jobs + nup + ((1 << l) - 2), 1 << l,
+    if ((rc = launch_narrow(nr, ops, dmaps + t->depth + l - 1, jobs + nup + ((1 << l) - 2), 1 << l,
                             P, s)))
       return rc;
   }

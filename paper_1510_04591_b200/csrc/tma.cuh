@@ -82,17 +82,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// One full BK chunk, branch-free: K tails and padded output columns are exact because the
-// operands beyond K are zero-padded (factor slots, TMA out-of-bounds fill) and the output
-// columns beyond N are never stored as accumulator values.
+// One BK chunk; kv (warp-uniform, a multiple of 4) is the chunk's valid depth.  Operands
+// are zero-padded past K (factor slots, TMA out-of-bounds fill), so rounding K up to a
+// multiple of 4 is exact; output columns beyond N are computed but never stored.
 template <class T>
 __device__ __forceinline__ void tmma_chunk(const double* __restrict__ sA, const double* __restrict__ sB,
-                                           double (&c)[T::MF][T::NF][2], int wm, int wn, int lane) {
+                                           double (&c)[T::MF][T::NF][2], int wm, int wn, int lane,
+                                           int kv = T::BK) {
   const int gr = lane >> 2, gc = lane & 3;
   const double* a0 = sA + (wm * T::MF * 8 + gr) * T::SA + gc;
   const double* b0 = sB + gc * T::SB + wn * T::NF * 8 + gr;
 #pragma unroll
   for (int kk = 0; kk < T::BK; kk += 4) {
+    if (kk >= kv) break;
     double a[T::MF], b[T::NF];
 #pragma unroll
     for (int i = 0; i < T::MF; ++i) a[i] = a0[i * 8 * T::SA + kk];

@@ -364,6 +364,7 @@ def finish_construct(tree, flops=None):
     mask = np.ones(nn, dtype=bool)
     mask[tree.root] = False
     tree.r_used = int(max(rU[mask].max(), rV[mask].max()))
+    tree.ct.rmax = tree.r_used      # the multiply sizes its output tiles to the ranks
     if flops is not None:
         flops.hss_construct += _construct_flops(tree, tree.k, tree.w)
     return tree
