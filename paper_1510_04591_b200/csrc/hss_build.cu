@@ -186,162 +186,22 @@ __device__ __forceinline__ double lapy2(double x, double y) {
   return wv * sqrt(1.0 + q * q);
 }
 
-// ---------------------------------------------------------------------------
-// Interpolative decomposition of one p x w matrix M (rows = candidates), hss.py:120-148.
-// Column-pivoted QR of A = M^T (w x p): candidate j of M is column j of A, stored
-// contiguously in shared memory (sA[j*SW + t] = A[t][j], SW odd => conflict-free when
-// consecutive threads own consecutive candidates).
-// Per elimination step: warp 0 picks the pivot (first max of the downdated norms,
-// idamax) and forms the Householder reflector (dlarfg); then every thread owns one
-// trailing candidate and applies the reflector and the dlaqp2 norm downdate to it.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double tol,
-                                                 const double* __restrict__ om, int64_t ldom,
-                                                 hsseig_status* st, int j0) {
-  extern __shared__ __align__(16) double sm[];
-  const int j = j0 + blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5, nthr = blockDim.x;
-  const int node = T.lnodes[(1 << level) - 1 + j];
-  const bool leaf = T.left[node] < 0;
+// Truncation, saturation flag, T = R11^{-1} R12 and the ID outputs for the factored M^T held
+// in shared memory in pivot order (sA[j*SW + t], piv[j] = candidate at position j).
+__device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, bool leaf, int p,
+                                          double nf, double tol, const double* __restrict__ om,
+                                          int64_t ldom, hsseig_status* st, const double* Mg,
+                                          double* sA, double* tail, double* red, int* piv) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int nthr = blockDim.x;
   const int w = T.w, ws = T.ws, SW = w | 1;
-  int p;
-  if (leaf) p = T.hi[node] - T.lo[node];
-  else {
-    int a = T.left[node], b = T.right[node];
-    p = side == 0 ? T.rU[a] + T.rU[b] : T.rV[a] + T.rV[b];
-  }
-  double* Mg = T.M + (size_t)(2 * j + side) * T.pmax * ws;
-  double* sA = sm;                              // p x SW
-  double* vn1 = sA + (size_t)T.pmax * SW;       // p
-  double* vn2 = vn1 + T.pmax;                   // p
-  double* tail = vn2 + T.pmax;                  // w + 1
-  double* red = tail + (w + 1);                 // 32 scratch
-  int* piv = reinterpret_cast<int*>(red + 32);  // p
-  __shared__ double s_tau, s_nf, s_resid;
+  __shared__ double s_resid;
   __shared__ int s_r, s_sat;
-
-  {
-    for (int e = tid; e < p * w; e += nthr) {
-      int row = e / w, c = e % w;
-      sA[row * SW + c] = Mg[(size_t)row * ws + c];
-    }
-  }
-  for (int e = tid; e < p; e += nthr) piv[e] = e;
-  __syncthreads();
-  // Frobenius norm (hss.py:128) and the initial column norms (dgeqp3: dnrm2 per column)
-  {
-    double s = 0.0;
-    for (int c = tid; c < p; c += nthr) {
-      const double* a = sA + c * SW;
-      double q0 = 0.0, q1 = 0.0;
-      int t = 0;
-      for (; t + 1 < w; t += 2) { q0 = fma(a[t], a[t], q0); q1 = fma(a[t + 1], a[t + 1], q1); }
-      if (t < w) q0 = fma(a[t], a[t], q0);
-      double q = q0 + q1;
-      vn1[c] = vn2[c] = sqrt(q);
-      s += q;
-    }
-    s = warp_sum(s);
-    if (lane == 0) red[warp] = s;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-    for (int t = 0; t < nwarps; ++t) s += red[t];
-    s_nf = sqrt(s);
-  }
-  __syncthreads();
-  const double nf = s_nf;
+  (void)red;
   int r = 0, sat = 0;
   double resid = 0.0;
   const int mn = min(w, p);
   if (!(nf == 0.0 || p == 0 || w == 0)) {
-    for (int i = 0; i < mn; ++i) {
-      if (warp == 0) {
-        double best = -1.0;
-        int bi = i;
-        for (int c = i + lane; c < p; c += 32) {
-          double v = vn1[c];
-          if (v > best) { best = v; bi = c; }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-        }
-        const int pvt = bi;
-        if (pvt != i) {
-          for (int t = lane; t < w; t += 32) {
-            double x0 = sA[i * SW + t];
-            sA[i * SW + t] = sA[pvt * SW + t];
-            sA[pvt * SW + t] = x0;
-          }
-          if (lane == 0) {
-            int tp = piv[pvt]; piv[pvt] = piv[i]; piv[i] = tp;
-            vn1[pvt] = vn1[i];
-            vn2[pvt] = vn2[i];
-          }
-        }
-        __syncwarp();
-        double* col = sA + i * SW;
-        double xs = 0.0;
-        for (int t = i + 1 + lane; t < w; t += 32) xs = fma(col[t], col[t], xs);
-        const double xnorm = sqrt(warp_sum(xs));
-        const double alpha = col[i];
-        double tau = 0.0, beta = alpha;
-        if (xnorm != 0.0) {
-          beta = -copysign(lapy2(alpha, xnorm), alpha);
-          tau = (beta - alpha) / beta;
-          const double scal = 1.0 / (alpha - beta);
-          for (int t = i + 1 + lane; t < w; t += 32) col[t] *= scal;
-        }
-        __syncwarp();
-        if (lane == 0) {
-          col[i] = beta;
-          s_tau = tau;
-        }
-      }
-      __syncthreads();
-      const double tau = s_tau;
-      const double* v = sA + i * SW;
-      for (int c = i + 1 + tid; c < p; c += nthr) {
-        double* a = sA + c * SW;
-        if (tau != 0.0) {
-          double d0 = a[i], d1 = 0.0, d2 = 0.0, d3 = 0.0;
-          int t = i + 1;
-          for (; t + 3 < w; t += 4) {
-            d0 = fma(v[t], a[t], d0);
-            d1 = fma(v[t + 1], a[t + 1], d1);
-            d2 = fma(v[t + 2], a[t + 2], d2);
-            d3 = fma(v[t + 3], a[t + 3], d3);
-          }
-          for (; t < w; ++t) d0 = fma(v[t], a[t], d0);
-          const double f = tau * ((d0 + d1) + (d2 + d3));
-          a[i] -= f;
-#pragma unroll 4
-          for (t = i + 1; t < w; ++t) a[t] = fma(-f, v[t], a[t]);
-        }
-        const double n1 = vn1[c];
-        if (n1 != 0.0) {
-          const double q = fabs(a[i]) / n1;
-          const double temp = fmax(1.0 - q * q, 0.0);
-          const double ratio = n1 / vn2[c];
-          if (temp * ratio * ratio <= kTol3z) {
-            double s0 = 0.0, s1 = 0.0;
-            int t = i + 1;
-            for (; t + 1 < w; t += 2) { s0 = fma(a[t], a[t], s0); s1 = fma(a[t + 1], a[t + 1], s1); }
-            if (t < w) s0 = fma(a[t], a[t], s0);
-            const double nv = (i + 1 < w) ? sqrt(s0 + s1) : 0.0;
-            vn1[c] = nv;
-            vn2[c] = nv;
-          } else {
-            vn1[c] = n1 * sqrt(temp);
-          }
-        }
-      }
-      __syncthreads();
-    }
     // trailing Frobenius mass of R's rows, cumulated from the bottom (hss.py:134-136)
     for (int t = warp; t < mn; t += nwarps) {
       double s = 0.0;
@@ -462,51 +322,234 @@ __global__ void __launch_bounds__(256) id_kernel(TreeDev T, int level, double to
     Sb = (side == 0 ? T.zcomp : T.ycomp) + slot_ww(T, b);
     lds = ws;
   }
-  // warp -> groups of 4 output rows t, lane -> up to 4 columns c; each S row is loaded
-  // once per group and feeds 16 independent FMA chains
+  // S rows are staged through shared memory in chunks of kSChunk (coalesced loads, one
+  // latency per chunk); warp -> groups of 4 output rows t, lane -> up to 4 columns c
   auto srow_ptr = [&](int q) -> const double* {
     return q < na ? Sa + (int64_t)q * lds : Sb + (int64_t)(q - na) * lds;
   };
-  for (int t0 = warp * 4; t0 < r; t0 += nwarps * 4) {
-    double acc[4][4];
+  // staging reuses the pivot columns of sA (positions < r), dead once X is written
+  double* sS = sA;
+  const int kSChunk = max(1, min(16, (r * SW) / max(w, 1)));
+  const int ngroups = (r + 3) / 4;
+  const int myg = (ngroups + nwarps - 1) / nwarps;   // groups per warp (<= 4 for w <= 128)
+  for (int gb = 0; gb < myg; gb += 2) {              // two groups per pass (register budget)
+    double acc[2][4][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int t = t0 + u;
-      const double* sr = srow_ptr(t < r ? piv[t] : piv[0]);
-#pragma unroll
-      for (int cq = 0; cq < 4; ++cq) {
-        const int c = lane + 32 * cq;
-        acc[u][cq] = (t < r && c < w) ? sr[c] : 0.0;
-      }
-    }
-#pragma unroll 2
-    for (int jj = r; jj < p; ++jj) {
-      const double* sr = srow_ptr(piv[jj]);
-      double sv[4];
-#pragma unroll
-      for (int cq = 0; cq < 4; ++cq) {
-        const int c = lane + 32 * cq;
-        sv[cq] = c < w ? sr[c] : 0.0;
-      }
+    for (int gi = 0; gi < 2; ++gi) {
+      const int t0 = (warp + (gb + gi) * nwarps) * 4;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const double coef = (t0 + u < r) ? sA[jj * SW + t0 + u] : 0.0;
+        const int t = t0 + u;
+        const double* sr = (gb + gi < myg && t < r) ? srow_ptr(piv[t]) : nullptr;
 #pragma unroll
-        for (int cq = 0; cq < 4; ++cq) acc[u][cq] = fma(coef, sv[cq], acc[u][cq]);
+        for (int cq = 0; cq < 4; ++cq) {
+          const int c = lane + 32 * cq;
+          acc[gi][u][cq] = (sr && c < w) ? sr[c] : 0.0;
+        }
+      }
+    }
+    for (int j0 = r; j0 < p; j0 += kSChunk) {
+      const int nj = min(kSChunk, p - j0);
+      __syncthreads();
+      for (int e = tid; e < nj * w; e += nthr) {
+        const int q = e / w, c = e % w;
+        sS[q * w + c] = srow_ptr(piv[j0 + q])[c];
+      }
+      __syncthreads();
+      for (int q = 0; q < nj; ++q) {
+        double sv[4];
+#pragma unroll
+        for (int cq = 0; cq < 4; ++cq) {
+          const int c = lane + 32 * cq;
+          sv[cq] = c < w ? sS[q * w + c] : 0.0;
+        }
+        const double* arow = sA + (j0 + q) * SW;
+#pragma unroll
+        for (int gi = 0; gi < 2; ++gi) {
+          const int t0 = (warp + (gb + gi) * nwarps) * 4;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double coef = (gb + gi < myg && t0 + u < r) ? arow[t0 + u] : 0.0;
+#pragma unroll
+            for (int cq = 0; cq < 4; ++cq) acc[gi][u][cq] = fma(coef, sv[cq], acc[gi][u][cq]);
+          }
+        }
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int t = t0 + u;
-      if (t >= r) continue;
+    for (int gi = 0; gi < 2; ++gi) {
+      const int t0 = (warp + (gb + gi) * nwarps) * 4;
 #pragma unroll
-      for (int cq = 0; cq < 4; ++cq) {
-        const int c = lane + 32 * cq;
-        if (c < w) comp[(size_t)t * ws + c] = acc[u][cq];
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u;
+        if (gb + gi >= myg || t >= r) continue;
+#pragma unroll
+        for (int cq = 0; cq < 4; ++cq) {
+          const int c = lane + 32 * cq;
+          if (c < w) comp[(size_t)t * ws + c] = acc[gi][u][cq];
+        }
       }
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// Interpolative decomposition of one p x w matrix M (rows = candidates), hss.py:120-148.
+// Column-pivoted QR of A = M^T (w x p): candidate j of M is column j of A, stored
+// contiguously in shared memory (sA[j*SW + t] = A[t][j], SW odd => conflict-free when
+// consecutive threads own consecutive candidates).
+// Per elimination step: warp 0 picks the pivot (first max of the downdated norms,
+// idamax) and forms the Householder reflector (dlarfg); then every thread owns one
+// trailing candidate and applies the reflector and the dlaqp2 norm downdate to it.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 2) id_kernel(TreeDev T, int level, double tol,
+                                                 const double* __restrict__ om, int64_t ldom,
+                                                 hsseig_status* st, int j0) {
+  extern __shared__ __align__(16) double sm[];
+  const int j = j0 + blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5, nthr = blockDim.x;
+  const int node = T.lnodes[(1 << level) - 1 + j];
+  const bool leaf = T.left[node] < 0;
+  const int w = T.w, ws = T.ws, SW = w | 1;
+  int p;
+  if (leaf) p = T.hi[node] - T.lo[node];
+  else {
+    int a = T.left[node], b = T.right[node];
+    p = side == 0 ? T.rU[a] + T.rU[b] : T.rV[a] + T.rV[b];
+  }
+  double* Mg = T.M + (size_t)(2 * j + side) * T.pmax * ws;
+  double* sA = sm;                              // p x SW
+  double* vn1 = sA + (size_t)T.pmax * SW;       // p
+  double* vn2 = vn1 + T.pmax;                   // p
+  double* tail = vn2 + T.pmax;                  // w + 1
+  double* red = tail + (w + 1);                 // 32 scratch
+  int* piv = reinterpret_cast<int*>(red + 32);  // p
+  __shared__ double s_tau, s_nf;
+
+  {
+    for (int e = tid; e < p * w; e += nthr) {
+      int row = e / w, c = e % w;
+      sA[row * SW + c] = Mg[(size_t)row * ws + c];
+    }
+  }
+  for (int e = tid; e < p; e += nthr) piv[e] = e;
+  __syncthreads();
+  // Frobenius norm (hss.py:128) and the initial column norms (dgeqp3: dnrm2 per column)
+  {
+    double s = 0.0;
+    for (int c = tid; c < p; c += nthr) {
+      const double* a = sA + c * SW;
+      double q0 = 0.0, q1 = 0.0;
+      int t = 0;
+      for (; t + 1 < w; t += 2) { q0 = fma(a[t], a[t], q0); q1 = fma(a[t + 1], a[t + 1], q1); }
+      if (t < w) q0 = fma(a[t], a[t], q0);
+      double q = q0 + q1;
+      vn1[c] = vn2[c] = sqrt(q);
+      s += q;
+    }
+    s = warp_sum(s);
+    if (lane == 0) red[warp] = s;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int t = 0; t < nwarps; ++t) s += red[t];
+    s_nf = sqrt(s);
+  }
+  __syncthreads();
+  const double nf = s_nf;
+  const int mn = min(w, p);
+  if (!(nf == 0.0 || p == 0 || w == 0)) {
+    for (int i = 0; i < mn; ++i) {
+      if (warp == 0) {
+        double best = -1.0;
+        int bi = i;
+        for (int c = i + lane; c < p; c += 32) {
+          double v = vn1[c];
+          if (v > best) { best = v; bi = c; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        const int pvt = bi;
+        if (pvt != i) {
+          for (int t = lane; t < w; t += 32) {
+            double x0 = sA[i * SW + t];
+            sA[i * SW + t] = sA[pvt * SW + t];
+            sA[pvt * SW + t] = x0;
+          }
+          if (lane == 0) {
+            int tp = piv[pvt]; piv[pvt] = piv[i]; piv[i] = tp;
+            vn1[pvt] = vn1[i];
+            vn2[pvt] = vn2[i];
+          }
+        }
+        __syncwarp();
+        double* col = sA + i * SW;
+        double xs = 0.0;
+        for (int t = i + 1 + lane; t < w; t += 32) xs = fma(col[t], col[t], xs);
+        const double xnorm = sqrt(warp_sum(xs));
+        const double alpha = col[i];
+        double tau = 0.0, beta = alpha;
+        if (xnorm != 0.0) {
+          beta = -copysign(lapy2(alpha, xnorm), alpha);
+          tau = (beta - alpha) / beta;
+          const double scal = 1.0 / (alpha - beta);
+          for (int t = i + 1 + lane; t < w; t += 32) col[t] *= scal;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          col[i] = beta;
+          s_tau = tau;
+        }
+      }
+      __syncthreads();
+      const double tau = s_tau;
+      const double* v = sA + i * SW;
+      for (int c = i + 1 + tid; c < p; c += nthr) {
+        double* a = sA + c * SW;
+        if (tau != 0.0) {
+          double d0 = a[i], d1 = 0.0, d2 = 0.0, d3 = 0.0;
+          int t = i + 1;
+          for (; t + 3 < w; t += 4) {
+            d0 = fma(v[t], a[t], d0);
+            d1 = fma(v[t + 1], a[t + 1], d1);
+            d2 = fma(v[t + 2], a[t + 2], d2);
+            d3 = fma(v[t + 3], a[t + 3], d3);
+          }
+          for (; t < w; ++t) d0 = fma(v[t], a[t], d0);
+          const double f = tau * ((d0 + d1) + (d2 + d3));
+          a[i] -= f;
+#pragma unroll 4
+          for (t = i + 1; t < w; ++t) a[t] = fma(-f, v[t], a[t]);
+        }
+        const double n1 = vn1[c];
+        if (n1 != 0.0) {
+          const double q = fabs(a[i]) / n1;
+          const double temp = fmax(1.0 - q * q, 0.0);
+          const double ratio = n1 / vn2[c];
+          if (temp * ratio * ratio <= kTol3z) {
+            double s0 = 0.0, s1 = 0.0;
+            int t = i + 1;
+            for (; t + 1 < w; t += 2) { s0 = fma(a[t], a[t], s0); s1 = fma(a[t + 1], a[t + 1], s1); }
+            if (t < w) s0 = fma(a[t], a[t], s0);
+            const double nv = (i + 1 < w) ? sqrt(s0 + s1) : 0.0;
+            vn1[c] = nv;
+            vn2[c] = nv;
+          } else {
+            vn1[c] = n1 * sqrt(temp);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  id_finish(T, side, node, leaf, p, nf, tol, om, ldom, st, Mg, sA, tail, red, piv);
+}
+
 
 }  // namespace hsseig
 
