@@ -309,6 +309,32 @@ def test_plugin_secular_all_contract(sec):
     assert np.abs(lam - sec[f"{name}_lam"]).max() <= 64 * EPS * scale
 
 
+@pytest.mark.parametrize("n", [2, 7, 25, 32])
+def test_plugin_tql2_contract(n):
+    # the base-case kernel seam (pkg/src/hsseig/_kernels.pyx:352-411 as called by
+    # dc.py:118-129): in place, status 0, eigenpairs equal to the reference QL's
+    from paper_1510_04591_b200 import plugin
+    from oracle import hss_oracle as orc
+    rng = np.random.default_rng(n)
+    a, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n - 1)
+    d, e, Z = a.copy(), b.copy(), np.eye(n)
+    assert plugin.tql2(d, e, Z, 30) == 0
+    d0, e0, Z0 = a.copy(), b.copy(), np.eye(n)
+    assert orc.tql2(d0, e0, Z0, 30) == 0
+    order = np.argsort(d0, kind="stable")
+    assert np.abs(d - d0[order]).max() <= 4 * EPS * np.abs(d0).max()
+    Zr = Z0[:, order]
+    Zg = Z * np.sign((Z * Zr).sum(0))
+    assert np.abs(Zg - Zr).max() <= 1e-13
+    # Z accumulates onto its input (Z <- Z Q), any number of rows
+    Zin = rng.standard_normal((3, n))
+    d2, e2, Z2 = a.copy(), b.copy(), Zin.copy()
+    assert plugin.tql2(d2, e2, Z2, 30) == 0
+    assert np.abs(Z2 - Zin @ Z).max() <= 1e-13
+    with pytest.raises(ValueError):
+        plugin.tql2(np.zeros(40), np.zeros(39), np.eye(40))
+
+
 def test_sharded_merge_driver_single_rank_nccl():
     # the multi-GPU driver (index-sharded roots/weights/samples, replicated tree,
     # row-local multiply) on a one-rank NCCL group against the single-GPU pipeline
