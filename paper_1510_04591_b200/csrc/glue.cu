@@ -117,15 +117,15 @@ __global__ void assemble_kernel(const double* __restrict__ Q1, int64_t n1, const
                                 int64_t n2, const int64_t* __restrict__ src, double* __restrict__ W,
                                 int64_t ldw) {
   const int64_t n = n1 + n2;
-  const int64_t row = blockIdx.y;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t sc = src[c];
-    double v = 0.0;
-    if (row < n1) { if (sc < n1) v = Q1[row * n1 + sc]; }
-    else if (sc >= n1) v = Q2[(row - n1) * n2 + (sc - n1)];
-    W[row * ldw + c] = v;
-  }
+  for (int64_t row = blockIdx.y; row < n; row += gridDim.y)   // gridDim.y <= 65535
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
+         c += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t sc = src[c];
+      double v = 0.0;
+      if (row < n1) { if (sc < n1) v = Q1[row * n1 + sc]; }
+      else if (sc >= n1) v = Q2[(row - n1) * n2 + (sc - n1)];
+      W[row * ldw + c] = v;
+    }
 }
 
 // deflation Givens rotations on column pairs, in order, every row independently
@@ -149,13 +149,13 @@ __global__ void rotate_kernel(double* __restrict__ W, int64_t ldw, int64_t rows,
 // out[:, c] = (src[c] < k ? A[:, src[c]] : B[:, src[c]])  (final eigenvalue order)
 __global__ void gather2_kernel(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
                                int64_t ldb, int64_t k, const int64_t* __restrict__ src, int64_t ncol,
-                               double* __restrict__ out, int64_t ldo) {
-  const int64_t row = blockIdx.y;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncol;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t sc = src[c];
-    out[row * ldo + c] = sc < k ? A[row * lda + sc] : B[row * ldb + sc];
-  }
+                               int64_t nrow, double* __restrict__ out, int64_t ldo) {
+  for (int64_t row = blockIdx.y; row < nrow; row += gridDim.y)   // gridDim.y <= 65535
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncol;
+         c += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t sc = src[c];
+      out[row * ldo + c] = sc < k ? A[row * lda + sc] : B[row * ldb + sc];
+    }
 }
 
 }  // namespace hsseig
@@ -177,7 +177,7 @@ extern "C" int hsseig_assemble_merge(const double* Q1, int64_t n1, const double*
                                      const int64_t* src, double* W, int64_t ldw, void* stream) {
   const int64_t n = n1 + n2;
   if (n <= 0 || ldw < n || n > 0x7fffffff) HSS_ARG_FAIL();
-  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)n);
+  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(n, 65535));
   assemble_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(Q1, n1, Q2, n2, src, W, ldw);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
@@ -199,8 +199,9 @@ extern "C" int hsseig_gather_columns(const double* A, int64_t lda, const double*
                                      double* out, int64_t ldo, void* stream) {
   if (rows < 0 || ncol < 0 || rows > 0x7fffffff) HSS_ARG_FAIL();
   if (rows == 0 || ncol == 0) return HSSEIG_OK;
-  dim3 grid((unsigned)std::min<int64_t>((ncol + 255) / 256, 64), (unsigned)rows);
-  gather2_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, B, ldb, k, src, ncol, out, ldo);
+  dim3 grid((unsigned)std::min<int64_t>((ncol + 255) / 256, 64), (unsigned)std::min<int64_t>(rows, 65535));
+  gather2_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, B, ldb, k, src, ncol, rows, out,
+                                                         ldo);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }

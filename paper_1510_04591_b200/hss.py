@@ -8,6 +8,7 @@ out by hsseig_tree_layout; per-node views are materialised only on request.
 """
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -370,6 +371,9 @@ def finish_construct(tree, flops=None):
     return tree
 
 
+MULT_WORK_BUDGET = int(float(os.environ.get("HSSEIG_MULT_WORK_GB", "16")) * (1 << 30))
+
+
 def hss_matmul_right(X, H, flops=None, out=None):
     """Structured product X @ H (hss.py:309-361) as per-level batched DMMA GEMMs."""
     X = dev_rows(X)
@@ -385,11 +389,18 @@ def hss_matmul_right(X, H, flops=None, out=None):
     lib = nat.load()
     if out is None:
         out = torch.empty(P, H.k, dtype=torch.float64, device="cuda")
-    work = torch.empty(int(lib.hsseig_matmul_work_doubles(P, ctypes.byref(H.ct))),
-                       dtype=torch.float64, device="cuda")
-    nat.check(lib.hsseig_hss_matmul_right(nat.ptr(X), X.stride(0), P, ctypes.byref(H.ct),
-                                          nat.ptr(out), out.stride(0), nat.ptr(work),
-                                          nat.stream_ptr()), "hss_matmul_right")
+    # the per-level G/F workspace grows with the rows: bound it by multiplying row chunks
+    base = int(lib.hsseig_matmul_work_doubles(0, ctypes.byref(H.ct)))
+    per_row = int(lib.hsseig_matmul_work_doubles(1, ctypes.byref(H.ct))) - base
+    chunk = max(128, (MULT_WORK_BUDGET // 8 - base) // max(per_row, 1) // 128 * 128)
+    chunk = min(chunk, P)
+    work = torch.empty(base + per_row * chunk, dtype=torch.float64, device="cuda")
+    for r0 in range(0, P, chunk):
+        r1 = min(P, r0 + chunk)
+        nat.check(lib.hsseig_hss_matmul_right(nat.ptr(X[r0:r1]), X.stride(0), r1 - r0,
+                                              ctypes.byref(H.ct), nat.ptr(out[r0:r1]),
+                                              out.stride(0), nat.ptr(work), nat.stream_ptr()),
+                  "hss_matmul_right")
     if flops is not None:
         flops.hss_mult += mult_flops(H, P)
     return out

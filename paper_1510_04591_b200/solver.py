@@ -145,6 +145,7 @@ def adc_solve(T, cfg=None):
         W = torch.empty(n, n, dtype=torch.float64, device="cuda")
         nat.check(lib.hsseig_assemble_merge(nat.ptr(Q1), n1, nat.ptr(Q2), n - n1, nat.ptr(_i64(src)),
                                             nat.ptr(W), n, s), "assemble")
+        del Q1, Q2     # the children's blocks are dead once assembled (memory at N = 65536)
         if nr:
             ca, cb = _i64(posW[perm[ri[:nr]]]), _i64(posW[perm[rj[:nr]]])
             cc, ss = _f64(rc[:nr]), _f64(rs[:nr])
@@ -159,11 +160,15 @@ def adc_solve(T, cfg=None):
         rec_.flops = {p: v - before[p] for p, v in flops.as_dict().items()}
         lam_cat = np.concatenate([lam_k, d_out[k:]])
         order = np.argsort(lam_cat, kind="stable")
-        Q = torch.empty(n, n, dtype=torch.float64, device="cuda")
-        nat.check(lib.hsseig_gather_columns(nat.ptr(Qk), Qk.stride(0), nat.ptr(W), n, k,
-                                            nat.ptr(_i64(order)), n, n, nat.ptr(Q), n, s), "gather")
-        del W, Qk
-        return lam_cat[order], Q
+        if k == 0:
+            return lam_cat[order], W[:, torch.as_tensor(order, device="cuda")].contiguous()
+        # gather into W's own storage: the deflated columns move to a compact copy first
+        Wd = W[:, k:].contiguous() if k < n else Qk
+        nat.check(lib.hsseig_gather_columns(nat.ptr(Qk), Qk.stride(0), ctypes.c_void_p(Wd.data_ptr() - 8 * k),
+                                            max(n - k, 1), k, nat.ptr(_i64(order)), n, n, nat.ptr(W),
+                                            n, s), "gather")
+        del Wd, Qk
+        return lam_cat[order], W
 
     lam, Q = rec(0, T.n)
     return EigenResult(lam=lam, Q=Q, merges=merges, flops=flops)
