@@ -268,6 +268,66 @@ int hsseig_gather_columns(const double *A, int64_t lda, const double *B, int64_t
                           const int64_t *src, int64_t ncol, int64_t rows, double *out,
                           int64_t ldo, void *stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Level-batched merges: every merge of one recursion depth of
+ * adc_solve (pkg/src/hsseig/dc.py:194-257) in one set of launches.  Merge m has n1[m] +
+ * n2[m] rows, concatenated at roff[m] (row_merge[r] = merge of row r); its children blocks
+ * are at device addresses q1[m], q2[m] (row-major n1 x n1, n2 x n2); its n x n block
+ * W_m at W + woff[m].  Kept rank-one systems s own roots [koff[s], koff[s+1]) of the
+ * concatenated root arrays; seg_of[i] = system of root i.  st[s] as hsseig_status_init.
+ * --------------------------------------------------------------------------------------- */
+/* z rows: [last row of Q1, first row of Q2] per merge (dc.py:112). */
+int hsseig_wave_zrows(const uint64_t *q1, const uint64_t *q2, const int64_t *n1,
+                      const int64_t *n2, const int64_t *roff, int64_t nm, double *zrow,
+                      void *stream);
+/* Host: joint sort + deflation of every merge (dc.py:205-235, secular.py:91-156); src /
+   d_out / z_out per row, rotations as W-column pairs [rot_off[m], rot_off[m+1]).  Returns
+   the total kept roots. */
+int64_t hsseig_wave_deflate(int64_t nm, const int64_t *n1, const int64_t *n2, const int64_t *roff,
+                            const double *L, const double *zrow, const double *bk, int64_t *kept,
+                            double *rho_eff, double *d_out, double *z_out, int64_t *src,
+                            int64_t *rot_off, int64_t *ca, int64_t *cb, double *rc, double *rs);
+/* W_m[:, c] = blockdiag(Q1, Q2)[:, src[c]] for every merge. */
+int hsseig_wave_assemble(const uint64_t *q1, const uint64_t *q2, const int64_t *n1,
+                         const int64_t *n2, const int64_t *roff, const int32_t *row_merge,
+                         const int64_t *src, double *W, const int64_t *woff, int64_t nrows,
+                         void *stream);
+/* Deflation rotations of every merge on its W_m (dc.py:225-230). */
+int hsseig_wave_rotate(double *W, const int64_t *woff, const int64_t *n, const int64_t *rot_off,
+                       const int64_t *ca, const int64_t *cb, const double *c, const double *s,
+                       int64_t nm, int64_t nmax, void *stream);
+/* Secular roots of every kept system (secular_all per system); work: ntot + nseg doubles. */
+int hsseig_wave_secular(const double *d, const double *z, const int64_t *koff,
+                        const int32_t *seg_of, const double *rho, int64_t nseg, int64_t ntot,
+                        double *lam, double *gamma, double *mu, int32_t *iters, double *work,
+                        hsseig_status *st, void *stream);
+int hsseig_wave_dnext(const double *d, const double *gamma, const double *mu, const int64_t *koff,
+                      const int32_t *seg_of, int64_t ntot, double *dnext, void *stream);
+int hsseig_wave_loewner(const double *d, const double *dnext, const double *gamma,
+                        const double *mu, const double *z, const int64_t *koff,
+                        const int32_t *seg_of, const double *rho, int64_t ntot, double *zhat,
+                        hsseig_status *st, void *stream);
+int hsseig_wave_normalizers(const double *d, const double *dnext, const double *gamma,
+                            const double *mu, const double *zhat, const int64_t *koff,
+                            const int32_t *seg_of, int64_t ntot, double *v, void *stream);
+/* Grouped dense updates out_s = W_s[:, :k_s] @ C_s (dc.py:132-138); tasks: (s, row tile,
+   column tile) int32 triples for tiles of hsseig_wave_tile_shape. */
+int hsseig_wave_dense_update(const double *W, const int64_t *woff, const int64_t *nrow,
+                             const double *d, const double *dnext, const double *gamma,
+                             const double *mu, const double *zhat, const double *v,
+                             const int64_t *koff, double *out, const int64_t *ooff,
+                             const int32_t *tasks, int64_t ntasks, void *stream);
+int hsseig_wave_tile_shape(int32_t *bm, int32_t *bn);
+/* Host: final order of every merge: stable argsort of [roots, deflated poles]
+   (dc.py:253-257). */
+int hsseig_wave_order(int64_t nm, const int64_t *roff, const int64_t *kept, const int64_t *koff,
+                      const double *lam, const double *d_out, int64_t *order, double *lam_out);
+/* out_m[:, c] = order[c] < k_m ? Qk_m[:, order[c]] : W_m[:, order[c]] for every merge. */
+int hsseig_wave_gather(const double *Qk, const int64_t *qoff, const int64_t *kept,
+                       const double *W, const int64_t *woff, const int64_t *roff,
+                       const int32_t *row_merge, const int64_t *order, double *out,
+                       const int64_t *ooff, int64_t nrows, void *stream);
+
 /* Plain batched helper used by tests/bench: out = A @ B (P x K)(K x N), FP64 DMMA. */
 int hsseig_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *stream);

@@ -189,19 +189,15 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int nsplit
   out[row * ldo + col] = s;
 }
 
-// out = Qb @ C with B-operand tiles of C generated in shared memory.
+// out = Qb @ C with B-operand tiles of C generated in shared memory; one BM x BN tile.
 template <class T>
-__global__ void __launch_bounds__(T::THREADS) dense_update_kernel(const double* __restrict__ Q,
-                                                                  int64_t ldq, int64_t P,
-                                                                  CauchyGen g,
-                                                                  double* __restrict__ out,
-                                                                  int64_t ldo) {
-  extern __shared__ __align__(16) double smem[];
+__device__ __forceinline__ void dense_update_tile(const double* __restrict__ Q, int64_t ldq,
+                                                  int64_t P, const CauchyGen& g,
+                                                  double* __restrict__ out, int64_t ldo,
+                                                  int64_t m0, int64_t n0, double* smem) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / T::WN, wn = warp % T::WN;
   const int64_t k = g.k;
-  const int64_t m0 = (int64_t)blockIdx.x * T::BM;
-  const int64_t n0 = (int64_t)blockIdx.y * T::BN;
   const int nch = (int)((k + T::BK - 1) / T::BK);
   Acc<T> acc;
   acc.zero();
@@ -232,6 +228,34 @@ __global__ void __launch_bounds__(T::THREADS) dense_update_kernel(const double* 
     __syncthreads();
   }
   store_acc<T>(acc, out + n0, ldo, P, m0, (int)imin64(T::BN, k - n0), 0, wm, wn, lane);
+}
+
+template <class T>
+__global__ void __launch_bounds__(T::THREADS) dense_update_kernel(const double* __restrict__ Q,
+                                                                  int64_t ldq, int64_t P,
+                                                                  CauchyGen g,
+                                                                  double* __restrict__ out,
+                                                                  int64_t ldo) {
+  extern __shared__ __align__(16) double smem[];
+  dense_update_tile<T>(Q, ldq, P, g, out, ldo, (int64_t)blockIdx.x * T::BM,
+                       (int64_t)blockIdx.y * T::BN, smem);
+}
+
+// Level-batched dense updates: task t = (system s, row tile, column tile) of
+// out_s = W_s[:, :k_s] @ C_s, with W_s the n_s x n_s merge block (ld n_s) and out_s n_s x k_s.
+template <class T>
+__global__ void __launch_bounds__(T::THREADS) wave_dense_kernel(
+    const double* __restrict__ W, const int64_t* __restrict__ woff, const int64_t* __restrict__ nrow,
+    CauchyGen g, const int64_t* __restrict__ koff, double* __restrict__ out,
+    const int64_t* __restrict__ ooff, const int32_t* __restrict__ tasks) {
+  extern __shared__ __align__(16) double smem[];
+  const int s = tasks[3 * blockIdx.x], mt = tasks[3 * blockIdx.x + 1], nt = tasks[3 * blockIdx.x + 2];
+  const int64_t a = koff[s], k = koff[s + 1] - a, n = nrow[s];
+  CauchyGen gs = g;
+  gs.d += a; gs.dnext += a; gs.gam += a; gs.mu += a; gs.zhat += a; gs.v += a;
+  gs.k = k;
+  dense_update_tile<T>(W + woff[s], n, n, gs, out + ooff[s], k, (int64_t)mt * T::BM,
+                       (int64_t)nt * T::BN, smem);
 }
 
 static void sample_split(int64_t k, int64_t nrows, int64_t bm, int64_t* nsplit, int64_t* kchunk) {
@@ -371,5 +395,34 @@ extern "C" int hsseig_dense_update(const double* Qb, int64_t ldq, int64_t P, con
   dense_update_kernel<T><<<grid, T::THREADS, smem, (cudaStream_t)stream>>>(Qb, ldq, P, to_gen(gen),
                                                                            out, ldo);
   HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_dense_update(const double* W, const int64_t* woff, const int64_t* nrow,
+                                        const double* d, const double* dnext, const double* gamma,
+                                        const double* mu, const double* zhat, const double* v,
+                                        const int64_t* koff, double* out, const int64_t* ooff,
+                                        const int32_t* tasks, int64_t ntasks, void* stream) {
+  if (ntasks < 0 || !W || !woff || !nrow || !koff || !out || !ooff || !tasks) HSS_ARG_FAIL();
+  if (ntasks == 0) return HSSEIG_OK;
+  using T = Tile<4, 8, 4, 2, 2>;
+  const size_t smem = sizeof(double) * T::STAGE_ELEMS * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(wave_dense_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  CauchyGen g;
+  g.d = d; g.dnext = dnext; g.gam = gamma; g.mu = mu; g.zhat = zhat; g.v = v; g.k = 0;
+  wave_dense_kernel<T><<<(unsigned)ntasks, T::THREADS, smem, (cudaStream_t)stream>>>(
+      W, woff, nrow, g, koff, out, ooff, tasks);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_tile_shape(int32_t* bm, int32_t* bn) {
+  using T = Tile<4, 8, 4, 2, 2>;
+  *bm = T::BM;
+  *bn = T::BN;
   return HSSEIG_OK;
 }

@@ -158,6 +158,91 @@ __global__ void gather2_kernel(const double* __restrict__ A, int64_t lda, const 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Level-batched ("wave") glue: every merge of one recursion depth per launch.  Merge m
+// has children blocks Q1 (n1 x n1) and Q2 (n2 x n2) at arbitrary device addresses, its
+// rows occupy [roff[m], roff[m+1]) of the concatenated row space and its n x n merge
+// block sits at W + woff[m]; row_merge maps a concatenated row to its merge.
+// ---------------------------------------------------------------------------
+__global__ void wave_zrows_kernel(const unsigned long long* __restrict__ q1,
+                                  const unsigned long long* __restrict__ q2,
+                                  const int64_t* __restrict__ n1, const int64_t* __restrict__ n2,
+                                  const int64_t* __restrict__ roff, double* __restrict__ zrow) {
+  const int m = blockIdx.x;
+  const int64_t a = n1[m], b = n2[m];
+  const double* Q1 = reinterpret_cast<const double*>(q1[m]);
+  const double* Q2 = reinterpret_cast<const double*>(q2[m]);
+  double* z = zrow + roff[m];
+  for (int64_t c = threadIdx.x; c < a + b; c += blockDim.x)
+    z[c] = c < a ? Q1[(a - 1) * a + c] : Q2[c - a];   // last row of Q1, first row of Q2
+}
+
+__global__ void wave_assemble_kernel(const unsigned long long* __restrict__ q1,
+                                     const unsigned long long* __restrict__ q2,
+                                     const int64_t* __restrict__ n1, const int64_t* __restrict__ n2,
+                                     const int64_t* __restrict__ roff,
+                                     const int32_t* __restrict__ row_merge,
+                                     const int64_t* __restrict__ src, double* __restrict__ W,
+                                     const int64_t* __restrict__ woff, int64_t nrows) {
+  for (int64_t gr = blockIdx.x; gr < nrows; gr += gridDim.x) {
+    const int m = row_merge[gr];
+    const int64_t a = n1[m], b = n2[m], n = a + b, row = gr - roff[m];
+    const double* Q1 = reinterpret_cast<const double*>(q1[m]);
+    const double* Q2 = reinterpret_cast<const double*>(q2[m]);
+    const int64_t* sm = src + roff[m];
+    double* w = W + woff[m] + row * n;
+    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
+      const int64_t sc = sm[c];
+      double v = 0.0;
+      if (row < a) { if (sc < a) v = Q1[row * a + sc]; }
+      else if (sc >= a) v = Q2[(row - a) * b + (sc - a)];
+      w[c] = v;
+    }
+  }
+}
+
+__global__ void wave_rotate_kernel(double* __restrict__ W, const int64_t* __restrict__ woff,
+                                   const int64_t* __restrict__ nn,
+                                   const int64_t* __restrict__ rot_off,
+                                   const int64_t* __restrict__ ca, const int64_t* __restrict__ cb,
+                                   const double* __restrict__ cs, const double* __restrict__ sn) {
+  const int m = blockIdx.y;
+  const int64_t n = nn[m], r0 = rot_off[m], r1 = rot_off[m + 1];
+  if (r0 == r1) return;
+  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    double* w = W + woff[m] + row * n;
+    for (int64_t t = r0; t < r1; ++t) {
+      const int64_t ia = ca[t], ib = cb[t];
+      const double c = cs[t], s = sn[t];
+      const double x = w[ia], y = w[ib];
+      w[ia] = __dadd_rn(__dmul_rn(c, x), __dmul_rn(s, y));
+      w[ib] = __dadd_rn(__dmul_rn(-s, x), __dmul_rn(c, y));
+    }
+  }
+}
+
+// out_m[:, c] = order[c] < k_m ? Qk_m[:, order[c]] : W_m[:, order[c]]
+__global__ void wave_gather_kernel(const double* __restrict__ Qk, const int64_t* __restrict__ qoff,
+                                   const int64_t* __restrict__ kept, const double* __restrict__ W,
+                                   const int64_t* __restrict__ woff, const int64_t* __restrict__ roff,
+                                   const int32_t* __restrict__ row_merge,
+                                   const int64_t* __restrict__ order, double* __restrict__ out,
+                                   const int64_t* __restrict__ ooff, int64_t nrows) {
+  for (int64_t gr = blockIdx.x; gr < nrows; gr += gridDim.x) {
+    const int m = row_merge[gr];
+    const int64_t n = roff[m + 1] - roff[m], row = gr - roff[m], k = kept[m];
+    const int64_t* om = order + roff[m];
+    const double* q = Qk + qoff[m] + row * k;
+    const double* w = W + woff[m] + row * n;
+    double* o = out + ooff[m] + row * n;
+    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
+      const int64_t sc = om[c];
+      o[c] = sc < k ? q[sc] : w[sc];
+    }
+  }
+}
+
 }  // namespace hsseig
 
 using namespace hsseig;
@@ -257,4 +342,146 @@ extern "C" int64_t hsseig_deflate(const double* d, const double* z, int64_t n, d
   *n_rot = nr;
   if (tol_out) *tol_out = tol;
   return (int64_t)kept.size();
+}
+
+// ---------------------------------------------------------------------------- wave ABI
+static unsigned rows_grid(int64_t nrows) { return (unsigned)std::min<int64_t>(nrows, 1 << 20); }
+
+extern "C" int hsseig_wave_zrows(const uint64_t* q1, const uint64_t* q2, const int64_t* n1,
+                                 const int64_t* n2, const int64_t* roff, int64_t nm, double* zrow,
+                                 void* stream) {
+  if (nm < 0 || !q1 || !q2 || !n1 || !n2 || !roff || !zrow) HSS_ARG_FAIL();
+  if (nm == 0) return HSSEIG_OK;
+  wave_zrows_kernel<<<(unsigned)nm, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const unsigned long long*>(q1), reinterpret_cast<const unsigned long long*>(q2),
+      n1, n2, roff, zrow);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_assemble(const uint64_t* q1, const uint64_t* q2, const int64_t* n1,
+                                    const int64_t* n2, const int64_t* roff, const int32_t* row_merge,
+                                    const int64_t* src, double* W, const int64_t* woff,
+                                    int64_t nrows, void* stream) {
+  if (nrows < 0 || !q1 || !q2 || !n1 || !n2 || !roff || !row_merge || !src || !W || !woff)
+    HSS_ARG_FAIL();
+  if (nrows == 0) return HSSEIG_OK;
+  wave_assemble_kernel<<<rows_grid(nrows), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const unsigned long long*>(q1), reinterpret_cast<const unsigned long long*>(q2),
+      n1, n2, roff, row_merge, src, W, woff, nrows);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_rotate(double* W, const int64_t* woff, const int64_t* n,
+                                  const int64_t* rot_off, const int64_t* ca, const int64_t* cb,
+                                  const double* c, const double* s, int64_t nm, int64_t nmax,
+                                  void* stream) {
+  if (nm < 0 || nmax < 0 || nm > 65535) HSS_ARG_FAIL();
+  if (nm == 0 || nmax == 0) return HSSEIG_OK;
+  dim3 grid((unsigned)std::min<int64_t>((nmax + 127) / 128, 1024), (unsigned)nm);
+  wave_rotate_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(W, woff, n, rot_off, ca, cb, c, s);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_gather(const double* Qk, const int64_t* qoff, const int64_t* kept,
+                                  const double* W, const int64_t* woff, const int64_t* roff,
+                                  const int32_t* row_merge, const int64_t* order, double* out,
+                                  const int64_t* ooff, int64_t nrows, void* stream) {
+  if (nrows < 0 || !W || !woff || !roff || !row_merge || !order || !out || !ooff || !kept || !qoff)
+    HSS_ARG_FAIL();
+  if (nrows == 0) return HSSEIG_OK;
+  wave_gather_kernel<<<rows_grid(nrows), 256, 0, (cudaStream_t)stream>>>(
+      Qk ? Qk : W, qoff, kept, W, woff, roff, row_merge, order, out, ooff, nrows);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+/*
+ * Host side of one depth of merges (dc.py:205-235 for every merge m of the depth):
+ * z from the boundary rows (theta = sign(b), 1/sqrt(2)), joint stable sort of [L1 L2],
+ * deflation (hsseig_deflate), the blockdiag column of every W slot (src, local) and the
+ * Givens rotations as W-column pairs.  rho == 0 merges (exactly decoupled) keep nothing
+ * and only sort.  Arrays over merges: n1, n2, bk, kept, rho_eff, rot_off (nm + 1);
+ * concatenated over rows (roff): L, zrow, d_out, z_out, src; rotations: ca, cb, rc, rs
+ * (capacity roff[nm]).  Returns the total number of kept roots.
+ */
+extern "C" int64_t hsseig_wave_deflate(int64_t nm, const int64_t* n1, const int64_t* n2,
+                                       const int64_t* roff, const double* L, const double* zrow,
+                                       const double* bk, int64_t* kept, double* rho_eff,
+                                       double* d_out, double* z_out, int64_t* src, int64_t* rot_off,
+                                       int64_t* ca, int64_t* cb, double* rc, double* rs) {
+  int64_t ktot = 0, nrot_tot = 0;
+  rot_off[0] = 0;
+  std::vector<int64_t> perm, dperm, ri, rj, posW;
+  std::vector<double> ds, zs, z, rcl, rsl;
+  for (int64_t m = 0; m < nm; ++m) {
+    const int64_t a = n1[m], n = a + n2[m], o = roff[m];
+    const double* Lm = L + o;
+    perm.resize(n);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(), [&](int64_t x, int64_t y) { return Lm[x] < Lm[y]; });
+    const double b = bk[m];
+    const double rho = std::fabs(b);
+    if (rho == 0.0) {   // dc.py:206-213: decoupled halves, merge by sorting only
+      kept[m] = 0;
+      rho_eff[m] = 0.0;
+      for (int64_t t = 0; t < n; ++t) { d_out[o + t] = Lm[perm[t]]; z_out[o + t] = 0.0; src[o + t] = perm[t]; }
+      rot_off[m + 1] = nrot_tot;
+      continue;
+    }
+    const double theta = b >= 0.0 ? 1.0 : -1.0;
+    z.resize(n);
+    for (int64_t t = 0; t < n; ++t) {
+      double zr = zrow[o + t];
+      if (t >= a) zr *= theta;
+      z[t] = zr / std::sqrt(2.0);
+    }
+    ds.resize(n); zs.resize(n);
+    for (int64_t t = 0; t < n; ++t) { ds[t] = Lm[perm[t]]; zs[t] = z[perm[t]]; }
+    dperm.resize(n); ri.resize(n); rj.resize(n); rcl.resize(n); rsl.resize(n);
+    int64_t nr = 0;
+    const int64_t k = hsseig_deflate(ds.data(), zs.data(), n, 2.0 * rho, d_out + o, z_out + o,
+                                     dperm.data(), ri.data(), rj.data(), rcl.data(), rsl.data(), &nr,
+                                     nullptr);
+    kept[m] = k;
+    rho_eff[m] = 2.0 * rho;
+    ktot += k;
+    posW.resize(n);
+    for (int64_t t = 0; t < n; ++t) {
+      src[o + t] = perm[dperm[t]];
+      posW[perm[dperm[t]]] = t;
+    }
+    for (int64_t t = 0; t < nr; ++t) {
+      ca[nrot_tot + t] = posW[perm[ri[t]]];
+      cb[nrot_tot + t] = posW[perm[rj[t]]];
+      rc[nrot_tot + t] = rcl[t];
+      rs[nrot_tot + t] = rsl[t];
+    }
+    nrot_tot += nr;
+    rot_off[m + 1] = nrot_tot;
+  }
+  return ktot;
+}
+
+/*
+ * Final order of every merge (dc.py:253-257): lam_cat = [roots, deflated poles], stable
+ * argsort.  lam (concatenated kept roots, koff) and d_out (rows) in; order / lam_out
+ * (rows) out.
+ */
+extern "C" int hsseig_wave_order(int64_t nm, const int64_t* roff, const int64_t* kept,
+                                 const int64_t* koff, const double* lam, const double* d_out,
+                                 int64_t* order, double* lam_out) {
+  std::vector<double> cat;
+  for (int64_t m = 0; m < nm; ++m) {
+    const int64_t o = roff[m], n = roff[m + 1] - o, k = kept[m];
+    cat.resize(n);
+    for (int64_t t = 0; t < n; ++t) cat[t] = t < k ? lam[koff[m] + t] : d_out[o + t];
+    int64_t* ord = order + o;
+    std::iota(ord, ord + n, 0);
+    std::stable_sort(ord, ord + n, [&](int64_t x, int64_t y) { return cat[x] < cat[y]; });
+    for (int64_t t = 0; t < n; ++t) lam_out[o + t] = cat[ord[t]];
+  }
+  return HSSEIG_OK;
 }

@@ -56,17 +56,13 @@ __global__ void square_sum_kernel(const double* __restrict__ z, int64_t k, doubl
   }
 }
 
-template <int R, int MINB>
-__global__ void __launch_bounds__(256, MINB) secular_kernel(
-    const double* __restrict__ d, const double* __restrict__ z2, const double* __restrict__ sumz2p,
-    int64_t k, double rho, int64_t ibeg, int64_t iend, double* __restrict__ lam,
+// Roots i0 .. i0+R-1 (those < iend) of one system, one warp; outputs at index i - ibeg.
+template <int R>
+__device__ __forceinline__ void secular_roots(
+    const double* __restrict__ d, const double* __restrict__ z2, double sumz2, int64_t k,
+    double rho, int64_t i0, int64_t ibeg, int64_t iend, double* __restrict__ lam,
     double* __restrict__ gam, double* __restrict__ mu, int32_t* __restrict__ iters,
-    hsseig_status* __restrict__ st) {
-  // roots [ibeg, iend) of the k; outputs are written at index i - ibeg
-  const int lane = threadIdx.x & 31;
-  const int64_t i0 = ibeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
-  if (i0 >= iend) return;
-  const double sumz2 = *sumz2p;
+    hsseig_status* __restrict__ st, int lane) {
 
   if (k == 1) {  // _kernels.pyx:204-209
     if (lane == 0) {
@@ -263,6 +259,19 @@ __global__ void __launch_bounds__(256, MINB) secular_kernel(
   }
 }
 
+template <int R, int MINB>
+__global__ void __launch_bounds__(256, MINB) secular_kernel(
+    const double* __restrict__ d, const double* __restrict__ z2, const double* __restrict__ sumz2p,
+    int64_t k, double rho, int64_t ibeg, int64_t iend, double* __restrict__ lam,
+    double* __restrict__ gam, double* __restrict__ mu, int32_t* __restrict__ iters,
+    hsseig_status* __restrict__ st) {
+  // roots [ibeg, iend) of the k; outputs are written at index i - ibeg
+  const int lane = threadIdx.x & 31;
+  const int64_t i0 = ibeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (i0 >= iend) return;
+  secular_roots<R>(d, z2, *sumz2p, k, rho, i0, ibeg, iend, lam, gam, mu, iters, st, lane);
+}
+
 // dnext[j] = d[j+1]; dnext[k-1] = d[k-1] + gamma[k-1] + mu[k-1]  (secular.py:199)
 __global__ void dnext_kernel(const double* __restrict__ d, const double* __restrict__ gam,
                              const double* __restrict__ mu, int64_t k, double* __restrict__ dn) {
@@ -273,13 +282,11 @@ __global__ void dnext_kernel(const double* __restrict__ d, const double* __restr
 
 // zhat_i = sign(z_i) sqrt( prod_{j!=i} (lam_j - d_i)/(d_j - d_i) * gamma_i / rho )
 template <int R>
-__global__ void __launch_bounds__(256) loewner_kernel(
+__device__ __forceinline__ void loewner_rows(
     const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
     const double* __restrict__ mu, const double* __restrict__ z, int64_t k, double rho,
-    int64_t ibeg, int64_t iend, double* __restrict__ zhat, hsseig_status* __restrict__ st) {
-  const int lane = threadIdx.x & 31;
-  const int64_t i0 = ibeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
-  if (i0 >= iend) return;
+    int64_t i0, int64_t ibeg, int64_t iend, double* __restrict__ zhat,
+    hsseig_status* __restrict__ st, int lane) {
   double di[R], pr[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -313,15 +320,23 @@ __global__ void __launch_bounds__(256) loewner_kernel(
   }
 }
 
+template <int R>
+__global__ void __launch_bounds__(256) loewner_kernel(
+    const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
+    const double* __restrict__ mu, const double* __restrict__ z, int64_t k, double rho,
+    int64_t ibeg, int64_t iend, double* __restrict__ zhat, hsseig_status* __restrict__ st) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i0 = ibeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (i0 >= iend) return;
+  loewner_rows<R>(d, dn, gam, mu, z, k, rho, i0, ibeg, iend, zhat, st, lane);
+}
+
 // v_j = 1 / sqrt( sum_i (zhat_i / (d_i - lam_j))^2 )
 template <int R>
-__global__ void __launch_bounds__(256) normalizer_kernel(
+__device__ __forceinline__ void normalizer_cols(
     const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
-    const double* __restrict__ mu, const double* __restrict__ zh, int64_t k, int64_t jbeg,
-    int64_t jend, double* __restrict__ v) {
-  const int lane = threadIdx.x & 31;
-  const int64_t j0 = jbeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
-  if (j0 >= jend) return;
+    const double* __restrict__ mu, const double* __restrict__ zh, int64_t k, int64_t j0,
+    int64_t jbeg, int64_t jend, double* __restrict__ v, int lane) {
   double dj[R], dnj[R], gj[R], mj[R], s[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -346,6 +361,92 @@ __global__ void __launch_bounds__(256) normalizer_kernel(
     double t = warp_sum(s[r]);
     if (lane == 0 && j0 + r < jend) v[j0 + r - jbeg] = 1.0 / sqrt(t);
   }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) normalizer_kernel(
+    const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
+    const double* __restrict__ mu, const double* __restrict__ zh, int64_t k, int64_t jbeg,
+    int64_t jend, double* __restrict__ v) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j0 = jbeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * R;
+  if (j0 >= jend) return;
+  normalizer_cols<R>(d, dn, gam, mu, zh, k, j0, jbeg, jend, v, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Level-batched ("wave") variants: every rank-one system of one recursion depth in one
+// launch.  System s owns roots [koff[s], koff[s+1]) of the concatenated arrays; seg_of
+// maps a root to its system.  One warp per root / row / column (R = 1), so a warp never
+// straddles two systems.
+// ---------------------------------------------------------------------------
+__global__ void wave_square_sum_kernel(const double* __restrict__ z, const int64_t* __restrict__ koff,
+                                       double* __restrict__ z2, double* __restrict__ sums) {
+  const int s = blockIdx.x;
+  const int64_t a = koff[s], k = koff[s + 1] - a;
+  __shared__ double part[32];
+  double acc = 0.0;
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    const double q = z[a + j] * z[a + j];
+    z2[a + j] = q;
+    acc += q;
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double t = (threadIdx.x < (blockDim.x >> 5)) ? part[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) sums[s] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) wave_secular_kernel(
+    const double* __restrict__ d, const double* __restrict__ z2, const double* __restrict__ sums,
+    const int64_t* __restrict__ koff, const int32_t* __restrict__ seg_of,
+    const double* __restrict__ rho, int64_t ntot, double* __restrict__ lam, double* __restrict__ gam,
+    double* __restrict__ mu, int32_t* __restrict__ iters, hsseig_status* __restrict__ st) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= ntot) return;
+  const int s = seg_of[g];
+  const int64_t a = koff[s], k = koff[s + 1] - a;
+  secular_roots<1>(d + a, z2 + a, sums[s], k, rho[s], g - a, 0, k, lam + a, gam + a, mu + a,
+                   iters + a, st + s, threadIdx.x & 31);
+}
+
+__global__ void wave_dnext_kernel(const double* __restrict__ d, const double* __restrict__ gam,
+                                  const double* __restrict__ mu, const int64_t* __restrict__ koff,
+                                  const int32_t* __restrict__ seg_of, int64_t ntot,
+                                  double* __restrict__ dn) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ntot) return;
+  const int64_t last = koff[seg_of[g] + 1] - 1;
+  dn[g] = (g < last) ? d[g + 1] : (d[last] + gam[last]) + mu[last];
+}
+
+__global__ void __launch_bounds__(256) wave_loewner_kernel(
+    const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
+    const double* __restrict__ mu, const double* __restrict__ z, const int64_t* __restrict__ koff,
+    const int32_t* __restrict__ seg_of, const double* __restrict__ rho, int64_t ntot,
+    double* __restrict__ zhat, hsseig_status* __restrict__ st) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= ntot) return;
+  const int s = seg_of[g];
+  const int64_t a = koff[s], k = koff[s + 1] - a;
+  loewner_rows<1>(d + a, dn + a, gam + a, mu + a, z + a, k, rho[s], g - a, 0, k, zhat + a, st + s,
+                  threadIdx.x & 31);
+}
+
+__global__ void __launch_bounds__(256) wave_normalizer_kernel(
+    const double* __restrict__ d, const double* __restrict__ dn, const double* __restrict__ gam,
+    const double* __restrict__ mu, const double* __restrict__ zh, const int64_t* __restrict__ koff,
+    const int32_t* __restrict__ seg_of, int64_t ntot, double* __restrict__ v) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= ntot) return;
+  const int s = seg_of[g];
+  const int64_t a = koff[s], k = koff[s + 1] - a;
+  normalizer_cols<1>(d + a, dn + a, gam + a, mu + a, zh + a, k, g - a, 0, k, v + a,
+                     threadIdx.x & 31);
 }
 
 }  // namespace hsseig
@@ -449,4 +550,59 @@ extern "C" int hsseig_normalizers(const double* d, const double* dnext, const do
                                   const double* mu, const double* zhat, int64_t k, double* v,
                                   void* stream) {
   return hsseig_normalizers_part(d, dnext, gamma, mu, zhat, k, 0, k, v, stream);
+}
+
+// ---------------------------------------------------------------------------- wave ABI
+extern "C" int hsseig_wave_secular(const double* d, const double* z, const int64_t* koff,
+                                   const int32_t* seg_of, const double* rho, int64_t nseg,
+                                   int64_t ntot, double* lam, double* gamma, double* mu,
+                                   int32_t* iters, double* work, hsseig_status* st, void* stream) {
+  if (nseg < 0 || ntot < 0 || !d || !z || !koff || !seg_of || !rho || !lam || !gamma || !mu ||
+      !iters || !work || !st)
+    HSS_ARG_FAIL();
+  if (nseg == 0 || ntot == 0) return HSSEIG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* z2 = work;
+  double* sums = work + ntot;
+  wave_square_sum_kernel<<<(unsigned)nseg, 256, 0, s>>>(z, koff, z2, sums);
+  HSS_CHECK_LAUNCH();
+  wave_secular_kernel<<<(unsigned)((ntot + 7) / 8), 256, 0, s>>>(d, z2, sums, koff, seg_of, rho, ntot,
+                                                                 lam, gamma, mu, iters, st);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_dnext(const double* d, const double* gamma, const double* mu,
+                                 const int64_t* koff, const int32_t* seg_of, int64_t ntot,
+                                 double* dnext, void* stream) {
+  if (ntot < 0) HSS_ARG_FAIL();
+  if (ntot == 0) return HSSEIG_OK;
+  wave_dnext_kernel<<<(unsigned)((ntot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      d, gamma, mu, koff, seg_of, ntot, dnext);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_loewner(const double* d, const double* dnext, const double* gamma,
+                                   const double* mu, const double* z, const int64_t* koff,
+                                   const int32_t* seg_of, const double* rho, int64_t ntot,
+                                   double* zhat, hsseig_status* st, void* stream) {
+  if (ntot < 0) HSS_ARG_FAIL();
+  if (ntot == 0) return HSSEIG_OK;
+  wave_loewner_kernel<<<(unsigned)((ntot + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
+      d, dnext, gamma, mu, z, koff, seg_of, rho, ntot, zhat, st);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_normalizers(const double* d, const double* dnext, const double* gamma,
+                                       const double* mu, const double* zhat, const int64_t* koff,
+                                       const int32_t* seg_of, int64_t ntot, double* v,
+                                       void* stream) {
+  if (ntot < 0) HSS_ARG_FAIL();
+  if (ntot == 0) return HSSEIG_OK;
+  wave_normalizer_kernel<<<(unsigned)((ntot + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
+      d, dnext, gamma, mu, zhat, koff, seg_of, ntot, v);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
 }

@@ -20,8 +20,11 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .dc import BaseCaseError, EigenResult, MergeRecord, SolverConfig, merge_update
-from .flops import FlopCounter
+from .cauchy import CauchyEvecMatrix
+from .dc import (BaseCaseError, EigenResult, MergeRecord, SolverConfig, merge_update,
+                 update_vectors_hss)
+from .flops import FlopCounter, cauchy_eval_flops, gemm_flops, secular_flops
+from .secular import SecularConvergenceError, WeightRecomputationError
 
 _SQRT2 = np.sqrt(2.0)
 MAX_BASE = 32
@@ -81,8 +84,8 @@ def _base_cases(a_mod, b, leaves, stream):
     return out
 
 
-def adc_solve(T, cfg=None):
-    """Full eigendecomposition of SymTridiagonal T (dc.py:174-191), merges on the GPU."""
+def adc_solve_recursive(T, cfg=None):
+    """Full eigendecomposition of SymTridiagonal T (dc.py:174-191), one merge at a time."""
     cfg = cfg or SolverConfig()
     if not (np.all(np.isfinite(T.a)) and np.all(np.isfinite(T.b))):
         raise ValueError("matrix has non-finite entries")
@@ -171,4 +174,242 @@ def adc_solve(T, cfg=None):
         return lam_cat[order], W
 
     lam, Q = rec(0, T.n)
+    return EigenResult(lam=lam, Q=Q, merges=merges, flops=flops)
+
+
+# ----------------------------------------------------------------------------------------
+# Level-batched schedule: every merge of one recursion depth runs in one set of launches.
+# ----------------------------------------------------------------------------------------
+def _tree(n, base):
+    """Recursion nodes (dc.py:194-203): split at n // 2, merge ids in postorder."""
+    nodes = []
+    ids = itertools.count()
+
+    def rec(lo, hi, depth):
+        if hi - lo <= base:
+            nodes.append({"lo": lo, "hi": hi, "depth": depth, "leaf": True})
+            return len(nodes) - 1
+        m = lo + (hi - lo) // 2
+        left = rec(lo, m, depth + 1)
+        right = rec(m, hi, depth + 1)
+        nodes.append({"lo": lo, "hi": hi, "depth": depth, "leaf": False, "left": left,
+                      "right": right, "split": m, "mid": next(ids)})
+        return len(nodes) - 1
+
+    root = rec(0, n, 0)
+    return nodes, root
+
+
+def _u64(ptrs):
+    return torch.as_tensor(np.asarray(ptrs, dtype=np.uint64).view(np.int64), device="cuda")
+
+
+def _i32(x):
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int32), device="cuda")
+
+
+def _cptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def adc_solve(T, cfg=None):
+    """Full eigendecomposition of SymTridiagonal T (dc.py:174-257), level-batched on the GPU.
+
+    The recursion, split, deflation, merge ids (HSS sample seeds) and merge records are
+    the reference's.  All merges of one depth share their launches: boundary rows ->
+    host deflation (one C call) -> assembly + Givens replay -> segmented secular /
+    Loewner / normalizers -> grouped dense updates (HSS merges individually) -> final
+    column order.  Two host synchronisations per depth.
+    """
+    cfg = cfg or SolverConfig()
+    if not (np.all(np.isfinite(T.a)) and np.all(np.isfinite(T.b))):
+        raise ValueError("matrix has non-finite entries")
+    if cfg.base_size > MAX_BASE:
+        raise ValueError(f"base_size above {MAX_BASE} is not supported by the device base case")
+    nat.require_cuda()
+    lib = nat.load()
+    s = nat.stream_ptr()
+    f64 = dict(dtype=torch.float64, device="cuda")
+    flops = FlopCounter()
+    a = np.asarray(T.a, dtype=np.float64)
+    b = np.asarray(T.b, dtype=np.float64)
+    a_mod, leaves = _plan(a, b, cfg.base_size)
+    base = _base_cases(a_mod, b, leaves, s)
+    nodes, root = _tree(T.n, cfg.base_size)
+    state = {}       # node -> (lam host, Q device view n x n)
+    for i, nd in enumerate(nodes):
+        if nd["leaf"]:
+            state[i] = base[(nd["lo"], nd["hi"])]
+    records = {}
+    bm = ctypes.c_int32(0)
+    bn = ctypes.c_int32(0)
+    lib.hsseig_wave_tile_shape(ctypes.byref(bm), ctypes.byref(bn))
+    bm, bn = bm.value, bn.value
+    maxdepth = max(nd["depth"] for nd in nodes)
+    for depth in range(maxdepth - 1, -1, -1):
+        ms = [i for i, nd in enumerate(nodes) if nd["depth"] == depth and not nd["leaf"]]
+        if not ms:
+            continue
+        nm = len(ms)
+        n1 = np.array([nodes[i]["split"] - nodes[i]["lo"] for i in ms], dtype=np.int64)
+        n2 = np.array([nodes[i]["hi"] - nodes[i]["split"] for i in ms], dtype=np.int64)
+        nv = n1 + n2
+        roff = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
+        nrows = int(roff[-1])
+        kids = [(state.pop(nodes[i]["left"]), state.pop(nodes[i]["right"])) for i in ms]
+        L = np.concatenate([np.concatenate([c1[0], c2[0]]) for c1, c2 in kids])
+        q1 = _u64([c1[1].data_ptr() for c1, _ in kids])
+        q2 = _u64([c2[1].data_ptr() for _, c2 in kids])
+        n1_d, n2_d, nv_d, roff_d = _i64(n1), _i64(n2), _i64(nv), _i64(roff)
+        # boundary rows -> host (sync 1)
+        zrow_d = torch.empty(nrows, **f64)
+        nat.check(lib.hsseig_wave_zrows(nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
+                                        nat.ptr(roff_d), nm, nat.ptr(zrow_d), s), "wave_zrows")
+        zrow = zrow_d.cpu().numpy()
+        bk = np.array([b[nodes[i]["split"] - 1] for i in ms], dtype=np.float64)
+        kept = np.empty(nm, dtype=np.int64)
+        rho_eff = np.empty(nm)
+        d_out, z_out = np.empty(nrows), np.empty(nrows)
+        src = np.empty(nrows, dtype=np.int64)
+        rot_off = np.empty(nm + 1, dtype=np.int64)
+        ca, cb = np.empty(nrows, dtype=np.int64), np.empty(nrows, dtype=np.int64)
+        rc, rs = np.empty(nrows), np.empty(nrows)
+        ktot = int(lib.hsseig_wave_deflate(nm, _cptr(n1), _cptr(n2), _cptr(roff), _cptr(L),
+                                           _cptr(zrow), _cptr(bk), _cptr(kept), _cptr(rho_eff),
+                                           _cptr(d_out), _cptr(z_out), _cptr(src), _cptr(rot_off),
+                                           _cptr(ca), _cptr(cb), _cptr(rc), _cptr(rs)))
+        # W blocks in [kept | deflated] column order, then the rotations
+        woff = np.concatenate([[0], np.cumsum(nv * nv)]).astype(np.int64)
+        W = torch.empty(int(woff[-1]), **f64)
+        woff_d = _i64(woff)
+        row_merge = _i32(np.repeat(np.arange(nm), nv))
+        nat.check(lib.hsseig_wave_assemble(nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
+                                           nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(_i64(src)),
+                                           nat.ptr(W), nat.ptr(woff_d), nrows, s), "wave_assemble")
+        del kids, q1, q2
+        nrot = int(rot_off[-1])
+        if nrot:
+            nat.check(lib.hsseig_wave_rotate(nat.ptr(W), nat.ptr(woff_d), nat.ptr(nv_d),
+                                             nat.ptr(_i64(rot_off)), nat.ptr(_i64(ca[:nrot])),
+                                             nat.ptr(_i64(cb[:nrot])), nat.ptr(_f64(rc[:nrot])),
+                                             nat.ptr(_f64(rs[:nrot])), nm, int(nv.max()), s),
+                      "wave_rotate")
+        # the kept rank-one systems, concatenated
+        segs = np.flatnonzero(kept > 0)
+        nseg = len(segs)
+        ks = kept[segs]
+        koff = np.concatenate([[0], np.cumsum(ks)]).astype(np.int64)
+        kidx = np.repeat(roff[segs] - koff[:-1], ks) + np.arange(ktot)
+        qoff = np.concatenate([[0], np.cumsum(nv * kept)]).astype(np.int64)
+        Qk = torch.empty(max(int(qoff[-1]), 1), **f64)
+        hss_m = set()
+        seg_iters = np.zeros(nseg, dtype=np.int64)
+        if nseg:
+            dk, zk = _f64(d_out[kidx]), _f64(z_out[kidx])
+            koff_d, seg_of = _i64(koff), _i32(np.repeat(np.arange(nseg), ks))
+            rho_d = _f64(rho_eff[segs])
+            lam_k, gam, mu, dn, zh, vv = (torch.empty(ktot, **f64) for _ in range(6))
+            its = torch.empty(ktot, dtype=torch.int32, device="cuda")
+            st0 = np.zeros((nseg, 8), dtype=np.int64)
+            st0[:, 1:4] = ks[:, None]
+            st = torch.as_tensor(st0, device="cuda")
+            work = torch.empty(ktot + nseg, **f64)
+            nat.check(lib.hsseig_wave_secular(nat.ptr(dk), nat.ptr(zk), nat.ptr(koff_d), nat.ptr(seg_of),
+                                              nat.ptr(rho_d), nseg, ktot, nat.ptr(lam_k), nat.ptr(gam),
+                                              nat.ptr(mu), nat.ptr(its), nat.ptr(work), nat.ptr(st), s),
+                      "wave_secular")
+            nat.check(lib.hsseig_wave_dnext(nat.ptr(dk), nat.ptr(gam), nat.ptr(mu), nat.ptr(koff_d),
+                                            nat.ptr(seg_of), ktot, nat.ptr(dn), s), "wave_dnext")
+            nat.check(lib.hsseig_wave_loewner(nat.ptr(dk), nat.ptr(dn), nat.ptr(gam), nat.ptr(mu),
+                                              nat.ptr(zk), nat.ptr(koff_d), nat.ptr(seg_of),
+                                              nat.ptr(rho_d), ktot, nat.ptr(zh), nat.ptr(st), s),
+                      "wave_loewner")
+            nat.check(lib.hsseig_wave_normalizers(nat.ptr(dk), nat.ptr(dn), nat.ptr(gam), nat.ptr(mu),
+                                                  nat.ptr(zh), nat.ptr(koff_d), nat.ptr(seg_of), ktot,
+                                                  nat.ptr(vv), s), "wave_normalizers")
+            # dense updates of every system not taking the HSS path, grouped in one launch
+            tasks = []
+            for q, m in enumerate(segs):
+                n, k = int(nv[m]), int(kept[m])
+                if cfg.method == "adc-rand" and k > cfg.hss_threshold:
+                    hss_m.add(q)
+                    continue
+                mt, nt = -(-n // bm), -(-k // bn)
+                t = np.empty((mt * nt, 3), dtype=np.int32)
+                t[:, 0] = q
+                t[:, 1] = np.repeat(np.arange(mt), nt)
+                t[:, 2] = np.tile(np.arange(nt), mt)
+                tasks.append(t)
+            if tasks:
+                tk = np.concatenate(tasks)
+                nat.check(lib.hsseig_wave_dense_update(
+                    nat.ptr(W), nat.ptr(_i64(woff[segs])), nat.ptr(_i64(nv[segs])), nat.ptr(dk),
+                    nat.ptr(dn), nat.ptr(gam), nat.ptr(mu), nat.ptr(zh), nat.ptr(vv), nat.ptr(koff_d),
+                    nat.ptr(Qk), nat.ptr(_i64(qoff[segs])), nat.ptr(_i32(tk.ravel())), len(tk), s),
+                    "wave_dense_update")
+            # statuses + roots (sync 2)
+            stv = st.cpu().numpy()
+            for q, m in enumerate(segs):
+                k = int(ks[q])
+                if stv[q, 1] < k or (k >= 2 and stv[q, 2] < k):
+                    bad = int(stv[q, 1] if stv[q, 1] < k else stv[q, 2])
+                    raise SecularConvergenceError(f"root {bad} lost its bracket")
+                if stv[q, 3] < k:
+                    raise WeightRecomputationError(f"non-positive radicand at index {int(stv[q, 3])}")
+            seg_iters = stv[:, 0]
+            for q in sorted(hss_m):
+                m = segs[q]
+                n, k = int(nv[m]), int(kept[m])
+                sl = slice(int(koff[q]), int(koff[q + 1]))
+                C = CauchyEvecMatrix(dk[sl], gam[sl], mu[sl], zh[sl], vv[sl], dnext=dn[sl])
+                nd = nodes[ms[m]]
+                rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
+                fc = FlopCounter()
+                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, n)
+                out = update_vectors_hss(Wm[:, :k], C, cfg, seed=[cfg.seed, nd["mid"]], flops=fc,
+                                         record=rec_)
+                Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k).copy_(out)
+                rec_.flops = fc.as_dict()
+                del out
+            lam_h = lam_k.cpu().numpy()
+        else:
+            lam_h = np.zeros(0)
+        # final column order of every merge
+        order = np.empty(nrows, dtype=np.int64)
+        lam_out = np.empty(nrows)
+        koff_all = np.zeros(nm, dtype=np.int64)
+        koff_all[segs] = koff[:-1]
+        lib.hsseig_wave_order(nm, _cptr(roff), _cptr(kept), _cptr(koff_all), _cptr(lam_h),
+                              _cptr(d_out), _cptr(order), _cptr(lam_out))
+        A = torch.empty(int(woff[-1]), **f64)
+        nat.check(lib.hsseig_wave_gather(nat.ptr(Qk), nat.ptr(_i64(qoff)), nat.ptr(_i64(kept)),
+                                         nat.ptr(W), nat.ptr(woff_d), nat.ptr(roff_d),
+                                         nat.ptr(row_merge), nat.ptr(_i64(order)), nat.ptr(A),
+                                         nat.ptr(woff_d), nrows, s), "wave_gather")
+        del W, Qk
+        # records and flop counts (reference conventions, dc.py:236-247)
+        for q, m in enumerate(segs):
+            nd = nodes[ms[m]]
+            n, k = int(nv[m]), int(kept[m])
+            sec = secular_flops(k, int(seg_iters[q])) + 14 * k * k
+            if q in hss_m:
+                rec_ = records[nd["mid"]]
+                rec_.flops["secular"] = rec_.flops.get("secular", 0) + sec
+            else:
+                rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
+                rec_.flops = {"secular": sec, "update_dense": cauchy_eval_flops(k * k) + gemm_flops(n, k, k),
+                              "hss_construct": 0, "hss_mult": 0}
+        for m in range(nm):
+            nd = nodes[ms[m]]
+            n = int(nv[m])
+            if kept[m] == 0 and rho_eff[m] != 0.0:
+                records.setdefault(nd["mid"], MergeRecord(size=n, kept=0, n_deflated=n)).flops = \
+                    {p: 0 for p in FlopCounter.PHASES}
+            state[ms[m]] = (lam_out[roff[m]:roff[m + 1]].copy(),
+                            A[int(woff[m]):int(woff[m + 1])].view(n, n))
+    lam, Q = state[root]
+    merges = [records[k] for k in sorted(records)]
+    for r in merges:
+        for p_ in FlopCounter.PHASES:
+            setattr(flops, p_, getattr(flops, p_) + r.flops.get(p_, 0))
     return EigenResult(lam=lam, Q=Q, merges=merges, flops=flops)

@@ -112,3 +112,76 @@ def test_config_generators():
     ev = np.linalg.eigvalsh(T.to_dense())
     np.testing.assert_allclose(np.sort(ev), np.sort(2 + 2 * np.cos(np.arange(1, 51) * np.pi / 51)),
                                atol=1e-13)
+
+
+def test_wave_deflate_matches_oracle_deflation():
+    # host side of the level-batched merges (csrc/glue.cu hsseig_wave_deflate / _order)
+    # against the oracle's restatement of secular.py:91-156 and dc.py:205-257, merge by merge
+    import ctypes
+    from oracle import hss_oracle as orc
+    from paper_1510_04591_b200 import _native as nat
+    lib = nat.load(build_if_missing=False)
+    rng = np.random.default_rng(5)
+    sizes = [(3, 4), (12, 13), (25, 25), (7, 8), (30, 31)]
+    L, Z, bk = [], [], []
+    for t, (a, b) in enumerate(sizes):
+        l1, l2 = np.sort(rng.uniform(-1, 1, a)), np.sort(rng.uniform(-1, 1, b))
+        if t == 1:                      # a near-duplicate pole pair -> Givens rotation
+            l2[3] = l1[5] + 1e-17
+        z = rng.standard_normal(a + b)
+        if t == 2:
+            z[4] = 1e-20                # negligible weight -> deflated at its pole
+        L.append(np.concatenate([l1, l2]))
+        Z.append(z)
+        bk.append([0.7, -0.3, 1.1, 0.0, -2.0][t])
+    nm = len(sizes)
+    n1 = np.array([s[0] for s in sizes], dtype=np.int64)
+    n2 = np.array([s[1] for s in sizes], dtype=np.int64)
+    nv = n1 + n2
+    roff = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
+    Lc, Zc, bkc = np.concatenate(L), np.concatenate(Z), np.array(bk)
+    nr = int(roff[-1])
+    kept, rho_eff = np.empty(nm, dtype=np.int64), np.empty(nm)
+    d_out, z_out, src = np.empty(nr), np.empty(nr), np.empty(nr, dtype=np.int64)
+    rot_off = np.empty(nm + 1, dtype=np.int64)
+    ca, cb, rc, rs = (np.empty(nr, dtype=np.int64), np.empty(nr, dtype=np.int64), np.empty(nr),
+                      np.empty(nr))
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    ktot = lib.hsseig_wave_deflate(nm, P(n1), P(n2), P(roff), P(Lc), P(Zc), P(bkc), P(kept),
+                                   P(rho_eff), P(d_out), P(z_out), P(src), P(rot_off), P(ca), P(cb),
+                                   P(rc), P(rs))
+    assert ktot == kept.sum()
+    for m in range(nm):
+        o, n, a = roff[m], nv[m], n1[m]
+        if bk[m] == 0.0:                 # decoupled: sort only
+            assert kept[m] == 0 and rot_off[m + 1] == rot_off[m]
+            assert np.array_equal(src[o:o + n], np.argsort(L[m], kind="stable"))
+            continue
+        th = 1.0 if bk[m] >= 0 else -1.0
+        z = np.concatenate([Z[m][:a], th * Z[m][a:]]) / np.sqrt(2.0)
+        pm = np.argsort(L[m], kind="stable")
+        dk, zk, dperm, rots, ldef, nd = orc.deflate(L[m][pm], z[pm], 2.0 * abs(bk[m]))
+        k = dk.size
+        assert kept[m] == k and rho_eff[m] == 2.0 * abs(bk[m])
+        assert np.array_equal(d_out[o:o + k], dk) and np.array_equal(z_out[o:o + k], zk)
+        assert np.array_equal(d_out[o + k:o + n], ldef)
+        assert np.array_equal(src[o:o + n], pm[dperm])
+        pos = np.empty(n, dtype=np.int64)
+        pos[pm[dperm]] = np.arange(n)
+        r0, r1 = rot_off[m], rot_off[m + 1]
+        assert r1 - r0 == len(rots)
+        for t, (i, j, c, s) in enumerate(rots):
+            assert ca[r0 + t] == pos[pm[i]] and cb[r0 + t] == pos[pm[j]]
+            assert rc[r0 + t] == c and rs[r0 + t] == s
+    assert kept[1] < nv[1] and kept[2] < nv[2]      # both deflation kinds exercised
+    # final order: stable argsort of [roots, deflated poles]
+    koff = np.concatenate([[0], np.cumsum(kept)]).astype(np.int64)
+    lam = np.concatenate([np.sort(rng.uniform(-3, 3, k)) for k in kept])
+    order, lam_out = np.empty(nr, dtype=np.int64), np.empty(nr)
+    lib.hsseig_wave_order(nm, P(roff), P(kept), P(koff[:-1].copy()), P(lam), P(d_out), P(order),
+                          P(lam_out))
+    for m in range(nm):
+        o, n, k = roff[m], nv[m], kept[m]
+        cat = np.concatenate([lam[koff[m]:koff[m] + k], d_out[o + k:o + n]])
+        ref = np.argsort(cat, kind="stable")
+        assert np.array_equal(order[o:o + n], ref) and np.array_equal(lam_out[o:o + n], cat[ref])
