@@ -282,17 +282,20 @@ def adc_solve(T, cfg=None):
         woff = np.concatenate([[0], np.cumsum(nv * nv)]).astype(np.int64)
         W = torch.empty(int(woff[-1]), **f64)
         woff_d = _i64(woff)
+        # (device temporaries stay referenced until their launch: a freed block is reused
+        #  by the next upload on the same stream)
         row_merge = _i32(np.repeat(np.arange(nm), nv))
+        src_d = _i64(src)
         nat.check(lib.hsseig_wave_assemble(nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
-                                           nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(_i64(src)),
+                                           nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(src_d),
                                            nat.ptr(W), nat.ptr(woff_d), nrows, s), "wave_assemble")
         del kids, q1, q2
         nrot = int(rot_off[-1])
         if nrot:
+            rot_d = (_i64(rot_off), _i64(ca[:nrot]), _i64(cb[:nrot]), _f64(rc[:nrot]),
+                     _f64(rs[:nrot]))
             nat.check(lib.hsseig_wave_rotate(nat.ptr(W), nat.ptr(woff_d), nat.ptr(nv_d),
-                                             nat.ptr(_i64(rot_off)), nat.ptr(_i64(ca[:nrot])),
-                                             nat.ptr(_i64(cb[:nrot])), nat.ptr(_f64(rc[:nrot])),
-                                             nat.ptr(_f64(rs[:nrot])), nm, int(nv.max()), s),
+                                             *(nat.ptr(t) for t in rot_d), nm, int(nv.max()), s),
                       "wave_rotate")
         # the kept rank-one systems, concatenated
         segs = np.flatnonzero(kept > 0)
@@ -342,10 +345,11 @@ def adc_solve(T, cfg=None):
                 tasks.append(t)
             if tasks:
                 tk = np.concatenate(tasks)
+                dd_ = (_i64(woff[segs]), _i64(nv[segs]), _i64(qoff[segs]), _i32(tk.ravel()))
                 nat.check(lib.hsseig_wave_dense_update(
-                    nat.ptr(W), nat.ptr(_i64(woff[segs])), nat.ptr(_i64(nv[segs])), nat.ptr(dk),
+                    nat.ptr(W), nat.ptr(dd_[0]), nat.ptr(dd_[1]), nat.ptr(dk),
                     nat.ptr(dn), nat.ptr(gam), nat.ptr(mu), nat.ptr(zh), nat.ptr(vv), nat.ptr(koff_d),
-                    nat.ptr(Qk), nat.ptr(_i64(qoff[segs])), nat.ptr(_i32(tk.ravel())), len(tk), s),
+                    nat.ptr(Qk), nat.ptr(dd_[2]), nat.ptr(dd_[3]), len(tk), s),
                     "wave_dense_update")
             # statuses + roots (sync 2)
             stv = st.cpu().numpy()
@@ -382,9 +386,10 @@ def adc_solve(T, cfg=None):
         lib.hsseig_wave_order(nm, _cptr(roff), _cptr(kept), _cptr(koff_all), _cptr(lam_h),
                               _cptr(d_out), _cptr(order), _cptr(lam_out))
         A = torch.empty(int(woff[-1]), **f64)
-        nat.check(lib.hsseig_wave_gather(nat.ptr(Qk), nat.ptr(_i64(qoff)), nat.ptr(_i64(kept)),
+        g_ = (_i64(qoff), _i64(kept), _i64(order))
+        nat.check(lib.hsseig_wave_gather(nat.ptr(Qk), nat.ptr(g_[0]), nat.ptr(g_[1]),
                                          nat.ptr(W), nat.ptr(woff_d), nat.ptr(roff_d),
-                                         nat.ptr(row_merge), nat.ptr(_i64(order)), nat.ptr(A),
+                                         nat.ptr(row_merge), nat.ptr(g_[2]), nat.ptr(A),
                                          nat.ptr(woff_d), nrows, s), "wave_gather")
         del W, Qk
         # records and flop counts (reference conventions, dc.py:236-247)
