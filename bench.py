@@ -185,10 +185,12 @@ def measure_dgemm_peak(torch):
 
 
 def eigh_lines():
-    """Full tridiagonal eigendecompositions (BASELINE configs 1-3) on the GPU: wall-s + accuracy.
+    """Full tridiagonal eigendecompositions (BASELINE configs 1, 2, 3, 5) on one GPU: wall-s
+    + accuracy (config 2 with ADC2: ADC1 has no reference implementation).
 
     CPU reference wall-s for the same configs (survey container, 8 cores) is in BASELINE.md:
-    1.32 s / 22.05 s / 124.5 s.
+    1.32 s / 22.05 s / 124.5 s; config 5 at N=65536 does not fit the reference's host
+    memory (48.3 s at N=16384).
     """
     import torch
 
@@ -202,6 +204,7 @@ def eigh_lines():
          np.sort(2 + 2 * np.cos(np.arange(1, 10001) * np.pi / 10001))),
         ("cfg3_kac_N20000", hb.gen_kac(20000), hb.SolverConfig(rank_eps=1e-13),
          -(20000 - 1) + 2.0 * np.arange(20000)),
+        ("cfg5_N65536", hb.gen_config5(65536, 0), hb.SolverConfig(rank_eps=1e-13), None),
     ]
     for name, T, cfg, exact in cases:
         hb.adc_solve(T, cfg)   # warm-up (allocator, tree buffers)
