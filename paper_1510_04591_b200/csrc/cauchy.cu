@@ -11,6 +11,9 @@
 // blockIdx.y; partial tiles go to a workspace and are summed in a fixed order so
 // the result is deterministic run to run (the reference's determinism-in-seed
 // contract, pkg/tests/test_hss.py:192-200).
+#include <cstdlib>
+#include <vector>
+
 #include "tma.cuh"
 
 namespace hsseig {
@@ -315,6 +318,182 @@ static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int
   return HSSEIG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Materialised sampling: the Cauchy panel is generated once into HBM (FP64 pipe,
+// HBM-write bound) and both products run on the TMA/DMMA engine without generator work
+// competing for the FP64 issue slots:  Y_R = C[R, :] Omega   and   Z_R^T = Omega^T C[:, R].
+// ---------------------------------------------------------------------------
+constexpr double kMatCapBytes = 12.0 * (1 << 30);   // largest panel pair materialised
+
+// out[i][j] = C[i0 + i][j0 + j] for i < ni, j < nj (MUFU reciprocal + 2 Newton steps, as the
+// fused sampling kernel: within 2 ulp of the reference's division)
+__global__ void gen_panel_kernel(CauchyGen g, int64_t i0, int64_t ni, int64_t j0, int64_t nj,
+                                 double* __restrict__ out, int64_t ld) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nj) return;
+  const int64_t gj = j0 + j;
+  const double dj = __ldg(g.d + gj), dnj = __ldg(g.dnext + gj), gmj = __ldg(g.gam + gj);
+  const double mj = __ldg(g.mu + gj), vj = __ldg(g.v + gj);
+  for (int64_t i = blockIdx.y; i < ni; i += gridDim.y) {
+    const int64_t gi = i0 + i;
+    const double gap = stable_gap(gi, gj, __ldg(g.d + gi), dj, dnj, gmj, mj);
+    out[i * ld + j] = (__ldg(g.zhat + gi) * vj) * rcp_nr(gap);
+  }
+}
+
+// out[c][i] = in[i][c]  (Omega^T, w x k)
+__global__ void transpose_kernel(const double* __restrict__ in, int64_t ldi, int64_t rows, int w,
+                                 double* __restrict__ out, int64_t ldo) {
+  __shared__ double t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t i = i0 + r;
+    const int c = c0 + threadIdx.x;
+    t[r][threadIdx.x] = (i < rows && c < w) ? in[i * ldi + c] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int c = c0 + r;
+    const int64_t i = i0 + threadIdx.x;
+    if (c < w && i < rows) out[(int64_t)c * ldo + i] = t[threadIdx.x][r];
+  }
+}
+
+// Z[row][c] = sum_p part[p][c][row], p ascending (fixed order)
+__global__ void splitk_reduce_t_kernel(const double* __restrict__ part, int nsplit, int64_t nrows,
+                                       int w, int64_t ldp, int64_t pstride, double* __restrict__ Z,
+                                       int64_t ldz) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nrows * w) return;
+  const int c = (int)(e / nrows);
+  const int64_t row = e % nrows;
+  double acc = 0.0;
+  for (int p = 0; p < nsplit; ++p) acc += part[(int64_t)p * pstride + (int64_t)c * ldp + row];
+  Z[row * ldz + c] = acc;
+}
+
+struct MatPlan {
+  int64_t nrows, kld, nld, ldp, sy, sz, kcy, kcz, tiles_n;
+  int64_t off_py, off_pz, off_omt, off_c1, off_c2, off_jobs, off_maps, total;
+  bool shared;   // C[R, :] and C[:, R] are the same panel (R = all rows)
+};
+
+static void split_k(int64_t k, int64_t items_per_split, int64_t* ns, int64_t* kc) {
+  int64_t n = (148 * 6 + items_per_split - 1) / items_per_split;
+  n = imax64(1, imin64(n, (k + 1023) / 1024));
+  int64_t c = (k + n - 1) / n;
+  c = (c + 15) / 16 * 16;
+  *ns = (k + c - 1) / c;
+  *kc = c;
+}
+
+static MatPlan mat_plan(int64_t k, int64_t w, int64_t nrows) {
+  MatPlan p;
+  p.nrows = nrows;
+  p.shared = nrows == k;
+  p.kld = k + (k & 1);
+  p.nld = nrows + (nrows & 1);
+  p.ldp = ((w + 1) / 2) * 2;
+  split_k(k, (nrows + 127) / 128, &p.sy, &p.kcy);
+  p.tiles_n = (nrows + 127) / 128;
+  split_k(k, p.tiles_n * ((w + 95) / 96), &p.sz, &p.kcz);
+  int64_t o = 0;
+  auto take = [&](int64_t n) { int64_t at = o; o += (n + 31) / 32 * 32; return at; };
+  p.off_py = take(p.sy * nrows * p.ldp);
+  p.off_pz = take(p.sz * w * p.nld);
+  p.off_omt = take(w * p.kld);
+  p.off_c1 = take(nrows * p.kld);
+  p.off_c2 = p.shared ? p.off_c1 : take(k * p.nld);
+  p.off_jobs = take(((p.sy + p.sz * p.tiles_n) * (int64_t)sizeof(TJob) + 7) / 8);
+  p.off_maps = take(2 * (int64_t)sizeof(MapSet) / 8 + 32);
+  p.total = o;
+  return p;
+}
+
+static bool mat_fits(int64_t k, int64_t nrows) {
+  const double bytes = 8.0 * (double)nrows * (double)k * (nrows == k ? 1.0 : 2.0);
+  return bytes <= kMatCapBytes;
+}
+
+static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom, int w, int64_t row0,
+                             int64_t row1, double* Y, double* Z, int64_t ldy, double* work,
+                             cudaStream_t s) {
+  const int64_t k = g.k;
+  const MatPlan p = mat_plan(k, w, row1 - row0);
+  const int64_t nr = p.nrows;
+  double* pY = work + p.off_py;
+  double* pZ = work + p.off_pz;
+  double* omt = work + p.off_omt;
+  double* C1 = work + p.off_c1;
+  double* C2 = work + p.off_c2;
+  TJob* djobs = reinterpret_cast<TJob*>(work + p.off_jobs);
+  MapSet* dmaps = reinterpret_cast<MapSet*>(
+      (reinterpret_cast<uintptr_t>(work + p.off_maps) + 255) & ~(uintptr_t)255);
+  // panels
+  {
+    // each thread walks many rows with its column's generators in registers
+    dim3 gr((unsigned)((k + 255) / 256), (unsigned)imin64(nr, 128));
+    gen_panel_kernel<<<gr, 256, 0, s>>>(g, row0, nr, 0, k, C1, p.kld);
+    HSS_CHECK_LAUNCH();
+    if (!p.shared) {
+      dim3 g2((unsigned)((nr + 255) / 256), (unsigned)imin64(k, 128));
+      gen_panel_kernel<<<g2, 256, 0, s>>>(g, 0, k, row0, nr, C2, p.nld);
+      HSS_CHECK_LAUNCH();
+    }
+    dim3 gt((unsigned)((k + 31) / 32), (unsigned)((w + 31) / 32));
+    transpose_kernel<<<gt, dim3(32, 8), 0, s>>>(om, ldom, k, w, omt, p.kld);
+    HSS_CHECK_LAUNCH();
+  }
+  // job tables: Y splits, then Z^T (split, column tile) pairs
+  std::vector<TJob> jobs((size_t)(p.sy + p.sz * p.tiles_n));
+  for (int64_t q = 0; q < p.sy; ++q) {
+    TJob& jb = jobs[q];
+    memset(&jb, 0, sizeof(jb));
+    jb.am[0] = 0; jb.acol[0] = (int32_t)(q * p.kcy); jb.K[0] = (int32_t)imin64(p.kcy, k - q * p.kcy);
+    jb.bm[0] = 4; jb.brow[0] = (int32_t)(q * p.kcy); jb.bcol[0] = 0;
+    jb.bm[1] = 4;
+    jb.N = jb.SW = w;
+    jb.C = pY + q * nr * p.ldp;
+    jb.ldc = p.ldp;
+  }
+  for (int64_t q = 0; q < p.sz; ++q)
+    for (int64_t t = 0; t < p.tiles_n; ++t) {
+      TJob& jb = jobs[p.sy + q * p.tiles_n + t];
+      memset(&jb, 0, sizeof(jb));
+      jb.am[0] = 0; jb.acol[0] = (int32_t)(q * p.kcz); jb.K[0] = (int32_t)imin64(p.kcz, k - q * p.kcz);
+      jb.bm[0] = 4; jb.brow[0] = (int32_t)(q * p.kcz); jb.bcol[0] = (int32_t)(t * 128);
+      jb.bm[1] = 4;
+      jb.N = jb.SW = (int32_t)imin64(128, nr - t * 128);
+      jb.C = pZ + q * w * p.nld + t * 128;
+      jb.ldc = p.nld;
+    }
+  if (cudaMemcpyAsync(djobs, jobs.data(), sizeof(TJob) * jobs.size(), cudaMemcpyHostToDevice, s) !=
+      cudaSuccess)
+    return HSSEIG_ERR_CUDA;
+  const Operand none{nullptr, 0, 0, 0};
+  int rc;
+  {
+    const Operand ops[kMaps] = {Operand{C1, (uint64_t)nr, (uint64_t)k, (uint64_t)p.kld}, none, none,
+                                none, Operand{om, (uint64_t)k, (uint64_t)w, (uint64_t)ldom}, none,
+                                none, none};
+    if ((rc = tma_jobs_gemm(0, w, ops, dmaps, djobs, (int)p.sy, nr, s))) return rc;
+  }
+  {
+    const Operand ops[kMaps] = {Operand{omt, (uint64_t)w, (uint64_t)k, (uint64_t)p.kld}, none, none,
+                                none, Operand{C2, (uint64_t)k, (uint64_t)nr, (uint64_t)p.nld}, none,
+                                none, none};
+    if ((rc = tma_jobs_gemm(2, 128, ops, dmaps + 1, djobs + p.sy, (int)(p.sz * p.tiles_n), w, s)))
+      return rc;
+  }
+  const unsigned rb = (unsigned)((nr * w + 255) / 256);
+  splitk_reduce_kernel<<<rb, 256, 0, s>>>(pY, (int)p.sy, nr, w, p.ldp, Y, ldy);
+  HSS_CHECK_LAUNCH();
+  splitk_reduce_t_kernel<<<rb, 256, 0, s>>>(pZ, (int)p.sz, nr, w, p.nld, w * p.nld, Z, ldy);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
 }  // namespace hsseig
 
 using namespace hsseig;
@@ -353,7 +532,13 @@ extern "C" int64_t hsseig_sample_work_doubles(int64_t k, int64_t w) {
     if (nrows == 1) break;
   }
   const int64_t ldp = ((w + 1) / 2) * 2;
-  return 2 * (worst + 64) * ldp + (int64_t)(sizeof(MapSet) + 512) / 8;
+  int64_t need = 2 * (worst + 64) * ldp + (int64_t)(sizeof(MapSet) + 512) / 8;
+  if (w <= 112) {   // materialised path: the full range, and the largest partial range that fits
+    if (mat_fits(k, k)) need = imax64(need, mat_plan(k, w, k).total + 64);
+    const int64_t np = imin64(k - 1, (int64_t)(kMatCapBytes / (16.0 * (double)k)));
+    if (np >= 1) need = imax64(need, mat_plan(k, w, np).total + 64);
+  }
+  return need;
 }
 
 extern "C" int hsseig_cauchy_sample_part(const hsseig_gen* gen, const double* omega, int64_t ldom,
@@ -365,6 +550,10 @@ extern "C" int hsseig_cauchy_sample_part(const hsseig_gen* gen, const double* om
   if (row0 == row1) return HSSEIG_OK;
   CauchyGen g = to_gen(gen);
   cudaStream_t s = (cudaStream_t)stream;
+  static const bool fused_only = getenv("HSSEIG_SAMPLE_FUSED") != nullptr;
+  if (!fused_only && w <= 112 && mat_fits(gen->k, row1 - row0) &&
+      (reinterpret_cast<uintptr_t>(work) & 15) == 0)
+    return launch_sample_mat(g, omega, ldom, (int)w, row0, row1, Y, Z, ldy, work, s);
   switch ((w + 31) / 32) {   // BM 64: 8 DMMA warps of 32 x 8NF + 8 generator warps
     case 1: return launch_sample<TTile<4, 1, 2, 4, 8>>(g, omega, ldom, (int)w, row0, row1, Y, Z, ldy, work, s);
     case 2: return launch_sample<TTile<4, 2, 2, 4, 8>>(g, omega, ldom, (int)w, row0, row1, Y, Z, ldy, work, s);

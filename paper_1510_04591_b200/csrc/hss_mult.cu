@@ -33,13 +33,6 @@ namespace hsseig {
 
 // tensor-map roles: 0 X, 1 G_l, 2 G_{l+1}, 3 F_{l-1} (or F_depth), 4 U, 5 B, 6 Vt, 7 D
 
-struct TJob {
-  int32_t am[2], acol[2];            // A map role and column offset per segment (rows = tile)
-  int32_t bm[2], brow[2], bcol[2];   // B map role, row and column offset per segment
-  int32_t K[2], N, SW;               // segment depths, output width, store width (zero fill)
-  double* C;
-  int64_t ldc;
-};
 
 template <class T>
 __global__ void __launch_bounds__(T::THREADS, T::MINB)
@@ -211,11 +204,6 @@ __global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs) {
 }
 
 // ---------------------------------------------------------------------------- host side
-// Raw operand descriptions (rows, cols, ld) for the 8 roles of one launch.
-struct Operand {
-  const double* base;
-  uint64_t rows, cols, ld;
-};
 
 static int g_sms = 0;
 
@@ -353,6 +341,15 @@ static int launch_wide(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJo
     case 7: return launch_tma<TTile<4, 7, 2, 4, 5>>(ops, dm, jobs, njobs, M, s);
     default: HSS_ARG_FAIL();
   }
+}
+
+// job-table GEMMs for other paths (sampling): shape 0 rank-width, 1 wide, 2 tall-N
+// (BM 96 x BN 128 for M = sample width, N = k)
+int tma_jobs_gemm(int shape, int n, const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jobs,
+                  int njobs, int64_t M, cudaStream_t s) {
+  if (shape == 0) return launch_narrow(n, ops, dmaps, jobs, njobs, M, s);
+  if (shape == 1) return launch_wide(n, ops, dmaps, jobs, njobs, M, s);
+  return launch_tma<TTile<3, 8, 4, 2, 6>>(ops, dmaps, jobs, njobs, M, s);
 }
 
 __global__ void plain_jobs_kernel(TJob* jobs, int nj, double* C, int64_t ldc, int N, int K) {

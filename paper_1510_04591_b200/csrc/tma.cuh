@@ -107,7 +107,26 @@ __device__ __forceinline__ void tmma_chunk(const double* __restrict__ sA, const 
   }
 }
 
+// One job of a batched two-segment GEMM C = A1 B1 + A2 B2 (tma_gemm_kernel, hss_mult.cu).
+struct TJob {
+  int32_t am[2], acol[2];            // A map role and column offset per segment (rows = tile)
+  int32_t bm[2], brow[2], bcol[2];   // B map role, row and column offset per segment
+  int32_t K[2], N, SW;               // segment depths, output width, store width (zero fill)
+  double* C;
+  int64_t ldc;
+};
+
 // ---------------------------------------------------------------------------- host side
+// Raw operand descriptions (rows, cols, ld) for the map roles of one launch.
+struct Operand {
+  const double* base;
+  uint64_t rows, cols, ld;
+};
+// Job-table GEMM on the TMA/DMMA engine (hss_mult.cu): shape 0 rank-width tiles for N = n,
+// 1 wide tiles, 2 tall-N tiles (BM 96, BN 128).  Maps go to dmaps (device), jobs are device.
+int tma_jobs_gemm(int shape, int n, const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jobs,
+                  int njobs, int64_t M, cudaStream_t s);
+
 static inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
