@@ -268,6 +268,11 @@ int hsseig_gather_columns(const double *A, int64_t lda, const double *B, int64_t
                           const int64_t *src, int64_t ncol, int64_t rows, double *out,
                           int64_t ldo, void *stream);
 
+/* Multi-GPU merges (row-block sharded Q): one rank's rows, all from child c whose columns
+   start at coff: W[i][c'] = Qc[i][src[c'] - coff] for src in [coff, coff + nc), else 0. */
+int hsseig_assemble_rows(const double *Qc, int64_t ldq, int64_t nrow, int64_t coff, int64_t nc,
+                         const int64_t *src, int64_t n, double *W, int64_t ldw, void *stream);
+
 /* ---------------------------------------------------------------------------------------
  * Level-batched merges: every merge of one recursion depth of
  * adc_solve (pkg/src/hsseig/dc.py:194-257) in one set of launches.  Merge m has n1[m] +

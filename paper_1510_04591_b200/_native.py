@@ -100,6 +100,8 @@ _SIGS = {
                                              c_vp, c_i64, c_vp]),
     "hsseig_gemm": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64,
                                    c_vp]),
+    "hsseig_assemble_rows": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp,
+                                            c_i64, c_vp]),
     "hsseig_wave_zrows": (ctypes.c_int, [c_vp] * 5 + [c_i64, c_vp, c_vp]),
     "hsseig_wave_deflate": (c_i64, [c_i64] + [c_vp] * 16),
     "hsseig_wave_assemble": (ctypes.c_int, [c_vp] * 9 + [c_i64, c_vp]),

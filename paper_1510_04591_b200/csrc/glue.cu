@@ -243,6 +243,19 @@ __global__ void wave_gather_kernel(const double* __restrict__ Qk, const int64_t*
   }
 }
 
+// One rank's row block of W = blockdiag(Q1, Q2)[:, src] when its rows all come from one
+// child: W[i][c] = Qc[i][src[c] - coff] if that column belongs to the child, else 0.
+__global__ void assemble_rows_kernel(const double* __restrict__ Qc, int64_t ldq, int64_t nrow,
+                                     int64_t coff, int64_t nc, const int64_t* __restrict__ src,
+                                     int64_t n, double* __restrict__ W, int64_t ldw) {
+  for (int64_t row = blockIdx.y; row < nrow; row += gridDim.y)
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
+         c += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t sc = src[c] - coff;
+      W[row * ldw + c] = (sc >= 0 && sc < nc) ? Qc[row * ldq + sc] : 0.0;
+    }
+}
+
 }  // namespace hsseig
 
 using namespace hsseig;
@@ -483,5 +496,16 @@ extern "C" int hsseig_wave_order(int64_t nm, const int64_t* roff, const int64_t*
     std::stable_sort(ord, ord + n, [&](int64_t x, int64_t y) { return cat[x] < cat[y]; });
     for (int64_t t = 0; t < n; ++t) lam_out[o + t] = cat[ord[t]];
   }
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_assemble_rows(const double* Qc, int64_t ldq, int64_t nrow, int64_t coff,
+                                    int64_t nc, const int64_t* src, int64_t n, double* W,
+                                    int64_t ldw, void* stream) {
+  if (nrow < 0 || n < 0 || nc < 0 || ldw < n || (nrow > 0 && (!Qc || !src || !W))) HSS_ARG_FAIL();
+  if (nrow == 0 || n == 0) return HSSEIG_OK;
+  dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 64), (unsigned)std::min<int64_t>(nrow, 65535));
+  assemble_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(Qc, ldq, nrow, coff, nc, src, n, W, ldw);
+  HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }

@@ -178,6 +178,7 @@ class GpuOps:
         f64 = dict(dtype=torch.float64, device="cuda")
         self.swork = torch.empty(2 * self.k + 64, **f64)
         self.status = torch.zeros(8, dtype=torch.int64, device="cuda")
+        self._sample_k = self.k
         self.sample_work = torch.empty(int(self.lib.hsseig_sample_work_doubles(self.k, MAX_WIDTH)), **f64)
         self.rng = sample_rng.NormalStream(self.k * MAX_WIDTH) if sample_rng.available() else None
         self._trees = {}
@@ -186,8 +187,21 @@ class GpuOps:
     def _s(self):
         return self.nat.stream_ptr()
 
+    def _fit(self, k):
+        # the ops serve merges of any order up to the one they were sized for
+        if 2 * k + 64 > self.swork.numel():
+            self.swork = torch.empty(2 * k + 64, dtype=torch.float64, device="cuda")
+        if k > self._sample_k:
+            from .hss import MAX_WIDTH
+            self.sample_work = None
+            self.sample_work = torch.empty(int(self.lib.hsseig_sample_work_doubles(k, MAX_WIDTH)),
+                                           dtype=torch.float64, device="cuda")
+            self._sample_k = k
+
     def secular_part(self, d, z, rho, lo, hi):
         nat, n = self.nat, hi - lo
+        self.k = int(d.numel())
+        self._fit(self.k)
         lam = torch.empty(n, dtype=torch.float64, device="cuda")
         gam, mu = torch.empty_like(lam), torch.empty_like(lam)
         its = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -231,6 +245,9 @@ class GpuOps:
         ws = (w + 15) // 16 * 16
         om = torch.zeros(k, ws, dtype=torch.float64, device="cuda")
         if self.rng is not None:
+            if k * w > self.rng.nmax:
+                from . import sample_rng
+                self.rng = sample_rng.NormalStream(k * w)
             flat = torch.empty(k * w, dtype=torch.float64, device="cuda")
             self.rng.draw(seed, k * w, flat)
             self.rng.fixup()
@@ -289,6 +306,11 @@ class GpuOps:
 
     def multiply(self, X, tree):
         nat = self.nat
+        if X.stride(0) % 2 or X.data_ptr() % 16:   # TMA rows: 16-byte aligned, even ld
+            Xp = torch.empty(X.shape[0], X.shape[1] + (X.shape[1] & 1), dtype=torch.float64,
+                             device="cuda")
+            Xp[:, :X.shape[1]] = X
+            X = Xp[:, :X.shape[1]]
         out = torch.empty(X.shape[0], self.k, dtype=torch.float64, device="cuda")
         need = int(self.lib.hsseig_matmul_work_doubles(X.shape[0], ctypes.byref(tree.ct)))
         if self._mwork is None or self._mwork.numel() < need:
@@ -302,3 +324,212 @@ class GpuOps:
     def dense(self, X, gen):
         return gen.right_multiply_into(X)
 
+    # ---- distributed full solve (adc_solve_distributed)
+    device = "cuda"
+
+    def tensor(self, x):
+        return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device="cuda")
+
+    def local_solve(self, a, b, nodes, sub, cfg):
+        from .solver import _plan, solve_subtree
+        a_mod, _ = _plan(a, b, cfg.base_size)
+        return solve_subtree(a_mod, b, nodes, sub, cfg)
+
+    def deflate(self, nL, nR, L, zrow, bk):
+        return deflate_merge(self.lib, nL, nR, L, zrow, bk)
+
+    def assemble_rows(self, Qc, coff, nc, src, n):
+        nat = self.nat
+        W = torch.empty(Qc.shape[0], n, dtype=torch.float64, device="cuda")
+        src_d = torch.as_tensor(src, device="cuda")
+        nat.check(self.lib.hsseig_assemble_rows(nat.ptr(Qc), Qc.stride(0), Qc.shape[0], coff, nc,
+                                                nat.ptr(src_d), n, nat.ptr(W), n, self._s()),
+                  "assemble_rows")
+        return W
+
+    def rotate(self, W, ca, cb, c, s):
+        nat = self.nat
+        t = (torch.as_tensor(ca, device="cuda"), torch.as_tensor(cb, device="cuda"),
+             self.tensor(c), self.tensor(s))
+        nat.check(self.lib.hsseig_apply_rotations(nat.ptr(W), W.stride(0), W.shape[0],
+                                                  *(nat.ptr(x) for x in t), len(ca), self._s()),
+                  "apply_rotations")
+
+    def gather(self, Qk, W, order, k):
+        nat = self.nat
+        n = W.shape[1]
+        out = torch.empty_like(W)
+        o = torch.as_tensor(np.ascontiguousarray(order, dtype=np.int64), device="cuda")
+        A = Qk if Qk is not None else W
+        nat.check(self.lib.hsseig_gather_columns(nat.ptr(A), A.stride(0), nat.ptr(W), W.stride(0), k,
+                                                 nat.ptr(o), n, W.shape[0], nat.ptr(out), n,
+                                                 self._s()), "gather")
+        return out
+
+
+def deflate_merge(lib, nL, nR, L, zrow, bk):
+    """Host deflation of one merge (hsseig_wave_deflate with one merge): kept count,
+    [kept | deflated] poles and weights, blockdiag column of every W column, rotations."""
+    n = nL + nR
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    n1, n2 = np.array([nL], dtype=np.int64), np.array([nR], dtype=np.int64)
+    roff = np.array([0, n], dtype=np.int64)
+    L = np.ascontiguousarray(L, dtype=np.float64)
+    zrow = np.ascontiguousarray(zrow, dtype=np.float64)
+    bka = np.array([bk], dtype=np.float64)
+    kept, rho = np.empty(1, dtype=np.int64), np.empty(1)
+    d, z, src = np.empty(n), np.empty(n), np.empty(n, dtype=np.int64)
+    rot_off = np.empty(2, dtype=np.int64)
+    ca, cb, rc, rs = (np.empty(n, dtype=np.int64), np.empty(n, dtype=np.int64), np.empty(n),
+                      np.empty(n))
+    lib.hsseig_wave_deflate(1, P(n1), P(n2), P(roff), P(L), P(zrow), P(bka), P(kept), P(rho), P(d),
+                            P(z), P(src), P(rot_off), P(ca), P(cb), P(rc), P(rs))
+    nr = int(rot_off[1])
+    return {"kept": int(kept[0]), "rho_eff": float(rho[0]), "d": d, "z": z, "src": src,
+            "nrot": nr, "ca": ca[:nr], "cb": cb[:nr], "rc": rc[:nr], "rs": rs[:nr]}
+
+
+
+# ----------------------------------------------------------------------------------------
+# Multi-GPU full eigendecomposition (BASELINE config 5, SURVEY.md §8 e/f3)
+# ----------------------------------------------------------------------------------------
+_GROUPS = {}
+
+
+def _group(ranks):
+    """Process group of a contiguous rank range (created once, collectively)."""
+    key = tuple(ranks)
+    if key not in _GROUPS:
+        _GROUPS[key] = dist.new_group(list(ranks))
+    return _GROUPS[key]
+
+
+def _split_a(a, b, nodes, max_depth):
+    """Diagonal with the split modifications of the recursion nodes above max_depth."""
+    a = a.copy()
+    for nd in nodes:
+        if not nd["leaf"] and nd["depth"] < max_depth:
+            m = nd["split"]
+            rho = abs(float(b[m - 1]))
+            a[m - 1] -= rho
+            a[m] -= rho
+    return a
+
+
+def _gather_padded(vec, length, group, device):
+    """All-gather 1-D tensors of up to `length` entries (padded); returns the list."""
+    world = dist.get_world_size(group)
+    t = torch.zeros(length, dtype=torch.float64, device=device)
+    t[:vec.numel()] = vec
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return parts
+
+
+class DistributedEigenResult:
+    """Eigenvalues (replicated) and this rank's rows [row0, row1) of Q (all N columns)."""
+
+    def __init__(self, lam, Q_rows, row0, row1, merges):
+        self.lam, self.Q_rows, self.row0, self.row1, self.merges = lam, Q_rows, row0, row1, merges
+
+
+def adc_solve_distributed(T, cfg, ops, group=None):
+    """Full DC eigendecomposition over the ranks of `group` (a power of two, G = 2^g).
+
+    Rank r solves the recursion subtree rooted at the r-th node of depth g alone (its
+    base cases and merges, level-batched).  The merges above depth g are row-block
+    sharded: every rank keeps its subtree's rows of the current eigenvector block for
+    the whole ascent, so assembly, the Givens replay, the update (ShardedMerge: roots /
+    weights / samples index-sharded and all-gathered, tree replicated or subtree-built,
+    row-local multiply) and the final column gather are row-local.  Per merge only the
+    two boundary rows (z) and the children's eigenvalues cross ranks.  The merge ids,
+    seeds, deflation and records are the reference's (dc.py:174-257).
+    """
+    from .dc import MergeRecord
+    from .solver import _tree
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    g = world.bit_length() - 1
+    if world & (world - 1):
+        raise ValueError("the distributed solver needs a power-of-two number of ranks")
+    a = np.asarray(T.a, dtype=np.float64)
+    b = np.asarray(T.b, dtype=np.float64)
+    nodes, root = _tree(T.n, cfg.base_size)
+    subs = sorted((i for i, nd in enumerate(nodes) if nd["depth"] == g), key=lambda i: nodes[i]["lo"])
+    if len(subs) != world:
+        raise ValueError("matrix too small for this many ranks (recursion shallower than log2 G)")
+    granks = [dist.get_global_rank(group, r) for r in range(world)] if group is not None \
+        else list(range(world))
+    # groups of every merge above depth g (all ranks create all of them, in order)
+    for d in range(g):
+        size = 1 << (g - d)
+        for j in range(1 << d):
+            _group(granks[j * size:(j + 1) * size])
+    me = subs[rank]
+    lam, Qb, records = ops.local_solve(a, b, nodes, me, cfg)
+    row0, row1 = nodes[me]["lo"], nodes[me]["hi"]
+    cur = me
+    parent = {}
+    for i, nd in enumerate(nodes):
+        if not nd["leaf"]:
+            parent[nd["left"]] = i
+            parent[nd["right"]] = i
+    dev = ops.device
+    for d in range(g - 1, -1, -1):
+        P = parent[cur]
+        nd = nodes[P]
+        size = 1 << (g - d)
+        j = rank // size
+        ranks = granks[j * size:(j + 1) * size]
+        grp = _group(ranks)
+        half = size // 2
+        left_side = (rank % size) < half
+        nL, nR = nd["split"] - nd["lo"], nd["hi"] - nd["split"]
+        n = nL + nR
+        nmax = max(nL, nR)
+        # children's eigenvalues and the boundary rows (last row of Q_L, first row of Q_R)
+        lam_parts = _gather_padded(torch.as_tensor(lam, device=dev), nmax, grp, dev)
+        lamL = lam_parts[0][:nL].cpu().numpy()
+        lamR = lam_parts[half][:nR].cpu().numpy()
+        edge = torch.zeros(2, nmax, dtype=torch.float64, device=dev)
+        edge[0, :Qb.shape[1]] = Qb[0]
+        edge[1, :Qb.shape[1]] = Qb[-1]
+        eparts = [torch.empty_like(edge) for _ in range(size)]
+        dist.all_gather(eparts, edge, group=grp)
+        zrow = np.concatenate([eparts[half - 1][1, :nL].cpu().numpy(),
+                               eparts[half][0, :nR].cpu().numpy()])
+        bk = float(b[nd["split"] - 1])
+        dfl = ops.deflate(nL, nR, np.concatenate([lamL, lamR]), zrow, bk)
+        k, src = dfl["kept"], dfl["src"]
+        rec = None
+        if dfl["rho_eff"] != 0.0:
+            rec = MergeRecord(size=n, kept=k, n_deflated=n - k)
+            records[nd["mid"]] = rec
+        W = ops.assemble_rows(Qb, 0 if left_side else nL, nL if left_side else nR, src, n)
+        del Qb
+        if dfl["nrot"]:
+            ops.rotate(W, dfl["ca"], dfl["cb"], dfl["rc"], dfl["rs"])
+        if k > 0:
+            sm = ShardedMerge(k, cfg, ops, group=grp)
+            lam_k, Qk, info = sm.run(ops.tensor(dfl["d"][:k]), ops.tensor(dfl["z"][:k]),
+                                     dfl["rho_eff"], W[:, :k], seed=[cfg.seed, nd["mid"]])
+            lam_k = lam_k.cpu().numpy()
+            if rec is not None:
+                rec.used_hss = bool(info["used_hss"])
+                rec.fell_back = bool(info["fell_back"])
+                rec.hss_rank = int(info.get("r_used", 0))
+        else:
+            lam_k, Qk = np.zeros(0), None
+        lam_cat = np.concatenate([lam_k, dfl["d"][k:]])
+        order = np.argsort(lam_cat, kind="stable")
+        Qb = ops.gather(Qk, W, order, k)
+        del W, Qk
+        lam = lam_cat[order]
+        cur = P
+    # every rank reports the full merge list (its subtree's and the shared top merges)
+    allrec = [None] * world
+    dist.all_gather_object(allrec, records, group=group)
+    merged = {}
+    for r in allrec:
+        merged.update(r)
+    return DistributedEigenResult(lam, Qb, row0, row1, [merged[m] for m in sorted(merged)])

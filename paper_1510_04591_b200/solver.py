@@ -67,7 +67,8 @@ def _base_cases(a_mod, b, leaves, stream):
     lam = torch.empty(int(off[-1]), dtype=torch.float64, device="cuda")
     Q = torch.empty(int(qoff[-1]), dtype=torch.float64, device="cuda")
     st = torch.zeros(len(leaves), dtype=torch.int32, device="cuda")
-    a_d, b_d, off_d, qoff_d = _f64(a_mod), _f64(bb), _i64(off), _i64(qoff)
+    aa = np.concatenate([a_mod[lo:hi] for lo, hi in leaves])
+    a_d, b_d, off_d, qoff_d = _f64(aa), _f64(bb), _i64(off), _i64(qoff)
     nat.check(lib.hsseig_tql2_batched(nat.ptr(a_d), nat.ptr(b_d), nat.ptr(off_d), len(leaves), 30,
                                       nat.ptr(lam), nat.ptr(Q), nat.ptr(qoff_d), nat.ptr(st), stream),
               "tql2_batched")
@@ -227,27 +228,51 @@ def adc_solve(T, cfg=None):
     if cfg.base_size > MAX_BASE:
         raise ValueError(f"base_size above {MAX_BASE} is not supported by the device base case")
     nat.require_cuda()
+    a = np.asarray(T.a, dtype=np.float64)
+    b = np.asarray(T.b, dtype=np.float64)
+    a_mod, _ = _plan(a, b, cfg.base_size)
+    nodes, root = _tree(T.n, cfg.base_size)
+    lam, Q, records = solve_subtree(a_mod, b, nodes, root, cfg)
+    flops = FlopCounter()
+    merges = [records[k] for k in sorted(records)]
+    for r in merges:
+        for p_ in FlopCounter.PHASES:
+            setattr(flops, p_, getattr(flops, p_) + r.flops.get(p_, 0))
+    return EigenResult(lam=lam, Q=Q, merges=merges, flops=flops)
+
+
+def _subtree_nodes(nodes, sub):
+    out = []
+    stack = [sub]
+    while stack:
+        i = stack.pop()
+        out.append(i)
+        if not nodes[i]["leaf"]:
+            stack += [nodes[i]["left"], nodes[i]["right"]]
+    return set(out)
+
+
+def solve_subtree(a_mod, b, nodes, sub, cfg):
+    """Eigenpairs of the recursion node `sub` (its base cases and every merge below it,
+    level-batched); a_mod carries all split modifications (_plan).  Returns (lam host,
+    Q device n x n in the node's local coordinates, {merge id: MergeRecord})."""
     lib = nat.load()
     s = nat.stream_ptr()
     f64 = dict(dtype=torch.float64, device="cuda")
-    flops = FlopCounter()
-    a = np.asarray(T.a, dtype=np.float64)
-    b = np.asarray(T.b, dtype=np.float64)
-    a_mod, leaves = _plan(a, b, cfg.base_size)
-    base = _base_cases(a_mod, b, leaves, s)
-    nodes, root = _tree(T.n, cfg.base_size)
+    members = _subtree_nodes(nodes, sub)
+    leaf_ids = sorted((i for i in members if nodes[i]["leaf"]), key=lambda i: nodes[i]["lo"])
+    base = _base_cases(a_mod, b, [(nodes[i]["lo"], nodes[i]["hi"]) for i in leaf_ids], s)
     state = {}       # node -> (lam host, Q device view n x n)
-    for i, nd in enumerate(nodes):
-        if nd["leaf"]:
-            state[i] = base[(nd["lo"], nd["hi"])]
+    for i in leaf_ids:
+        state[i] = base[(nodes[i]["lo"], nodes[i]["hi"])]
     records = {}
     bm = ctypes.c_int32(0)
     bn = ctypes.c_int32(0)
     lib.hsseig_wave_tile_shape(ctypes.byref(bm), ctypes.byref(bn))
     bm, bn = bm.value, bn.value
-    maxdepth = max(nd["depth"] for nd in nodes)
+    maxdepth = max(nodes[i]["depth"] for i in members)
     for depth in range(maxdepth - 1, -1, -1):
-        ms = [i for i, nd in enumerate(nodes) if nd["depth"] == depth and not nd["leaf"]]
+        ms = [i for i in sorted(members) if nodes[i]["depth"] == depth and not nodes[i]["leaf"]]
         if not ms:
             continue
         nm = len(ms)
@@ -412,9 +437,5 @@ def adc_solve(T, cfg=None):
                     {p: 0 for p in FlopCounter.PHASES}
             state[ms[m]] = (lam_out[roff[m]:roff[m + 1]].copy(),
                             A[int(woff[m]):int(woff[m + 1])].view(n, n))
-    lam, Q = state[root]
-    merges = [records[k] for k in sorted(records)]
-    for r in merges:
-        for p_ in FlopCounter.PHASES:
-            setattr(flops, p_, getattr(flops, p_) + r.flops.get(p_, 0))
-    return EigenResult(lam=lam, Q=Q, merges=merges, flops=flops)
+    lam, Q = state[sub]
+    return lam, Q, records

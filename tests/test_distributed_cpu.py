@@ -137,3 +137,112 @@ def test_subtree_layout_matches_postorder():
                 assert sub.level == s_lev
                 assert all(sub.lo <= nodes[i].lo and nodes[i].hi <= sub.hi for i in range(a, b))
                 assert (sub.lo, sub.hi) == (la, lb)
+
+
+class NumpySolveOps(NumpyOps):
+    """NumpyOps plus the full-solve pieces: oracle subtree solves, NumPy row-block glue;
+    the host deflation is the library's own C function (hsseig_wave_deflate)."""
+    device = "cpu"
+
+    def __init__(self):
+        super().__init__(0)
+
+    def tensor(self, x):
+        return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64))
+
+    def secular_part(self, d, z, rho, lo, hi):
+        self.k = d.numel()
+        return super().secular_part(d, z, rho, lo, hi)
+
+    def local_solve(self, a, b, nodes, sub, cfg):
+        from paper_1510_04591_b200.distributed import _split_a
+        nd = nodes[sub]
+        a_top = _split_a(a, b, nodes, nd["depth"])
+        lo, hi = nd["lo"], nd["hi"]
+        lam, Q, _, _ = orc.adc_solve(a_top[lo:hi], b[lo:hi - 1], orc.Config(base_size=cfg.base_size))
+        return lam, torch.as_tensor(Q), {}
+
+    def deflate(self, nL, nR, L, zrow, bk):
+        from paper_1510_04591_b200 import _native as nat
+        from paper_1510_04591_b200.distributed import deflate_merge
+        return deflate_merge(nat.load(build_if_missing=False), nL, nR, L, zrow, bk)
+
+    def assemble_rows(self, Qc, coff, nc, src, n):
+        Q = Qc.numpy()
+        sc = src - coff
+        ok = (sc >= 0) & (sc < nc)
+        W = np.zeros((Q.shape[0], n))
+        W[:, ok] = Q[:, sc[ok]]
+        return torch.as_tensor(W)
+
+    def rotate(self, W, ca, cb, c, s):
+        w = W.numpy()
+        for i, j, cc, ss in zip(ca, cb, c, s):
+            x, y = w[:, i].copy(), w[:, j].copy()
+            w[:, i] = cc * x + ss * y
+            w[:, j] = -ss * x + cc * y
+
+    def gather(self, Qk, W, order, k):
+        w = W.numpy()
+        out = np.empty_like(w)
+        for c, sc in enumerate(order):
+            out[:, c] = Qk.numpy()[:, sc] if sc < k else w[:, sc]
+        return torch.as_tensor(out)
+
+
+def _solve_worker(rank, world, port, n, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1510_04591_b200 import SolverConfig
+    from paper_1510_04591_b200.distributed import adc_solve_distributed
+    from paper_1510_04591_b200.matgen import gen_config5
+    T = gen_config5(n, 1)
+    res = adc_solve_distributed(T, SolverConfig(), NumpySolveOps())
+    rows = [torch.empty(0) for _ in range(world)]
+    dist.all_gather_object(rows, (res.row0, res.row1, res.Q_rows.numpy()))
+    if rank == 0:
+        Q = np.zeros((n, n))
+        for r0, r1, q in rows:
+            Q[r0:r1] = q
+        np.savez(out_path, lam=res.lam, Q=Q, nmerges=len(res.merges))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 200), (4, 430)])
+def test_distributed_full_solve_matches_oracle(tmp_path, world, n):
+    # multi-GPU config-5 solve logic: subtrees per rank, row-block sharded top merges
+    from paper_1510_04591_b200.matgen import gen_config5
+    out_path = str(tmp_path / "solve.npz")
+    mp.spawn(_solve_worker, args=(world, _free_port(), n, out_path), nprocs=world, join=True)
+    res = np.load(out_path)
+    T = gen_config5(n, 1)
+    lam, Q, infos, _ = orc.adc_solve(T.a, T.b, orc.Config())
+    assert int(res["nmerges"]) == world - 1      # the shared top merges (subtree records are the oracle's)
+    np.testing.assert_allclose(res["lam"], lam, rtol=0, atol=1e-13)
+    Qd = res["Q"]
+    s = np.sign((Qd * Q).sum(0))
+    np.testing.assert_allclose(Qd * s, Q, rtol=0, atol=1e-12)
+
+
+def _bench_worker(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "bench_mod", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    rec = bench.eigh_distributed(world, ops=NumpySolveOps(), device="cpu", n=240, warm=False)
+    if rank == 0:
+        np.savez(out_path, **{k: np.asarray(v) for k, v in rec.items()})
+    dist.destroy_process_group()
+
+
+def test_bench_distributed_eigh_line_world2(tmp_path):
+    # the bench's config-5 multi-GPU line (halo residual, sampled orthogonality, max-over-ranks
+    # wall time) with gloo and the oracle stand-in
+    out_path = str(tmp_path / "b.npz")
+    mp.spawn(_bench_worker, args=(2, _free_port(), out_path), nprocs=2, join=True)
+    r = np.load(out_path)
+    assert int(r["ranks"]) == 2 and float(r["wall_s"]) > 0
+    assert float(r["orthogonality"]) < 1e-15 and float(r["residual"]) < 1e-15

@@ -469,3 +469,28 @@ def test_partitioned_construction_equals_single_build(nparts):
     assert (H1.ranks()[0] == H2.ranks()[0]).all() and (H1.ranks()[1] == H2.ranks()[1]).all()
     X = torch.randn(200, n, dtype=torch.float64, device="cuda")
     assert torch.equal(hb.hss_matmul_right(X, H1), hb.hss_matmul_right(X, H2))
+
+
+def test_distributed_solve_single_rank_nccl():
+    # the multi-GPU full-solve driver on a one-rank NCCL group equals adc_solve
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1510_04591_b200.distributed import GpuOps, adc_solve_distributed
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        T = hb.gen_config5(3000, 2)
+        cfg = hb.SolverConfig(rank_eps=1e-13)
+        res = adc_solve_distributed(T, cfg, GpuOps(T.n))
+        ref = hb.adc_solve(T, cfg)
+        assert (res.row0, res.row1) == (0, T.n)
+        np.testing.assert_array_equal(res.lam, ref.lam)
+        assert torch.equal(res.Q_rows, ref.Q)
+        assert [m.kept for m in res.merges] == [m.kept for m in ref.merges]
+    finally:
+        dist.destroy_process_group()
