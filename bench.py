@@ -432,6 +432,13 @@ def run_ours(args):
                "d2h_bytes_per_step": int(hOut.numel() * 8)}
         del hQ, hOut
 
+    # the full solves below need the HBM the merge bench holds (Q_old, outputs, workspaces)
+    pipe = sm = step = Xd = None   # noqa: F841
+    del Qloc, out
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+
     eigh_d = None
     if world > 1 and not args.no_eigh and (world & (world - 1)) == 0:
         eigh_d = eigh_distributed(world)

@@ -300,8 +300,7 @@ static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int
   for (int r = 1; r < kMaps; ++r) make_map(&maps.m[r], nullptr, 0, 0, 0, 0, 0);
   if (!make_map(&maps.m[0], om, (uint64_t)k, (uint64_t)w, (uint64_t)ldom, T::SB, T::BK))
     HSS_ARG_FAIL();
-  if (cudaMemcpyAsync(dmap, &maps, sizeof(MapSet), cudaMemcpyHostToDevice, s) != cudaSuccess)
-    return HSSEIG_ERR_CUDA;
+  if (!upload_maps(maps, dmap, s)) return HSSEIG_ERR_CUDA;
   const int64_t items = tiles * nsplit;
   const int grid = (int)imin64(items, (int64_t)sms * per_sm);
   sample_ws_kernel<T, false><<<grid, threads, T::SMEM_BYTES, s>>>(g, dmap, w, pY, ldp, (int)kchunk,
@@ -416,6 +415,33 @@ static bool mat_fits(int64_t k, int64_t nrows) {
   return bytes <= kMatCapBytes;
 }
 
+__global__ void mat_jobs_kernel(TJob* __restrict__ jobs, int sy, int sz, int tiles_n, int64_t k,
+                                int64_t nr, int w, int64_t kcy, int64_t kcz, int64_t ldp,
+                                int64_t nld, double* pY, double* pZ) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= sy + sz * tiles_n) return;
+  TJob jb;
+  jb.am[0] = jb.am[1] = 0;
+  jb.acol[1] = 0; jb.K[1] = 0;
+  jb.bm[0] = jb.bm[1] = 4;
+  jb.brow[1] = jb.bcol[1] = 0;
+  if (q < sy) {
+    jb.acol[0] = (int32_t)(q * kcy); jb.K[0] = (int32_t)imin64(kcy, k - q * kcy);
+    jb.brow[0] = (int32_t)(q * kcy); jb.bcol[0] = 0;
+    jb.N = jb.SW = w;
+    jb.C = pY + (int64_t)q * nr * ldp;
+    jb.ldc = ldp;
+  } else {
+    const int qq = (q - sy) / tiles_n, t = (q - sy) % tiles_n;
+    jb.acol[0] = (int32_t)(qq * kcz); jb.K[0] = (int32_t)imin64(kcz, k - qq * kcz);
+    jb.brow[0] = (int32_t)(qq * kcz); jb.bcol[0] = t * 128;
+    jb.N = jb.SW = (int32_t)imin64(128, nr - (int64_t)t * 128);
+    jb.C = pZ + (int64_t)qq * w * nld + (int64_t)t * 128;
+    jb.ldc = nld;
+  }
+  jobs[q] = jb;
+}
+
 static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom, int w, int64_t row0,
                              int64_t row1, double* Y, double* Z, int64_t ldy, double* work,
                              cudaStream_t s) {
@@ -445,32 +471,11 @@ static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom,
     transpose_kernel<<<gt, dim3(32, 8), 0, s>>>(om, ldom, k, w, omt, p.kld);
     HSS_CHECK_LAUNCH();
   }
-  // job tables: Y splits, then Z^T (split, column tile) pairs
-  std::vector<TJob> jobs((size_t)(p.sy + p.sz * p.tiles_n));
-  for (int64_t q = 0; q < p.sy; ++q) {
-    TJob& jb = jobs[q];
-    memset(&jb, 0, sizeof(jb));
-    jb.am[0] = 0; jb.acol[0] = (int32_t)(q * p.kcy); jb.K[0] = (int32_t)imin64(p.kcy, k - q * p.kcy);
-    jb.bm[0] = 4; jb.brow[0] = (int32_t)(q * p.kcy); jb.bcol[0] = 0;
-    jb.bm[1] = 4;
-    jb.N = jb.SW = w;
-    jb.C = pY + q * nr * p.ldp;
-    jb.ldc = p.ldp;
-  }
-  for (int64_t q = 0; q < p.sz; ++q)
-    for (int64_t t = 0; t < p.tiles_n; ++t) {
-      TJob& jb = jobs[p.sy + q * p.tiles_n + t];
-      memset(&jb, 0, sizeof(jb));
-      jb.am[0] = 0; jb.acol[0] = (int32_t)(q * p.kcz); jb.K[0] = (int32_t)imin64(p.kcz, k - q * p.kcz);
-      jb.bm[0] = 4; jb.brow[0] = (int32_t)(q * p.kcz); jb.bcol[0] = (int32_t)(t * 128);
-      jb.bm[1] = 4;
-      jb.N = jb.SW = (int32_t)imin64(128, nr - t * 128);
-      jb.C = pZ + q * w * p.nld + t * 128;
-      jb.ldc = p.nld;
-    }
-  if (cudaMemcpyAsync(djobs, jobs.data(), sizeof(TJob) * jobs.size(), cudaMemcpyHostToDevice, s) !=
-      cudaSuccess)
-    return HSSEIG_ERR_CUDA;
+  // job tables (built on the device): Y splits, then Z^T (split, column tile) pairs
+  const int njobs = (int)(p.sy + p.sz * p.tiles_n);
+  mat_jobs_kernel<<<(njobs + 127) / 128, 128, 0, s>>>(djobs, (int)p.sy, (int)p.sz, (int)p.tiles_n,
+                                                      k, nr, w, p.kcy, p.kcz, p.ldp, p.nld, pY, pZ);
+  HSS_CHECK_LAUNCH();
   const Operand none{nullptr, 0, 0, 0};
   int rc;
   {

@@ -234,8 +234,7 @@ static int launch_tma(const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jo
     if (!make_map(&maps.m[r], ops[r].base, ops[r].rows, ops[r].cols, ops[r].ld, bc, br))
       HSS_ARG_FAIL();
   }
-  if (cudaMemcpyAsync(dmaps, &maps, sizeof(MapSet), cudaMemcpyHostToDevice, s) != cudaSuccess)
-    return HSSEIG_ERR_CUDA;
+  if (!upload_maps(maps, dmaps, s)) return HSSEIG_ERR_CUDA;
   const int tiles_m = (int)((M + T::BM - 1) / T::BM);
   const int64_t total = (int64_t)tiles_m * njobs;
   const int grid = (int)imin64(total, (int64_t)g_sms * per_sm);

@@ -116,7 +116,20 @@ struct TJob {
   int64_t ldc;
 };
 
+// Tensor maps reach device memory through a kernel parameter (stream-ordered, no host
+// blocking on a pageable copy that would queue behind bulk host<->device traffic).
+static __global__ void put_maps_kernel(const __grid_constant__ MapSet maps, MapSet* dst) {
+  const uint4* src = reinterpret_cast<const uint4*>(&maps);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(MapSet) / 16); i += blockDim.x) d[i] = src[i];
+}
+
 // ---------------------------------------------------------------------------- host side
+static inline bool upload_maps(const MapSet& maps, MapSet* dst, cudaStream_t s) {
+  put_maps_kernel<<<1, 64, 0, s>>>(maps, dst);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError() == cudaSuccess;
+}
 // Raw operand descriptions (rows, cols, ld) for the map roles of one launch.
 struct Operand {
   const double* base;

@@ -315,6 +315,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                                            nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(src_d),
                                            nat.ptr(W), nat.ptr(woff_d), nrows, s), "wave_assemble")
         del kids, q1, q2
+        A = None      # the previous depth's arena is dead once assembled
         nrot = int(rot_off[-1])
         if nrot:
             rot_d = (_i64(rot_off), _i64(ca[:nrot]), _i64(cb[:nrot]), _f64(rc[:nrot]),
