@@ -414,7 +414,8 @@ def run_ours(args):
             if world == 1:
                 # public streaming API: Q_old rows land in chunks while the factors are built,
                 # Q_new rows go back while later chunks are multiplied
-                pipe.run(dd, du, rho, Xd, seed=[SEED, 0], out=out, host_io=(hQ, hOut))
+                pipe.run(dd, du, rho, Xd, seed=[SEED, 0], out=out, host_io=(hQ, hOut),
+                         chunks=int(os.environ.get("HSSEIG_IO_CHUNKS", "8")))
             else:
                 Xd.copy_(hQ, non_blocking=True)
                 step(Xd, out, dd, du)
