@@ -243,10 +243,6 @@ static int launch_tma(const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jo
   return HSSEIG_OK;
 }
 
-static int tile_choice(const char* var, int dflt) {
-  const char* v = getenv(var);
-  return v ? atoi(v) : dflt;
-}
 
 // Rank-width tiles: 8 consumer warps stacked along M (BM = 128), one warp spans the whole
 // output width in NF 8-column fragments, so N is padded to a multiple of 8 only.
@@ -258,81 +254,30 @@ constexpr int narrow_stages(int nf) {
 template <int NF>
 using RankTile = TTile<2, NF, 8, 1, narrow_stages(NF)>;
 
-// narrow outputs (ranks, N <= 112)
+// narrow outputs (ranks, N <= 112).  Measured alternatives (BM 64 with 8 warps of 32 x 8NF,
+// BM 128 with NF = N/16, two CTAs per SM) were 5-10% slower at config 4.
 static int launch_narrow(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJob* jobs, int njobs,
                          int64_t M, cudaStream_t s) {
-  static const int variant = tile_choice("HSSEIG_TILE_NARROW", 3);
-  if (variant == 3) {
-    switch ((n + 7) / 8) {
-      case 1: case 2: case 3: case 4: return launch_tma<RankTile<4>>(ops, dm, jobs, njobs, M, s);
-      case 5: return launch_tma<RankTile<5>>(ops, dm, jobs, njobs, M, s);
-      case 6: return launch_tma<RankTile<6>>(ops, dm, jobs, njobs, M, s);
-      case 7: return launch_tma<RankTile<7>>(ops, dm, jobs, njobs, M, s);
-      case 8: return launch_tma<RankTile<8>>(ops, dm, jobs, njobs, M, s);
-      case 9: return launch_tma<RankTile<9>>(ops, dm, jobs, njobs, M, s);
-      case 10: return launch_tma<RankTile<10>>(ops, dm, jobs, njobs, M, s);
-      case 11: return launch_tma<RankTile<11>>(ops, dm, jobs, njobs, M, s);
-      case 12: return launch_tma<RankTile<12>>(ops, dm, jobs, njobs, M, s);
-      case 13: return launch_tma<RankTile<13>>(ops, dm, jobs, njobs, M, s);
-      case 14: return launch_tma<RankTile<14>>(ops, dm, jobs, njobs, M, s);
-      default: HSS_ARG_FAIL();
-    }
-  }
-  if (variant == 2) {   // BM 64, 4-stage ring: two CTAs per SM
-    switch ((n + 31) / 32) {
-      case 1: case 2: return launch_tma<TTile<4, 2, 2, 4, 4>>(ops, dm, jobs, njobs, M, s);
-      case 3: return launch_tma<TTile<4, 3, 2, 4, 4>>(ops, dm, jobs, njobs, M, s);
-      case 4: return launch_tma<TTile<4, 4, 2, 4, 3>>(ops, dm, jobs, njobs, M, s);
-      default: HSS_ARG_FAIL();
-    }
-  }
-  if (variant == 0) {   // BM 128: 8 consumer warps of 32 x 8NF, NF = ceil(n/16)
-    switch ((n + 15) / 16) {
-      case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      case 5: return launch_tma<TTile<4, 5, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      case 6: return launch_tma<TTile<4, 6, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      case 7: return launch_tma<TTile<4, 7, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      default: HSS_ARG_FAIL();
-    }
-  }
-  // default: BM 64: 8 consumer warps of 32 x 8NF, NF = ceil(n/32)
-  switch ((n + 31) / 32) {
-    case 1: case 2: return launch_tma<TTile<4, 2, 2, 4, 8>>(ops, dm, jobs, njobs, M, s);
-    case 3: return launch_tma<TTile<4, 3, 2, 4, 8>>(ops, dm, jobs, njobs, M, s);
-    case 4: return launch_tma<TTile<4, 4, 2, 4, 6>>(ops, dm, jobs, njobs, M, s);
+  switch ((n + 7) / 8) {
+    case 1: case 2: case 3: case 4: return launch_tma<RankTile<4>>(ops, dm, jobs, njobs, M, s);
+    case 5: return launch_tma<RankTile<5>>(ops, dm, jobs, njobs, M, s);
+    case 6: return launch_tma<RankTile<6>>(ops, dm, jobs, njobs, M, s);
+    case 7: return launch_tma<RankTile<7>>(ops, dm, jobs, njobs, M, s);
+    case 8: return launch_tma<RankTile<8>>(ops, dm, jobs, njobs, M, s);
+    case 9: return launch_tma<RankTile<9>>(ops, dm, jobs, njobs, M, s);
+    case 10: return launch_tma<RankTile<10>>(ops, dm, jobs, njobs, M, s);
+    case 11: return launch_tma<RankTile<11>>(ops, dm, jobs, njobs, M, s);
+    case 12: return launch_tma<RankTile<12>>(ops, dm, jobs, njobs, M, s);
+    case 13: return launch_tma<RankTile<13>>(ops, dm, jobs, njobs, M, s);
+    case 14: return launch_tma<RankTile<14>>(ops, dm, jobs, njobs, M, s);
     default: HSS_ARG_FAIL();
   }
 }
 
-// wide outputs (leaf finish N = leaf size; plain GEMM tiles), N <= 224
+// wide outputs (leaf finish N = leaf size; plain GEMM tiles), N <= 224: BM 64, 8 consumer
+// warps of 32 x 8NF, NF = ceil(n/32) (94% of the DMMA pipe at config 4)
 static int launch_wide(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJob* jobs, int njobs,
                        int64_t M, cudaStream_t s) {
-  static const int variant = tile_choice("HSSEIG_TILE_WIDE", 1);
-  if (variant == 2) {   // BM 64, short ring: two CTAs per SM
-    switch ((n + 31) / 32) {
-      case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 2, 4, 4>>(ops, dm, jobs, njobs, M, s);
-      case 5: return launch_tma<TTile<4, 5, 2, 4, 3>>(ops, dm, jobs, njobs, M, s);
-      case 6: return launch_tma<TTile<4, 6, 2, 4, 3>>(ops, dm, jobs, njobs, M, s);
-      case 7: return launch_tma<TTile<4, 7, 2, 4, 2>>(ops, dm, jobs, njobs, M, s);
-      default: HSS_ARG_FAIL();
-    }
-  }
-  if (variant == 0) {   // BM 64: 8 consumer warps of 16 x 8NF, NF = ceil(n/16)
-    switch ((n + 15) / 16) {
-      case 1: case 2: case 3: case 4: case 5: case 6:
-        return launch_tma<TTile<2, 6, 4, 2, 6>>(ops, dm, jobs, njobs, M, s);
-      case 7: return launch_tma<TTile<2, 7, 4, 2, 6>>(ops, dm, jobs, njobs, M, s);
-      case 8: return launch_tma<TTile<2, 8, 4, 2, 6>>(ops, dm, jobs, njobs, M, s);
-      case 9: return launch_tma<TTile<2, 9, 4, 2, 6>>(ops, dm, jobs, njobs, M, s);
-      case 10: return launch_tma<TTile<2, 10, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      case 11: return launch_tma<TTile<2, 11, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      case 12: return launch_tma<TTile<2, 12, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      case 13: return launch_tma<TTile<2, 13, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      case 14: return launch_tma<TTile<2, 14, 4, 2, 5>>(ops, dm, jobs, njobs, M, s);
-      default: HSS_ARG_FAIL();
-    }
-  }
-  // default: BM 64: 8 consumer warps of 32 x 8NF, NF = ceil(n/32)
   switch ((n + 31) / 32) {
     case 1: case 2: case 3: case 4: return launch_tma<TTile<4, 4, 2, 4, 6>>(ops, dm, jobs, njobs, M, s);
     case 5: return launch_tma<TTile<4, 5, 2, 4, 6>>(ops, dm, jobs, njobs, M, s);

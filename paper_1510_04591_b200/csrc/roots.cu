@@ -477,24 +477,13 @@ extern "C" int hsseig_secular_part(const double* d, const double* z, int64_t k, 
   double* sum = work + k;
   square_sum_kernel<<<1, 1024, 0, s>>>(z, k, z2, sum);
   HSS_CHECK_LAUNCH();
-  // default: two roots per warp, four CTAs per SM (measured fastest at k = 32768)
-  static const int variant = getenv("HSSEIG_SEC_VARIANT") ? atoi(getenv("HSSEIG_SEC_VARIANT")) : 2;
-  auto launch = [&](auto kern, int R) {
-    const int64_t warps = (iend - ibeg + R - 1) / R;
-    const int blocks = (int)((warps + 7) / 8);
-    kern<<<blocks, 256, 0, s>>>(d, z2, sum, k, rho, ibeg, iend, lam, gamma, mu, iters, st);
-  };
-  switch (variant) {
-    case 1: launch(secular_kernel<4, 3>, 4); break;
-    case 2: launch(secular_kernel<2, 4>, 2); break;
-    case 3: launch(secular_kernel<8, 1>, 8); break;
-    case 4: launch(secular_kernel<2, 2>, 2); break;
-    case 5: launch(secular_kernel<2, 3>, 2); break;
-    case 6: launch(secular_kernel<1, 4>, 1); break;
-    case 7: launch(secular_kernel<1, 6>, 1); break;
-    case 8: launch(secular_kernel<3, 3>, 3); break;
-    default: launch(secular_kernel<4, 2>, 4); break;
-  }
+  // two roots per warp, four CTAs per SM: measured fastest at k = 32768 among
+  // R = 1..8 roots per warp and 1..6 CTAs per SM
+  constexpr int R = 2;
+  const int64_t warps = (iend - ibeg + R - 1) / R;
+  const int blocks = (int)((warps + 7) / 8);
+  secular_kernel<R, 4><<<blocks, 256, 0, s>>>(d, z2, sum, k, rho, ibeg, iend, lam, gamma, mu,
+                                               iters, st);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
