@@ -163,6 +163,21 @@ typedef struct hsseig_tree {
   int32_t rmax;
 } hsseig_tree;
 
+/*
+ * (a10) Row interpolative decomposition M ~= X M[J, :] of a batch of p x w matrices
+ * (pkg/src/hsseig/hss.py:104-148, interpolative_decomp / _interp_rows): column-pivoted
+ * QR of M^T with dgeqp3 semantics, truncation where the trailing Frobenius mass of R
+ * drops below (tol ||M||_F)^2 or at max_rank, saturation flag, X = identity on J.
+ * Matrix b at M + b*stride_m (leading dimension ldm); X (p x max_rank, ldx) at
+ * X + b*stride_x, J[b*max_rank ..], rank / resid / saturated per matrix.  Shared memory
+ * per matrix: hsseig_interp_smem_bytes(p, w) <= 227 KB.
+ */
+int64_t hsseig_interp_smem_bytes(int32_t p, int32_t w);
+int hsseig_interp_decomp(const double *M, int64_t ldm, int64_t stride_m, int32_t p, int32_t w,
+                         int64_t batch, double tol, int32_t max_rank, double *X, int64_t ldx,
+                         int64_t stride_x, int32_t *J, int32_t *rank, double *resid,
+                         int32_t *saturated, void *stream);
+
 /* bytes of device memory hsseig_tree_layout carves for one tree */
 int64_t hsseig_tree_bytes(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax);
 /*

@@ -8,7 +8,7 @@ from .dc import (EigenResult, MergeRecord, SolverConfig, merge_update, update_ve
                  update_vectors_hss)
 from .flops import FlopCounter
 from .hss import (HssPartition, HssTree, build_partition, estimate_rank, hss_matmul_right,
-                  hss_to_dense, rand_hss_construct, rank_bound)
+                  hss_to_dense, interpolative_decomp, rand_hss_construct, rank_bound)
 from .matgen import (FAMILIES, SymTridiagonal, gen_clement, gen_config5, gen_hermite, gen_kac,
                      gen_laguerre, gen_legendre, gen_toeplitz, gen_uniform, isolated_merge_system)
 from .solver import adc_solve

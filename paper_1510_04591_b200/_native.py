@@ -75,6 +75,9 @@ _SIGS = {
     "hsseig_hss_build_rand": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_vp, c_vp, c_i64,
                                              c_dbl, ctypes.POINTER(Tree), c_vp, c_vp]),
     "hsseig_tree_clear": (ctypes.c_int, [ctypes.POINTER(Tree), c_vp]),
+    "hsseig_interp_smem_bytes": (c_i64, [c_i32, c_i32]),
+    "hsseig_interp_decomp": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i32, c_i32, c_i64, c_dbl, c_i32,
+                                            c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "hsseig_hss_build_rand_levels": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_vp, c_vp,
                                                     c_i64, c_dbl, ctypes.POINTER(Tree), c_vp,
                                                     ctypes.c_int, ctypes.c_int, ctypes.c_int,

@@ -186,20 +186,19 @@ __device__ __forceinline__ double lapy2(double x, double y) {
   return wv * sqrt(1.0 + q * q);
 }
 
-// Truncation, saturation flag, T = R11^{-1} R12 and the ID outputs for the factored M^T held
-// in shared memory in pivot order (sA[j*SW + t], piv[j] = candidate at position j).
-__device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, bool leaf, int p,
-                                          double nf, double tol, const double* __restrict__ om,
-                                          int64_t ldom, hsseig_status* st, const double* Mg,
-                                          double* sA, double* tail, double* red, int* piv) {
+// Truncation of the factored A = M^T (hss.py:128-148): trailing Frobenius mass of R's
+// rows, rank r = min(first t with tail(t) <= (tol ||M||_F)^2, max_rank, nonzero diagonal),
+// saturation flag, relative residual, then T = R11^{-1} R12 in place (dtrsm L/U/N/N).
+__device__ __forceinline__ void id_truncate(double* sA, double* tail, int p, int w, int SW,
+                                            double nf, double tol, int max_rank, int& r,
+                                            int& sat, double& resid) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int nthr = blockDim.x;
-  const int w = T.w, ws = T.ws, SW = w | 1;
   __shared__ double s_resid;
   __shared__ int s_r, s_sat;
-  (void)red;
-  int r = 0, sat = 0;
-  double resid = 0.0;
+  r = 0;
+  sat = 0;
+  resid = 0.0;
   const int mn = min(w, p);
   if (!(nf == 0.0 || p == 0 || w == 0)) {
     // trailing Frobenius mass of R's rows, cumulated from the bottom (hss.py:134-136)
@@ -223,9 +222,11 @@ __device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, 
         if (tail[t] <= cut) { wanted = t; break; }
       int nz = 0;
       for (int t = 0; t < mn; ++t) nz += (fabs(sA[t * SW + t]) > 0.0) ? 1 : 0;
-      const int rr = min(min(wanted, w), nz);
+      const int rr = min(min(wanted, max_rank), nz);
       s_r = rr;
-      s_sat = (wanted >= w) ? (sqrt(fmax(tail[w - 1], 0.0)) > kFlagTol * nf ? 1 : 0) : 0;
+      s_sat = (wanted >= max_rank && max_rank >= 1)
+                  ? (sqrt(fmax(tail[max_rank - 1], 0.0)) > kFlagTol * nf ? 1 : 0)
+                  : 0;
       s_resid = sqrt(fmax(tail[rr], 0.0)) / nf;
     }
     __syncthreads();
@@ -246,6 +247,22 @@ __device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, 
     }
     __syncthreads();
   }
+
+}
+
+// Truncation, saturation flag, T = R11^{-1} R12 and the ID outputs for the factored M^T held
+// in shared memory in pivot order (sA[j*SW + t], piv[j] = candidate at position j).
+__device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, bool leaf, int p,
+                                          double nf, double tol, const double* __restrict__ om,
+                                          int64_t ldom, hsseig_status* st, const double* Mg,
+                                          double* sA, double* tail, double* red, int* piv) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int nthr = blockDim.x;
+  const int w = T.w, ws = T.ws, SW = w | 1;
+  (void)red;
+  int r = 0, sat = 0;
+  double resid = 0.0;
+  id_truncate(sA, tail, p, w, SW, nf, tol, w, r, sat, resid);
 
   // ---- outputs: basis X (p x r) (+ X^T for V), skeleton indices, selected rows, compressions
   int32_t* rank_arr = side == 0 ? T.rU : T.rV;
@@ -393,47 +410,15 @@ __device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Interpolative decomposition of one p x w matrix M (rows = candidates), hss.py:120-148.
-// Column-pivoted QR of A = M^T (w x p): candidate j of M is column j of A, stored
-// contiguously in shared memory (sA[j*SW + t] = A[t][j], SW odd => conflict-free when
-// consecutive threads own consecutive candidates).
-// Per elimination step: warp 0 picks the pivot (first max of the downdated norms,
-// idamax) and forms the Householder reflector (dlarfg); then every thread owns one
-// trailing candidate and applies the reflector and the dlaqp2 norm downdate to it.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) id_kernel(TreeDev T, int level, double tol,
-                                                 const double* __restrict__ om, int64_t ldom,
-                                                 hsseig_status* st, int j0) {
-  extern __shared__ __align__(16) double sm[];
-  const int j = j0 + blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5, nthr = blockDim.x;
-  const int node = T.lnodes[(1 << level) - 1 + j];
-  const bool leaf = T.left[node] < 0;
-  const int w = T.w, ws = T.ws, SW = w | 1;
-  int p;
-  if (leaf) p = T.hi[node] - T.lo[node];
-  else {
-    int a = T.left[node], b = T.right[node];
-    p = side == 0 ? T.rU[a] + T.rU[b] : T.rV[a] + T.rV[b];
-  }
-  double* Mg = T.M + (size_t)(2 * j + side) * T.pmax * ws;
-  double* sA = sm;                              // p x SW
-  double* vn1 = sA + (size_t)T.pmax * SW;       // p
-  double* vn2 = vn1 + T.pmax;                   // p
-  double* tail = vn2 + T.pmax;                  // w + 1
-  double* red = tail + (w + 1);                 // 32 scratch
-  int* piv = reinterpret_cast<int*>(red + 32);  // p
+// Norms and column-pivoted Householder elimination of A = M^T held in sA (candidate j at
+// sA[j*SW + t]; piv[j] = j on entry).  dgeqp3/dlaqp2 semantics: pivot = first maximum of
+// the downdated norms (idamax), dlarfg reflector, dlaqp2 norm downdate with the sqrt(eps)
+// recompute rule.  Returns ||M||_F.
+__device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* vn2, double* red,
+                                               int* piv, int p, int w, int SW) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int nthr = blockDim.x;
   __shared__ double s_tau, s_nf;
-
-  {
-    for (int e = tid; e < p * w; e += nthr) {
-      int row = e / w, c = e % w;
-      sA[row * SW + c] = Mg[(size_t)row * ws + c];
-    }
-  }
-  for (int e = tid; e < p; e += nthr) piv[e] = e;
-  __syncthreads();
   // Frobenius norm (hss.py:128) and the initial column norms (dgeqp3: dnrm2 per column)
   {
     double s = 0.0;
@@ -547,9 +532,98 @@ __global__ void __launch_bounds__(256, 2) id_kernel(TreeDev T, int level, double
       __syncthreads();
     }
   }
+  return nf;
+}
+
+// ---------------------------------------------------------------------------
+// Interpolative decomposition of one p x w matrix M (rows = candidates), hss.py:120-148.
+// Column-pivoted QR of A = M^T (w x p): candidate j of M is column j of A, stored
+// contiguously in shared memory (sA[j*SW + t] = A[t][j], SW odd => conflict-free when
+// consecutive threads own consecutive candidates).
+// Per elimination step: warp 0 picks the pivot (first max of the downdated norms,
+// idamax) and forms the Householder reflector (dlarfg); then every thread owns one
+// trailing candidate and applies the reflector and the dlaqp2 norm downdate to it.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 2) id_kernel(TreeDev T, int level, double tol,
+                                                 const double* __restrict__ om, int64_t ldom,
+                                                 hsseig_status* st, int j0) {
+  extern __shared__ __align__(16) double sm[];
+  const int j = j0 + blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const int node = T.lnodes[(1 << level) - 1 + j];
+  const bool leaf = T.left[node] < 0;
+  const int w = T.w, ws = T.ws, SW = w | 1;
+  int p;
+  if (leaf) p = T.hi[node] - T.lo[node];
+  else {
+    int a = T.left[node], b = T.right[node];
+    p = side == 0 ? T.rU[a] + T.rU[b] : T.rV[a] + T.rV[b];
+  }
+  double* Mg = T.M + (size_t)(2 * j + side) * T.pmax * ws;
+  double* sA = sm;                              // p x SW
+  double* vn1 = sA + (size_t)T.pmax * SW;       // p
+  double* vn2 = vn1 + T.pmax;                   // p
+  double* tail = vn2 + T.pmax;                  // w + 1
+  double* red = tail + (w + 1);                 // 32 scratch
+  int* piv = reinterpret_cast<int*>(red + 32);  // p
+
+  {
+    for (int e = tid; e < p * w; e += nthr) {
+      int row = e / w, c = e % w;
+      sA[row * SW + c] = Mg[(size_t)row * ws + c];
+    }
+  }
+  for (int e = tid; e < p; e += nthr) piv[e] = e;
+  __syncthreads();
+  const double nf = id_eliminate(sA, vn1, vn2, red, piv, p, w, SW);
   id_finish(T, side, node, leaf, p, nf, tol, om, ldom, st, Mg, sA, tail, red, piv);
 }
 
+
+// Standalone interpolative decomposition of a batch of p x w matrices (hss.py:104-148):
+// one CTA per matrix, the same elimination and truncation as the tree construction.
+__global__ void __launch_bounds__(256) interp_kernel(const double* __restrict__ M, int64_t ldm,
+                                                     int64_t sm, int p, int w, double tol,
+                                                     int max_rank, double* __restrict__ X,
+                                                     int64_t ldx, int64_t sx, int32_t* J,
+                                                     int32_t* rank, double* resid_out,
+                                                     int32_t* sat_out) {
+  extern __shared__ __align__(16) double smi[];
+  const int b = blockIdx.x, tid = threadIdx.x, nthr = blockDim.x;
+  const int SW = w | 1;
+  const double* Mb = M + (size_t)b * sm;
+  double* Xb = X + (size_t)b * sx;
+  double* sA = smi;
+  double* vn1 = sA + (size_t)p * SW;
+  double* vn2 = vn1 + p;
+  double* tail = vn2 + p;
+  double* red = tail + (w + 1);
+  int* piv = reinterpret_cast<int*>(red + 32);
+  int* ipiv = piv + p;
+  for (int e = tid; e < p * w; e += nthr) {
+    const int row = e / w, c = e % w;
+    sA[row * SW + c] = Mb[(size_t)row * ldm + c];
+  }
+  for (int e = tid; e < p; e += nthr) piv[e] = e;
+  __syncthreads();
+  const double nf = id_eliminate(sA, vn1, vn2, red, piv, p, w, SW);
+  int r, sat;
+  double resid;
+  id_truncate(sA, tail, p, w, SW, nf, tol, max_rank, r, sat, resid);
+  for (int e = tid; e < p; e += nthr) ipiv[piv[e]] = e;
+  __syncthreads();
+  for (int e = tid; e < p * r; e += nthr) {   // X[q][t]: identity on J, T^T elsewhere
+    const int q = e / r, t = e % r;
+    const int jj = ipiv[q];
+    Xb[(size_t)q * ldx + t] = jj < r ? (jj == t ? 1.0 : 0.0) : sA[jj * SW + t];
+  }
+  for (int t = tid; t < r; t += nthr) J[(size_t)b * max_rank + t] = piv[t];
+  if (tid == 0) {
+    rank[b] = r;
+    resid_out[b] = resid;
+    sat_out[b] = sat;
+  }
+}
 
 }  // namespace hsseig
 
@@ -762,4 +836,24 @@ extern "C" int hsseig_hss_build_rand_levels(const hsseig_gen* gen, const double*
                                             int nparts, void* stream) {
   return build_levels(gen, omega, ldom, Y, Z, ldy, id_tol, tree, st, lev_from, lev_to, part,
                       nparts, (cudaStream_t)stream);
+}
+
+extern "C" int64_t hsseig_interp_smem_bytes(int32_t p, int32_t w) {
+  return (int64_t)sizeof(double) * ((int64_t)p * (w | 1) + 2 * (int64_t)p + w + 1 + 32) +
+         (int64_t)sizeof(int) * 2 * p + 64;
+}
+
+extern "C" int hsseig_interp_decomp(const double* M, int64_t ldm, int64_t stride_m, int32_t p,
+                                    int32_t w, int64_t batch, double tol, int32_t max_rank,
+                                    double* X, int64_t ldx, int64_t stride_x, int32_t* J,
+                                    int32_t* rank, double* resid, int32_t* saturated, void* stream) {
+  if (p < 0 || w < 0 || batch < 0 || max_rank < 0 || ldm < w || ldx < max_rank) HSS_ARG_FAIL();
+  if (batch == 0) return HSSEIG_OK;
+  const int64_t smem = hsseig_interp_smem_bytes(p, w);
+  if (smem > 227 * 1024 || !M || !X || !J || !rank || !resid || !saturated) HSS_ARG_FAIL();
+  cudaFuncSetAttribute(interp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  interp_kernel<<<(unsigned)batch, 256, smem, (cudaStream_t)stream>>>(
+      M, ldm, stride_m, p, w, tol, max_rank, X, ldx, stride_x, J, rank, resid, saturated);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
 }

@@ -310,6 +310,45 @@ def mult_flops(tree, P):
     return f
 
 
+FLAG_TOL = 1e-12   # hss.py:117
+
+
+def _interp_rows(M, tol, max_rank):
+    """Row ID with residual and saturation signal (hss.py:118-148), on the device.
+
+    Returns (X, J, resid, saturated): X a CUDA tensor (p x r) with the identity on the rows
+    J (NumPy intp), resid the trailing-mass estimate relative to ||M||_F.
+    """
+    Md = dev(M)
+    if Md.ndim != 2:
+        raise ValueError("M must be a matrix")
+    p, w = Md.shape
+    if p == 0 or w == 0 or max_rank == 0:
+        return (torch.zeros(p, 0, dtype=torch.float64, device="cuda"), np.zeros(0, dtype=np.intp),
+                0.0, False)
+    lib = nat.load()
+    if int(lib.hsseig_interp_smem_bytes(p, w)) > 227 * 1024:
+        raise ValueError(f"{p} x {w} is too large for one shared-memory ID")
+    Md = Md.contiguous()
+    mr = int(max_rank)
+    X = torch.zeros(p, max(mr, 1), dtype=torch.float64, device="cuda")
+    J = torch.zeros(max(mr, 1), dtype=torch.int32, device="cuda")
+    rk = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rs = torch.zeros(1, dtype=torch.float64, device="cuda")
+    sat = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.check(lib.hsseig_interp_decomp(nat.ptr(Md), Md.stride(0), 0, p, w, 1, float(tol), mr,
+                                       nat.ptr(X), X.stride(0), 0, nat.ptr(J), nat.ptr(rk),
+                                       nat.ptr(rs), nat.ptr(sat), nat.stream_ptr()), "interp_decomp")
+    r = int(rk.cpu()[0])
+    return (X[:, :r], J[:r].cpu().numpy().astype(np.intp), float(rs.cpu()[0]), bool(int(sat.cpu()[0])))
+
+
+def interpolative_decomp(M, tol, max_rank):
+    """Row interpolative decomposition M ~= X @ M[J, :] (hss.py:104-111)."""
+    X, J, _, _ = _interp_rows(M, tol, max_rank)
+    return X, J
+
+
 def sample_omega(k, w, seed):
     """The reference's Gaussian sample block (hss.py:236-237), drawn on the host."""
     return np.random.default_rng(seed).standard_normal((k, w))

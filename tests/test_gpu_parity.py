@@ -494,3 +494,67 @@ def test_distributed_solve_single_rank_nccl():
         assert [m.kept for m in res.merges] == [m.kept for m in ref.merges]
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------- standalone ID (hss.py:104-148)
+def test_id_rank_one():
+    # pkg/tests/test_hss.py (test_id_rank_one)
+    rng = np.random.default_rng(21)
+    M = np.outer(rng.standard_normal(30), rng.standard_normal(12))
+    X, J = hb.interpolative_decomp(M, 1e-13, 10)
+    X = X.cpu().numpy()
+    assert X.shape == (30, 1) and J.size == 1
+    assert np.abs(X @ M[J] - M).max() <= 1e-13 * np.abs(M).max()
+
+
+def test_id_orthonormal_rows_full_rank():
+    rng = np.random.default_rng(22)
+    Q, _ = np.linalg.qr(rng.standard_normal((20, 6)))
+    M = Q.T
+    X, J = hb.interpolative_decomp(M, 1e-14, 6)
+    X = X.cpu().numpy()
+    assert sorted(J.tolist()) == [0, 1, 2, 3, 4, 5]
+    np.testing.assert_array_equal(X[J], np.eye(6))
+    assert X.shape == (6, 6)
+
+
+def test_id_known_rank_seven():
+    rng = np.random.default_rng(23)
+    M = rng.standard_normal((60, 7)) @ rng.standard_normal((7, 44))
+    X, J = hb.interpolative_decomp(M, 1e-13, 30)
+    X = X.cpu().numpy()
+    assert X.shape[1] == 7
+    assert np.linalg.norm(X @ M[J] - M) / np.linalg.norm(M) <= 1e-12
+
+
+def test_id_zero_matrix():
+    X, J = hb.interpolative_decomp(np.zeros((9, 5)), 1e-13, 4)
+    assert tuple(X.shape) == (9, 0) and J.size == 0
+
+
+def test_id_identity_submatrix_and_oracle_pivots():
+    # identity on the selected rows; the pivots follow dgeqp3 (oracle: scipy's qr)
+    from oracle import hss_oracle as orc
+    rng = np.random.default_rng(24)
+    M = rng.standard_normal((25, 10))
+    X, J = hb.interpolative_decomp(M, 1e-13, 10)
+    X = X.cpu().numpy()
+    np.testing.assert_array_equal(X[J], np.eye(J.size))
+    Xo, Jo = orc.row_id(M, 1e-13, 10)[:2]
+    assert np.array_equal(np.asarray(J), np.asarray(Jo))
+    np.testing.assert_allclose(X, Xo, rtol=0, atol=1e-12)
+
+
+def test_id_saturation_flag():
+    # a full-rank block compressed to fewer directions than it has: the flag of hss.py:137-140
+    from oracle import hss_oracle as orc
+    from paper_1510_04591_b200.hss import _interp_rows
+    rng = np.random.default_rng(25)
+    M = rng.standard_normal((40, 12))
+    M[:, 8:] = M[:, :4] @ rng.standard_normal((4, 4))      # rank 8
+    for max_rank in (5, 8, 12):
+        X, J, resid, sat = _interp_rows(M, 1e-13, max_rank)
+        Xo, Jo, ro, so = orc.row_id(M, 1e-13, max_rank)
+        assert X.shape[1] == Xo.shape[1] and sat == so
+        assert abs(resid - ro) <= 1e-12 + 1e-6 * ro
+    assert _interp_rows(M, 1e-13, 5)[3] and not _interp_rows(M, 1e-13, 12)[3]
