@@ -269,6 +269,71 @@ class HssTree:
         return flat.view(drows, mm)[1:m + 1, :m].cpu().numpy().copy()
 
 
+def tree_from_factors(partition, factors, w=None):
+    """An HssTree holding given generators (the reference's HssNode fields, hss.py:151-185).
+
+    factors maps a postorder node index to a dict with U, V (leaf: m x r, inner:
+    (r_left + r_right) x r), B (r x r_sibling, every non-root node) and D (leaves, m x m).
+    The slots are laid out exactly as the construction writes them, so the multiply and
+    hss_to_dense run on it unchanged (used to test the multiply against closed forms).
+    """
+    ranks_u = {i: np.asarray(f["U"]).shape[1] for i, f in factors.items() if "U" in f}
+    ranks_v = {i: np.asarray(f["V"]).shape[1] for i, f in factors.items() if "V" in f}
+    rmax = max(list(ranks_u.values()) + list(ranks_v.values()) + [1])
+    w = int(w or rmax)
+    if w > partition.min_leaf or w > MAX_WIDTH:
+        raise ValueError("ranks above the smallest leaf / supported width")
+    tree = HssTree(partition, w)
+    ct, nn = tree.ct, tree.ct.n_nodes
+    lib = nat.load()
+    nat.check(lib.hsseig_tree_clear(ctypes.byref(ct), nat.stream_ptr()), "tree_clear")
+    ws, pmax = ct.ws, ct.pmax
+    f64 = dict(dtype=torch.float64, device="cuda")
+    rU = np.zeros(nn, dtype=np.int32)
+    rV = np.zeros(nn, dtype=np.int32)
+    for i in range(nn):
+        rU[i] = ranks_u.get(i, 0)
+        rV[i] = ranks_v.get(i, 0)
+    tree._view("rU", torch.int32, nn, 0).copy_(torch.as_tensor(rU))
+    tree._view("rV", torch.int32, nn, 0).copy_(torch.as_tensor(rV))
+    Bv = tree._view("B", torch.float64, nn * ws * ws, 0).view(nn, ws, ws)
+    Bv.zero_()
+    drows = (ct.mmax + 1 + 15) // 16 * 16 + 2
+    Dv = tree._view("D", torch.float64, partition.n_leaves * drows * ct.dld, 0).view(
+        partition.n_leaves, drows, ct.dld)
+    Dv.zero_()
+    Uv = tree._view("U", torch.float64, nn * pmax * ws, 0).view(nn, pmax, ws)
+    Vv = tree._view("V", torch.float64, nn * pmax * ws, 0).view(nn, pmax, ws)
+    Vt = tree._view("Vt", torch.float64, nn * ws * pmax, 0).view(nn, ws, pmax)
+    for nd in tree.nodes:
+        i = nd.index
+        f = factors.get(i, {})
+        if i == tree.root:
+            continue
+        U = torch.as_tensor(np.asarray(f["U"], dtype=np.float64), **f64)
+        V = torch.as_tensor(np.asarray(f["V"], dtype=np.float64), **f64)
+        Uv[i, 1:1 + U.shape[0], :U.shape[1]] = U
+        Vv[i, 1:1 + V.shape[0], :V.shape[1]] = V
+        # V^T: candidate q at column q; an inner node's right-child candidates start at an
+        # even column (16-byte TMA box starts)
+        if nd.is_leaf:
+            Vt[i, :V.shape[1], :V.shape[0]] = V.T
+        else:
+            na = int(rV[nd.left])
+            sh = na & 1
+            Vt[i, :V.shape[1], :na] = V[:na].T
+            Vt[i, :V.shape[1], na + sh:V.shape[0] + sh] = V[na:].T
+        B = torch.as_tensor(np.asarray(f["B"], dtype=np.float64), **f64)
+        Bv[i, :B.shape[0], :B.shape[1]] = B
+        if nd.is_leaf:
+            D = torch.as_tensor(np.asarray(f["D"], dtype=np.float64), **f64)
+            Dv[tree._leaf_pos[i], 1:1 + D.shape[0], :D.shape[1]] = D
+    tree._ranks = None
+    tree.r_used = int(max(rU.max(), rV.max()))
+    tree.ct.rmax = tree.r_used
+    return tree
+
+
 def _construct_flops(tree, k, w):
     rU, rV = tree.ranks()
     f = 2 * (gemm_flops(k, k, w) + cauchy_eval_flops(k * k))
