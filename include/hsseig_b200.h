@@ -271,6 +271,10 @@ int hsseig_tql2_batched(const double *a, const double *b, const int64_t *off, in
 int64_t hsseig_deflate(const double *d, const double *z, int64_t n, double rho, double *d_out,
                        double *z_out, int64_t *perm, int64_t *ri, int64_t *rj, double *rc,
                        double *rs, int64_t *n_rot, double *tol_out);
+/* The same with an explicit tolerance (deflate(..., eps_scale), secular.py:91-96). */
+int64_t hsseig_deflate_tol(const double *d, const double *z, int64_t n, double rho, double tol,
+                           double *d_out, double *z_out, int64_t *perm, int64_t *ri, int64_t *rj,
+                           double *rc, double *rs, int64_t *n_rot);
 /* W[:, c] = blockdiag(Q1, Q2)[:, src[c]] (dc.py:222-224, 241, 255). */
 int hsseig_assemble_merge(const double *Q1, int64_t n1, const double *Q2, int64_t n2,
                           const int64_t *src, double *W, int64_t ldw, void *stream);

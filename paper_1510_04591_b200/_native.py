@@ -96,6 +96,8 @@ _SIGS = {
                                            c_vp, c_vp]),
     "hsseig_deflate": (c_i64, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                c_vp, c_vp]),
+    "hsseig_deflate_tol": (c_i64, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                   c_vp, c_vp, c_vp]),
     "hsseig_assemble_merge": (ctypes.c_int, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp]),
     "hsseig_apply_rotations": (ctypes.c_int, [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64,
                                               c_vp]),

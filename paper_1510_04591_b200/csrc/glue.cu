@@ -312,6 +312,11 @@ extern "C" int hsseig_gather_columns(const double* A, int64_t lda, const double*
  * of each output slot; rotations (ri, rj, rc, rs; n_rot <= n) in sorted-input indices.
  * Returns k.
  */
+extern "C" int64_t hsseig_deflate_tol(const double* d, const double* z, int64_t n, double rho,
+                                      double tol, double* d_out, double* z_out, int64_t* perm,
+                                      int64_t* ri, int64_t* rj, double* rc, double* rs,
+                                      int64_t* n_rot);
+
 extern "C" int64_t hsseig_deflate(const double* d, const double* z, int64_t n, double rho,
                                   double* d_out, double* z_out, int64_t* perm, int64_t* ri,
                                   int64_t* rj, double* rc, double* rs, int64_t* n_rot,
@@ -322,7 +327,16 @@ extern "C" int64_t hsseig_deflate(const double* d, const double* z, int64_t n, d
     dmax = std::max(dmax, std::fabs(d[t]));
     zz += z[t] * z[t];
   }
-  const double tol = 8.0 * kEps * std::max(dmax, rho * zz);
+  const double tol = 8.0 * kEps * std::max(dmax, rho * zz);   // secular.py:91-93
+  if (tol_out) *tol_out = tol;
+  return hsseig_deflate_tol(d, z, n, rho, tol, d_out, z_out, perm, ri, rj, rc, rs, n_rot);
+}
+
+extern "C" int64_t hsseig_deflate_tol(const double* d, const double* z, int64_t n, double rho,
+                                      double tol, double* d_out, double* z_out, int64_t* perm,
+                                      int64_t* ri, int64_t* rj, double* rc, double* rs,
+                                      int64_t* n_rot) {
+  if (n < 1) return -1;
   std::vector<int64_t> order(n);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return d[x] < d[y]; });
@@ -353,7 +367,6 @@ extern "C" int64_t hsseig_deflate(const double* d, const double* z, int64_t n, d
   for (int64_t t : kept) { d_out[q] = ds[t]; z_out[q] = zs[t]; perm[q] = order[t]; ++q; }
   for (int64_t t : defl) { d_out[q] = ds[t]; z_out[q] = zs[t]; perm[q] = order[t]; ++q; }
   *n_rot = nr;
-  if (tol_out) *tol_out = tol;
   return (int64_t)kept.size();
 }
 

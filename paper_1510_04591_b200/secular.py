@@ -4,6 +4,7 @@ Host mirror of pkg/src/hsseig/secular.py (same names, argument meaning and
 exceptions).  Arrays live on the CUDA device as float64 torch tensors; numpy
 inputs are uploaded.  Compute runs in libhsseig_b200.so (csrc/roots.cu).
 """
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -101,6 +102,61 @@ class SecularSolution:
     @property
     def pole_bound(self):
         return float(self.lam[-1] + self.mu[-1])
+
+
+EPS = float(np.finfo(np.float64).eps)
+
+
+def deflation_tolerance(d, z, rho, eps_scale=1.0):
+    """secular.py:91-93"""
+    d = np.asarray(d, dtype=np.float64)
+    z = np.asarray(z, dtype=np.float64)
+    return eps_scale * 8.0 * EPS * max(float(np.abs(d).max()), rho * float(np.sum(z * z)))
+
+
+@dataclass
+class DeflationOutcome:
+    """secular.py (DeflationOutcome): the kept system, the column permutation (kept first,
+    then the deflated poles ascending), Givens rotations in the caller's indices."""
+
+    kept: RankOneSystem
+    permutation: np.ndarray
+    rotations: list
+    deflated_eigenvalues: list
+    n_deflated: int
+    tol: float
+
+
+def deflate(d, z, rho, eps_scale=1.0):
+    """Deflate negligible weights and (near-)equal pole pairs (secular.py:96-156).
+
+    O(n) host work (the restated C routine of csrc/glue.cu, the same one the solver
+    runs for every merge); the kept system is returned on the device.
+    """
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    if d.shape != z.shape or d.ndim != 1 or d.size < 1:
+        raise ValueError("d and z must be 1-D arrays of equal positive length")
+    if not (np.all(np.isfinite(d)) and np.all(np.isfinite(z)) and np.isfinite(rho)):
+        raise ValueError("non-finite input")
+    if rho <= 0.0:
+        raise ValueError("rho must be positive")
+    n = d.size
+    tol = deflation_tolerance(d, z, rho, eps_scale)
+    d_out, z_out = np.empty(n), np.empty(n)
+    perm = np.empty(n, dtype=np.int64)
+    ri, rj = np.empty(n, dtype=np.int64), np.empty(n, dtype=np.int64)
+    rc, rs = np.empty(n), np.empty(n)
+    nrot = ctypes.c_int64(0)
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    k = int(nat.load().hsseig_deflate_tol(P(d), P(z), n, float(rho), float(tol), P(d_out), P(z_out),
+                                          P(perm), P(ri), P(rj), P(rc), P(rs), ctypes.byref(nrot)))
+    nr = int(nrot.value)
+    rotations = [(int(ri[t]), int(rj[t]), float(rc[t]), float(rs[t])) for t in range(nr)]
+    deflated = [(int(perm[t]), float(d_out[t])) for t in range(k, n)]
+    kept = RankOneSystem(d_out[:k].copy(), z_out[:k].copy(), float(rho))
+    return DeflationOutcome(kept=kept, permutation=perm.astype(np.intp), rotations=rotations,
+                            deflated_eigenvalues=deflated, n_deflated=n - k, tol=tol)
 
 
 def solve_secular(sys, flops=None, check=True):

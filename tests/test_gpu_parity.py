@@ -558,3 +558,68 @@ def test_id_saturation_flag():
         assert X.shape[1] == Xo.shape[1] and sat == so
         assert abs(resid - ro) <= 1e-12 + 1e-6 * ro
     assert _interp_rows(M, 1e-13, 5)[3] and not _interp_rows(M, 1e-13, 12)[3]
+
+
+# ------------------------------------------------- deflation (secular.py:91-156)
+def test_deflate_zero_weight():
+    from paper_1510_04591_b200.secular import deflate
+    out = deflate(np.array([1.0, 2.0, 3.0]), np.array([0.3, 0.0, 0.5]), 1.0)
+    assert out.n_deflated == 1
+    assert out.deflated_eigenvalues == [(1, 2.0)]
+    assert out.kept.size == 2
+    assert not out.rotations
+
+
+def test_deflate_equal_poles_givens():
+    from paper_1510_04591_b200.secular import deflate
+    out = deflate(np.array([1.0, 1.0]), np.array([3.0 / 5.0, 4.0 / 5.0]), 1.0)
+    assert len(out.rotations) == 1
+    i, j, c, s = out.rotations[0]
+    assert (i, j) == (0, 1)
+    np.testing.assert_allclose([c, s], [3.0 / 5.0, 4.0 / 5.0], rtol=0, atol=1e-15)
+    assert abs(out.deflated_eigenvalues[0][1] - 1.0) <= 1e-15
+    sol = hb.solve_secular(out.kept)
+    assert abs(float(sol.lam[0]) - 2.0) <= 1e-14
+
+
+def test_deflate_well_separated_keeps_everything():
+    from paper_1510_04591_b200.secular import deflate
+    rng = np.random.default_rng(41)
+    d = np.arange(8, dtype=float)
+    z = rng.uniform(0.1, 1.0, 8) * rng.choice([-1.0, 1.0], 8)
+    out = deflate(d, z, 1.0)
+    assert out.n_deflated == 0
+    np.testing.assert_array_equal(out.kept.d.cpu().numpy(), d)
+
+
+def test_deflate_reconstruction_invariant():
+    from paper_1510_04591_b200.secular import deflate
+    rng = np.random.default_rng(42)
+    n = 30
+    d = np.round(rng.uniform(-2, 2, n), 1)
+    z = rng.standard_normal(n) * (rng.random(n) > 0.2)
+    rho = 1.7
+    out = deflate(d, z, rho)
+    ds, zs = d.copy(), z.copy()
+    for i, j, c, s in out.rotations:
+        zi, zj = zs[i], zs[j]
+        zs[i], zs[j] = c * zi + s * zj, -s * zi + c * zj
+        di, dj = ds[i], ds[j]
+        ds[i], ds[j] = c * c * di + s * s * dj, s * s * di + c * c * dj
+    k = out.kept.size
+    np.testing.assert_allclose(ds[out.permutation[:k]], out.kept.d.cpu().numpy(), rtol=4 * EPS)
+    np.testing.assert_allclose(zs[out.permutation[:k]], out.kept.z.cpu().numpy(), rtol=4 * EPS)
+    assert np.all(np.abs(zs[out.permutation[k:]]) * rho <= out.tol * (1 + 4 * EPS))
+    defl_vals = np.array([v for _, v in out.deflated_eigenvalues])
+    np.testing.assert_allclose(ds[out.permutation[k:]], defl_vals, rtol=4 * EPS)
+    assert k + out.n_deflated == n
+    if k > 1:
+        assert np.diff(out.kept.d.cpu().numpy()).min() > out.tol
+
+
+def test_deflate_rejects_bad_input():
+    from paper_1510_04591_b200.secular import deflate
+    with pytest.raises(ValueError):
+        deflate(np.array([1.0, np.nan]), np.array([1.0, 1.0]), 1.0)
+    with pytest.raises(ValueError):
+        deflate(np.array([1.0]), np.array([1.0]), -2.0)
