@@ -419,6 +419,30 @@ def sample_omega(k, w, seed):
     return np.random.default_rng(seed).standard_normal((k, w))
 
 
+_STREAM = {"ns": None}
+
+
+def draw_omega(k, w, seed):
+    """default_rng(seed).standard_normal((k, w)) on the device, bit-identical to the host
+    draw (csrc/normals.cu, checked against NumPy once per process); rows padded to an even
+    leading dimension for the TMA sampler.  Falls back to the host draw only when NumPy's
+    ziggurat tables cannot be located."""
+    from . import sample_rng
+    if not sample_rng.available():
+        return dev(sample_omega(k, w, seed))
+    n = k * w
+    ns = _STREAM["ns"]
+    if ns is None or ns.nmax < n:
+        ns = _STREAM["ns"] = sample_rng.NormalStream(n)
+    ld = w + (w & 1)
+    om = torch.empty(k, ld, dtype=torch.float64, device="cuda")
+    if ld != w:
+        om[:, w:] = 0.0
+    ns.draw(seed, n, om, w=w, ld=ld)
+    ns.fixup()
+    return om[:, :w]
+
+
 def rand_hss_construct(A, partition, r, p=10, seed=0, id_tol=DEFAULT_ID_TOL, flops=None,
                        omega=None, finish=True):
     """Randomized bottom-up construction from one Gaussian sample (hss.py:217-306)."""
@@ -431,9 +455,7 @@ def rand_hss_construct(A, partition, r, p=10, seed=0, id_tol=DEFAULT_ID_TOL, flo
         raise ValueError(f"sample width {w} exceeds smallest leaf {partition.min_leaf}")
     if w > MAX_WIDTH:
         raise ValueError(f"sample width {w} above the supported {MAX_WIDTH}")
-    if omega is None:
-        omega = sample_omega(A.k, w, seed)
-    om = dev(omega)
+    om = dev(omega) if omega is not None else draw_omega(A.k, w, seed)
     Y, Z = A.sample(om)
     tree = HssTree(partition, w, seed=seed)
     st = Status(A.k)
