@@ -34,6 +34,18 @@ def shard_range(k, rank, world):
     return lo, min(k, lo + c), c
 
 
+def _all_gather(parts, t, group=None):
+    """dist.all_gather; CUDA tensors go through host memory on a gloo group (the CPU test
+    backend), NCCL gathers them in place."""
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        hp = [torch.empty(p.shape, dtype=p.dtype) for p in parts]
+        dist.all_gather(hp, t.cpu(), group=group)
+        for p, h in zip(parts, hp):
+            p.copy_(h)
+        return
+    dist.all_gather(parts, t, group=group)
+
+
 def gather_rows(local, chunk, k, group=None):
     """All-gather equal-size row chunks (padded to `chunk` rows) and trim to k rows."""
     world = dist.get_world_size(group)
@@ -42,7 +54,7 @@ def gather_rows(local, chunk, k, group=None):
                           device=local.device)
         local = torch.cat([local, pad])
     parts = [torch.empty_like(local) for _ in range(world)]
-    dist.all_gather(parts, local.contiguous(), group=group)
+    _all_gather(parts, local.contiguous(), group)
     return torch.cat(parts)[:k]
 
 
@@ -160,7 +172,7 @@ def gather_subtrees(tree, s_lev, group=None):
         lo, hi = rng[rank]
         mine = tree.mem[off + lo * nb: off + hi * nb]
         parts = [torch.empty_like(mine) for _ in range(world)]
-        dist.all_gather(parts, mine.contiguous(), group=group)
+        _all_gather(parts, mine.contiguous(), group)
         for r, (a, b) in enumerate(rng):
             if r != rank:
                 tree.mem[off + a * nb: off + b * nb].copy_(parts[r])
@@ -422,7 +434,7 @@ def _gather_padded(vec, length, group, device):
     t = torch.zeros(length, dtype=torch.float64, device=device)
     t[:vec.numel()] = vec
     parts = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(parts, t, group=group)
+    _all_gather(parts, t, group)
     return parts
 
 
@@ -495,7 +507,7 @@ def adc_solve_distributed(T, cfg, ops, group=None):
         edge[0, :Qb.shape[1]] = Qb[0]
         edge[1, :Qb.shape[1]] = Qb[-1]
         eparts = [torch.empty_like(edge) for _ in range(size)]
-        dist.all_gather(eparts, edge, group=grp)
+        _all_gather(eparts, edge, grp)
         zrow = np.concatenate([eparts[half - 1][1, :nL].cpu().numpy(),
                                eparts[half][0, :nR].cpu().numpy()])
         bk = float(b[nd["split"] - 1])
