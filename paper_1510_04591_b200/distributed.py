@@ -123,7 +123,14 @@ class ShardedMerge:
         if tree is not None and not ops.flagged(tree):
             info["used_hss"] = True
             info["r_used"] = ops.r_used(tree)
+            timed = X.is_cuda
+            if timed:   # the row-local multiply's device time (bench's roofline)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
             out = ops.multiply(X, tree)
+            if timed:
+                e1.record()
+                info["multiply_events"] = (e0, e1)
         else:
             info["fell_back"] = tree is not None
             out = ops.dense(X, gen)
