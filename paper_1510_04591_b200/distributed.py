@@ -159,30 +159,41 @@ def subtree_layout(depth, s_lev):
 
 
 def gather_subtrees(tree, s_lev, group=None):
-    """All-gather the node slots each rank built for its subtree (contiguous postorder
-    blocks; D by leaf) so every rank holds the full tree below level s_lev."""
+    """All-gather what the other ranks built for their subtrees, in one collective: every
+    node's ranks, flags, skeletons, U, V^T and B (what the multiply and the upper levels
+    read), the leaves' D, and only for the subtree roots the selected rows and
+    compressions the upper levels consume."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     ct = tree.ct
     depth, ws, pmax, dld = ct.depth, ct.ws, ct.pmax, ct.dld
     blocks, leaves = subtree_layout(depth, s_lev)
+    roots = [(b - 1, b) for _, b in blocks]          # a subtree root is last in its block
     per_node = {"rU": 4, "rV": 4, "flags": 8, "rres": 8, "cres": 8, "rsel": 4 * ws, "csel": 4 * ws,
-                "rloc": 4 * ws, "cloc": 4 * ws, "U": 8 * pmax * ws, "V": 8 * pmax * ws,
-                "Vt": 8 * ws * pmax, "B": 8 * ws * ws, "psel": 8 * ws * ws, "tsel": 8 * ws * ws,
-                "ycomp": 8 * ws * ws, "zcomp": 8 * ws * ws}
+                "rloc": 4 * ws, "cloc": 4 * ws, "U": 8 * pmax * ws, "Vt": 8 * ws * pmax,
+                "B": 8 * ws * ws}
+    root_only = {"psel": 8 * ws * ws, "tsel": 8 * ws * ws, "ycomp": 8 * ws * ws,
+                 "zcomp": 8 * ws * ws}
     base = tree.mem.data_ptr()
-    regions = [(name, nb, blocks) for name, nb in per_node.items()]
     drows = (ct.mmax + 1 + 15) // 16 * 16 + 2
-    regions.append(("D", 8 * drows * dld, leaves))
+    regions = ([(name, nb, blocks) for name, nb in per_node.items()]
+               + [(name, nb, roots) for name, nb in root_only.items()]
+               + [("D", 8 * drows * dld, leaves)])
+    spans = []
     for name, nb, rng in regions:
         off = getattr(ct, name) - base
-        lo, hi = rng[rank]
-        mine = tree.mem[off + lo * nb: off + hi * nb]
-        parts = [torch.empty_like(mine) for _ in range(world)]
-        _all_gather(parts, mine.contiguous(), group)
-        for r, (a, b) in enumerate(rng):
-            if r != rank:
-                tree.mem[off + a * nb: off + b * nb].copy_(parts[r])
+        spans.append([(off + a * nb, off + b * nb) for a, b in rng])
+    mine = torch.cat([tree.mem[sp[rank][0]:sp[rank][1]] for sp in spans])
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    _all_gather(parts, mine, group)
+    for r in range(world):
+        if r == rank:
+            continue
+        pos = 0
+        for sp in spans:
+            a, b = sp[r]
+            tree.mem[a:b].copy_(parts[r][pos:pos + (b - a)])
+            pos += b - a
 
 
 class GpuOps:
