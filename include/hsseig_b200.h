@@ -352,6 +352,15 @@ int hsseig_wave_gather(const double *Qk, const int64_t *qoff, const int64_t *kep
                        const int32_t *row_merge, const int64_t *order, double *out,
                        const int64_t *ooff, int64_t nrows, void *stream);
 
+/* The dense update through materialised column panels of C (the reference's to_dense
+   entries) and the TMA/DMMA GEMM engine (k >= 1024, 16-byte aligned Qb rows, even ldq);
+   otherwise the same as hsseig_dense_update.  work: hsseig_dense_update_work_doubles(k,
+   panel_cols) doubles for panels of up to panel_cols columns. */
+int64_t hsseig_dense_update_work_doubles(int64_t k, int64_t panel_cols);
+int hsseig_dense_update_ws(const double *Qb, int64_t ldq, int64_t P, const hsseig_gen *gen,
+                           double *out, int64_t ldo, double *work, int64_t work_doubles,
+                           void *stream);
+
 /* Plain batched helper used by tests/bench: out = A @ B (P x K)(K x N), FP64 DMMA. */
 int hsseig_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *stream);

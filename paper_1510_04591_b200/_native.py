@@ -87,6 +87,9 @@ _SIGS = {
                                                c_i64, c_vp, c_vp]),
     "hsseig_dense_update": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(Gen), c_vp, c_i64,
                                            c_vp]),
+    "hsseig_dense_update_work_doubles": (c_i64, [c_i64, c_i64]),
+    "hsseig_dense_update_ws": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(Gen), c_vp, c_i64,
+                                              c_vp, c_i64, c_vp]),
     "hsseig_set_normal_tables": (ctypes.c_int, [c_vp, c_vp, c_vp]),
     "hsseig_normals_work_bytes": (c_i64, [c_i64]),
     "hsseig_pcg64_normals": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,

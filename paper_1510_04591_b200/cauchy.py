@@ -11,6 +11,8 @@ from .flops import cauchy_eval_flops, gemm_flops
 from .secular import column_normalizers, dev, dev_rows, stable_gap
 
 MAX_SAMPLE_WIDTH = 128
+DENSE_PANEL_MIN_K = 1024          # below: the fused kernel (C tiles generated in smem)
+DENSE_PANEL_BYTES = 2 << 30       # column panels of C materialised for the dense update
 
 
 class CauchyEvecMatrix:
@@ -130,7 +132,21 @@ class CauchyEvecMatrix:
             raise ValueError("inner dimensions do not match")
         if out is None:
             out = torch.empty(Q.shape[0], self.k, dtype=torch.float64, device="cuda")
-        nat.check(nat.load().hsseig_dense_update(nat.ptr(Q), Q.stride(0), Q.shape[0], self._gen,
-                                                 nat.ptr(out), out.stride(0), nat.stream_ptr()),
+        lib = nat.load()
+        if self.k >= DENSE_PANEL_MIN_K and Q.shape[0] > 0:
+            # materialised column panels of C (<= DENSE_PANEL_BYTES) on the TMA/DMMA engine
+            if Q.stride(0) % 2 or Q.data_ptr() % 16:
+                Qp = torch.empty(Q.shape[0], self.k + (self.k & 1), dtype=torch.float64, device="cuda")
+                Qp[:, :self.k] = Q
+                Q = Qp[:, :self.k]
+            cols = max(128, DENSE_PANEL_BYTES // (8 * self.k))
+            work = torch.empty(int(lib.hsseig_dense_update_work_doubles(self.k, cols)),
+                               dtype=torch.float64, device="cuda")
+            nat.check(lib.hsseig_dense_update_ws(nat.ptr(Q), Q.stride(0), Q.shape[0], self._gen,
+                                                 nat.ptr(out), out.stride(0), nat.ptr(work),
+                                                 work.numel(), nat.stream_ptr()), "dense_update")
+            return out
+        nat.check(lib.hsseig_dense_update(nat.ptr(Q), Q.stride(0), Q.shape[0], self._gen,
+                                          nat.ptr(out), out.stride(0), nat.stream_ptr()),
                   "dense_update")
         return out

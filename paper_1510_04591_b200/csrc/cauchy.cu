@@ -326,6 +326,7 @@ constexpr double kMatCapBytes = 12.0 * (1 << 30);   // largest panel pair materi
 
 // out[i][j] = C[i0 + i][j0 + j] for i < ni, j < nj (MUFU reciprocal + 2 Newton steps, as the
 // fused sampling kernel: within 2 ulp of the reference's division)
+template <bool DIV>
 __global__ void gen_panel_kernel(CauchyGen g, int64_t i0, int64_t ni, int64_t j0, int64_t nj,
                                  double* __restrict__ out, int64_t ld) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -336,7 +337,8 @@ __global__ void gen_panel_kernel(CauchyGen g, int64_t i0, int64_t ni, int64_t j0
   for (int64_t i = blockIdx.y; i < ni; i += gridDim.y) {
     const int64_t gi = i0 + i;
     const double gap = stable_gap(gi, gj, __ldg(g.d + gi), dj, dnj, gmj, mj);
-    out[i * ld + j] = (__ldg(g.zhat + gi) * vj) * rcp_nr(gap);
+    // DIV: the reference's entry (to_dense, IEEE division); else MUFU reciprocal + 2 Newton
+    out[i * ld + j] = DIV ? (__ldg(g.zhat + gi) * vj) / gap : (__ldg(g.zhat + gi) * vj) * rcp_nr(gap);
   }
 }
 
@@ -460,11 +462,11 @@ static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom,
   {
     // each thread walks many rows with its column's generators in registers
     dim3 gr((unsigned)((k + 255) / 256), (unsigned)imin64(nr, 128));
-    gen_panel_kernel<<<gr, 256, 0, s>>>(g, row0, nr, 0, k, C1, p.kld);
+    gen_panel_kernel<false><<<gr, 256, 0, s>>>(g, row0, nr, 0, k, C1, p.kld);
     HSS_CHECK_LAUNCH();
     if (!p.shared) {
       dim3 g2((unsigned)((nr + 255) / 256), (unsigned)imin64(k, 128));
-      gen_panel_kernel<<<g2, 256, 0, s>>>(g, 0, k, row0, nr, C2, p.nld);
+      gen_panel_kernel<false><<<g2, 256, 0, s>>>(g, 0, k, row0, nr, C2, p.nld);
       HSS_CHECK_LAUNCH();
     }
     dim3 gt((unsigned)((k + 31) / 32), (unsigned)((w + 31) / 32));
@@ -618,5 +620,48 @@ extern "C" int hsseig_wave_tile_shape(int32_t* bm, int32_t* bn) {
   using T = Tile<4, 8, 4, 2, 2>;
   *bm = T::BM;
   *bn = T::BN;
+  return HSSEIG_OK;
+}
+
+// Dense update out = Qb C through materialised column panels of C (the reference's
+// to_dense entries) and the TMA/DMMA engine; falls back to the fused kernel when the
+// workspace is too small.  work: hsseig_dense_update_work_doubles(k, panel_cols).
+static int64_t dense_ws_overhead(int64_t k) {
+  return ((k + 127) / 128 * (int64_t)sizeof(TJob) + 7) / 8 + (int64_t)(sizeof(MapSet) + 512) / 8 + 64;
+}
+
+extern "C" int64_t hsseig_dense_update_work_doubles(int64_t k, int64_t panel_cols) {
+  if (k < 1 || panel_cols < 1) return -1;
+  const int64_t kc = imin64(k, (panel_cols + 127) / 128 * 128);
+  return k * (kc + (kc & 1)) + dense_ws_overhead(k);
+}
+
+extern "C" int hsseig_dense_update_ws(const double* Qb, int64_t ldq, int64_t P,
+                                      const hsseig_gen* gen, double* out, int64_t ldo,
+                                      double* work, int64_t work_doubles, void* stream) {
+  if (!gen || P < 0 || ldq < gen->k || ldo < gen->k) HSS_ARG_FAIL();
+  if (P == 0) return HSSEIG_OK;
+  const int64_t k = gen->k;
+  const bool aligned = !(reinterpret_cast<uintptr_t>(Qb) & 15) && !(ldq & 1) &&
+                       !(reinterpret_cast<uintptr_t>(work) & 15);
+  int64_t kc = work ? (work_doubles - dense_ws_overhead(k)) / (k + 1) : 0;
+  kc = imin64(k, kc / 128 * 128);
+  if (k < 1024 || !aligned || kc < 128)
+    return hsseig_dense_update(Qb, ldq, P, gen, out, ldo, stream);
+  const int64_t ldp = kc + (kc & 1);
+  double* panel = work;
+  TJob* jobs = reinterpret_cast<TJob*>(work + k * ldp);
+  MapSet* dmaps = reinterpret_cast<MapSet*>(
+      (reinterpret_cast<uintptr_t>(jobs + (k + 127) / 128) + 255) & ~(uintptr_t)255);
+  CauchyGen g = to_gen(gen);
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int64_t c0 = 0; c0 < k; c0 += kc) {
+    const int64_t nc = imin64(kc, k - c0);
+    dim3 gr((unsigned)((nc + 255) / 256), (unsigned)imin64(k, 128));
+    gen_panel_kernel<true><<<gr, 256, 0, s>>>(g, 0, k, c0, nc, panel, ldp);
+    HSS_CHECK_LAUNCH();
+    const int rc = tma_plain_gemm(Qb, ldq, panel, ldp, out + c0, ldo, P, nc, k, jobs, dmaps, s);
+    if (rc) return rc;
+  }
   return HSSEIG_OK;
 }

@@ -379,19 +379,33 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   return launch_wide(t->mmax, ops, dmaps + 2 * t->depth, jobs + 2 * nup, n, P, s);
 }
 
-extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
-                           int64_t ldc, int64_t M, int64_t N, int64_t K, void* stream) {
-  // Test/bench helper: plain C = A B on the same TMA/DMMA engine, N split in 128-wide jobs.
-  static TJob* jobs = nullptr;
-  static MapSet* dmaps = nullptr;
-  static int cap = 0;
+namespace hsseig {
+int tma_plain_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                   int64_t ldc, int64_t M, int64_t N, int64_t K, TJob* jobs, MapSet* dmaps,
+                   cudaStream_t s) {
   if (M < 0 || N < 0 || K < 0 || lda < K || ldb < N || ldc < N) HSS_ARG_FAIL();
   if (M == 0 || N == 0) return HSSEIG_OK;
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15) || (lda & 1) ||
       (ldb & 1) || K == 0)
     HSS_ARG_FAIL();
   const int nj = (int)((N + 127) / 128);
-  cudaStream_t s = (cudaStream_t)stream;
+  plain_jobs_kernel<<<(nj + 127) / 128, 128, 0, s>>>(jobs, nj, C, ldc, (int)N, (int)K);
+  HSS_CHECK_LAUNCH();
+  // the maps carry the exact extents, so TMA zero-fills the K / N tails
+  const Operand none{nullptr, 0, 0, 0};
+  const Operand ops[kMaps] = {Operand{A, (uint64_t)M, (uint64_t)K, (uint64_t)lda}, none, none, none,
+                              Operand{B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb}, none, none, none};
+  return launch_wide(128, ops, dmaps, jobs, nj, M, s);
+}
+}  // namespace hsseig
+
+extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                           int64_t ldc, int64_t M, int64_t N, int64_t K, void* stream) {
+  // Test/bench helper: plain C = A B on the same TMA/DMMA engine, N split in 128-wide jobs.
+  static TJob* jobs = nullptr;
+  static MapSet* dmaps = nullptr;
+  static int cap = 0;
+  const int nj = (int)((N + 127) / 128);
   if (nj > cap) {
     if (jobs) cudaFree(jobs);
     if (cudaMalloc(&jobs, sizeof(TJob) * nj) != cudaSuccess) return HSSEIG_ERR_CUDA;
@@ -400,13 +414,7 @@ extern "C" int hsseig_gemm(const double* A, int64_t lda, const double* B, int64_
   if (!dmaps) {
     if (cudaMalloc(&dmaps, sizeof(MapSet)) != cudaSuccess) return HSSEIG_ERR_CUDA;
   }
-  plain_jobs_kernel<<<(nj + 127) / 128, 128, 0, s>>>(jobs, nj, C, ldc, (int)N, (int)K);
-  HSS_CHECK_LAUNCH();
-  // the maps carry the exact extents, so TMA zero-fills the K / N tails
-  const Operand none{nullptr, 0, 0, 0};
-  const Operand ops[kMaps] = {Operand{A, (uint64_t)M, (uint64_t)K, (uint64_t)lda}, none, none, none,
-                              Operand{B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb}, none, none, none};
-  return launch_wide(128, ops, dmaps, jobs, nj, M, s);
+  return tma_plain_gemm(A, lda, B, ldb, C, ldc, M, N, K, jobs, dmaps, (cudaStream_t)stream);
 }
 
 extern "C" const char* hsseig_version(void) { return "hsseig_b200 0.2 sm_100a"; }

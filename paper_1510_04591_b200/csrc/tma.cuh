@@ -139,6 +139,11 @@ struct Operand {
 // 1 wide tiles, 2 tall-N tiles (BM 96, BN 128).  Maps go to dmaps (device), jobs are device.
 int tma_jobs_gemm(int shape, int n, const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jobs,
                   int njobs, int64_t M, cudaStream_t s);
+// Plain C = A B (row-major, 16-byte aligned A / B rows) on the engine; jobs: (N+127)/128
+// device TJobs, dmaps: one device MapSet (hss_mult.cu).
+int tma_plain_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                   int64_t ldc, int64_t M, int64_t N, int64_t K, TJob* jobs, MapSet* dmaps,
+                   cudaStream_t s);
 
 static inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
