@@ -297,7 +297,7 @@ int hsseig_assemble_rows(const double *Qc, int64_t ldq, int64_t nrow, int64_t co
  * adc_solve (pkg/src/hsseig/dc.py:194-257) in one set of launches.  Merge m has n1[m] +
  * n2[m] rows, concatenated at roff[m] (row_merge[r] = merge of row r); its children blocks
  * are at device addresses q1[m], q2[m] (row-major n1 x n1, n2 x n2); its n x n block
- * W_m at W + woff[m].  Kept rank-one systems s own roots [koff[s], koff[s+1]) of the
+ * W_m at W + woff[m] with an even leading dimension n + (n & 1).  Kept rank-one systems s own roots [koff[s], koff[s+1]) of the
  * concatenated root arrays; seg_of[i] = system of root i.  st[s] as hsseig_status_init.
  * --------------------------------------------------------------------------------------- */
 /* z rows: [last row of Q1, first row of Q2] per merge (dc.py:112). */
@@ -353,7 +353,7 @@ int hsseig_wave_gather(const double *Qk, const int64_t *qoff, const int64_t *kep
                        const int64_t *ooff, int64_t nrows, void *stream);
 
 /* The dense update through materialised column panels of C (the reference's to_dense
-   entries) and the TMA/DMMA GEMM engine (k >= 1024, 16-byte aligned Qb rows, even ldq);
+   entries) and the TMA/DMMA GEMM engine (k >= 512, 16-byte aligned Qb rows, even ldq);
    otherwise the same as hsseig_dense_update.  work: hsseig_dense_update_work_doubles(k,
    panel_cols) doubles for panels of up to panel_cols columns. */
 int64_t hsseig_dense_update_work_doubles(int64_t k, int64_t panel_cols);

@@ -11,7 +11,7 @@ from .flops import cauchy_eval_flops, gemm_flops
 from .secular import column_normalizers, dev, dev_rows, stable_gap
 
 MAX_SAMPLE_WIDTH = 128
-DENSE_PANEL_MIN_K = 1024          # below: the fused kernel (C tiles generated in smem)
+DENSE_PANEL_MIN_K = 512           # below: the fused kernel (C tiles generated in smem)
 DENSE_PANEL_BYTES = 2 << 30       # column panels of C materialised for the dense update
 
 

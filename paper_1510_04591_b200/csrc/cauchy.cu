@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(T::THREADS) wave_dense_kernel(
   CauchyGen gs = g;
   gs.d += a; gs.dnext += a; gs.gam += a; gs.mu += a; gs.zhat += a; gs.v += a;
   gs.k = k;
-  dense_update_tile<T>(W + woff[s], n, n, gs, out + ooff[s], k, (int64_t)mt * T::BM,
+  dense_update_tile<T>(W + woff[s], n + (n & 1), n, gs, out + ooff[s], k, (int64_t)mt * T::BM,
                        (int64_t)nt * T::BN, smem);
 }
 
@@ -646,7 +646,7 @@ extern "C" int hsseig_dense_update_ws(const double* Qb, int64_t ldq, int64_t P,
                        !(reinterpret_cast<uintptr_t>(work) & 15);
   int64_t kc = work ? (work_doubles - dense_ws_overhead(k)) / (k + 1) : 0;
   kc = imin64(k, kc / 128 * 128);
-  if (k < 1024 || !aligned || kc < 128)
+  if (k < 512 || !aligned || kc < 128)
     return hsseig_dense_update(Qb, ldq, P, gen, out, ldo, stream);
   const int64_t ldp = kc + (kc & 1);
   double* panel = work;

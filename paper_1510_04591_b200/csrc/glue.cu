@@ -162,7 +162,8 @@ __global__ void gather2_kernel(const double* __restrict__ A, int64_t lda, const 
 // Level-batched ("wave") glue: every merge of one recursion depth per launch.  Merge m
 // has children blocks Q1 (n1 x n1) and Q2 (n2 x n2) at arbitrary device addresses, its
 // rows occupy [roff[m], roff[m+1]) of the concatenated row space and its n x n merge
-// block sits at W + woff[m]; row_merge maps a concatenated row to its merge.
+// block sits at W + woff[m] with rows padded to an even leading dimension n + (n & 1) (16-byte
+// aligned rows for the TMA update engine); row_merge maps a concatenated row to its merge.
 // ---------------------------------------------------------------------------
 __global__ void wave_zrows_kernel(const unsigned long long* __restrict__ q1,
                                   const unsigned long long* __restrict__ q2,
@@ -190,7 +191,7 @@ __global__ void wave_assemble_kernel(const unsigned long long* __restrict__ q1,
     const double* Q1 = reinterpret_cast<const double*>(q1[m]);
     const double* Q2 = reinterpret_cast<const double*>(q2[m]);
     const int64_t* sm = src + roff[m];
-    double* w = W + woff[m] + row * n;
+    double* w = W + woff[m] + row * (n + (n & 1));
     for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
       const int64_t sc = sm[c];
       double v = 0.0;
@@ -211,7 +212,7 @@ __global__ void wave_rotate_kernel(double* __restrict__ W, const int64_t* __rest
   if (r0 == r1) return;
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
        row += (int64_t)gridDim.x * blockDim.x) {
-    double* w = W + woff[m] + row * n;
+    double* w = W + woff[m] + row * (n + (n & 1));
     for (int64_t t = r0; t < r1; ++t) {
       const int64_t ia = ca[t], ib = cb[t];
       const double c = cs[t], s = sn[t];
@@ -234,7 +235,7 @@ __global__ void wave_gather_kernel(const double* __restrict__ Qk, const int64_t*
     const int64_t n = roff[m + 1] - roff[m], row = gr - roff[m], k = kept[m];
     const int64_t* om = order + roff[m];
     const double* q = Qk + qoff[m] + row * k;
-    const double* w = W + woff[m] + row * n;
+    const double* w = W + woff[m] + row * (n + (n & 1));
     double* o = out + ooff[m] + row * n;
     for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
       const int64_t sc = om[c];

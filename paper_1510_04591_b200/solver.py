@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .cauchy import CauchyEvecMatrix
+from .cauchy import DENSE_PANEL_MIN_K, CauchyEvecMatrix
 from .dc import (BaseCaseError, EigenResult, MergeRecord, SolverConfig, merge_update,
                  update_vectors_hss)
 from .flops import FlopCounter, cauchy_eval_flops, gemm_flops, secular_flops
@@ -304,7 +304,11 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                                            _cptr(d_out), _cptr(z_out), _cptr(src), _cptr(rot_off),
                                            _cptr(ca), _cptr(cb), _cptr(rc), _cptr(rs)))
         # W blocks in [kept | deflated] column order, then the rotations
-        woff = np.concatenate([[0], np.cumsum(nv * nv)]).astype(np.int64)
+        # W_m rows padded to an even leading dimension (16-byte aligned for the TMA engine);
+        # the gathered output blocks are dense n x n
+        npad = nv + (nv & 1)
+        woff = np.concatenate([[0], np.cumsum(nv * npad)]).astype(np.int64)
+        ooff = np.concatenate([[0], np.cumsum(nv * nv)]).astype(np.int64)
         W = torch.empty(int(woff[-1]), **f64)
         woff_d = _i64(woff)
         # (device temporaries stay referenced until their launch: a freed block is reused
@@ -356,12 +360,17 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             nat.check(lib.hsseig_wave_normalizers(nat.ptr(dk), nat.ptr(dn), nat.ptr(gam), nat.ptr(mu),
                                                   nat.ptr(zh), nat.ptr(koff_d), nat.ptr(seg_of), ktot,
                                                   nat.ptr(vv), s), "wave_normalizers")
-            # dense updates of every system not taking the HSS path, grouped in one launch
+            # dense updates of every system not taking the HSS path: the large ones through
+            # materialised C panels on the TMA/DMMA engine, the rest grouped in one launch
             tasks = []
+            big = []
             for q, m in enumerate(segs):
                 n, k = int(nv[m]), int(kept[m])
                 if cfg.method == "adc-rand" and k > cfg.hss_threshold:
                     hss_m.add(q)
+                    continue
+                if k >= DENSE_PANEL_MIN_K:
+                    big.append(q)
                     continue
                 mt, nt = -(-n // bm), -(-k // bn)
                 t = np.empty((mt * nt, 3), dtype=np.int32)
@@ -369,6 +378,13 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 t[:, 1] = np.repeat(np.arange(mt), nt)
                 t[:, 2] = np.tile(np.arange(nt), mt)
                 tasks.append(t)
+            for q in big:
+                m = segs[q]
+                n, k = int(nv[m]), int(kept[m])
+                sl = slice(int(koff[q]), int(koff[q + 1]))
+                C = CauchyEvecMatrix(dk[sl], gam[sl], mu[sl], zh[sl], vv[sl], dnext=dn[sl])
+                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(npad[m]))
+                C.right_multiply_into(Wm[:, :k], out=Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k))
             if tasks:
                 tk = np.concatenate(tasks)
                 dd_ = (_i64(woff[segs]), _i64(nv[segs]), _i64(qoff[segs]), _i32(tk.ravel()))
@@ -395,7 +411,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 nd = nodes[ms[m]]
                 rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
                 fc = FlopCounter()
-                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, n)
+                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(npad[m]))
                 out = update_vectors_hss(Wm[:, :k], C, cfg, seed=[cfg.seed, nd["mid"]], flops=fc,
                                          record=rec_)
                 Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k).copy_(out)
@@ -411,12 +427,13 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         koff_all[segs] = koff[:-1]
         lib.hsseig_wave_order(nm, _cptr(roff), _cptr(kept), _cptr(koff_all), _cptr(lam_h),
                               _cptr(d_out), _cptr(order), _cptr(lam_out))
-        A = torch.empty(int(woff[-1]), **f64)
+        A = torch.empty(int(ooff[-1]), **f64)
+        ooff_d = _i64(ooff)
         g_ = (_i64(qoff), _i64(kept), _i64(order))
         nat.check(lib.hsseig_wave_gather(nat.ptr(Qk), nat.ptr(g_[0]), nat.ptr(g_[1]),
                                          nat.ptr(W), nat.ptr(woff_d), nat.ptr(roff_d),
                                          nat.ptr(row_merge), nat.ptr(g_[2]), nat.ptr(A),
-                                         nat.ptr(woff_d), nrows, s), "wave_gather")
+                                         nat.ptr(ooff_d), nrows, s), "wave_gather")
         del W, Qk
         # records and flop counts (reference conventions, dc.py:236-247)
         for q, m in enumerate(segs):
@@ -437,6 +454,6 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 records.setdefault(nd["mid"], MergeRecord(size=n, kept=0, n_deflated=n)).flops = \
                     {p: 0 for p in FlopCounter.PHASES}
             state[ms[m]] = (lam_out[roff[m]:roff[m + 1]].copy(),
-                            A[int(woff[m]):int(woff[m + 1])].view(n, n))
+                            A[int(ooff[m]):int(ooff[m + 1])].view(n, n))
     lam, Q = state[sub]
     return lam, Q, records
