@@ -311,15 +311,22 @@ int64_t hsseig_wave_deflate(int64_t nm, const int64_t *n1, const int64_t *n2, co
                             const double *L, const double *zrow, const double *bk, int64_t *kept,
                             double *rho_eff, double *d_out, double *z_out, int64_t *src,
                             int64_t *rot_off, int64_t *ca, int64_t *cb, double *rc, double *rs);
-/* W_m[:, c] = blockdiag(Q1, Q2)[:, src[c]] for every merge. */
+/* Host: compact W layout (kept positions + deflated positions a rotation touches): widths
+   wd, compact blockdiag columns csrc (offsets coff), position -> compact map cmap (-1: not
+   materialised), rotation pairs rewritten to compact indices.  Returns the total width. */
+int64_t hsseig_wave_compact(int64_t nm, const int64_t *roff, const int64_t *kept,
+                            const int64_t *src, const int64_t *rot_off, int64_t *ca, int64_t *cb,
+                            int64_t *wd, int64_t *coff, int64_t *csrc, int64_t *cmap);
+/* Compact W_m (n x wd[m], leading dimension wd + (wd & 1)):
+   W_m[:, j] = blockdiag(Q1, Q2)[:, csrc[coff[m] + j]]. */
 int hsseig_wave_assemble(const uint64_t *q1, const uint64_t *q2, const int64_t *n1,
                          const int64_t *n2, const int64_t *roff, const int32_t *row_merge,
-                         const int64_t *src, double *W, const int64_t *woff, int64_t nrows,
-                         void *stream);
+                         const int64_t *csrc, const int64_t *coff, const int64_t *wd, double *W,
+                         const int64_t *woff, int64_t nrows, void *stream);
 /* Deflation rotations of every merge on its W_m (dc.py:225-230). */
-int hsseig_wave_rotate(double *W, const int64_t *woff, const int64_t *n, const int64_t *rot_off,
-                       const int64_t *ca, const int64_t *cb, const double *c, const double *s,
-                       int64_t nm, int64_t nmax, void *stream);
+int hsseig_wave_rotate(double *W, const int64_t *woff, const int64_t *n, const int64_t *wd,
+                       const int64_t *rot_off, const int64_t *ca, const int64_t *cb,
+                       const double *c, const double *s, int64_t nm, int64_t nmax, void *stream);
 /* Secular roots of every kept system (secular_all per system); work: ntot + nseg doubles. */
 int hsseig_wave_secular(const double *d, const double *z, const int64_t *koff,
                         const int32_t *seg_of, const double *rho, int64_t nseg, int64_t ntot,
@@ -337,7 +344,7 @@ int hsseig_wave_normalizers(const double *d, const double *dnext, const double *
 /* Grouped dense updates out_s = W_s[:, :k_s] @ C_s (dc.py:132-138); tasks: (s, row tile,
    column tile) int32 triples for tiles of hsseig_wave_tile_shape. */
 int hsseig_wave_dense_update(const double *W, const int64_t *woff, const int64_t *nrow,
-                             const double *d, const double *dnext, const double *gamma,
+                             const int64_t *ldw, const double *d, const double *dnext, const double *gamma,
                              const double *mu, const double *zhat, const double *v,
                              const int64_t *koff, double *out, const int64_t *ooff,
                              const int32_t *tasks, int64_t ntasks, void *stream);
@@ -346,11 +353,14 @@ int hsseig_wave_tile_shape(int32_t *bm, int32_t *bn);
    (dc.py:253-257). */
 int hsseig_wave_order(int64_t nm, const int64_t *roff, const int64_t *kept, const int64_t *koff,
                       const double *lam, const double *d_out, int64_t *order, double *lam_out);
-/* out_m[:, c] = order[c] < k_m ? Qk_m[:, order[c]] : W_m[:, order[c]] for every merge. */
+/* out_m[:, c] from desc[roff[m] + c] = (source << 40) | index: source 0 = column of Qk_m
+   (n x k_m), 1 = compact W_m column, 2 = blockdiag(Q1, Q2) column read from the children. */
 int hsseig_wave_gather(const double *Qk, const int64_t *qoff, const int64_t *kept,
-                       const double *W, const int64_t *woff, const int64_t *roff,
-                       const int32_t *row_merge, const int64_t *order, double *out,
-                       const int64_t *ooff, int64_t nrows, void *stream);
+                       const double *W, const int64_t *woff, const int64_t *wd,
+                       const int64_t *desc, const uint64_t *q1, const uint64_t *q2,
+                       const int64_t *n1, const int64_t *n2, const int64_t *roff,
+                       const int32_t *row_merge, double *out, const int64_t *ooff, int64_t nrows,
+                       void *stream);
 
 /* The dense update through materialised column panels of C (the reference's to_dense
    entries) and the TMA/DMMA GEMM engine (k >= 512, 16-byte aligned Qb rows, even ldq);

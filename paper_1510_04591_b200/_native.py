@@ -112,16 +112,17 @@ _SIGS = {
                                             c_i64, c_vp]),
     "hsseig_wave_zrows": (ctypes.c_int, [c_vp] * 5 + [c_i64, c_vp, c_vp]),
     "hsseig_wave_deflate": (c_i64, [c_i64] + [c_vp] * 16),
-    "hsseig_wave_assemble": (ctypes.c_int, [c_vp] * 9 + [c_i64, c_vp]),
-    "hsseig_wave_rotate": (ctypes.c_int, [c_vp] * 8 + [c_i64, c_i64, c_vp]),
+    "hsseig_wave_compact": (c_i64, [c_i64] + [c_vp] * 10),
+    "hsseig_wave_assemble": (ctypes.c_int, [c_vp] * 11 + [c_i64, c_vp]),
+    "hsseig_wave_rotate": (ctypes.c_int, [c_vp] * 9 + [c_i64, c_i64, c_vp]),
     "hsseig_wave_secular": (ctypes.c_int, [c_vp] * 5 + [c_i64, c_i64] + [c_vp] * 7),
     "hsseig_wave_dnext": (ctypes.c_int, [c_vp] * 5 + [c_i64, c_vp, c_vp]),
     "hsseig_wave_loewner": (ctypes.c_int, [c_vp] * 8 + [c_i64, c_vp, c_vp, c_vp]),
     "hsseig_wave_normalizers": (ctypes.c_int, [c_vp] * 7 + [c_i64, c_vp, c_vp]),
-    "hsseig_wave_dense_update": (ctypes.c_int, [c_vp] * 13 + [c_i64, c_vp]),
+    "hsseig_wave_dense_update": (ctypes.c_int, [c_vp] * 14 + [c_i64, c_vp]),
     "hsseig_wave_tile_shape": (ctypes.c_int, [c_vp, c_vp]),
     "hsseig_wave_order": (ctypes.c_int, [c_i64] + [c_vp] * 7),
-    "hsseig_wave_gather": (ctypes.c_int, [c_vp] * 10 + [c_i64, c_vp]),
+    "hsseig_wave_gather": (ctypes.c_int, [c_vp] * 15 + [c_i64, c_vp]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -249,15 +249,15 @@ __global__ void __launch_bounds__(T::THREADS) dense_update_kernel(const double* 
 template <class T>
 __global__ void __launch_bounds__(T::THREADS) wave_dense_kernel(
     const double* __restrict__ W, const int64_t* __restrict__ woff, const int64_t* __restrict__ nrow,
-    CauchyGen g, const int64_t* __restrict__ koff, double* __restrict__ out,
-    const int64_t* __restrict__ ooff, const int32_t* __restrict__ tasks) {
+    const int64_t* __restrict__ ldw, CauchyGen g, const int64_t* __restrict__ koff,
+    double* __restrict__ out, const int64_t* __restrict__ ooff, const int32_t* __restrict__ tasks) {
   extern __shared__ __align__(16) double smem[];
   const int s = tasks[3 * blockIdx.x], mt = tasks[3 * blockIdx.x + 1], nt = tasks[3 * blockIdx.x + 2];
   const int64_t a = koff[s], k = koff[s + 1] - a, n = nrow[s];
   CauchyGen gs = g;
   gs.d += a; gs.dnext += a; gs.gam += a; gs.mu += a; gs.zhat += a; gs.v += a;
   gs.k = k;
-  dense_update_tile<T>(W + woff[s], n + (n & 1), n, gs, out + ooff[s], k, (int64_t)mt * T::BM,
+  dense_update_tile<T>(W + woff[s], ldw[s], n, gs, out + ooff[s], k, (int64_t)mt * T::BM,
                        (int64_t)nt * T::BN, smem);
 }
 
@@ -595,11 +595,12 @@ extern "C" int hsseig_dense_update(const double* Qb, int64_t ldq, int64_t P, con
 }
 
 extern "C" int hsseig_wave_dense_update(const double* W, const int64_t* woff, const int64_t* nrow,
+                                        const int64_t* ldw,
                                         const double* d, const double* dnext, const double* gamma,
                                         const double* mu, const double* zhat, const double* v,
                                         const int64_t* koff, double* out, const int64_t* ooff,
                                         const int32_t* tasks, int64_t ntasks, void* stream) {
-  if (ntasks < 0 || !W || !woff || !nrow || !koff || !out || !ooff || !tasks) HSS_ARG_FAIL();
+  if (ntasks < 0 || !W || !woff || !nrow || !ldw || !koff || !out || !ooff || !tasks) HSS_ARG_FAIL();
   if (ntasks == 0) return HSSEIG_OK;
   using T = Tile<4, 8, 4, 2, 2>;
   const size_t smem = sizeof(double) * T::STAGE_ELEMS * 2;
@@ -611,7 +612,7 @@ extern "C" int hsseig_wave_dense_update(const double* W, const int64_t* woff, co
   CauchyGen g;
   g.d = d; g.dnext = dnext; g.gam = gamma; g.mu = mu; g.zhat = zhat; g.v = v; g.k = 0;
   wave_dense_kernel<T><<<(unsigned)ntasks, T::THREADS, smem, (cudaStream_t)stream>>>(
-      W, woff, nrow, g, koff, out, ooff, tasks);
+      W, woff, nrow, ldw, g, koff, out, ooff, tasks);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }

@@ -178,21 +178,25 @@ __global__ void wave_zrows_kernel(const unsigned long long* __restrict__ q1,
     z[c] = c < a ? Q1[(a - 1) * a + c] : Q2[c - a];   // last row of Q1, first row of Q2
 }
 
+// W_m holds only the columns the update and the rotations need (the kept ones first, then
+// the deflated columns a rotation touches): n x wd[m], leading dimension wd + (wd & 1);
+// csrc[coff[m] + j] is the blockdiag column of compact column j.
 __global__ void wave_assemble_kernel(const unsigned long long* __restrict__ q1,
                                      const unsigned long long* __restrict__ q2,
                                      const int64_t* __restrict__ n1, const int64_t* __restrict__ n2,
                                      const int64_t* __restrict__ roff,
                                      const int32_t* __restrict__ row_merge,
-                                     const int64_t* __restrict__ src, double* __restrict__ W,
+                                     const int64_t* __restrict__ csrc, const int64_t* __restrict__ coff,
+                                     const int64_t* __restrict__ wd, double* __restrict__ W,
                                      const int64_t* __restrict__ woff, int64_t nrows) {
   for (int64_t gr = blockIdx.x; gr < nrows; gr += gridDim.x) {
     const int m = row_merge[gr];
-    const int64_t a = n1[m], b = n2[m], n = a + b, row = gr - roff[m];
+    const int64_t a = n1[m], b = n2[m], row = gr - roff[m], nc = wd[m];
     const double* Q1 = reinterpret_cast<const double*>(q1[m]);
     const double* Q2 = reinterpret_cast<const double*>(q2[m]);
-    const int64_t* sm = src + roff[m];
-    double* w = W + woff[m] + row * (n + (n & 1));
-    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
+    const int64_t* sm = csrc + coff[m];
+    double* w = W + woff[m] + row * (nc + (nc & 1));
+    for (int64_t c = threadIdx.x; c < nc; c += blockDim.x) {
       const int64_t sc = sm[c];
       double v = 0.0;
       if (row < a) { if (sc < a) v = Q1[row * a + sc]; }
@@ -203,16 +207,16 @@ __global__ void wave_assemble_kernel(const unsigned long long* __restrict__ q1,
 }
 
 __global__ void wave_rotate_kernel(double* __restrict__ W, const int64_t* __restrict__ woff,
-                                   const int64_t* __restrict__ nn,
+                                   const int64_t* __restrict__ nn, const int64_t* __restrict__ wd,
                                    const int64_t* __restrict__ rot_off,
                                    const int64_t* __restrict__ ca, const int64_t* __restrict__ cb,
                                    const double* __restrict__ cs, const double* __restrict__ sn) {
   const int m = blockIdx.y;
-  const int64_t n = nn[m], r0 = rot_off[m], r1 = rot_off[m + 1];
+  const int64_t n = nn[m], r0 = rot_off[m], r1 = rot_off[m + 1], ld = wd[m] + (wd[m] & 1);
   if (r0 == r1) return;
   for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
        row += (int64_t)gridDim.x * blockDim.x) {
-    double* w = W + woff[m] + row * (n + (n & 1));
+    double* w = W + woff[m] + row * ld;
     for (int64_t t = r0; t < r1; ++t) {
       const int64_t ia = ca[t], ib = cb[t];
       const double c = cs[t], s = sn[t];
@@ -223,23 +227,40 @@ __global__ void wave_rotate_kernel(double* __restrict__ W, const int64_t* __rest
   }
 }
 
-// out_m[:, c] = order[c] < k_m ? Qk_m[:, order[c]] : W_m[:, order[c]]
+// out_m[:, c] from the column descriptor desc[c] = (source << 40) | index: source 0 = Qk_m
+// column (an updated eigenvector), 1 = compact W_m column (a rotated deflated column), 2 =
+// blockdiag(Q1, Q2) column read straight from the children (an untouched deflated column).
 __global__ void wave_gather_kernel(const double* __restrict__ Qk, const int64_t* __restrict__ qoff,
                                    const int64_t* __restrict__ kept, const double* __restrict__ W,
-                                   const int64_t* __restrict__ woff, const int64_t* __restrict__ roff,
-                                   const int32_t* __restrict__ row_merge,
-                                   const int64_t* __restrict__ order, double* __restrict__ out,
+                                   const int64_t* __restrict__ woff, const int64_t* __restrict__ wd,
+                                   const int64_t* __restrict__ desc,
+                                   const unsigned long long* __restrict__ q1,
+                                   const unsigned long long* __restrict__ q2,
+                                   const int64_t* __restrict__ n1, const int64_t* __restrict__ n2,
+                                   const int64_t* __restrict__ roff,
+                                   const int32_t* __restrict__ row_merge, double* __restrict__ out,
                                    const int64_t* __restrict__ ooff, int64_t nrows) {
+  constexpr int64_t kMask = (1ll << 40) - 1;
   for (int64_t gr = blockIdx.x; gr < nrows; gr += gridDim.x) {
     const int m = row_merge[gr];
-    const int64_t n = roff[m + 1] - roff[m], row = gr - roff[m], k = kept[m];
-    const int64_t* om = order + roff[m];
+    const int64_t a = n1[m], b = n2[m], n = a + b, row = gr - roff[m], k = kept[m];
+    const int64_t* dm = desc + roff[m];
     const double* q = Qk + qoff[m] + row * k;
-    const double* w = W + woff[m] + row * (n + (n & 1));
+    const double* w = W + woff[m] + row * (wd[m] + (wd[m] & 1));
+    // this row's half of blockdiag(Q1, Q2): child columns [c0, c0 + nc)
+    const bool top = row < a;
+    const double* qc = top ? reinterpret_cast<const double*>(q1[m]) + row * a
+                           : reinterpret_cast<const double*>(q2[m]) + (row - a) * b;
+    const int64_t c0 = top ? 0 : a, nc = top ? a : b;
     double* o = out + ooff[m] + row * n;
     for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
-      const int64_t sc = om[c];
-      o[c] = sc < k ? q[sc] : w[sc];
+      const int64_t dsc = dm[c];
+      const int64_t src = dsc >> 40, idx = dsc & kMask;
+      double v;
+      if (src == 0) v = q[idx];
+      else if (src == 1) v = w[idx];
+      else v = (idx >= c0 && idx < c0 + nc) ? qc[idx - c0] : 0.0;
+      o[c] = v;
     }
   }
 }
@@ -256,6 +277,7 @@ __global__ void assemble_rows_kernel(const double* __restrict__ Qc, int64_t ldq,
       W[row * ldw + c] = (sc >= 0 && sc < nc) ? Qc[row * ldq + sc] : 0.0;
     }
 }
+
 
 }  // namespace hsseig
 
@@ -340,7 +362,8 @@ extern "C" int64_t hsseig_deflate_tol(const double* d, const double* z, int64_t 
   if (n < 1) return -1;
   std::vector<int64_t> order(n);
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return d[x] < d[y]; });
+  if (!std::is_sorted(d, d + n))   // callers usually pass sorted poles: stable order is identity
+    std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return d[x] < d[y]; });
   std::vector<double> ds(n), zs(n);
   for (int64_t t = 0; t < n; ++t) { ds[t] = d[order[t]]; zs[t] = z[order[t]]; }
   std::vector<char> keep(n, 1);
@@ -363,7 +386,8 @@ extern "C" int64_t hsseig_deflate_tol(const double* d, const double* z, int64_t 
   }
   std::vector<int64_t> kept, defl;
   for (int64_t t = 0; t < n; ++t) (keep[t] ? kept : defl).push_back(t);
-  std::stable_sort(defl.begin(), defl.end(), [&](int64_t x, int64_t y) { return ds[x] < ds[y]; });
+  if (!std::is_sorted(defl.begin(), defl.end(), [&](int64_t x, int64_t y) { return ds[x] < ds[y]; }))
+    std::stable_sort(defl.begin(), defl.end(), [&](int64_t x, int64_t y) { return ds[x] < ds[y]; });
   int64_t q = 0;
   for (int64_t t : kept) { d_out[q] = ds[t]; z_out[q] = zs[t]; perm[q] = order[t]; ++q; }
   for (int64_t t : defl) { d_out[q] = ds[t]; z_out[q] = zs[t]; perm[q] = order[t]; ++q; }
@@ -388,39 +412,45 @@ extern "C" int hsseig_wave_zrows(const uint64_t* q1, const uint64_t* q2, const i
 
 extern "C" int hsseig_wave_assemble(const uint64_t* q1, const uint64_t* q2, const int64_t* n1,
                                     const int64_t* n2, const int64_t* roff, const int32_t* row_merge,
-                                    const int64_t* src, double* W, const int64_t* woff,
-                                    int64_t nrows, void* stream) {
-  if (nrows < 0 || !q1 || !q2 || !n1 || !n2 || !roff || !row_merge || !src || !W || !woff)
+                                    const int64_t* csrc, const int64_t* coff, const int64_t* wd,
+                                    double* W, const int64_t* woff, int64_t nrows, void* stream) {
+  if (nrows < 0 || !q1 || !q2 || !n1 || !n2 || !roff || !row_merge || !csrc || !coff || !wd || !W ||
+      !woff)
     HSS_ARG_FAIL();
   if (nrows == 0) return HSSEIG_OK;
   wave_assemble_kernel<<<rows_grid(nrows), 256, 0, (cudaStream_t)stream>>>(
       reinterpret_cast<const unsigned long long*>(q1), reinterpret_cast<const unsigned long long*>(q2),
-      n1, n2, roff, row_merge, src, W, woff, nrows);
+      n1, n2, roff, row_merge, csrc, coff, wd, W, woff, nrows);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
 
 extern "C" int hsseig_wave_rotate(double* W, const int64_t* woff, const int64_t* n,
-                                  const int64_t* rot_off, const int64_t* ca, const int64_t* cb,
-                                  const double* c, const double* s, int64_t nm, int64_t nmax,
-                                  void* stream) {
+                                  const int64_t* wd, const int64_t* rot_off, const int64_t* ca,
+                                  const int64_t* cb, const double* c, const double* s, int64_t nm,
+                                  int64_t nmax, void* stream) {
   if (nm < 0 || nmax < 0 || nm > 65535) HSS_ARG_FAIL();
   if (nm == 0 || nmax == 0) return HSSEIG_OK;
   dim3 grid((unsigned)std::min<int64_t>((nmax + 127) / 128, 1024), (unsigned)nm);
-  wave_rotate_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(W, woff, n, rot_off, ca, cb, c, s);
+  wave_rotate_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(W, woff, n, wd, rot_off, ca, cb, c, s);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
 
 extern "C" int hsseig_wave_gather(const double* Qk, const int64_t* qoff, const int64_t* kept,
-                                  const double* W, const int64_t* woff, const int64_t* roff,
-                                  const int32_t* row_merge, const int64_t* order, double* out,
-                                  const int64_t* ooff, int64_t nrows, void* stream) {
-  if (nrows < 0 || !W || !woff || !roff || !row_merge || !order || !out || !ooff || !kept || !qoff)
+                                  const double* W, const int64_t* woff, const int64_t* wd,
+                                  const int64_t* desc, const uint64_t* q1, const uint64_t* q2,
+                                  const int64_t* n1, const int64_t* n2, const int64_t* roff,
+                                  const int32_t* row_merge, double* out, const int64_t* ooff,
+                                  int64_t nrows, void* stream) {
+  if (nrows < 0 || !W || !woff || !wd || !desc || !q1 || !q2 || !n1 || !n2 || !roff ||
+      !row_merge || !out || !ooff || !kept || !qoff)
     HSS_ARG_FAIL();
   if (nrows == 0) return HSSEIG_OK;
   wave_gather_kernel<<<rows_grid(nrows), 256, 0, (cudaStream_t)stream>>>(
-      Qk ? Qk : W, qoff, kept, W, woff, roff, row_merge, order, out, ooff, nrows);
+      Qk ? Qk : W, qoff, kept, W, woff, wd, desc,
+      reinterpret_cast<const unsigned long long*>(q1), reinterpret_cast<const unsigned long long*>(q2),
+      n1, n2, roff, row_merge, out, ooff, nrows);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
@@ -434,6 +464,22 @@ extern "C" int hsseig_wave_gather(const double* Qk, const int64_t* qoff, const i
  * concatenated over rows (roff): L, zrow, d_out, z_out, src; rotations: ca, cb, rc, rs
  * (capacity roff[nm]).  Returns the total number of kept roots.
  */
+// Stable argsort of key[0..n) made of two ascending runs [0, split) and [split, n) (children's
+// eigenvalues, or roots followed by deflated poles): a stable merge, O(n); a full stable
+// sort when a run is not sorted.  Equal keys keep their original order, as np.argsort(kind=
+// "stable") does.
+static void stable_argsort_runs(const double* key, int64_t split, int64_t n, int64_t* out) {
+  std::vector<int64_t> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  auto lt = [&](int64_t x, int64_t y) { return key[x] < key[y]; };
+  if (std::is_sorted(key, key + split) && std::is_sorted(key + split, key + n)) {
+    std::merge(idx.begin(), idx.begin() + split, idx.begin() + split, idx.end(), out, lt);
+  } else {
+    std::stable_sort(idx.begin(), idx.end(), lt);
+    std::copy(idx.begin(), idx.end(), out);
+  }
+}
+
 extern "C" int64_t hsseig_wave_deflate(int64_t nm, const int64_t* n1, const int64_t* n2,
                                        const int64_t* roff, const double* L, const double* zrow,
                                        const double* bk, int64_t* kept, double* rho_eff,
@@ -448,7 +494,7 @@ extern "C" int64_t hsseig_wave_deflate(int64_t nm, const int64_t* n1, const int6
     const double* Lm = L + o;
     perm.resize(n);
     std::iota(perm.begin(), perm.end(), 0);
-    std::stable_sort(perm.begin(), perm.end(), [&](int64_t x, int64_t y) { return Lm[x] < Lm[y]; });
+    stable_argsort_runs(Lm, a, n, perm.data());
     const double b = bk[m];
     const double rho = std::fabs(b);
     if (rho == 0.0) {   // dc.py:206-213: decoupled halves, merge by sorting only
@@ -507,7 +553,7 @@ extern "C" int hsseig_wave_order(int64_t nm, const int64_t* roff, const int64_t*
     for (int64_t t = 0; t < n; ++t) cat[t] = t < k ? lam[koff[m] + t] : d_out[o + t];
     int64_t* ord = order + o;
     std::iota(ord, ord + n, 0);
-    std::stable_sort(ord, ord + n, [&](int64_t x, int64_t y) { return cat[x] < cat[y]; });
+    stable_argsort_runs(cat.data(), k, n, ord);
     for (int64_t t = 0; t < n; ++t) lam_out[o + t] = cat[ord[t]];
   }
   return HSSEIG_OK;
@@ -522,4 +568,41 @@ extern "C" int hsseig_assemble_rows(const double* Qc, int64_t ldq, int64_t nrow,
   assemble_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(Qc, ldq, nrow, coff, nc, src, n, W, ldw);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
+}
+
+/*
+ * Compact W layout of one depth of merges: merge m materialises only its kept positions
+ * [0, k_m) and the deflated positions some rotation touches (ascending), wd[m] columns.
+ * csrc (at coff[m]) = blockdiag column of each compact column; cmap (rows layout, roff) =
+ * compact column of each W position or -1; the rotation column pairs ca / cb are rewritten
+ * in place to compact indices.  Returns the total compact width.
+ */
+extern "C" int64_t hsseig_wave_compact(int64_t nm, const int64_t* roff, const int64_t* kept,
+                                       const int64_t* src, const int64_t* rot_off, int64_t* ca,
+                                       int64_t* cb, int64_t* wd, int64_t* coff, int64_t* csrc,
+                                       int64_t* cmap) {
+  int64_t tot = 0;
+  coff[0] = 0;
+  for (int64_t m = 0; m < nm; ++m) {
+    const int64_t o = roff[m], n = roff[m + 1] - o, k = kept[m];
+    int64_t* cm = cmap + o;
+    for (int64_t p = 0; p < n; ++p) cm[p] = p < k ? p : -1;
+    for (int64_t t = rot_off[m]; t < rot_off[m + 1]; ++t) {
+      if (ca[t] >= k) cm[ca[t]] = -2;
+      if (cb[t] >= k) cm[cb[t]] = -2;
+    }
+    int64_t nc = k;
+    for (int64_t p = k; p < n; ++p)
+      if (cm[p] == -2) cm[p] = nc++;
+    for (int64_t p = 0; p < n; ++p)
+      if (cm[p] >= 0) csrc[tot + cm[p]] = src[o + p];
+    for (int64_t t = rot_off[m]; t < rot_off[m + 1]; ++t) {
+      ca[t] = cm[ca[t]];
+      cb[t] = cm[cb[t]];
+    }
+    wd[m] = nc;
+    tot += nc;
+    coff[m + 1] = tot;
+  }
+  return tot;
 }

@@ -303,28 +303,33 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                                            _cptr(zrow), _cptr(bk), _cptr(kept), _cptr(rho_eff),
                                            _cptr(d_out), _cptr(z_out), _cptr(src), _cptr(rot_off),
                                            _cptr(ca), _cptr(cb), _cptr(rc), _cptr(rs)))
-        # W blocks in [kept | deflated] column order, then the rotations
-        # W_m rows padded to an even leading dimension (16-byte aligned for the TMA engine);
-        # the gathered output blocks are dense n x n
-        npad = nv + (nv & 1)
-        woff = np.concatenate([[0], np.cumsum(nv * npad)]).astype(np.int64)
+        # W_m holds only the kept columns and the deflated columns a rotation touches (the
+        # other deflated columns are plain child eigenvectors, read by the final gather);
+        # rows padded to an even leading dimension for the TMA engine
+        wd = np.empty(nm, dtype=np.int64)
+        coff = np.empty(nm + 1, dtype=np.int64)
+        csrc = np.empty(nrows, dtype=np.int64)
+        cmap = np.empty(nrows, dtype=np.int64)
+        lib.hsseig_wave_compact(nm, _cptr(roff), _cptr(kept), _cptr(src), _cptr(rot_off), _cptr(ca),
+                                _cptr(cb), _cptr(wd), _cptr(coff), _cptr(csrc), _cptr(cmap))
+        ldw = wd + (wd & 1)
+        woff = np.concatenate([[0], np.cumsum(nv * ldw)]).astype(np.int64)
         ooff = np.concatenate([[0], np.cumsum(nv * nv)]).astype(np.int64)
-        W = torch.empty(int(woff[-1]), **f64)
-        woff_d = _i64(woff)
+        W = torch.empty(max(int(woff[-1]), 2), **f64)
+        woff_d, wd_d = _i64(woff), _i64(wd)
         # (device temporaries stay referenced until their launch: a freed block is reused
         #  by the next upload on the same stream)
         row_merge = _i32(np.repeat(np.arange(nm), nv))
-        src_d = _i64(src)
+        csrc_d, coff_d = _i64(csrc[:max(int(coff[-1]), 1)]), _i64(coff)
         nat.check(lib.hsseig_wave_assemble(nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
-                                           nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(src_d),
-                                           nat.ptr(W), nat.ptr(woff_d), nrows, s), "wave_assemble")
-        del kids, q1, q2
-        A = None      # the previous depth's arena is dead once assembled
+                                           nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(csrc_d),
+                                           nat.ptr(coff_d), nat.ptr(wd_d), nat.ptr(W), nat.ptr(woff_d),
+                                           nrows, s), "wave_assemble")
         nrot = int(rot_off[-1])
         if nrot:
             rot_d = (_i64(rot_off), _i64(ca[:nrot]), _i64(cb[:nrot]), _f64(rc[:nrot]),
                      _f64(rs[:nrot]))
-            nat.check(lib.hsseig_wave_rotate(nat.ptr(W), nat.ptr(woff_d), nat.ptr(nv_d),
+            nat.check(lib.hsseig_wave_rotate(nat.ptr(W), nat.ptr(woff_d), nat.ptr(nv_d), nat.ptr(wd_d),
                                              *(nat.ptr(t) for t in rot_d), nm, int(nv.max()), s),
                       "wave_rotate")
         # the kept rank-one systems, concatenated
@@ -383,13 +388,14 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 n, k = int(nv[m]), int(kept[m])
                 sl = slice(int(koff[q]), int(koff[q + 1]))
                 C = CauchyEvecMatrix(dk[sl], gam[sl], mu[sl], zh[sl], vv[sl], dnext=dn[sl])
-                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(npad[m]))
+                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(ldw[m]))
                 C.right_multiply_into(Wm[:, :k], out=Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k))
             if tasks:
                 tk = np.concatenate(tasks)
-                dd_ = (_i64(woff[segs]), _i64(nv[segs]), _i64(qoff[segs]), _i32(tk.ravel()))
+                dd_ = (_i64(woff[segs]), _i64(nv[segs]), _i64(qoff[segs]), _i32(tk.ravel()),
+                       _i64(ldw[segs]))
                 nat.check(lib.hsseig_wave_dense_update(
-                    nat.ptr(W), nat.ptr(dd_[0]), nat.ptr(dd_[1]), nat.ptr(dk),
+                    nat.ptr(W), nat.ptr(dd_[0]), nat.ptr(dd_[1]), nat.ptr(dd_[4]), nat.ptr(dk),
                     nat.ptr(dn), nat.ptr(gam), nat.ptr(mu), nat.ptr(zh), nat.ptr(vv), nat.ptr(koff_d),
                     nat.ptr(Qk), nat.ptr(dd_[2]), nat.ptr(dd_[3]), len(tk), s),
                     "wave_dense_update")
@@ -411,7 +417,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 nd = nodes[ms[m]]
                 rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
                 fc = FlopCounter()
-                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(npad[m]))
+                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(ldw[m]))
                 out = update_vectors_hss(Wm[:, :k], C, cfg, seed=[cfg.seed, nd["mid"]], flops=fc,
                                          record=rec_)
                 Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k).copy_(out)
@@ -429,12 +435,19 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                               _cptr(d_out), _cptr(order), _cptr(lam_out))
         A = torch.empty(int(ooff[-1]), **f64)
         ooff_d = _i64(ooff)
-        g_ = (_i64(qoff), _i64(kept), _i64(order))
+        # column descriptors: (0, Qk column) | (1, compact W column) | (2, child column)
+        rm = np.repeat(np.arange(nm), nv)
+        pg = order + roff[rm]
+        cmg = cmap[pg]
+        desc = np.where(order < kept[rm], order,
+                        np.where(cmg >= 0, (1 << 40) | cmg, (2 << 40) | src[pg])).astype(np.int64)
+        g_ = (_i64(qoff), _i64(kept), _i64(desc))
         nat.check(lib.hsseig_wave_gather(nat.ptr(Qk), nat.ptr(g_[0]), nat.ptr(g_[1]),
-                                         nat.ptr(W), nat.ptr(woff_d), nat.ptr(roff_d),
-                                         nat.ptr(row_merge), nat.ptr(g_[2]), nat.ptr(A),
+                                         nat.ptr(W), nat.ptr(woff_d), nat.ptr(wd_d), nat.ptr(g_[2]),
+                                         nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
+                                         nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(A),
                                          nat.ptr(ooff_d), nrows, s), "wave_gather")
-        del W, Qk
+        del W, Qk, kids, q1, q2      # the children's blocks are dead once gathered
         # records and flop counts (reference conventions, dc.py:236-247)
         for q, m in enumerate(segs):
             nd = nodes[ms[m]]
