@@ -58,30 +58,72 @@ def _plan(a, b, base):
     return a, leaves
 
 
-def _base_cases(a_mod, b, leaves, stream):
+class _Pack:
+    """Host arrays packed into one pinned staging buffer and sent with ONE host->device
+    copy (a level of the wave schedule uploads ~20 small index arrays; one pageable
+    upload each cost ~70 us of host time at config 5).  The device views keep the
+    buffer alive until the launches reading them are queued."""
+    _T = {np.dtype(np.int64): torch.int64, np.dtype(np.float64): torch.float64,
+          np.dtype(np.int32): torch.int32}
+
+    def __init__(self):
+        self.parts = []
+
+    def add(self, x, dtype=np.int64):
+        self.parts.append(np.ascontiguousarray(x, dtype=dtype).reshape(-1))
+        return self
+
+    def send(self):
+        offs, o = [], 0
+        for p in self.parts:
+            offs.append(o)
+            o += max(16, (p.nbytes + 15) & ~15)
+        host = torch.empty(o, dtype=torch.uint8, pin_memory=True)
+        hv = host.numpy()
+        for p, q in zip(self.parts, offs):
+            hv[q:q + p.nbytes] = p.view(np.uint8)
+        dev = host.to("cuda", non_blocking=True)
+        return [dev[q:q + max(p.nbytes, p.itemsize)].view(self._T[p.dtype])
+                for p, q in zip(self.parts, offs)]
+
+
+def _base_cases_flat(a_mod, b, lo, hi, stream):
+    """Every leaf (rows [lo[t], hi[t]), contiguous and ascending) solved in one launch
+    (batched QL, csrc/glue.cu).  Returns (eigenvalues of all leaves on the host in row
+    order, Q buffer on the device, qoff): leaf t's Q is Q[qoff[t]:qoff[t+1]] (n x n)."""
     lib = nat.load()
-    sizes = np.array([hi - lo for lo, hi in leaves], dtype=np.int64)
-    off = np.concatenate([[0], np.cumsum(sizes)])
-    qoff = np.concatenate([[0], np.cumsum(sizes * sizes)])
-    bb = np.concatenate([b[lo:hi - 1] for lo, hi in leaves] + [np.zeros(1)])
+    lo = np.asarray(lo, dtype=np.int64)
+    hi = np.asarray(hi, dtype=np.int64)
+    sizes = hi - lo
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    qoff = np.concatenate([[0], np.cumsum(sizes * sizes)]).astype(np.int64)
+    L0, L1 = int(lo[0]), int(hi[-1])
+    # off-diagonals of every leaf: drop the couplings b[hi - 1] between neighbours
+    bb = np.concatenate([np.delete(b[L0:L1 - 1], hi[:-1] - 1 - L0), [0.0]])
+    a_d, b_d, off_d, qoff_d = (_Pack().add(a_mod[L0:L1], np.float64).add(bb, np.float64)
+                               .add(off).add(qoff).send())
     lam = torch.empty(int(off[-1]), dtype=torch.float64, device="cuda")
     Q = torch.empty(int(qoff[-1]), dtype=torch.float64, device="cuda")
-    st = torch.zeros(len(leaves), dtype=torch.int32, device="cuda")
-    aa = np.concatenate([a_mod[lo:hi] for lo, hi in leaves])
-    a_d, b_d, off_d, qoff_d = _f64(aa), _f64(bb), _i64(off), _i64(qoff)
-    nat.check(lib.hsseig_tql2_batched(nat.ptr(a_d), nat.ptr(b_d), nat.ptr(off_d), len(leaves), 30,
+    st = torch.zeros(len(lo), dtype=torch.int32, device="cuda")
+    nat.check(lib.hsseig_tql2_batched(nat.ptr(a_d), nat.ptr(b_d), nat.ptr(off_d), len(lo), 30,
                                       nat.ptr(lam), nat.ptr(Q), nat.ptr(qoff_d), nat.ptr(st), stream),
               "tql2_batched")
     bad = st.cpu().numpy()
     if bad.any():
         i = int(np.flatnonzero(bad)[0])
         raise BaseCaseError(f"QL iteration stalled on eigenvalue {int(bad[i]) - 1}")
-    lam_h = lam.cpu().numpy()
+    return lam.cpu().numpy(), Q, qoff
+
+
+def _base_cases(a_mod, b, leaves, stream):
+    lo = np.array([l for l, _ in leaves], dtype=np.int64)
+    hi = np.array([h for _, h in leaves], dtype=np.int64)
+    lam_h, Q, qoff = _base_cases_flat(a_mod, b, lo, hi, stream)
     out = {}
-    for t, (lo, hi) in enumerate(leaves):
-        n = hi - lo
-        out[(lo, hi)] = (lam_h[off[t]:off[t + 1]].copy(),
-                         Q[int(qoff[t]):int(qoff[t]) + n * n].view(n, n))
+    for t, (l, h) in enumerate(leaves):
+        n = h - l
+        out[(l, h)] = (lam_h[l - lo[0]:h - lo[0]].copy(),
+                       Q[int(qoff[t]):int(qoff[t]) + n * n].view(n, n))
     return out
 
 
@@ -241,17 +283,6 @@ def adc_solve(T, cfg=None):
     return EigenResult(lam=lam, Q=Q, merges=merges, flops=flops)
 
 
-def _subtree_nodes(nodes, sub):
-    out = []
-    stack = [sub]
-    while stack:
-        i = stack.pop()
-        out.append(i)
-        if not nodes[i]["leaf"]:
-            stack += [nodes[i]["left"], nodes[i]["right"]]
-    return set(out)
-
-
 def solve_subtree(a_mod, b, nodes, sub, cfg):
     """Eigenpairs of the recursion node `sub` (its base cases and every merge below it,
     level-batched); a_mod carries all split modifications (_plan).  Returns (lam host,
@@ -259,39 +290,55 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
     lib = nat.load()
     s = nat.stream_ptr()
     f64 = dict(dtype=torch.float64, device="cuda")
-    members = _subtree_nodes(nodes, sub)
-    leaf_ids = sorted((i for i in members if nodes[i]["leaf"]), key=lambda i: nodes[i]["lo"])
-    base = _base_cases(a_mod, b, [(nodes[i]["lo"], nodes[i]["hi"]) for i in leaf_ids], s)
-    state = {}       # node -> (lam host, Q device view n x n)
-    for i in leaf_ids:
-        state[i] = base[(nodes[i]["lo"], nodes[i]["hi"])]
+    # nodes are in postorder, so the subtree is the id range [leftmost leaf, sub]
+    first = sub
+    while not nodes[first]["leaf"]:
+        first = nodes[first]["left"]
+    tab = nodes[first:sub + 1]
+    lo_a = np.array([nd["lo"] for nd in tab], dtype=np.int64)
+    hi_a = np.array([nd["hi"] for nd in tab], dtype=np.int64)
+    dep_a = np.array([nd["depth"] for nd in tab], dtype=np.int64)
+    leaf_a = np.array([nd["leaf"] for nd in tab], dtype=bool)
+    split_a = np.array([nd.get("split", 0) for nd in tab], dtype=np.int64)
+    left_a = np.array([nd.get("left", first) for nd in tab], dtype=np.int64) - first
+    right_a = np.array([nd.get("right", first) for nd in tab], dtype=np.int64) - first
+    base_lo = int(lo_a[-1])
+    leaf_idx = np.flatnonzero(leaf_a)        # postorder visits the leaves left to right
+    lam_all, Qbase, lqoff = _base_cases_flat(a_mod, b, lo_a[leaf_idx], hi_a[leaf_idx], s)
+    # per node: device address of its Q block (row-major n x n) and the buffer holding it
+    qptr = np.zeros(len(tab), dtype=np.uint64)
+    qptr[leaf_idx] = np.uint64(Qbase.data_ptr()) + (8 * lqoff[:-1]).astype(np.uint64)
+    live = {}
     records = {}
     bm = ctypes.c_int32(0)
     bn = ctypes.c_int32(0)
     lib.hsseig_wave_tile_shape(ctypes.byref(bm), ctypes.byref(bn))
     bm, bn = bm.value, bn.value
-    maxdepth = max(nodes[i]["depth"] for i in members)
-    for depth in range(maxdepth - 1, -1, -1):
-        ms = [i for i in sorted(members) if nodes[i]["depth"] == depth and not nodes[i]["leaf"]]
-        if not ms:
+    internal = np.flatnonzero(~leaf_a)
+    top = int(dep_a[-1])
+    for depth in range(int(dep_a.max()) - 1, top - 1, -1):
+        ms = internal[dep_a[internal] == depth]
+        if not len(ms):
             continue
         nm = len(ms)
-        n1 = np.array([nodes[i]["split"] - nodes[i]["lo"] for i in ms], dtype=np.int64)
-        n2 = np.array([nodes[i]["hi"] - nodes[i]["split"] for i in ms], dtype=np.int64)
+        lo_m, sp_m = lo_a[ms], split_a[ms]
+        n1 = sp_m - lo_m
+        n2 = hi_a[ms] - sp_m
         nv = n1 + n2
         roff = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
         nrows = int(roff[-1])
-        kids = [(state.pop(nodes[i]["left"]), state.pop(nodes[i]["right"])) for i in ms]
-        L = np.concatenate([np.concatenate([c1[0], c2[0]]) for c1, c2 in kids])
-        q1 = _u64([c1[1].data_ptr() for c1, _ in kids])
-        q2 = _u64([c2[1].data_ptr() for _, c2 in kids])
-        n1_d, n2_d, nv_d, roff_d = _i64(n1), _i64(n2), _i64(nv), _i64(roff)
+        rm = np.repeat(np.arange(nm), nv)
+        rows = lo_m[rm] - base_lo + np.arange(nrows) - roff[rm]
+        L = lam_all[rows]
+        q1, q2, n1_d, n2_d, nv_d, roff_d = (
+            _Pack().add(qptr[left_a[ms]].view(np.int64)).add(qptr[right_a[ms]].view(np.int64))
+            .add(n1).add(n2).add(nv).add(roff).send())
         # boundary rows -> host (sync 1)
         zrow_d = torch.empty(nrows, **f64)
         nat.check(lib.hsseig_wave_zrows(nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
                                         nat.ptr(roff_d), nm, nat.ptr(zrow_d), s), "wave_zrows")
         zrow = zrow_d.cpu().numpy()
-        bk = np.array([b[nodes[i]["split"] - 1] for i in ms], dtype=np.float64)
+        bk = np.ascontiguousarray(b[sp_m - 1], dtype=np.float64)
         kept = np.empty(nm, dtype=np.int64)
         rho_eff = np.empty(nm)
         d_out, z_out = np.empty(nrows), np.empty(nrows)
@@ -315,23 +362,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         ldw = wd + (wd & 1)
         woff = np.concatenate([[0], np.cumsum(nv * ldw)]).astype(np.int64)
         ooff = np.concatenate([[0], np.cumsum(nv * nv)]).astype(np.int64)
-        W = torch.empty(max(int(woff[-1]), 2), **f64)
-        woff_d, wd_d = _i64(woff), _i64(wd)
-        # (device temporaries stay referenced until their launch: a freed block is reused
-        #  by the next upload on the same stream)
-        row_merge = _i32(np.repeat(np.arange(nm), nv))
-        csrc_d, coff_d = _i64(csrc[:max(int(coff[-1]), 1)]), _i64(coff)
-        nat.check(lib.hsseig_wave_assemble(nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
-                                           nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(csrc_d),
-                                           nat.ptr(coff_d), nat.ptr(wd_d), nat.ptr(W), nat.ptr(woff_d),
-                                           nrows, s), "wave_assemble")
         nrot = int(rot_off[-1])
-        if nrot:
-            rot_d = (_i64(rot_off), _i64(ca[:nrot]), _i64(cb[:nrot]), _f64(rc[:nrot]),
-                     _f64(rs[:nrot]))
-            nat.check(lib.hsseig_wave_rotate(nat.ptr(W), nat.ptr(woff_d), nat.ptr(nv_d), nat.ptr(wd_d),
-                                             *(nat.ptr(t) for t in rot_d), nm, int(nv.max()), s),
-                      "wave_rotate")
         # the kept rank-one systems, concatenated
         segs = np.flatnonzero(kept > 0)
         nseg = len(segs)
@@ -339,18 +370,47 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         koff = np.concatenate([[0], np.cumsum(ks)]).astype(np.int64)
         kidx = np.repeat(roff[segs] - koff[:-1], ks) + np.arange(ktot)
         qoff = np.concatenate([[0], np.cumsum(nv * kept)]).astype(np.int64)
+        # update route of every system: HSS (adc-rand above the threshold), a materialised
+        # C panel on the TMA/DMMA engine (k >= DENSE_PANEL_MIN_K) or the grouped dense tiles
+        nvs = nv[segs]
+        hss_q = (ks > cfg.hss_threshold) if cfg.method == "adc-rand" else np.zeros(nseg, bool)
+        big_q = ~hss_q & (ks >= DENSE_PANEL_MIN_K)
+        small = np.flatnonzero(~hss_q & ~big_q)
+        mt, nt = -(-nvs[small] // bm), -(-ks[small] // bn)
+        cnt = mt * nt
+        tk = np.empty((int(cnt.sum()), 3), dtype=np.int32)
+        if len(tk):
+            tq = np.repeat(np.arange(len(small)), cnt)
+            loc = np.arange(len(tk)) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+            tk[:, 0] = small[tq]
+            tk[:, 1] = loc // nt[tq]
+            tk[:, 2] = loc % nt[tq]
+        st0 = np.zeros((nseg, 8), dtype=np.int64)
+        st0[:, 1:4] = ks[:, None]
+        (woff_d, wd_d, row_merge, csrc_d, coff_d, rot_d0, rot_d1, rot_d2, rot_d3, rot_d4, dk, zk,
+         koff_d, seg_of, rho_d, st, t_woff, t_nv, t_qoff, t_tk, t_ldw) = (
+            _Pack().add(woff).add(wd).add(rm, np.int32).add(csrc[:int(coff[-1])]).add(coff)
+            .add(rot_off).add(ca[:nrot]).add(cb[:nrot]).add(rc[:nrot], np.float64)
+            .add(rs[:nrot], np.float64).add(d_out[kidx], np.float64).add(z_out[kidx], np.float64)
+            .add(koff).add(np.repeat(np.arange(nseg), ks), np.int32)
+            .add(rho_eff[segs], np.float64).add(st0).add(woff[segs]).add(nvs).add(qoff[segs])
+            .add(tk, np.int32).add(ldw[segs]).send())
+        W = torch.empty(max(int(woff[-1]), 2), **f64)
+        nat.check(lib.hsseig_wave_assemble(nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
+                                           nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(csrc_d),
+                                           nat.ptr(coff_d), nat.ptr(wd_d), nat.ptr(W), nat.ptr(woff_d),
+                                           nrows, s), "wave_assemble")
+        if nrot:
+            nat.check(lib.hsseig_wave_rotate(nat.ptr(W), nat.ptr(woff_d), nat.ptr(nv_d), nat.ptr(wd_d),
+                                             nat.ptr(rot_d0), nat.ptr(rot_d1), nat.ptr(rot_d2),
+                                             nat.ptr(rot_d3), nat.ptr(rot_d4), nm, int(nv.max()), s),
+                      "wave_rotate")
         Qk = torch.empty(max(int(qoff[-1]), 1), **f64)
-        hss_m = set()
+        hss_m = set(np.flatnonzero(hss_q).tolist())
         seg_iters = np.zeros(nseg, dtype=np.int64)
         if nseg:
-            dk, zk = _f64(d_out[kidx]), _f64(z_out[kidx])
-            koff_d, seg_of = _i64(koff), _i32(np.repeat(np.arange(nseg), ks))
-            rho_d = _f64(rho_eff[segs])
             lam_k, gam, mu, dn, zh, vv = (torch.empty(ktot, **f64) for _ in range(6))
             its = torch.empty(ktot, dtype=torch.int32, device="cuda")
-            st0 = np.zeros((nseg, 8), dtype=np.int64)
-            st0[:, 1:4] = ks[:, None]
-            st = torch.as_tensor(st0, device="cuda")
             work = torch.empty(ktot + nseg, **f64)
             nat.check(lib.hsseig_wave_secular(nat.ptr(dk), nat.ptr(zk), nat.ptr(koff_d), nat.ptr(seg_of),
                                               nat.ptr(rho_d), nseg, ktot, nat.ptr(lam_k), nat.ptr(gam),
@@ -365,56 +425,36 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             nat.check(lib.hsseig_wave_normalizers(nat.ptr(dk), nat.ptr(dn), nat.ptr(gam), nat.ptr(mu),
                                                   nat.ptr(zh), nat.ptr(koff_d), nat.ptr(seg_of), ktot,
                                                   nat.ptr(vv), s), "wave_normalizers")
-            # dense updates of every system not taking the HSS path: the large ones through
-            # materialised C panels on the TMA/DMMA engine, the rest grouped in one launch
-            tasks = []
-            big = []
-            for q, m in enumerate(segs):
-                n, k = int(nv[m]), int(kept[m])
-                if cfg.method == "adc-rand" and k > cfg.hss_threshold:
-                    hss_m.add(q)
-                    continue
-                if k >= DENSE_PANEL_MIN_K:
-                    big.append(q)
-                    continue
-                mt, nt = -(-n // bm), -(-k // bn)
-                t = np.empty((mt * nt, 3), dtype=np.int32)
-                t[:, 0] = q
-                t[:, 1] = np.repeat(np.arange(mt), nt)
-                t[:, 2] = np.tile(np.arange(nt), mt)
-                tasks.append(t)
-            for q in big:
+            for q in np.flatnonzero(big_q).tolist():
                 m = segs[q]
                 n, k = int(nv[m]), int(kept[m])
                 sl = slice(int(koff[q]), int(koff[q + 1]))
                 C = CauchyEvecMatrix(dk[sl], gam[sl], mu[sl], zh[sl], vv[sl], dnext=dn[sl])
                 Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(ldw[m]))
                 C.right_multiply_into(Wm[:, :k], out=Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k))
-            if tasks:
-                tk = np.concatenate(tasks)
-                dd_ = (_i64(woff[segs]), _i64(nv[segs]), _i64(qoff[segs]), _i32(tk.ravel()),
-                       _i64(ldw[segs]))
+            if len(tk):
                 nat.check(lib.hsseig_wave_dense_update(
-                    nat.ptr(W), nat.ptr(dd_[0]), nat.ptr(dd_[1]), nat.ptr(dd_[4]), nat.ptr(dk),
+                    nat.ptr(W), nat.ptr(t_woff), nat.ptr(t_nv), nat.ptr(t_ldw), nat.ptr(dk),
                     nat.ptr(dn), nat.ptr(gam), nat.ptr(mu), nat.ptr(zh), nat.ptr(vv), nat.ptr(koff_d),
-                    nat.ptr(Qk), nat.ptr(dd_[2]), nat.ptr(dd_[3]), len(tk), s),
+                    nat.ptr(Qk), nat.ptr(t_qoff), nat.ptr(t_tk), len(tk), s),
                     "wave_dense_update")
             # statuses + roots (sync 2)
-            stv = st.cpu().numpy()
-            for q, m in enumerate(segs):
-                k = int(ks[q])
-                if stv[q, 1] < k or (k >= 2 and stv[q, 2] < k):
-                    bad = int(stv[q, 1] if stv[q, 1] < k else stv[q, 2])
+            stv = st.view(nseg, 8).cpu().numpy()
+            bad_b = (stv[:, 1] < ks) | ((ks >= 2) & (stv[:, 2] < ks))
+            bad_r = stv[:, 3] < ks
+            if (bad_b | bad_r).any():
+                q = int(np.flatnonzero(bad_b | bad_r)[0])
+                if bad_b[q]:
+                    bad = int(stv[q, 1] if stv[q, 1] < ks[q] else stv[q, 2])
                     raise SecularConvergenceError(f"root {bad} lost its bracket")
-                if stv[q, 3] < k:
-                    raise WeightRecomputationError(f"non-positive radicand at index {int(stv[q, 3])}")
+                raise WeightRecomputationError(f"non-positive radicand at index {int(stv[q, 3])}")
             seg_iters = stv[:, 0]
             for q in sorted(hss_m):
                 m = segs[q]
                 n, k = int(nv[m]), int(kept[m])
                 sl = slice(int(koff[q]), int(koff[q + 1]))
                 C = CauchyEvecMatrix(dk[sl], gam[sl], mu[sl], zh[sl], vv[sl], dnext=dn[sl])
-                nd = nodes[ms[m]]
+                nd = tab[ms[m]]
                 rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
                 fc = FlopCounter()
                 Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(ldw[m]))
@@ -434,23 +474,25 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         lib.hsseig_wave_order(nm, _cptr(roff), _cptr(kept), _cptr(koff_all), _cptr(lam_h),
                               _cptr(d_out), _cptr(order), _cptr(lam_out))
         A = torch.empty(int(ooff[-1]), **f64)
-        ooff_d = _i64(ooff)
         # column descriptors: (0, Qk column) | (1, compact W column) | (2, child column)
-        rm = np.repeat(np.arange(nm), nv)
         pg = order + roff[rm]
         cmg = cmap[pg]
         desc = np.where(order < kept[rm], order,
                         np.where(cmg >= 0, (1 << 40) | cmg, (2 << 40) | src[pg])).astype(np.int64)
-        g_ = (_i64(qoff), _i64(kept), _i64(desc))
-        nat.check(lib.hsseig_wave_gather(nat.ptr(Qk), nat.ptr(g_[0]), nat.ptr(g_[1]),
-                                         nat.ptr(W), nat.ptr(woff_d), nat.ptr(wd_d), nat.ptr(g_[2]),
+        g_qoff, g_kept, g_desc, ooff_d = _Pack().add(qoff).add(kept).add(desc).add(ooff).send()
+        nat.check(lib.hsseig_wave_gather(nat.ptr(Qk), nat.ptr(g_qoff), nat.ptr(g_kept),
+                                         nat.ptr(W), nat.ptr(woff_d), nat.ptr(wd_d), nat.ptr(g_desc),
                                          nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
                                          nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(A),
                                          nat.ptr(ooff_d), nrows, s), "wave_gather")
-        del W, Qk, kids, q1, q2      # the children's blocks are dead once gathered
+        del W, Qk
+        live.pop(depth + 1, None)      # the children's blocks are dead once gathered
+        live[depth] = A
+        lam_all[rows] = lam_out
+        qptr[ms] = np.uint64(A.data_ptr()) + (8 * ooff[:-1]).astype(np.uint64)
         # records and flop counts (reference conventions, dc.py:236-247)
-        for q, m in enumerate(segs):
-            nd = nodes[ms[m]]
+        for q, m in enumerate(segs.tolist()):
+            nd = tab[ms[m]]
             n, k = int(nv[m]), int(kept[m])
             sec = secular_flops(k, int(seg_iters[q])) + 14 * k * k
             if q in hss_m:
@@ -460,13 +502,13 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
                 rec_.flops = {"secular": sec, "update_dense": cauchy_eval_flops(k * k) + gemm_flops(n, k, k),
                               "hss_construct": 0, "hss_mult": 0}
-        for m in range(nm):
-            nd = nodes[ms[m]]
+        for m in np.flatnonzero((kept == 0) & (rho_eff != 0.0)).tolist():
             n = int(nv[m])
-            if kept[m] == 0 and rho_eff[m] != 0.0:
-                records.setdefault(nd["mid"], MergeRecord(size=n, kept=0, n_deflated=n)).flops = \
-                    {p: 0 for p in FlopCounter.PHASES}
-            state[ms[m]] = (lam_out[roff[m]:roff[m + 1]].copy(),
-                            A[int(ooff[m]):int(ooff[m + 1])].view(n, n))
-    lam, Q = state[sub]
-    return lam, Q, records
+            records.setdefault(tab[ms[m]]["mid"], MergeRecord(size=n, kept=0, n_deflated=n)).flops = \
+                {p: 0 for p in FlopCounter.PHASES}
+    n = int(hi_a[-1] - lo_a[-1])
+    if leaf_a[-1]:
+        Q = Qbase[int(lqoff[0]):int(lqoff[0]) + n * n].view(n, n)
+    else:
+        Q = live[top].view(n, n)
+    return lam_all, Q, records
