@@ -424,7 +424,7 @@ def run_ours(args):
                 # public streaming API: Q_old rows land in chunks while the factors are built,
                 # Q_new rows go back while later chunks are multiplied
                 pipe.run(dd, du, rho, Xd, seed=[SEED, 0], out=out, host_io=(hQ, hOut),
-                         chunks=int(os.environ.get("HSSEIG_IO_CHUNKS", "8")))
+                         chunks=int(os.environ.get("HSSEIG_IO_CHUNKS", "16")))
             else:
                 Xd.copy_(hQ, non_blocking=True)
                 step(Xd, out, dd, du)

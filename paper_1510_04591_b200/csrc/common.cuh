@@ -14,6 +14,10 @@ extern std::atomic<long long> g_launches;
 }
 namespace hsseig {
 void set_arg_error(const char* file, int line);
+// Small host->device uploads that return without waiting: the parts are staged in a
+// pinned ring slot (reused only after its copies have completed, tracked by an event).
+bool upload_async(int nparts, void* const* dst, const void* const* src, const size_t* bytes,
+                  cudaStream_t s);
 }
 // argument / configuration failure: remember where (hsseig_last_error) and return code 1
 #define HSS_ARG_FAIL()                               \

@@ -4,13 +4,61 @@
 //   * device assembly of blockdiag(Q1, Q2) permuted to [kept | deflated], the deflation
 //     Givens rotations, and the final eigenvalue-order column gather (dc.py:215-257)
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstring>
+#include <mutex>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
 
 namespace hsseig {
+
+namespace {
+struct UploadSlot {
+  char* host = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+};
+std::mutex g_upload_mu;
+UploadSlot g_upload_ring[32];
+int g_upload_next = 0;
+}  // namespace
+
+bool upload_async(int nparts, void* const* dst, const void* const* src, const size_t* bytes,
+                  cudaStream_t s) {
+  size_t total = 0;
+  for (int i = 0; i < nparts; ++i) total += (bytes[i] + 15) & ~size_t(15);
+  std::lock_guard<std::mutex> g(g_upload_mu);
+  UploadSlot& sl = g_upload_ring[g_upload_next];
+  g_upload_next = (g_upload_next + 1) % 32;
+  if (sl.done) {
+    if (cudaEventSynchronize(sl.done) != cudaSuccess) return false;   // normally long done
+  } else if (cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess) {
+    return false;
+  }
+  if (sl.cap < total) {
+    if (sl.host) cudaFreeHost(sl.host);
+    sl.cap = std::max<size_t>(total, 1 << 16);
+    if (cudaHostAlloc(reinterpret_cast<void**>(&sl.host), sl.cap, cudaHostAllocDefault) != cudaSuccess) {
+      sl.host = nullptr;
+      sl.cap = 0;
+      return false;
+    }
+  }
+  size_t off = 0;
+  for (int i = 0; i < nparts; ++i) {
+    if (bytes[i]) {
+      std::memcpy(sl.host + off, src[i], bytes[i]);
+      if (cudaMemcpyAsync(dst[i], sl.host + off, bytes[i], cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return false;
+    }
+    off += (bytes[i] + 15) & ~size_t(15);
+  }
+  return cudaEventRecord(sl.done, s) == cudaSuccess;
+}
 
 // ---------------------------------------------------------------------------
 // batched implicit QL with Wilkinson shift, one warp per tridiagonal (n <= 32);
@@ -480,20 +528,42 @@ static void stable_argsort_runs(const double* key, int64_t split, int64_t n, int
   }
 }
 
+// The merges of one level are independent: the host-side passes over them (deflation,
+// final order) run on a small thread pool once a level carries enough rows to pay for it.
+template <class F>
+static void for_each_merge(int64_t nm, const int64_t* roff, F&& f) {
+  const int64_t rows = roff[nm] - roff[0];
+  const int64_t hw = std::max<int64_t>(1, std::min<unsigned>(std::thread::hardware_concurrency(), 32u));
+  const int64_t nt = std::min<int64_t>({hw, nm, rows / 4096 + 1});
+  if (nt <= 1) {
+    for (int64_t m = 0; m < nm; ++m) f(m);
+    return;
+  }
+  const int64_t chunk = std::max<int64_t>(1, nm / (nt * 8));
+  std::atomic<int64_t> next{0};
+  auto work = [&] {
+    for (int64_t m0; (m0 = next.fetch_add(chunk)) < nm;)
+      for (int64_t m = m0; m < std::min(nm, m0 + chunk); ++m) f(m);
+  };
+  std::vector<std::thread> pool;
+  for (int64_t t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+}
+
 extern "C" int64_t hsseig_wave_deflate(int64_t nm, const int64_t* n1, const int64_t* n2,
                                        const int64_t* roff, const double* L, const double* zrow,
                                        const double* bk, int64_t* kept, double* rho_eff,
                                        double* d_out, double* z_out, int64_t* src, int64_t* rot_off,
                                        int64_t* ca, int64_t* cb, double* rc, double* rs) {
-  int64_t ktot = 0, nrot_tot = 0;
-  rot_off[0] = 0;
-  std::vector<int64_t> perm, dperm, ri, rj, posW;
-  std::vector<double> ds, zs, z, rcl, rsl;
-  for (int64_t m = 0; m < nm; ++m) {
-    const int64_t a = n1[m], n = a + n2[m], o = roff[m];
+  // pass 1 (parallel): merge m leaves its rotations at its own row offset of ca/cb/rc/rs
+  std::vector<int64_t> nrot(nm, 0);
+  for_each_merge(nm, roff, [&](int64_t m) {
+    thread_local std::vector<int64_t> perm, dperm, ri, rj, posW;
+    thread_local std::vector<double> ds, zs, z;
+    const int64_t a = n1[m], n = a + n2[m], o = roff[m], r0 = o - roff[0];
     const double* Lm = L + o;
     perm.resize(n);
-    std::iota(perm.begin(), perm.end(), 0);
     stable_argsort_runs(Lm, a, n, perm.data());
     const double b = bk[m];
     const double rho = std::fabs(b);
@@ -501,8 +571,7 @@ extern "C" int64_t hsseig_wave_deflate(int64_t nm, const int64_t* n1, const int6
       kept[m] = 0;
       rho_eff[m] = 0.0;
       for (int64_t t = 0; t < n; ++t) { d_out[o + t] = Lm[perm[t]]; z_out[o + t] = 0.0; src[o + t] = perm[t]; }
-      rot_off[m + 1] = nrot_tot;
-      continue;
+      return;
     }
     const double theta = b >= 0.0 ? 1.0 : -1.0;
     z.resize(n);
@@ -513,27 +582,39 @@ extern "C" int64_t hsseig_wave_deflate(int64_t nm, const int64_t* n1, const int6
     }
     ds.resize(n); zs.resize(n);
     for (int64_t t = 0; t < n; ++t) { ds[t] = Lm[perm[t]]; zs[t] = z[perm[t]]; }
-    dperm.resize(n); ri.resize(n); rj.resize(n); rcl.resize(n); rsl.resize(n);
+    dperm.resize(n); ri.resize(n); rj.resize(n);
     int64_t nr = 0;
     const int64_t k = hsseig_deflate(ds.data(), zs.data(), n, 2.0 * rho, d_out + o, z_out + o,
-                                     dperm.data(), ri.data(), rj.data(), rcl.data(), rsl.data(), &nr,
+                                     dperm.data(), ri.data(), rj.data(), rc + r0, rs + r0, &nr,
                                      nullptr);
     kept[m] = k;
     rho_eff[m] = 2.0 * rho;
-    ktot += k;
     posW.resize(n);
     for (int64_t t = 0; t < n; ++t) {
       src[o + t] = perm[dperm[t]];
       posW[perm[dperm[t]]] = t;
     }
     for (int64_t t = 0; t < nr; ++t) {
-      ca[nrot_tot + t] = posW[perm[ri[t]]];
-      cb[nrot_tot + t] = posW[perm[rj[t]]];
-      rc[nrot_tot + t] = rcl[t];
-      rs[nrot_tot + t] = rsl[t];
+      ca[r0 + t] = posW[perm[ri[t]]];
+      cb[r0 + t] = posW[perm[rj[t]]];
+    }
+    nrot[m] = nr;
+  });
+  // pass 2: pack the rotations (a merge's packed offset never passes its row offset, so
+  // forward moves in merge order are safe)
+  int64_t ktot = 0, nrot_tot = 0;
+  rot_off[0] = 0;
+  for (int64_t m = 0; m < nm; ++m) {
+    const int64_t r0 = roff[m] - roff[0], nr = nrot[m];
+    if (nr && r0 != nrot_tot) {
+      std::memmove(ca + nrot_tot, ca + r0, nr * sizeof(int64_t));
+      std::memmove(cb + nrot_tot, cb + r0, nr * sizeof(int64_t));
+      std::memmove(rc + nrot_tot, rc + r0, nr * sizeof(double));
+      std::memmove(rs + nrot_tot, rs + r0, nr * sizeof(double));
     }
     nrot_tot += nr;
     rot_off[m + 1] = nrot_tot;
+    ktot += kept[m];
   }
   return ktot;
 }
@@ -546,16 +627,15 @@ extern "C" int64_t hsseig_wave_deflate(int64_t nm, const int64_t* n1, const int6
 extern "C" int hsseig_wave_order(int64_t nm, const int64_t* roff, const int64_t* kept,
                                  const int64_t* koff, const double* lam, const double* d_out,
                                  int64_t* order, double* lam_out) {
-  std::vector<double> cat;
-  for (int64_t m = 0; m < nm; ++m) {
+  for_each_merge(nm, roff, [&](int64_t m) {
+    thread_local std::vector<double> cat;
     const int64_t o = roff[m], n = roff[m + 1] - o, k = kept[m];
     cat.resize(n);
     for (int64_t t = 0; t < n; ++t) cat[t] = t < k ? lam[koff[m] + t] : d_out[o + t];
     int64_t* ord = order + o;
-    std::iota(ord, ord + n, 0);
     stable_argsort_runs(cat.data(), k, n, ord);
     for (int64_t t = 0; t < n; ++t) lam_out[o + t] = cat[ord[t]];
-  }
+  });
   return HSSEIG_OK;
 }
 

@@ -743,11 +743,10 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
   t->ycomp = reinterpret_cast<double*>(base + c.off_ycomp);
   t->zcomp = reinterpret_cast<double*>(base + c.off_zcomp);
   cudaStream_t s = (cudaStream_t)stream;
-  bool ok = cudaMemcpyAsync((void*)t->lo, lo.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
-            cudaMemcpyAsync((void*)t->hi, hi.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
-            cudaMemcpyAsync((void*)t->left, left.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
-            cudaMemcpyAsync((void*)t->right, right.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
-            cudaMemcpyAsync((void*)t->level_nodes, lnodes.data(), 4 * nn, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+  void* dst[5] = {(void*)t->lo, (void*)t->hi, (void*)t->left, (void*)t->right, (void*)t->level_nodes};
+  const void* src[5] = {lo.data(), hi.data(), left.data(), right.data(), lnodes.data()};
+  const size_t nb[5] = {4u * nn, 4u * nn, 4u * nn, 4u * nn, 4u * nn};
+  bool ok = upload_async(5, dst, src, nb, s) &&
             cudaMemsetAsync(t->rU, 0, 4 * nn, s) == cudaSuccess &&
             cudaMemsetAsync(t->rV, 0, 4 * nn, s) == cudaSuccess &&
             cudaMemsetAsync(t->flags, 0, 8 * nn, s) == cudaSuccess &&
@@ -755,8 +754,6 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
             cudaMemsetAsync(t->V, 0, (size_t)8 * nn * t->pmax * t->ws, s) == cudaSuccess &&
             cudaMemsetAsync(t->B, 0, (size_t)8 * nn * t->ws * t->ws, s) == cudaSuccess;
   if (!ok) return HSSEIG_ERR_CUDA;
-  // host vectors die here: wait for the copies
-  if (cudaStreamSynchronize(s) != cudaSuccess) return HSSEIG_ERR_CUDA;
   return HSSEIG_OK;
 }
 

@@ -10,9 +10,9 @@
 //                writes its 64-bit outputs;
 //   2. walk    : every segment parses the rejection chain from the first E entry
 //                offsets it can be entered at and records exit position and count;
-//   3. resolve : one block fixes the true entry offset of each segment (chains
-//                from nearby offsets merge within a few draws, so the look-back
-//                is short) and prefix-sums the counts;
+//   3. resolve : every segment fixes its true entry offset (chains from nearby
+//                offsets merge within a few draws, so the look-back is short);
+//                a two-level scan turns the per-segment counts into output indices;
 //   4. emit    : every segment re-walks from its true entry and writes its normals
 //                at their global index.
 // The ziggurat tables are NumPy's own (ki/wi/fi), loaded once by the host from the
@@ -23,7 +23,7 @@ namespace hsseig {
 
 typedef unsigned __int128 u128;
 
-constexpr int kSeg = 256;      // raw draws per segment
+constexpr int kSeg = 32;       // raw draws per segment (short: one thread per segment, latency-bound walk)
 constexpr int kEntries = 16;   // entry offsets tried per segment
 constexpr double kZigR = 3.6541528853610088;
 constexpr double kZigInvR = 0.27366123732975828;
@@ -163,18 +163,19 @@ __global__ void walk_kernel(const uint64_t* __restrict__ U, int64_t L, int nseg,
   }
 }
 
-// one block: true entry offset of every segment, then an exclusive scan of the counts
-__global__ void resolve_kernel(const int64_t* __restrict__ exitpos, const int32_t* __restrict__ count,
-                               int nseg, int64_t n, int32_t* __restrict__ entry,
-                               int64_t* __restrict__ base, int32_t* __restrict__ fail) {
-  __shared__ int64_t part[1024];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int per = (nseg + nt - 1) / nt;
-  const int s0 = tid * per, s1 = min(nseg, s0 + per);
-  // entry of segment t: from the previous segment's exit; a segment whose exit does not
-  // depend on its entry ("merged") makes the next entry known without looking further back
-  for (int t = s0; t < s1; ++t) {
-    // nearest earlier segment q0 whose exit does not depend on its entry
+// true entry offset of every segment (look back to the nearest segment whose exit does
+// not depend on its entry, then compose forward), the segment's normal count, and a
+// block-local exclusive scan of the counts; bsum[block] = the block's total
+constexpr int kResolveThreads = 256;
+
+__global__ void __launch_bounds__(kResolveThreads) resolve_kernel(
+    const int64_t* __restrict__ exitpos, const int32_t* __restrict__ count, int nseg,
+    int32_t* __restrict__ entry, int64_t* __restrict__ base, int64_t* __restrict__ bsum,
+    int32_t* __restrict__ fail) {
+  __shared__ int64_t sc[kResolveThreads];
+  const int t = blockIdx.x * kResolveThreads + threadIdx.x;
+  int64_t c = 0;
+  if (t < nseg) {
     int q0 = t - 1;
     while (q0 >= 0) {
       const int64_t* x = exitpos + (int64_t)q0 * kEntries;
@@ -197,10 +198,30 @@ __global__ void resolve_kernel(const int64_t* __restrict__ exitpos, const int32_
     }
     if (eq < 0 || eq >= kEntries) { *fail = 1; eq = 0; }
     entry[t] = eq;
+    c = count[(int64_t)t * kEntries + eq];
   }
+  // block-local exclusive scan (Hillis-Steele over 256 entries)
+  sc[threadIdx.x] = c;
   __syncthreads();
+  for (int off = 1; off < kResolveThreads; off <<= 1) {
+    const int64_t v = threadIdx.x >= off ? sc[threadIdx.x - off] : 0;
+    __syncthreads();
+    sc[threadIdx.x] += v;
+    __syncthreads();
+  }
+  if (t < nseg) base[t] = sc[threadIdx.x] - c;
+  if (threadIdx.x == kResolveThreads - 1) bsum[blockIdx.x] = sc[threadIdx.x];
+}
+
+// one block: exclusive scan of the per-block totals (in place); checks the stream length
+__global__ void scan_blocks_kernel(int64_t* __restrict__ bsum, int nblk, int64_t n,
+                                   int32_t* __restrict__ fail) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (nblk + nt - 1) / nt;
+  const int s0 = min(nblk, tid * per), s1 = min(nblk, s0 + per);
   int64_t s = 0;
-  for (int t = s0; t < s1; ++t) s += count[(int64_t)t * kEntries + entry[t]];
+  for (int b = s0; b < s1; ++b) s += bsum[b];
   part[tid] = s;
   __syncthreads();
   if (tid == 0) {
@@ -210,28 +231,26 @@ __global__ void resolve_kernel(const int64_t* __restrict__ exitpos, const int32_
       part[q] = acc;
       acc += v;
     }
+    if (acc < n) *fail = 2;   // raw stream too short (never at the sizes the margin covers)
   }
   __syncthreads();
   int64_t acc = part[tid];
-  for (int t = s0; t < s1; ++t) {
-    base[t] = acc;
-    acc += count[(int64_t)t * kEntries + entry[t]];
-  }
-  if (tid == nt - 1) {
-    base[nseg] = acc;
-    if (acc < n) *fail = 2;   // raw stream too short (never at the sizes the margin covers)
+  for (int b = s0; b < s1; ++b) {
+    const int64_t v = bsum[b];
+    bsum[b] = acc;
+    acc += v;
   }
 }
 
 __global__ void emit_kernel(const uint64_t* __restrict__ U, int64_t L, int nseg,
                             const int32_t* __restrict__ entry, const int64_t* __restrict__ base,
-                            int64_t n, int64_t w, int64_t ldo, double* __restrict__ out,
+                            const int64_t* __restrict__ bsum, int64_t n, int64_t w, int64_t ldo, double* __restrict__ out,
                             int64_t* __restrict__ tails, int64_t tail_cap,
                             int32_t* __restrict__ fail) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nseg) return;
   const int64_t a = (int64_t)t * kSeg, b = a + kSeg;
-  int64_t p = a + entry[t], i = base[t];
+  int64_t p = a + entry[t], i = base[t] + bsum[t / kResolveThreads];
   while (p < b && i < n) {
     double v;
     uint64_t tu = 0;
@@ -277,7 +296,8 @@ extern "C" int hsseig_set_normal_tables(const uint64_t* ki, const double* wi, co
 extern "C" int64_t hsseig_normals_work_bytes(int64_t n) {
   const int64_t L = raw_len(n);
   const int64_t nseg = L / kSeg;
-  return 8 * L + nseg * kEntries * (8 + 4) + nseg * 4 + (nseg + 1) * 8 + 1024;
+  const int64_t nblk = (nseg + kResolveThreads - 1) / kResolveThreads;
+  return 8 * L + nseg * kEntries * (8 + 4) + nseg * 4 + (nseg + 1) * 8 + nblk * 8 + 1024;
 }
 
 extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
@@ -297,14 +317,18 @@ extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64
   int32_t* entry = count + (int64_t)nseg * kEntries;
   int64_t* base = reinterpret_cast<int64_t*>(
       (reinterpret_cast<uintptr_t>(entry + nseg) + 7) & ~(uintptr_t)7);
-  raw_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(state_hi, state_lo, inc_hi, inc_lo, L, U);
+  raw_kernel<<<(nseg + 63) / 64, 64, 0, s>>>(state_hi, state_lo, inc_hi, inc_lo, L, U);
   HSS_CHECK_LAUNCH();
-  walk_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(U, L, nseg, exitpos, count);
+  walk_kernel<<<(nseg + 63) / 64, 64, 0, s>>>(U, L, nseg, exitpos, count);
   HSS_CHECK_LAUNCH();
-  resolve_kernel<<<1, 1024, 0, s>>>(exitpos, count, nseg, n, entry, base, fail_dev);
+  const int nblk = (nseg + kResolveThreads - 1) / kResolveThreads;
+  int64_t* bsum = base + nseg + 1;
+  resolve_kernel<<<nblk, kResolveThreads, 0, s>>>(exitpos, count, nseg, entry, base, bsum, fail_dev);
+  HSS_CHECK_LAUNCH();
+  scan_blocks_kernel<<<1, 1024, 0, s>>>(bsum, nblk, n, fail_dev);
   HSS_CHECK_LAUNCH();
   if (tails && cudaMemsetAsync(tails, 0, sizeof(int64_t), s) != cudaSuccess) return HSSEIG_ERR_CUDA;
-  emit_kernel<<<(nseg + 127) / 128, 128, 0, s>>>(U, L, nseg, entry, base, n, w, ldo, out, tails,
+  emit_kernel<<<(nseg + 63) / 64, 64, 0, s>>>(U, L, nseg, entry, base, bsum, n, w, ldo, out, tails,
                                                  tail_cap, fail_dev);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;

@@ -457,10 +457,10 @@ extern "C" int hsseig_status_init(hsseig_status* st, int64_t k, void* stream) {
   hsseig_status h;
   for (int t = 0; t < 8; ++t) h.v[t] = 0;
   h.v[1] = h.v[2] = h.v[3] = k;
-  if (cudaMemcpyAsync(st, &h, sizeof(h), cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
-    return HSSEIG_ERR_CUDA;
-  // the host struct goes out of scope: make the copy complete before returning
-  if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return HSSEIG_ERR_CUDA;
+  void* dst[1] = {st};
+  const void* src[1] = {&h};
+  const size_t nb[1] = {sizeof(h)};
+  if (!upload_async(1, dst, src, nb, (cudaStream_t)stream)) return HSSEIG_ERR_CUDA;
   return HSSEIG_OK;
 }
 

@@ -12,8 +12,8 @@ import torch
 
 from .cauchy import CauchyEvecMatrix
 from .flops import FlopCounter, cauchy_eval_flops, gemm_flops
-from .hss import (MAX_WIDTH, build_partition, estimate_rank, finish_construct, hss_matmul_right,
-                  rand_hss_construct)
+from .hss import (MAX_WIDTH, build_partition, draw_omegas, estimate_rank, finish_construct,
+                  hss_matmul_right, rand_hss_construct)
 from .secular import RankOneSystem, dev, dev_rows, recompute_weights, solve_secular
 
 METHODS = ("dense-dc", "adc-rand")
@@ -142,6 +142,60 @@ def update_vectors_hss(Qblock, C, cfg, seed=0, flops=None, record=None, omega=No
         record.hss_rank = H.r_used
     out = hss_matmul_right(Qblock, H, flops=flops)
     return (out, H) if return_tree else out
+
+
+@dataclass
+class HssJob:
+    """One update_vectors_hss call of a batch: Qblock, C, seed, flops, record as there;
+    d / gamma / mu are the host copies of C's generators (partition and rank estimate),
+    out receives Qblock @ Q'."""
+    Q: object
+    C: object
+    seed: object
+    flops: object
+    record: object
+    d: np.ndarray
+    gamma: np.ndarray
+    mu: np.ndarray
+    out: object
+
+
+def update_vectors_hss_many(jobs, cfg):
+    """update_vectors_hss (dc.py:141-171) for every HSS merge of one recursion level, phase
+    by phase so the level pays a handful of host waits instead of ~9 per merge: host
+    partitions / rank estimates, every Gaussian draw (one wait), every sample +
+    construction (one wait), then the multiplies.  Per job the operations and their
+    inputs are exactly those of update_vectors_hss."""
+    def dense_fallback(j):
+        j.record.used_hss = False
+        j.record.fell_back = True
+        j.out.copy_(update_vectors_dense(j.Q, j.C, flops=j.flops))
+
+    live = []
+    for j in jobs:
+        try:
+            part = build_partition(j.C.k, cfg.leaf_size, j.d, j.gamma, j.mu)
+        except ValueError:
+            dense_fallback(j)
+            continue
+        r_est = estimate_rank(part, j.d, j.gamma, j.mu, cfg.rank_eps, cfg.rank_cap)
+        r = min(r_est, part.min_leaf - cfg.oversample)
+        if r < 1 or r + cfg.oversample > MAX_WIDTH:
+            dense_fallback(j)
+            continue
+        live.append((j, part, r))
+    oms = draw_omegas([(j.C.k, r + cfg.oversample, j.seed) for j, _, r in live])
+    trees = [rand_hss_construct(j.C, part, r, p=cfg.oversample, seed=j.seed, omega=om, finish=False)
+             for (j, part, r), om in zip(live, oms)]
+    del oms
+    for (j, _, _), H in zip(live, trees):
+        finish_construct(H, j.flops)
+        if H.flagged:
+            dense_fallback(j)
+            continue
+        j.record.used_hss = True
+        j.record.hss_rank = H.r_used
+        j.out.copy_(hss_matmul_right(j.Q, H, flops=j.flops))
 
 
 def merge_update(d, z, rho, Qblock, cfg, seed=0, flops=None, record=None, omega=None):

@@ -443,6 +443,32 @@ def draw_omega(k, w, seed):
     return om[:, :w]
 
 
+def draw_omegas(specs):
+    """draw_omega for several (k, w, seed) at once: every draw is enqueued first, then one
+    wait covers all their tail read-backs (a recursion level's HSS merges share it)."""
+    from . import sample_rng
+    if not sample_rng.available():
+        return [draw_omega(k, w, seed) for k, w, seed in specs]
+    pool = _STREAM.setdefault("pool", [])
+    out = []
+    for i, (k, w, seed) in enumerate(specs):
+        n = k * w
+        if i == len(pool):
+            pool.append(None)
+        if pool[i] is None or pool[i].nmax < n:
+            pool[i] = None
+            pool[i] = sample_rng.NormalStream(n)
+        ld = w + (w & 1)
+        om = torch.empty(k, ld, dtype=torch.float64, device="cuda")
+        if ld != w:
+            om[:, w:] = 0.0
+        pool[i].draw(seed, n, om, w=w, ld=ld)
+        out.append(om[:, :w])
+    for i in range(len(specs)):
+        pool[i].fixup()
+    return out
+
+
 def rand_hss_construct(A, partition, r, p=10, seed=0, id_tol=DEFAULT_ID_TOL, flops=None,
                        omega=None, finish=True):
     """Randomized bottom-up construction from one Gaussian sample (hss.py:217-306)."""
@@ -472,11 +498,17 @@ def rand_hss_construct(A, partition, r, p=10, seed=0, id_tol=DEFAULT_ID_TOL, flo
 
 def finish_construct(tree, flops=None):
     """Host read-back after construction: flags, ranks, r_used and the flop counter."""
-    v = tree._status.read()
     nn = tree.ct.n_nodes
-    fl = tree._view("flags", torch.int32, 2 * nn, 0).cpu().numpy().reshape(nn, 2)
-    rr = tree._view("rres", torch.float64, nn, 0).cpu().numpy()
-    cr = tree._view("cres", torch.float64, nn, 0).cpu().numpy()
+    # one read-back for flags, residuals and ranks
+    parts = [tree._view("rres", torch.float64, nn, 0), tree._view("cres", torch.float64, nn, 0),
+             tree._view("flags", torch.int32, 2 * nn, 0), tree._view("rU", torch.int32, nn, 0),
+             tree._view("rV", torch.int32, nn, 0)]
+    blob = torch.cat([t.view(torch.uint8) for t in parts]).cpu().numpy()
+    rr = blob[:8 * nn].view(np.float64)
+    cr = blob[8 * nn:16 * nn].view(np.float64)
+    fl = blob[16 * nn:24 * nn].view(np.int32).reshape(nn, 2)
+    tree._ranks = (blob[24 * nn:28 * nn].view(np.int32).copy(), blob[28 * nn:32 * nn].view(np.int32).copy())
+    tree._status.read()
     tree.flags = []
     # the reference appends flags in processing order: deepest level first, postorder within
     for idx in sorted((n.index for n in tree.nodes if n.index != tree.root),
@@ -486,7 +518,6 @@ def finish_construct(tree, flops=None):
         if fl[idx, 1]:
             tree.flags.append((idx, "col", float(cr[idx])))
     tree.flagged = bool(fl.any())        # per-node saturation flags (also right after a gather)
-    tree._ranks = None
     rU, rV = tree.ranks()
     mask = np.ones(nn, dtype=bool)
     mask[tree.root] = False

@@ -21,8 +21,8 @@ import torch
 
 from . import _native as nat
 from .cauchy import DENSE_PANEL_MIN_K, CauchyEvecMatrix
-from .dc import (BaseCaseError, EigenResult, MergeRecord, SolverConfig, merge_update,
-                 update_vectors_hss)
+from .dc import (BaseCaseError, EigenResult, HssJob, MergeRecord, SolverConfig, merge_update,
+                 update_vectors_hss_many)
 from .flops import FlopCounter, cauchy_eval_flops, gemm_flops, secular_flops
 from .secular import SecularConvergenceError, WeightRecomputationError
 
@@ -449,20 +449,25 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                     raise SecularConvergenceError(f"root {bad} lost its bracket")
                 raise WeightRecomputationError(f"non-positive radicand at index {int(stv[q, 3])}")
             seg_iters = stv[:, 0]
-            for q in sorted(hss_m):
-                m = segs[q]
-                n, k = int(nv[m]), int(kept[m])
-                sl = slice(int(koff[q]), int(koff[q + 1]))
-                C = CauchyEvecMatrix(dk[sl], gam[sl], mu[sl], zh[sl], vv[sl], dnext=dn[sl])
-                nd = tab[ms[m]]
-                rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
-                fc = FlopCounter()
-                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(ldw[m]))
-                out = update_vectors_hss(Wm[:, :k], C, cfg, seed=[cfg.seed, nd["mid"]], flops=fc,
-                                         record=rec_)
-                Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k).copy_(out)
-                rec_.flops = fc.as_dict()
-                del out
+            if hss_m:
+                # the level's HSS merges, phase-batched (partition / rank from host roots)
+                gam_h, mu_h, dk_h = gam.cpu().numpy(), mu.cpu().numpy(), d_out[kidx]
+                jobs = []
+                for q in sorted(hss_m):
+                    m = segs[q]
+                    n, k = int(nv[m]), int(kept[m])
+                    sl = slice(int(koff[q]), int(koff[q + 1]))
+                    C = CauchyEvecMatrix(dk[sl], gam[sl], mu[sl], zh[sl], vv[sl], dnext=dn[sl])
+                    nd = tab[ms[m]]
+                    rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
+                    Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(ldw[m]))
+                    jobs.append(HssJob(Q=Wm[:, :k], C=C, seed=[cfg.seed, nd["mid"]], flops=FlopCounter(),
+                                       record=rec_, d=dk_h[sl], gamma=gam_h[sl], mu=mu_h[sl],
+                                       out=Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k)))
+                update_vectors_hss_many(jobs, cfg)
+                for j in jobs:
+                    j.record.flops = j.flops.as_dict()
+                del jobs
             lam_h = lam_k.cpu().numpy()
         else:
             lam_h = np.zeros(0)

@@ -14,7 +14,7 @@ cfg_id, n = sys.argv[1], int(sys.argv[2])
 if cfg_id == "1":
     T, cfg = hb.gen_uniform(n, 0), hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13)
 elif cfg_id == "2":
-    T, cfg = hb.gen_toeplitz(n), hb.SolverConfig(leaf_size=64, rank_eps=1e-13)
+    T, cfg = hb.gen_toeplitz(n), hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13)
 elif cfg_id == "3":
     T, cfg = hb.gen_kac(n) if hasattr(hb, "gen_kac") else hb.gen_clement(n), hb.SolverConfig(rank_eps=1e-13)
 else:
