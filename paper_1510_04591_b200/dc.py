@@ -160,12 +160,27 @@ class HssJob:
     out: object
 
 
-def update_vectors_hss_many(jobs, cfg):
-    """update_vectors_hss (dc.py:141-171) for every HSS merge of one recursion level, phase
-    by phase so the level pays a handful of host waits instead of ~9 per merge: host
-    partitions / rank estimates, every Gaussian draw (one wait), every sample +
-    construction (one wait), then the multiplies.  Per job the operations and their
-    inputs are exactly those of update_vectors_hss."""
+_SIDE = []
+
+
+def _side_streams(n):
+    while len(_SIDE) < n:
+        _SIDE.append(torch.cuda.Stream())
+    return _SIDE[:n]
+
+
+def update_vectors_hss_many(jobs, cfg, max_streams=8):
+    """update_vectors_hss (dc.py:141-171) for every HSS merge of one recursion level.
+
+    Phase by phase, so the level pays a handful of host waits instead of ~9 per merge
+    (host partitions / rank estimates, every Gaussian draw, every sample + construction,
+    then the multiplies), and merge i runs on side stream i mod max_streams so the
+    latency-bound small kernels (interpolative decompositions, tree levels) of different
+    merges overlap on the GPU.  Per job the operations and their inputs are exactly those
+    of update_vectors_hss.  The caller's stream waits for all of it before returning.
+    """
+    main = torch.cuda.current_stream()
+
     def dense_fallback(j):
         j.record.used_hss = False
         j.record.fell_back = True
@@ -184,18 +199,30 @@ def update_vectors_hss_many(jobs, cfg):
             dense_fallback(j)
             continue
         live.append((j, part, r))
-    oms = draw_omegas([(j.C.k, r + cfg.oversample, j.seed) for j, _, r in live])
-    trees = [rand_hss_construct(j.C, part, r, p=cfg.oversample, seed=j.seed, omega=om, finish=False)
-             for (j, part, r), om in zip(live, oms)]
+    if not live:
+        return
+    side = _side_streams(min(len(live), max_streams))
+    for s in side:
+        s.wait_stream(main)
+    st = [side[i % len(side)] for i in range(len(live))]
+    oms = draw_omegas([(j.C.k, r + cfg.oversample, j.seed) for j, _, r in live], streams=st)
+    trees = []
+    for (j, part, r), om, s in zip(live, oms, st):
+        with torch.cuda.stream(s):
+            trees.append(rand_hss_construct(j.C, part, r, p=cfg.oversample, seed=j.seed, omega=om,
+                                            finish=False))
     del oms
-    for (j, _, _), H in zip(live, trees):
-        finish_construct(H, j.flops)
-        if H.flagged:
-            dense_fallback(j)
-            continue
-        j.record.used_hss = True
-        j.record.hss_rank = H.r_used
-        j.out.copy_(hss_matmul_right(j.Q, H, flops=j.flops))
+    for (j, _, _), H, s in zip(live, trees, st):
+        with torch.cuda.stream(s):
+            finish_construct(H, j.flops)
+            if H.flagged:
+                dense_fallback(j)
+                continue
+            j.record.used_hss = True
+            j.record.hss_rank = H.r_used
+            j.out.copy_(hss_matmul_right(j.Q, H, flops=j.flops))
+    for s in side:
+        main.wait_stream(s)
 
 
 def merge_update(d, z, rho, Qblock, cfg, seed=0, flops=None, record=None, omega=None):

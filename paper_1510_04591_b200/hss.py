@@ -443,12 +443,18 @@ def draw_omega(k, w, seed):
     return om[:, :w]
 
 
-def draw_omegas(specs):
-    """draw_omega for several (k, w, seed) at once: every draw is enqueued first, then one
-    wait covers all their tail read-backs (a recursion level's HSS merges share it)."""
+def draw_omegas(specs, streams=None):
+    """draw_omega for several (k, w, seed) at once: every draw is enqueued first (draw i on
+    streams[i] when given), then one wait per draw covers its tail read-back."""
     from . import sample_rng
+    cur = torch.cuda.current_stream()
+    st = [streams[i] if streams else cur for i in range(len(specs))]
     if not sample_rng.available():
-        return [draw_omega(k, w, seed) for k, w, seed in specs]
+        out = []
+        for (k, w, seed), s in zip(specs, st):
+            with torch.cuda.stream(s):
+                out.append(draw_omega(k, w, seed))
+        return out
     pool = _STREAM.setdefault("pool", [])
     out = []
     for i, (k, w, seed) in enumerate(specs):
@@ -459,13 +465,15 @@ def draw_omegas(specs):
             pool[i] = None
             pool[i] = sample_rng.NormalStream(n)
         ld = w + (w & 1)
-        om = torch.empty(k, ld, dtype=torch.float64, device="cuda")
-        if ld != w:
-            om[:, w:] = 0.0
-        pool[i].draw(seed, n, om, w=w, ld=ld)
+        with torch.cuda.stream(st[i]):
+            om = torch.empty(k, ld, dtype=torch.float64, device="cuda")
+            if ld != w:
+                om[:, w:] = 0.0
+            pool[i].draw(seed, n, om, w=w, ld=ld)
         out.append(om[:, :w])
     for i in range(len(specs)):
-        pool[i].fixup()
+        with torch.cuda.stream(st[i]):
+            pool[i].fixup()
     return out
 
 
