@@ -114,3 +114,39 @@ def test_ragged_sizes_match_lapack(n):
     assert np.abs(res.lam - ref).max() <= 1e-13 * T.norm_max() * max(1, np.log2(n))
     Q = res.Q.cpu().numpy()
     assert np.abs(Q.T @ Q - np.eye(n)).max() <= 1e-13 * n
+
+
+def test_level_batched_hss_equals_one_merge_at_a_time():
+    # the level's HSS merges run phase by phase on side streams (dc.update_vectors_hss_many);
+    # every output must be bit-identical to update_vectors_hss called merge by merge
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from helpers import config4_system
+    from paper_1510_04591_b200 import secular
+    from paper_1510_04591_b200.cauchy import CauchyEvecMatrix
+    from paper_1510_04591_b200.dc import HssJob, MergeRecord, update_vectors_hss, update_vectors_hss_many
+    from paper_1510_04591_b200.flops import FlopCounter
+    cfg = hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13)
+    jobs, refs = [], []
+    for i, n in enumerate([700, 1024, 1500, 900, 2048, 640, 1200, 800, 1300]):
+        d, u, rho = config4_system(n, 20 + i)
+        s = secular.RankOneSystem(d, u, rho)
+        sol = secular.solve_secular(s)
+        secular.recompute_weights(s.d, sol, s.z, rho=rho)
+        C = CauchyEvecMatrix.from_secular(s, sol)
+        Q = torch.as_tensor(np.random.default_rng(i).standard_normal((n + 17, n)), device="cuda")
+        rec1, rec2 = MergeRecord(size=n, kept=n, n_deflated=0), MergeRecord(size=n, kept=n, n_deflated=0)
+        f1, f2 = FlopCounter(), FlopCounter()
+        refs.append((update_vectors_hss(Q, C, cfg, seed=[3, i], flops=f1, record=rec1), rec1, f1))
+        jobs.append(HssJob(Q=Q, C=C, seed=[3, i], flops=f2, record=rec2, d=C.d.cpu().numpy(),
+                           gamma=C.gamma.cpu().numpy(), mu=C.mu.cpu().numpy(),
+                           out=torch.empty(n + 17, n, dtype=torch.float64, device="cuda")))
+    update_vectors_hss_many(jobs, cfg, max_streams=4)
+    torch.cuda.synchronize()
+    assert any(r.used_hss for _, r, _ in refs)
+    for (ref, rec1, f1), j in zip(refs, jobs):
+        assert torch.equal(ref, j.out)
+        assert (rec1.used_hss, rec1.fell_back, rec1.hss_rank) == \
+            (j.record.used_hss, j.record.fell_back, j.record.hss_rank)
+        assert f1.as_dict() == j.flops.as_dict()
