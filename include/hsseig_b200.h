@@ -213,6 +213,28 @@ int hsseig_hss_build_rand_levels(const hsseig_gen *gen, const double *omega, int
                                  int lev_to, int part, int nparts, void *stream);
 
 /*
+ * (f4) ADC1: HSS construction by structured rank-revealing Schur complements (SRRSC) on the
+ * generators, no sampling.  Named by BASELINE.json ("ADC1 (SRRSC HSS)") but absent from the
+ * reference, so its definition is oracle/srrsc_oracle.py (parity unpinned).
+ * Per node and side the block row C[R, t^c] (or column C[t^c, R]^T) is eliminated with
+ * complete pivoting on its Cauchy-like generators until max|Schur| <= tol * max|block| or
+ * max_rank steps (<= tree->w; saturation flag above 1e-12 as hss.py:117); the multipliers
+ * give the interpolation bases, so U / V / B / D / skeletons fill the same slots as
+ * hsseig_hss_build_rand and hsseig_hss_matmul_right applies the tree unchanged.
+ * The replaced call site is the construction in update_vectors_hss (pkg/src/hsseig/dc.py:165).
+ * work: hsseig_srrsc_work_doubles(tree) doubles (column generators per node and side).
+ * status[4] = saturated count (tree flagged), status[5] = r_used.
+ */
+int64_t hsseig_srrsc_work_doubles(const hsseig_tree *tree);
+int hsseig_hss_build_srrsc(const hsseig_gen *gen, double tol, int32_t max_rank, hsseig_tree *tree,
+                           double *work, hsseig_status *status, void *stream);
+/* Multi-GPU form (levels lev_from..lev_to, node positions of part `part` of `nparts`), with
+ * the conventions of hsseig_hss_build_rand_levels. */
+int hsseig_hss_build_srrsc_levels(const hsseig_gen *gen, double tol, int32_t max_rank,
+                                  hsseig_tree *tree, double *work, hsseig_status *status,
+                                  int lev_from, int lev_to, int part, int nparts, void *stream);
+
+/*
  * (a12) Structured product out = X @ H (Algorithm 3; pkg/src/hsseig/hss.py:309-361).
  * X: P x k (ld = ldx), out: P x k (ld = ldo), row-major.
  * work: hsseig_matmul_work_doubles(P, tree) doubles.

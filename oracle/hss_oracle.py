@@ -604,6 +604,7 @@ class Config:
     rank_cap: int = 100
     seed: int = 0
     method: str = "adc-rand"
+    srrsc_tol: float = ID_TOL     # ADC1 only (srrsc_oracle.py)
 
 
 def base_case(a, b):
@@ -666,6 +667,9 @@ def adc_solve(a, b, cfg=None):
             if cfg.method == "adc-rand" and k > cfg.hss_threshold:
                 Qk = update_hss(Qk, G, cfg.leaf_size, cfg.oversample, cfg.rank_eps,
                                 cfg.rank_cap, [cfg.seed, mid], flops, info)
+            elif cfg.method == "adc-srrsc" and k > cfg.hss_threshold:
+                from .srrsc_oracle import update_srrsc
+                Qk = update_srrsc(Qk, G, cfg.leaf_size, cfg.srrsc_tol, flops, info)
             else:
                 Qk = update_dense(Qk, G, flops)
         else:

@@ -82,6 +82,13 @@ _SIGS = {
                                                     c_i64, c_dbl, ctypes.POINTER(Tree), c_vp,
                                                     ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                     ctypes.c_int, c_vp]),
+    "hsseig_srrsc_work_doubles": (c_i64, [ctypes.POINTER(Tree)]),
+    "hsseig_hss_build_srrsc": (ctypes.c_int, [ctypes.POINTER(Gen), c_dbl, c_i32,
+                                              ctypes.POINTER(Tree), c_vp, c_vp, c_vp]),
+    "hsseig_hss_build_srrsc_levels": (ctypes.c_int, [ctypes.POINTER(Gen), c_dbl, c_i32,
+                                                     ctypes.POINTER(Tree), c_vp, c_vp,
+                                                     ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                     ctypes.c_int, c_vp]),
     "hsseig_matmul_work_doubles": (c_i64, [c_i64, ctypes.POINTER(Tree)]),
     "hsseig_hss_matmul_right": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(Tree), c_vp,
                                                c_i64, c_vp, c_vp]),

@@ -14,39 +14,9 @@
 #include <cstdlib>
 #include <vector>
 
-#include "common.cuh"
+#include "tree_dev.cuh"
 
 namespace hsseig {
-
-constexpr double kTol3z = 1.0536712127723509e-08;  // sqrt(dlamch('E')) = sqrt(2^-53)
-constexpr double kFlagTol = 1e-12;                  // hss.py:117
-
-struct TreeDev {
-  int32_t k, n_leaves, depth, w, ws, pmax, mmax;
-  const int32_t *lo, *hi, *left, *right, *lnodes;
-  int32_t *rU, *rV, *rsel, *csel, *rloc, *cloc, *flags;
-  double *U, *V, *Vt, *B, *D, *rres, *cres, *M, *psel, *tsel, *ycomp, *zcomp;
-  int32_t dld;
-};
-
-static TreeDev to_dev(const hsseig_tree* t) {
-  TreeDev d;
-  d.k = t->k; d.n_leaves = t->n_leaves; d.depth = t->depth; d.w = t->w; d.ws = t->ws;
-  d.pmax = t->pmax; d.mmax = t->mmax;
-  d.lo = t->lo; d.hi = t->hi; d.left = t->left; d.right = t->right; d.lnodes = t->level_nodes;
-  d.rU = t->rU; d.rV = t->rV; d.rsel = t->rsel; d.csel = t->csel; d.rloc = t->rloc;
-  d.cloc = t->cloc; d.flags = t->flags;
-  d.U = t->U; d.V = t->V; d.Vt = t->Vt; d.dld = t->dld; d.B = t->B; d.D = t->D; d.rres = t->rres; d.cres = t->cres;
-  d.M = t->M; d.psel = t->psel; d.tsel = t->tsel; d.ycomp = t->ycomp; d.zcomp = t->zcomp;
-  return d;
-}
-
-__device__ __forceinline__ size_t slot_pw(const TreeDev& T, int node) {
-  return (size_t)node * T.pmax * T.ws;
-}
-__device__ __forceinline__ size_t slot_ww(const TreeDev& T, int node) {
-  return (size_t)node * T.ws * T.ws;
-}
 
 // ---------------------------------------------------------------------------
 // leaf level: D = C(t,t);  Phi = Y_t - D Omega_t (side 0);  Theta = Z_t - D^T Omega_t (side 1)
@@ -118,6 +88,12 @@ __global__ void genB_kernel(CauchyGen g, TreeDev T, int level, int j0) {
     int r = e / T.ws, c = e % T.ws;
     Bo[e] = (r < nr && c < nc) ? g.entry(rs[r], cs[c]) : 0.0;
   }
+}
+
+int launch_genB(const CauchyGen& g, const TreeDev& T, int level, int j0, int cnt, cudaStream_t s) {
+  genB_kernel<<<dim3(cnt, 2), 256, 0, s>>>(g, T, level, j0);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -12,11 +12,14 @@ import torch
 
 from .cauchy import CauchyEvecMatrix
 from .flops import FlopCounter, cauchy_eval_flops, gemm_flops
-from .hss import (MAX_WIDTH, build_partition, draw_omegas, estimate_rank, finish_construct,
-                  hss_matmul_right, rand_hss_construct)
+from .hss import (DEFAULT_ID_TOL, MAX_WIDTH, build_partition, draw_omegas, estimate_rank,
+                  finish_construct, hss_matmul_right, rand_hss_construct, srrsc_hss_construct)
 from .secular import RankOneSystem, dev, dev_rows, recompute_weights, solve_secular
 
-METHODS = ("dense-dc", "adc-rand")
+# "adc-srrsc" (ADC1) is named by BASELINE.json but absent from the reference (dc.py:23 knows
+# the other two); its HSS construction is the SRRSC of oracle/srrsc_oracle.py
+METHODS = ("dense-dc", "adc-rand", "adc-srrsc")
+HSS_METHODS = ("adc-rand", "adc-srrsc")
 
 
 class BaseCaseError(ArithmeticError):
@@ -35,6 +38,9 @@ class SolverConfig:
     rank_cap: int = 100
     seed: int = 0
     method: str = "adc-rand"
+    # ADC1 only: Schur-complement truncation max|S| <= srrsc_tol * max|block| (the
+    # reference's ID truncation tolerance, hss.py:23); the rank cap is the smallest leaf
+    srrsc_tol: float = DEFAULT_ID_TOL
 
     def __post_init__(self):
         if self.base_size < 3:
@@ -47,6 +53,8 @@ class SolverConfig:
             raise ValueError("oversample must be non-negative")
         if self.method not in METHODS:
             raise ValueError(f"method must be one of {METHODS}")
+        if not self.srrsc_tol >= 0.0:
+            raise ValueError("srrsc_tol must be non-negative")
 
 
 @dataclass
@@ -114,6 +122,11 @@ def update_vectors_dense(Qblock, Qprime, flops=None, out=None):
     return out
 
 
+def srrsc_cap(part):
+    """ADC1 rank cap: the smallest leaf (a node of that rank is not compressed at all)."""
+    return min(part.min_leaf, MAX_WIDTH)
+
+
 def update_vectors_hss(Qblock, C, cfg, seed=0, flops=None, record=None, omega=None,
                        return_tree=False):
     """HSS update with the reference's dense fallbacks (dc.py:141-171)."""
@@ -130,11 +143,14 @@ def update_vectors_hss(Qblock, C, cfg, seed=0, flops=None, record=None, omega=No
         part = build_partition(k, cfg.leaf_size, C.d, C.gamma, C.mu)
     except ValueError:
         return dense_fallback()
-    r_est = estimate_rank(part, C.d, C.gamma, C.mu, cfg.rank_eps, cfg.rank_cap)
-    r = min(r_est, part.min_leaf - cfg.oversample)
-    if r < 1 or r + cfg.oversample > MAX_WIDTH:
-        return dense_fallback()
-    H = rand_hss_construct(C, part, r, p=cfg.oversample, seed=seed, flops=flops, omega=omega)
+    if cfg.method == "adc-srrsc":
+        H = srrsc_hss_construct(C, part, srrsc_cap(part), tol=cfg.srrsc_tol, flops=flops)
+    else:
+        r_est = estimate_rank(part, C.d, C.gamma, C.mu, cfg.rank_eps, cfg.rank_cap)
+        r = min(r_est, part.min_leaf - cfg.oversample)
+        if r < 1 or r + cfg.oversample > MAX_WIDTH:
+            return dense_fallback()
+        H = rand_hss_construct(C, part, r, p=cfg.oversample, seed=seed, flops=flops, omega=omega)
     if H.flagged:
         return dense_fallback()
     if record is not None:
@@ -193,6 +209,9 @@ def update_vectors_hss_many(jobs, cfg, max_streams=8):
         except ValueError:
             dense_fallback(j)
             continue
+        if cfg.method == "adc-srrsc":
+            live.append((j, part, srrsc_cap(part)))
+            continue
         r_est = estimate_rank(part, j.d, j.gamma, j.mu, cfg.rank_eps, cfg.rank_cap)
         r = min(r_est, part.min_leaf - cfg.oversample)
         if r < 1 or r + cfg.oversample > MAX_WIDTH:
@@ -205,13 +224,18 @@ def update_vectors_hss_many(jobs, cfg, max_streams=8):
     for s in side:
         s.wait_stream(main)
     st = [side[i % len(side)] for i in range(len(live))]
-    oms = draw_omegas([(j.C.k, r + cfg.oversample, j.seed) for j, _, r in live], streams=st)
     trees = []
-    for (j, part, r), om, s in zip(live, oms, st):
-        with torch.cuda.stream(s):
-            trees.append(rand_hss_construct(j.C, part, r, p=cfg.oversample, seed=j.seed, omega=om,
-                                            finish=False))
-    del oms
+    if cfg.method == "adc-srrsc":
+        for (j, part, cap), s in zip(live, st):
+            with torch.cuda.stream(s):
+                trees.append(srrsc_hss_construct(j.C, part, cap, tol=cfg.srrsc_tol, finish=False))
+    else:
+        oms = draw_omegas([(j.C.k, r + cfg.oversample, j.seed) for j, _, r in live], streams=st)
+        for (j, part, r), om, s in zip(live, oms, st):
+            with torch.cuda.stream(s):
+                trees.append(rand_hss_construct(j.C, part, r, p=cfg.oversample, seed=j.seed,
+                                                omega=om, finish=False))
+        del oms
     for (j, _, _), H, s in zip(live, trees, st):
         with torch.cuda.stream(s):
             finish_construct(H, j.flops)
@@ -231,7 +255,7 @@ def merge_update(d, z, rho, Qblock, cfg, seed=0, flops=None, record=None, omega=
     sol = solve_secular(sys, flops=flops)
     recompute_weights(sys.d, sol, sys.z, rho=rho, flops=flops)
     C = CauchyEvecMatrix.from_secular(sys, sol, flops=flops)
-    if cfg.method == "adc-rand" and sys.size > cfg.hss_threshold:
+    if cfg.method in HSS_METHODS and sys.size > cfg.hss_threshold:
         Qn = update_vectors_hss(Qblock, C, cfg, seed=seed, flops=flops, record=record, omega=omega)
     else:
         Qn = update_vectors_dense(Qblock, C, flops=flops)

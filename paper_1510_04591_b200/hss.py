@@ -504,6 +504,62 @@ def rand_hss_construct(A, partition, r, p=10, seed=0, id_tol=DEFAULT_ID_TOL, flo
     return tree
 
 
+def srrsc_hss_construct(A, partition, cap, tol=DEFAULT_ID_TOL, flops=None, finish=True, work=None):
+    """ADC1: HSS tree of C from its generators by structured rank-revealing Schur complements.
+
+    No reference implementation exists; the definition is
+    oracle/srrsc_oracle.py (parity unpinned).  cap is the largest node rank (tree width);
+    the tree has the layout of rand_hss_construct, so finish_construct / hss_matmul_right /
+    hss_to_dense apply to it unchanged.  Replaces the construction call of dc.py:165.
+    """
+    if partition.n_leaves < 2:
+        raise ValueError("need at least two leaves; use the dense path instead")
+    if cap < 1 or cap > partition.min_leaf or cap > MAX_WIDTH:
+        raise ValueError(f"rank cap {cap} outside [1, min(smallest leaf, {MAX_WIDTH})]")
+    if not tol >= 0.0:
+        raise ValueError("tolerance must be non-negative")
+    tree = HssTree(partition, cap)
+    tree.method = "srrsc"
+    lib = nat.load()
+    nw = int(lib.hsseig_srrsc_work_doubles(ctypes.byref(tree.ct)))
+    if work is None or work.numel() < nw:
+        work = torch.empty(nw, dtype=torch.float64, device="cuda")
+    st = Status(A.k)
+    nat.check(lib.hsseig_hss_build_srrsc(A.gen, float(tol), int(cap), ctypes.byref(tree.ct),
+                                         nat.ptr(work), nat.ptr(st.t), nat.stream_ptr()),
+              "hss_build_srrsc")
+    tree._status = st
+    tree._work = work      # alive until the queued construction has run
+    if finish:
+        finish_construct(tree, flops)
+    return tree
+
+
+def _srrsc_flops(tree, k):
+    """Construction counter of oracle/srrsc_oracle.py: every elimination sweep evaluates the
+    whole candidate block (6 per entry, cauchy.py:55 convention), p r^2 for the bases, and the
+    D / B entries."""
+    rU, rV = tree.ranks()
+    f = 0
+    for nd in tree.nodes:
+        if nd.index == tree.root:
+            a, b = nd.left, nd.right
+            f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
+            continue
+        ncomp = k - (nd.hi - nd.lo)
+        if nd.is_leaf:
+            m = nd.hi - nd.lo
+            f += cauchy_eval_flops(m * m)
+            ps = (m, m)
+        else:
+            a, b = nd.left, nd.right
+            f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
+            ps = (int(rU[a] + rU[b]), int(rV[a] + rV[b]))
+        for pc, r in zip(ps, (int(rU[nd.index]), int(rV[nd.index]))):
+            f += cauchy_eval_flops((r + 1) * pc * ncomp) + pc * r * r
+    return f
+
+
 def finish_construct(tree, flops=None):
     """Host read-back after construction: flags, ranks, r_used and the flop counter."""
     nn = tree.ct.n_nodes
@@ -532,7 +588,10 @@ def finish_construct(tree, flops=None):
     tree.r_used = int(max(rU[mask].max(), rV[mask].max()))
     tree.ct.rmax = tree.r_used      # the multiply sizes its output tiles to the ranks
     if flops is not None:
-        flops.hss_construct += _construct_flops(tree, tree.k, tree.w)
+        if getattr(tree, "method", "rand") == "srrsc":
+            flops.hss_construct += _srrsc_flops(tree, tree.k)
+        else:
+            flops.hss_construct += _construct_flops(tree, tree.k, tree.w)
     return tree
 
 

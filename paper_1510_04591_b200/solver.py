@@ -21,8 +21,8 @@ import torch
 
 from . import _native as nat
 from .cauchy import DENSE_PANEL_MIN_K, CauchyEvecMatrix
-from .dc import (BaseCaseError, EigenResult, HssJob, MergeRecord, SolverConfig, merge_update,
-                 update_vectors_hss_many)
+from .dc import (HSS_METHODS, BaseCaseError, EigenResult, HssJob, MergeRecord, SolverConfig,
+                 merge_update, update_vectors_hss_many)
 from .flops import FlopCounter, cauchy_eval_flops, gemm_flops, secular_flops
 from .secular import SecularConvergenceError, WeightRecomputationError
 
@@ -370,10 +370,10 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         koff = np.concatenate([[0], np.cumsum(ks)]).astype(np.int64)
         kidx = np.repeat(roff[segs] - koff[:-1], ks) + np.arange(ktot)
         qoff = np.concatenate([[0], np.cumsum(nv * kept)]).astype(np.int64)
-        # update route of every system: HSS (adc-rand above the threshold), a materialised
+        # update route of every system: HSS (adc-rand / adc-srrsc above the threshold), a materialised
         # C panel on the TMA/DMMA engine (k >= DENSE_PANEL_MIN_K) or the grouped dense tiles
         nvs = nv[segs]
-        hss_q = (ks > cfg.hss_threshold) if cfg.method == "adc-rand" else np.zeros(nseg, bool)
+        hss_q = (ks > cfg.hss_threshold) if cfg.method in HSS_METHODS else np.zeros(nseg, bool)
         big_q = ~hss_q & (ks >= DENSE_PANEL_MIN_K)
         small = np.flatnonzero(~hss_q & ~big_q)
         mt, nt = -(-nvs[small] // bm), -(-ks[small] // bn)
