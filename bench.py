@@ -186,7 +186,8 @@ def measure_dgemm_peak(torch):
 
 def eigh_lines():
     """Full tridiagonal eigendecompositions (BASELINE configs 1, 2, 3, 5) on one GPU: wall-s
-    + accuracy (config 2 with ADC2: ADC1 has no reference implementation).
+    + accuracy.  Config 2 is ADC1 as BASELINE names it (SRRSC construction, method
+    "adc-srrsc"; no reference implementation exists) and, beside it, ADC2.
 
     CPU reference wall-s for the same configs (survey container, 8 cores) is in BASELINE.md:
     1.32 s / 22.05 s / 124.5 s; config 5 at N=65536 does not fit the reference's host
@@ -199,6 +200,9 @@ def eigh_lines():
     cases = [
         ("cfg1_uniform_N2000", hb.gen_uniform(2000, 0),
          hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13), None),
+        ("cfg2_toeplitz_N10000_adc1", hb.gen_toeplitz(10000),
+         hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13, method="adc-srrsc"),
+         np.sort(2 + 2 * np.cos(np.arange(1, 10001) * np.pi / 10001))),
         ("cfg2_toeplitz_N10000_adc2", hb.gen_toeplitz(10000),
          hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13),
          np.sort(2 + 2 * np.cos(np.arange(1, 10001) * np.pi / 10001))),
@@ -229,8 +233,9 @@ def eigh_lines():
         G.diagonal().sub_(1.0)
         orth = float(G.abs().max()) / n
         del G
-        rec = {"wall_s": best, "merges": len(res.merges),
+        rec = {"wall_s": best, "method": cfg.method, "merges": len(res.merges),
                "hss_merges": int(sum(m.used_hss for m in res.merges)),
+               "top_merge_hss": bool(res.merges[-1].used_hss),
                "orthogonality": orth, "residual": resid / (n * T.norm_max())}
         if exact is not None:
             rec["eig_err_over_normT"] = float(np.abs(res.lam - exact).max()) / T.norm_max()

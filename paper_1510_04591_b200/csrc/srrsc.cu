@@ -24,14 +24,20 @@
 // sweep costs two DADD (the stable gap), one DMUL and one compare.
 // Cost: sum over nodes of |R| (k - |t|) rank entries, O(k^2 r) per merge, the complexity the
 // paper quotes for ADC1.
+#include <algorithm>
 #include <climits>
+
+#include <cooperative_groups.h>
 
 #include "tree_dev.cuh"
 
 namespace hsseig {
 
+namespace cg = cooperative_groups;
+
 constexpr int kSrThreads = 256;
-constexpr int kSrCols = 4;  // columns a thread holds in registers during a sweep
+constexpr int kSrCols = 4;      // columns a thread holds in registers during a sweep
+constexpr int kSrMaxCluster = 16;
 
 // lam_a - lam_b for eigen indices a != b through the pole between them (both terms carry the
 // sign of the result):  a < b: ((d_{a+1} - d_b) - gam_b) - mu_a;  a > b: mu_b - ((d_{b+1} - d_a) - gam_a)
@@ -44,18 +50,144 @@ __device__ __forceinline__ bool better(double v, long long key, double bv, long 
   return v > bv || (v == bv && key < bk);
 }
 
+// Row data the sweep reads per candidate (fixed during the elimination except s):
+//   e  = the folded row point of the gap (side 0: d_i; side 1: d_j + gam_j for columns left
+//        of the node, d_{j+1} - mu_j for columns right of it),
+//   sl = the rounding slack of that fold (side 1) — see the filter below.
+struct SweepPivot {          // previous pivot, for the deferred column rescaling
+  int gb, past;              // its global column index (-1: none yet) and candidate row
+  double d, g, n, m;         // column point data (side 0: d, gam, dnext, mu; side 1: d)
+  double rx, ry, rz, rw;     // its row's points (sX, sY, sZ, sW)
+};
+
+// One sweep over columns [c_lo, c_hi) (all left (RIGHT = false) or all right of the node):
+// apply the previous pivot's rescaling to the column generators, then search the largest
+// |s t / g| with the division-free filter
+//     |s| |t| / best + slack >= |e - c|     (e - c the gap up to the folded rounding)
+// and the exact IEEE value and row-major argmax only for entries that pass it.
+template <int SIDE, bool RIGHT>
+__device__ __forceinline__ void sr_sweep(const CauchyGen& g, int c_lo, int c_hi, int lo, int width,
+                                         int ncomp, int p, int step, const SweepPivot& pv,
+                                         double* __restrict__ tstate, const double* sS,
+                                         const double* sX, const double* sY, const double* sZ,
+                                         const double* sW, const double2* sE, double& bv,
+                                         long long& bk, double& bt) {
+  const int tid = threadIdx.x;
+  const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  for (int c0 = c_lo; c0 < c_hi; c0 += kSrThreads * kSrCols) {
+    double tv[kSrCols], ce[kSrCols], cs[kSrCols], tb[kSrCols];
+#pragma unroll
+    for (int u = 0; u < kSrCols; ++u) {
+      const int c = c0 + u * kSrThreads + tid;
+      double t = 0.0;
+      double cy = kNaN, cz = kNaN;   // invalid column: NaN gaps never pass a compare
+      if (c < c_hi) {
+        const int b = c < lo ? c : c + width;
+        if (SIDE == 0) {     // columns are eigen indices
+          const double db = __ldg(g.d + b), gb = __ldg(g.gam + b);
+          const double nb = __ldg(g.dnext + b), mb = __ldg(g.mu + b);
+          cy = RIGHT ? db : nb;
+          cz = RIGHT ? gb : -mb;       // g = (x - cy) - cz  ==  (x - dnext) + mu on the left
+          if (step == 0) {
+            t = __ldg(g.v + b);
+          } else if (b == pv.gb) {
+            t = 0.0;
+          } else {
+            const double gp = (pv.rx - cy) - cz;
+            const double cf = lamdiff(pv.gb, b, pv.d, pv.g, pv.n, pv.m, db, gb, nb, mb) / gp;
+            t = tstate[c] * cf;
+          }
+        } else {             // columns are poles
+          const double db = __ldg(g.d + b);
+          cy = db;
+          if (step == 0) {
+            t = __ldg(g.zhat + b);
+          } else if (b == pv.gb) {
+            t = 0.0;
+          } else {
+            const double gp = RIGHT ? ((db - pv.rz) - pv.rw) : ((db - pv.rx) - pv.ry);
+            const double cf = (db - pv.d) / gp;
+            t = tstate[c] * cf;
+          }
+        }
+        tstate[c] = t;
+      }
+      tv[u] = t;
+      if (SIDE == 0) {
+        ce[u] = cy + cz;
+        cs[u] = 0x1p-50 * (fabs(cy) + fabs(cz));
+      } else {
+        ce[u] = cy;
+        cs[u] = 0.0;
+      }
+    }
+    double rthr = bv > 0.0 ? 1.0 / (bv * (1.0 - 1e-9)) : kInf;
+#pragma unroll
+    for (int u = 0; u < kSrCols; ++u) tb[u] = fabs(tv[u]) * rthr;
+    // two rows per iteration (independent filter chains); p is padded by a zero row
+    // (s = 0 never passes) when odd, see the row setup
+    for (int a0 = 0; a0 < p; a0 += 2) {
+      const double as0 = fabs(sS[a0]), as1 = fabs(sS[a0 + 1]);
+      const double2 e0 = sE[a0], e1 = sE[a0 + 1];  // (folded point, slack) for this branch
+      unsigned hm = 0;   // bit u: (row a0, column u) passes; bit kSrCols + u: row a0 + 1
+#pragma unroll
+      for (int u = 0; u < kSrCols; ++u) {
+        hm |= (fma(as0, tb[u], SIDE == 0 ? cs[u] : e0.y) >= fabs(ce[u] - e0.x)) ? 1u << u : 0u;
+        hm |= (fma(as1, tb[u], SIDE == 0 ? cs[u] : e1.y) >= fabs(ce[u] - e1.x))
+                  ? 1u << (kSrCols + u) : 0u;
+      }
+      if (!hm) continue;
+      for (int a = a0; a < a0 + 2; ++a, hm >>= kSrCols) {   // rare: exact values, argmax
+        const double sa = sS[a];
+        if (sa == 0.0) continue;
+#pragma unroll
+        for (int u = 0; u < kSrCols; ++u) {
+          const int c = c0 + u * kSrThreads + tid;
+          if (!((hm >> u) & 1u) || c >= c_hi) continue;
+          const int b = c < lo ? c : c + width;   // exact gap from the column's points again
+          double gv;
+          if (SIDE == 0) {
+            gv = RIGHT ? ((sX[a] - __ldg(g.d + b)) - __ldg(g.gam + b))
+                       : ((sX[a] - __ldg(g.dnext + b)) - (-__ldg(g.mu + b)));
+          } else {
+            const double db = __ldg(g.d + b);
+            gv = RIGHT ? ((db - sZ[a]) - sW[a]) : ((db - sX[a]) - sY[a]);
+          }
+          const double val = fabs((sa * tv[u]) / gv);
+          const long long key = (long long)a * ncomp + c;
+          if (better(val, key, bv, bk)) { bv = val; bk = key; bt = tv[u]; }
+        }
+      }
+      rthr = bv > 0.0 ? 1.0 / (bv * (1.0 - 1e-9)) : rthr;
+#pragma unroll
+      for (int u = 0; u < kSrCols; ++u) tb[u] = fabs(tv[u]) * rthr;
+    }
+  }
+}
+
+// One thread-block cluster of CL CTAs per (node, side): every CTA keeps the candidate rows
+// (replicated, updated identically), CTA `rank` owns the column slice [cbeg, cend).  Per
+// elimination step each CTA publishes its slice's (max, key, t at the max) in shared memory
+// (double-buffered by step parity), one cluster barrier, and every CTA reads the CL records
+// through DSMEM and takes the same decision.
 __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev T, int level,
                                                            int j0, double tol, int cap,
                                                            double* __restrict__ work, int64_t ldw,
                                                            hsseig_status* st) {
   extern __shared__ __align__(16) double sm[];
-  const int j = j0 + blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+  const int j = j0 + blockIdx.x / CL, side = blockIdx.y, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int node = T.lnodes[(1 << level) - 1 + j];
   const bool leaf = T.left[node] < 0;
   const int lo = T.lo[node], hi = T.hi[node], width = hi - lo;
   const int ncomp = T.k - width;
+  const int slice = (ncomp + CL - 1) / CL;
+  const int cbeg = min(ncomp, rank * slice), cend = min(ncomp, cbeg + slice);
   const int P = T.pmax, ws = T.ws;
+  const bool lead = rank == 0;
   int p, na = 0;
   if (leaf) {
     p = width;
@@ -72,13 +204,17 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
   double* sY = sX + P;
   double* sZ = sY + P;
   double* sW = sZ + P;
-  int* sG = reinterpret_cast<int*>(sW + P);  // global index of the candidate
+  double2* sEL = reinterpret_cast<double2*>(sW + P);  // (folded point, slack), left columns
+  double2* sER = sEL + P;                               // the same for right columns
+  int* sG = reinterpret_cast<int*>(sER + P);  // global index of the candidate
   int* sPos = sG + P;                         // elimination step that pivoted it, or -1
   int* sPiv = sPos + P;                       // candidate pivoted at each step
-  __shared__ double sRedV[kSrThreads / 32];
+  __shared__ double sRedV[kSrThreads / 32], sRedT[kSrThreads / 32];
   __shared__ long long sRedK[kSrThreads / 32];
+  __shared__ double sPartV[2], sPartT[2];     // this CTA's slice record, by step parity
+  __shared__ long long sPartK[2];
   __shared__ double sMax0, sMx, sPv, sTq, sPd, sPg, sPn, sPm;
-  __shared__ int sStop, sAst, sGb, sStep;
+  __shared__ int sStop, sAst, sGb;
 
   double* tstate = work + (size_t)(2 * j + side) * ldw;
   double* Lm = T.M + (size_t)(2 * j + side) * P * ws;   // multipliers L[a][s] at a * ws + s
@@ -97,16 +233,28 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
     if (side == 0) {
       sS[a] = __ldg(g.zhat + ga);
       sX[a] = __ldg(g.d + ga);
+      sY[a] = 0.0; sZ[a] = 0.0; sW[a] = 0.0;
+      sEL[a] = make_double2(sX[a], 0.0);
+      sER[a] = make_double2(sX[a], 0.0);
     } else {
+      const double x = __ldg(g.d + ga), y = __ldg(g.gam + ga);
+      const double z = __ldg(g.dnext + ga), w = -__ldg(g.mu + ga);
       sS[a] = __ldg(g.v + ga);
-      sX[a] = __ldg(g.d + ga);
-      sY[a] = __ldg(g.gam + ga);
-      sZ[a] = __ldg(g.dnext + ga);
-      sW[a] = -__ldg(g.mu + ga);
+      sX[a] = x; sY[a] = y; sZ[a] = z; sW[a] = w;
+      // gap (c - x) - y  ~  c - (x + y), rounding of the fold and of the subtraction covered
+      const double el = x + y, er = z + w;
+      sEL[a] = make_double2(el, 0x1p-50 * (fabs(x) + fabs(y) + fabs(el)));
+      sER[a] = make_double2(er, 0x1p-50 * (fabs(z) + fabs(w) + fabs(er)));
     }
   }
+  if (tid == 0 && (p & 1)) {   // pad row for the two-row sweep: s = 0 never passes the filter
+    sS[p] = 0.0;
+    sX[p] = sY[p] = sZ[p] = sW[p] = 0.0;
+    sEL[p] = make_double2(0.0, 0.0);
+    sER[p] = make_double2(0.0, 0.0);
+  }
   // leaf D = C(t, t) (hss.py:263), written once by the row side
-  if (leaf && side == 0) {
+  if (leaf && side == 0 && lead) {
     const int drows = hsseig_drows(T.mmax);
     double* Dslot = T.D + (size_t)j * drows * T.dld;
     for (int e = tid; e < drows * T.dld; e += kSrThreads) {
@@ -116,111 +264,67 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
   }
   if (tid == 0) {
     sGb = -1;
-    sStep = 0;
+    sPd = sPg = sPn = sPm = 0.0;
   }
   __syncthreads();
 
   int step = 0;
   for (;; ++step) {
-    // ---- sweep: apply the previous pivot's column rescaling, search max |M^(step)| ----
-    const int pgb = sGb, past = sStep > 0 ? sPiv[step - 1] : 0;
-    double bv = 0.0;
+    // ---- sweep of this CTA's slice: apply the previous pivot's column rescaling, search max ----
+    SweepPivot pv;
+    pv.gb = sGb;
+    pv.past = step > 0 ? sPiv[step - 1] : 0;
+    pv.d = sPd; pv.g = sPg; pv.n = sPn; pv.m = sPm;
+    pv.rx = sX[pv.past]; pv.ry = sY[pv.past]; pv.rz = sZ[pv.past]; pv.rw = sW[pv.past];
+    double bv = 0.0, bt = 0.0;
     long long bk = LLONG_MAX;
-    for (int c0 = 0; c0 < ncomp; c0 += kSrThreads * kSrCols) {
-      double tv[kSrCols], cy[kSrCols], cz[kSrCols], tb[kSrCols];
-      bool right[kSrCols];
-      int cc[kSrCols];
-#pragma unroll
-      for (int u = 0; u < kSrCols; ++u) {
-        const int c = c0 + u * kSrThreads + tid;
-        cc[u] = c;
-        double t = 0.0;
-        cy[u] = 0.0;
-        cz[u] = 0.0;
-        right[u] = false;
-        if (c < ncomp) {
-          const int b = c < lo ? c : c + width;
-          right[u] = b >= hi;
-          if (side == 0) {   // columns are eigen indices
-            const double db = __ldg(g.d + b), gb = __ldg(g.gam + b);
-            const double nb = __ldg(g.dnext + b), mb = __ldg(g.mu + b);
-            cy[u] = right[u] ? db : nb;
-            cz[u] = right[u] ? gb : -mb;   // g = (x - cy) - cz  ==  (x - dnext) + mu on the left
-            if (step == 0) {
-              t = __ldg(g.v + b);
-            } else if (b == pgb) {
-              t = 0.0;
-            } else {
-              const double gp = (sX[past] - cy[u]) - cz[u];
-              const double cf = lamdiff(pgb, b, sPd, sPg, sPn, sPm, db, gb, nb, mb) / gp;
-              t = tstate[c] * cf;
-            }
-          } else {           // columns are poles
-            const double db = __ldg(g.d + b);
-            cy[u] = db;
-            if (step == 0) {
-              t = __ldg(g.zhat + b);
-            } else if (b == pgb) {
-              t = 0.0;
-            } else {
-              const double gp = right[u] ? ((db - sZ[past]) - sW[past]) : ((db - sX[past]) - sY[past]);
-              const double cf = (db - sPd) / gp;
-              t = tstate[c] * cf;
-            }
-          }
-          tstate[c] = t;
-        }
-        tv[u] = t;
-      }
-      double rthr = bv > 0.0 ? 1.0 / (bv * (1.0 - 1e-9)) : __longlong_as_double(0x7ff0000000000000LL);
-#pragma unroll
-      for (int u = 0; u < kSrCols; ++u) tb[u] = fabs(tv[u]) * rthr;
-      for (int a = 0; a < p; ++a) {
-        const double sa = sS[a];
-        if (sa == 0.0) continue;
-        const double asa = fabs(sa);
-        double gv[kSrCols];
-        if (side == 0) {
-          const double x = sX[a];
-#pragma unroll
-          for (int u = 0; u < kSrCols; ++u) gv[u] = (x - cy[u]) - cz[u];
-        } else {
-          const double xl = sX[a], yl = sY[a], xr = sZ[a], yr = sW[a];
-#pragma unroll
-          for (int u = 0; u < kSrCols; ++u)
-            gv[u] = right[u] ? ((cy[u] - xr) - yr) : ((cy[u] - xl) - yl);
-        }
-        bool hit = false;
-#pragma unroll
-        for (int u = 0; u < kSrCols; ++u) hit |= (asa * tb[u] >= fabs(gv[u])) && cc[u] < ncomp;
-        if (hit) {   // rare: exact values and the argmax compare
-#pragma unroll
-          for (int u = 0; u < kSrCols; ++u) {
-            if (cc[u] >= ncomp) continue;
-            const double val = fabs((sa * tv[u]) / gv[u]);
-            const long long key = (long long)a * ncomp + cc[u];
-            if (better(val, key, bv, bk)) { bv = val; bk = key; }
-          }
-          rthr = bv > 0.0 ? 1.0 / (bv * (1.0 - 1e-9)) : rthr;
-#pragma unroll
-          for (int u = 0; u < kSrCols; ++u) tb[u] = fabs(tv[u]) * rthr;
-        }
+    {
+      const int l0 = cbeg, l1 = min(cend, lo), r0 = max(cbeg, lo), r1 = cend;
+      if (side == 0) {
+        sr_sweep<0, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bv, bk, bt);
+        sr_sweep<0, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bv, bk, bt);
+      } else {
+        sr_sweep<1, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bv, bk, bt);
+        sr_sweep<1, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bv, bk, bt);
       }
     }
-    // ---- CTA argmax (first maximum in row-major order) ----
+    // ---- slice argmax (first maximum in row-major order), then across the cluster ----
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const long long ok = __shfl_xor_sync(0xffffffffu, bk, o);
-      if (better(ov, ok, bv, bk)) { bv = ov; bk = ok; }
+      const double ot = __shfl_xor_sync(0xffffffffu, bt, o);
+      if (better(ov, ok, bv, bk)) { bv = ov; bk = ok; bt = ot; }
     }
-    if (lane == 0) { sRedV[warp] = bv; sRedK[warp] = bk; }
+    if (lane == 0) { sRedV[warp] = bv; sRedK[warp] = bk; sRedT[warp] = bt; }
     __syncthreads();
+    const int par = step & 1;
     if (tid == 0) {
-      double mv = sRedV[0];
+      double mv = sRedV[0], mt = sRedT[0];
       long long mk = sRedK[0];
       for (int w2 = 1; w2 < kSrThreads / 32; ++w2)
-        if (better(sRedV[w2], sRedK[w2], mv, mk)) { mv = sRedV[w2]; mk = sRedK[w2]; }
+        if (better(sRedV[w2], sRedK[w2], mv, mk)) { mv = sRedV[w2]; mk = sRedK[w2]; mt = sRedT[w2]; }
+      sPartV[par] = mv;
+      sPartK[par] = mk;
+      sPartT[par] = mt;
+    }
+    cluster.sync();
+    if (warp == 0) {   // lane r reads CTA r's record (one DSMEM round trip), then a shuffle argmax
+      double mv = 0.0, tq = 0.0;
+      long long mk = LLONG_MAX;
+      if (lane < CL) {
+        mv = *cluster.map_shared_rank(&sPartV[par], lane);
+        mk = *cluster.map_shared_rank(&sPartK[par], lane);
+        tq = *cluster.map_shared_rank(&sPartT[par], lane);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, mv, o);
+        const long long ok = __shfl_xor_sync(0xffffffffu, mk, o);
+        const double ot = __shfl_xor_sync(0xffffffffu, tq, o);
+        if (better(ov, ok, mv, mk)) { mv = ov; mk = ok; tq = ot; }
+      }
+      if (lane == 0) {
       if (step == 0) sMax0 = mv;
       sMx = mv;
       const bool stop = mv == 0.0 || mv <= tol * sMax0 || step == cap;
@@ -228,7 +332,6 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
       if (!stop) {
         const int ast = (int)(mk / ncomp), cst = (int)(mk % ncomp);
         const int gb = cst < lo ? cst : cst + width;
-        const double tq = tstate[cst];
         double gpv;
         if (side == 0) {
           const double db = __ldg(g.d + gb), gg = __ldg(g.gam + gb);
@@ -245,7 +348,7 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
         sTq = tq;
         sPv = (sS[ast] * tq) / gpv;
         sPiv[step] = ast;
-        sStep = step + 1;
+      }
       }
     }
     __syncthreads();
@@ -277,11 +380,14 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
           const double rf = rf_num / ga;
           sS[a] = sS[a] * rf;
         }
-        Lm[(size_t)a * ws + step] = L;
+        if (lead) Lm[(size_t)a * ws + step] = L;
       }
     }
     __syncthreads();
   }
+  // no CTA may leave while another can still read its slice records
+  cluster.sync();
+  if (!lead) return;
   const int r = step;
   const double max0 = sMax0;
   const double resid = max0 > 0.0 ? sMx / max0 : 0.0;
@@ -331,6 +437,17 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
 
 using namespace hsseig;
 
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 static int64_t srrsc_ldw(const hsseig_tree* t) { return ((int64_t)t->k + 31) / 32 * 32; }
 
 extern "C" int64_t hsseig_srrsc_work_doubles(const hsseig_tree* tree) {
@@ -349,10 +466,15 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
   g.d = gen->d; g.dnext = gen->dnext; g.gam = gen->gamma; g.mu = gen->mu; g.zhat = gen->zhat;
   g.v = gen->v; g.k = gen->k;
   TreeDev T = to_dev(tree);
-  const size_t smem = sizeof(double) * 5 * (size_t)T.pmax + sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1);
+  const size_t smem = sizeof(double) * 9 * (size_t)T.pmax + sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1);
   if (smem > 227 * 1024) HSS_ARG_FAIL();
   cudaFuncSetAttribute(srrsc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(srrsc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const int64_t ldw = srrsc_ldw(tree);
+  // resident CTAs of the whole GPU: a level is sized to fill them in one wave
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srrsc_kernel, kSrThreads, smem);
+  const int slots = std::max(1, per_sm) * sm_count();
   for (int lev = lev_from; lev >= lev_to && lev >= 1; --lev) {
     const int npos = 1 << lev;
     if (npos % nparts) HSS_ARG_FAIL();
@@ -361,8 +483,25 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
       const int rc = launch_genB(g, T, lev, j0, cnt, s);
       if (rc) return rc;
     }
-    srrsc_kernel<<<dim3(cnt, 2), kSrThreads, smem, s>>>(g, T, lev, j0, tol, max_rank, work, ldw, st);
-    HSS_CHECK_LAUNCH();
+    // columns of a node split over a cluster so that a level fills about four CTAs per SM
+    int cl = 1;
+    while (cl < kSrMaxCluster && 2 * cnt * cl * 2 <= slots) cl *= 2;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(cnt * cl, 2);
+    lc.blockDim = dim3(kSrThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (cudaLaunchKernelEx(&lc, srrsc_kernel, g, T, lev, j0, tol, (int)max_rank, work, ldw, st) !=
+        cudaSuccess)
+      return HSSEIG_ERR_CUDA;
   }
   if (lev_to == 0) return launch_genB(g, T, 0, 0, 1, s);
   return HSSEIG_OK;

@@ -19,6 +19,9 @@ elif cfg_id == "3":
     T, cfg = hb.gen_kac(n) if hasattr(hb, "gen_kac") else hb.gen_clement(n), hb.SolverConfig(rank_eps=1e-13)
 else:
     T, cfg = hb.gen_config5(n, 0), hb.SolverConfig(rank_eps=1e-13)
+meth = os.environ.get("HSSEIG_METHOD")
+if meth:
+    cfg.method = meth
 hb.adc_solve(T, cfg)   # warm-up
 torch.cuda.synchronize()
 pr = cProfile.Profile()
@@ -29,4 +32,5 @@ torch.cuda.synchronize()
 pr.disable()
 print("wall", time.perf_counter() - t0, "merges", len(res.merges),
       "hss", sum(m.used_hss for m in res.merges), "peak GB", torch.cuda.max_memory_allocated() / 1e9)
-pstats.Stats(pr).sort_stats("tottime").print_stats(25)
+if os.environ.get("HSSEIG_NOPROF") is None:
+    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
