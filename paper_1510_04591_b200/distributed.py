@@ -103,7 +103,16 @@ class ShardedMerge:
         info["flops_secular"] = secular_flops(k, iters) + 14 * k * k
         gen = ops.generators(d, dn, gam, mu, zh, v)
         tree = None
-        if cfg.method == "adc-rand" and k > cfg.hss_threshold:
+        if cfg.method == "adc-srrsc" and k > cfg.hss_threshold:
+            # ADC1: no sample; the construction is partitioned by subtree like ADC2's
+            try:
+                part = build_partition(k, cfg.leaf_size, None, None, mu.cpu().numpy())
+            except ValueError:
+                part = None
+            if part is not None:
+                cap = min(part.min_leaf, ops.max_width)
+                tree = ops.build_srrsc(gen, part, cap, cfg.srrsc_tol, self.group)
+        elif cfg.method == "adc-rand" and k > cfg.hss_threshold:
             mu_h = mu.cpu().numpy()
             try:
                 part = build_partition(k, cfg.leaf_size, None, None, mu_h)
@@ -213,6 +222,7 @@ class GpuOps:
         self.rng = sample_rng.NormalStream(self.k * MAX_WIDTH) if sample_rng.available() else None
         self._trees = {}
         self._mwork = None
+        self._swork = None
 
     def _s(self):
         return self.nat.stream_ptr()
@@ -324,6 +334,38 @@ class GpuOps:
                       "build_levels")
         else:
             nat.check(self.lib.hsseig_hss_build_rand(*args, self._s()), "hss_build_rand")
+        tree._status = st
+        finish_construct(tree)
+        return tree
+
+    def build_srrsc(self, gen, part, cap, tol, group=None):
+        """ADC1 construction (csrc/srrsc.cu) partitioned like build(): each rank eliminates
+        its subtrees below level log2(world), the node slots are all-gathered, the upper
+        levels are built on every rank."""
+        from .hss import HssTree, finish_construct
+        from .secular import Status
+        nat = self.nat
+        tree = HssTree(part, cap)
+        tree.method = "srrsc"
+        need = int(self.lib.hsseig_srrsc_work_doubles(ctypes.byref(tree.ct)))
+        if self._swork is None or self._swork.numel() < need:
+            self._swork = torch.empty(need, dtype=torch.float64, device="cuda")
+        st = Status(self.k)
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        args = (gen.gen, float(tol), int(cap), ctypes.byref(tree.ct), nat.ptr(self._swork),
+                nat.ptr(st.t))
+        depth = tree.ct.depth
+        if world > 1 and (1 << depth) >= world and (world & (world - 1)) == 0:
+            s_lev = world.bit_length() - 1
+            nat.check(self.lib.hsseig_tree_clear(ctypes.byref(tree.ct), self._s()), "tree_clear")
+            nat.check(self.lib.hsseig_hss_build_srrsc_levels(*args, depth, s_lev, rank, world,
+                                                             self._s()), "build_srrsc_levels")
+            gather_subtrees(tree, s_lev, group)
+            nat.check(self.lib.hsseig_hss_build_srrsc_levels(*args, s_lev - 1, 0, 0, 1,
+                                                             self._s()), "build_srrsc_levels")
+        else:
+            nat.check(self.lib.hsseig_hss_build_srrsc(*args, self._s()), "hss_build_srrsc")
         tree._status = st
         finish_construct(tree)
         return tree

@@ -56,6 +56,10 @@ class NumpyOps:
         assert np.allclose(Z.numpy(), G.t_times(om.numpy()), rtol=0, atol=1e-13)
         return orc.rand_construct(G, list(part.ranges), w - 10, 10, Omega=om.numpy())
 
+    def build_srrsc(self, G, part, cap, tol, group=None):
+        from oracle import srrsc_oracle as so
+        return so.srrsc_construct(G, list(part.ranges), cap, tol)
+
     def flagged(self, T):
         return T.flagged
 
@@ -69,7 +73,7 @@ class NumpyOps:
         return torch.as_tensor(orc.update_dense(X.numpy(), G))
 
 
-def _worker(rank, world, port, k, P, out_path):
+def _worker(rank, world, port, k, P, out_path, method="adc-rand"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1510_04591_b200 import SolverConfig
@@ -77,7 +81,7 @@ def _worker(rank, world, port, k, P, out_path):
     d, u, rho = config4_system(k, 3)
     X = np.random.default_rng(7).standard_normal((P, k))
     r0, r1 = rank * P // world, (rank + 1) * P // world
-    cfg = SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13)
+    cfg = SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13, method=method)
     sm = ShardedMerge(k, cfg, NumpyOps(k))
     lam, out, info = sm.run(torch.as_tensor(d), torch.as_tensor(u), rho, torch.as_tensor(X[r0:r1]),
                             seed=[0, 0])
@@ -109,6 +113,22 @@ def test_sharded_merge_world2_matches_single_process(tmp_path, k, P):
     X = np.random.default_rng(7).standard_normal((P, k))
     G, lam, _ = orc.generators_from_roots(d, u, rho)
     ref = orc.update_hss(X, G, 64, 10, 1e-13, 100, [0, 0])
+    assert bool(res["used"])
+    np.testing.assert_array_equal(res["lam"], lam)
+    np.testing.assert_allclose(res["out"], ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+
+
+def test_sharded_merge_adc1_world2_matches_single_process(tmp_path):
+    # ADC1 through the same sharded driver: gathered generators, SRRSC tree, row-local product
+    from oracle import srrsc_oracle as so
+    k, P = 600, 40
+    out_path = str(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(2, _free_port(), k, P, out_path, "adc-srrsc"), nprocs=2, join=True)
+    res = np.load(out_path)
+    d, u, rho = config4_system(k, 3)
+    X = np.random.default_rng(7).standard_normal((P, k))
+    G, lam, _ = orc.generators_from_roots(d, u, rho)
+    ref = so.update_srrsc(X, G, 64, 1e-15)
     assert bool(res["used"])
     np.testing.assert_array_equal(res["lam"], lam)
     np.testing.assert_allclose(res["out"], ref, rtol=0, atol=1e-13 * np.abs(ref).max())

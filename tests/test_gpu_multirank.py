@@ -39,16 +39,22 @@ def _worker(rank, world, port, out_path):
     sm = ShardedMerge(n, cfg, GpuOps(n))
     lam, out, info = sm.run(torch.as_tensor(d, device="cuda"), torch.as_tensor(u, device="cuda"),
                             rho, X[r0:r1].contiguous(), seed=[0, 7])
+    cfg1 = hb.SolverConfig(leaf_size=64, hss_threshold=256, method="adc-srrsc")
+    _, out1, info1 = ShardedMerge(n, cfg1, GpuOps(n)).run(
+        torch.as_tensor(d, device="cuda"), torch.as_tensor(u, device="cuda"), rho,
+        X[r0:r1].contiguous(), seed=[0, 7])
     T = hb.gen_config5(1024, 4)
     res = adc_solve_distributed(T, hb.SolverConfig(rank_eps=1e-13), GpuOps(512))
     outs = [None] * world
-    dist.all_gather_object(outs, (out.cpu().numpy(), res.row0, res.row1, res.Q_rows.cpu().numpy()))
+    dist.all_gather_object(outs, (out.cpu().numpy(), res.row0, res.row1, res.Q_rows.cpu().numpy(),
+                                  out1.cpu().numpy(), bool(info1["used_hss"])))
     if rank == 0:
         Q = np.zeros((1024, 1024))
-        for _, a, b, q in outs:
+        for _, a, b, q, _, _ in outs:
             Q[a:b] = q
         np.savez(out_path, lam=lam.cpu().numpy(), out=np.concatenate([o[0] for o in outs]),
-                 used=info["used_hss"], elam=res.lam, Q=Q)
+                 used=info["used_hss"], elam=res.lam, Q=Q,
+                 out1=np.concatenate([o[4] for o in outs]), used1=all(o[5] for o in outs))
     dist.destroy_process_group()
 
 
@@ -67,6 +73,12 @@ def test_two_ranks_match_single_gpu(tmp_path):
     np.testing.assert_allclose(r["lam"], lam.cpu().numpy(), rtol=0, atol=64 * 2.2e-16 * np.abs(r["lam"]).max())
     refn = ref.cpu().numpy()
     np.testing.assert_allclose(r["out"], refn, rtol=0, atol=1e-12 * np.abs(refn).max())
+    # ADC1 (SRRSC construction partitioned by subtree, slots all-gathered)
+    cfg1 = hb.SolverConfig(leaf_size=64, hss_threshold=256, method="adc-srrsc")
+    _, ref1, _ = hb.merge_update(d, u, rho, X, cfg1, seed=[0, 7])
+    assert bool(r["used1"])
+    ref1 = ref1.cpu().numpy()
+    np.testing.assert_allclose(r["out1"], ref1, rtol=0, atol=1e-12 * np.abs(ref1).max())
     T = hb.gen_config5(1024, 4)
     res = hb.adc_solve(T, hb.SolverConfig(rank_eps=1e-13))
     np.testing.assert_allclose(r["elam"], res.lam, rtol=0, atol=1e-13 * T.norm_max())
