@@ -184,6 +184,39 @@ def measure_dgemm_peak(torch):
     return 2 * n ** 3 / (e0.elapsed_time(e1) / 4 * 1e-3) / 1e12
 
 
+def adc1_merge(d, u, rho, Q, out, reps=2):
+    """Config-4 merge with ADC1 (method "adc-srrsc"): secular -> Loewner -> normalizers ->
+    SRRSC construction -> HSS x Q_old, device-timed phase by phase (best of reps)."""
+    import torch
+
+    import paper_1510_04591_b200 as hb
+    from paper_1510_04591_b200.flops import FlopCounter
+    best = None
+    for _ in range(reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        fl = FlopCounter()
+        ev[0].record()
+        sys_ = hb.RankOneSystem(d, u, rho)
+        sol = hb.solve_secular(sys_, flops=fl)
+        hb.recompute_weights(sys_.d, sol, sys_.z, rho=rho, flops=fl)
+        C = hb.CauchyEvecMatrix.from_secular(sys_, sol, flops=fl)
+        ev[1].record()
+        part = hb.build_partition(C.k, 128, C.d, C.gamma, C.mu)
+        H = hb.srrsc_hss_construct(C, part, hb.srrsc_cap(part), tol=1e-15, flops=fl)
+        ev[2].record()
+        if not H.flagged:
+            hb.hss_matmul_right(Q, H, flops=fl, out=out)
+        ev[3].record()
+        torch.cuda.synchronize()
+        ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
+        rec = {"ms": sum(ms), "secular_loewner_normalizers_ms": ms[0], "construct_ms": ms[1],
+               "multiply_ms": ms[2], "r_used": int(H.r_used), "flagged": bool(H.flagged),
+               "flops": fl.as_dict()}
+        if best is None or rec["ms"] < best["ms"]:
+            best = rec
+    return best
+
+
 def eigh_lines():
     """Full tridiagonal eigendecompositions (BASELINE configs 1, 2, 3, 5) on one GPU: wall-s
     + accuracy.  Config 2 is ADC1 as BASELINE names it (SRRSC construction, method
@@ -447,6 +480,11 @@ def run_ours(args):
                "d2h_bytes_per_step": int(hOut.numel() * 8)}
         del hQ, hOut
 
+    # ---- the same config-4 merge with ADC1 (SRRSC construction, no sample): informational
+    adc1 = None
+    if world == 1 and not args.no_eigh:
+        adc1 = adc1_merge(d, u, rho, Qloc, out)
+
     # the full solves below need the HBM the merge bench holds (Q_old, outputs, workspaces)
     pipe = sm = step = Xd = None   # noqa: F841
     del Qloc, out
@@ -486,6 +524,8 @@ def run_ours(args):
         }
         if world == 1 and not args.no_eigh:
             line["eigh"] = eigh_lines()
+        if adc1 is not None:
+            line["config4_adc1"] = adc1
         if world > 1 and eigh_d is not None:
             line["eigh"] = {"cfg5_N65536_distributed": eigh_d}
         if not args.no_cpu and world == 1:

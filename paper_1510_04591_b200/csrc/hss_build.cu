@@ -105,14 +105,20 @@ __global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level, i
   // one CTA per (node, side, half): rows [off, off + nrow) of Phi (side 0) or Theta (side 1).
   // B block and sibling compression are staged in shared memory; every thread carries 4
   // independent output columns so the contraction is not latency bound.
+  // blockIdx.z = half + 2 * (row chunk): upper levels have few nodes, so each half's rows
+  // are split over gridDim.z / 2 CTAs (latency-bound otherwise)
   extern __shared__ __align__(16) double fs[];
-  const int j = j0 + blockIdx.x, side = blockIdx.y, half = blockIdx.z, tid = threadIdx.x;
+  const int j = j0 + blockIdx.x, side = blockIdx.y, half = blockIdx.z & 1, tid = threadIdx.x;
+  const int rc = blockIdx.z >> 1, nrc = gridDim.z >> 1;
   const int node = T.lnodes[(1 << level) - 1 + j];
   const int a = T.left[node], b = T.right[node], w = T.w, ws = T.ws;
   const int me = half == 0 ? a : b, sib = half == 0 ? b : a;
   const int na = side == 0 ? T.rU[a] : T.rV[a];
-  const int nrow = side == 0 ? T.rU[me] : T.rV[me];
-  const int off = half == 0 ? 0 : na;
+  const int nall = side == 0 ? T.rU[me] : T.rV[me];
+  const int rchunk = (nall + nrc - 1) / nrc;
+  const int r0 = min(nall, rc * rchunk);
+  const int nrow = min(nall, r0 + rchunk) - r0;
+  const int off = (half == 0 ? 0 : na) + r0;
   const int nk = side == 0 ? T.rV[sib] : T.rU[sib];
   double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * ws;
   const double* comp = (side == 0 ? T.ycomp : T.zcomp) + slot_ww(T, sib);
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level, i
   double* sCm = fs + (size_t)w * SK;     // nk x w
   for (int e = tid; e < nrow * nk; e += blockDim.x) {
     const int r = e / nk, t = e % nk;
-    sBt[r * SK + t] = side == 0 ? Bb[(size_t)r * ws + t] : Bb[(size_t)t * ws + r];
+    sBt[r * SK + t] = side == 0 ? Bb[(size_t)(r0 + r) * ws + t] : Bb[(size_t)t * ws + r0 + r];
   }
   for (int e = tid; e < nk * w; e += blockDim.x) {
     const int t = e / w, c = e % w;
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level, i
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int c = c0 + q * cq;
-      if (c < w) Mo[(size_t)(off + r) * ws + c] = sel[(size_t)r * ws + c] - acc[q];
+      if (c < w) Mo[(size_t)(off + r) * ws + c] = sel[(size_t)(r0 + r) * ws + c] - acc[q];
     }
   }
 }
@@ -217,7 +223,15 @@ __device__ __forceinline__ void id_truncate(double* sA, double* tail, int p, int
         x[t] = xt;
         if (xt != 0.0) {
           const double* rc = sA + t * SW;
-          for (int s2 = 0; s2 < t; ++s2) x[s2] = fma(-xt, rc[s2], x[s2]);
+          int s2 = 0;
+          for (; s2 + 7 < t; s2 += 8) {   // loads ahead of the stores (x, rc in one array)
+            double rr[8], xx[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { rr[u] = rc[s2 + u]; xx[u] = x[s2 + u]; }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[s2 + u] = fma(-xt, rr[u], xx[u]);
+          }
+          for (; s2 < t; ++s2) x[s2] = fma(-xt, rc[s2], x[s2]);
         }
       }
     }
@@ -484,8 +498,16 @@ __device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* 
           for (; t < w; ++t) d0 = fma(v[t], a[t], d0);
           const double f = tau * ((d0 + d1) + (d2 + d3));
           a[i] -= f;
-#pragma unroll 4
-          for (t = i + 1; t < w; ++t) a[t] = fma(-f, v[t], a[t]);
+          // eight loads in flight before the stores (a and v never overlap, but the
+          // compiler cannot prove it, so a plain loop serialises load -> fma -> store)
+          for (t = i + 1; t + 7 < w; t += 8) {
+            double vv[8], aa[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { vv[u] = v[t + u]; aa[u] = a[t + u]; }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a[t + u] = fma(-f, vv[u], aa[u]);
+          }
+          for (; t < w; ++t) a[t] = fma(-f, v[t], a[t]);
         }
         const double n1 = vn1[c];
         if (n1 != 0.0) {
@@ -767,7 +789,8 @@ static int build_levels(const hsseig_gen* gen, const double* omega, int64_t ldom
     } else {
       genB_kernel<<<grid, 256, 0, s>>>(g, T, lev, j0);
       HSS_CHECK_LAUNCH();
-      inner_form_kernel<<<dim3(cnt, 2, 2), 256, smem_form, s>>>(T, lev, j0);
+      const int nrc = cnt >= 64 ? 1 : (cnt >= 16 ? 2 : 4);   // row chunks per half
+      inner_form_kernel<<<dim3(cnt, 2, 2 * nrc), 256, smem_form, s>>>(T, lev, j0);
     }
     HSS_CHECK_LAUNCH();
     id_kernel<<<grid, 256, smem_id, s>>>(T, lev, id_tol, omega, ldom, st, j0);
