@@ -375,6 +375,10 @@ int hsseig_wave_tile_shape(int32_t *bm, int32_t *bn);
    (dc.py:253-257). */
 int hsseig_wave_order(int64_t nm, const int64_t *roff, const int64_t *kept, const int64_t *koff,
                       const double *lam, const double *d_out, int64_t *order, double *lam_out);
+/* Column descriptors of the gather from the final order (local positions), the compact-W
+   map (cmap, -1 = not materialised) and the blockdiag source columns (src). */
+int hsseig_wave_desc(int64_t nm, const int64_t *roff, const int64_t *kept, const int64_t *order,
+                     const int64_t *cmap, const int64_t *src, int64_t *desc);
 /* out_m[:, c] from desc[roff[m] + c] = (source << 40) | index: source 0 = column of Qk_m
    (n x k_m), 1 = compact W_m column, 2 = blockdiag(Q1, Q2) column read from the children. */
 int hsseig_wave_gather(const double *Qk, const int64_t *qoff, const int64_t *kept,
@@ -383,6 +387,14 @@ int hsseig_wave_gather(const double *Qk, const int64_t *qoff, const int64_t *kep
                        const int64_t *n1, const int64_t *n2, const int64_t *roff,
                        const int32_t *row_merge, double *out, const int64_t *ooff, int64_t nrows,
                        void *stream);
+/* Rows sel_row[i] of merge sel_merge[i] of the same gather, written to out + sel_off[i]
+ * (the boundary rows the next depth's z needs, dc.py:112, taken before the full gather). */
+int hsseig_wave_gather_rows(const double *Qk, const int64_t *qoff, const int64_t *kept,
+                            const double *W, const int64_t *woff, const int64_t *wd,
+                            const int64_t *desc, const uint64_t *q1, const uint64_t *q2,
+                            const int64_t *n1, const int64_t *n2, const int64_t *roff,
+                            const int32_t *sel_merge, const int64_t *sel_row,
+                            const int64_t *sel_off, int64_t nsel, double *out, void *stream);
 
 /* The dense update through materialised column panels of C (the reference's to_dense
    entries) and the TMA/DMMA GEMM engine (k >= 512, 16-byte aligned Qb rows, even ldq);

@@ -129,7 +129,9 @@ _SIGS = {
     "hsseig_wave_dense_update": (ctypes.c_int, [c_vp] * 14 + [c_i64, c_vp]),
     "hsseig_wave_tile_shape": (ctypes.c_int, [c_vp, c_vp]),
     "hsseig_wave_order": (ctypes.c_int, [c_i64] + [c_vp] * 7),
+    "hsseig_wave_desc": (ctypes.c_int, [c_i64] + [c_vp] * 6),
     "hsseig_wave_gather": (ctypes.c_int, [c_vp] * 15 + [c_i64, c_vp]),
+    "hsseig_wave_gather_rows": (ctypes.c_int, [c_vp] * 15 + [c_i64, c_vp, c_vp]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -278,39 +278,55 @@ __global__ void wave_rotate_kernel(double* __restrict__ W, const int64_t* __rest
 // out_m[:, c] from the column descriptor desc[c] = (source << 40) | index: source 0 = Qk_m
 // column (an updated eigenvector), 1 = compact W_m column (a rotated deflated column), 2 =
 // blockdiag(Q1, Q2) column read straight from the children (an untouched deflated column).
-__global__ void wave_gather_kernel(const double* __restrict__ Qk, const int64_t* __restrict__ qoff,
-                                   const int64_t* __restrict__ kept, const double* __restrict__ W,
-                                   const int64_t* __restrict__ woff, const int64_t* __restrict__ wd,
-                                   const int64_t* __restrict__ desc,
-                                   const unsigned long long* __restrict__ q1,
-                                   const unsigned long long* __restrict__ q2,
-                                   const int64_t* __restrict__ n1, const int64_t* __restrict__ n2,
-                                   const int64_t* __restrict__ roff,
-                                   const int32_t* __restrict__ row_merge, double* __restrict__ out,
-                                   const int64_t* __restrict__ ooff, int64_t nrows) {
+struct GatherSrc {
+  const double* Qk;
+  const int64_t *qoff, *kept;
+  const double* W;
+  const int64_t *woff, *wd, *desc;
+  const unsigned long long *q1, *q2;
+  const int64_t *n1, *n2, *roff;
+};
+
+// Row `row` of merge m's output in eigenvalue order, written to o (n doubles).
+__device__ __forceinline__ void gather_row(const GatherSrc& g, int m, int64_t row, double* o) {
   constexpr int64_t kMask = (1ll << 40) - 1;
+  const int64_t a = g.n1[m], b = g.n2[m], n = a + b, k = g.kept[m];
+  const int64_t* dm = g.desc + g.roff[m];
+  const double* q = g.Qk + g.qoff[m] + row * k;
+  const double* w = g.W + g.woff[m] + row * (g.wd[m] + (g.wd[m] & 1));
+  // this row's half of blockdiag(Q1, Q2): child columns [c0, c0 + nc)
+  const bool top = row < a;
+  const double* qc = top ? reinterpret_cast<const double*>(g.q1[m]) + row * a
+                         : reinterpret_cast<const double*>(g.q2[m]) + (row - a) * b;
+  const int64_t c0 = top ? 0 : a, nc = top ? a : b;
+  for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
+    const int64_t dsc = dm[c];
+    const int64_t src = dsc >> 40, idx = dsc & kMask;
+    double v;
+    if (src == 0) v = q[idx];
+    else if (src == 1) v = w[idx];
+    else v = (idx >= c0 && idx < c0 + nc) ? qc[idx - c0] : 0.0;
+    o[c] = v;
+  }
+}
+
+__global__ void wave_gather_kernel(GatherSrc g, const int32_t* __restrict__ row_merge,
+                                   double* __restrict__ out, const int64_t* __restrict__ ooff,
+                                   int64_t nrows) {
   for (int64_t gr = blockIdx.x; gr < nrows; gr += gridDim.x) {
     const int m = row_merge[gr];
-    const int64_t a = n1[m], b = n2[m], n = a + b, row = gr - roff[m], k = kept[m];
-    const int64_t* dm = desc + roff[m];
-    const double* q = Qk + qoff[m] + row * k;
-    const double* w = W + woff[m] + row * (wd[m] + (wd[m] & 1));
-    // this row's half of blockdiag(Q1, Q2): child columns [c0, c0 + nc)
-    const bool top = row < a;
-    const double* qc = top ? reinterpret_cast<const double*>(q1[m]) + row * a
-                           : reinterpret_cast<const double*>(q2[m]) + (row - a) * b;
-    const int64_t c0 = top ? 0 : a, nc = top ? a : b;
-    double* o = out + ooff[m] + row * n;
-    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
-      const int64_t dsc = dm[c];
-      const int64_t src = dsc >> 40, idx = dsc & kMask;
-      double v;
-      if (src == 0) v = q[idx];
-      else if (src == 1) v = w[idx];
-      else v = (idx >= c0 && idx < c0 + nc) ? qc[idx - c0] : 0.0;
-      o[c] = v;
-    }
+    const int64_t row = gr - g.roff[m], n = g.n1[m] + g.n2[m];
+    gather_row(g, m, row, out + ooff[m] + row * n);
   }
+}
+
+// Selected rows only (the boundary rows the next depth's z needs, before the full gather).
+__global__ void wave_gather_rows_kernel(GatherSrc g, const int32_t* __restrict__ sel_merge,
+                                        const int64_t* __restrict__ sel_row,
+                                        const int64_t* __restrict__ sel_off, int64_t nsel,
+                                        double* __restrict__ out) {
+  for (int64_t i = blockIdx.x; i < nsel; i += gridDim.x)
+    gather_row(g, sel_merge[i], sel_row[i], out + sel_off[i]);
 }
 
 // One rank's row block of W = blockdiag(Q1, Q2)[:, src] when its rows all come from one
@@ -495,10 +511,31 @@ extern "C" int hsseig_wave_gather(const double* Qk, const int64_t* qoff, const i
       !row_merge || !out || !ooff || !kept || !qoff)
     HSS_ARG_FAIL();
   if (nrows == 0) return HSSEIG_OK;
-  wave_gather_kernel<<<rows_grid(nrows), 256, 0, (cudaStream_t)stream>>>(
-      Qk ? Qk : W, qoff, kept, W, woff, wd, desc,
-      reinterpret_cast<const unsigned long long*>(q1), reinterpret_cast<const unsigned long long*>(q2),
-      n1, n2, roff, row_merge, out, ooff, nrows);
+  GatherSrc g{Qk ? Qk : W, qoff, kept, W, woff, wd, desc,
+              reinterpret_cast<const unsigned long long*>(q1),
+              reinterpret_cast<const unsigned long long*>(q2), n1, n2, roff};
+  wave_gather_kernel<<<rows_grid(nrows), 256, 0, (cudaStream_t)stream>>>(g, row_merge, out, ooff,
+                                                                          nrows);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_gather_rows(const double* Qk, const int64_t* qoff, const int64_t* kept,
+                                       const double* W, const int64_t* woff, const int64_t* wd,
+                                       const int64_t* desc, const uint64_t* q1, const uint64_t* q2,
+                                       const int64_t* n1, const int64_t* n2, const int64_t* roff,
+                                       const int32_t* sel_merge, const int64_t* sel_row,
+                                       const int64_t* sel_off, int64_t nsel, double* out,
+                                       void* stream) {
+  if (nsel < 0 || !W || !woff || !wd || !desc || !q1 || !q2 || !n1 || !n2 || !roff || !kept ||
+      !qoff || !sel_merge || !sel_row || !sel_off || !out)
+    HSS_ARG_FAIL();
+  if (nsel == 0) return HSSEIG_OK;
+  GatherSrc g{Qk ? Qk : W, qoff, kept, W, woff, wd, desc,
+              reinterpret_cast<const unsigned long long*>(q1),
+              reinterpret_cast<const unsigned long long*>(q2), n1, n2, roff};
+  wave_gather_rows_kernel<<<rows_grid(nsel), 256, 0, (cudaStream_t)stream>>>(
+      g, sel_merge, sel_row, sel_off, nsel, out);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
@@ -635,6 +672,20 @@ extern "C" int hsseig_wave_order(int64_t nm, const int64_t* roff, const int64_t*
     int64_t* ord = order + o;
     stable_argsort_runs(cat.data(), k, n, ord);
     for (int64_t t = 0; t < n; ++t) lam_out[o + t] = cat[ord[t]];
+  });
+  return HSSEIG_OK;
+}
+
+extern "C" int hsseig_wave_desc(int64_t nm, const int64_t* roff, const int64_t* kept,
+                                const int64_t* order, const int64_t* cmap, const int64_t* src,
+                                int64_t* desc) {
+  for_each_merge(nm, roff, [&](int64_t m) {
+    const int64_t o = roff[m], n = roff[m + 1] - o, k = kept[m];
+    for (int64_t t = 0; t < n; ++t) {
+      const int64_t p = order[o + t];
+      const int64_t cm = cmap[o + p];
+      desc[o + t] = p < k ? p : (cm >= 0 ? ((1ll << 40) | cm) : ((2ll << 40) | src[o + p]));
+    }
   });
   return HSSEIG_OK;
 }

@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .cauchy import DENSE_PANEL_MIN_K, CauchyEvecMatrix
+from .cauchy import DENSE_PANEL_BYTES, DENSE_PANEL_MIN_K, CauchyEvecMatrix
 from .dc import (HSS_METHODS, BaseCaseError, EigenResult, HssJob, MergeRecord, SolverConfig,
                  merge_update, update_vectors_hss_many)
 from .flops import FlopCounter, cauchy_eval_flops, gemm_flops, secular_flops
@@ -305,6 +305,27 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
     base_lo = int(lo_a[-1])
     leaf_idx = np.flatnonzero(leaf_a)        # postorder visits the leaves left to right
     lam_all, Qbase, lqoff = _base_cases_flat(a_mod, b, lo_a[leaf_idx], hi_a[leaf_idx], s)
+    # boundary rows (the z of dc.py:112) of every finished block on the host, by node: the
+    # leaves' from the base cases here, a merge's from the early row gather of its depth,
+    # so the next depth's deflation runs while the device is still gathering
+    nl = hi_a[leaf_idx] - lo_a[leaf_idx]
+    rows_h = np.zeros(0)
+    if len(leaf_idx):
+        first_i = np.repeat(lqoff[:-1], nl) + (np.arange(int(nl.sum())) - np.repeat(np.cumsum(nl) - nl, nl))
+        last_i = first_i + np.repeat((nl - 1) * nl, nl)
+        rows_h = Qbase[torch.as_tensor(np.concatenate([first_i, last_i]), device="cuda")].cpu().numpy()
+    lrow0 = np.concatenate([[0], np.cumsum(nl)]).astype(np.int64)
+    # offsets of every node's first / last row in [leaf rows | the last depth's row gather]
+    first_off = np.zeros(len(tab), dtype=np.int64)
+    last_off = np.zeros(len(tab), dtype=np.int64)
+    first_off[leaf_idx] = lrow0[:-1]
+    last_off[leaf_idx] = int(lrow0[-1]) + lrow0[:-1]
+    is_left = np.zeros(len(tab), dtype=bool)
+    has_parent = np.zeros(len(tab), dtype=bool)
+    for j in np.flatnonzero(~leaf_a).tolist():
+        is_left[left_a[j]] = True
+        has_parent[left_a[j]] = has_parent[right_a[j]] = True
+    pending = None      # (event, pinned rows, node ids, offsets, sizes) of the last depth
     # per node: device address of its Q block (row-major n x n) and the buffer holding it
     qptr = np.zeros(len(tab), dtype=np.uint64)
     qptr[leaf_idx] = np.uint64(Qbase.data_ptr()) + (8 * lqoff[:-1]).astype(np.uint64)
@@ -333,11 +354,17 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         q1, q2, n1_d, n2_d, nv_d, roff_d = (
             _Pack().add(qptr[left_a[ms]].view(np.int64)).add(qptr[right_a[ms]].view(np.int64))
             .add(n1).add(n2).add(nv).add(roff).send())
-        # boundary rows -> host (sync 1)
-        zrow_d = torch.empty(nrows, **f64)
-        nat.check(lib.hsseig_wave_zrows(nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
-                                        nat.ptr(roff_d), nm, nat.ptr(zrow_d), s), "wave_zrows")
-        zrow = zrow_d.cpu().numpy()
+        # boundary rows of the children (sync 1: the early row gather of the previous depth)
+        src_rows = rows_h
+        if pending is not None:
+            ev_rows, rows_pin = pending
+            ev_rows.synchronize()
+            src_rows = np.concatenate([rows_h, rows_pin.numpy()])
+            pending = None
+        # z rows: [last row of the left child | first row of the right child] per merge
+        st_z = np.stack([last_off[left_a[ms]], first_off[right_a[ms]]], 1).reshape(-1)
+        ln_z = np.stack([n1, n2], 1).reshape(-1)
+        zrow = src_rows[np.repeat(st_z - (np.cumsum(ln_z) - ln_z), ln_z) + np.arange(nrows)]
         bk = np.ascontiguousarray(b[sp_m - 1], dtype=np.float64)
         kept = np.empty(nm, dtype=np.int64)
         rho_eff = np.empty(nm)
@@ -425,21 +452,48 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             nat.check(lib.hsseig_wave_normalizers(nat.ptr(dk), nat.ptr(dn), nat.ptr(gam), nat.ptr(mu),
                                                   nat.ptr(zh), nat.ptr(koff_d), nat.ptr(seg_of), ktot,
                                                   nat.ptr(vv), s), "wave_normalizers")
-            for q in np.flatnonzero(big_q).tolist():
-                m = segs[q]
-                n, k = int(nv[m]), int(kept[m])
-                sl = slice(int(koff[q]), int(koff[q + 1]))
-                C = CauchyEvecMatrix(dk[sl], gam[sl], mu[sl], zh[sl], vv[sl], dnext=dn[sl])
-                Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(ldw[m]))
-                C.right_multiply_into(Wm[:, :k], out=Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k))
+            # statuses and roots (sync 2) go to pinned host buffers right behind the secular
+            # stage; the dense updates are queued before the host waits, so the host-side
+            # checks, HSS set-up and final ordering below overlap them on the device
+            st_pin = torch.empty((nseg, 8), dtype=torch.int64, pin_memory=True)
+            lam_pin = torch.empty(ktot, dtype=torch.float64, pin_memory=True)
+            st_pin.copy_(st.view(nseg, 8), non_blocking=True)
+            lam_pin.copy_(lam_k, non_blocking=True)
+            if hss_m:
+                gam_pin = torch.empty(ktot, dtype=torch.float64, pin_memory=True)
+                mu_pin = torch.empty(ktot, dtype=torch.float64, pin_memory=True)
+                gam_pin.copy_(gam, non_blocking=True)
+                mu_pin.copy_(mu, non_blocking=True)
+            roots_ready = torch.cuda.Event()
+            roots_ready.record()
+            big = np.flatnonzero(big_q)
+            if len(big):
+                # materialised-panel updates straight through the C ABI (one generator struct
+                # and one shared workspace; cauchy.py's right_multiply_into per merge costs
+                # ~70 us of host time each at config 5)
+                kmax = int(ks[big].max())
+                pw = torch.empty(int(lib.hsseig_dense_update_work_doubles(
+                    kmax, max(128, DENSE_PANEL_BYTES // (8 * kmax)))), **f64)
+                gb = [t.data_ptr() for t in (dk, dn, gam, mu, zh, vv)]
+                Wb, Qb = W.data_ptr(), Qk.data_ptr()
+                for q in big.tolist():
+                    m = segs[q]
+                    n, k, o8 = int(nv[m]), int(kept[m]), 8 * int(koff[q])
+                    g = nat.Gen(gb[0] + o8, gb[1] + o8, gb[2] + o8, gb[3] + o8, gb[4] + o8,
+                                gb[5] + o8, k)
+                    nw = int(lib.hsseig_dense_update_work_doubles(k, max(128, DENSE_PANEL_BYTES // (8 * k))))
+                    nat.check(lib.hsseig_dense_update_ws(
+                        ctypes.c_void_p(Wb + 8 * int(woff[m])), int(ldw[m]), n, ctypes.byref(g),
+                        ctypes.c_void_p(Qb + 8 * int(qoff[m])), k, nat.ptr(pw), nw, s),
+                        "dense_update")
             if len(tk):
                 nat.check(lib.hsseig_wave_dense_update(
                     nat.ptr(W), nat.ptr(t_woff), nat.ptr(t_nv), nat.ptr(t_ldw), nat.ptr(dk),
                     nat.ptr(dn), nat.ptr(gam), nat.ptr(mu), nat.ptr(zh), nat.ptr(vv), nat.ptr(koff_d),
                     nat.ptr(Qk), nat.ptr(t_qoff), nat.ptr(t_tk), len(tk), s),
                     "wave_dense_update")
-            # statuses + roots (sync 2)
-            stv = st.view(nseg, 8).cpu().numpy()
+            roots_ready.synchronize()
+            stv = st_pin.numpy()
             bad_b = (stv[:, 1] < ks) | ((ks >= 2) & (stv[:, 2] < ks))
             bad_r = stv[:, 3] < ks
             if (bad_b | bad_r).any():
@@ -451,7 +505,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             seg_iters = stv[:, 0]
             if hss_m:
                 # the level's HSS merges, phase-batched (partition / rank from host roots)
-                gam_h, mu_h, dk_h = gam.cpu().numpy(), mu.cpu().numpy(), d_out[kidx]
+                gam_h, mu_h, dk_h = gam_pin.numpy(), mu_pin.numpy(), d_out[kidx]
                 jobs = []
                 for q in sorted(hss_m):
                     m = segs[q]
@@ -468,7 +522,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 for j in jobs:
                     j.record.flops = j.flops.as_dict()
                 del jobs
-            lam_h = lam_k.cpu().numpy()
+            lam_h = lam_pin.numpy()
         else:
             lam_h = np.zeros(0)
         # final column order of every merge
@@ -480,11 +534,34 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                               _cptr(d_out), _cptr(order), _cptr(lam_out))
         A = torch.empty(int(ooff[-1]), **f64)
         # column descriptors: (0, Qk column) | (1, compact W column) | (2, child column)
-        pg = order + roff[rm]
-        cmg = cmap[pg]
-        desc = np.where(order < kept[rm], order,
-                        np.where(cmg >= 0, (1 << 40) | cmg, (2 << 40) | src[pg])).astype(np.int64)
-        g_qoff, g_kept, g_desc, ooff_d = _Pack().add(qoff).add(kept).add(desc).add(ooff).send()
+        desc = np.empty(nrows, dtype=np.int64)
+        lib.hsseig_wave_desc(nm, _cptr(roff), _cptr(kept), _cptr(order), _cptr(cmap), _cptr(src),
+                             _cptr(desc))
+        sel = np.flatnonzero(has_parent[ms])
+        sel_left = is_left[ms[sel]]
+        sel_off = np.concatenate([[0], np.cumsum(nv[sel])]).astype(np.int64)
+        (g_qoff, g_kept, g_desc, ooff_d, sel_m, sel_r, sel_o) = (
+            _Pack().add(qoff).add(kept).add(desc).add(ooff).add(sel, np.int32)
+            .add(np.where(sel_left, nv[sel] - 1, 0)).add(sel_off[:-1]).send())
+        if len(sel):
+            # the rows the next depth's z needs (a left child's last row, a right child's
+            # first), gathered ahead of the full gather and sent to the host behind it
+            rows_d = torch.empty(int(sel_off[-1]), **f64)
+            nat.check(lib.hsseig_wave_gather_rows(nat.ptr(Qk), nat.ptr(g_qoff), nat.ptr(g_kept),
+                                                  nat.ptr(W), nat.ptr(woff_d), nat.ptr(wd_d),
+                                                  nat.ptr(g_desc), nat.ptr(q1), nat.ptr(q2),
+                                                  nat.ptr(n1_d), nat.ptr(n2_d), nat.ptr(roff_d),
+                                                  nat.ptr(sel_m), nat.ptr(sel_r), nat.ptr(sel_o),
+                                                  len(sel), nat.ptr(rows_d), s), "wave_gather_rows")
+            rows_pin = torch.empty(int(sel_off[-1]), dtype=torch.float64, pin_memory=True)
+            rows_pin.copy_(rows_d, non_blocking=True)
+            ev_rows = torch.cuda.Event()
+            ev_rows.record()
+            pending = (ev_rows, rows_pin)
+            gsel = ms[sel]
+            base = len(rows_h) + sel_off[:-1]
+            last_off[gsel[sel_left]] = base[sel_left]
+            first_off[gsel[~sel_left]] = base[~sel_left]
         nat.check(lib.hsseig_wave_gather(nat.ptr(Qk), nat.ptr(g_qoff), nat.ptr(g_kept),
                                          nat.ptr(W), nat.ptr(woff_d), nat.ptr(wd_d), nat.ptr(g_desc),
                                          nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
