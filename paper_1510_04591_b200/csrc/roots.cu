@@ -104,7 +104,7 @@ __device__ __forceinline__ void secular_roots(
     const double dj = __ldg(d + j), qj = __ldg(z2 + j);
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (live[r] && !outer[r]) fh[r] = fma(rho * qj, rcp_nr((dj - dori[r]) - half[r]), fh[r]);
+      if (live[r] && !outer[r]) fh[r] = fma(rho * qj, rcp_c3((dj - dori[r]) - half[r]), fh[r]);
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -157,7 +157,7 @@ __device__ __forceinline__ void secular_roots(
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double g = (dj - dori[r]) - x[r];
-        const double inv = rcp_nr(g);
+        const double inv = rcp_c3(g);
         const double t = qj * inv;
         sl[r] += t;
         dl[r] = fma(t, inv, dl[r]);
@@ -169,7 +169,7 @@ __device__ __forceinline__ void secular_roots(
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double g = (dj - dori[r]) - x[r];
-        const double inv = rcp_nr(g);
+        const double inv = rcp_c3(g);
         const double t = qj * inv;
         const double td = t * inv;
         if (j <= split[r]) { sl[r] += t; dl[r] += td; }
@@ -182,7 +182,7 @@ __device__ __forceinline__ void secular_roots(
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double g = (dj - dori[r]) - x[r];
-        const double inv = rcp_nr(g);
+        const double inv = rcp_c3(g);
         const double t = qj * inv;
         sr[r] += t;
         dr[r] = fma(t, inv, dr[r]);
@@ -301,7 +301,7 @@ __device__ __forceinline__ void loewner_rows(
       if (j == i) continue;
       const double num = -stable_gap(i, j, di[r], dj, dnj, gj, mj);
       const double den = dj - di[r];
-      pr[r] *= num * rcp_nr(den);
+      pr[r] *= num * rcp_c3(den);
     }
   }
 #pragma unroll
@@ -352,7 +352,7 @@ __device__ __forceinline__ void normalizer_cols(
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       double g = stable_gap(i, j0 + r, di, dj[r], dnj[r], gj[r], mj[r]);
-      double q = zi * rcp_nr(g);
+      double q = zi * rcp_c3(g);
       s[r] = fma(q, q, s[r]);
     }
   }
