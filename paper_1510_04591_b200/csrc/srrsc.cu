@@ -16,12 +16,15 @@
 // X = L L_J^{-1} (identity on the skeleton J).  Stop when max|M^(s)| <= tol * max|M^(0)|
 // or at the rank cap (saturation flag when the residual is still above 1e-12).
 //
-// One CTA per (node, side); the candidate rows and their generators live in shared memory,
-// the column generators (k - |t| of them) in a per-(node, side) HBM/L2 vector that each
-// elimination step sweeps once: the sweep applies the previous pivot's column rescaling and
-// searches the new maximum.  The search is division-free: an entry only reaches the exact
-// IEEE value |s t / g| (and the argmax compare) when |s| |t| / best >= |g|, so per entry the
-// sweep costs two DADD (the stable gap), one DMUL and one compare.
+// One thread-block cluster (1-16 CTAs) per (node, side); the candidate rows and their
+// generators live in every CTA's shared memory, the column generators (k - |t| of them) in a
+// per-(node, side) HBM/L2 vector whose columns are split over the cluster and swept once per
+// elimination step: the sweep applies the previous pivot's column rescaling and searches the
+// new maximum, and the CTAs' records meet through DSMEM after one cluster barrier.  The
+// search is division-free: an entry only reaches the exact IEEE value |s t / g| (and the
+// argmax compare) when |s| |t| / best + slack >= |e - c| (the gap with the rounding of its
+// folded form covered by the slack), so per entry the sweep costs one DADD, one DFMA and
+// one compare.
 // Cost: sum over nodes of |R| (k - |t|) rank entries, O(k^2 r) per merge, the complexity the
 // paper quotes for ADC1.
 #include <algorithm>
