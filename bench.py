@@ -397,6 +397,7 @@ def run_ours(args):
             return {"ms": {"total": e0.elapsed_time(e1), "multiply": mult},
                     "flops": {"secular": info["flops_secular"], "hss_construct": fl_con,
                               "hss_mult_local": fl_loc, "hss_mult": fl_mult, "update_dense": 0},
+                    "sample_gather": info.get("sample_gather"),
                     "flops_total_fullP": info["flops_secular"] + fl_con + fl_mult,
                     "r_used": info["r_used"], "used_hss": info["used_hss"]}
 
@@ -510,7 +511,10 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded config-4 system; Q_old = QR of a seeded Gaussian)",
-            "config": config_dict(n, world),
+            "config": dict(config_dict(n, world), **(
+                {"sample_gather": "CUDA-IPC peer stores fused in the split-K reduction"
+                 if rec.get("sample_gather") == "peer" else "NCCL all-gather"}
+                if world > 1 else {})),
             "merge_wall_s": ms / 1e3,
             "phases_ms": {k: statistics.median(p["ms"][k] for p in phase_ms) for k in rec["ms"]},
             "flops": rec["flops"], "hss_rank": rec["r_used"], "used_hss": rec["used_hss"],

@@ -128,6 +128,18 @@ int hsseig_cauchy_sample_part(const hsseig_gen *gen, const double *omega, int64_
                               double *work, void *stream);
 
 /*
+ * Multi-GPU form fused with the all-gather: rows [row0, row1) of Y and Z are computed here
+ * and stored by the split-K reduction kernels straight into every rank's full k x w Y / Z
+ * (Yp / Zp: npeers device pointers, this rank's own included, IPC-mapped peer buffers over
+ * NVLink / NVSwitch).  The caller synchronises its stream and barriers the group before
+ * reading.  Materialised-panel path only (HSSEIG_ERR_ARG otherwise: use the NCCL gather).
+ */
+int hsseig_cauchy_sample_part_peers(const hsseig_gen *gen, const double *omega, int64_t ldom,
+                                    int64_t w, int64_t row0, int64_t row1, const uint64_t *Yp,
+                                    const uint64_t *Zp, int32_t npeers, int64_t ldy, double *work,
+                                    void *stream);
+
+/*
  * HSS tree (pkg/src/hsseig/hss.py:151-214): nodes in the reference's postorder
  * numbering over a power-of-two leaf count.  Topology arrays are filled by the
  * host (hsseig_tree_layout); numeric slots by hsseig_hss_build_rand.

@@ -60,6 +60,9 @@ _SIGS = {
                                                c_vp, c_vp]),
     "hsseig_cauchy_sample_part": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_i64, c_i64,
                                                  c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "hsseig_cauchy_sample_part_peers": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_i64,
+                                                       c_i64, c_i64, c_vp, c_vp, c_i32, c_i64,
+                                                       c_vp, c_vp]),
     "hsseig_dnext": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "hsseig_loewner": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp,
                                       c_vp]),

@@ -361,6 +361,48 @@ __global__ void transpose_kernel(const double* __restrict__ in, int64_t ldi, int
   }
 }
 
+// Peer destinations of a fused gather: the reduced value of a row of this rank's block goes
+// straight to row (row0 + row) of every rank's full buffer (IPC-mapped over NVLink), so the
+// split-K reduction and the all-gather are one kernel; a system-scope fence publishes the
+// stores before the kernel retires (the host then synchronises and barriers the group).
+struct PeerOut {
+  const uint64_t* base;   // npeers device pointers (this rank's own buffer included)
+  int npeers;
+  int64_t row0, ld;
+};
+
+__device__ __forceinline__ void peer_store(const PeerOut& po, int64_t row, int col, double v) {
+  for (int q = 0; q < po.npeers; ++q)
+    reinterpret_cast<double*>(po.base[q])[(po.row0 + row) * po.ld + col] = v;
+}
+
+__global__ void splitk_reduce_peers_kernel(const double* __restrict__ part, int nsplit, int64_t k,
+                                           int w, int64_t ldp, PeerOut po) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < k * w) {
+    int64_t row = e / w;
+    int col = (int)(e % w);
+    double s = 0.0;
+    for (int t = 0; t < nsplit; ++t) s += part[(int64_t)t * k * ldp + row * ldp + col];
+    peer_store(po, row, col, s);
+  }
+  __threadfence_system();
+}
+
+__global__ void splitk_reduce_t_peers_kernel(const double* __restrict__ part, int nsplit,
+                                             int64_t nrows, int w, int64_t ldp, int64_t pstride,
+                                             PeerOut po) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nrows * w) {
+    const int c = (int)(e / nrows);
+    const int64_t row = e % nrows;
+    double acc = 0.0;
+    for (int p = 0; p < nsplit; ++p) acc += part[(int64_t)p * pstride + (int64_t)c * ldp + row];
+    peer_store(po, row, c, acc);
+  }
+  __threadfence_system();
+}
+
 // Z[row][c] = sum_p part[p][c][row], p ascending (fixed order)
 __global__ void splitk_reduce_t_kernel(const double* __restrict__ part, int nsplit, int64_t nrows,
                                        int w, int64_t ldp, int64_t pstride, double* __restrict__ Z,
@@ -446,7 +488,8 @@ __global__ void mat_jobs_kernel(TJob* __restrict__ jobs, int sy, int sz, int til
 
 static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom, int w, int64_t row0,
                              int64_t row1, double* Y, double* Z, int64_t ldy, double* work,
-                             cudaStream_t s) {
+                             cudaStream_t s, const PeerOut* peY = nullptr,
+                             const PeerOut* peZ = nullptr) {
   const int64_t k = g.k;
   const MatPlan p = mat_plan(k, w, row1 - row0);
   const int64_t nr = p.nrows;
@@ -494,6 +537,13 @@ static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom,
       return rc;
   }
   const unsigned rb = (unsigned)((nr * w + 255) / 256);
+  if (peY) {   // fused with the all-gather: rows land in every rank's full Y / Z
+    splitk_reduce_peers_kernel<<<rb, 256, 0, s>>>(pY, (int)p.sy, nr, w, p.ldp, *peY);
+    HSS_CHECK_LAUNCH();
+    splitk_reduce_t_peers_kernel<<<rb, 256, 0, s>>>(pZ, (int)p.sz, nr, w, p.nld, w * p.nld, *peZ);
+    HSS_CHECK_LAUNCH();
+    return HSSEIG_OK;
+  }
   splitk_reduce_kernel<<<rb, 256, 0, s>>>(pY, (int)p.sy, nr, w, p.ldp, Y, ldy);
   HSS_CHECK_LAUNCH();
   splitk_reduce_t_kernel<<<rb, 256, 0, s>>>(pZ, (int)p.sz, nr, w, p.nld, w * p.nld, Z, ldy);
@@ -567,6 +617,26 @@ extern "C" int hsseig_cauchy_sample_part(const hsseig_gen* gen, const double* om
     case 3: return launch_sample<TTile<4, 3, 2, 4, 8>>(g, omega, ldom, (int)w, row0, row1, Y, Z, ldy, work, s);
     default: return launch_sample<TTile<4, 4, 2, 4, 6>>(g, omega, ldom, (int)w, row0, row1, Y, Z, ldy, work, s);
   }
+}
+
+// Rows [row0, row1) of Y and Z written straight into every rank's full Y / Z (row-major,
+// leading dimension ldy): the split-K reductions store to the peers' IPC-mapped buffers.
+extern "C" int hsseig_cauchy_sample_part_peers(const hsseig_gen* gen, const double* omega,
+                                               int64_t ldom, int64_t w, int64_t row0, int64_t row1,
+                                               const uint64_t* Yp, const uint64_t* Zp,
+                                               int32_t npeers, int64_t ldy, double* work,
+                                               void* stream) {
+  if (!gen || w < 1 || w > 112 || ldom < w || ldy < w || row0 < 0 || row1 > gen->k ||
+      row0 > row1 || !Yp || !Zp || npeers < 1 || !work)
+    HSS_ARG_FAIL();
+  if ((reinterpret_cast<uintptr_t>(omega) & 15) || (ldom & 1) ||
+      (reinterpret_cast<uintptr_t>(work) & 15))
+    HSS_ARG_FAIL();
+  if (!mat_fits(gen->k, row1 - row0)) HSS_ARG_FAIL();   // the materialised path only
+  if (row0 == row1) return HSSEIG_OK;
+  const PeerOut py{Yp, npeers, row0, ldy}, pz{Zp, npeers, row0, ldy};
+  return launch_sample_mat(to_gen(gen), omega, ldom, (int)w, row0, row1, nullptr, nullptr, ldy,
+                           work, (cudaStream_t)stream, &py, &pz);
 }
 
 extern "C" int hsseig_cauchy_sample(const hsseig_gen* gen, const double* omega, int64_t ldom,

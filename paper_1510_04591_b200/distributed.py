@@ -58,6 +58,41 @@ def gather_rows(local, chunk, k, group=None):
     return torch.cat(parts)[:k]
 
 
+class PeerBuffers:
+    """Full-size float64 buffers that every rank of `group` stores into directly: each rank
+    allocates its own, shares them through CUDA IPC (torch's own handle export) and maps the
+    others', so a kernel can write its block of a result into all ranks' copies over
+    NVLink / NVSwitch (one process per GPU; on one device across processes in the tests).
+    `ptrs[b]` is the device array of the ranks' base pointers of buffer b (rank order)."""
+
+    def __init__(self, shapes, group=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.local = [torch.zeros(sh, dtype=torch.float64, device="cuda") for sh in shapes]
+        torch.cuda.synchronize()
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        handles = [None] * world
+        dist.all_gather_object(handles, [reduce_tensor(t) for t in self.local], group=group)
+        self.views, self.ptrs = [], []
+        for b in range(len(shapes)):
+            ts = []
+            for r in range(world):
+                if r == rank:
+                    ts.append(self.local[b])
+                else:
+                    fn, args = handles[r][b]
+                    ts.append(fn(*args))
+            self.views.append(ts)          # keeps the peers' mappings alive
+            self.ptrs.append(torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64,
+                                          device="cuda"))
+
+
+def peer_fence(group=None):
+    """Every rank's peer stores so far have landed: local stream drained, then a barrier."""
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)
+
+
 def rank_from(part, span, mu_h, eps, cap):
     """estimate_rank (hss.py:87-103) from host copies of the boundary gaps."""
     if part.n_leaves < 2:
@@ -125,9 +160,18 @@ class ShardedMerge:
                 w = r + cfg.oversample
                 if r >= 1 and w <= ops.max_width:
                     om = ops.omega(seed, k, w)
-                    Y_l, Z_l = ops.sample_part(gen, om, w, lo, hi)
-                    Y = gather_rows(Y_l, c, k, self.group)
-                    Z = gather_rows(Z_l, c, k, self.group)
+                    fused = getattr(ops, "sample_gather", None)
+                    YZ = fused(gen, om, w, lo, hi, self.group) if fused else None
+                    if YZ is not None:
+                        # sample rows stored straight into every rank's Y / Z (one kernel
+                        # for the split-K reduction and the all-gather), then one fence
+                        Y, Z = YZ
+                        info["sample_gather"] = "peer"
+                    else:
+                        info["sample_gather"] = "nccl"
+                        Y_l, Z_l = ops.sample_part(gen, om, w, lo, hi)
+                        Y = gather_rows(Y_l, c, k, self.group)
+                        Z = gather_rows(Z_l, c, k, self.group)
                     tree = ops.build(gen, part, w, om, Y, Z, self.group)
         if tree is not None and not ops.flagged(tree):
             info["used_hss"] = True
@@ -223,6 +267,9 @@ class GpuOps:
         self._trees = {}
         self._mwork = None
         self._swork = None
+        self._peer = None
+        self._peer_key = None
+        self._peer_n = 0
 
     def _s(self):
         return self.nat.stream_ptr()
@@ -306,6 +353,36 @@ class GpuOps:
                                                      nat.ptr(Z), ws, nat.ptr(self.sample_work),
                                                      self._s()), "cauchy_sample_part")
         return Y, Z
+
+    def sample_gather(self, gen, om, w, lo, hi, group=None):
+        """Y = C Omega, Z = C^T Omega on every rank with this rank's rows [lo, hi) computed
+        here and stored into all ranks' copies by the reduction kernels (CUDA IPC peers);
+        None when the fused path does not apply (one rank, HSSEIG_PEER=0, a panel above the
+        materialisation cap), and the caller all-gathers through NCCL instead."""
+        import os
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        if world < 2 or os.environ.get("HSSEIG_PEER", "1") == "0":
+            return None
+        nat = self.nat
+        k, ws = self.k, om.shape[1]
+        key = (k, ws, id(group))
+        if self._peer_key != key:
+            # two sets, alternating: a rank writes set n % 2 only after every rank passed
+            # the fence of call n - 1, i.e. finished reading set (n - 1) % 2 ... n - 2
+            self._peer = [PeerBuffers([(k, ws), (k, ws)], group) for _ in range(2)]
+            self._peer_key = key
+            self._peer_n = 0
+        pb = self._peer[self._peer_n % 2]
+        self._peer_n += 1
+        rc = self.lib.hsseig_cauchy_sample_part_peers(gen.gen, nat.ptr(om), ws, w, lo, hi,
+                                                      nat.ptr(pb.ptrs[0]), nat.ptr(pb.ptrs[1]),
+                                                      world, ws, nat.ptr(self.sample_work),
+                                                      self._s())
+        if rc == nat.HSSEIG_ERR_ARG:
+            return None
+        nat.check(rc, "cauchy_sample_part_peers")
+        peer_fence(group)
+        return pb.local[0], pb.local[1]
 
     def build(self, gen, part, w, om, Y, Z, group=None):
         """Construction; with several ranks each builds its subtrees below level log2(world),

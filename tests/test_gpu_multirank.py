@@ -45,6 +45,9 @@ def _worker(rank, world, port, out_path):
         X[r0:r1].contiguous(), seed=[0, 7])
     T = hb.gen_config5(1024, 4)
     res = adc_solve_distributed(T, hb.SolverConfig(rank_eps=1e-13), GpuOps(512))
+    # the sample rows went straight into both ranks' Y / Z (CUDA IPC peer stores fused in
+    # the split-K reduction), not through a separate all-gather
+    assert info.get("sample_gather") == "peer", info.get("sample_gather")
     outs = [None] * world
     dist.all_gather_object(outs, (out.cpu().numpy(), res.row0, res.row1, res.Q_rows.cpu().numpy(),
                                   out1.cpu().numpy(), bool(info1["used_hss"])))
