@@ -72,8 +72,18 @@ class PeerBuffers:
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
         handles = [None] * world
-        dist.all_gather_object(handles, [reduce_tensor(t) for t in self.local], group=group)
+        me = torch.cuda.current_device()
+        dist.all_gather_object(handles, (me, [reduce_tensor(t) for t in self.local]), group=group)
+        # every peer device must be reachable with loads / stores (NVLink P2P, or the same
+        # device when processes share one in the tests); otherwise the caller falls back
+        ok = all(dv == me or torch.cuda.can_device_access_peer(me, dv) for dv, _ in handles)
+        oks = [None] * world
+        dist.all_gather_object(oks, ok, group=group)
+        self.ok = all(oks)                 # one decision for the whole group
+        handles = [h for _, h in handles]
         self.views, self.ptrs = [], []
+        if not self.ok:
+            return
         for b in range(len(shapes)):
             ts = []
             for r in range(world):
@@ -373,6 +383,8 @@ class GpuOps:
             self._peer_key = key
             self._peer_n = 0
         pb = self._peer[self._peer_n % 2]
+        if not pb.ok:
+            return None
         self._peer_n += 1
         rc = self.lib.hsseig_cauchy_sample_part_peers(gen.gen, nat.ptr(om), ws, w, lo, hi,
                                                       nat.ptr(pb.ptrs[0]), nat.ptr(pb.ptrs[1]),

@@ -5,7 +5,7 @@ import paper_1510_04591_b200.solver as S
 import inspect, textwrap, collections
 src = inspect.getsource(S.solve_subtree)
 marks = [
- ("if pending is not None:", "setup"),
+ ("src_rows = rows_h", "setup"),
  ("bk = np.ascontiguousarray(b[sp_m - 1], dtype=np.float64)", "zrows_sync"),
  ("wd = np.empty(nm, dtype=np.int64)", "deflate"),
  ("W = torch.empty(max(int(woff[-1]), 2), **f64)", "index_pack"),
