@@ -293,7 +293,15 @@ __device__ __forceinline__ void loewner_rows(
     di[r] = (i0 + r < iend) ? __ldg(d + i0 + r) : 0.0;
     pr[r] = 1.0;
   }
-  for (int64_t j = lane; j < k; j += 32) {
+  // three ranges so the stable-gap branch is uniform: j < i0 (every row i > j: the
+  // (d_i - d_{j+1}) + mu_j form), the band [i0, i0 + R) and j >= i0 + R (i <= j)
+  const int64_t jb = min(i0, k), je = min(i0 + R, k);
+  for (int64_t j = lane; j < jb; j += 32) {
+    const double dj = __ldg(d + j), dnj = __ldg(dn + j), mj = __ldg(mu + j);
+#pragma unroll
+    for (int r = 0; r < R; ++r) pr[r] *= -((di[r] - dnj) + mj) * rcp_c3(dj - di[r]);
+  }
+  for (int64_t j = jb + lane; j < je; j += 32) {
     const double dj = __ldg(d + j), dnj = __ldg(dn + j), gj = __ldg(gam + j), mj = __ldg(mu + j);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -303,6 +311,11 @@ __device__ __forceinline__ void loewner_rows(
       const double den = dj - di[r];
       pr[r] *= num * rcp_c3(den);
     }
+  }
+  for (int64_t j = je + lane; j < k; j += 32) {
+    const double dj = __ldg(d + j), gj = __ldg(gam + j);
+#pragma unroll
+    for (int r = 0; r < R; ++r) pr[r] *= -((di[r] - dj) - gj) * rcp_c3(dj - di[r]);
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -347,12 +360,31 @@ __device__ __forceinline__ void normalizer_cols(
     mj[r] = __ldg(mu + j);
     s[r] = 0.0;
   }
-  for (int64_t i = lane; i < k; i += 32) {
+  // rows i <= j0 use (d_i - d_j) - gam_j for every column of the warp, rows i > j0 + R - 1
+  // the (d_i - d_{j+1}) + mu_j form; only the band between needs the branch
+  const int64_t ib = min(j0 + 1, k), ie = min(j0 + R, k);
+  for (int64_t i = lane; i < ib; i += 32) {
+    const double di = __ldg(d + i), zi = __ldg(zh + i);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double q = zi * rcp_c3((di - dj[r]) - gj[r]);
+      s[r] = fma(q, q, s[r]);
+    }
+  }
+  for (int64_t i = ib + lane; i < ie; i += 32) {
     const double di = __ldg(d + i), zi = __ldg(zh + i);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       double g = stable_gap(i, j0 + r, di, dj[r], dnj[r], gj[r], mj[r]);
       double q = zi * rcp_c3(g);
+      s[r] = fma(q, q, s[r]);
+    }
+  }
+  for (int64_t i = ie + lane; i < k; i += 32) {
+    const double di = __ldg(d + i), zi = __ldg(zh + i);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double q = zi * rcp_c3((di - dnj[r]) + mj[r]);
       s[r] = fma(q, q, s[r]);
     }
   }
