@@ -22,22 +22,40 @@ namespace hsseig {
 // leaf level: D = C(t,t);  Phi = Y_t - D Omega_t (side 0);  Theta = Z_t - D^T Omega_t (side 1)
 // (hss.py:261-268)
 // ---------------------------------------------------------------------------
+// shared-memory strides that keep the DMMA fragment loads conflict-free: A (D chunk) rows
+// at a stride of 4 (mod 8) doubles, B (Omega_t) rows at 8 or 24 (mod 32)
+__host__ __device__ __forceinline__ int leaf_kp(int mmax) { return (mmax + 3) / 4 * 4; }
+__host__ __device__ __forceinline__ int leaf_sd(int mmax) {
+  const int kp = leaf_kp(mmax);
+  return kp % 8 == 0 ? kp + 4 : kp;
+}
+__host__ __device__ __forceinline__ int leaf_so(int w) {
+  int s = (w + 7) / 8 * 8;
+  while (s % 32 != 8 && s % 32 != 24) s += 8;
+  return s;
+}
 __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
                                                         const double* __restrict__ om,
                                                         int64_t ldom,
                                                         const double* __restrict__ Y,
                                                         const double* __restrict__ Z,
                                                         int64_t ldy, int j0) {
+  // D Omega_t on the DMMA pipe: 16-row chunks of D generated in shared memory (A operand,
+  // row stride SD = 4 mod 8), Omega_t resident (B operand, row stride SO = 8|24 mod 32),
+  // 2 x ceil(w/8) output fragments of 8 x 8 spread over the 8 warps, K padded to 4 with zeros
   extern __shared__ __align__(16) double sm[];
   const int j = j0 + blockIdx.x, side = blockIdx.y, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int node = T.lnodes[(1 << T.depth) - 1 + j];
   const int lo = T.lo[node], m = T.hi[node] - lo, w = T.w;
   constexpr int RA = 16;
-  double* sOm = sm;                  // m x w
-  double* sD = sm + (size_t)T.mmax * w;  // RA x m chunk
-  for (int e = tid; e < m * w; e += blockDim.x) {
-    int b = e / w, c = e % w;
-    sOm[e] = om[(int64_t)(lo + b) * ldom + c];
+  const int KP = leaf_kp(T.mmax), SO = leaf_so(w), SD = leaf_sd(T.mmax);
+  const int kp = (m + 3) / 4 * 4, nf = (w + 7) / 8;
+  double* sOm = sm;                       // KP x SO (rows >= m and columns >= w zero)
+  double* sD = sm + (size_t)KP * SO;      // RA x SD chunk (columns >= m zero)
+  for (int e = tid; e < kp * SO; e += blockDim.x) {
+    const int b = e / SO, c = e % SO;
+    sOm[e] = (b < m && c < w) ? om[(int64_t)(lo + b) * ldom + c] : 0.0;
   }
   const double* src = side == 0 ? Y : Z;
   double* Mo = T.M + (size_t)(2 * j + side) * T.pmax * T.ws;
@@ -50,22 +68,33 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
       if (a < 0 || a >= m || b >= m) Dslot[e] = 0.0;
     }
   }
+  const int gr = lane >> 2, gc = lane & 3;
   for (int a0 = 0; a0 < m; a0 += RA) {
     const int na = min(RA, m - a0);
     __syncthreads();
-    for (int e = tid; e < na * m; e += blockDim.x) {
-      int aa = e / m, b = e % m;
-      double val = side == 0 ? g.entry(lo + a0 + aa, lo + b) : g.entry(lo + b, lo + a0 + aa);
-      sD[aa * m + b] = val;
-      if (side == 0) Dslot[(size_t)(a0 + aa + 1) * T.dld + b] = val;
+    for (int e = tid; e < RA * kp; e += blockDim.x) {
+      const int aa = e / kp, b = e % kp;
+      double val = 0.0;
+      if (aa < na && b < m) {
+        val = side == 0 ? g.entry(lo + a0 + aa, lo + b) : g.entry(lo + b, lo + a0 + aa);
+        if (side == 0) Dslot[(size_t)(a0 + aa + 1) * T.dld + b] = val;
+      }
+      sD[aa * SD + b] = val;
     }
     __syncthreads();
-    for (int e = tid; e < na * w; e += blockDim.x) {
-      int aa = e / w, c = e % w;
-      double s = 0.0;
-      const double* drow = sD + aa * m;
-      for (int b = 0; b < m; ++b) s = fma(drow[b], sOm[b * w + c], s);
-      Mo[(size_t)(a0 + aa) * T.ws + c] = src[(int64_t)(lo + a0 + aa) * ldy + c] - s;
+    for (int f = warp; f < 2 * nf; f += 8) {     // fragment (mi, ni) = (f / nf, f % nf)
+      const int mi = f / nf, ni = f % nf;
+      double c0 = 0.0, c1 = 0.0;
+      const double* arow = sD + (mi * 8 + gr) * SD + gc;
+      const double* bcol = sOm + gc * SO + ni * 8 + gr;
+      for (int k0 = 0; k0 < kp; k0 += 4) dmma_8x8x4(c0, c1, arow[k0], bcol[k0 * SO]);
+      const int r = mi * 8 + gr, c = ni * 8 + 2 * gc;
+      if (r < na) {
+        const int64_t yr = (int64_t)(lo + a0 + r) * ldy;
+        double* mo = Mo + (size_t)(a0 + r) * T.ws;
+        if (c < w) mo[c] = src[yr + c] - c0;
+        if (c + 1 < w) mo[c + 1] = src[yr + c + 1] - c1;
+      }
     }
   }
 }
@@ -770,7 +799,8 @@ static int build_levels(const hsseig_gen* gen, const double* omega, int64_t ldom
   g.d = gen->d; g.dnext = gen->dnext; g.gam = gen->gamma; g.mu = gen->mu; g.zhat = gen->zhat;
   g.v = gen->v; g.k = gen->k;
   TreeDev T = to_dev(tree);
-  const size_t smem_leaf = sizeof(double) * ((size_t)T.mmax * T.w + 16 * (size_t)T.mmax);
+  const size_t smem_leaf = sizeof(double) * ((size_t)leaf_kp(T.mmax) * leaf_so(T.w) +
+                                             16 * (size_t)leaf_sd(T.mmax));
   if (T.pmax > 4096) HSS_ARG_FAIL();
   const size_t smem_id = sizeof(double) * ((size_t)T.pmax * (T.w | 1) + 2 * T.pmax + T.w + 1 + 32) +
                          sizeof(int) * 2 * T.pmax + 64;
