@@ -132,8 +132,7 @@ int launch_genB(const CauchyGen& g, const TreeDev& T, int level, int j0, int cnt
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level, int j0) {
   // one CTA per (node, side, half): rows [off, off + nrow) of Phi (side 0) or Theta (side 1).
-  // B block and sibling compression are staged in shared memory; every thread carries 4
-  // independent output columns so the contraction is not latency bound.
+  // B block and sibling compression are staged in shared memory.
   // blockIdx.z = half + 2 * (row chunk): upper levels have few nodes, so each half's rows
   // are split over gridDim.z / 2 CTAs (latency-bound otherwise)
   extern __shared__ __align__(16) double fs[];
@@ -153,37 +152,36 @@ __global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level, i
   const double* comp = (side == 0 ? T.ycomp : T.zcomp) + slot_ww(T, sib);
   const double* sel = (side == 0 ? T.psel : T.tsel) + slot_ww(T, me);
   const double* Bb = T.B + slot_ww(T, side == 0 ? me : sib);
-  const int SK = nk | 1;                 // odd stride for the B tile rows
-  double* sBt = fs;                      // nrow x nk  (B_me, or B_sib^T)
-  double* sCm = fs + (size_t)w * SK;     // nk x w
-  for (int e = tid; e < nrow * nk; e += blockDim.x) {
-    const int r = e / nk, t = e % nk;
-    sBt[r * SK + t] = side == 0 ? Bb[(size_t)(r0 + r) * ws + t] : Bb[(size_t)t * ws + r0 + r];
+  // B_me rows (A operand, stride SA = 4 mod 8) times the sibling compression (B operand,
+  // stride SO = 8|24 mod 32) on the DMMA pipe, K padded to 4 and rows to 8 with zeros
+  const int kpm = (w + 3) / 4 * 4, SA = kpm % 8 == 0 ? kpm + 4 : kpm, SO = leaf_so(w);
+  const int kp = (nk + 3) / 4 * 4, mr = (nrow + 7) / 8 * 8, nf = (w + 7) / 8;
+  double* sBt = fs;                          // mr x SA  (B_me, or B_sib^T)
+  double* sCm = fs + (size_t)((w + 7) / 8 * 8) * SA;   // kpm x SO
+  for (int e = tid; e < mr * kp; e += blockDim.x) {
+    const int r = e / kp, t = e % kp;
+    sBt[r * SA + t] = (r < nrow && t < nk)
+                          ? (side == 0 ? Bb[(size_t)(r0 + r) * ws + t] : Bb[(size_t)t * ws + r0 + r])
+                          : 0.0;
   }
-  for (int e = tid; e < nk * w; e += blockDim.x) {
-    const int t = e / w, c = e % w;
-    sCm[e] = comp[(size_t)t * ws + c];
+  for (int e = tid; e < kp * SO; e += blockDim.x) {
+    const int t = e / SO, c = e % SO;
+    sCm[e] = (t < nk && c < w) ? comp[(size_t)t * ws + c] : 0.0;
   }
   __syncthreads();
-  const int cq = (w + 3) / 4;            // columns per quarter
-  for (int e = tid; e < nrow * cq; e += blockDim.x) {
-    const int r = e / cq, c0 = e % cq;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    const double* br = sBt + r * SK;
-#pragma unroll 2
-    for (int t = 0; t < nk; ++t) {
-      const double bv = br[t];
-      const double* cr = sCm + t * w;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = c0 + q * cq;
-        if (c < w) acc[q] = fma(bv, cr[c], acc[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c = c0 + q * cq;
-      if (c < w) Mo[(size_t)(off + r) * ws + c] = sel[(size_t)(r0 + r) * ws + c] - acc[q];
+  const int lane = tid & 31, warp = tid >> 5, gr = lane >> 2, gc = lane & 3;
+  for (int f = warp; f < (mr / 8) * nf; f += blockDim.x >> 5) {
+    const int mi = f / nf, ni = f % nf;
+    double c0 = 0.0, c1 = 0.0;
+    const double* arow = sBt + (mi * 8 + gr) * SA + gc;
+    const double* bcol = sCm + gc * SO + ni * 8 + gr;
+    for (int k0 = 0; k0 < kp; k0 += 4) dmma_8x8x4(c0, c1, arow[k0], bcol[k0 * SO]);
+    const int r = mi * 8 + gr, c = ni * 8 + 2 * gc;
+    if (r < nrow) {
+      const double* sr = sel + (size_t)(r0 + r) * ws;
+      double* mo = Mo + (size_t)(off + r) * ws;
+      if (c < w) mo[c] = sr[c] - c0;
+      if (c + 1 < w) mo[c + 1] = sr[c + 1] - c1;
     }
   }
 }
@@ -804,7 +802,9 @@ static int build_levels(const hsseig_gen* gen, const double* omega, int64_t ldom
   if (T.pmax > 4096) HSS_ARG_FAIL();
   const size_t smem_id = sizeof(double) * ((size_t)T.pmax * (T.w | 1) + 2 * T.pmax + T.w + 1 + 32) +
                          sizeof(int) * 2 * T.pmax + 64;
-  const size_t smem_form = sizeof(double) * ((size_t)T.w * ((T.w | 1) + T.w) + 8);
+  const int kpm = (T.w + 3) / 4 * 4;
+  const size_t smem_form = sizeof(double) * ((size_t)((T.w + 7) / 8 * 8) * (kpm % 8 == 0 ? kpm + 4 : kpm) +
+                                             (size_t)kpm * leaf_so(T.w) + 8);
   if (smem_leaf > 227 * 1024 || smem_id > 227 * 1024 || smem_form > 227 * 1024) HSS_ARG_FAIL();
   cudaFuncSetAttribute(inner_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_form);
   cudaFuncSetAttribute(leaf_form_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_leaf);
