@@ -71,30 +71,38 @@ class PeerBuffers:
         torch.cuda.synchronize()
         world = dist.get_world_size(group)
         rank = dist.get_rank(group)
-        handles = [None] * world
         me = torch.cuda.current_device()
-        dist.all_gather_object(handles, (me, [reduce_tensor(t) for t in self.local]), group=group)
-        # every peer device must be reachable with loads / stores (NVLink P2P, or the same
-        # device when processes share one in the tests); otherwise the caller falls back
-        ok = all(dv == me or torch.cuda.can_device_access_peer(me, dv) for dv, _ in handles)
+        self.views, self.ptrs = [], []
+        # every step below is agreed on by the whole group, so a rank that cannot export or
+        # map a peer buffer makes all ranks fall back to the NCCL gather together
+        try:
+            mine = (me, [reduce_tensor(t) for t in self.local])
+        except Exception:          # noqa: BLE001 (no CUDA IPC here)
+            mine = None
+        handles = [None] * world
+        dist.all_gather_object(handles, mine, group=group)
+        ok = all(h is not None for h in handles) and all(
+            dv == me or torch.cuda.can_device_access_peer(me, dv) for dv, _ in handles)
+        if ok:
+            try:
+                for b in range(len(shapes)):
+                    ts = []
+                    for r in range(world):
+                        if r == rank:
+                            ts.append(self.local[b])
+                        else:
+                            fn, args = handles[r][1][b]
+                            ts.append(fn(*args))
+                    self.views.append(ts)          # keeps the peers' mappings alive
+                    self.ptrs.append(torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64,
+                                                  device="cuda"))
+            except Exception:      # noqa: BLE001 (a peer mapping failed)
+                ok = False
         oks = [None] * world
         dist.all_gather_object(oks, ok, group=group)
         self.ok = all(oks)                 # one decision for the whole group
-        handles = [h for _, h in handles]
-        self.views, self.ptrs = [], []
         if not self.ok:
-            return
-        for b in range(len(shapes)):
-            ts = []
-            for r in range(world):
-                if r == rank:
-                    ts.append(self.local[b])
-                else:
-                    fn, args = handles[r][b]
-                    ts.append(fn(*args))
-            self.views.append(ts)          # keeps the peers' mappings alive
-            self.ptrs.append(torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64,
-                                          device="cuda"))
+            self.views, self.ptrs = [], []
 
 
 def peer_fence(group=None):
