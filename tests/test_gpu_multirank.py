@@ -22,7 +22,8 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, peer="1"):
+    os.environ["HSSEIG_PEER"] = peer
     import sys
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -47,7 +48,7 @@ def _worker(rank, world, port, out_path):
     res = adc_solve_distributed(T, hb.SolverConfig(rank_eps=1e-13), GpuOps(512))
     # the sample rows went straight into both ranks' Y / Z (CUDA IPC peer stores fused in
     # the split-K reduction), not through a separate all-gather
-    assert info.get("sample_gather") == "peer", info.get("sample_gather")
+    assert info.get("sample_gather") == ("peer" if peer == "1" else "nccl"), info.get("sample_gather")
     outs = [None] * world
     dist.all_gather_object(outs, (out.cpu().numpy(), res.row0, res.row1, res.Q_rows.cpu().numpy(),
                                   out1.cpu().numpy(), bool(info1["used_hss"])))
@@ -61,11 +62,14 @@ def _worker(rank, world, port, out_path):
     dist.destroy_process_group()
 
 
-def test_two_ranks_match_single_gpu(tmp_path):
+@pytest.mark.parametrize("peer", ["1", "0"])
+def test_two_ranks_match_single_gpu(tmp_path, peer):
+    # peer = "1": sample rows stored into both ranks' Y / Z by the reduction kernels (CUDA
+    # IPC); "0": the NCCL-style all-gather fallback (gloo here)
     import paper_1510_04591_b200 as hb
     from helpers import config4_system
     out_path = str(tmp_path / "mr.npz")
-    mp.spawn(_worker, args=(2, _port(), out_path), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _port(), out_path, peer), nprocs=2, join=True)
     r = np.load(out_path)
     n = 2048
     d, u, rho = config4_system(n, 5)
