@@ -325,7 +325,8 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
     for j in np.flatnonzero(~leaf_a).tolist():
         is_left[left_a[j]] = True
         has_parent[left_a[j]] = has_parent[right_a[j]] = True
-    pending = None      # (event, pinned rows, node ids, offsets, sizes) of the last depth
+    pending = None      # (event, pinned rows) of the last depth's early row gather
+    pending_records = []
     # per node: device address of its Q block (row-major n x n) and the buffer holding it
     qptr = np.zeros(len(tab), dtype=np.uint64)
     qptr[leaf_idx] = np.uint64(Qbase.data_ptr()) + (8 * lqoff[:-1]).astype(np.uint64)
@@ -572,7 +573,11 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         live[depth] = A
         lam_all[rows] = lam_out
         qptr[ms] = np.uint64(A.data_ptr()) + (8 * ooff[:-1]).astype(np.uint64)
-        # records and flop counts (reference conventions, dc.py:236-247)
+        # records and flop counts are built after the last depth is queued (the host is
+        # otherwise the bottleneck of the deep, small-merge depths)
+        pending_records.append((ms, segs, nv, kept, rho_eff, seg_iters, hss_m))
+    # records and flop counts (reference conventions, dc.py:236-247)
+    for ms, segs, nv, kept, rho_eff, seg_iters, hss_m in pending_records:
         for q, m in enumerate(segs.tolist()):
             nd = tab[ms[m]]
             n, k = int(nv[m]), int(kept[m])
