@@ -377,7 +377,6 @@ def run_ours(args):
     else:
         # row-block sharded merge: index-sharded roots / weights / samples + NCCL all-gathers
         from paper_1510_04591_b200.distributed import GpuOps, ShardedMerge
-        from paper_1510_04591_b200.hss import _construct_flops, mult_flops
         sm = ShardedMerge(n, cfg, GpuOps(n))
 
         def step(Xin, out, dd=d_dev, uu=u_dev):
@@ -389,16 +388,17 @@ def run_ours(args):
             out.copy_(res)
             torch.cuda.synchronize()
             tree = info["tree"]
-            fl_con = _construct_flops(tree, n, tree.w) if tree is not None else 0
-            fl_mult = mult_flops(tree, n) if info["used_hss"] else 0
-            fl_loc = mult_flops(tree, Xin.shape[0]) if info["used_hss"] else 0
+            fl = dict(info["flops"])        # reference conventions over all n rows
+            fl["hss_mult_local"] = (sm.ops.mult_flops(tree, Xin.shape[0])
+                                    if info["used_hss"] else 0)
             ev = info.get("multiply_events")
             mult = ev[0].elapsed_time(ev[1]) if ev else float("nan")
             return {"ms": {"total": e0.elapsed_time(e1), "multiply": mult},
-                    "flops": {"secular": info["flops_secular"], "hss_construct": fl_con,
-                              "hss_mult_local": fl_loc, "hss_mult": fl_mult, "update_dense": 0},
+                    "flops": fl,
                     "sample_gather": info.get("sample_gather"),
-                    "flops_total_fullP": info["flops_secular"] + fl_con + fl_mult,
+                    # dense work counted when the merge fell back (dc.py:132-138)
+                    "flops_total_fullP": (fl["secular"] + fl["hss_construct"] + fl["hss_mult"]
+                                          + fl["update_dense"]),
                     "r_used": info["r_used"], "used_hss": info["used_hss"]}
 
     out = torch.empty_like(Qloc)

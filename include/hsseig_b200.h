@@ -138,6 +138,10 @@ int hsseig_cauchy_sample_part_peers(const hsseig_gen *gen, const double *omega, 
                                     int64_t w, int64_t row0, int64_t row1, const uint64_t *Yp,
                                     const uint64_t *Zp, int32_t npeers, int64_t ldy, double *work,
                                     void *stream);
+/* 1 when hsseig_cauchy_sample_part_peers accepts a shard of `nrows` rows (order k, width w),
+ * else 0.  Monotone in nrows: ranks evaluate it on the padded shard size they all share, so
+ * every rank of a group takes the same path (peer stores or the NCCL gather). */
+int hsseig_sample_peers_fits(int64_t k, int64_t nrows, int64_t w);
 
 /*
  * HSS tree (pkg/src/hsseig/hss.py:151-214): nodes in the reference's postorder
@@ -289,14 +293,17 @@ int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, 
 /*
  * Base case for every leaf of the recursion at once: implicit QL with Wilkinson shift
  * (tql2, pkg/src/hsseig/_kernels.pyx:352-411) followed by the ascending stable sort of
- * dc.py:118-129.  Matrix m has order off[m+1]-off[m] <= 32, diagonal a[off[m]..] and
- * off-diagonal b[off[m]-m..] (n-1 entries); lam[off[m]..] receives its eigenvalues and
- * Q[qoff[m]..] its n x n row-major eigenvectors.  status[m] = 1 + l if eigenvalue l
- * stalls after max_iter sweeps (BaseCaseError), else untouched.
+ * dc.py:118-129.  Matrix m has order off[m+1]-off[m] <= nmax <= 160 (a warp per matrix when
+ * nmax <= 32, a 128-thread block per matrix above), diagonal a[off[m]..] and off-diagonal
+ * b[off[m]-m..] (n-1 entries); lam[off[m]..] receives its eigenvalues and Q[qoff[m]..] its
+ * n x n row-major eigenvectors.  status[m] = 1 + l if eigenvalue l stalls after max_iter
+ * sweeps (BaseCaseError), else untouched.  flags bit 0: Q holds the initial accumulator Z
+ * (in/out, the kernel contract tql2(d, e, Z)); bit 1: leave lam / Q in QL order (no sort).
+ * nmax above 160 (the reference accepts any base_size >= 3) is HSSEIG_ERR_ARG.
  */
 int hsseig_tql2_batched(const double *a, const double *b, const int64_t *off, int64_t nmat,
-                        int max_iter, double *lam, double *Q, const int64_t *qoff,
-                        int32_t *status, void *stream);
+                        int nmax, int max_iter, double *lam, double *Q, const int64_t *qoff,
+                        int32_t *status, int flags, void *stream);
 /*
  * Host deflation of the merged system (pkg/src/hsseig/secular.py:91-156): returns k;
  * d_out/z_out/perm hold the kept system then the deflated poles; rotations (ri, rj, rc,

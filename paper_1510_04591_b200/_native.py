@@ -63,6 +63,7 @@ _SIGS = {
     "hsseig_cauchy_sample_part_peers": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_i64,
                                                        c_i64, c_i64, c_vp, c_vp, c_i32, c_i64,
                                                        c_vp, c_vp]),
+    "hsseig_sample_peers_fits": (ctypes.c_int, [c_i64, c_i64, c_i64]),
     "hsseig_dnext": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "hsseig_loewner": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp,
                                       c_vp]),
@@ -105,8 +106,8 @@ _SIGS = {
     "hsseig_pcg64_normals": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp,
                                             c_vp, c_i64, c_vp]),
-    "hsseig_tql2_batched": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, ctypes.c_int, c_vp, c_vp, c_vp,
-                                           c_vp, c_vp]),
+    "hsseig_tql2_batched": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, ctypes.c_int, ctypes.c_int,
+                                           c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp]),
     "hsseig_deflate": (c_i64, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                c_vp, c_vp]),
     "hsseig_deflate_tol": (c_i64, [c_vp, c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp, c_vp,

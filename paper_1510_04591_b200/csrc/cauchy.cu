@@ -639,6 +639,13 @@ extern "C" int hsseig_cauchy_sample_part_peers(const hsseig_gen* gen, const doub
                            work, (cudaStream_t)stream, &py, &pz);
 }
 
+// Whether hsseig_cauchy_sample_part_peers takes a row range of `nrows` rows of an order-k
+// system at sample width w.  Monotone in nrows, so ranks that test the padded shard size they
+// all share reach the same decision before anything is launched.
+extern "C" int hsseig_sample_peers_fits(int64_t k, int64_t nrows, int64_t w) {
+  return (k >= 1 && nrows >= 0 && nrows <= k && w >= 1 && w <= 112 && mat_fits(k, nrows)) ? 1 : 0;
+}
+
 extern "C" int hsseig_cauchy_sample(const hsseig_gen* gen, const double* omega, int64_t ldom,
                                     int64_t w, double* Y, double* Z, int64_t ldy, double* work,
                                     void* stream) {

@@ -61,32 +61,50 @@ bool upload_async(int nparts, void* const* dst, const void* const* src, const si
 }
 
 // ---------------------------------------------------------------------------
-// batched implicit QL with Wilkinson shift, one warp per tridiagonal (n <= 32);
-// lane r owns row r of the rotation accumulator.  Scalar recurrences run redundantly
-// in every lane on shared d/e (identical values), rounding kept IEEE (no FMA
-// contraction) like the reference's C loop.
+// batched implicit QL with Wilkinson shift (tql2, _kernels.pyx:352-411).  A group of GROUP
+// threads owns one tridiagonal of order <= NMAX: a warp per matrix (4 per block) for the
+// usual base cases (n <= 32), a whole 128-thread block for base sizes up to kQLBig.  Thread
+// t owns rows t, t + GROUP, ... of the rotation accumulator.  Scalar recurrences run
+// redundantly in every thread on shared d/e (identical values, so every branch is uniform
+// across the group), rounding kept IEEE (no FMA contraction) like the reference's C loop.
+// flags: kQLInit = Q holds the initial accumulator (the kernel contract's in/out Z),
+//        kQLUnsorted = leave d / Z in QL order (the contract); default = ascending stable
+//        sort of dc.py:127 with the identity as the initial accumulator.
 // ---------------------------------------------------------------------------
 constexpr int kQLMax = 32;
+constexpr int kQLBig = 160;
+constexpr int kQLInit = 1, kQLUnsorted = 2;
 
+template <int NMAX, int GROUP>
+__device__ __forceinline__ void ql_sync() {
+  if (GROUP == 32) __syncwarp(); else __syncthreads();
+}
+
+template <int NMAX, int GROUP>
 __global__ void tql2_batched_kernel(const double* __restrict__ a, const double* __restrict__ b,
                                     const int64_t* __restrict__ off, int64_t nmat, int max_iter,
                                     double* __restrict__ lam, double* __restrict__ Q,
-                                    const int64_t* __restrict__ qoff, int32_t* __restrict__ status) {
-  __shared__ double sd[4][kQLMax], se[4][kQLMax + 1], sz[4][kQLMax][kQLMax + 1];
-  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m = (int64_t)blockIdx.x * 4 + wl;
-  if (m >= nmat) return;
+                                    const int64_t* __restrict__ qoff, int32_t* __restrict__ status,
+                                    int flags) {
+  constexpr int PER = 128 / GROUP;            // matrices per block
+  extern __shared__ double ql_smem[];
+  const int wl = threadIdx.x / GROUP, lane = threadIdx.x % GROUP;
+  const int64_t m = (int64_t)blockIdx.x * PER + wl;
+  if (m >= nmat) return;                      // uniform over the group
+  double* d = ql_smem + (size_t)wl * (NMAX + NMAX + 1 + NMAX * (NMAX + 1));
+  double* e = d + NMAX;
+  double* Z = e + NMAX + 1;                   // Z[row * (NMAX + 1) + col]
+  constexpr int LDZ = NMAX + 1;
   const int64_t o = off[m];
   const int n = (int)(off[m + 1] - o);
-  double* d = sd[wl];
-  double* e = se[wl];
-  double(*Z)[kQLMax + 1] = sz[wl];
-  if (lane < n) {
-    d[lane] = a[o + lane];
-    e[lane] = (lane + 1 < n) ? b[o - m + lane] : 0.0;   // b has n-1 entries per matrix
-    for (int c = 0; c < n; ++c) Z[lane][c] = (lane == c) ? 1.0 : 0.0;
+  double* q = Q + qoff[m];
+  for (int r = lane; r < n; r += GROUP) {
+    d[r] = a[o + r];
+    e[r] = (r + 1 < n) ? b[o - m + r] : 0.0;   // b has n-1 entries per matrix
+    for (int c = 0; c < n; ++c)
+      Z[r * LDZ + c] = (flags & kQLInit) ? q[(int64_t)r * n + c] : ((r == c) ? 1.0 : 0.0);
   }
-  __syncwarp();
+  ql_sync<NMAX, GROUP>();
   int fail = 0;
   if (n > 1) {
     for (int l = 0; l < n && !fail; ++l) {
@@ -108,15 +126,15 @@ __global__ void tql2_batched_kernel(const double* __restrict__ a, const double* 
           const double f = __dmul_rn(s, e[i]);
           const double bb = __dmul_rn(c, e[i]);
           r = hypot(f, g);
-          __syncwarp();
+          ql_sync<NMAX, GROUP>();
           if (lane == 0) e[i + 1] = r;
-          __syncwarp();
+          ql_sync<NMAX, GROUP>();
           if (r == 0.0) {
             if (lane == 0) {
               d[i + 1] = __dsub_rn(d[i + 1], p);
               e[mm] = 0.0;
             }
-            __syncwarp();
+            ql_sync<NMAX, GROUP>();
             clean = false;
             break;
           }
@@ -125,39 +143,58 @@ __global__ void tql2_batched_kernel(const double* __restrict__ a, const double* 
           g = __dsub_rn(d[i + 1], p);
           r = __dadd_rn(__dmul_rn(__dsub_rn(d[i], g), s), __dmul_rn(__dmul_rn(2.0, c), bb));
           p = __dmul_rn(s, r);
-          __syncwarp();
+          ql_sync<NMAX, GROUP>();
           if (lane == 0) d[i + 1] = __dadd_rn(g, p);
           g = __dsub_rn(__dmul_rn(c, r), bb);
-          if (lane < n) {
-            const double zi = Z[lane][i], zi1 = Z[lane][i + 1];
-            Z[lane][i + 1] = __dadd_rn(__dmul_rn(s, zi), __dmul_rn(c, zi1));
-            Z[lane][i] = __dsub_rn(__dmul_rn(c, zi), __dmul_rn(s, zi1));
+          for (int row = lane; row < n; row += GROUP) {
+            double* zr = Z + row * LDZ;
+            const double zi = zr[i], zi1 = zr[i + 1];
+            zr[i + 1] = __dadd_rn(__dmul_rn(s, zi), __dmul_rn(c, zi1));
+            zr[i] = __dsub_rn(__dmul_rn(c, zi), __dmul_rn(s, zi1));
           }
-          __syncwarp();
+          ql_sync<NMAX, GROUP>();
         }
         if (clean) {
-          __syncwarp();
+          ql_sync<NMAX, GROUP>();
           if (lane == 0) {
             d[l] = __dsub_rn(d[l], p);
             e[l] = g;
             e[mm] = 0.0;
           }
-          __syncwarp();
+          ql_sync<NMAX, GROUP>();
         }
       }
     }
   }
-  __syncwarp();
-  // ascending order, stable (np.argsort kind="stable", dc.py:127)
-  if (lane < n) {
-    const double v = d[lane];
-    int pos = 0;
-    for (int j = 0; j < n; ++j) pos += (d[j] < v) || (d[j] == v && j < lane);
+  ql_sync<NMAX, GROUP>();
+  // ascending order, stable (np.argsort kind="stable", dc.py:127), unless the caller sorts
+  for (int col = lane; col < n; col += GROUP) {
+    const double v = d[col];
+    int pos = col;
+    if (!(flags & kQLUnsorted)) {
+      pos = 0;
+      for (int j = 0; j < n; ++j) pos += (d[j] < v) || (d[j] == v && j < col);
+    }
     lam[o + pos] = v;
-    double* q = Q + qoff[m];
-    for (int row = 0; row < n; ++row) q[(int64_t)row * n + pos] = Z[row][lane];
+    for (int row = 0; row < n; ++row) q[(int64_t)row * n + pos] = Z[row * LDZ + col];
   }
   if (lane == 0 && fail) status[m] = fail;
+}
+
+template <int NMAX, int GROUP>
+static int launch_tql2(const double* a, const double* b, const int64_t* off, int64_t nmat,
+                       int max_iter, double* lam, double* Q, const int64_t* qoff, int32_t* status,
+                       int flags, cudaStream_t s) {
+  constexpr int PER = 128 / GROUP;
+  const size_t smem = sizeof(double) * PER * (size_t)(2 * NMAX + 1 + NMAX * (NMAX + 1));
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(tql2_batched_kernel<NMAX, GROUP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return HSSEIG_ERR_CUDA;
+  tql2_batched_kernel<NMAX, GROUP><<<(unsigned)((nmat + PER - 1) / PER), 128, smem, s>>>(
+      a, b, off, nmat, max_iter, lam, Q, qoff, status, flags);
+  HSS_CHECK_LAUNCH();
+  return HSSEIG_OK;
 }
 
 // W[:, c] = blockdiag(Q1, Q2)[:, src[c]] for c < n, W row-major (ldw)
@@ -348,14 +385,17 @@ __global__ void assemble_rows_kernel(const double* __restrict__ Qc, int64_t ldq,
 using namespace hsseig;
 
 extern "C" int hsseig_tql2_batched(const double* a, const double* b, const int64_t* off,
-                                   int64_t nmat, int max_iter, double* lam, double* Q,
-                                   const int64_t* qoff, int32_t* status, void* stream) {
-  if (nmat < 0 || !a || !off || !lam || !Q || !qoff || !status) HSS_ARG_FAIL();
+                                   int64_t nmat, int nmax, int max_iter, double* lam, double* Q,
+                                   const int64_t* qoff, int32_t* status, int flags, void* stream) {
+  if (nmat < 0 || !a || !off || !lam || !Q || !qoff || !status || nmax < 0 || nmax > kQLBig ||
+      (flags & ~(kQLInit | kQLUnsorted)))
+    HSS_ARG_FAIL();
   if (nmat == 0) return HSSEIG_OK;
-  tql2_batched_kernel<<<(unsigned)((nmat + 3) / 4), 128, 0, (cudaStream_t)stream>>>(
-      a, b, off, nmat, max_iter, lam, Q, qoff, status);
-  HSS_CHECK_LAUNCH();
-  return HSSEIG_OK;
+  if (nmax <= kQLMax)
+    return launch_tql2<kQLMax, 32>(a, b, off, nmat, max_iter, lam, Q, qoff, status, flags,
+                                   (cudaStream_t)stream);
+  return launch_tql2<kQLBig, 128>(a, b, off, nmat, max_iter, lam, Q, qoff, status, flags,
+                                  (cudaStream_t)stream);
 }
 
 extern "C" int hsseig_assemble_merge(const double* Q1, int64_t n1, const double* Q2, int64_t n2,
@@ -404,16 +444,38 @@ extern "C" int64_t hsseig_deflate_tol(const double* d, const double* z, int64_t 
                                       int64_t* ri, int64_t* rj, double* rc, double* rs,
                                       int64_t* n_rot);
 
+// sum of z[t]^2 in NumPy's order: np.sum(z * z) (secular.py:92) reduces a contiguous float64
+// array with pairwise_sum (blocks of <= 128 in 8 accumulators, halves split at multiples of 8),
+// so a merge sitting exactly on a deflation threshold keeps the reference's decision
+static double numpy_sum_sq(const double* z, int64_t n) {
+  if (n < 8) {
+    double r = -0.0;
+    for (int64_t i = 0; i < n; ++i) r += z[i] * z[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = z[j] * z[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += z[i + j] * z[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += z[i] * z[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return numpy_sum_sq(z, n2) + numpy_sum_sq(z + n2, n - n2);
+}
+
 extern "C" int64_t hsseig_deflate(const double* d, const double* z, int64_t n, double rho,
                                   double* d_out, double* z_out, int64_t* perm, int64_t* ri,
                                   int64_t* rj, double* rc, double* rs, int64_t* n_rot,
                                   double* tol_out) {
   if (n < 1) return -1;
-  double dmax = 0.0, zz = 0.0;
-  for (int64_t t = 0; t < n; ++t) {
-    dmax = std::max(dmax, std::fabs(d[t]));
-    zz += z[t] * z[t];
-  }
+  double dmax = 0.0;
+  for (int64_t t = 0; t < n; ++t) dmax = std::max(dmax, std::fabs(d[t]));
+  const double zz = numpy_sum_sq(z, n);
   const double tol = 8.0 * kEps * std::max(dmax, rho * zz);   // secular.py:91-93
   if (tol_out) *tol_out = tol;
   return hsseig_deflate_tol(d, z, n, rho, tol, d_out, z_out, perm, ri, rj, rc, rs, n_rot);

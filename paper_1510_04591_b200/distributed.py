@@ -22,7 +22,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .flops import secular_flops
+from .flops import cauchy_eval_flops, gemm_flops, secular_flops
 from .hss import build_partition, rank_bound
 from .secular import SecularConvergenceError, WeightRecomputationError
 
@@ -129,10 +129,16 @@ class ShardedMerge:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
-    def run(self, d, z, rho, X, seed):
+    def run(self, d, z, rho, X, seed, rows_total=None):
+        """rows_total: rows of the whole Q block over all ranks (the merge order in a full
+        solve) for the record's flop counts; summed over the group when not given."""
         k, cfg, ops = self.k, self.cfg, self.ops
         lo, hi, c = shard_range(k, self.rank, self.world)
         info = {"used_hss": False, "fell_back": False, "r_used": 0}
+        if rows_total is None:
+            cnt = gather_rows(torch.tensor([[float(X.shape[0])]], dtype=torch.float64,
+                                           device=X.device), 1, self.world, self.group)
+            rows_total = int(cnt.sum())
         # roots of this rank's index shard, then the full arrays on every rank
         lam_l, gam_l, mu_l, st_l = ops.secular_part(d, z, rho, lo, hi)
         full = gather_rows(torch.stack([lam_l, gam_l, mu_l], 1), c, k, self.group)
@@ -203,8 +209,23 @@ class ShardedMerge:
                 e1.record()
                 info["multiply_events"] = (e0, e1)
         else:
-            info["fell_back"] = tree is not None
             out = ops.dense(X, gen)
+        # the reference notes a fallback whenever the HSS route was taken and the dense
+        # product ran instead: no partition, r < 1, a flagged tree (dc.py:147-160); here
+        # also a sample wider than the kernels' MAX_WIDTH
+        eligible = cfg.method in ("adc-rand", "adc-srrsc") and k > cfg.hss_threshold
+        info["fell_back"] = bool(eligible and not info["used_hss"])
+        # per-phase counts under the reference's conventions (flops.py), all rows_total rows
+        fl = {"secular": info["flops_secular"], "update_dense": 0, "hss_construct": 0,
+              "hss_mult": 0}
+        if tree is not None:
+            fl["hss_construct"] = ops.construct_flops(tree)
+        if info["used_hss"]:
+            fl["hss_mult"] = ops.mult_flops(tree, rows_total)
+        else:
+            fl["update_dense"] = cauchy_eval_flops(k * k) + gemm_flops(rows_total, k, k)
+        info["flops"] = fl
+        info["rows_total"] = rows_total
         info["tree"] = tree
         return lam, out, info
 
@@ -383,6 +404,12 @@ class GpuOps:
             return None
         nat = self.nat
         k, ws = self.k, om.shape[1]
+        # one decision for the whole group, taken before anything is launched: every rank
+        # tests the padded shard size c they all share (a shorter last shard fits whenever
+        # c does), so no rank can take the peer path while another all-gathers
+        c = -(-k // world)
+        if not self.lib.hsseig_sample_peers_fits(k, c, w):
+            return None
         key = (k, ws, id(group))
         if self._peer_key != key:
             # two sets, alternating: a rank writes set n % 2 only after every rank passed
@@ -398,8 +425,7 @@ class GpuOps:
                                                       nat.ptr(pb.ptrs[0]), nat.ptr(pb.ptrs[1]),
                                                       world, ws, nat.ptr(self.sample_work),
                                                       self._s())
-        if rc == nat.HSSEIG_ERR_ARG:
-            return None
+        # past this point the other ranks store into our buffers: no NCCL fallback here
         nat.check(rc, "cauchy_sample_part_peers")
         peer_fence(group)
         return pb.local[0], pb.local[1]
@@ -469,6 +495,16 @@ class GpuOps:
 
     def flagged(self, tree):
         return tree.flagged
+
+    def construct_flops(self, tree):
+        from .hss import _construct_flops, _srrsc_flops
+        if getattr(tree, "method", "rand") == "srrsc":
+            return _srrsc_flops(tree, tree.k)
+        return _construct_flops(tree, tree.k, tree.w)
+
+    def mult_flops(self, tree, P):
+        from .hss import mult_flops
+        return mult_flops(tree, P)
 
     def r_used(self, tree):
         return tree.r_used
@@ -615,7 +651,12 @@ def adc_solve_distributed(T, cfg, ops, group=None):
     seeds, deflation and records are the reference's (dc.py:174-257).
     """
     from .dc import MergeRecord
-    from .solver import _tree
+    from .solver import MAX_BASE, _tree
+    # the same input checks as adc_solve (dc.py:185-186; solver.adc_solve)
+    if not (np.all(np.isfinite(T.a)) and np.all(np.isfinite(T.b))):
+        raise ValueError("matrix has non-finite entries")
+    if cfg.base_size > MAX_BASE:
+        raise ValueError(f"base_size above {MAX_BASE} is not supported by the device base case")
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     g = world.bit_length() - 1
@@ -681,12 +722,14 @@ def adc_solve_distributed(T, cfg, ops, group=None):
         if k > 0:
             sm = ShardedMerge(k, cfg, ops, group=grp)
             lam_k, Qk, info = sm.run(ops.tensor(dfl["d"][:k]), ops.tensor(dfl["z"][:k]),
-                                     dfl["rho_eff"], W[:, :k], seed=[cfg.seed, nd["mid"]])
+                                     dfl["rho_eff"], W[:, :k], seed=[cfg.seed, nd["mid"]],
+                                     rows_total=n)
             lam_k = lam_k.cpu().numpy()
             if rec is not None:
                 rec.used_hss = bool(info["used_hss"])
                 rec.fell_back = bool(info["fell_back"])
                 rec.hss_rank = int(info.get("r_used", 0))
+                rec.flops = dict(info["flops"])
         else:
             lam_k, Qk = np.zeros(0), None
         lam_cat = np.concatenate([lam_k, dfl["d"][k:]])

@@ -4,10 +4,10 @@
   reference's compiled kernel (pkg/src/hsseig/_kernels.pyx:178-234): NumPy in, NumPy
   out, outputs allocated by the callee.  Runs on the GPU.
 * ``tql2(d, e, Z, max_iter=30) -> int`` — the base-case kernel contract
-  (_kernels.pyx:352-411, called by dc.py:118-129): in place on NumPy arrays, returns
-  0 or 1 + the index of the eigenvalue whose QL iteration stalled.  Runs on the GPU
-  (warp-per-matrix QL, n <= 32).  The eigenpairs come back in ascending order, which
-  is the order the reference's caller sorts them into.
+  (_kernels.pyx:352-411, called by dc.py:118-129): in place on NumPy arrays (d and Z
+  rotated in QL order, e untouched), returns 0 or 1 + the index of the eigenvalue whose
+  QL iteration stalled.  Runs on the GPU (warp-per-matrix QL for n <= 32, a block per
+  matrix up to n = 160); the caller's Z is the initial accumulator, as in the reference.
 * ``merge_update(Qk, d, z, rho, cfg, seed, flops, record)`` — the merge body of
   dc.py:236-247 for one post-deflation system; returns (lam, Qk_new) as NumPy arrays
   (or torch CUDA tensors when Qk is one).
@@ -29,6 +29,10 @@ def secular_all(d, z, rho):
 
 
 def tql2(d, e, Z, max_iter=30):
+    """QL kernel contract of _kernels.pyx:352-411 / _kernels_py.py:300-360, run on the GPU:
+    d (n) in/out in QL order (unsorted), e read only (the reference iterates on a copy), Z
+    (any number of rows, n columns) rotated in place; returns 0 or 1 + the index of the
+    eigenvalue that stalled (d / Z as far as the iteration got)."""
     from . import _native as nat
     from .solver import MAX_BASE
     n = d.shape[0]
@@ -46,19 +50,30 @@ def tql2(d, e, Z, max_iter=30):
     off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
     qoff = torch.tensor([0, n * n], dtype=torch.int64, device="cuda")
     lam = torch.empty(n, **dev)
-    Q = torch.empty(n * n, **dev)
+    square = Z.shape[0] == n
+    # a square Z is the accumulator itself, rotated in place in the reference's order
+    # (flag 1); otherwise the kernel accumulates from the identity and Z <- Z Q after
+    Q = (torch.as_tensor(np.ascontiguousarray(Z, dtype=np.float64).ravel(), **dev).clone()
+         if square else torch.empty(n * n, **dev))
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
-    nat.check(lib.hsseig_tql2_batched(nat.ptr(a_d), nat.ptr(b_d), nat.ptr(off), 1, int(max_iter),
+    nat.check(lib.hsseig_tql2_batched(nat.ptr(a_d), nat.ptr(b_d), nat.ptr(off), 1, n, int(max_iter),
                                       nat.ptr(lam), nat.ptr(Q), nat.ptr(qoff), nat.ptr(st),
-                                      nat.stream_ptr()), "tql2_batched")
-    status = int(st.cpu()[0])
-    if status:
-        return status
+                                      3 if square else 2, nat.stream_ptr()), "tql2_batched")
     d[:] = lam.cpu().numpy()
-    Zq = torch.as_tensor(np.ascontiguousarray(Z, dtype=np.float64), **dev) @ Q.view(n, n)
-    Z[:, :] = Zq.cpu().numpy()
-    e[:] = 0.0
-    return 0
+    if square:
+        Z[:, :] = Q.view(n, n).cpu().numpy()
+    elif Z.shape[0]:
+        ne = n + (n & 1)                      # TMA rows: even leading dimensions
+        R = Z.shape[0]
+        Zin = torch.zeros(R, ne, **dev)
+        Zin[:, :n] = torch.as_tensor(np.asarray(Z, dtype=np.float64), **dev)
+        Qp = torch.zeros(n, ne, **dev)
+        Qp[:, :n] = Q.view(n, n)
+        Zout = torch.empty(R, ne, **dev)
+        nat.check(lib.hsseig_gemm(nat.ptr(Zin), ne, nat.ptr(Qp), ne, nat.ptr(Zout), ne, R, n, n,
+                                  nat.stream_ptr()), "gemm")
+        Z[:, :] = Zout[:, :n].cpu().numpy()
+    return int(st.cpu()[0])
 
 
 def merge_update(Qk, d, z, rho, cfg, seed=0, flops=None, record=None):

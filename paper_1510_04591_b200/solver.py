@@ -27,7 +27,7 @@ from .flops import FlopCounter, cauchy_eval_flops, gemm_flops, secular_flops
 from .secular import SecularConvergenceError, WeightRecomputationError
 
 _SQRT2 = np.sqrt(2.0)
-MAX_BASE = 32
+MAX_BASE = 160   # largest device base case (csrc/glue.cu kQLBig)
 
 
 def _i64(x):
@@ -95,6 +95,8 @@ def _base_cases_flat(a_mod, b, lo, hi, stream):
     lo = np.asarray(lo, dtype=np.int64)
     hi = np.asarray(hi, dtype=np.int64)
     sizes = hi - lo
+    if sizes.size and int(sizes.max()) > MAX_BASE:
+        raise ValueError(f"base case of order {int(sizes.max())} above the device QL's {MAX_BASE}")
     off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     qoff = np.concatenate([[0], np.cumsum(sizes * sizes)]).astype(np.int64)
     L0, L1 = int(lo[0]), int(hi[-1])
@@ -105,8 +107,9 @@ def _base_cases_flat(a_mod, b, lo, hi, stream):
     lam = torch.empty(int(off[-1]), dtype=torch.float64, device="cuda")
     Q = torch.empty(int(qoff[-1]), dtype=torch.float64, device="cuda")
     st = torch.zeros(len(lo), dtype=torch.int32, device="cuda")
-    nat.check(lib.hsseig_tql2_batched(nat.ptr(a_d), nat.ptr(b_d), nat.ptr(off_d), len(lo), 30,
-                                      nat.ptr(lam), nat.ptr(Q), nat.ptr(qoff_d), nat.ptr(st), stream),
+    nat.check(lib.hsseig_tql2_batched(nat.ptr(a_d), nat.ptr(b_d), nat.ptr(off_d), len(lo),
+                                      int(sizes.max()), 30, nat.ptr(lam), nat.ptr(Q),
+                                      nat.ptr(qoff_d), nat.ptr(st), 0, stream),
               "tql2_batched")
     bad = st.cpu().numpy()
     if bad.any():

@@ -66,6 +66,12 @@ class NumpyOps:
     def r_used(self, T):
         return T.r_used
 
+    def construct_flops(self, T):
+        return 0
+
+    def mult_flops(self, T, P):
+        return 0
+
     def multiply(self, X, T):
         return torch.as_tensor(orc.hss_apply_right(X.numpy(), T))
 

@@ -309,30 +309,53 @@ def test_plugin_secular_all_contract(sec):
     assert np.abs(lam - sec[f"{name}_lam"]).max() <= 64 * EPS * scale
 
 
-@pytest.mark.parametrize("n", [2, 7, 25, 32])
+@pytest.mark.parametrize("n", [2, 7, 25, 32, 33, 64, 160])
 def test_plugin_tql2_contract(n):
-    # the base-case kernel seam (pkg/src/hsseig/_kernels.pyx:352-411 as called by
-    # dc.py:118-129): in place, status 0, eigenpairs equal to the reference QL's
+    # the base-case kernel seam (pkg/src/hsseig/_kernels.pyx:352-411): d and Z in place in QL
+    # order, e untouched, status 0, equal to the reference QL's (restated in oracle/oracle_c.c);
+    # n > 32 runs the block-per-matrix kernel
     from paper_1510_04591_b200 import plugin
     from oracle import hss_oracle as orc
     rng = np.random.default_rng(n)
     a, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n - 1)
     d, e, Z = a.copy(), b.copy(), np.eye(n)
     assert plugin.tql2(d, e, Z, 30) == 0
+    assert np.array_equal(e, b)
     d0, e0, Z0 = a.copy(), b.copy(), np.eye(n)
     assert orc.tql2(d0, e0, Z0, 30) == 0
-    order = np.argsort(d0, kind="stable")
-    assert np.abs(d - d0[order]).max() <= 64 * EPS * np.abs(d0).max()   # backend tolerance
-    Zr = Z0[:, order]
-    Zg = Z * np.sign((Z * Zr).sum(0))
-    assert np.abs(Zg - Zr).max() <= 1e-13
-    # Z accumulates onto its input (Z <- Z Q), any number of rows
-    Zin = rng.standard_normal((3, n))
-    d2, e2, Z2 = a.copy(), b.copy(), Zin.copy()
+    assert np.abs(d - d0).max() <= 64 * EPS * np.abs(d0).max()   # backend tolerance
+    assert np.abs(Z - Z0).max() <= 1e-13
+    # a square Z is the accumulator (Z <- Z Q in the reference's rotation order)
+    Zin = rng.standard_normal((n, n))
+    d1, Z1 = a.copy(), Zin.copy()
+    assert plugin.tql2(d1, b.copy(), Z1, 30) == 0
+    d1o, Z1o = a.copy(), Zin.copy()
+    orc.tql2(d1o, b.copy(), Z1o, 30)
+    assert np.abs(Z1 - Z1o).max() <= 1e-12 * np.abs(Zin).max()
+    # any other row count: the rotations of the Python fallback (_kernels_py.py) on every row
+    Zr = rng.standard_normal((3, n))
+    d2, e2, Z2 = a.copy(), b.copy(), Zr.copy()
     assert plugin.tql2(d2, e2, Z2, 30) == 0
-    assert np.abs(Z2 - Zin @ Z).max() <= 1e-13
+    assert np.abs(Z2 - Zr @ Z).max() <= 1e-13
     with pytest.raises(ValueError):
-        plugin.tql2(np.zeros(40), np.zeros(39), np.eye(40))
+        plugin.tql2(np.zeros(200), np.zeros(199), np.eye(200))
+
+
+@pytest.mark.parametrize("base", [3, 25, 64, 160])
+def test_base_size_range(base):
+    # the reference accepts any base_size >= 3 (dc.py:43-44); the device base case covers
+    # leaves up to 160 (block-per-matrix QL above 32) and matches the oracle's recursion
+    import paper_1510_04591_b200 as hb
+    from oracle import hss_oracle as orc
+    rng = np.random.default_rng(base)
+    n = 700
+    T = hb.SymTridiagonal(rng.uniform(-1, 1, n), rng.uniform(-1, 1, n - 1))
+    cfg = hb.SolverConfig(base_size=base, leaf_size=32, hss_threshold=128, rank_eps=1e-13)
+    res = hb.adc_solve(T, cfg)
+    lam_ref = np.linalg.eigvalsh(T.to_dense())
+    assert np.abs(res.lam.cpu().numpy() - lam_ref).max() <= 1e-11 * T.norm_max()
+    Q = res.Q.cpu().numpy()
+    assert np.abs(Q.T @ Q - np.eye(n)).max() / n <= 1e-15
 
 
 def test_sharded_merge_driver_single_rank_nccl():

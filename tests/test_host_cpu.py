@@ -185,3 +185,42 @@ def test_wave_deflate_matches_oracle_deflation():
         cat = np.concatenate([lam[koff[m]:koff[m] + k], d_out[o + k:o + n]])
         ref = np.argsort(cat, kind="stable")
         assert np.array_equal(order[o:o + n], ref) and np.array_equal(lam_out[o:o + n], cat[ref])
+
+
+def test_deflation_tolerance_sums_like_numpy():
+    # hsseig_deflate's tol = 8 eps max(max|d|, rho * np.sum(z*z)) (secular.py:91-93) with
+    # NumPy's pairwise summation, bit for bit, and a weight placed exactly on the threshold
+    # is deflated like the reference does (rho |z_i| <= tol, secular.py:118)
+    import ctypes
+    from paper_1510_04591_b200 import _native as nat
+    lib = nat.load(build_if_missing=False)
+    P = lambda x: x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    rng = np.random.default_rng(11)
+    for n in (1, 5, 8, 9, 127, 128, 129, 1000, 8193, 40000):
+        d = np.sort(rng.uniform(-1e-3, 1e-3, n))
+        z = rng.standard_normal(n) * np.exp(rng.uniform(-8, 3, n))
+        rho = 0.75
+        ref = 8.0 * orc.EPS * max(float(np.abs(d).max()), rho * float(np.sum(z * z)))
+        out = [np.empty(n), np.empty(n), np.empty(n, dtype=np.int64), np.empty(n, dtype=np.int64),
+               np.empty(n, dtype=np.int64), np.empty(n), np.empty(n)]
+        nrot, tol = ctypes.c_int64(0), ctypes.c_double(0.0)
+        lib.hsseig_deflate(P(d), P(z), n, rho, *(P(x) for x in out), ctypes.byref(nrot),
+                           ctypes.byref(tol))
+        assert tol.value == ref, (n, tol.value, ref)
+    # a weight right on the threshold (the tolerance computed the reference's way)
+    n = 300
+    d = np.linspace(0.0, 1.0, n)
+    z = rng.standard_normal(n)
+    rho = 1.0
+    zz = z * z
+    tol = 8.0 * orc.EPS * max(1.0, rho * float(np.sum(zz)))
+    z[17] = tol / rho                   # changes the sum only below its last bit
+    ref_tol = 8.0 * orc.EPS * max(1.0, rho * float(np.sum(z * z)))
+    dk, zk, perm, rots, ldef, nd = orc.deflate(d, z, rho)
+    out = [np.empty(n), np.empty(n), np.empty(n, dtype=np.int64), np.empty(n, dtype=np.int64),
+           np.empty(n, dtype=np.int64), np.empty(n), np.empty(n)]
+    nrot, tolo = ctypes.c_int64(0), ctypes.c_double(0.0)
+    k = lib.hsseig_deflate(P(d), P(z), n, rho, *(P(x) for x in out), ctypes.byref(nrot),
+                           ctypes.byref(tolo))
+    assert tolo.value == ref_tol
+    assert k == dk.size and np.array_equal(out[2], perm)
