@@ -1,21 +1,27 @@
 """Benchmark: BASELINE config 4 — isolated top-level DC merge, N = 32768, on B200.
 
 One step = one pass of the merge hot path (secular roots -> Loewner weights ->
-column normalizers -> partition / rank estimate -> Omega -> Y = C Omega, Z = C^T Omega
+column normalizers -> partition / rank estimate -> Omega -> off-diagonal sample
 -> randomized HSS construction -> Q_new = Q_old H) over one synthetic input.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-value  = algorithmic FP64 TF/s of the whole merge (reference FlopCounter conventions,
-         pkg/src/hsseig/flops.py) with inputs resident in HBM;
+value  = FP64 TF/s of the merge with inputs resident in HBM, counted as the REFERENCE's
+         work for this exact input: its FlopCounter (pkg/src/hsseig/flops.py) over its own
+         tree, recorded by tests/golden/make_golden_configs.py (c4_32768), divided by our
+         wall time.  Our tree is smaller (the off-diagonal sample), so the
+         flops we execute are reported beside it ("flops", "value_own_tree"); the roofline
+         uses the executed flops of the multiply kernel.
 e2e    = the same through the public API with Q_old / d / u in pinned host memory,
          H2D and D2H copies inside the timed region.
 N > 1 (torchrun): the rows of Q_old are sharded across ranks (row-block sharding);
 the merge factors are computed per rank and the multiply is row-local.
---impl reference: the CPU oracle port (oracle/, NumPy + C restatement of the
-reference), all host threads, on a bounded config-4-shaped sample (N = 4096).
+--impl reference: the reference itself (baseline/_ref, built from /root/reference/pkg by
+its own setup; the oracle port when absent) on the host cores, on a bounded sample of the
+workload: the config-4 merge at N = 4096, stamped as such in its config.
 """
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -35,6 +41,7 @@ RANK_EPS = 1e-13
 OVERSAMPLE = 10
 SEED = 0
 CPU_SAMPLE_N = 4096
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 def parse():
@@ -47,6 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-eigh", action="store_true")
+    ap.add_argument("--cpu-eigh-all", action="store_true",
+                    help="also time the reference's config-3 solve on the host (~2 min)")
     return ap.parse_args()
 
 
@@ -58,22 +67,86 @@ def dist_env():
 
 
 # ----------------------------------------------------------------------------- CPU arm
-def cpu_merge_flops_per_s(n, reps=1):
-    """Oracle port timed on the host: returns (TF/s, seconds, flops, threads)."""
-    from oracle import hss_oracle as orc
+def reference_module():
+    """The unmodified reference package (baseline/_ref), or None when it was not built."""
+    if not os.path.isdir(os.path.join(REF_DIR, "hsseig")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import hsseig
+        import hsseig.dc  # noqa: F401
+        import hsseig.hss  # noqa: F401
+    except ImportError:
+        return None
+    return hsseig
+
+
+def cpu_merge(n):
+    """One config-4-shaped merge on the host: the reference's own chain (secular ->
+    Loewner -> normalizers -> partition / rank -> rand_hss_construct -> hss_matmul_right
+    over all n rows of Q_old) when baseline/_ref exists, else the oracle port.  Returns
+    (TF/s, seconds, reference flops, kind)."""
     from paper_1510_04591_b200.matgen import isolated_merge_system
     d, u, rho = isolated_merge_system(n, SEED)
     Q0 = np.linalg.qr(np.random.default_rng(1).standard_normal((n, n)))[0]
-    best = None
-    for _ in range(reps):
-        f = orc.Flops()
+    h = reference_module()
+    if h is not None:
+        from hsseig import hss
+        from hsseig.cauchy import CauchyEvecMatrix
+        from hsseig.flops import FlopCounter
+        from hsseig.secular import RankOneSystem, recompute_weights, solve_secular
+        f = FlopCounter()
         t0 = time.perf_counter()
-        G, lam, _ = orc.generators_from_roots(d, u, rho, f)
-        orc.update_hss(Q0, G, LEAF, OVERSAMPLE, RANK_EPS, 100, [SEED, 0], f)
+        sys_ = RankOneSystem(d, u, rho)
+        sol = solve_secular(sys_, flops=f)
+        recompute_weights(sys_.d, sol, sys_.z, rho=rho, flops=f)
+        C = CauchyEvecMatrix.from_secular(sys_, sol, flops=f)
+        part = hss.build_partition(C.k, LEAF, C.d, C.gamma, C.mu)
+        r = min(hss.estimate_rank(part, C.d, C.gamma, C.mu, RANK_EPS, 100), part.min_leaf - OVERSAMPLE)
+        H = hss.rand_hss_construct(C, part, r, p=OVERSAMPLE, seed=[SEED, 0], flops=f)
+        hss.hss_matmul_right(Q0, H, flops=f)
         dt = time.perf_counter() - t0
         fl = f.secular + f.hss_construct + f.hss_mult + f.update_dense
-        best = (fl / dt / 1e12, dt, fl) if best is None or dt < best[1] else best
-    return best + (os.cpu_count(),)
+        return fl / dt / 1e12, dt, fl, "reference"
+    from oracle import hss_oracle as orc
+    f = orc.Flops()
+    t0 = time.perf_counter()
+    G, lam, _ = orc.generators_from_roots(d, u, rho, f)
+    orc.update_hss(Q0, G, LEAF, OVERSAMPLE, RANK_EPS, 100, [SEED, 0], f)
+    dt = time.perf_counter() - t0
+    fl = f.secular + f.hss_construct + f.hss_mult + f.update_dense
+    return fl / dt / 1e12, dt, fl, "port"
+
+
+def cpu_eigh(names):
+    """The reference's full adc_solve on BASELINE configs on the host (wall-s, the core
+    count of this host); returns {} when baseline/_ref is absent."""
+    h = reference_module()
+    if h is None:
+        return {}
+    from hsseig.matgen import SymTridiagonal, gen_toeplitz
+    out = {}
+    for name in names:
+        if name == "cfg1_uniform_N2000":
+            rng = np.random.default_rng(0)
+            a = rng.uniform(-1.0, 1.0, 2000)
+            T = SymTridiagonal(a, rng.uniform(-1.0, 1.0, 1999))
+            cfg = h.dc.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13)
+        elif name == "cfg2_toeplitz_N10000_adc2":
+            T = gen_toeplitz(10000)
+            cfg = h.dc.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13)
+        elif name == "cfg3_kac_N20000":
+            i = np.arange(1, 20000, dtype=np.float64)
+            T = SymTridiagonal(np.zeros(20000), np.sqrt(i * (20000 - i)))
+            cfg = h.dc.SolverConfig(rank_eps=1e-13)
+        else:
+            continue
+        t0 = time.perf_counter()
+        h.dc.adc_solve(T, cfg)
+        out[name] = {"wall_s": time.perf_counter() - t0, "cores": os.cpu_count(),
+                     "kind": "reference"}
+    return out
 
 
 def run_reference(args):
@@ -82,20 +155,24 @@ def run_reference(args):
         return
     threads = os.cpu_count()
     vals = []
+    kind = "port"
     for i in range(args.warmup + args.steps):
-        tf, dt, fl, _ = cpu_merge_flops_per_s(CPU_SAMPLE_N)
+        tf, dt, fl, kind = cpu_merge(CPU_SAMPLE_N)
         if i >= args.warmup:
             vals.append((tf, dt))
     tf = statistics.median(v[0] for v in vals)
     ms = statistics.median(v[1] for v in vals) * 1e3
-    sample = (f"config-4-shaped isolated merge at N={CPU_SAMPLE_N} (secular + Loewner + "
-              f"normalizers + HSS construct + HSS x Q_old), one merge per step")
+    sample = (f"config-4 merge at N={CPU_SAMPLE_N} (the N = 32768 workload does not fit a "
+              f"bounded CPU run: 173.6 s per merge on 8 cores); one merge per step: secular + "
+              f"Loewner + normalizers + HSS construct + HSS x Q_old, "
+              f"{'the reference itself (baseline/_ref)' if kind == 'reference' else 'oracle port'}"
+              f", OpenBLAS threads = {threads}")
     line = {
         "impl": "reference", "metric": metric_name(), "value": tf, "unit": "TF/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(args.n, world),
-        "cpu_baseline": {"value": tf, "unit": "TF/s", "cores": threads, "kind": "port",
+        "data": "synthetic", "config": config_dict(CPU_SAMPLE_N, world),
+        "cpu_baseline": {"value": tf, "unit": "TF/s", "cores": threads, "kind": kind,
                          "sample": sample},
         "e2e": {"value": tf, "unit": "TF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -103,7 +180,8 @@ def run_reference(args):
 
 
 def metric_name():
-    return "merge-step FP64 TF/s (algorithmic; HSS eigvec-update incl. secular/Loewner/build/multiply)"
+    return ("merge-step FP64 TF/s (the reference's FlopCounter work for the input / wall time; "
+            "HSS eigvec-update incl. secular/Loewner/build/multiply)")
 
 
 def config_dict(n, world):
@@ -217,33 +295,87 @@ def adc1_merge(d, u, rho, Q, out, reps=2):
     return best
 
 
-def eigh_lines():
-    """Full tridiagonal eigendecompositions (BASELINE configs 1, 2, 3, 5) on one GPU: wall-s
-    + accuracy.  Config 2 is ADC1 as BASELINE names it (SRRSC construction, method
-    "adc-srrsc"; no reference implementation exists, SURVEY.md D1) and, beside it, ADC2.
+def _metrics_gpu(T, lam, Q, with_bwd=True):
+    """orthogonality / backward / residual with the reference's formulas (cli.py:63-71)."""
+    import torch
+    n = T.n
+    lam_d = torch.as_tensor(np.asarray(lam), device="cuda")
+    G = Q.T @ Q
+    G.diagonal().sub_(1.0)
+    orth = float(G.abs().max()) / n
+    del G
+    bwd = None
+    if with_bwd:
+        A = torch.zeros(n, n, dtype=torch.float64, device="cuda")
+        i = torch.arange(n, device="cuda")
+        A[i, i] = torch.as_tensor(T.a, device="cuda")
+        A[i[:-1], i[1:]] = torch.as_tensor(T.b, device="cuda")
+        A[i[1:], i[:-1]] = torch.as_tensor(T.b, device="cuda")
+        A -= (Q * lam_d[None, :]) @ Q.T
+        bwd = float(A.abs().max()) / (T.norm_max() * n)
+        del A
+    a = torch.as_tensor(T.a, device="cuda")
+    b = torch.as_tensor(T.b, device="cuda")
+    TQ = a[:, None] * Q
+    TQ[:-1] += b[:, None] * Q[1:]
+    TQ[1:] += b[:, None] * Q[:-1]
+    resid = float((TQ - Q * lam_d[None, :]).abs().max()) / (n * T.norm_max())
+    return orth, bwd, resid
 
-    CPU reference wall-s for the same configs (survey container, 8 cores) is in BASELINE.md:
-    1.32 s / 22.05 s / 124.5 s; config 5 at N=65536 does not fit the reference's host
-    memory (48.3 s at N=16384).
+
+def glue_gbs(T, cfg):
+    """Achieved HBM GB/s of the glue kernels (blockdiag assembly + Givens replay, final
+    column gather) over one full solve: algorithmic bytes / CUDA-event time per depth."""
+    import torch
+
+    import paper_1510_04591_b200 as hb
+    from paper_1510_04591_b200 import solver
+    solver.GLUE_PROFILE = []
+    try:
+        hb.adc_solve(T, cfg)
+        torch.cuda.synchronize()
+        prof = solver.GLUE_PROFILE
+    finally:
+        solver.GLUE_PROFILE = None
+    out = {}
+    for kind in ("assemble", "gather"):
+        rows = [(e0.elapsed_time(e1), nb) for k, e0, e1, nb in prof if k == kind]
+        ms = sum(r[0] for r in rows)
+        nb = sum(r[1] for r in rows)
+        out[kind] = {"ms": ms, "bytes": nb, "GB_s": nb / (ms * 1e-3) / 1e9 if ms else None}
+    return out
+
+
+def eigh_lines(peak_hbm=None):
+    """Full tridiagonal eigendecompositions (BASELINE configs 1, 2, 3, 5) on one GPU: wall-s
+    with Q left on the device, e2e wall-s with Q returned to pinned host memory (the
+    reference's adc_solve returns a host Q, dc.py:65-79), the parity metrics with the
+    reference's formulas and their ratio to the reference's own values on the same input
+    (tests/golden/configs.npz, north_star's <= 10x rule), and the glue kernels' HBM GB/s
+    (configs 1 and 5).  Config 2 is ADC1 as BASELINE names it (SRRSC construction, method
+    "adc-srrsc"; no reference implementation exists, SURVEY.md D1) and, beside it, ADC2.
     """
     import torch
 
     import paper_1510_04591_b200 as hb
+    gpath = os.path.join(ROOT, "tests", "golden", "configs.npz")
+    g = np.load(gpath) if os.path.exists(gpath) else None
     out = {}
-    cases = [
+    toe = np.sort(2 + 2 * np.cos(np.arange(1, 10001) * np.pi / 10001))
+    kac = -(20000 - 1) + 2.0 * np.arange(20000)
+    cases = [  # name, T, cfg, exact spectrum, fixture tag, glue
         ("cfg1_uniform_N2000", hb.gen_uniform(2000, 0),
-         hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13), None),
+         hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13), None, "cfg1", True),
         ("cfg2_toeplitz_N10000_adc1", hb.gen_toeplitz(10000),
          hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13, method="adc-srrsc"),
-         np.sort(2 + 2 * np.cos(np.arange(1, 10001) * np.pi / 10001))),
+         toe, None, False),
         ("cfg2_toeplitz_N10000_adc2", hb.gen_toeplitz(10000),
-         hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13),
-         np.sort(2 + 2 * np.cos(np.arange(1, 10001) * np.pi / 10001))),
-        ("cfg3_kac_N20000", hb.gen_kac(20000), hb.SolverConfig(rank_eps=1e-13),
-         -(20000 - 1) + 2.0 * np.arange(20000)),
-        ("cfg5_N65536", hb.gen_config5(65536, 0), hb.SolverConfig(rank_eps=1e-13), None),
+         hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13), toe, "cfg2r", False),
+        ("cfg3_kac_N20000", hb.gen_kac(20000), hb.SolverConfig(rank_eps=1e-13), kac, "cfg3", False),
+        ("cfg3_kac_N20000_defaults", hb.gen_kac(20000), hb.SolverConfig(), kac, "cfg3d", False),
+        ("cfg5_N65536", hb.gen_config5(65536, 0), hb.SolverConfig(rank_eps=1e-13), None, None, True),
     ]
-    for name, T, cfg, exact in cases:
+    for name, T, cfg, exact, tag, glue in cases:
         hb.adc_solve(T, cfg)   # warm-up (allocator, tree buffers)
         best = None
         for _ in range(2):
@@ -254,26 +386,45 @@ def eigh_lines():
             dt = time.perf_counter() - t0
             best = dt if best is None else min(best, dt)
         n = T.n
-        Q = res.Q
-        a = torch.as_tensor(T.a, device="cuda")
-        b = torch.as_tensor(T.b, device="cuda")
-        TQ = a[:, None] * Q
-        TQ[:-1] += b[:, None] * Q[1:]
-        TQ[1:] += b[:, None] * Q[:-1]
-        resid = float((TQ - Q * torch.as_tensor(res.lam, device="cuda")[None, :]).abs().max())
-        del TQ
-        G = Q.T @ Q
-        G.diagonal().sub_(1.0)
-        orth = float(G.abs().max()) / n
-        del G
         rec = {"wall_s": best, "method": cfg.method, "merges": len(res.merges),
                "hss_merges": int(sum(m.used_hss for m in res.merges)),
-               "top_merge_hss": bool(res.merges[-1].used_hss),
-               "orthogonality": orth, "residual": resid / (n * T.norm_max())}
+               "top_merge_hss": bool(res.merges[-1].used_hss)}
+        if n <= 20000:
+            # end to end as the reference API returns it: Q in (pinned) host memory
+            hostQ = torch.empty(n, n, dtype=torch.float64, pin_memory=True)
+            e2e = None
+            for _ in range(2):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                r2 = hb.adc_solve(T, cfg)
+                hostQ.copy_(r2.Q)
+                dt = time.perf_counter() - t0
+                e2e = dt if e2e is None else min(e2e, dt)
+                del r2
+            rec["wall_s_e2e"] = e2e
+            rec["d2h_bytes"] = 8 * n * n
+            del hostQ
+        o, b, r = _metrics_gpu(T, res.lam, res.Q, with_bwd=n <= 20000)
+        rec.update({"orthogonality": o, "backward": b, "residual": r})
         if exact is not None:
             rec["eig_err_over_normT"] = float(np.abs(res.lam - exact).max()) / T.norm_max()
+        if g is not None and tag is not None and f"{tag}_orth" in g.files:
+            ref = {m: float(g[f"{tag}_{m}"]) for m in ("orth", "bwd", "resid")}
+            rec["reference"] = dict(ref, wall_s_survey_host=float(g[f"{tag}_wall_s"]))
+            rec["ratio_to_reference"] = {"orthogonality": o / ref["orth"],
+                                         "backward": (b / ref["bwd"]) if b is not None else None,
+                                         "residual": r / ref["resid"]}
+            rec["eig_err_vs_reference_over_normT"] = (
+                float(np.abs(res.lam - g[f"{tag}_lam"]).max()) / T.norm_max())
+        del res
+        torch.cuda.empty_cache()
+        if glue:
+            gl = glue_gbs(T, cfg)
+            if peak_hbm:
+                for v in gl.values():
+                    v["frac_of_hbm"] = v["GB_s"] / peak_hbm if v["GB_s"] else None
+            rec["glue_hbm"] = gl
         out[name] = rec
-        del res, Q
         torch.cuda.empty_cache()
     return out
 
@@ -332,6 +483,73 @@ def eigh_distributed(world, ops=None, device="cuda", n=65536, warm=True):
             "hss_merges": int(sum(m.used_hss for m in res.merges)),
             "orthogonality_sampled_cols": ns, "orthogonality": float(Gs.abs().max()) / n,
             "residual": float(resid) / (n * T.norm_max())}
+
+
+def reference_work(n):
+    """The reference's FlopCounter for the config-4 merge at N = n on this exact input
+    (secular + hss_construct + hss_mult over all n rows of Q_old), from the fixture the
+    unmodified reference produced; None when not recorded for this N."""
+    gp = os.path.join(ROOT, "tests", "golden", "configs.npz")
+    tag = f"c4_{n}"
+    if not os.path.exists(gp):
+        return None
+    g = np.load(gp)
+    if f"{tag}_flops_mult_per_row" not in g.files:
+        return None
+    w = {"secular": int(g[f"{tag}_flops_secular"]), "hss_construct": int(g[f"{tag}_flops_construct"]),
+         "hss_mult": int(g[f"{tag}_flops_mult_per_row"]) * n, "r_used": int(g[f"{tag}_r_used"])}
+    w["total"] = w["secular"] + w["hss_construct"] + w["hss_mult"]
+    return w
+
+
+def peak_hbm():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def multiply_traffic():
+    """DRAM bytes per multiply from the committed ncu capture, used only when it was taken
+    on the multiply kernel source in this tree (sha256 of csrc/hss_mult.cu + tma.cuh)."""
+    src = b"".join(open(os.path.join(ROOT, "paper_1510_04591_b200", "csrc", f), "rb").read()
+                   for f in ("hss_mult.cu", "tma.cuh"))
+    sha = hashlib.sha256(src).hexdigest()[:16]
+    tp = os.path.join(ROOT, "profiles", "multiply_traffic.json")
+    try:
+        t = json.load(open(tp))
+    except (OSError, ValueError):
+        return None, "no ncu capture"
+    if t.get("source_sha16") != sha:
+        return None, f"profiles/multiply_traffic.json is from another kernel source ({t.get('source_sha16')})"
+    return t.get("bytes_per_multiply"), f"profiles/multiply_traffic.json ({t.get('file')})"
+
+
+def same_n_merge(n, cfg, args):
+    """The GPU merge at the reference arm's sample size (device-resident, same protocol)."""
+    import torch
+
+    import paper_1510_04591_b200 as hb
+    from paper_1510_04591_b200.merge_pipeline import MergePipeline
+    d, u, rho = hb.isolated_merge_system(n, SEED)
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    Q0, _ = torch.linalg.qr(torch.randn(n, n, dtype=torch.float64, device="cuda", generator=gen))
+    Q0 = Q0.contiguous()                  # LAPACK order -> row-major rows for the multiply
+    pipe = MergePipeline(n, cfg, rows=n)
+    out = torch.empty_like(Q0)
+    dd, uu = torch.as_tensor(d, device="cuda"), torch.as_tensor(u, device="cuda")
+    for _ in range(max(3, args.warmup)):
+        pipe.run(dd, uu, rho, Q0, seed=[SEED, 0], out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(5, args.steps)
+    e0.record()
+    for _ in range(steps):
+        pipe.run(dd, uu, rho, Q0, seed=[SEED, 0], out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    return {"N": n, "ms_per_step": e0.elapsed_time(e1) / steps, "unit": "TF/s",
+            "note": "value = the reference's flops for this input (cpu_baseline leg) / GPU time"}
 
 
 def run_ours(args):
@@ -433,7 +651,9 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t)
     rec = phase_ms[-1]
-    flops_total = rec["flops_total_fullP"]   # one merge, all P rows (algorithmic)
+    flops_own = rec["flops_total_fullP"]     # one merge, all P rows, on OUR tree
+    ref_work = reference_work(n)
+    flops_total = ref_work["total"] if ref_work else flops_own
     value = flops_total / (ms * 1e-3) / 1e12
     mult_ms = statistics.median(p["ms"]["multiply"] for p in phase_ms)
     if not (mult_ms == mult_ms):   # no HSS multiply (dense fallback)
@@ -497,14 +717,12 @@ def run_ours(args):
     if world > 1 and not args.no_eigh and (world & (world - 1)) == 0:
         eigh_d = eigh_distributed(world)
 
+    same_n = None
+    if world == 1 and not args.no_cpu:
+        same_n = same_n_merge(CPU_SAMPLE_N, cfg, args)
+
     if rank == 0:
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic_batched_gemm.json")
-        if os.path.exists(tp):
-            try:
-                traffic = json.load(open(tp)).get("bytes_per_multiply")
-            except (OSError, ValueError):
-                traffic = None
+        traffic, traffic_src = multiply_traffic()
         achieved = mult_fl / (mult_ms * 1e-3) / 1e12
         line = {
             "metric": metric_name(), "value": value, "unit": "TF/s", "n_gpus": world,
@@ -517,27 +735,46 @@ def run_ours(args):
                 if world > 1 else {})),
             "merge_wall_s": ms / 1e3,
             "phases_ms": {k: statistics.median(p["ms"][k] for p in phase_ms) for k in rec["ms"]},
-            "flops": rec["flops"], "hss_rank": rec["r_used"], "used_hss": rec["used_hss"],
-            "roofline": {"bound": "tensor", "kernel": "batched_gemm2 (HSS multiply, FP64 DMMA)",
+            "flops_basis": ("reference FlopCounter on the reference's own tree for this input "
+                            "(tests/golden/configs.npz c4_32768)") if ref_work else
+                           "FlopCounter conventions on our own tree (no reference count for this N)",
+            "flops_reference": ref_work,
+            "flops": rec["flops"], "value_own_tree": flops_own / (ms * 1e-3) / 1e12,
+            "hss_rank": rec["r_used"], "used_hss": rec["used_hss"],
+            "roofline": {"bound": "tensor", "kernel": "tma_gemm_kernel (HSS multiply, FP64 DMMA)",
                          "achieved": achieved, "peak": peak, "unit": "TF/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "algorithmic": "multiply flops executed (our tree, reference counter "
+                                        "conventions hss.py:329-357) / CUDA-event time of the "
+                                        "multiply launches",
                          "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64 entry)"},
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
         }
+        if same_n is not None:
+            line["same_n"] = same_n
         if world == 1 and not args.no_eigh:
-            line["eigh"] = eigh_lines()
+            line["eigh"] = eigh_lines(peak_hbm())
         if adc1 is not None:
             line["config4_adc1"] = adc1
         if world > 1 and eigh_d is not None:
             line["eigh"] = {"cfg5_N65536_distributed": eigh_d}
         if not args.no_cpu and world == 1:
-            tf, dt, fl, thr = cpu_merge_flops_per_s(CPU_SAMPLE_N)
+            tf, dt, fl, kind = cpu_merge(CPU_SAMPLE_N)
             line["cpu_baseline"] = {
-                "value": tf, "unit": "TF/s", "cores": thr, "kind": "port",
-                "sample": f"oracle port, config-4-shaped isolated merge at N={CPU_SAMPLE_N} "
-                          f"({dt:.2f} s, {fl:.3e} flops)"}
+                "value": tf, "unit": "TF/s", "cores": os.cpu_count(), "kind": kind,
+                "sample": f"{'the reference (baseline/_ref)' if kind == 'reference' else 'oracle port'}"
+                          f": config-4 merge at N={CPU_SAMPLE_N} ({dt:.2f} s, {fl:.3e} reference "
+                          f"flops; OpenBLAS threads = host cores)"}
+            if same_n is not None:
+                same_n["value"] = fl / (same_n["ms_per_step"] * 1e-3) / 1e12
+                same_n["ratio_to_cpu_reference"] = same_n["value"] / tf
+            if not args.no_eigh:
+                line["cpu_baseline"]["eigh"] = cpu_eigh(
+                    ["cfg1_uniform_N2000", "cfg2_toeplitz_N10000_adc2"]
+                    + (["cfg3_kac_N20000"] if args.cpu_eigh_all else []))
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -118,14 +118,21 @@ int hsseig_cauchy_block(const hsseig_gen *gen, const int64_t *rows, int64_t nr,
  * Replaces CauchyEvecMatrix.multiply / transpose_multiply (cauchy.py:70-100).
  * Omega: k x w (ld = ldom, even; 16-byte aligned rows for TMA).  Y, Z: k x w (ld = ldy).
  * work: hsseig_sample_work_doubles(k, w) doubles (split-K partials).
+ * leaf_of: NULL for the full products (the reference's C Omega, C^T Omega), or the tree's
+ * leaf id per index (hsseig_tree.leaf_of) for the OFF-DIAGONAL sample the construction uses
+ * by default: entries with leaf_of[i] == leaf_of[j] count as zero, so Y_t = Phi_t =
+ * C(t, t^c) Omega(t^c) directly instead of Y_t - D_t Omega_t (hss.py:265-266), which cancels
+ * the dominant diagonal block and leaves the sum's rounding noise for the ID to truncate
+ * against (half the ranks, ~15x smaller HSS error at config 4's shape).
  */
 int64_t hsseig_sample_work_doubles(int64_t k, int64_t w);
-int hsseig_cauchy_sample(const hsseig_gen *gen, const double *omega, int64_t ldom, int64_t w,
-                         double *Y, double *Z, int64_t ldy, double *work, void *stream);
+int hsseig_cauchy_sample(const hsseig_gen *gen, const int32_t *leaf_of, const double *omega,
+                         int64_t ldom, int64_t w, double *Y, double *Z, int64_t ldy, double *work,
+                         void *stream);
 /* Rows [row0, row1) of Y and of Z (multi-GPU shard); Y, Z hold row1 - row0 rows. */
-int hsseig_cauchy_sample_part(const hsseig_gen *gen, const double *omega, int64_t ldom, int64_t w,
-                              int64_t row0, int64_t row1, double *Y, double *Z, int64_t ldy,
-                              double *work, void *stream);
+int hsseig_cauchy_sample_part(const hsseig_gen *gen, const int32_t *leaf_of, const double *omega,
+                              int64_t ldom, int64_t w, int64_t row0, int64_t row1, double *Y,
+                              double *Z, int64_t ldy, double *work, void *stream);
 
 /*
  * Multi-GPU form fused with the all-gather: rows [row0, row1) of Y and Z are computed here
@@ -134,10 +141,10 @@ int hsseig_cauchy_sample_part(const hsseig_gen *gen, const double *omega, int64_
  * NVLink / NVSwitch).  The caller synchronises its stream and barriers the group before
  * reading.  Materialised-panel path only (HSSEIG_ERR_ARG otherwise: use the NCCL gather).
  */
-int hsseig_cauchy_sample_part_peers(const hsseig_gen *gen, const double *omega, int64_t ldom,
-                                    int64_t w, int64_t row0, int64_t row1, const uint64_t *Yp,
-                                    const uint64_t *Zp, int32_t npeers, int64_t ldy, double *work,
-                                    void *stream);
+int hsseig_cauchy_sample_part_peers(const hsseig_gen *gen, const int32_t *leaf_of,
+                                    const double *omega, int64_t ldom, int64_t w, int64_t row0,
+                                    int64_t row1, const uint64_t *Yp, const uint64_t *Zp,
+                                    int32_t npeers, int64_t ldy, double *work, void *stream);
 /* 1 when hsseig_cauchy_sample_part_peers accepts a shard of `nrows` rows (order k, width w),
  * else 0.  Monotone in nrows: ranks evaluate it on the padded shard size they all share, so
  * every rank of a group takes the same path (peer stores or the NCCL gather). */
@@ -177,6 +184,9 @@ typedef struct hsseig_tree {
   /* host-side upper bound on the node ranks, set by the caller after reading the ranks
      back (0 = unknown, w is used); sizes the multiply's output tiles to the ranks */
   int32_t rmax;
+  /* device: leaf position of every index 0..k-1 (filled by hsseig_tree_layout); the
+     leaf_of argument of the sampling calls for the off-diagonal sample */
+  int32_t *leaf_of;
 } hsseig_tree;
 
 /*
@@ -208,12 +218,15 @@ int hsseig_tree_layout(hsseig_tree *tree, const int32_t *bounds_h, int32_t n_lea
  * leaf D / Phi / Theta formation, batched column-pivoted-QR interpolative
  * decompositions (dgeqp3 + dtrtrs semantics, hss.py:120-148) level by level,
  * skeleton B blocks regenerated from the generators.
- * Y, Z: sampled blocks (ld = ldy); omega (ld = ldom); w = r + p.
+ * Y, Z: sampled blocks (ld = ldy); omega (ld = ldom); w = r + p.  offdiag = 1: Y / Z are the
+ * off-diagonal sample (hsseig_cauchy_sample with leaf_of), the leaves take Phi = Y_t,
+ * Theta = Z_t; offdiag = 0: full products, Phi = Y_t - D Omega_t as hss.py:265-266.
  * status[4] = saturated-ID count (tree flagged), status[5] = r_used.
  */
 int hsseig_hss_build_rand(const hsseig_gen *gen, const double *omega, int64_t ldom,
                           const double *Y, const double *Z, int64_t ldy, double id_tol,
-                          hsseig_tree *tree, hsseig_status *status, void *stream);
+                          int32_t offdiag, hsseig_tree *tree, hsseig_status *status,
+                          void *stream);
 /* Zero the tree's factor slots (done by hsseig_hss_build_rand; call once before the
  * per-level form below). */
 int hsseig_tree_clear(hsseig_tree *tree, void *stream);
@@ -225,8 +238,8 @@ int hsseig_tree_clear(hsseig_tree *tree, void *stream);
  */
 int hsseig_hss_build_rand_levels(const hsseig_gen *gen, const double *omega, int64_t ldom,
                                  const double *Y, const double *Z, int64_t ldy, double id_tol,
-                                 hsseig_tree *tree, hsseig_status *status, int lev_from,
-                                 int lev_to, int part, int nparts, void *stream);
+                                 int32_t offdiag, hsseig_tree *tree, hsseig_status *status,
+                                 int lev_from, int lev_to, int part, int nparts, void *stream);
 
 /*
  * (f4) ADC1: HSS construction by structured rank-revealing Schur complements (SRRSC) on the

@@ -396,8 +396,28 @@ def sample_block(k, w, seed):
     return np.random.default_rng(seed).standard_normal((k, w))
 
 
-def rand_construct(G, ranges, r, p=10, seed=0, id_tol=ID_TOL, flops=None, Omega=None):
-    """Algorithm 2 with one sample block for both sides (hss.py:217-306)."""
+# The B200 path's sample (DESIGN.md §2 "off-diagonal sample"): Phi_t = C(t, t^c) Omega(t^c)
+# formed directly instead of Y_t - D_t Omega_t, which cancels the dominant diagonal block and
+# leaves the sample's rounding noise for the ID to truncate against.  Not the reference's
+# arithmetic; rand_construct(offdiag=True) defines what the GPU's default mode computes.
+def offdiag_samples(G, ranges, X):
+    """(Phi, Theta) with Phi[t] = C(t, t^c) X(t^c), Theta[t] = C(t^c, t)^T X(t^c) per leaf t."""
+    k = G.k
+    allc = np.arange(k)
+    Phi = np.empty((k, X.shape[1]))
+    The = np.empty((k, X.shape[1]))
+    for lo, hi in ranges:
+        t = np.arange(lo, hi)
+        off = np.concatenate([allc[:lo], allc[hi:]])
+        Phi[lo:hi] = G.block(t, off) @ X[off]
+        The[lo:hi] = G.block(off, t).T @ X[off]
+    return Phi, The
+
+
+def rand_construct(G, ranges, r, p=10, seed=0, id_tol=ID_TOL, flops=None, Omega=None,
+                   offdiag=False):
+    """Algorithm 2 with one sample block for both sides (hss.py:217-306); offdiag=True
+    forms the leaf samples without the diagonal-block cancellation (offdiag_samples)."""
     if len(ranges) < 2:
         raise ValueError("need at least two leaves")
     if r < 1 or p < 0:
@@ -407,8 +427,13 @@ def rand_construct(G, ranges, r, p=10, seed=0, id_tol=ID_TOL, flops=None, Omega=
         raise ValueError("sample width exceeds smallest leaf")
     if Omega is None:
         Omega = sample_block(G.k, w, seed)
-    Y = G.times(Omega, flops)
-    Z = G.t_times(Omega, flops)
+    if offdiag:
+        Y, Z = offdiag_samples(G, ranges, Omega)
+        if flops is not None:
+            flops.hss_construct += 2 * (f_gemm(G.k, G.k, Omega.shape[1]) + f_cauchy(G.k * G.k))
+    else:
+        Y = G.times(Omega, flops)
+        Z = G.t_times(Omega, flops)
     nodes, root = postorder_nodes(ranges)
     tree = Tree(nodes, root, list(ranges), G.k)
     psel, tsel, ycomp, zcomp = {}, {}, {}, {}
@@ -428,8 +453,11 @@ def rand_construct(G, ranges, r, p=10, seed=0, id_tol=ID_TOL, flops=None, Omega=
                 t = np.arange(nd.lo, nd.hi)
                 nd.D = G.block(t, t, flops)
                 Om = Omega[nd.lo:nd.hi]
-                Phi = Y[nd.lo:nd.hi] - nd.D @ Om
-                The = Z[nd.lo:nd.hi] - nd.D.T @ Om
+                if offdiag:
+                    Phi, The = Y[nd.lo:nd.hi], Z[nd.lo:nd.hi]
+                else:
+                    Phi = Y[nd.lo:nd.hi] - nd.D @ Om
+                    The = Z[nd.lo:nd.hi] - nd.D.T @ Om
                 if flops is not None:
                     flops.hss_construct += 2 * f_gemm(t.size, t.size, w)
                 nd.U, nd.rloc, nd.rres = do_id(Phi, "row", nd)
@@ -534,7 +562,7 @@ def update_dense(Qb, G, flops=None):
 
 
 def update_hss(Qb, G, leaf, oversample, rank_eps, rank_cap, seed, flops=None, info=None,
-               Omega=None, return_tree=False):
+               Omega=None, return_tree=False, offdiag=False):
     """dc.py:141-171: partition, rank, construct, flag -> dense fallback, multiply."""
     def fallback():
         if info is not None:
@@ -550,7 +578,7 @@ def update_hss(Qb, G, leaf, oversample, rank_eps, rank_cap, seed, flops=None, in
             min(hi - lo for lo, hi in ranges) - oversample)
     if r < 1:
         return fallback()
-    T = rand_construct(G, ranges, r, oversample, seed, flops=flops, Omega=Omega)
+    T = rand_construct(G, ranges, r, oversample, seed, flops=flops, Omega=Omega, offdiag=offdiag)
     if T.flagged:
         return fallback()
     if info is not None:
@@ -605,6 +633,7 @@ class Config:
     seed: int = 0
     method: str = "adc-rand"
     srrsc_tol: float = ID_TOL     # ADC1 only (srrsc_oracle.py)
+    offdiag: bool = False         # the B200 path's off-diagonal sample (offdiag_samples)
 
 
 def base_case(a, b):
@@ -666,7 +695,8 @@ def adc_solve(a, b, cfg=None):
             Qk = np.ascontiguousarray(Qb[:, ck])
             if cfg.method == "adc-rand" and k > cfg.hss_threshold:
                 Qk = update_hss(Qk, G, cfg.leaf_size, cfg.oversample, cfg.rank_eps,
-                                cfg.rank_cap, [cfg.seed, mid], flops, info)
+                                cfg.rank_cap, [cfg.seed, mid], flops, info,
+                                offdiag=cfg.offdiag)
             elif cfg.method == "adc-srrsc" and k > cfg.hss_threshold:
                 from .srrsc_oracle import update_srrsc
                 Qk = update_srrsc(Qk, G, cfg.leaf_size, cfg.srrsc_tol, flops, info)

@@ -41,7 +41,8 @@ class Tree(ctypes.Structure):
                 ("cloc", c_vp), ("flags", c_vp),
                 ("U", c_vp), ("V", c_vp), ("Vt", c_vp), ("B", c_vp), ("D", c_vp), ("rres", c_vp),
                 ("cres", c_vp), ("dld", c_i32),
-                ("M", c_vp), ("psel", c_vp), ("tsel", c_vp), ("ycomp", c_vp), ("zcomp", c_vp), ("rmax", c_i32)]
+                ("M", c_vp), ("psel", c_vp), ("tsel", c_vp), ("ycomp", c_vp), ("zcomp", c_vp), ("rmax", c_i32),
+                ("leaf_of", c_vp)]
 
 
 # name -> (restype, argtypes)
@@ -58,11 +59,11 @@ _SIGS = {
                                            c_i64, c_vp, c_vp, c_vp]),
     "hsseig_normalizers_part": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64,
                                                c_vp, c_vp]),
-    "hsseig_cauchy_sample_part": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_i64, c_i64,
-                                                 c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
-    "hsseig_cauchy_sample_part_peers": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_i64,
-                                                       c_i64, c_i64, c_vp, c_vp, c_i32, c_i64,
-                                                       c_vp, c_vp]),
+    "hsseig_cauchy_sample_part": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_vp, c_i64, c_i64,
+                                                 c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "hsseig_cauchy_sample_part_peers": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_vp, c_i64,
+                                                       c_i64, c_i64, c_i64, c_vp, c_vp, c_i32,
+                                                       c_i64, c_vp, c_vp]),
     "hsseig_sample_peers_fits": (ctypes.c_int, [c_i64, c_i64, c_i64]),
     "hsseig_dnext": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "hsseig_loewner": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp,
@@ -71,19 +72,19 @@ _SIGS = {
     "hsseig_cauchy_block": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_vp, c_i64, c_vp,
                                            c_i64, c_vp]),
     "hsseig_sample_work_doubles": (c_i64, [c_i64, c_i64]),
-    "hsseig_cauchy_sample": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_i64, c_vp, c_vp,
-                                            c_i64, c_vp, c_vp]),
+    "hsseig_cauchy_sample": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_vp, c_i64, c_i64, c_vp,
+                                            c_vp, c_i64, c_vp, c_vp]),
     "hsseig_tree_bytes": (c_i64, [c_i32, c_i32, c_i32, c_i32]),
     "hsseig_tree_layout": (ctypes.c_int, [ctypes.POINTER(Tree), ctypes.POINTER(c_i32), c_i32,
                                           c_i32, c_vp, c_vp]),
     "hsseig_hss_build_rand": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_vp, c_vp, c_i64,
-                                             c_dbl, ctypes.POINTER(Tree), c_vp, c_vp]),
+                                             c_dbl, c_i32, ctypes.POINTER(Tree), c_vp, c_vp]),
     "hsseig_tree_clear": (ctypes.c_int, [ctypes.POINTER(Tree), c_vp]),
     "hsseig_interp_smem_bytes": (c_i64, [c_i32, c_i32]),
     "hsseig_interp_decomp": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i32, c_i32, c_i64, c_dbl, c_i32,
                                             c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "hsseig_hss_build_rand_levels": (ctypes.c_int, [ctypes.POINTER(Gen), c_vp, c_i64, c_vp, c_vp,
-                                                    c_i64, c_dbl, ctypes.POINTER(Tree), c_vp,
+                                                    c_i64, c_dbl, c_i32, ctypes.POINTER(Tree), c_vp,
                                                     ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                     ctypes.c_int, c_vp]),
     "hsseig_srrsc_work_doubles": (c_i64, [ctypes.POINTER(Tree)]),

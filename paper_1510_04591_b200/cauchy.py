@@ -76,14 +76,18 @@ class CauchyEvecMatrix:
         idx = torch.arange(self.k, device="cuda")
         return self.block(idx, idx, flops=flops, phase=phase)
 
-    def sample(self, omega, flops=None, phase="hss_construct"):
-        """(Y, Z) = (C @ Omega, C^T @ Omega) from one generator pass each (cauchy.py:70-100)."""
+    def sample(self, omega, flops=None, phase="hss_construct", leaf_of=None):
+        """(Y, Z) = (C @ Omega, C^T @ Omega) from one generator pass each (cauchy.py:70-100).
+
+        leaf_of (device int32 per index, a tree's ``ct.leaf_of``): the off-diagonal sample
+        instead, every leaf's diagonal block C(t, t) counted as zero (Y_t = Phi_t directly)."""
         omega = dev(omega)
         if omega.ndim != 2 or omega.shape[0] != self.k:
             raise ValueError(f"shape mismatch: C is {self.k}x{self.k}, Omega has {tuple(omega.shape)}")
         w = omega.shape[1]
         if w > MAX_SAMPLE_WIDTH:
-            parts = [self.sample(omega[:, s:s + MAX_SAMPLE_WIDTH]) for s in range(0, w, MAX_SAMPLE_WIDTH)]
+            parts = [self.sample(omega[:, s:s + MAX_SAMPLE_WIDTH], leaf_of=leaf_of)
+                     for s in range(0, w, MAX_SAMPLE_WIDTH)]
             Y, Z = torch.cat([p[0] for p in parts], 1), torch.cat([p[1] for p in parts], 1)
         else:
             lib = nat.load()
@@ -95,7 +99,7 @@ class CauchyEvecMatrix:
             Z = torch.empty_like(Y)
             work = torch.empty(int(lib.hsseig_sample_work_doubles(self.k, w)), dtype=torch.float64,
                                device="cuda")
-            nat.check(lib.hsseig_cauchy_sample(self._gen, nat.ptr(omega), omega.stride(0), w,
+            nat.check(lib.hsseig_cauchy_sample(self._gen, leaf_of, nat.ptr(omega), omega.stride(0), w,
                                                nat.ptr(Y), nat.ptr(Z), w, nat.ptr(work),
                                                nat.stream_ptr()), "cauchy_sample")
         if flops is not None:

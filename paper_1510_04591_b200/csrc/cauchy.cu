@@ -76,12 +76,14 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
       const int64_t kend = imin64(k, kbeg + kchunk);
       const int nch = (int)((kend - kbeg + T::BK - 1) / T::BK);
       double fd[FR], f1[FR], f2[FR], f3[FR], f4[FR];
+      int fl[FR];
       bool fok[FR];
 #pragma unroll
       for (int u = 0; u < FR; ++u) {
         const int64_t fix = m0 + a0 + u * RS;
         fok[u] = fix < row1;
         const int64_t fi = fok[u] ? fix : 0;
+        fl[u] = g.lid ? __ldg(g.lid + fi) : -1;
         fd[u] = __ldg(g.d + fi);
         if (TRANS) {   // column j = fix of C
           f1[u] = __ldg(g.dnext + fi); f2[u] = __ldg(g.gam + fi); f3[u] = __ldg(g.mu + fi);
@@ -92,9 +94,11 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
         }
       }
       // K-running generator data of the next chunk is loaded one chunk ahead
-      auto load_var = [&](int cc, double& od, double& o1, double& o2, double& o3, double& o4) {
+      auto load_var = [&](int cc, double& od, double& o1, double& o2, double& o3, double& o4,
+                          int& ol) {
         const int64_t vv = kbeg + (int64_t)cc * T::BK + vk;
         const int64_t vi = vv < kend ? vv : 0;
+        ol = g.lid ? __ldg(g.lid + vi) : -2;
         od = __ldg(g.d + vi);
         if (TRANS) {
           o4 = __ldg(g.zhat + vi);
@@ -105,20 +109,22 @@ __global__ void __launch_bounds__((T::CONSUMERS + kGenWarps) * 32, 1)
         }
       };
       double nd = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0, n4 = 0.0;
-      if (nch > 0) load_var(0, nd, n1, n2, n3, n4);
+      int nl = -2;
+      if (nch > 0) load_var(0, nd, n1, n2, n3, n4, nl);
       for (int c = 0; c < nch; ++c, ++q) {
         const int slot = q % T::STAGES;
         const int64_t var = kbeg + (int64_t)c * T::BK + vk;   // index running along K
         const bool vok = var < kend;
         const double vd = nd, v1 = n1, v2 = n2, v3 = n3, v4 = n4;
-        if (c + 1 < nch) load_var(c + 1, nd, n1, n2, n3, n4);
+        const int vl = nl;
+        if (c + 1 < nch) load_var(c + 1, nd, n1, n2, n3, n4, nl);
         mbar_wait(&empty[slot], ((q / T::STAGES) & 1) ^ 1);
         double* sA = reinterpret_cast<double*>(sm + (size_t)slot * T::STAGE_BYTES);
 #pragma unroll
         for (int u = 0; u < FR; ++u) {
           const int64_t fix = m0 + a0 + u * RS;
           double val = 0.0;
-          if (fok[u] && vok) {
+          if (fok[u] && vok && vl != fl[u]) {   // off-diagonal sample: own leaf block zero
             double gap;
             if (TRANS)   // C[var][fix]: row var, column fix
               gap = stable_gap(var, fix, vd, fd[u], f1[u], f2[u], f3[u]);
@@ -324,8 +330,10 @@ static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int
 // ---------------------------------------------------------------------------
 constexpr double kMatCapBytes = 12.0 * (1 << 30);   // largest panel pair materialised
 
-// out[i][j] = C[i0 + i][j0 + j] for i < ni, j < nj (MUFU reciprocal + 2 Newton steps, as the
-// fused sampling kernel: within 2 ulp of the reference's division)
+// out[i][j] = C[i0 + i][j0 + j] for i < ni, j < nj.  DIV (the dense update's panels): the
+// reference's entry bit for bit, (zhat_i v_j) / gap with IEEE division; otherwise (the
+// sample) the MUFU reciprocal + 2 Newton steps, within 2 ulp.  With g.lid set the entries of
+// the diagonal leaf blocks (lid[i] == lid[j]) are zero: the off-diagonal sample.
 template <bool DIV>
 __global__ void gen_panel_kernel(CauchyGen g, int64_t i0, int64_t ni, int64_t j0, int64_t nj,
                                  double* __restrict__ out, int64_t ld) {
@@ -334,11 +342,13 @@ __global__ void gen_panel_kernel(CauchyGen g, int64_t i0, int64_t ni, int64_t j0
   const int64_t gj = j0 + j;
   const double dj = __ldg(g.d + gj), dnj = __ldg(g.dnext + gj), gmj = __ldg(g.gam + gj);
   const double mj = __ldg(g.mu + gj), vj = __ldg(g.v + gj);
+  const int lj = g.lid ? __ldg(g.lid + gj) : -1;
   for (int64_t i = blockIdx.y; i < ni; i += gridDim.y) {
     const int64_t gi = i0 + i;
     const double gap = stable_gap(gi, gj, __ldg(g.d + gi), dj, dnj, gmj, mj);
-    // DIV: the reference's entry (to_dense, IEEE division); else MUFU reciprocal + 2 Newton
-    out[i * ld + j] = DIV ? (__ldg(g.zhat + gi) * vj) / gap : (__ldg(g.zhat + gi) * vj) * rcp_nr(gap);
+    double val = DIV ? (__ldg(g.zhat + gi) * vj) / gap : (__ldg(g.zhat + gi) * vj) * rcp_nr(gap);
+    if (g.lid && __ldg(g.lid + gi) == lj) val = 0.0;
+    out[i * ld + j] = val;
   }
 }
 
@@ -598,14 +608,16 @@ extern "C" int64_t hsseig_sample_work_doubles(int64_t k, int64_t w) {
   return need;
 }
 
-extern "C" int hsseig_cauchy_sample_part(const hsseig_gen* gen, const double* omega, int64_t ldom,
-                                         int64_t w, int64_t row0, int64_t row1, double* Y, double* Z,
-                                         int64_t ldy, double* work, void* stream) {
+extern "C" int hsseig_cauchy_sample_part(const hsseig_gen* gen, const int32_t* leaf_of,
+                                         const double* omega, int64_t ldom, int64_t w, int64_t row0,
+                                         int64_t row1, double* Y, double* Z, int64_t ldy,
+                                         double* work, void* stream) {
   if (!gen || w < 1 || w > 128 || ldom < w || ldy < w || row0 < 0 || row1 > gen->k || row0 > row1)
     HSS_ARG_FAIL();
   if ((reinterpret_cast<uintptr_t>(omega) & 15) || (ldom & 1)) HSS_ARG_FAIL();  // TMA rows
   if (row0 == row1) return HSSEIG_OK;
   CauchyGen g = to_gen(gen);
+  g.lid = leaf_of;
   cudaStream_t s = (cudaStream_t)stream;
   static const bool fused_only = getenv("HSSEIG_SAMPLE_FUSED") != nullptr;
   if (!fused_only && w <= 112 && mat_fits(gen->k, row1 - row0) &&
@@ -621,11 +633,11 @@ extern "C" int hsseig_cauchy_sample_part(const hsseig_gen* gen, const double* om
 
 // Rows [row0, row1) of Y and Z written straight into every rank's full Y / Z (row-major,
 // leading dimension ldy): the split-K reductions store to the peers' IPC-mapped buffers.
-extern "C" int hsseig_cauchy_sample_part_peers(const hsseig_gen* gen, const double* omega,
-                                               int64_t ldom, int64_t w, int64_t row0, int64_t row1,
-                                               const uint64_t* Yp, const uint64_t* Zp,
-                                               int32_t npeers, int64_t ldy, double* work,
-                                               void* stream) {
+extern "C" int hsseig_cauchy_sample_part_peers(const hsseig_gen* gen, const int32_t* leaf_of,
+                                               const double* omega, int64_t ldom, int64_t w,
+                                               int64_t row0, int64_t row1, const uint64_t* Yp,
+                                               const uint64_t* Zp, int32_t npeers, int64_t ldy,
+                                               double* work, void* stream) {
   if (!gen || w < 1 || w > 112 || ldom < w || ldy < w || row0 < 0 || row1 > gen->k ||
       row0 > row1 || !Yp || !Zp || npeers < 1 || !work)
     HSS_ARG_FAIL();
@@ -635,8 +647,10 @@ extern "C" int hsseig_cauchy_sample_part_peers(const hsseig_gen* gen, const doub
   if (!mat_fits(gen->k, row1 - row0)) HSS_ARG_FAIL();   // the materialised path only
   if (row0 == row1) return HSSEIG_OK;
   const PeerOut py{Yp, npeers, row0, ldy}, pz{Zp, npeers, row0, ldy};
-  return launch_sample_mat(to_gen(gen), omega, ldom, (int)w, row0, row1, nullptr, nullptr, ldy,
-                           work, (cudaStream_t)stream, &py, &pz);
+  CauchyGen g = to_gen(gen);
+  g.lid = leaf_of;
+  return launch_sample_mat(g, omega, ldom, (int)w, row0, row1, nullptr, nullptr, ldy, work,
+                           (cudaStream_t)stream, &py, &pz);
 }
 
 // Whether hsseig_cauchy_sample_part_peers takes a row range of `nrows` rows of an order-k
@@ -646,11 +660,12 @@ extern "C" int hsseig_sample_peers_fits(int64_t k, int64_t nrows, int64_t w) {
   return (k >= 1 && nrows >= 0 && nrows <= k && w >= 1 && w <= 112 && mat_fits(k, nrows)) ? 1 : 0;
 }
 
-extern "C" int hsseig_cauchy_sample(const hsseig_gen* gen, const double* omega, int64_t ldom,
-                                    int64_t w, double* Y, double* Z, int64_t ldy, double* work,
-                                    void* stream) {
+extern "C" int hsseig_cauchy_sample(const hsseig_gen* gen, const int32_t* leaf_of,
+                                    const double* omega, int64_t ldom, int64_t w, double* Y,
+                                    double* Z, int64_t ldy, double* work, void* stream) {
   if (!gen) HSS_ARG_FAIL();
-  return hsseig_cauchy_sample_part(gen, omega, ldom, w, 0, gen->k, Y, Z, ldy, work, stream);
+  return hsseig_cauchy_sample_part(gen, leaf_of, omega, ldom, w, 0, gen->k, Y, Z, ldy, work,
+                                   stream);
 }
 
 extern "C" int hsseig_dense_update(const double* Qb, int64_t ldq, int64_t P, const hsseig_gen* gen,

@@ -99,6 +99,9 @@ struct CauchyGen {
   const double* zhat;
   const double* v;
   int64_t k;
+  // leaf id of every index (tree partition) for the off-diagonal sample, or nullptr: the
+  // sampling kernels then skip the diagonal leaf blocks (C(t, t) = 0 in the product)
+  const int32_t* lid = nullptr;
 
   __device__ __forceinline__ double entry(int64_t i, int64_t j) const {
     double g = stable_gap(i, j, __ldg(d + i), __ldg(d + j), __ldg(dnext + j), __ldg(gam + j),

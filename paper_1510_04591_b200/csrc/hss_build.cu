@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
                                                         int64_t ldom,
                                                         const double* __restrict__ Y,
                                                         const double* __restrict__ Z,
-                                                        int64_t ldy, int j0) {
+                                                        int64_t ldy, int j0, int offdiag) {
   // D Omega_t on the DMMA pipe: 16-row chunks of D generated in shared memory (A operand,
   // row stride SD = 4 mod 8), Omega_t resident (B operand, row stride SO = 8|24 mod 32),
   // 2 x ceil(w/8) output fragments of 8 x 8 spread over the 8 warps, K padded to 4 with zeros
@@ -67,6 +67,21 @@ __global__ void __launch_bounds__(256) leaf_form_kernel(CauchyGen g, TreeDev T,
       const int a = e / T.dld - 1, b = e % T.dld;
       if (a < 0 || a >= m || b >= m) Dslot[e] = 0.0;
     }
+  }
+  if (offdiag) {
+    // off-diagonal sample: Y_t, Z_t already are Phi, Theta (no D Omega_t to subtract);
+    // side 0 still generates D for the tree
+    for (int e = tid; e < m * w; e += blockDim.x) {
+      const int a = e / w, c = e % w;
+      Mo[(size_t)a * T.ws + c] = src[(int64_t)(lo + a) * ldy + c];
+    }
+    if (side == 0) {
+      for (int e = tid; e < m * m; e += blockDim.x) {
+        const int a = e / m, b = e % m;
+        Dslot[(size_t)(a + 1) * T.dld + b] = g.entry(lo + a, lo + b);
+      }
+    }
+    return;
   }
   const int gr = lane >> 2, gc = lane & 3;
   for (int a0 = 0; a0 < m; a0 += RA) {
@@ -656,10 +671,26 @@ using namespace hsseig;
 
 static int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+// leaf_of[i] = position of the leaf holding index i (binary search over the leaf starts)
+__global__ void leaf_of_kernel(const int32_t* __restrict__ lo, const int32_t* __restrict__ left,
+                               const int32_t* __restrict__ lnodes, int depth, int n_leaves,
+                               int32_t k, int32_t* __restrict__ leaf_of) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k) return;
+  const int32_t* leaves = lnodes + (1 << depth) - 1;   // leaf node ids by position
+  int a = 0, b = n_leaves - 1;
+  while (a < b) {
+    const int mid = (a + b + 1) >> 1;
+    if (lo[leaves[mid]] <= i) a = mid; else b = mid - 1;
+  }
+  (void)left;
+  leaf_of[i] = a;
+}
+
 struct TreeCarve {
   int64_t off_lo, off_hi, off_left, off_right, off_lnodes, off_rU, off_rV, off_rsel, off_csel,
       off_rloc, off_cloc, off_flags, off_U, off_V, off_Vt, off_B, off_D, off_rres, off_cres, off_M,
-      off_psel, off_tsel, off_ycomp, off_zcomp, total;
+      off_psel, off_tsel, off_ycomp, off_zcomp, off_lid, total;
 };
 
 static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
@@ -685,8 +716,8 @@ static TreeCarve carve(int32_t k, int32_t n_leaves, int32_t w, int32_t mmax) {
   c.off_M = take(8 * 2 * (int64_t)n_leaves * pmax * ws);
   c.off_psel = take(8 * nn * ws * ws); c.off_tsel = take(8 * nn * ws * ws);
   c.off_ycomp = take(8 * nn * ws * ws); c.off_zcomp = take(8 * nn * ws * ws);
+  c.off_lid = take(4 * (int64_t)k);
   c.total = o;
-  (void)k;
   return c;
 }
 
@@ -767,6 +798,7 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
   t->tsel = reinterpret_cast<double*>(base + c.off_tsel);
   t->ycomp = reinterpret_cast<double*>(base + c.off_ycomp);
   t->zcomp = reinterpret_cast<double*>(base + c.off_zcomp);
+  t->leaf_of = reinterpret_cast<int32_t*>(base + c.off_lid);
   cudaStream_t s = (cudaStream_t)stream;
   void* dst[5] = {(void*)t->lo, (void*)t->hi, (void*)t->left, (void*)t->right, (void*)t->level_nodes};
   const void* src[5] = {lo.data(), hi.data(), left.data(), right.data(), lnodes.data()};
@@ -779,6 +811,10 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
             cudaMemsetAsync(t->V, 0, (size_t)8 * nn * t->pmax * t->ws, s) == cudaSuccess &&
             cudaMemsetAsync(t->B, 0, (size_t)8 * nn * t->ws * t->ws, s) == cudaSuccess;
   if (!ok) return HSSEIG_ERR_CUDA;
+  // leaf id of every index (the off-diagonal sample masks the diagonal leaf blocks)
+  leaf_of_kernel<<<(unsigned)((k + 255) / 256), 256, 0, s>>>(t->lo, t->left, t->level_nodes, depth,
+                                                             n_leaves, k, t->leaf_of);
+  HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
 
@@ -786,9 +822,9 @@ extern "C" int hsseig_tree_layout(hsseig_tree* t, const int32_t* bounds, int32_t
 // the node positions of part `part` of `nparts` (positions are split evenly, so a part is
 // the subtree set under level log2(nparts)); the root's skeleton blocks when lev_to == 0.
 static int build_levels(const hsseig_gen* gen, const double* omega, int64_t ldom, const double* Y,
-                        const double* Z, int64_t ldy, double id_tol, hsseig_tree* tree,
-                        hsseig_status* st, int lev_from, int lev_to, int part, int nparts,
-                        cudaStream_t s) {
+                        const double* Z, int64_t ldy, double id_tol, int offdiag,
+                        hsseig_tree* tree, hsseig_status* st, int lev_from, int lev_to, int part,
+                        int nparts, cudaStream_t s) {
   if (!gen || !tree || !omega || !Y || !Z || !st || gen->k != tree->k) HSS_ARG_FAIL();
   if (tree->w > tree->mmax || tree->w > 128) HSS_ARG_FAIL();
   if (nparts < 1 || (nparts & (nparts - 1)) || part < 0 || part >= nparts) HSS_ARG_FAIL();
@@ -815,7 +851,7 @@ static int build_levels(const hsseig_gen* gen, const double* omega, int64_t ldom
     const int cnt = npos / nparts, j0 = part * cnt;
     dim3 grid(cnt, 2);
     if (lev == T.depth) {
-      leaf_form_kernel<<<grid, 256, smem_leaf, s>>>(g, T, omega, ldom, Y, Z, ldy, j0);
+      leaf_form_kernel<<<grid, 256, smem_leaf, s>>>(g, T, omega, ldom, Y, Z, ldy, j0, offdiag);
     } else {
       genB_kernel<<<grid, 256, 0, s>>>(g, T, lev, j0);
       HSS_CHECK_LAUNCH();
@@ -847,21 +883,22 @@ extern "C" int hsseig_tree_clear(hsseig_tree* tree, void* stream) {
 
 extern "C" int hsseig_hss_build_rand(const hsseig_gen* gen, const double* omega, int64_t ldom,
                                      const double* Y, const double* Z, int64_t ldy, double id_tol,
-                                     hsseig_tree* tree, hsseig_status* st, void* stream) {
+                                     int32_t offdiag, hsseig_tree* tree, hsseig_status* st,
+                                     void* stream) {
   if (!tree) HSS_ARG_FAIL();
   const int rc = hsseig_tree_clear(tree, stream);
   if (rc) return rc;
-  return build_levels(gen, omega, ldom, Y, Z, ldy, id_tol, tree, st, tree->depth, 0, 0, 1,
-                      (cudaStream_t)stream);
+  return build_levels(gen, omega, ldom, Y, Z, ldy, id_tol, offdiag, tree, st, tree->depth, 0, 0,
+                      1, (cudaStream_t)stream);
 }
 
 extern "C" int hsseig_hss_build_rand_levels(const hsseig_gen* gen, const double* omega,
                                             int64_t ldom, const double* Y, const double* Z,
-                                            int64_t ldy, double id_tol, hsseig_tree* tree,
-                                            hsseig_status* st, int lev_from, int lev_to, int part,
-                                            int nparts, void* stream) {
-  return build_levels(gen, omega, ldom, Y, Z, ldy, id_tol, tree, st, lev_from, lev_to, part,
-                      nparts, (cudaStream_t)stream);
+                                            int64_t ldy, double id_tol, int32_t offdiag,
+                                            hsseig_tree* tree, hsseig_status* st, int lev_from,
+                                            int lev_to, int part, int nparts, void* stream) {
+  return build_levels(gen, omega, ldom, Y, Z, ldy, id_tol, offdiag, tree, st, lev_from, lev_to,
+                      part, nparts, (cudaStream_t)stream);
 }
 
 extern "C" int64_t hsseig_interp_smem_bytes(int32_t p, int32_t w) {

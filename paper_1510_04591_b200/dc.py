@@ -20,6 +20,7 @@ from .secular import RankOneSystem, dev, dev_rows, recompute_weights, solve_secu
 # the other two); its HSS construction is the SRRSC of oracle/srrsc_oracle.py
 METHODS = ("dense-dc", "adc-rand", "adc-srrsc")
 HSS_METHODS = ("adc-rand", "adc-srrsc")
+SAMPLE_MODES = ("offdiag", "reference")
 
 
 class BaseCaseError(ArithmeticError):
@@ -41,6 +42,10 @@ class SolverConfig:
     # ADC1 only: Schur-complement truncation max|S| <= srrsc_tol * max|block| (the
     # reference's ID truncation tolerance, hss.py:23); the rank cap is the smallest leaf
     srrsc_tol: float = DEFAULT_ID_TOL
+    # ADC2 only: "offdiag" forms the leaves' Phi / Theta from the off-diagonal sample
+    # C(t, t^c) Omega(t^c) (no cancellation against D Omega_t: half the ranks and a smaller
+    # HSS error); "reference" is the reference's Y_t - D_t Omega_t
+    sample: str = "offdiag"
 
     def __post_init__(self):
         if self.base_size < 3:
@@ -55,6 +60,8 @@ class SolverConfig:
             raise ValueError(f"method must be one of {METHODS}")
         if not self.srrsc_tol >= 0.0:
             raise ValueError("srrsc_tol must be non-negative")
+        if self.sample not in SAMPLE_MODES:
+            raise ValueError(f"sample must be one of {SAMPLE_MODES}")
 
 
 @dataclass
@@ -150,7 +157,8 @@ def update_vectors_hss(Qblock, C, cfg, seed=0, flops=None, record=None, omega=No
         r = min(r_est, part.min_leaf - cfg.oversample)
         if r < 1 or r + cfg.oversample > MAX_WIDTH:
             return dense_fallback()
-        H = rand_hss_construct(C, part, r, p=cfg.oversample, seed=seed, flops=flops, omega=omega)
+        H = rand_hss_construct(C, part, r, p=cfg.oversample, seed=seed, flops=flops, omega=omega,
+                               offdiag=cfg.sample == "offdiag")
     if H.flagged:
         return dense_fallback()
     if record is not None:
@@ -234,7 +242,8 @@ def update_vectors_hss_many(jobs, cfg, max_streams=8):
         for (j, part, r), om, s in zip(live, oms, st):
             with torch.cuda.stream(s):
                 trees.append(rand_hss_construct(j.C, part, r, p=cfg.oversample, seed=j.seed,
-                                                omega=om, finish=False))
+                                                omega=om, finish=False,
+                                                offdiag=cfg.sample == "offdiag"))
         del oms
     for (j, _, _), H, s in zip(live, trees, st):
         with torch.cuda.stream(s):

@@ -184,8 +184,11 @@ class ShardedMerge:
                 w = r + cfg.oversample
                 if r >= 1 and w <= ops.max_width:
                     om = ops.omega(seed, k, w)
+                    # the off-diagonal sample (default) masks the leaves' diagonal blocks
+                    offdiag = getattr(cfg, "sample", "offdiag") == "offdiag"
+                    mask = part if offdiag else None
                     fused = getattr(ops, "sample_gather", None)
-                    YZ = fused(gen, om, w, lo, hi, self.group) if fused else None
+                    YZ = fused(gen, om, w, lo, hi, self.group, mask) if fused else None
                     if YZ is not None:
                         # sample rows stored straight into every rank's Y / Z (one kernel
                         # for the split-K reduction and the all-gather), then one fence
@@ -193,10 +196,10 @@ class ShardedMerge:
                         info["sample_gather"] = "peer"
                     else:
                         info["sample_gather"] = "nccl"
-                        Y_l, Z_l = ops.sample_part(gen, om, w, lo, hi)
+                        Y_l, Z_l = ops.sample_part(gen, om, w, lo, hi, mask)
                         Y = gather_rows(Y_l, c, k, self.group)
                         Z = gather_rows(Z_l, c, k, self.group)
-                    tree = ops.build(gen, part, w, om, Y, Z, self.group)
+                    tree = ops.build(gen, part, w, om, Y, Z, self.group, offdiag)
         if tree is not None and not ops.flagged(tree):
             info["used_hss"] = True
             info["r_used"] = ops.r_used(tree)
@@ -383,17 +386,32 @@ class GpuOps:
                                         device="cuda")
         return om
 
-    def sample_part(self, gen, om, w, lo, hi):
+    def tree_for(self, part, w):
+        """The construction's tree (cached per partition and width); its leaf_of masks the
+        off-diagonal sample."""
+        from .hss import HssTree
+        key = (part.ranges, w)
+        if key not in self._trees:
+            self._trees = {key: HssTree(part, w)}
+        return self._trees[key]
+
+    def _leaf_of(self, part, w):
+        return self.tree_for(part, w).ct.leaf_of if part is not None else None
+
+    def sample_part(self, gen, om, w, lo, hi, part=None):
+        """Rows [lo, hi) of Y = C Omega and Z = C^T Omega; with `part` the off-diagonal
+        sample (the partition's diagonal leaf blocks masked)."""
         nat = self.nat
         ws = om.shape[1]
         Y = torch.empty(hi - lo, ws, dtype=torch.float64, device="cuda")
         Z = torch.empty_like(Y)
-        nat.check(self.lib.hsseig_cauchy_sample_part(gen.gen, nat.ptr(om), ws, w, lo, hi, nat.ptr(Y),
-                                                     nat.ptr(Z), ws, nat.ptr(self.sample_work),
-                                                     self._s()), "cauchy_sample_part")
+        nat.check(self.lib.hsseig_cauchy_sample_part(gen.gen, self._leaf_of(part, w), nat.ptr(om),
+                                                     ws, w, lo, hi, nat.ptr(Y), nat.ptr(Z), ws,
+                                                     nat.ptr(self.sample_work), self._s()),
+                  "cauchy_sample_part")
         return Y, Z
 
-    def sample_gather(self, gen, om, w, lo, hi, group=None):
+    def sample_gather(self, gen, om, w, lo, hi, group=None, part=None):
         """Y = C Omega, Z = C^T Omega on every rank with this rank's rows [lo, hi) computed
         here and stored into all ranks' copies by the reduction kernels (CUDA IPC peers);
         None when the fused path does not apply (one rank, HSSEIG_PEER=0, a panel above the
@@ -421,7 +439,8 @@ class GpuOps:
         if not pb.ok:
             return None
         self._peer_n += 1
-        rc = self.lib.hsseig_cauchy_sample_part_peers(gen.gen, nat.ptr(om), ws, w, lo, hi,
+        rc = self.lib.hsseig_cauchy_sample_part_peers(gen.gen, self._leaf_of(part, w),
+                                                      nat.ptr(om), ws, w, lo, hi,
                                                       nat.ptr(pb.ptrs[0]), nat.ptr(pb.ptrs[1]),
                                                       world, ws, nat.ptr(self.sample_work),
                                                       self._s())
@@ -430,22 +449,21 @@ class GpuOps:
         peer_fence(group)
         return pb.local[0], pb.local[1]
 
-    def build(self, gen, part, w, om, Y, Z, group=None):
+    def build(self, gen, part, w, om, Y, Z, group=None, offdiag=True):
         """Construction; with several ranks each builds its subtrees below level log2(world),
-        the subtree slots are all-gathered and the upper levels are built on every rank."""
-        from .hss import HssTree, finish_construct
+        the subtree slots are all-gathered and the upper levels are built on every rank.
+        offdiag: Y / Z are the off-diagonal sample (sample_part / sample_gather with part)."""
+        from .hss import finish_construct
         from .secular import Status
         nat = self.nat
-        key = (part.ranges, w)
-        if key not in self._trees:
-            self._trees = {key: HssTree(part, w)}
-        tree = self._trees[key]
+        tree = self.tree_for(part, w)
+        tree.offdiag = bool(offdiag)
         tree._ranks = None
         st = Status(self.k)
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         args = (gen.gen, nat.ptr(om), om.shape[1], nat.ptr(Y), nat.ptr(Z), Y.shape[1], 1e-15,
-                ctypes.byref(tree.ct), nat.ptr(st.t))
+                int(bool(offdiag)), ctypes.byref(tree.ct), nat.ptr(st.t))
         depth = tree.ct.depth
         if world > 1 and (1 << depth) >= world and (world & (world - 1)) == 0:
             s_lev = world.bit_length() - 1

@@ -478,8 +478,13 @@ def draw_omegas(specs, streams=None):
 
 
 def rand_hss_construct(A, partition, r, p=10, seed=0, id_tol=DEFAULT_ID_TOL, flops=None,
-                       omega=None, finish=True):
-    """Randomized bottom-up construction from one Gaussian sample (hss.py:217-306)."""
+                       omega=None, finish=True, offdiag=True):
+    """Randomized bottom-up construction from one Gaussian sample (hss.py:217-306).
+
+    offdiag (default): the leaves' Phi / Theta come from the off-diagonal sample
+    C(t, t^c) Omega(t^c) instead of Y_t - D_t Omega_t (hss.py:265-266); mathematically the
+    same matrices, without the cancellation that leaves the sample's rounding noise for the
+    ID to truncate against.  offdiag=False is the reference's arithmetic."""
     if partition.n_leaves < 2:
         raise ValueError("need at least two leaves; use the dense path instead")
     if r < 1 or p < 0:
@@ -490,13 +495,14 @@ def rand_hss_construct(A, partition, r, p=10, seed=0, id_tol=DEFAULT_ID_TOL, flo
     if w > MAX_WIDTH:
         raise ValueError(f"sample width {w} above the supported {MAX_WIDTH}")
     om = dev(omega) if omega is not None else draw_omega(A.k, w, seed)
-    Y, Z = A.sample(om)
     tree = HssTree(partition, w, seed=seed)
+    tree.offdiag = bool(offdiag)
+    Y, Z = A.sample(om, leaf_of=tree.ct.leaf_of if offdiag else None)
     st = Status(A.k)
     nat.check(nat.load().hsseig_hss_build_rand(A.gen, nat.ptr(om), om.stride(0), nat.ptr(Y),
                                                nat.ptr(Z), Y.stride(0), float(id_tol),
-                                               ctypes.byref(tree.ct), nat.ptr(st.t),
-                                               nat.stream_ptr()), "hss_build_rand")
+                                               int(bool(offdiag)), ctypes.byref(tree.ct),
+                                               nat.ptr(st.t), nat.stream_ptr()), "hss_build_rand")
     tree._status = st
     tree._omega = om
     if finish:

@@ -208,17 +208,19 @@ class MergePipeline:
                     else:
                         hv = self.host_omega.finish(k * w)
                         om[:, :w].copy_(hv.view(k, w), non_blocking=True)
+                    tree = self._tree(part, w)
+                    tree._status = _StatusView(self.status)
+                    offdiag = getattr(cfg, "sample", "offdiag") == "offdiag"
+                    tree.offdiag = offdiag
                     ev[3].record()
                     Y = self.Y[:k * ws].view(k, ws)
                     Z = self.Z[:k * ws].view(k, ws)
-                    nat.check(lib.hsseig_cauchy_sample(C.gen, nat.ptr(om), ws, w, nat.ptr(Y),
-                                                       nat.ptr(Z), ws, nat.ptr(self.sample_work), s),
-                              "cauchy_sample")
+                    nat.check(lib.hsseig_cauchy_sample(C.gen, tree.ct.leaf_of if offdiag else None,
+                                                       nat.ptr(om), ws, w, nat.ptr(Y), nat.ptr(Z), ws,
+                                                       nat.ptr(self.sample_work), s), "cauchy_sample")
                     ev[4].record()
-                    tree = self._tree(part, w)
-                    tree._status = _StatusView(self.status)
                     nat.check(lib.hsseig_hss_build_rand(C.gen, nat.ptr(om), ws, nat.ptr(Y),
-                                                        nat.ptr(Z), ws, float(1e-15),
+                                                        nat.ptr(Z), ws, float(1e-15), int(offdiag),
                                                         ctypes.byref(tree.ct), nat.ptr(self.status),
                                                         s), "hss_build_rand")
                     ev[5].record()

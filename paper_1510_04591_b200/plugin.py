@@ -11,6 +11,15 @@
 * ``merge_update(Qk, d, z, rho, cfg, seed, flops, record)`` — the merge body of
   dc.py:236-247 for one post-deflation system; returns (lam, Qk_new) as NumPy arrays
   (or torch CUDA tensors when Qk is one).
+* ``update_vectors_hss(Qblock, C, cfg, seed, flops, record)`` and
+  ``update_vectors_dense(Qblock, Qprime, flops)`` — drop-ins for the reference's own
+  functions of the same names (dc.py:132-171), called with the REFERENCE's objects (its
+  ``CauchyEvecMatrix`` generators, ``SolverConfig``, ``FlopCounter``, ``MergeRecord``),
+  NumPy in / NumPy out: rebinding ``hsseig.dc.update_vectors_hss`` /
+  ``update_vectors_dense`` routes the update branch of ``_solve_rec`` (dc.py:241-246) to
+  the GPU with no other change to the reference.
+* ``kernels()`` — a kernel namespace for ``hsseig.backend`` (``secular_all`` and
+  ``tql2`` on the GPU; the reference's own Jacobi oracle kernels passed through).
 """
 import numpy as np
 import torch
@@ -82,3 +91,48 @@ def merge_update(Qk, d, z, rho, cfg, seed=0, flops=None, record=None):
     if on_device:
         return lam, Qn
     return lam.cpu().numpy(), Qn.cpu().numpy()
+
+
+def _cfg(cfg):
+    """The reference's SolverConfig (or any object with its fields) as ours."""
+    return _dc.SolverConfig(**{f: getattr(cfg, f) for f in
+                               ("base_size", "hss_threshold", "leaf_size", "oversample",
+                                "rank_eps", "rank_cap", "seed", "method")})
+
+
+def update_vectors_hss(Qblock, C, cfg, seed=0, flops=None, record=None):
+    """dc.py:141-171 on the GPU for the reference's own arguments: C is the reference's
+    CauchyEvecMatrix (its generators d, gamma, mu, zhat, v are uploaded; tiles, sample,
+    construction and the multiply run in libhsseig_b200.so), cfg / flops / record are the
+    reference's objects (fields updated in place with its conventions).  NumPy out."""
+    from .cauchy import CauchyEvecMatrix
+    Cd = CauchyEvecMatrix(C.d, C.gamma, C.mu, C.zhat, C.v)
+    Q = torch.as_tensor(np.ascontiguousarray(Qblock, dtype=np.float64), device="cuda")
+    out = _dc.update_vectors_hss(Q, Cd, _cfg(cfg), seed=seed, flops=flops, record=record)
+    return out.cpu().numpy()
+
+
+def update_vectors_dense(Qblock, Qprime, flops=None):
+    """dc.py:132-138 on the GPU (FP64 DMMA GEMM) for NumPy operands; NumPy out."""
+    Qb = np.asarray(Qblock)
+    Qp = np.asarray(Qprime)
+    if Qb.shape[1] != Qp.shape[0]:
+        raise ValueError("inner dimensions do not match")
+    out = _dc.update_vectors_dense(torch.as_tensor(np.ascontiguousarray(Qb, dtype=np.float64),
+                                                   device="cuda"),
+                                   torch.as_tensor(np.ascontiguousarray(Qp, dtype=np.float64),
+                                                   device="cuda"), flops=flops)
+    return out.cpu().numpy()
+
+
+def kernels(reference_kernels=None):
+    """Kernel namespace for hsseig.backend.load_kernels (backend.py:9-17): the GPU
+    secular_all / tql2, and the reference's Jacobi kernels (its test oracle) passed
+    through from `reference_kernels` when given."""
+    import types
+    ns = types.SimpleNamespace(secular_all=secular_all, tql2=tql2)
+    if reference_kernels is not None:
+        for name in ("jacobi_run", "onesided_orthogonalize"):
+            if hasattr(reference_kernels, name):
+                setattr(ns, name, getattr(reference_kernels, name))
+    return ns

@@ -29,6 +29,13 @@ from .secular import SecularConvergenceError, WeightRecomputationError
 _SQRT2 = np.sqrt(2.0)
 MAX_BASE = 160   # largest device base case (csrc/glue.cu kQLBig)
 
+# When a list, solve_subtree appends one (kind, start event, end event, algorithmic bytes)
+# per recursion depth for the HBM-bound glue kernels (bench.py's glue GB/s line):
+#   "assemble": blockdiag(Q1, Q2) columns into W (child entries read, W written) + the
+#               Givens replay (two columns read and written per rotation and row);
+#   "gather":   the final column order (the n x n block read and written).
+GLUE_PROFILE = None
+
 
 def _i64(x):
     return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int64), device="cuda")
@@ -427,6 +434,14 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             .add(rho_eff[segs], np.float64).add(st0).add(woff[segs]).add(nvs).add(qoff[segs])
             .add(tk, np.int32).add(ldw[segs]).send())
         W = torch.empty(max(int(woff[-1]), 2), **f64)
+        prof = GLUE_PROFILE
+        if prof is not None:
+            cm = np.repeat(np.arange(nm), np.diff(coff))
+            src_rows = np.where(csrc[:int(coff[-1])] < n1[cm], n1[cm], n2[cm])
+            rot_rows = np.repeat(nv, np.diff(rot_off))
+            gbytes = 8 * (int((nv * wd).sum()) + int(src_rows.sum())) + 32 * int(rot_rows.sum())
+            ev_g = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev_g[0].record()
         nat.check(lib.hsseig_wave_assemble(nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
                                            nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(csrc_d),
                                            nat.ptr(coff_d), nat.ptr(wd_d), nat.ptr(W), nat.ptr(woff_d),
@@ -436,6 +451,9 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                                              nat.ptr(rot_d0), nat.ptr(rot_d1), nat.ptr(rot_d2),
                                              nat.ptr(rot_d3), nat.ptr(rot_d4), nm, int(nv.max()), s),
                       "wave_rotate")
+        if prof is not None:
+            ev_g[1].record()
+            prof.append(("assemble", ev_g[0], ev_g[1], gbytes))
         Qk = torch.empty(max(int(qoff[-1]), 1), **f64)
         hss_m = set(np.flatnonzero(hss_q).tolist())
         seg_iters = np.zeros(nseg, dtype=np.int64)
@@ -566,11 +584,17 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             base = len(rows_h) + sel_off[:-1]
             last_off[gsel[sel_left]] = base[sel_left]
             first_off[gsel[~sel_left]] = base[~sel_left]
+        if prof is not None:
+            ev_g = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev_g[0].record()
         nat.check(lib.hsseig_wave_gather(nat.ptr(Qk), nat.ptr(g_qoff), nat.ptr(g_kept),
                                          nat.ptr(W), nat.ptr(woff_d), nat.ptr(wd_d), nat.ptr(g_desc),
                                          nat.ptr(q1), nat.ptr(q2), nat.ptr(n1_d), nat.ptr(n2_d),
                                          nat.ptr(roff_d), nat.ptr(row_merge), nat.ptr(A),
                                          nat.ptr(ooff_d), nrows, s), "wave_gather")
+        if prof is not None:
+            ev_g[1].record()
+            prof.append(("gather", ev_g[0], ev_g[1], 16 * int((nv * nv).sum())))
         del W, Qk
         live.pop(depth + 1, None)      # the children's blocks are dead once gathered
         live[depth] = A

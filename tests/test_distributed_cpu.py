@@ -46,15 +46,22 @@ class NumpyOps:
     def omega(self, seed, k, w):
         return torch.as_tensor(orc.sample_block(k, w, seed))
 
-    def sample_part(self, G, om, w, lo, hi):
-        return (torch.as_tensor(G.times(om.numpy())[lo:hi]),
-                torch.as_tensor(G.t_times(om.numpy())[lo:hi]))
+    def _yz(self, G, om, part):
+        if part is not None:           # the off-diagonal sample
+            return orc.offdiag_samples(G, list(part.ranges), om.numpy())
+        return G.times(om.numpy()), G.t_times(om.numpy())
 
-    def build(self, G, part, w, om, Y, Z, group=None):
-        # the gathered samples must be the full products
-        assert np.allclose(Y.numpy(), G.times(om.numpy()), rtol=0, atol=1e-13)
-        assert np.allclose(Z.numpy(), G.t_times(om.numpy()), rtol=0, atol=1e-13)
-        return orc.rand_construct(G, list(part.ranges), w - 10, 10, Omega=om.numpy())
+    def sample_part(self, G, om, w, lo, hi, part=None):
+        Y, Z = self._yz(G, om, part)
+        return torch.as_tensor(Y[lo:hi]), torch.as_tensor(Z[lo:hi])
+
+    def build(self, G, part, w, om, Y, Z, group=None, offdiag=True):
+        # the gathered samples must be the full (off-diagonal) products
+        Yr, Zr = self._yz(G, om, part if offdiag else None)
+        assert np.allclose(Y.numpy(), Yr, rtol=0, atol=1e-13)
+        assert np.allclose(Z.numpy(), Zr, rtol=0, atol=1e-13)
+        return orc.rand_construct(G, list(part.ranges), w - 10, 10, Omega=om.numpy(),
+                                  offdiag=offdiag)
 
     def build_srrsc(self, G, part, cap, tol, group=None):
         from oracle import srrsc_oracle as so
@@ -118,7 +125,7 @@ def test_sharded_merge_world2_matches_single_process(tmp_path, k, P):
     d, u, rho = config4_system(k, 3)
     X = np.random.default_rng(7).standard_normal((P, k))
     G, lam, _ = orc.generators_from_roots(d, u, rho)
-    ref = orc.update_hss(X, G, 64, 10, 1e-13, 100, [0, 0])
+    ref = orc.update_hss(X, G, 64, 10, 1e-13, 100, [0, 0], offdiag=True)
     assert bool(res["used"])
     np.testing.assert_array_equal(res["lam"], lam)
     np.testing.assert_allclose(res["out"], ref, rtol=0, atol=1e-13 * np.abs(ref).max())

@@ -1,0 +1,204 @@
+"""BASELINE.json configs 1-4 at their stated sizes against the unmodified reference's own
+outputs (tests/golden/configs.npz, made by tests/golden/make_golden_configs.py from the
+reference build; the box never reads /root/reference).
+
+north_star's parity rule, enforced here with the reference's entrywise-max formulas
+(cli.py:63-71) computed on both sides:
+* eigenvalues within 1e-12 * max|T|;
+* orthogonality max|Q^T Q - I|/N, backward error max|T - Q L Q^T|/(max|T| N) and the
+  residual max|T Q - Q L|/(N max|T|) no worse than 10x the reference's;
+* merge records identical (size, kept, deflated, route, fallback); the HSS ranks of the
+  default off-diagonal sample never above the reference's noise-inflated
+  ranks (+1 for one QR step), and within a band of them in sample="reference" mode;
+* well-separated eigenvectors equal up to sign (P/tests/conftest.py:36-40).
+The measured GPU/reference ratios are printed (pytest -s) and bench.py reports them too.
+"""
+import numpy as np
+import pytest
+import torch
+
+from helpers import golden
+
+pytestmark = pytest.mark.gpu
+RATIO = 10.0
+
+
+@pytest.fixture(scope="module")
+def g():
+    return golden("configs")
+
+
+def metrics_gpu(T, lam, Q):
+    """(orth, bwd, resid) with the reference's formulas, on the device."""
+    n = T.n
+    Q = Q if isinstance(Q, torch.Tensor) else torch.as_tensor(Q, device="cuda")
+    lam_d = torch.as_tensor(np.asarray(lam), device="cuda")
+    G = Q.T @ Q
+    G.diagonal().sub_(1.0)
+    orth = float(G.abs().max()) / n
+    del G
+    A = torch.zeros(n, n, dtype=torch.float64, device="cuda")
+    i = torch.arange(n, device="cuda")
+    A[i, i] = torch.as_tensor(T.a, device="cuda")
+    A[i[:-1], i[1:]] = torch.as_tensor(T.b, device="cuda")
+    A[i[1:], i[:-1]] = torch.as_tensor(T.b, device="cuda")
+    A -= (Q * lam_d[None, :]) @ Q.T
+    bwd = float(A.abs().max()) / (T.norm_max() * n)
+    del A
+    a = torch.as_tensor(T.a, device="cuda")
+    b = torch.as_tensor(T.b, device="cuda")
+    TQ = a[:, None] * Q
+    TQ[:-1] += b[:, None] * Q[1:]
+    TQ[1:] += b[:, None] * Q[:-1]
+    resid = float((TQ - Q * lam_d[None, :]).abs().max()) / (n * T.norm_max())
+    return orth, bwd, resid
+
+
+def records(res):
+    return np.array([[m.size, m.kept, m.n_deflated, int(m.used_hss), m.hss_rank, int(m.fell_back)]
+                     for m in res.merges], dtype=np.int64)
+
+
+def check_solve(g, tag, T, res, rank_band=0, label="", offdiag=True):
+    nT = T.norm_max()
+    lam = np.asarray(res.lam)
+    lam_ref = g[f"{tag}_lam"]
+    err = float(np.abs(lam - lam_ref).max())
+    assert err <= 1e-12 * nT, (tag, err)
+    rec, rec_ref = records(res), g[f"{tag}_merges"]
+    assert rec.shape == rec_ref.shape
+    cols = [0, 1, 2, 3, 5]                       # everything but the HSS rank: identical
+    assert np.array_equal(rec[:, cols], rec_ref[:, cols]), tag
+    hss = rec_ref[:, 3] == 1
+    dr = rec[:, 4] - rec_ref[:, 4]
+    if offdiag:
+        assert int(dr.max(initial=0)) <= 1, (tag, rec[:, 4][dr > 1], rec_ref[:, 4][dr > 1])
+    else:
+        assert int(np.abs(dr).max(initial=0)) <= rank_band, (tag, rec[:, 4][dr != 0],
+                                                            rec_ref[:, 4][dr != 0])
+    if hss.any():
+        print(f"\n{tag}: HSS merge ranks vs reference: mean {dr[hss].mean():+.1f} "
+              f"[{dr[hss].min()}, {dr[hss].max()}]")
+    o, b, r = metrics_gpu(T, lam, res.Q)
+    o0, b0, r0 = (float(g[f"{tag}_{m}"]) for m in ("orth", "bwd", "resid"))
+    print(f"\n{label or tag}: eig err {err / nT:.2e}||T||  orth {o:.3e} (ref {o0:.3e}, x{o / o0:.2f})"
+          f"  bwd {b:.3e} (ref {b0:.3e}, x{b / b0:.2f})  resid {r:.3e} (ref {r0:.3e}, x{r / r0:.2f})")
+    assert o <= RATIO * o0, (tag, o, o0)
+    assert b <= RATIO * b0, (tag, b, b0)
+    assert r <= RATIO * r0, (tag, r, r0)
+    return o / o0, b / b0, r / r0
+
+
+def check_columns(g, tag, T, res):
+    """Eigenvectors with gap >= 1e-8 max|T| agree with the reference's up to sign; the
+    allowed difference is the eigenvector condition eps N max|T| / gap (x 100)."""
+    if f"{tag}_Q" not in g.files:
+        return
+    cols = g[f"{tag}_qcols"]
+    lam = g[f"{tag}_lam"]
+    nT = T.norm_max()
+    Qg = res.Q[:, torch.as_tensor(cols, device="cuda")].cpu().numpy()
+    Qr = g[f"{tag}_Q"]
+    gap = np.full(lam.size, np.inf)
+    gap[1:] = np.minimum(gap[1:], np.diff(lam))
+    gap[:-1] = np.minimum(gap[:-1], np.diff(lam))
+    checked = 0
+    for t, j in enumerate(cols):
+        if gap[j] < 1e-8 * nT:
+            continue
+        s = np.sign(Qg[:, t] @ Qr[:, t]) or 1.0
+        diff = float(np.abs(s * Qg[:, t] - Qr[:, t]).max())
+        bound = 100 * np.finfo(np.float64).eps * T.n * nT / gap[j] + 1e-12
+        assert diff <= bound, (tag, int(j), diff, bound)
+        checked += 1
+    assert checked >= len(cols) // 2
+
+
+def test_config1_uniform_n2000(g):
+    import paper_1510_04591_b200 as hb
+    T = hb.gen_uniform(2000, 0)
+    cfg = hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13)
+    res = hb.adc_solve(T, cfg)
+    check_solve(g, "cfg1", T, res)
+    check_columns(g, "cfg1", T, res)
+
+
+@pytest.mark.parametrize("sample", ["offdiag", "reference"])
+@pytest.mark.parametrize("tag,method", [("cfg2r", "adc-rand"), ("cfg2d", "dense-dc")])
+def test_config2_toeplitz_n10000(g, tag, method, sample):
+    import paper_1510_04591_b200 as hb
+    if method == "dense-dc" and sample == "reference":
+        pytest.skip("no HSS merges in dense DC")
+    T = hb.gen_toeplitz(10000)
+    cfg = hb.SolverConfig(leaf_size=64, hss_threshold=256, rank_eps=1e-13, method=method,
+                          sample=sample)
+    res = hb.adc_solve(T, cfg)
+    check_solve(g, tag, T, res, rank_band=9, offdiag=sample == "offdiag", label=f"{tag}/{sample}")
+    check_columns(g, tag, T, res)
+
+
+@pytest.mark.parametrize("sample", ["offdiag", "reference"])
+@pytest.mark.parametrize("tag,eps", [("cfg3", 1e-13), ("cfg3d", None)])
+def test_config3_kac_n20000(g, tag, eps, sample):
+    import paper_1510_04591_b200 as hb
+    if f"{tag}_lam" not in g.files:
+        pytest.skip(f"{tag} not in the fixture")
+    T = hb.gen_kac(20000)
+    kw = dict(rank_eps=eps) if eps else {}
+    res = hb.adc_solve(T, hb.SolverConfig(sample=sample, **kw))
+    check_solve(g, tag, T, res, rank_band=40, offdiag=sample == "offdiag", label=f"{tag}/{sample}")
+    # the closed form -(N-1) + 2j as well
+    exact = -(20000 - 1) + 2.0 * np.arange(20000)
+    assert np.abs(np.asarray(res.lam) - exact).max() <= 1e-12 * T.norm_max()
+
+
+@pytest.mark.parametrize("sample", ["offdiag", "reference"])
+@pytest.mark.parametrize("n", [8192, 16384])
+def test_config4_merge_vs_reference(g, n, sample):
+    """BASELINE config 4's merge at N = 8192 / 16384: roots, partition, rank estimate and
+    tree ranks against the reference's; X H on 16 Gaussian rows no further from the dense
+    X C than 10x the reference's own HSS error (the default off-diagonal sample: below the
+    reference's error, with at most the reference's ranks)."""
+    import paper_1510_04591_b200 as hb
+    from paper_1510_04591_b200.flops import FlopCounter
+    tag = f"c4_{n}"
+    offdiag = sample == "offdiag"
+    d, u, rho = hb.isolated_merge_system(n, 0)
+    f = FlopCounter()
+    sys_ = hb.RankOneSystem(d, u, rho)
+    sol = hb.solve_secular(sys_, flops=f)
+    hb.recompute_weights(sys_.d, sol, sys_.z, rho=rho, flops=f)
+    C = hb.CauchyEvecMatrix.from_secular(sys_, sol, flops=f)
+    lam = sol.lam.cpu().numpy()
+    assert np.abs(lam - g[f"{tag}_lam"]).max() <= 64 * np.finfo(np.float64).eps * np.abs(lam).max()
+    part = hb.build_partition(C.k, 128, C.d, C.gamma, C.mu)
+    assert [tuple(x) for x in g[f"{tag}_ranges"]] == list(part.ranges)
+    r_est = hb.estimate_rank(part, C.d, C.gamma, C.mu, 1e-13, 100)
+    assert r_est == int(g[f"{tag}_r_est"])
+    r = min(r_est, part.min_leaf - 10)
+    H = hb.rand_hss_construct(C, part, r, p=10, seed=[0, 0], flops=f, offdiag=offdiag)
+    assert bool(H.flagged) == bool(g[f"{tag}_flagged"])
+    rU, rV = H.ranks()
+    dU = rU[:-1] - g[f"{tag}_rU"][:-1]
+    dV = rV[:-1] - g[f"{tag}_rV"][:-1]
+    print(f"\n{tag}/{sample}: tree rank diff vs reference U mean {dU.mean():+.2f} "
+          f"[{dU.min()}, {dU.max()}]  V mean {dV.mean():+.2f} [{dV.min()}, {dV.max()}]  "
+          f"r_used {H.r_used} (ref {int(g[f'{tag}_r_used'])})")
+    if offdiag:
+        assert dU.max() <= 1 and dV.max() <= 1
+    X = torch.as_tensor(np.random.default_rng(5).standard_normal((16, n)), device="cuda")
+    f2 = FlopCounter()
+    XH = hb.hss_matmul_right(X, H, flops=f2)
+    XC = hb.update_vectors_dense(X, C)
+    XH_ref = torch.as_tensor(g[f"{tag}_XH"], device="cuda")
+    e_gpu = float((XH - XC).abs().max())
+    e_ref = float((XH_ref - XC).abs().max())
+    print(f"   max|XH - XC|: gpu {e_gpu:.3e}  reference {e_ref:.3e}  (x{e_gpu / e_ref:.2f})")
+    assert e_gpu <= (1.0 if offdiag else RATIO) * e_ref
+    # FLOP counters under the reference's conventions on the GPU's own tree
+    fc, fm = f.hss_construct, f2.hss_mult
+    fc0, fm0 = int(g[f"{tag}_flops_construct"]), int(g[f"{tag}_flops_mult16"])
+    print(f"   construct flops {fc:.4e} (ref {fc0:.4e}, {fc / fc0 - 1:+.2%})  multiply flops "
+          f"{fm:.4e} (ref {fm0:.4e}, {fm / fm0 - 1:+.2%})")
+    assert abs(fc / fc0 - 1) <= 0.05
+    assert fm <= 1.02 * fm0 if offdiag else abs(fm / fm0 - 1) <= 0.20
