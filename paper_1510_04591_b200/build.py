@@ -28,11 +28,27 @@ def _stale():
 
 
 def build(force=False, verbose=False):
-    """Compile every .cu under csrc/ into libhsseig_b200.so (in place)."""
+    """Compile every .cu under csrc/ into libhsseig_b200.so (in place): one nvcc per source
+    in parallel, then one shared link."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *sources()]
+    odir = os.path.join(os.path.dirname(PKG), "build", "obj")
+    os.makedirs(odir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "shared")]
+
+    def comp(src):
+        obj = os.path.join(odir, os.path.basename(src)[:-3] + ".o")
+        cmd = [nvcc, *cflags, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(sources())) as ex:
+        objs = list(ex.map(comp, sources()))
+    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

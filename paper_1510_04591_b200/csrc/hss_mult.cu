@@ -18,8 +18,8 @@
 // fragment load bank-conflict free without a swizzle.
 //
 // Exactness of K tails: factor slots are stored zero-padded to the 16-aligned slot
-// width and G/F slots get zeros beyond their rank (store width SW), so a chunk that
-// runs past a segment's K multiplies finite values by zeros.
+// width and G/F slots get zeros from their rank up to the next multiple of 4 (store width
+// SW), so a k-step that runs past a segment's K multiplies finite values by zeros.
 //
 // Job descriptors are built on the device from the ranks the construction wrote, so
 // no host synchronisation is needed between construction and multiply.
@@ -33,6 +33,30 @@ namespace hsseig {
 
 // tensor-map roles: 0 X, 1 G_l, 2 G_{l+1}, 3 F_{l-1} (or F_depth), 4 U, 5 B, 6 Vt, 7 D
 
+
+// All k-chunks of one job (both segments) for a warp whose first JM n-fragments are live.
+template <class T, int JM>
+__device__ __forceinline__ void consume_job(const TJob& jb, unsigned char* sm, uint64_t* full,
+                                            uint64_t* empty, uint32_t& q,
+                                            double (&acc)[T::MF][T::NF][2], int wm, int wn,
+                                            int lane) {
+  for (int sg = 0; sg < 2; ++sg) {
+    const int K = jb.K[sg];
+    const int nc = (K + T::BK - 1) / T::BK;
+    for (int c = 0; c < nc; ++c, ++q) {
+      const int slot = q % T::STAGES;
+      mbar_wait(&full[slot], (q / T::STAGES) & 1);
+      const double* sA = reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES);
+      const double* sB =
+          reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES);
+      if (K - c * T::BK >= T::BK)
+        tmma_chunk_j<T, JM, true>(sA, sB, acc, wm, wn, lane, T::BK);
+      else
+        tmma_chunk_j<T, JM, false>(sA, sB, acc, wm, wn, lane, (K - c * T::BK + 3) & ~3);
+      stage_release(&empty[slot], lane);
+    }
+  }
+}
 
 template <class T>
 __global__ void __launch_bounds__(T::THREADS, T::MINB)
@@ -90,22 +114,22 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
     const TJob jb = jobs[t / tiles_m];
     if (jb.N <= 0) continue;
     const int64_t m0 = (int64_t)(t % tiles_m) * T::BM;
+    // n-fragments of this warp that carry output columns of this job (warp-uniform)
+    const int jmax = min(T::NF, max(0, (jb.N - wn * T::NF * 8 + 7) >> 3));
 #pragma unroll
     for (int i = 0; i < T::MF; ++i)
 #pragma unroll
       for (int j = 0; j < T::NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int sg = 0; sg < 2; ++sg) {
-      const int K = jb.K[sg];
-      const int nc = (K + T::BK - 1) / T::BK;
-      for (int c = 0; c < nc; ++c, ++q) {
-        const int slot = q % T::STAGES;
-        mbar_wait(&full[slot], (q / T::STAGES) & 1);
-        const double* sA = reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES);
-        const double* sB =
-            reinterpret_cast<const double*>(sm + (size_t)slot * T::STAGE_BYTES + T::A_BYTES);
-        tmma_chunk<T>(sA, sB, acc, wm, wn, lane, min(T::BK, (K - c * T::BK + 3) & ~3));
-        stage_release(&empty[slot], lane);
-      }
+    switch (jmax) {
+#define HSS_JM_CASE(J)                                                              \
+  case J:                                                                           \
+    if constexpr (J <= T::NF) consume_job<T, J>(jb, sm, full, empty, q, acc, wm, wn, lane); \
+    break;
+      HSS_JM_CASE(0) HSS_JM_CASE(1) HSS_JM_CASE(2) HSS_JM_CASE(3) HSS_JM_CASE(4)
+      HSS_JM_CASE(5) HSS_JM_CASE(6) HSS_JM_CASE(7) HSS_JM_CASE(8) HSS_JM_CASE(9)
+      HSS_JM_CASE(10) HSS_JM_CASE(11) HSS_JM_CASE(12) HSS_JM_CASE(13) HSS_JM_CASE(14)
+#undef HSS_JM_CASE
+      default: break;
     }
     // epilogue: accumulators for columns < N, zeros in [N, SW)
 #pragma unroll
@@ -158,7 +182,6 @@ __global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs) {
     const int j = q - ((1 << l) - 2);
     const int node = p.lnodes[(1 << l) - 1 + j];
     jb.ldc = (int64_t)(1 << l) * ws;
-    jb.SW = ws;
     if (up) {
       jb.C = p.Gb + lvl_off(p.P, ws, l) + (int64_t)j * ws;
       jb.N = p.rU[node];
@@ -188,6 +211,9 @@ __global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs) {
         jb.bm[1] = 6; jb.brow[1] = par * ws; jb.bcol[1] = (j & 1) ? nl + (nl & 1) : 0;
       }
     }
+    // a consumer reads this slot's columns up to its K rounded to 4 (tmma_chunk's k-steps),
+    // so zeros are stored only up to there, not across the whole slot width
+    jb.SW = (jb.N + 3) & ~3;
   } else {
     const int j = e - 2 * nup;
     const int node = p.lnodes[(1 << p.depth) - 1 + j];

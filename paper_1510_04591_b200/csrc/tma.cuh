@@ -107,6 +107,33 @@ __device__ __forceinline__ void tmma_chunk(const double* __restrict__ sA, const 
   }
 }
 
+// Same chunk with only this warp's first JM n-fragments live (compile-time, straight-line
+// code): a tile sized for the widest job of a launch does no DMMA work on the padding of
+// narrower jobs (HSS levels mix ranks; the tile covers the largest one).
+// FULL: all BK k-columns live (no per-k-step exits, so the compiler can hoist the
+// fragment loads of later k-steps over the DMMAs of earlier ones).
+template <class T, int JM, bool FULL>
+__device__ __forceinline__ void tmma_chunk_j(const double* __restrict__ sA, const double* __restrict__ sB,
+                                             double (&c)[T::MF][T::NF][2], int wm, int wn, int lane,
+                                             int kv) {
+  const int gr = lane >> 2, gc = lane & 3;
+  const double* a0 = sA + (wm * T::MF * 8 + gr) * T::SA + gc;
+  const double* b0 = sB + gc * T::SB + wn * T::NF * 8 + gr;
+#pragma unroll
+  for (int kk = 0; kk < T::BK; kk += 4) {
+    if (!FULL && kk >= kv) break;
+    double a[T::MF], b[JM > 0 ? JM : 1];
+#pragma unroll
+    for (int i = 0; i < T::MF; ++i) a[i] = a0[i * 8 * T::SA + kk];
+#pragma unroll
+    for (int j = 0; j < JM; ++j) b[j] = b0[kk * T::SB + j * 8];
+#pragma unroll
+    for (int j = 0; j < JM; ++j)
+#pragma unroll
+      for (int i = 0; i < T::MF; ++i) dmma_8x8x4(c[i][j][0], c[i][j][1], a[i], b[j]);
+  }
+}
+
 // One job of a batched two-segment GEMM C = A1 B1 + A2 B2 (tma_gemm_kernel, hss_mult.cu).
 struct TJob {
   int32_t am[2], acol[2];            // A map role and column offset per segment (rows = tile)

@@ -64,6 +64,27 @@ class SolverConfig:
             raise ValueError(f"sample must be one of {SAMPLE_MODES}")
 
 
+def split(T, k=None):
+    """T = blockdiag(T1, T2) + rho v v^T, v = e_k + theta e_{k+1} (dc.py:82-102).
+
+    rho = |b_k|, theta = sign(b_k): both corner diagonals drop by rho.  The level-batched
+    solver applies the same arithmetic to every node of the recursion (solver._plan)."""
+    from .matgen import SymTridiagonal
+    n = T.n
+    if k is None:
+        k = n // 2
+    if not 1 <= k < n:
+        raise ValueError(f"split index {k} out of range for order {n}")
+    bk = float(T.b[k - 1])
+    rho = abs(bk)
+    theta = 1.0 if bk >= 0.0 else -1.0
+    a1 = T.a[:k].copy()
+    a1[-1] -= rho
+    a2 = T.a[k:].copy()
+    a2[0] -= rho
+    return SymTridiagonal(a1, T.b[:k - 1].copy()), SymTridiagonal(a2, T.b[k:].copy()), rho, theta
+
+
 @dataclass
 class MergeRecord:
     """dc.py:54-62"""

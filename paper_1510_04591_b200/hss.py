@@ -641,3 +641,44 @@ def hss_to_dense(H, bound=DENSE_BOUND):
     if H.k > bound:
         raise ValueError(f"order {H.k} above the dense reconstruction bound {bound}")
     return hss_matmul_right(torch.eye(H.k, dtype=torch.float64, device="cuda"), H)
+
+
+def audit_tree(H):
+    """Structural invariants of a constructed tree (hss.py:397-431); AssertionError on failure.
+
+    Postorder topology, children tiling their parent, contiguous leaves, and the identity
+    rows of every interpolation basis at its skeleton (U[rows_local] = I, V[cols_local] = I)
+    read back from the device slots."""
+    nodes = H.nodes
+    root = nodes[H.root]
+    assert H.root == len(nodes) - 1, "root must be last in postorder"
+    leaves = []
+    for nd in nodes:
+        if nd.is_leaf:
+            leaves.append(nd)
+            continue
+        lt, rt = nodes[nd.left], nodes[nd.right]
+        assert nd.left < nd.right < nd.index, f"postorder violated at {nd.index}"
+        assert lt.parent == nd.index and rt.parent == nd.index
+        assert lt.sibling == nd.right and rt.sibling == nd.left
+        assert (lt.lo, rt.hi) == (nd.lo, nd.hi) and lt.hi == rt.lo, \
+            f"children ranges must tile node {nd.index}"
+        assert lt.level == rt.level == nd.level + 1
+    leaves.sort(key=lambda n: n.lo)
+    assert leaves[0].lo == 0 and leaves[-1].hi == H.k
+    for a, b in zip(leaves, leaves[1:]):
+        assert a.hi == b.lo, "leaf ranges must be contiguous"
+    assert (root.lo, root.hi) == (0, H.k)
+    for nd in nodes:
+        if nd.index == H.root:
+            continue
+        U, V = nd.U, nd.V
+        assert np.array_equal(U[nd.rows_local], np.eye(U.shape[1])), \
+            f"U of node {nd.index} lost its identity submatrix"
+        assert np.array_equal(V[nd.cols_local], np.eye(V.shape[1])), \
+            f"V of node {nd.index} lost its identity submatrix"
+        rs, cs = nd.rows_sel, nd.cols_sel
+        if rs.size:
+            assert nd.lo <= rs.min() and rs.max() < nd.hi
+        if cs.size:
+            assert nd.lo <= cs.min() and cs.max() < nd.hi
