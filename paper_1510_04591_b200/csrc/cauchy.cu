@@ -329,6 +329,7 @@ static int launch_sample(const CauchyGen& g, const double* om, int64_t ldom, int
 // competing for the FP64 issue slots:  Y_R = C[R, :] Omega   and   Z_R^T = Omega^T C[:, R].
 // ---------------------------------------------------------------------------
 constexpr double kMatCapBytes = 12.0 * (1 << 30);   // largest panel pair materialised
+constexpr int64_t kPanelChunks = 4;
 
 // out[i][j] = C[i0 + i][j0 + j] for i < ni, j < nj.  DIV (the dense update's panels): the
 // reference's entry bit for bit, (zhat_i v_j) / gap with IEEE division; otherwise (the
@@ -427,15 +428,40 @@ __global__ void splitk_reduce_t_kernel(const double* __restrict__ part, int nspl
 }
 
 struct MatPlan {
-  int64_t nrows, kld, nld, ldp, sy, sz, kcy, kcz, tiles_n;
+  int64_t nrows, kld, nld, ldp, sy, sz, kcy, kcz, tiles_n, nch;
   int64_t off_py, off_pz, off_omt, off_c1, off_c2, off_jobs, off_maps, total;
   bool shared;   // C[R, :] and C[:, R] are the same panel (R = all rows)
+  // panel row chunk c (shared panel): rows [row_of(c), row_of(c + 1)), Z splits
+  // [zsplit_of(c), zsplit_of(c + 1)) -- chunk bounds are Z split-K bounds
+  __host__ __device__ int64_t zsplit_of(int64_t c) const { return c * sz / nch; }
+  __host__ __device__ int64_t row_of(int64_t c) const {
+    const int64_t r = zsplit_of(c) * kcz;
+    return r < nrows ? r : nrows;
+  }
 };
 
-static void split_k(int64_t k, int64_t items_per_split, int64_t* ns, int64_t* kc) {
-  int64_t n = (148 * 6 + items_per_split - 1) / items_per_split;
-  n = imax64(1, imin64(n, (k + 1023) / 1024));
-  int64_t c = (k + n - 1) / n;
+// Split-K factor for a persistent launch of tiles x ns work items on one CTA per SM: the
+// smallest ns (at most one split per 512 columns of K) whose items fill at least three waves
+// and leave the least idle SM time in the last wave -- a launch of whole waves keeps every
+// SM busy to the end (6.05 waves cost as much as 7).
+static void split_k(int64_t k, int64_t tiles, int64_t* ns, int64_t* kc) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms < 1) sms = 148;
+  }
+  const int64_t nmax = imax64(1, (k + 511) / 512);
+  int64_t best = 1;
+  double best_eff = -1.0;
+  for (int64_t n = 1; n <= imin64(nmax, 64); ++n) {
+    const int64_t items = tiles * n;
+    const int64_t waves = (items + sms - 1) / sms;
+    const double eff = (double)items / (double)(waves * sms) - (waves < 3 ? 0.5 : 0.0);
+    if (eff > best_eff + 0.02) { best_eff = eff; best = n; }
+  }
+  int64_t c = (k + best - 1) / best;
   c = (c + 15) / 16 * 16;
   *ns = (k + c - 1) / c;
   *kc = c;
@@ -448,9 +474,20 @@ static MatPlan mat_plan(int64_t k, int64_t w, int64_t nrows) {
   p.kld = k + (k & 1);
   p.nld = nrows + (nrows & 1);
   p.ldp = ((w + 1) / 2) * 2;
-  split_k(k, (nrows + 127) / 128, &p.sy, &p.kcy);
+  // the shared panel is generated in row chunks on a side stream, each chunk's products
+  // starting as soon as it is written (the HBM-bound generation hides under the DMMA-bound
+  // products of the previous chunk); the split-K factors are sized for one chunk's tiles
   p.tiles_n = (nrows + 127) / 128;
-  split_k(k, p.tiles_n * ((w + 95) / 96), &p.sz, &p.kcz);
+  const int64_t chunks = p.shared ? kPanelChunks : 1;
+  const int64_t ctiles = (p.tiles_n + chunks - 1) / chunks;
+  split_k(k, ctiles, &p.sy, &p.kcy);
+  // Z^T: a chunk's launch holds (its q splits) x tiles_n items; q is picked for one chunk's
+  // K range, and every chunk gets q splits
+  int64_t q, kcq;
+  split_k((k + chunks - 1) / chunks, p.tiles_n, &q, &kcq);
+  p.kcz = (((k + q * chunks - 1) / (q * chunks)) + 15) / 16 * 16;
+  p.sz = (k + p.kcz - 1) / p.kcz;
+  p.nch = imin64(chunks, p.sz);
   int64_t o = 0;
   auto take = [&](int64_t n) { int64_t at = o; o += (n + 31) / 32 * 32; return at; };
   p.off_py = take(p.sy * nrows * p.ldp);
@@ -458,8 +495,8 @@ static MatPlan mat_plan(int64_t k, int64_t w, int64_t nrows) {
   p.off_omt = take(w * p.kld);
   p.off_c1 = take(nrows * p.kld);
   p.off_c2 = p.shared ? p.off_c1 : take(k * p.nld);
-  p.off_jobs = take(((p.sy + p.sz * p.tiles_n) * (int64_t)sizeof(TJob) + 7) / 8);
-  p.off_maps = take(2 * (int64_t)sizeof(MapSet) / 8 + 32);
+  p.off_jobs = take(((p.nch * p.sy + p.sz * p.tiles_n) * (int64_t)sizeof(TJob) + 7) / 8);
+  p.off_maps = take((p.nch + 1) * (int64_t)sizeof(MapSet) / 8 + 32);
   p.total = o;
   return p;
 }
@@ -469,32 +506,50 @@ static bool mat_fits(int64_t k, int64_t nrows) {
   return bytes <= kMatCapBytes;
 }
 
-__global__ void mat_jobs_kernel(TJob* __restrict__ jobs, int sy, int sz, int tiles_n, int64_t k,
-                                int64_t nr, int w, int64_t kcy, int64_t kcz, int64_t ldp,
-                                int64_t nld, double* pY, double* pZ) {
+// Y jobs: chunk-major (chunk c, K split q) with the chunk's rows; then Z^T jobs
+// (split qq, column tile t), split-major so a chunk's Z jobs are contiguous.
+__global__ void mat_jobs_kernel(TJob* __restrict__ jobs, MatPlan p, int64_t k, int w, double* pY,
+                                double* pZ) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= sy + sz * tiles_n) return;
+  const int64_t nr = p.nrows;
+  if (q >= p.nch * p.sy + p.sz * p.tiles_n) return;
   TJob jb;
   jb.am[0] = jb.am[1] = 0;
   jb.acol[1] = 0; jb.K[1] = 0;
   jb.bm[0] = jb.bm[1] = 4;
   jb.brow[1] = jb.bcol[1] = 0;
-  if (q < sy) {
-    jb.acol[0] = (int32_t)(q * kcy); jb.K[0] = (int32_t)imin64(kcy, k - q * kcy);
-    jb.brow[0] = (int32_t)(q * kcy); jb.bcol[0] = 0;
+  if (q < p.nch * p.sy) {
+    const int64_t c = q / p.sy, sp = q % p.sy;
+    jb.acol[0] = (int32_t)(sp * p.kcy); jb.K[0] = (int32_t)imin64(p.kcy, k - sp * p.kcy);
+    jb.brow[0] = (int32_t)(sp * p.kcy); jb.bcol[0] = 0;
     jb.N = jb.SW = w;
-    jb.C = pY + (int64_t)q * nr * ldp;
-    jb.ldc = ldp;
+    jb.C = pY + sp * nr * p.ldp + p.row_of(c) * p.ldp;
+    jb.ldc = p.ldp;
   } else {
-    const int qq = (q - sy) / tiles_n, t = (q - sy) % tiles_n;
-    jb.acol[0] = (int32_t)(qq * kcz); jb.K[0] = (int32_t)imin64(kcz, k - qq * kcz);
-    jb.brow[0] = (int32_t)(qq * kcz); jb.bcol[0] = t * 128;
-    jb.N = jb.SW = (int32_t)imin64(128, nr - (int64_t)t * 128);
-    jb.C = pZ + (int64_t)qq * w * nld + (int64_t)t * 128;
-    jb.ldc = nld;
+    const int64_t e = q - p.nch * p.sy;
+    const int64_t qq = e / p.tiles_n, t = e % p.tiles_n;
+    jb.acol[0] = (int32_t)(qq * p.kcz); jb.K[0] = (int32_t)imin64(p.kcz, k - qq * p.kcz);
+    jb.brow[0] = (int32_t)(qq * p.kcz); jb.bcol[0] = (int32_t)(t * 128);
+    jb.N = jb.SW = (int32_t)imin64(128, nr - t * 128);
+    jb.C = pZ + qq * w * p.nld + t * 128;
+    jb.ldc = p.nld;
   }
   jobs[q] = jb;
 }
+
+// side stream + events of the chunked panel generation (one set per process: the library
+// drives one device per process)
+struct PanelSide {
+  cudaStream_t s = nullptr;
+  cudaEvent_t in = nullptr, gen[kPanelChunks] = {};
+  bool ok = false;
+  PanelSide() {
+    ok = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&in, cudaEventDisableTiming) == cudaSuccess;
+    for (int c = 0; ok && c < kPanelChunks; ++c)
+      ok = cudaEventCreateWithFlags(&gen[c], cudaEventDisableTiming) == cudaSuccess;
+  }
+};
 
 static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom, int w, int64_t row0,
                              int64_t row1, double* Y, double* Z, int64_t ldy, double* work,
@@ -511,40 +566,65 @@ static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom,
   TJob* djobs = reinterpret_cast<TJob*>(work + p.off_jobs);
   MapSet* dmaps = reinterpret_cast<MapSet*>(
       (reinterpret_cast<uintptr_t>(work + p.off_maps) + 255) & ~(uintptr_t)255);
-  // panels
-  {
-    // each thread walks many rows with its column's generators in registers
+  const Operand none{nullptr, 0, 0, 0};
+  const int njobs = (int)(p.nch * p.sy + p.sz * p.tiles_n);
+  int rc;
+  // Omega^T and the job tables (built on the device)
+  dim3 gt((unsigned)((k + 31) / 32), (unsigned)((w + 31) / 32));
+  transpose_kernel<<<gt, dim3(32, 8), 0, s>>>(om, ldom, k, w, omt, p.kld);
+  HSS_CHECK_LAUNCH();
+  mat_jobs_kernel<<<(njobs + 127) / 128, 128, 0, s>>>(djobs, p, k, w, pY, pZ);
+  HSS_CHECK_LAUNCH();
+  auto z_gemm = [&](int64_t c) -> int {
+    const int64_t q0 = p.zsplit_of(c), q1 = p.zsplit_of(c + 1);
+    if (q1 <= q0) return HSSEIG_OK;
+    const Operand ops[kMaps] = {Operand{omt, (uint64_t)w, (uint64_t)k, (uint64_t)p.kld}, none, none,
+                                none, Operand{C2, (uint64_t)k, (uint64_t)nr, (uint64_t)p.nld}, none,
+                                none, none};
+    return tma_jobs_gemm(2, w, ops, dmaps + p.nch, djobs + p.nch * p.sy + q0 * p.tiles_n,
+                         (int)((q1 - q0) * p.tiles_n), w, s);
+  };
+  if (p.shared) {
+    static PanelSide side;
+    if (!side.ok) return HSSEIG_ERR_CUDA;
+    // generators and the panel's previous readers are ordered before the first chunk
+    if (cudaEventRecord(side.in, s) != cudaSuccess || cudaStreamWaitEvent(side.s, side.in, 0) != cudaSuccess)
+      return HSSEIG_ERR_CUDA;
+    for (int64_t c = 0; c < p.nch; ++c) {
+      const int64_t r0 = p.row_of(c), r1 = p.row_of(c + 1);
+      if (r1 > r0) {
+        // each thread walks many rows with its column's generators in registers
+        dim3 gr((unsigned)((k + 255) / 256), (unsigned)imin64(r1 - r0, 128));
+        gen_panel_kernel<false><<<gr, 256, 0, side.s>>>(g, row0 + r0, r1 - r0, 0, k,
+                                                        C1 + r0 * p.kld, p.kld);
+        HSS_CHECK_LAUNCH();
+      }
+      if (cudaEventRecord(side.gen[c], side.s) != cudaSuccess) return HSSEIG_ERR_CUDA;
+    }
+    for (int64_t c = 0; c < p.nch; ++c) {
+      const int64_t r0 = p.row_of(c), r1 = p.row_of(c + 1);
+      if (cudaStreamWaitEvent(s, side.gen[c], 0) != cudaSuccess) return HSSEIG_ERR_CUDA;
+      if (r1 <= r0) continue;
+      const Operand ops[kMaps] = {Operand{C1 + r0 * p.kld, (uint64_t)(r1 - r0), (uint64_t)k,
+                                          (uint64_t)p.kld},
+                                  none, none, none, Operand{om, (uint64_t)k, (uint64_t)w, (uint64_t)ldom},
+                                  none, none, none};
+      if ((rc = tma_jobs_gemm(0, w, ops, dmaps + c, djobs + c * p.sy, (int)p.sy, r1 - r0, s)))
+        return rc;
+      if ((rc = z_gemm(c))) return rc;
+    }
+  } else {
     dim3 gr((unsigned)((k + 255) / 256), (unsigned)imin64(nr, 128));
     gen_panel_kernel<false><<<gr, 256, 0, s>>>(g, row0, nr, 0, k, C1, p.kld);
     HSS_CHECK_LAUNCH();
-    if (!p.shared) {
-      dim3 g2((unsigned)((nr + 255) / 256), (unsigned)imin64(k, 128));
-      gen_panel_kernel<false><<<g2, 256, 0, s>>>(g, 0, k, row0, nr, C2, p.nld);
-      HSS_CHECK_LAUNCH();
-    }
-    dim3 gt((unsigned)((k + 31) / 32), (unsigned)((w + 31) / 32));
-    transpose_kernel<<<gt, dim3(32, 8), 0, s>>>(om, ldom, k, w, omt, p.kld);
+    dim3 g2((unsigned)((nr + 255) / 256), (unsigned)imin64(k, 128));
+    gen_panel_kernel<false><<<g2, 256, 0, s>>>(g, 0, k, row0, nr, C2, p.nld);
     HSS_CHECK_LAUNCH();
-  }
-  // job tables (built on the device): Y splits, then Z^T (split, column tile) pairs
-  const int njobs = (int)(p.sy + p.sz * p.tiles_n);
-  mat_jobs_kernel<<<(njobs + 127) / 128, 128, 0, s>>>(djobs, (int)p.sy, (int)p.sz, (int)p.tiles_n,
-                                                      k, nr, w, p.kcy, p.kcz, p.ldp, p.nld, pY, pZ);
-  HSS_CHECK_LAUNCH();
-  const Operand none{nullptr, 0, 0, 0};
-  int rc;
-  {
     const Operand ops[kMaps] = {Operand{C1, (uint64_t)nr, (uint64_t)k, (uint64_t)p.kld}, none, none,
                                 none, Operand{om, (uint64_t)k, (uint64_t)w, (uint64_t)ldom}, none,
                                 none, none};
     if ((rc = tma_jobs_gemm(0, w, ops, dmaps, djobs, (int)p.sy, nr, s))) return rc;
-  }
-  {
-    const Operand ops[kMaps] = {Operand{omt, (uint64_t)w, (uint64_t)k, (uint64_t)p.kld}, none, none,
-                                none, Operand{C2, (uint64_t)k, (uint64_t)nr, (uint64_t)p.nld}, none,
-                                none, none};
-    if ((rc = tma_jobs_gemm(2, 128, ops, dmaps + 1, djobs + p.sy, (int)(p.sz * p.tiles_n), w, s)))
-      return rc;
+    if ((rc = z_gemm(0))) return rc;
   }
   const unsigned rb = (unsigned)((nr * w + 255) / 256);
   if (peY) {   // fused with the all-gather: rows land in every rank's full Y / Z

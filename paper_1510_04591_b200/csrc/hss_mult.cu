@@ -313,13 +313,36 @@ static int launch_wide(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJo
   }
 }
 
-// job-table GEMMs for other paths (sampling): shape 0 rank-width, 1 wide, 2 tall-N
-// (BM 96 x BN 128 for M = sample width, N = k)
+// short-M outputs (M = the sample width m <= 112, N = k: Z^T = Omega^T C): one warp row
+// spans all M rows in ceil(m/8) fragments (M padded to 8 only), 8 warps of 16 columns
+template <int MF>
+using ShortTile = TTile<MF, 2, 1, 8, 6>;
+static int launch_short(int m, const Operand (&ops)[kMaps], MapSet* dm, const TJob* jobs, int njobs,
+                        cudaStream_t s) {
+  switch ((m + 7) / 8) {
+    case 1: case 2: case 3: case 4: return launch_tma<ShortTile<4>>(ops, dm, jobs, njobs, m, s);
+    case 5: return launch_tma<ShortTile<5>>(ops, dm, jobs, njobs, m, s);
+    case 6: return launch_tma<ShortTile<6>>(ops, dm, jobs, njobs, m, s);
+    case 7: return launch_tma<ShortTile<7>>(ops, dm, jobs, njobs, m, s);
+    case 8: return launch_tma<ShortTile<8>>(ops, dm, jobs, njobs, m, s);
+    case 9: return launch_tma<ShortTile<9>>(ops, dm, jobs, njobs, m, s);
+    case 10: return launch_tma<ShortTile<10>>(ops, dm, jobs, njobs, m, s);
+    case 11: return launch_tma<ShortTile<11>>(ops, dm, jobs, njobs, m, s);
+    case 12: return launch_tma<ShortTile<12>>(ops, dm, jobs, njobs, m, s);
+    case 13: return launch_tma<ShortTile<13>>(ops, dm, jobs, njobs, m, s);
+    case 14: return launch_tma<ShortTile<14>>(ops, dm, jobs, njobs, m, s);
+    default: HSS_ARG_FAIL();
+  }
+}
+
+// job-table GEMMs for other paths (sampling): shape 0 rank-width (N = n), 1 wide, 2 short-M
+// (M = n = the sample width, N = 128-column jobs)
 int tma_jobs_gemm(int shape, int n, const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jobs,
                   int njobs, int64_t M, cudaStream_t s) {
   if (shape == 0) return launch_narrow(n, ops, dmaps, jobs, njobs, M, s);
   if (shape == 1) return launch_wide(n, ops, dmaps, jobs, njobs, M, s);
-  return launch_tma<TTile<3, 8, 4, 2, 6>>(ops, dmaps, jobs, njobs, M, s);
+  if (M != n) HSS_ARG_FAIL();
+  return launch_short(n, ops, dmaps, jobs, njobs, s);
 }
 
 __global__ void plain_jobs_kernel(TJob* jobs, int nj, double* C, int64_t ldc, int N, int K) {

@@ -68,14 +68,20 @@ def _cases(h):
     ]
 
 
-def _compare(T, stock, seamed, same_lam_bits=False, routes=None):
+def _compare(T, stock, seamed, same_lam_bits=False, routes=None, route_flips=0):
     """routes: the expected records when they are not the stock run's (see
-    test_merge_seam_gpu_update)."""
+    test_merge_seam_gpu_update); route_flips: how many merges may swap (used_hss, fell_back)
+    = (True, False) <-> (False, True), i.e. a flag decision on the saturation threshold."""
     nT = T.norm_max()
     assert np.abs(seamed.lam - stock.lam).max() <= 1e-12 * nT
     if same_lam_bits:
         assert np.array_equal(seamed.lam, stock.lam)
-    assert _records(seamed) == (routes if routes is not None else _records(stock))
+    want, got = (routes if routes is not None else _records(stock)), _records(seamed)
+    assert len(want) == len(got)
+    diff = [(a, b) for a, b in zip(got, want) if a != b]
+    assert len(diff) <= route_flips, diff
+    for a, b in diff:
+        assert a[:3] == b[:3] and {a[3:], b[3:]} == {(True, False), (False, True)}, (a, b)
     o0, b0 = _metrics(T, stock)
     o1, b1 = _metrics(T, seamed)
     eps_n = np.finfo(np.float64).eps / T.n     # floor: one rounding over the order
@@ -113,7 +119,8 @@ def test_merge_seam_gpu_update(hsseig, monkeypatch, case, method):
     # The plugin builds with the off-diagonal sample; where a tree sits on
     # the saturation-flag threshold (Kac 900 at leaf 32: a width-32 sample) that sample's
     # flag decision can differ from the reference's, so the expected routes are those of
-    # its CPU definition (oracle adc_solve with offdiag=True) on the same input
+    # its CPU definition (oracle adc_solve with offdiag=True) on the same input, up to one
+    # more such flip between the device sample and the oracle's (their sums round apart)
     routes = None
     if method == "adc-rand":
         from oracle import hss_oracle as orc
@@ -123,7 +130,7 @@ def test_merge_seam_gpu_update(hsseig, monkeypatch, case, method):
                   for i in infos]
         flips = sum(a != b for a, b in zip(routes, _records(stock)))
         assert flips <= 1, flips
-    _compare(T, stock, seamed, routes=routes)
+    _compare(T, stock, seamed, routes=routes, route_flips=1 if method == "adc-rand" else 0)
     if method == "adc-rand" and name in ("toeplitz", "kac"):
         assert any(m.used_hss for m in seamed.merges)
     if method == "adc-rand" and name == "toeplitz_flagged":
