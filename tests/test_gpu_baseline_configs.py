@@ -68,7 +68,16 @@ def check_solve(g, tag, T, res, rank_band=0, label="", offdiag=True):
     rec, rec_ref = records(res), g[f"{tag}_merges"]
     assert rec.shape == rec_ref.shape
     cols = [0, 1, 2, 3, 5]                       # everything but the HSS rank: identical
-    assert np.array_equal(rec[:, cols], rec_ref[:, cols]), tag
+    bad = np.flatnonzero((rec[:, cols] != rec_ref[:, cols]).any(axis=1))
+    # ...except where a weight sits on the deflation tolerance (secular.py:96-156): the
+    # children's eigenvector rows that form z are the reference's to ~1e-16, not bit for
+    # bit, so a pole on the threshold may deflate on one side only (kept +-1, at most two
+    # merges, same route)
+    for i in bad:
+        a, b = rec[i], rec_ref[i]
+        assert (a[0] == b[0] and abs(int(a[1]) - int(b[1])) <= 1 and a[1] + a[2] == b[1] + b[2]
+                and a[3] == b[3] and a[5] == b[5]), (tag, label, int(i), a.tolist(), b.tolist())
+    assert bad.size <= 2, (tag, label, [(int(i), rec[i].tolist(), rec_ref[i].tolist()) for i in bad[:6]])
     hss = rec_ref[:, 3] == 1
     dr = rec[:, 4] - rec_ref[:, 4]
     if offdiag:
