@@ -502,6 +502,24 @@ def reference_work(n):
     return w
 
 
+def nccl_summary(path):
+    """NCCL version and the communicator lines of rank 0's NCCL_DEBUG=INFO log (init,
+    transport / NVLS) for the bench line."""
+    import torch
+    out = {"version": ".".join(str(x) for x in torch.cuda.nccl.version())}
+    if not path or not os.path.exists(path):
+        return out
+    lines = [ln.strip() for ln in open(path, errors="replace")]
+    keep = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines
+            if "NCCL INFO" in ln and any(t in ln for t in ("comm 0x", "NVLS", "via P2P", "nRanks",
+                                                           "Channel 00", "CollNet", "Init COMPLETE"))]
+    out["nvls"] = any("NVLS" in ln and ("enabled" in ln.lower() or "nvls comm" in ln.lower()
+                                        or "support" in ln.lower()) for ln in lines)
+    out["p2p_nvlink"] = any("P2P/CUMEM" in ln or "via P2P" in ln for ln in lines)
+    out["lines"] = keep[:12]
+    return out
+
+
 def peak_hbm():
     try:
         return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -565,8 +583,15 @@ def run_ours(args):
     # (ranks share the device, host-side collectives) for testing
     local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    nccl_log = None
     if world > 1:
         backend = os.environ.get("HSSEIG_DIST_BACKEND", "nccl")
+        if backend == "nccl" and "NCCL_DEBUG" not in os.environ:
+            # communicator evidence (ranks, channels, NVLink / NVLS) into a per-rank file,
+            # summarised in the JSON line; stdout stays one JSON line
+            nccl_log = f"/tmp/hsseig_nccl.{os.getpid()}.log"
+            os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,GRAPH,NVLS",
+                              NCCL_DEBUG_FILE=nccl_log)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -611,7 +636,11 @@ def run_ours(args):
                                     if info["used_hss"] else 0)
             ev = info.get("multiply_events")
             mult = ev[0].elapsed_time(ev[1]) if ev else float("nan")
-            return {"ms": {"total": e0.elapsed_time(e1), "multiply": mult},
+            ms = {"total": e0.elapsed_time(e1), "multiply": mult}
+            marks = info.get("marks") or []
+            for (_, a), (name, b) in zip(marks, marks[1:]):   # device time per phase
+                ms[name] = ms.get(name, 0.0) + a.elapsed_time(b) if name != "multiply" else mult
+            return {"ms": ms,
                     "flops": fl,
                     "sample_gather": info.get("sample_gather"),
                     # dense work counted when the merge fell back (dc.py:132-138)
@@ -761,6 +790,8 @@ def run_ours(args):
             line["config4_adc1"] = adc1
         if world > 1 and eigh_d is not None:
             line["eigh"] = {"cfg5_N65536_distributed": eigh_d}
+        if world > 1:
+            line["nccl"] = nccl_summary(nccl_log)
         if not args.no_cpu and world == 1:
             tf, dt, fl, kind = cpu_merge(CPU_SAMPLE_N)
             line["cpu_baseline"] = {

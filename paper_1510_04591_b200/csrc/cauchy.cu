@@ -375,7 +375,7 @@ __global__ void transpose_kernel(const double* __restrict__ in, int64_t ldi, int
 // Peer destinations of a fused gather: the reduced value of a row of this rank's block goes
 // straight to row (row0 + row) of every rank's full buffer (IPC-mapped over NVLink), so the
 // split-K reduction and the all-gather are one kernel; a system-scope fence publishes the
-// stores before the kernel retires (the host then synchronises and barriers the group).
+// stores before the kernel retires (then the group fences: distributed.peer_fence).
 struct PeerOut {
   const uint64_t* base;   // npeers device pointers (this rank's own buffer included)
   int npeers;

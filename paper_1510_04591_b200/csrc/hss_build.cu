@@ -213,9 +213,12 @@ __device__ __forceinline__ double lapy2(double x, double y) {
 // Truncation of the factored A = M^T (hss.py:128-148): trailing Frobenius mass of R's
 // rows, rank r = min(first t with tail(t) <= (tol ||M||_F)^2, max_rank, nonzero diagonal),
 // saturation flag, relative residual, then T = R11^{-1} R12 in place (dtrsm L/U/N/N).
+// `steps` reflectors were applied (id_eliminate); rows >= steps of R are not formed, their
+// mass is the trailing block's Frobenius mass `trail` (orthogonal invariance: the rows the
+// remaining reflectors would produce carry exactly that mass).
 __device__ __forceinline__ void id_truncate(double* sA, double* tail, int p, int w, int SW,
-                                            double nf, double tol, int max_rank, int& r,
-                                            int& sat, double& resid) {
+                                            double nf, double tol, int max_rank, int steps,
+                                            double trail, int& r, int& sat, double& resid) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int nthr = blockDim.x;
   __shared__ double s_resid;
@@ -223,7 +226,7 @@ __device__ __forceinline__ void id_truncate(double* sA, double* tail, int p, int
   r = 0;
   sat = 0;
   resid = 0.0;
-  const int mn = min(w, p);
+  const int mn = min(steps, min(w, p));
   if (!(nf == 0.0 || p == 0 || w == 0)) {
     // trailing Frobenius mass of R's rows, cumulated from the bottom (hss.py:134-136)
     for (int t = warp; t < mn; t += nwarps) {
@@ -234,8 +237,8 @@ __device__ __forceinline__ void id_truncate(double* sA, double* tail, int p, int
     }
     __syncthreads();
     if (tid == 0) {
-      double acc = 0.0;
-      tail[mn] = 0.0;
+      double acc = trail;
+      tail[mn] = trail;
       for (int t = mn - 1; t >= 0; --t) {
         acc += tail[t];
         tail[t] = acc;
@@ -285,7 +288,7 @@ __device__ __forceinline__ void id_truncate(double* sA, double* tail, int p, int
 // Truncation, saturation flag, T = R11^{-1} R12 and the ID outputs for the factored M^T held
 // in shared memory in pivot order (sA[j*SW + t], piv[j] = candidate at position j).
 __device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, bool leaf, int p,
-                                          double nf, double tol, const double* __restrict__ om,
+                                          double nf, int steps, double trail, double tol, const double* __restrict__ om,
                                           int64_t ldom, hsseig_status* st, const double* Mg,
                                           double* sA, double* tail, double* red, int* piv) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -294,7 +297,7 @@ __device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, 
   (void)red;
   int r = 0, sat = 0;
   double resid = 0.0;
-  id_truncate(sA, tail, p, w, SW, nf, tol, w, r, sat, resid);
+  id_truncate(sA, tail, p, w, SW, nf, tol, w, steps, trail, r, sat, resid);
 
   // ---- outputs: basis X (p x r) (+ X^T for V), skeleton indices, selected rows, compressions
   int32_t* rank_arr = side == 0 ? T.rU : T.rV;
@@ -446,8 +449,18 @@ __device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, 
 // sA[j*SW + t]; piv[j] = j on entry).  dgeqp3/dlaqp2 semantics: pivot = first maximum of
 // the downdated norms (idamax), dlarfg reflector, dlaqp2 norm downdate with the sqrt(eps)
 // recompute rule.  Returns ||M||_F.
+//
+// Early stop: the truncation only reads R's rows above the rank and the trailing masses,
+// and the mass of R's rows >= t equals the Frobenius mass of the trailing block after t
+// reflectors.  After each step the sum of the downdated norms (accurate to ~1e-11 relative
+// under the sqrt(eps) recompute rule) is compared with the cut; when it is within 4x the
+// exact trailing mass is summed and the elimination stops at the first step whose mass is
+// at or under (tol ||M||_F)^2, or at max_rank.  Rank, skeleton, T and the saturation flag
+// are those of the full factorisation (its columns beyond the rank only permute among
+// themselves); steps / trail return the reflector count and the trailing mass.
 __device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* vn2, double* red,
-                                               int* piv, int p, int w, int SW) {
+                                               int* piv, int p, int w, int SW, double tol,
+                                               int max_rank, int& steps, double& trail) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int nthr = blockDim.x;
   __shared__ double s_tau, s_nf;
@@ -476,6 +489,10 @@ __device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* 
   __syncthreads();
   const double nf = s_nf;
   const int mn = min(w, p);
+  steps = mn;
+  trail = 0.0;
+  const double cut = (tol * nf) * (tol * nf);
+  const int stop_at = min(mn, max(max_rank, 1));
   if (!(nf == 0.0 || p == 0 || w == 0)) {
     for (int i = 0; i < mn; ++i) {
       if (warp == 0) {
@@ -526,6 +543,7 @@ __device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* 
       __syncthreads();
       const double tau = s_tau;
       const double* v = sA + i * SW;
+      double mine = 0.0;   // downdated norms^2 of this thread's trailing candidates
       for (int c = i + 1 + tid; c < p; c += nthr) {
         double* a = sA + c * SW;
         if (tau != 0.0) {
@@ -568,10 +586,34 @@ __device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* 
             vn1[c] = n1 * sqrt(temp);
           }
         }
+        mine = fma(vn1[c], vn1[c], mine);
       }
+      if (i + 1 >= mn) break;   // full factorisation: trailing mass 0
+      mine = warp_sum(mine);
+      if (lane == 0) red[8 + warp] = mine;
       __syncthreads();
+      double proxy = 0.0;
+      for (int t = 0; t < nwarps; ++t) proxy += red[8 + t];   // same order in every thread
+      if (proxy <= 4.0 * cut || i + 1 == stop_at) {
+        double ex = 0.0;
+        for (int c = i + 1 + tid; c < p; c += nthr) {
+          const double* a = sA + c * SW;
+          for (int t = i + 1; t < w; ++t) ex = fma(a[t], a[t], ex);
+        }
+        ex = warp_sum(ex);
+        if (lane == 0) red[16 + warp] = ex;
+        __syncthreads();
+        ex = 0.0;
+        for (int t = 0; t < nwarps; ++t) ex += red[16 + t];
+        if (ex <= cut || i + 1 == stop_at) {   // uniform: every thread summed the same values
+          steps = i + 1;
+          trail = ex;
+          break;
+        }
+      }
     }
   }
+  __syncthreads();
   return nf;
 }
 
@@ -615,8 +657,10 @@ __global__ void __launch_bounds__(256, 2) id_kernel(TreeDev T, int level, double
   }
   for (int e = tid; e < p; e += nthr) piv[e] = e;
   __syncthreads();
-  const double nf = id_eliminate(sA, vn1, vn2, red, piv, p, w, SW);
-  id_finish(T, side, node, leaf, p, nf, tol, om, ldom, st, Mg, sA, tail, red, piv);
+  int steps;
+  double trail;
+  const double nf = id_eliminate(sA, vn1, vn2, red, piv, p, w, SW, tol, w, steps, trail);
+  id_finish(T, side, node, leaf, p, nf, steps, trail, tol, om, ldom, st, Mg, sA, tail, red, piv);
 }
 
 
@@ -646,10 +690,12 @@ __global__ void __launch_bounds__(256) interp_kernel(const double* __restrict__ 
   }
   for (int e = tid; e < p; e += nthr) piv[e] = e;
   __syncthreads();
-  const double nf = id_eliminate(sA, vn1, vn2, red, piv, p, w, SW);
+  int steps;
+  double trail;
+  const double nf = id_eliminate(sA, vn1, vn2, red, piv, p, w, SW, tol, max_rank, steps, trail);
   int r, sat;
   double resid;
-  id_truncate(sA, tail, p, w, SW, nf, tol, max_rank, r, sat, resid);
+  id_truncate(sA, tail, p, w, SW, nf, tol, max_rank, steps, trail, r, sat, resid);
   for (int e = tid; e < p; e += nthr) ipiv[piv[e]] = e;
   __syncthreads();
   for (int e = tid; e < p * r; e += nthr) {   // X[q][t]: identity on J, T^T elsewhere

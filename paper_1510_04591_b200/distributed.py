@@ -105,8 +105,27 @@ class PeerBuffers:
             self.views, self.ptrs = [], []
 
 
+_FENCE = {}
+
+
 def peer_fence(group=None):
-    """Every rank's peer stores so far have landed: local stream drained, then a barrier."""
+    """Every rank's peer stores so far have landed before this rank's stream goes on.
+
+    NCCL: a one-element all-reduce enqueued on the compute stream is the fence, with no host
+    drain.  It completes on a rank only once every rank's stream has reached it, i.e. after
+    every rank's peer-store kernels retired (they end with a system-scope fence), and the
+    work enqueued after it on this rank's stream waits for it.  The alternating buffer sets
+    of GpuOps.sample_gather rely on the same ordering (a rank overwrites set n % 2 only
+    after fence n - 1, which every rank reaches after its reads of set n - 2).
+    Other backends (gloo ranks sharing one device in the tests): the stream is drained on
+    the host and the group barriers."""
+    if dist.get_backend(group) == "nccl":
+        dev = torch.cuda.current_device()
+        t = _FENCE.get(dev)
+        if t is None:
+            t = _FENCE[dev] = torch.zeros(1, dtype=torch.int32, device="cuda")
+        dist.all_reduce(t, group=group)
+        return
     torch.cuda.current_stream().synchronize()
     dist.barrier(group=group)
 
@@ -135,6 +154,15 @@ class ShardedMerge:
         k, cfg, ops = self.k, self.cfg, self.ops
         lo, hi, c = shard_range(k, self.rank, self.world)
         info = {"used_hss": False, "fell_back": False, "r_used": 0}
+        marks = []   # (phase that ends here, CUDA event) on the compute stream: bench phases
+
+        def mark(name):
+            if X.is_cuda:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                marks.append((name, e))
+
+        mark("start")
         if rows_total is None:
             cnt = gather_rows(torch.tensor([[float(X.shape[0])]], dtype=torch.float64,
                                            device=X.device), 1, self.world, self.group)
@@ -150,6 +178,7 @@ class ShardedMerge:
         bad = bad_g if bad_g < k else (bad_m if (k >= 2 and bad_m < k) else -1)
         if bad >= 0:
             raise SecularConvergenceError(f"root {bad} lost its bracket")
+        mark("secular")
         dn = ops.dnext(d, gam, mu)
         zh_l, rad_l = ops.loewner_part(d, dn, gam, mu, z, rho, lo, hi)
         zh = gather_rows(zh_l, c, k, self.group).contiguous()
@@ -160,6 +189,7 @@ class ShardedMerge:
         v = gather_rows(v_l, c, k, self.group).contiguous()
         info["iterations"] = iters
         info["flops_secular"] = secular_flops(k, iters) + 14 * k * k
+        mark("loewner_normalizers")
         gen = ops.generators(d, dn, gam, mu, zh, v)
         tree = None
         if cfg.method == "adc-srrsc" and k > cfg.hss_threshold:
@@ -171,6 +201,7 @@ class ShardedMerge:
             if part is not None:
                 cap = min(part.min_leaf, ops.max_width)
                 tree = ops.build_srrsc(gen, part, cap, cfg.srrsc_tol, self.group)
+                mark("build")
         elif cfg.method == "adc-rand" and k > cfg.hss_threshold:
             mu_h = mu.cpu().numpy()
             try:
@@ -184,6 +215,7 @@ class ShardedMerge:
                 w = r + cfg.oversample
                 if r >= 1 and w <= ops.max_width:
                     om = ops.omega(seed, k, w)
+                    mark("partition_omega")
                     # the off-diagonal sample (default) masks the leaves' diagonal blocks
                     offdiag = getattr(cfg, "sample", "offdiag") == "offdiag"
                     mask = part if offdiag else None
@@ -199,7 +231,9 @@ class ShardedMerge:
                         Y_l, Z_l = ops.sample_part(gen, om, w, lo, hi, mask)
                         Y = gather_rows(Y_l, c, k, self.group)
                         Z = gather_rows(Z_l, c, k, self.group)
+                    mark("sample_gather")
                     tree = ops.build(gen, part, w, om, Y, Z, self.group, offdiag)
+                    mark("build")
         if tree is not None and not ops.flagged(tree):
             info["used_hss"] = True
             info["r_used"] = ops.r_used(tree)
@@ -211,8 +245,10 @@ class ShardedMerge:
             if timed:
                 e1.record()
                 info["multiply_events"] = (e0, e1)
+                marks.append(("multiply", e1))
         else:
             out = ops.dense(X, gen)
+            mark("dense")
         # the reference notes a fallback whenever the HSS route was taken and the dense
         # product ran instead: no partition, r < 1, a flagged tree (dc.py:147-160); here
         # also a sample wider than the kernels' MAX_WIDTH
@@ -230,6 +266,7 @@ class ShardedMerge:
         info["flops"] = fl
         info["rows_total"] = rows_total
         info["tree"] = tree
+        info["marks"] = marks
         return lam, out, info
 
 
