@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_MERGE)
+    # HSSEIG_BENCH_N: the same under torchrun (whose parser takes --n for its own options)
+    ap.add_argument("--n", type=int, default=int(os.environ.get("HSSEIG_BENCH_N", N_MERGE)))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-eigh", action="store_true")
@@ -188,7 +189,8 @@ def config_dict(n, world):
     return {"workload": "config4_isolated_top_merge", "N": n, "leaf_size": LEAF,
             "rank_eps": RANK_EPS, "oversample": OVERSAMPLE, "id_tol": 1e-15, "rho": 1.0,
             "method": "adc-rand", "parallelism": f"rowblock{world}" if world > 1 else "single",
-            "l2": "inputs larger than L2 (Q_old 8.6 GB)"}
+            "l2": (f"inputs larger than L2 (Q_old {n * n * 8 / 1e9:.1f} GB)" if n * n * 8 > 126e6
+                   else f"Q_old {n * n * 8 / 1e6:.0f} MB fits L2 (126 MB)")}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -765,7 +767,7 @@ def run_ours(args):
             "merge_wall_s": ms / 1e3,
             "phases_ms": {k: statistics.median(p["ms"][k] for p in phase_ms) for k in rec["ms"]},
             "flops_basis": ("reference FlopCounter on the reference's own tree for this input "
-                            "(tests/golden/configs.npz c4_32768)") if ref_work else
+                            f"(tests/golden/configs.npz c4_{n})") if ref_work else
                            "FlopCounter conventions on our own tree (no reference count for this N)",
             "flops_reference": ref_work,
             "flops": rec["flops"], "value_own_tree": flops_own / (ms * 1e-3) / 1e12,

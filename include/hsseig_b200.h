@@ -294,6 +294,17 @@ int hsseig_dense_update(const double *Qb, int64_t ldq, int64_t P, const hsseig_g
  * fed to log1p and the sign bit.  NumPy evaluates those with the C library's log1p; the
  * host re-evaluates them (value = +-(r - log1p(-u) / r)) so the block is bit-identical.
  */
+/*
+ * Tail fix-up of a draw: h_tails is the host copy of the draw's tails block (pinned), the
+ * values are re-evaluated with the C library's log1p (zig_r / zig_inv_r: NumPy's
+ * ziggurat_nor_r and ziggurat_nor_inv_r) into h_pairs (pinned, 2*tail_cap int64), copied
+ * to d_pairs (device, 2*tail_cap int64) and scattered into out on the stream.  Returns the
+ * number of values fixed, or -status.  (The Python loop of the reference's own draw,
+ * numpy/random/src/distributions/distributions.c random_standard_normal, tail branch.)
+ */
+int64_t hsseig_normals_fixup(const int64_t *h_tails, int64_t tail_cap, double zig_r,
+                             double zig_inv_r, int64_t *h_pairs, int64_t *d_pairs, double *out,
+                             void *stream);
 int hsseig_set_normal_tables(const uint64_t *ki, const double *wi, const double *fi);
 int64_t hsseig_normals_work_bytes(int64_t n);
 int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,

@@ -104,6 +104,7 @@ _SIGS = {
                                               c_vp, c_i64, c_vp]),
     "hsseig_set_normal_tables": (ctypes.c_int, [c_vp, c_vp, c_vp]),
     "hsseig_normals_work_bytes": (c_i64, [c_i64]),
+    "hsseig_normals_fixup": (c_i64, [c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp]),
     "hsseig_pcg64_normals": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint64, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp,
                                             c_vp, c_i64, c_vp]),

@@ -34,12 +34,20 @@ namespace hsseig {
 // tensor-map roles: 0 X, 1 G_l, 2 G_{l+1}, 3 F_{l-1} (or F_depth), 4 U, 5 B, 6 Vt, 7 D
 
 
-// All k-chunks of one job (both segments) for a warp whose first JM n-fragments are live.
+// One job tile for a warp whose first JM n-fragments are live (compile-time): accumulators,
+// k-chunks (both segments) and the epilogue are all sized by JM, so a tile sized for the
+// widest job of a launch spends neither DMMA work nor zeroing / store instructions on the
+// padding fragments of narrower jobs (inner HSS levels: ranks 34..82 under one tile shape).
 template <class T, int JM>
-__device__ __forceinline__ void consume_job(const TJob& jb, unsigned char* sm, uint64_t* full,
-                                            uint64_t* empty, uint32_t& q,
-                                            double (&acc)[T::MF][T::NF][2], int wm, int wn,
-                                            int lane) {
+__device__ __forceinline__ void run_job(const TJob& jb, unsigned char* sm, uint64_t* full,
+                                        uint64_t* empty, uint32_t& q, int64_t m0, int64_t M,
+                                        int wm, int wn, int lane) {
+  constexpr int JA = JM > 0 ? JM : 1;
+  double acc[T::MF][JA][2];
+#pragma unroll
+  for (int i = 0; i < T::MF; ++i)
+#pragma unroll
+    for (int j = 0; j < JA; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int sg = 0; sg < 2; ++sg) {
     const int K = jb.K[sg];
     const int nc = (K + T::BK - 1) / T::BK;
@@ -54,6 +62,29 @@ __device__ __forceinline__ void consume_job(const TJob& jb, unsigned char* sm, u
       else
         tmma_chunk_j<T, JM, false>(sA, sB, acc, wm, wn, lane, (K - c * T::BK + 3) & ~3);
       stage_release(&empty[slot], lane);
+    }
+  }
+  if (JM == 0) return;
+  // epilogue: accumulators for columns < N, zeros in [N, SW); a thread owns column pairs
+  // (2 gc, 2 gc + 1), stored as one 16-byte store when the job's rows are 16-byte aligned
+  const int gr = lane >> 2, gc = lane & 3;
+  const bool vec = ((reinterpret_cast<uintptr_t>(jb.C) | (uintptr_t)(jb.ldc * 8)) & 15) == 0;
+#pragma unroll
+  for (int i = 0; i < T::MF; ++i) {
+    const int64_t row = m0 + wm * T::MF * 8 + i * 8 + gr;
+    if (row >= M) continue;
+    double* crow = jb.C + row * jb.ldc;
+#pragma unroll
+    for (int j = 0; j < JA; ++j) {
+      const int col = wn * T::NF * 8 + j * 8 + 2 * gc;
+      const double v0 = col < jb.N ? acc[i][j][0] : 0.0;
+      const double v1 = col + 1 < jb.N ? acc[i][j][1] : 0.0;
+      if (vec && col + 1 < jb.SW) {
+        *reinterpret_cast<double2*>(crow + col) = make_double2(v0, v1);
+      } else {
+        if (col < jb.SW) crow[col] = v0;
+        if (col + 1 < jb.SW) crow[col + 1] = v1;
+      }
     }
   }
 }
@@ -107,42 +138,23 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
 
   // ---------------- DMMA consumers ----------------
   const int wm = warp / T::WN, wn = warp % T::WN;
-  const int gr = lane >> 2, gc = lane & 3;
   uint32_t q = 0;
-  double acc[T::MF][T::NF][2];
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
     const TJob jb = jobs[t / tiles_m];
     if (jb.N <= 0) continue;
     const int64_t m0 = (int64_t)(t % tiles_m) * T::BM;
     // n-fragments of this warp that carry output columns of this job (warp-uniform)
     const int jmax = min(T::NF, max(0, (jb.N - wn * T::NF * 8 + 7) >> 3));
-#pragma unroll
-    for (int i = 0; i < T::MF; ++i)
-#pragma unroll
-      for (int j = 0; j < T::NF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     switch (jmax) {
-#define HSS_JM_CASE(J)                                                              \
-  case J:                                                                           \
-    if constexpr (J <= T::NF) consume_job<T, J>(jb, sm, full, empty, q, acc, wm, wn, lane); \
+#define HSS_JM_CASE(J)                                                                   \
+  case J:                                                                                \
+    if constexpr (J <= T::NF) run_job<T, J>(jb, sm, full, empty, q, m0, M, wm, wn, lane); \
     break;
       HSS_JM_CASE(0) HSS_JM_CASE(1) HSS_JM_CASE(2) HSS_JM_CASE(3) HSS_JM_CASE(4)
       HSS_JM_CASE(5) HSS_JM_CASE(6) HSS_JM_CASE(7) HSS_JM_CASE(8) HSS_JM_CASE(9)
       HSS_JM_CASE(10) HSS_JM_CASE(11) HSS_JM_CASE(12) HSS_JM_CASE(13) HSS_JM_CASE(14)
 #undef HSS_JM_CASE
       default: break;
-    }
-    // epilogue: accumulators for columns < N, zeros in [N, SW)
-#pragma unroll
-    for (int i = 0; i < T::MF; ++i) {
-      const int64_t row = m0 + wm * T::MF * 8 + i * 8 + gr;
-      if (row >= M) continue;
-      double* crow = jb.C + row * jb.ldc;
-#pragma unroll
-      for (int j = 0; j < T::NF; ++j) {
-        const int col = wn * T::NF * 8 + j * 8 + 2 * gc;
-        if (col < jb.SW) crow[col] = col < jb.N ? acc[i][j][0] : 0.0;
-        if (col + 1 < jb.SW) crow[col + 1] = col + 1 < jb.N ? acc[i][j][1] : 0.0;
-      }
     }
   }
 }

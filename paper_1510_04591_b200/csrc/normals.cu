@@ -17,6 +17,9 @@
 //                at their global index.
 // The ziggurat tables are NumPy's own (ki/wi/fi), loaded once by the host from the
 // installed NumPy and checked against NumPy output before use.
+#include <cmath>
+#include <cstring>
+
 #include "common.cuh"
 
 namespace hsseig {
@@ -333,3 +336,44 @@ extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
+
+// Ziggurat-tail re-evaluation with the host C library's log1p (NumPy's random_standard_normal
+// evaluates the tail as -log1p(-u) / r with libm), then one ordered H2D copy of the
+// (offset, value) pairs and a scatter on the stream: no Python loop, no blocking upload.
+__global__ void tail_scatter_kernel(const int64_t* __restrict__ pairs, int64_t cnt,
+                                    double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < cnt) out[pairs[2 * t]] = __longlong_as_double(pairs[2 * t + 1]);
+}
+
+extern "C" int64_t hsseig_normals_fixup(const int64_t* h_tails, int64_t tail_cap, double zig_r,
+                                        double zig_inv_r, int64_t* h_pairs, int64_t* d_pairs,
+                                        double* out, void* stream) {
+  // returns the number of values fixed, or -status
+  if (!h_tails || !h_pairs || !d_pairs || !out || tail_cap < 0 || h_tails[0] < 0 ||
+      h_tails[0] > tail_cap) {
+    set_arg_error(__FILE__, __LINE__);
+    return -HSSEIG_ERR_ARG;
+  }
+  const int64_t cnt = h_tails[0];
+  for (int64_t t = 0; t < cnt; ++t) {
+    const int64_t* rec = h_tails + 1 + 3 * t;
+    const uint64_t u = static_cast<uint64_t>(rec[1]) >> 11;
+    const double xx = -zig_inv_r * log1p(-(static_cast<double>(u) * (1.0 / 9007199254740992.0)));
+    const double v = rec[2] ? -(zig_r + xx) : zig_r + xx;
+    int64_t bits;
+    memcpy(&bits, &v, sizeof(bits));
+    h_pairs[2 * t] = rec[0];
+    h_pairs[2 * t + 1] = bits;
+  }
+  if (cnt == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(d_pairs, h_pairs, sizeof(int64_t) * 2 * cnt, cudaMemcpyHostToDevice, s) !=
+      cudaSuccess)
+    return -HSSEIG_ERR_CUDA;
+  tail_scatter_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(d_pairs, cnt, out);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (cudaPeekAtLastError() != cudaSuccess) return -HSSEIG_ERR_CUDA;
+  return cnt;
+}
+

@@ -112,9 +112,9 @@ __device__ __forceinline__ void tmma_chunk(const double* __restrict__ sA, const 
 // narrower jobs (HSS levels mix ranks; the tile covers the largest one).
 // FULL: all BK k-columns live (no per-k-step exits, so the compiler can hoist the
 // fragment loads of later k-steps over the DMMAs of earlier ones).
-template <class T, int JM, bool FULL>
+template <class T, int JM, bool FULL, int JA>
 __device__ __forceinline__ void tmma_chunk_j(const double* __restrict__ sA, const double* __restrict__ sB,
-                                             double (&c)[T::MF][T::NF][2], int wm, int wn, int lane,
+                                             double (&c)[T::MF][JA][2], int wm, int wn, int lane,
                                              int kv) {
   const int gr = lane >> 2, gc = lane & 3;
   const double* a0 = sA + (wm * T::MF * 8 + gr) * T::SA + gc;

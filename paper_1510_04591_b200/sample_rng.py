@@ -9,7 +9,6 @@ callers draw on the host with NumPy (the reference's own call).
 """
 import ctypes
 import glob
-import math
 import os
 
 import numpy as np
@@ -85,7 +84,10 @@ class NormalStream:
         self.tails = torch.zeros(1 + 3 * TAIL_CAP, dtype=torch.int64, device="cuda")
         self.h_tails = torch.empty(1 + 3 * TAIL_CAP, dtype=torch.int64, pin_memory=True)
         self.h_fail = torch.empty(1, dtype=torch.int32, pin_memory=True)
+        self.h_pairs = torch.empty(2 * TAIL_CAP, dtype=torch.int64, pin_memory=True)
+        self.d_pairs = torch.empty(2 * TAIL_CAP, dtype=torch.int64, device="cuda")
         self._ev = None
+        self._fix_ev = None
 
     def draw(self, seed, n, out, w=None, ld=None, state=None):
         """Enqueue the first n normals of default_rng(seed) into out (device float64).
@@ -118,17 +120,16 @@ class NormalStream:
         self._ev.synchronize()
         if int(self.h_fail[0]):
             raise RuntimeError("device normal stream could not resolve the rejection chain")
-        cnt = int(self.h_tails[0])
-        if cnt == 0:
-            return 0
-        rec = self.h_tails[1:1 + 3 * cnt].numpy().reshape(cnt, 3)
-        vals = np.empty(cnt)
-        for t in range(cnt):
-            u = (int(rec[t, 1]) & 0xFFFFFFFFFFFFFFFF) >> 11
-            xx = -ZIG_INV_R * math.log1p(-(u * (1.0 / 9007199254740992.0)))
-            vals[t] = -(ZIG_R + xx) if rec[t, 2] else ZIG_R + xx
-        idx = torch.as_tensor(rec[:, 0].copy()).to("cuda", non_blocking=False)
-        self._out.view(-1)[idx] = torch.as_tensor(vals).to("cuda")
+        if self._fix_ev is not None:      # the previous fix-up's upload has left h_pairs
+            self._fix_ev.synchronize()
+        # host C (the C library's log1p, as NumPy) + one ordered upload + scatter kernel
+        cnt = int(self.lib.hsseig_normals_fixup(nat.ptr(self.h_tails), TAIL_CAP, ZIG_R, ZIG_INV_R,
+                                                nat.ptr(self.h_pairs), nat.ptr(self.d_pairs),
+                                                nat.ptr(self._out), nat.stream_ptr()))
+        if cnt < 0:
+            nat.check(-cnt, "normals_fixup")
+        self._fix_ev = torch.cuda.Event()
+        self._fix_ev.record()
         return cnt
 
     def failed(self):

@@ -39,7 +39,8 @@ out = {"file": os.path.basename(sys.argv[2]) if len(sys.argv) > 2 else sys.argv[
        "source_sha16": sha, "launches": 17, "bytes_read": rd, "bytes_write": wr,
        "bytes_per_multiply": rd + wr, "ncu_time_s": t,
        "algorithmic_bytes": 2 * 32768 * 32768 * 8,
-       "note": "one whole config-4 multiply (P = 32768 rows in one call, MergePipeline), ncu --set full replay (cold caches); algorithmic = Q_old read once + Q_new written once"}
+       "note": "one whole config-4 multiply (P = 32768 rows in one call, MergePipeline), ncu kernel replay "
+               "(cold caches); algorithmic = Q_old read once + Q_new written once"}
 if len(sys.argv) > 2:
     import shutil
     shutil.copy(sys.argv[1], sys.argv[2])
