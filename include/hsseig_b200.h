@@ -297,8 +297,10 @@ int hsseig_dense_update(const double *Qb, int64_t ldq, int64_t P, const hsseig_g
 /*
  * Tail fix-up of a draw: h_tails is the host copy of the draw's tails block (pinned), the
  * values are re-evaluated with the C library's log1p (zig_r / zig_inv_r: NumPy's
- * ziggurat_nor_r and ziggurat_nor_inv_r) into h_pairs (pinned, 2*tail_cap int64), copied
- * to d_pairs (device, 2*tail_cap int64) and scattered into out on the stream.  Returns the
+ * ziggurat_nor_r and ziggurat_nor_inv_r) into h_pairs (pinned, 2*tail_cap int64) and
+ * scattered into out on the stream by a kernel that reads them in place (mapped pinned
+ * memory; d_pairs, device 2*tail_cap int64, is the staging used only where host memory
+ * is not device-mapped).  Returns the
  * number of values fixed, or -status.  (The Python loop of the reference's own draw,
  * numpy/random/src/distributions/distributions.c random_standard_normal, tail branch.)
  */

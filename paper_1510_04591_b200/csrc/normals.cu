@@ -338,8 +338,8 @@ extern "C" int hsseig_pcg64_normals(uint64_t state_hi, uint64_t state_lo, uint64
 }
 
 // Ziggurat-tail re-evaluation with the host C library's log1p (NumPy's random_standard_normal
-// evaluates the tail as -log1p(-u) / r with libm), then one ordered H2D copy of the
-// (offset, value) pairs and a scatter on the stream: no Python loop, no blocking upload.
+// evaluates the tail as -log1p(-u) / r with libm), then a scatter kernel on the stream that
+// reads the (offset, value) pairs from pinned host memory: no Python loop, no blocking upload.
 __global__ void tail_scatter_kernel(const int64_t* __restrict__ pairs, int64_t cnt,
                                     double* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -368,10 +368,20 @@ extern "C" int64_t hsseig_normals_fixup(const int64_t* h_tails, int64_t tail_cap
   }
   if (cnt == 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemcpyAsync(d_pairs, h_pairs, sizeof(int64_t) * 2 * cnt, cudaMemcpyHostToDevice, s) !=
-      cudaSuccess)
-    return -HSSEIG_ERR_CUDA;
-  tail_scatter_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(d_pairs, cnt, out);
+  // the scatter reads the pinned pairs in place (mapped host memory): no copy-engine transfer,
+  // which would queue behind a bulk host->device stream (MergePipeline's streamed Q_old)
+  const int64_t* src = nullptr;
+  void* mapped = nullptr;
+  if (cudaHostGetDevicePointer(&mapped, h_pairs, 0) == cudaSuccess && mapped) {
+    src = static_cast<const int64_t*>(mapped);
+  } else {
+    cudaGetLastError();
+    if (cudaMemcpyAsync(d_pairs, h_pairs, sizeof(int64_t) * 2 * cnt, cudaMemcpyHostToDevice, s) !=
+        cudaSuccess)
+      return -HSSEIG_ERR_CUDA;
+    src = d_pairs;
+  }
+  tail_scatter_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(src, cnt, out);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (cudaPeekAtLastError() != cudaSuccess) return -HSSEIG_ERR_CUDA;
   return cnt;

@@ -566,19 +566,46 @@ def _srrsc_flops(tree, k):
     return f
 
 
-def finish_construct(tree, flops=None):
-    """Host read-back after construction: flags, ranks, r_used and the flop counter."""
+def _construct_parts(tree):
     nn = tree.ct.n_nodes
-    # one read-back for flags, residuals and ranks
     parts = [tree._view("rres", torch.float64, nn, 0), tree._view("cres", torch.float64, nn, 0),
              tree._view("flags", torch.int32, 2 * nn, 0), tree._view("rU", torch.int32, nn, 0),
              tree._view("rV", torch.int32, nn, 0)]
-    blob = torch.cat([t.view(torch.uint8) for t in parts]).cpu().numpy()
+    return torch.cat([t.view(torch.uint8) for t in parts])
+
+
+def prefetch_construct(tree, extra=None):
+    """Queue the host read-back finish_construct needs (flags, residuals, ranks; plus
+    `extra` = (device tensor, pinned host tensor) pairs) as pinned async copies behind the
+    construction, so later work (the multiply) can be queued before the host waits.
+    Returns the handle for finish_construct(pre=...)."""
+    dev = _construct_parts(tree)
+    buf = getattr(tree, "_host_blob", None)
+    if buf is None or buf.numel() != dev.numel():
+        buf = tree._host_blob = torch.empty(dev.numel(), dtype=torch.uint8, pin_memory=True)
+    buf.copy_(dev, non_blocking=True)
+    for d, h in (extra or ()):
+        h.copy_(d, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    return buf, ev
+
+
+def finish_construct(tree, flops=None, pre=None):
+    """Host read-back after construction: flags, ranks, r_used and the flop counter.
+    pre: the handle of prefetch_construct (waits for that read-back only, not the stream)."""
+    nn = tree.ct.n_nodes
+    # one read-back for flags, residuals and ranks
+    if pre is None:
+        blob = _construct_parts(tree).cpu().numpy()
+        tree._status.read()
+    else:
+        pre[1].synchronize()
+        blob = pre[0].numpy()
     rr = blob[:8 * nn].view(np.float64)
     cr = blob[8 * nn:16 * nn].view(np.float64)
     fl = blob[16 * nn:24 * nn].view(np.int32).reshape(nn, 2)
     tree._ranks = (blob[24 * nn:28 * nn].view(np.int32).copy(), blob[28 * nn:32 * nn].view(np.int32).copy())
-    tree._status.read()
     tree.flags = []
     # the reference appends flags in processing order: deepest level first, postorder within
     for idx in sorted((n.index for n in tree.nodes if n.index != tree.root),

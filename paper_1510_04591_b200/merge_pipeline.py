@@ -27,7 +27,7 @@ from . import sample_rng
 from .cauchy import CauchyEvecMatrix
 from .flops import cauchy_eval_flops, gemm_flops, secular_flops
 from .hss import (MAX_WIDTH, HssTree, _construct_flops, build_partition, finish_construct,
-                  mult_flops, rank_bound)
+                  mult_flops, prefetch_construct, rank_bound)
 from .secular import SecularConvergenceError, WeightRecomputationError
 
 _POOL = cf.ThreadPoolExecutor(max_workers=1)
@@ -224,17 +224,19 @@ class MergePipeline:
                                                         ctypes.byref(tree.ct), nat.ptr(self.status),
                                                         s), "hss_build_rand")
                     ev[5].record()
-                    finish_construct(tree)   # synchronises: flags, ranks, r_used
-                    fl_con = _construct_flops(tree, k, w)
-        if not self.device_rng:
-            self.host_omega.finish(0)
-        st = self.status.cpu().tolist()
-        if st[3] < k:
-            raise WeightRecomputationError(f"non-positive radicand at index {st[3]}")
         if out is None:
             out = torch.empty(X.shape[0], k, dtype=torch.float64, device="cuda")
         ev_m0 = torch.cuda.Event(enable_timing=True)
-        if tree is not None and not tree.flagged:
+        pre = None
+        if tree is not None:
+            # the multiply is queued right behind the construction and the async read-back of
+            # its flags / ranks / the status block, before the host waits for that read-back
+            # (the multiply's job table is built on the device from the ranks, its tiles
+            # cover the sample width); a flagged tree (rare) is then replaced by the dense
+            # fallback below, which overwrites out: the decision is the reference's
+            # (dc.py:147-160), only its latency is hidden
+            pre = prefetch_construct(tree, extra=[(self.status, self.h_status)])
+            tree.ct.rmax = 0
             rows_max = P if bounds is None else max(r1 - r0 for r0, r1 in bounds)
             need = int(lib.hsseig_matmul_work_doubles(rows_max, ctypes.byref(tree.ct)))
             if self._mwork is None or self._mwork.numel() < need:
@@ -261,6 +263,14 @@ class MergePipeline:
                     with torch.cuda.stream(self._d2h):
                         Oh[r0:r1].copy_(out[r0:r1], non_blocking=True)
             ev[6].record()
+            finish_construct(tree, pre=pre)   # waits for the read-back: flags, ranks, r_used
+            fl_con = _construct_flops(tree, k, w)
+        if not self.device_rng:
+            self.host_omega.finish(0)
+        st = self.h_status.tolist() if pre is not None else self.status.cpu().tolist()
+        if st[3] < k:
+            raise WeightRecomputationError(f"non-positive radicand at index {st[3]}")
+        if tree is not None and not tree.flagged:
             info["used_hss"] = True
             info["r_used"] = tree.r_used
             fl_mult_local = mult_flops(tree, X.shape[0])
@@ -270,6 +280,7 @@ class MergePipeline:
             if bounds is not None:
                 for e in ev_in:
                     torch.cuda.current_stream().wait_event(e)
+            ev_m0 = torch.cuda.Event(enable_timing=True)
             ev_m0.record()
             C.right_multiply_into(X, out=out)
             ev[6].record()

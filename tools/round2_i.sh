@@ -1,0 +1,5 @@
+export PYTHONUNBUFFERED=1
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/round2_i_tests.log 2>&1; echo "tests rc=$?"; grep -E "passed|failed|FAILED" gpurun_out/round2_i_tests.log | head -20
+timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu --no-eigh > gpurun_out/round2_i_bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/round2_i_bench.log | python -c "
+import json,sys; d=json.loads(sys.stdin.read())
+for k in ['value','ms_per_step','phases_ms','roofline','e2e']: print(k, json.dumps(d.get(k)))"
