@@ -271,6 +271,15 @@ int hsseig_hss_build_srrsc_levels(const hsseig_gen *gen, double tol, int32_t max
 int64_t hsseig_matmul_work_doubles(int64_t P, const hsseig_tree *tree);
 int hsseig_hss_matmul_right(const double *X, int64_t ldx, int64_t P, const hsseig_tree *tree,
                             double *out, int64_t ldo, double *work, void *stream);
+/*
+ * The same product in two parts: part 0 = the leaf up-level G = X U_leaf only (it reads
+ * nothing above the tree's leaf level, so it may run on a second stream beside the
+ * construction of the upper levels, on at most max_ctas SMs; 0 = no cap); part 1 = the
+ * rest, once part 0 and the whole construction are done.  Same work buffer for both.
+ */
+int hsseig_hss_matmul_right_part(const double *X, int64_t ldx, int64_t P,
+                                 const hsseig_tree *tree, double *out, int64_t ldo, double *work,
+                                 int32_t part, int32_t max_ctas, void *stream);
 
 /*
  * (a14) Dense update out = Qb @ C with C generated on the fly (fallback path).

@@ -97,6 +97,8 @@ _SIGS = {
     "hsseig_matmul_work_doubles": (c_i64, [c_i64, ctypes.POINTER(Tree)]),
     "hsseig_hss_matmul_right": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(Tree), c_vp,
                                                c_i64, c_vp, c_vp]),
+    "hsseig_hss_matmul_right_part": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(Tree), c_vp,
+                                                    c_i64, c_vp, ctypes.c_int32, ctypes.c_int32, c_vp]),
     "hsseig_dense_update": (ctypes.c_int, [c_vp, c_i64, c_i64, ctypes.POINTER(Gen), c_vp, c_i64,
                                            c_vp]),
     "hsseig_dense_update_work_doubles": (c_i64, [c_i64, c_i64]),

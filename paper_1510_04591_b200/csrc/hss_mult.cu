@@ -175,11 +175,13 @@ __host__ __device__ __forceinline__ int64_t lvl_off(int64_t P, int ws, int l) {
 
 // Job table: up-sweep level l at [2^l - 2, 2^{l+1} - 2) for l = 1..depth (2n-2 jobs),
 // down-sweep the same offsets shifted by 2n-2, the leaf finish last (n jobs).
-__global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs) {
+// Entries [e_lo, e_hi) only (a split multiply builds the leaf up-level's jobs first, the
+// rest once the upper ranks exist).
+__global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs, int e_lo, int e_hi) {
   const int n = p.n_leaves;
   const int nup = 2 * n - 2;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= 2 * nup + n) return;
+  const int e = e_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= e_hi || e >= 2 * nup + n) return;
   const int ws = p.ws;
   TJob jb;
   jb.am[0] = jb.am[1] = 0;
@@ -247,9 +249,11 @@ static int g_sms = 0;
 
 // Tensor maps live in device memory (one MapSet per launch, filled by an ordered H2D copy
 // on the launch stream) so the kernel can pick a map by role at run time.
+// max_ctas > 0 caps the persistent grid (a split multiply leaves SMs to the construction
+// kernels running beside it).
 template <class T>
 static int launch_tma(const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jobs, int njobs,
-                      int64_t M, cudaStream_t s) {
+                      int64_t M, cudaStream_t s, int max_ctas = 0) {
   if (njobs <= 0 || M <= 0) return HSSEIG_OK;
   static int per_sm = 0;
   if (!per_sm) {
@@ -275,7 +279,9 @@ static int launch_tma(const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jo
   if (!upload_maps(maps, dmaps, s)) return HSSEIG_ERR_CUDA;
   const int tiles_m = (int)((M + T::BM - 1) / T::BM);
   const int64_t total = (int64_t)tiles_m * njobs;
-  const int grid = (int)imin64(total, (int64_t)g_sms * per_sm);
+  int64_t cap = (int64_t)g_sms * per_sm;
+  if (max_ctas > 0 && max_ctas < cap) cap = max_ctas;
+  const int grid = (int)imin64(total, cap);
   tma_gemm_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(dmaps, jobs, njobs, M, tiles_m);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
@@ -295,19 +301,19 @@ using RankTile = TTile<2, NF, 8, 1, narrow_stages(NF)>;
 // narrow outputs (ranks, N <= 112).  Measured alternatives (BM 64 with 8 warps of 32 x 8NF,
 // BM 128 with NF = N/16, two CTAs per SM) were 5-10% slower at config 4.
 static int launch_narrow(int n, const Operand (&ops)[kMaps], MapSet* dm, const TJob* jobs, int njobs,
-                         int64_t M, cudaStream_t s) {
+                         int64_t M, cudaStream_t s, int max_ctas = 0) {
   switch ((n + 7) / 8) {
-    case 1: case 2: case 3: case 4: return launch_tma<RankTile<4>>(ops, dm, jobs, njobs, M, s);
-    case 5: return launch_tma<RankTile<5>>(ops, dm, jobs, njobs, M, s);
-    case 6: return launch_tma<RankTile<6>>(ops, dm, jobs, njobs, M, s);
-    case 7: return launch_tma<RankTile<7>>(ops, dm, jobs, njobs, M, s);
-    case 8: return launch_tma<RankTile<8>>(ops, dm, jobs, njobs, M, s);
-    case 9: return launch_tma<RankTile<9>>(ops, dm, jobs, njobs, M, s);
-    case 10: return launch_tma<RankTile<10>>(ops, dm, jobs, njobs, M, s);
-    case 11: return launch_tma<RankTile<11>>(ops, dm, jobs, njobs, M, s);
-    case 12: return launch_tma<RankTile<12>>(ops, dm, jobs, njobs, M, s);
-    case 13: return launch_tma<RankTile<13>>(ops, dm, jobs, njobs, M, s);
-    case 14: return launch_tma<RankTile<14>>(ops, dm, jobs, njobs, M, s);
+    case 1: case 2: case 3: case 4: return launch_tma<RankTile<4>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 5: return launch_tma<RankTile<5>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 6: return launch_tma<RankTile<6>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 7: return launch_tma<RankTile<7>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 8: return launch_tma<RankTile<8>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 9: return launch_tma<RankTile<9>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 10: return launch_tma<RankTile<10>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 11: return launch_tma<RankTile<11>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 12: return launch_tma<RankTile<12>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 13: return launch_tma<RankTile<13>>(ops, dm, jobs, njobs, M, s, max_ctas);
+    case 14: return launch_tma<RankTile<14>>(ops, dm, jobs, njobs, M, s, max_ctas);
     default: HSS_ARG_FAIL();
   }
 }
@@ -385,15 +391,17 @@ extern "C" int64_t hsseig_matmul_work_doubles(int64_t P, const hsseig_tree* t) {
   return 2 * P * (int64_t)t->ws * (2 * (int64_t)t->n_leaves - 2) + jobs_doubles(t->n_leaves);
 }
 
-extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
-                                       const hsseig_tree* t, double* out, int64_t ldo,
-                                       double* work, void* stream) {
+// part -1: the whole product; part 0: only the leaf up-level G_depth = X U_leaf (it needs
+// nothing above the leaf level of the tree, so it can run beside the construction of the
+// upper levels, on at most max_ctas SMs); part 1: the rest, after part 0 and the full build.
+static int matmul_right(const double* X, int64_t ldx, int64_t P, const hsseig_tree* t, double* out,
+                        int64_t ldo, double* work, int part, int max_ctas, cudaStream_t s) {
   if (!t || !X || !out || !work || P < 0 || ldx < t->k || ldo < t->k) HSS_ARG_FAIL();
+  if (part < -1 || part > 1) HSS_ARG_FAIL();
   if (P == 0) return HSSEIG_OK;
   if ((reinterpret_cast<uintptr_t>(X) & 15) || (ldx & 1) || (reinterpret_cast<uintptr_t>(work) & 15))
     HSS_ARG_FAIL();   // TMA needs 16-byte aligned rows
   if (P > 0x7fffffff) HSS_ARG_FAIL();
-  cudaStream_t s = (cudaStream_t)stream;
   const int ws = t->ws, n = t->n_leaves, nn = t->n_nodes, nup = 2 * n - 2;
   const int64_t lvl_total = P * (int64_t)ws * (2 * (int64_t)n - 2);
   MultPlan p;
@@ -409,8 +417,17 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   MapSet* dmaps = reinterpret_cast<MapSet*>(
       (reinterpret_cast<uintptr_t>(jobs + njob_total) + 255) & ~(uintptr_t)255);
   if (t->depth > 31) HSS_ARG_FAIL();
-  setup_jobs_kernel<<<(2 * nup + n + 127) / 128, 128, 0, s>>>(p, jobs);
-  HSS_CHECK_LAUNCH();
+  const int D = t->depth;
+  const int leaf_lo = (1 << D) - 2, leaf_hi = (1 << (D + 1)) - 2;   // the leaf up-level's jobs
+  auto setup = [&](int e_lo, int e_hi) -> int {
+    if (e_hi <= e_lo) return HSSEIG_OK;
+    setup_jobs_kernel<<<(e_hi - e_lo + 127) / 128, 128, 0, s>>>(p, jobs, e_lo, e_hi);
+    HSS_CHECK_LAUNCH();
+    return HSSEIG_OK;
+  };
+  if (part == -1) setup(0, njob_total);
+  else if (part == 0) setup(leaf_lo, leaf_hi);
+  else { setup(0, leaf_lo); setup(leaf_hi, njob_total); }
   auto lvl = [&](double* base, int l) -> Operand {
     if (l < 1 || l > t->depth) return Operand{nullptr, 0, 0, 0};
     const uint64_t cols = (uint64_t)(1u << l) * ws;
@@ -425,19 +442,35 @@ extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
   int rc;
   // output tiles cover the ranks (host bound rmax when the caller supplied it)
   const int nr = (t->rmax > 0 && t->rmax < t->w) ? t->rmax : t->w;
-  for (int l = t->depth; l >= 1; --l) {
+  for (int l = D; l >= 1; --l) {
+    if ((part == 0 && l != D) || (part == 1 && l == D)) continue;
     const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), lvl(p.Gb, l + 1), none, Uop, Bop, Vtop, Dop};
-    if ((rc = launch_narrow(nr, ops, dmaps + (t->depth - l), jobs + ((1 << l) - 2), 1 << l, P, s)))
+    if ((rc = launch_narrow(nr, ops, dmaps + (D - l), jobs + ((1 << l) - 2), 1 << l, P, s,
+                            part == 0 ? max_ctas : 0)))
       return rc;
   }
-  for (int l = 1; l <= t->depth; ++l) {
+  if (part == 0) return HSSEIG_OK;
+  for (int l = 1; l <= D; ++l) {
     const Operand ops[kMaps] = {Xop, lvl(p.Gb, l), none, lvl(p.Fb, l - 1), Uop, Bop, Vtop, Dop};
-    if ((rc = launch_narrow(nr, ops, dmaps + t->depth + l - 1, jobs + nup + ((1 << l) - 2), 1 << l,
-                            P, s)))
+    if ((rc = launch_narrow(nr, ops, dmaps + D + l - 1, jobs + nup + ((1 << l) - 2), 1 << l, P, s)))
       return rc;
   }
-  const Operand ops[kMaps] = {Xop, none, none, lvl(p.Fb, t->depth), Uop, Bop, Vtop, Dop};
-  return launch_wide(t->mmax, ops, dmaps + 2 * t->depth, jobs + 2 * nup, n, P, s);
+  const Operand ops[kMaps] = {Xop, none, none, lvl(p.Fb, D), Uop, Bop, Vtop, Dop};
+  return launch_wide(t->mmax, ops, dmaps + 2 * D, jobs + 2 * nup, n, P, s);
+}
+
+extern "C" int hsseig_hss_matmul_right(const double* X, int64_t ldx, int64_t P,
+                                       const hsseig_tree* t, double* out, int64_t ldo,
+                                       double* work, void* stream) {
+  return matmul_right(X, ldx, P, t, out, ldo, work, -1, 0, (cudaStream_t)stream);
+}
+
+extern "C" int hsseig_hss_matmul_right_part(const double* X, int64_t ldx, int64_t P,
+                                            const hsseig_tree* t, double* out, int64_t ldo,
+                                            double* work, int32_t part, int32_t max_ctas,
+                                            void* stream) {
+  if (part != 0 && part != 1) HSS_ARG_FAIL();
+  return matmul_right(X, ldx, P, t, out, ldo, work, part, max_ctas, (cudaStream_t)stream);
 }
 
 namespace hsseig {

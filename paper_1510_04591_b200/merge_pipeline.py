@@ -18,6 +18,7 @@ Per-phase device times are taken with CUDA events on the launching stream.
 """
 import concurrent.futures as cf
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -31,6 +32,9 @@ from .hss import (MAX_WIDTH, HssTree, _construct_flops, build_partition, finish_
 from .secular import SecularConvergenceError, WeightRecomputationError
 
 _POOL = cf.ThreadPoolExecutor(max_workers=1)
+# SMs left to the upper levels' construction while the multiply's leaf up-level runs beside
+# it (0: build, then multiply, in sequence)
+SPLIT_RESERVE = int(os.environ.get("HSSEIG_SPLIT_RESERVE", "48"))
 MAX_W = MAX_WIDTH
 CHUNK = 1 << 18
 
@@ -121,6 +125,8 @@ class MergePipeline:
         ev = self._events(7)
         ev[0].record()
         P = X.shape[0]
+        if out is None:
+            out = torch.empty(P, k, dtype=torch.float64, device="cuda")
         bounds = None
         if host_io is not None:
             Xh, Oh = host_io
@@ -182,6 +188,7 @@ class MergePipeline:
         use_hss = cfg.method == "adc-rand" and k > cfg.hss_threshold
         tree = None
         fl_con = 0
+        split = None
         if use_hss:
             mu_h = self.h_mu.numpy()
             try:
@@ -219,16 +226,37 @@ class MergePipeline:
                                                        nat.ptr(om), ws, w, nat.ptr(Y), nat.ptr(Z), ws,
                                                        nat.ptr(self.sample_work), s), "cauchy_sample")
                     ev[4].record()
-                    nat.check(lib.hsseig_hss_build_rand(C.gen, nat.ptr(om), ws, nat.ptr(Y),
-                                                        nat.ptr(Z), ws, float(1e-15), int(offdiag),
-                                                        ctypes.byref(tree.ct), nat.ptr(self.status),
-                                                        s), "hss_build_rand")
+                    bargs = (C.gen, nat.ptr(om), ws, nat.ptr(Y), nat.ptr(Z), ws, float(1e-15),
+                             int(offdiag), ctypes.byref(tree.ct), nat.ptr(self.status))
+                    depth = tree.ct.depth
+                    if bounds is None and SPLIT_RESERVE > 0 and depth >= 2:
+                        # leaf level first; its up-sweep product G = X U_leaf then runs on a
+                        # side stream (grid capped) beside the upper levels' construction
+                        nat.check(lib.hsseig_tree_clear(ctypes.byref(tree.ct), s), "tree_clear")
+                        nat.check(lib.hsseig_hss_build_rand_levels(*bargs, depth, depth, 0, 1, s),
+                                  "hss_build_rand_levels")
+                        split = self._leaf_up(X, out, tree)
+                        nat.check(lib.hsseig_hss_build_rand_levels(*bargs, depth - 1, 0, 0, 1, s),
+                                  "hss_build_rand_levels")
+                    else:
+                        nat.check(lib.hsseig_hss_build_rand(*bargs, s), "hss_build_rand")
                     ev[5].record()
-        if out is None:
-            out = torch.empty(X.shape[0], k, dtype=torch.float64, device="cuda")
         ev_m0 = torch.cuda.Event(enable_timing=True)
         pre = None
-        if tree is not None:
+        if tree is not None and split is not None:
+            # the leaf up-level already ran beside the construction: the rest of the product
+            pre = prefetch_construct(tree, extra=[(self.status, self.h_status)])
+            cur = torch.cuda.current_stream()
+            cur.wait_event(split[2])
+            ev_m0.record()
+            nat.check(lib.hsseig_hss_matmul_right_part(nat.ptr(X), X.stride(0), X.shape[0],
+                                                       ctypes.byref(tree.ct), nat.ptr(out),
+                                                       out.stride(0), nat.ptr(self._mwork), 1, 0, s),
+                      "hss_matmul_right_part")
+            ev[6].record()
+            finish_construct(tree, pre=pre)   # waits for the read-back: flags, ranks, r_used
+            fl_con = _construct_flops(tree, k, w)
+        elif tree is not None:
             # the multiply is queued right behind the construction and the async read-back of
             # its flags / ranks / the status block, before the host waits for that read-back
             # (the multiply's job table is built on the device from the ranks, its tiles
@@ -298,6 +326,12 @@ class MergePipeline:
               "loewner_normalizers": ev[1].elapsed_time(ev[2]),
               "multiply": ev_m0.elapsed_time(ev[6]),
               "total": ev[0].elapsed_time(ev[6])}
+        if split is not None and info["used_hss"]:
+            # kernel time of the product = its leaf up-level (side stream, beside the
+            # construction) + the rest; the span is from the leaf up-level's start
+            ms["multiply_leaf_up"] = split[1].elapsed_time(split[2])
+            ms["multiply"] += ms["multiply_leaf_up"]
+            ms["multiply_span"] = split[1].elapsed_time(ev[6])
         if info["used_hss"]:
             ms["host_partition_omega"] = ev[2].elapsed_time(ev[3])
             ms["sample"] = ev[3].elapsed_time(ev[4])
@@ -309,6 +343,35 @@ class MergePipeline:
         info["flops_total_fullP"] = fl_sec + fl_con + fl_mult_full + fl_dense
         info["iterations"] = iters
         return info
+
+    def _leaf_up(self, X, out, tree):
+        """Queue the multiply's leaf up-level on the side stream behind the leaf level of the
+        construction (grid capped to leave SPLIT_RESERVE SMs to the upper levels); returns
+        (stream, start event, done event)."""
+        lib = self.lib
+        P = X.shape[0]
+        tree.ct.rmax = 0       # ranks not read back yet: tiles cover the sample width
+        need = int(lib.hsseig_matmul_work_doubles(P, ctypes.byref(tree.ct)))
+        if self._mwork is None or self._mwork.numel() < need:
+            self._mwork = None
+            torch.cuda.empty_cache()
+            self._mwork = torch.empty(need, dtype=torch.float64, device="cuda")
+        if not hasattr(self, "_mult_stream"):
+            self._mult_stream = torch.cuda.Stream()
+        side = self._mult_stream
+        side.wait_stream(torch.cuda.current_stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sms = torch.cuda.get_device_properties(X.device).multi_processor_count
+        with torch.cuda.stream(side):
+            e0.record(side)
+            nat.check(lib.hsseig_hss_matmul_right_part(nat.ptr(X), X.stride(0), P,
+                                                       ctypes.byref(tree.ct), nat.ptr(out),
+                                                       out.stride(0), nat.ptr(self._mwork), 0,
+                                                       max(1, sms - SPLIT_RESERVE),
+                                                       nat.stream_ptr(side)),
+                      "hss_matmul_right_part")
+            e1.record(side)
+        return side, e0, e1
 
     def _tree(self, part, w):
         key = (part.ranges, w)
