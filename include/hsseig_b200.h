@@ -54,7 +54,7 @@ int hsseig_status_init(hsseig_status *status_dev, int64_t k, void *stream);
  * solve_secular (pkg/src/hsseig/secular.py:159-180).
  * d: k strictly ascending poles; z: k nonzero weights; rho > 0.
  * lam/gamma/mu: k outputs; iters: k per-root iteration counts (int32).
- * work: >= 2*k + 64 doubles of device scratch.
+ * work: >= 2*k + 64 doubles of device scratch, 16-byte aligned (packed poles).
  * status[0] += total iterations; status[1]/[2] = first bracket loss.
  */
 int hsseig_secular(const double *d, const double *z, int64_t k, double rho, double *lam,

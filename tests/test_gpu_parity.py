@@ -522,6 +522,29 @@ def test_pipeline_streamed_host_io_matches_device_run():
     assert torch.equal(Oh, out.cpu())
 
 
+@pytest.mark.parametrize("reserve", [8, 48, 100])
+def test_pipeline_split_leaf_up_matches_sequential(monkeypatch, reserve):
+    # the multiply's leaf up-level on a side stream beside the upper construction levels
+    # (capped grid) computes exactly what the sequential build -> multiply does
+    from paper_1510_04591_b200 import merge_pipeline as mp
+    n = 4096
+    d, u, rho = config4_system(n, 9)
+    cfg = hb.SolverConfig(leaf_size=128, hss_threshold=512, rank_eps=1e-13)
+    X = torch.randn(700, n, dtype=torch.float64, device="cuda")
+    dd, uu = torch.as_tensor(d, device="cuda"), torch.as_tensor(u, device="cuda")
+    outs, infos = [], []
+    for r in (0, reserve):
+        monkeypatch.setattr(mp, "SPLIT_RESERVE", r)
+        pipe = mp.MergePipeline(n, cfg, rows=700)
+        out = torch.empty_like(X)
+        infos.append(pipe.run(dd, uu, rho, X, seed=[0, 3], out=out))
+        outs.append(out)
+    assert "multiply_leaf_up" not in infos[0]["ms"] and "multiply_leaf_up" in infos[1]["ms"]
+    assert infos[0]["used_hss"] and infos[1]["used_hss"]
+    assert infos[0]["r_used"] == infos[1]["r_used"]
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("nparts", [2, 4])
 def test_partitioned_construction_equals_single_build(nparts):
     # the multi-GPU construction: every part builds its subtrees below level log2(nparts),
