@@ -399,10 +399,15 @@ int hsseig_wave_assemble(const uint64_t *q1, const uint64_t *q2, const int64_t *
                          const int64_t *n2, const int64_t *roff, const int32_t *row_merge,
                          const int64_t *csrc, const int64_t *coff, const int64_t *wd, double *W,
                          const int64_t *woff, int64_t nrows, void *stream);
-/* Deflation rotations of every merge on its W_m (dc.py:225-230). */
+/* Deflation rotations of every merge on its W_m (dc.py:225-230).  A merge's rotations
+ * (deflation's (survivor, deflated) pairs) split into runs sharing one survivor; run_t lists
+ * the first rotation of every run over all merges plus a final sentinel (the rotation
+ * count), run_off (nm + 1) each merge's first run.  Runs touch disjoint columns, so each
+ * (row, run) pair is an independent task; max_tasks = max over merges of n_m * runs_m. */
 int hsseig_wave_rotate(double *W, const int64_t *woff, const int64_t *n, const int64_t *wd,
-                       const int64_t *rot_off, const int64_t *ca, const int64_t *cb,
-                       const double *c, const double *s, int64_t nm, int64_t nmax, void *stream);
+                       const int64_t *run_t, const int64_t *run_off, const int64_t *ca,
+                       const int64_t *cb, const double *c, const double *s, int64_t nm,
+                       int64_t max_tasks, void *stream);
 /* Secular roots of every kept system (secular_all per system); work: ntot + nseg doubles. */
 int hsseig_wave_secular(const double *d, const double *z, const int64_t *koff,
                         const int32_t *seg_of, const double *rho, int64_t nseg, int64_t ntot,

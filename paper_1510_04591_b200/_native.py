@@ -129,7 +129,7 @@ _SIGS = {
     "hsseig_wave_deflate": (c_i64, [c_i64] + [c_vp] * 16),
     "hsseig_wave_compact": (c_i64, [c_i64] + [c_vp] * 10),
     "hsseig_wave_assemble": (ctypes.c_int, [c_vp] * 11 + [c_i64, c_vp]),
-    "hsseig_wave_rotate": (ctypes.c_int, [c_vp] * 9 + [c_i64, c_i64, c_vp]),
+    "hsseig_wave_rotate": (ctypes.c_int, [c_vp] * 10 + [c_i64, c_i64, c_vp]),
     "hsseig_wave_secular": (ctypes.c_int, [c_vp] * 5 + [c_i64, c_i64] + [c_vp] * 7),
     "hsseig_wave_dnext": (ctypes.c_int, [c_vp] * 5 + [c_i64, c_vp, c_vp]),
     "hsseig_wave_loewner": (ctypes.c_int, [c_vp] * 8 + [c_i64, c_vp, c_vp, c_vp]),

@@ -291,24 +291,38 @@ __global__ void wave_assemble_kernel(const unsigned long long* __restrict__ q1,
   }
 }
 
+// Deflation rotations (dc.py:225-230: col_a = c*a + s*b, col_b = -s*a + c*b, no FMA
+// contraction), split into runs: deflation's pair t is (survivor, deflated) (secular.py:
+// 96-156); a survivor holds for a contiguous run of rotations and is never deflated later,
+// and each deflated column appears once, so different runs touch disjoint columns.  Every
+// (row, run) pair is an independent task -- consecutive threads take consecutive runs of
+// one row (neighbouring columns) -- and a run carries its survivor in a register.
 __global__ void wave_rotate_kernel(double* __restrict__ W, const int64_t* __restrict__ woff,
                                    const int64_t* __restrict__ nn, const int64_t* __restrict__ wd,
-                                   const int64_t* __restrict__ rot_off,
+                                   const int64_t* __restrict__ run_t,
+                                   const int64_t* __restrict__ run_off,
                                    const int64_t* __restrict__ ca, const int64_t* __restrict__ cb,
                                    const double* __restrict__ cs, const double* __restrict__ sn) {
   const int m = blockIdx.y;
-  const int64_t n = nn[m], r0 = rot_off[m], r1 = rot_off[m + 1], ld = wd[m] + (wd[m] & 1);
-  if (r0 == r1) return;
-  for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n;
-       row += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t q0 = run_off[m], nr = run_off[m + 1] - q0;
+  if (nr <= 0) return;
+  const int64_t n = nn[m], ld = wd[m] + (wd[m] & 1), ntask = n * nr;
+  for (int64_t task = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; task < ntask;
+       task += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = task / nr, r = task - row * nr;
+    const int64_t t0 = __ldg(run_t + q0 + r), t1 = __ldg(run_t + q0 + r + 1);
     double* w = W + woff[m] + row * ld;
-    for (int64_t t = r0; t < r1; ++t) {
-      const int64_t ia = ca[t], ib = cb[t];
-      const double c = cs[t], s = sn[t];
-      const double x = w[ia], y = w[ib];
-      w[ia] = __dadd_rn(__dmul_rn(c, x), __dmul_rn(s, y));
-      w[ib] = __dadd_rn(__dmul_rn(-s, x), __dmul_rn(c, y));
+    const int64_t ia = __ldg(ca + t0);
+    double xa = w[ia];
+    for (int64_t t = t0; t < t1; ++t) {
+      const int64_t ib = __ldg(cb + t);
+      const double c = __ldg(cs + t), s = __ldg(sn + t);
+      const double y = w[ib];
+      const double na = __dadd_rn(__dmul_rn(c, xa), __dmul_rn(s, y));
+      w[ib] = __dadd_rn(__dmul_rn(-s, xa), __dmul_rn(c, y));
+      xa = na;
     }
+    w[ia] = xa;
   }
 }
 
@@ -552,13 +566,14 @@ extern "C" int hsseig_wave_assemble(const uint64_t* q1, const uint64_t* q2, cons
 }
 
 extern "C" int hsseig_wave_rotate(double* W, const int64_t* woff, const int64_t* n,
-                                  const int64_t* wd, const int64_t* rot_off, const int64_t* ca,
-                                  const int64_t* cb, const double* c, const double* s, int64_t nm,
-                                  int64_t nmax, void* stream) {
-  if (nm < 0 || nmax < 0 || nm > 65535) HSS_ARG_FAIL();
-  if (nm == 0 || nmax == 0) return HSSEIG_OK;
-  dim3 grid((unsigned)std::min<int64_t>((nmax + 127) / 128, 1024), (unsigned)nm);
-  wave_rotate_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(W, woff, n, wd, rot_off, ca, cb, c, s);
+                                  const int64_t* wd, const int64_t* run_t, const int64_t* run_off,
+                                  const int64_t* ca, const int64_t* cb, const double* c,
+                                  const double* s, int64_t nm, int64_t max_tasks, void* stream) {
+  if (nm < 0 || max_tasks < 0 || nm > 65535 || !W || !run_t || !run_off) HSS_ARG_FAIL();
+  if (nm == 0 || max_tasks == 0) return HSSEIG_OK;
+  dim3 grid((unsigned)std::min<int64_t>((max_tasks + 255) / 256, 8192), (unsigned)nm);
+  wave_rotate_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(W, woff, n, wd, run_t, run_off, ca, cb,
+                                                             c, s);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }

@@ -423,16 +423,28 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             tk[:, 0] = small[tq]
             tk[:, 1] = loc // nt[tq]
             tk[:, 2] = loc % nt[tq]
+        # rotation runs (one survivor each; disjoint columns): the rotate kernel's tasks
+        if nrot:
+            ca_h = ca[:nrot]
+            starts = np.ones(nrot, dtype=bool)
+            starts[1:] = ca_h[1:] != ca_h[:-1]
+            starts[rot_off[:-1][np.diff(rot_off) > 0]] = True     # merge boundaries
+            run_t = np.flatnonzero(starts)
+            run_off = np.searchsorted(run_t, rot_off).astype(np.int64)
+            run_t = np.append(run_t, nrot)
+            rot_tasks = int((nv * np.diff(run_off)).max())
+        else:
+            run_t, run_off, rot_tasks = np.zeros(1, np.int64), np.zeros(nm + 1, np.int64), 0
         st0 = np.zeros((nseg, 8), dtype=np.int64)
         st0[:, 1:4] = ks[:, None]
-        (woff_d, wd_d, row_merge, csrc_d, coff_d, rot_d0, rot_d1, rot_d2, rot_d3, rot_d4, dk, zk,
-         koff_d, seg_of, rho_d, st, t_woff, t_nv, t_qoff, t_tk, t_ldw) = (
+        (woff_d, wd_d, row_merge, csrc_d, coff_d, rot_d1, rot_d2, rot_d3, rot_d4, dk, zk,
+         koff_d, seg_of, rho_d, st, t_woff, t_nv, t_qoff, t_tk, t_ldw, run_t_d, run_off_d) = (
             _Pack().add(woff).add(wd).add(rm, np.int32).add(csrc[:int(coff[-1])]).add(coff)
-            .add(rot_off).add(ca[:nrot]).add(cb[:nrot]).add(rc[:nrot], np.float64)
+            .add(ca[:nrot]).add(cb[:nrot]).add(rc[:nrot], np.float64)
             .add(rs[:nrot], np.float64).add(d_out[kidx], np.float64).add(z_out[kidx], np.float64)
             .add(koff).add(np.repeat(np.arange(nseg), ks), np.int32)
             .add(rho_eff[segs], np.float64).add(st0).add(woff[segs]).add(nvs).add(qoff[segs])
-            .add(tk, np.int32).add(ldw[segs]).send())
+            .add(tk, np.int32).add(ldw[segs]).add(run_t).add(run_off).send())
         W = torch.empty(max(int(woff[-1]), 2), **f64)
         prof = GLUE_PROFILE
         if prof is not None:
@@ -448,8 +460,9 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                                            nrows, s), "wave_assemble")
         if nrot:
             nat.check(lib.hsseig_wave_rotate(nat.ptr(W), nat.ptr(woff_d), nat.ptr(nv_d), nat.ptr(wd_d),
-                                             nat.ptr(rot_d0), nat.ptr(rot_d1), nat.ptr(rot_d2),
-                                             nat.ptr(rot_d3), nat.ptr(rot_d4), nm, int(nv.max()), s),
+                                             nat.ptr(run_t_d), nat.ptr(run_off_d), nat.ptr(rot_d1),
+                                             nat.ptr(rot_d2), nat.ptr(rot_d3), nat.ptr(rot_d4), nm,
+                                             rot_tasks, s),
                       "wave_rotate")
         if prof is not None:
             ev_g[1].record()
