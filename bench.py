@@ -481,6 +481,8 @@ def eigh_distributed(world, ops=None, device="cuda", n=65536, warm=True):
     Gs = Q[:, cols].T @ Q
     dist.all_reduce(Gs)
     Gs[torch.arange(ns, device=device), cols] -= 1.0
+    if hasattr(ops, "close"):
+        ops.close()                # CUDA-IPC peer buffers unmapped in group order
     return {"wall_s": best, "ranks": world, "merges": len(res.merges),
             "hss_merges": int(sum(m.used_hss for m in res.merges)),
             "orthogonality_sampled_cols": ns, "orthogonality": float(Gs.abs().max()) / n,
@@ -628,7 +630,7 @@ def run_ours(args):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            lam, res, info = sm.run(dd, uu, rho, Xin, seed=[SEED, 0])
+            lam, res, info = sm.run(dd, uu, rho, Xin, seed=[SEED, 0], rows_total=n)
             e1.record()
             out.copy_(res)
             torch.cuda.synchronize()
@@ -746,6 +748,8 @@ def run_ours(args):
         adc1 = adc1_merge(d, u, rho, Qloc, out)
 
     # the full solves below need the HBM the merge bench holds (Q_old, outputs, workspaces)
+    if world > 1:
+        sm.ops.close()             # CUDA-IPC peer buffers unmapped in group order
     pipe = sm = step = Xd = None   # noqa: F841
     del Qloc, out
     import gc

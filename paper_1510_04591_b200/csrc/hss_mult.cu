@@ -91,7 +91,7 @@ __device__ __forceinline__ void run_job(const TJob& jb, unsigned char* sm, uint6
 
 template <class T>
 __global__ void __launch_bounds__(T::THREADS, T::MINB)
-    tma_gemm_kernel(const MapSet* __restrict__ maps, const TJob* __restrict__ jobs, int njobs,
+    tma_gemm_kernel(const __grid_constant__ MapSet maps, const TJob* __restrict__ jobs, int njobs,
                     int64_t M, int tiles_m) {
   extern __shared__ __align__(128) unsigned char smraw[];
   // 128-byte aligned ring; pointer arithmetic on the __shared__ array keeps the shared
@@ -113,7 +113,6 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
   if (warp == T::CONSUMERS) {
     // ---------------- TMA producer (one lane) ----------------
     if (lane == 0) {
-      for (int r = 0; r < kMaps; ++r) tmap_acquire(&maps->m[r]);
       uint32_t q = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const TJob jb = jobs[t / tiles_m];
@@ -126,8 +125,8 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB)
             mbar_wait(&empty[slot], ((q / T::STAGES) & 1) ^ 1);
             mbar_expect_tx(&full[slot], T::A_BYTES + T::B_BYTES);
             unsigned char* st = sm + (size_t)slot * T::STAGE_BYTES;
-            tma_load_2d(st, &maps->m[jb.am[sg]], jb.acol[sg] + c * T::BK, m0, &full[slot]);
-            tma_load_2d(st + T::A_BYTES, &maps->m[jb.bm[sg]], jb.bcol[sg], jb.brow[sg] + c * T::BK,
+            tma_load_2d(st, &maps.m[jb.am[sg]], jb.acol[sg] + c * T::BK, m0, &full[slot]);
+            tma_load_2d(st + T::A_BYTES, &maps.m[jb.bm[sg]], jb.bcol[sg], jb.brow[sg] + c * T::BK,
                         &full[slot]);
           }
         }
@@ -247,8 +246,9 @@ __global__ void setup_jobs_kernel(MultPlan p, TJob* __restrict__ jobs, int e_lo,
 
 static int g_sms = 0;
 
-// Tensor maps live in device memory (one MapSet per launch, filled by an ordered H2D copy
-// on the launch stream) so the kernel can pick a map by role at run time.
+// The launch's tensor maps travel as one __grid_constant__ MapSet kernel parameter (no
+// device copy, no extra launch); the producer picks a map by role at run time through its
+// parameter-space address.
 // max_ctas > 0 caps the persistent grid (a split multiply leaves SMs to the construction
 // kernels running beside it).
 template <class T>
@@ -276,13 +276,13 @@ static int launch_tma(const Operand (&ops)[kMaps], MapSet* dmaps, const TJob* jo
     if (!make_map(&maps.m[r], ops[r].base, ops[r].rows, ops[r].cols, ops[r].ld, bc, br))
       HSS_ARG_FAIL();
   }
-  if (!upload_maps(maps, dmaps, s)) return HSSEIG_ERR_CUDA;
+  (void)dmaps;   // the maps travel as a __grid_constant__ kernel parameter
   const int tiles_m = (int)((M + T::BM - 1) / T::BM);
   const int64_t total = (int64_t)tiles_m * njobs;
   int64_t cap = (int64_t)g_sms * per_sm;
   if (max_ctas > 0 && max_ctas < cap) cap = max_ctas;
   const int grid = (int)imin64(total, cap);
-  tma_gemm_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(dmaps, jobs, njobs, M, tiles_m);
+  tma_gemm_kernel<T><<<grid, T::THREADS, T::SMEM_BYTES, s>>>(maps, jobs, njobs, M, tiles_m);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }

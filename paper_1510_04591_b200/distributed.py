@@ -101,8 +101,25 @@ class PeerBuffers:
         oks = [None] * world
         dist.all_gather_object(oks, ok, group=group)
         self.ok = all(oks)                 # one decision for the whole group
+        self.group = group
         if not self.ok:
             self.views, self.ptrs = [], []
+
+    def close(self):
+        """Unmap the peers' buffers before anyone frees its own: every rank drains its
+        stream, the group agrees, the imported views are dropped, and the group agrees again
+        (an exporter that exits while an importer still maps its memory can take the
+        importer down at teardown)."""
+        if not self.views and not self.local:
+            return
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        self.views, self.ptrs = [], []
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        self.local = []
 
 
 _FENCE = {}
@@ -128,6 +145,26 @@ def peer_fence(group=None):
         return
     torch.cuda.current_stream().synchronize()
     dist.barrier(group=group)
+
+
+def _host_copy(ts):
+    """Small device tensors to pinned host memory behind the current stream (async, one
+    event); CPU tensors (the gloo test ops) are taken as they are."""
+    if not ts[0].is_cuda:
+        return [t.clone() for t in ts], None
+    hs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in ts]
+    for h, t in zip(hs, ts):
+        h.copy_(t, non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    return hs, ev
+
+
+def _host_wait(p):
+    hs, ev = p
+    if ev is not None:
+        ev.synchronize()
+    return [h.numpy() for h in hs]
 
 
 def rank_from(part, span, mu_h, eps, cap):
@@ -172,21 +209,33 @@ class ShardedMerge:
         full = gather_rows(torch.stack([lam_l, gam_l, mu_l], 1), c, k, self.group)
         lam, gam, mu = full[:, 0].contiguous(), full[:, 1].contiguous(), full[:, 2].contiguous()
         st = gather_rows(st_l.view(1, -1), 1, self.world, self.group)   # world x 3
-        iters = int(st[:, 0].sum())
-        bad_g = int(st[:, 1].min())
-        bad_m = int(st[:, 2].min())
-        bad = bad_g if bad_g < k else (bad_m if (k >= 2 and bad_m < k) else -1)
-        if bad >= 0:
-            raise SecularConvergenceError(f"root {bad} lost its bracket")
+        # what the host decides on (bracket status, the pole gaps for the partition, the
+        # span) comes back through async pinned copies while Loewner / normalizers run
+        pend = _host_copy([st.reshape(-1).to(torch.int64),
+                           torch.cat([mu.reshape(-1), torch.stack([d[0], d[-1], gam[-1]])])])
         mark("secular")
         dn = ops.dnext(d, gam, mu)
         zh_l, rad_l = ops.loewner_part(d, dn, gam, mu, z, rho, lo, hi)
         zh = gather_rows(zh_l, c, k, self.group).contiguous()
         rad = gather_rows(rad_l.view(1, -1), 1, self.world, self.group)
-        if int(rad.min()) < k:
-            raise WeightRecomputationError(f"non-positive radicand at index {int(rad.min())}")
+        pend_rad = _host_copy([rad.reshape(-1).to(torch.int64)])
         v_l = ops.normalizers_part(d, dn, gam, mu, zh, lo, hi)
         v = gather_rows(v_l, c, k, self.group).contiguous()
+        st_h, muh = _host_wait(pend)
+        st_h = st_h.reshape(self.world, -1)
+        iters = int(st_h[:, 0].sum())
+        bad_g = int(st_h[:, 1].min())
+        bad_m = int(st_h[:, 2].min())
+        bad = bad_g if bad_g < k else (bad_m if (k >= 2 and bad_m < k) else -1)
+        if bad >= 0:
+            raise SecularConvergenceError(f"root {bad} lost its bracket")
+        mu_h, (d0_h, dl_h, gl_h) = muh[:k], muh[k:]
+
+        def check_weights():
+            rmin = int(_host_wait(pend_rad)[0].min())
+            if rmin < k:
+                raise WeightRecomputationError(f"non-positive radicand at index {rmin}")
+
         info["iterations"] = iters
         info["flops_secular"] = secular_flops(k, iters) + 14 * k * k
         mark("loewner_normalizers")
@@ -195,7 +244,7 @@ class ShardedMerge:
         if cfg.method == "adc-srrsc" and k > cfg.hss_threshold:
             # ADC1: no sample; the construction is partitioned by subtree like ADC2's
             try:
-                part = build_partition(k, cfg.leaf_size, None, None, mu.cpu().numpy())
+                part = build_partition(k, cfg.leaf_size, None, None, mu_h)
             except ValueError:
                 part = None
             if part is not None:
@@ -203,13 +252,12 @@ class ShardedMerge:
                 tree = ops.build_srrsc(gen, part, cap, cfg.srrsc_tol, self.group)
                 mark("build")
         elif cfg.method == "adc-rand" and k > cfg.hss_threshold:
-            mu_h = mu.cpu().numpy()
             try:
                 part = build_partition(k, cfg.leaf_size, None, None, mu_h)
             except ValueError:
                 part = None
             if part is not None:
-                span = float((d[-1] + gam[-1]) - d[0])
+                span = float((dl_h + gl_h) - d0_h)
                 r = min(rank_from(part, span, mu_h, cfg.rank_eps, cfg.rank_cap),
                         part.min_leaf - cfg.oversample)
                 w = r + cfg.oversample
@@ -234,6 +282,7 @@ class ShardedMerge:
                     mark("sample_gather")
                     tree = ops.build(gen, part, w, om, Y, Z, self.group, offdiag)
                     mark("build")
+        check_weights()   # the construction has synchronised: the radicands are long back
         if tree is not None and not ops.flagged(tree):
             info["used_hss"] = True
             info["r_used"] = ops.r_used(tree)
@@ -352,6 +401,13 @@ class GpuOps:
 
     def _s(self):
         return self.nat.stream_ptr()
+
+    def close(self):
+        """Release the CUDA-IPC peer buffers in group order (call on every rank before
+        destroy_process_group)."""
+        for pb in self._peer or []:
+            pb.close()
+        self._peer, self._peer_key = None, None
 
     def _fit(self, k):
         # the ops serve merges of any order up to the one they were sized for

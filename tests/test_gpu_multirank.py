@@ -41,11 +41,13 @@ def _worker(rank, world, port, out_path, peer="1"):
     lam, out, info = sm.run(torch.as_tensor(d, device="cuda"), torch.as_tensor(u, device="cuda"),
                             rho, X[r0:r1].contiguous(), seed=[0, 7])
     cfg1 = hb.SolverConfig(leaf_size=64, hss_threshold=256, method="adc-srrsc")
-    _, out1, info1 = ShardedMerge(n, cfg1, GpuOps(n)).run(
+    ops1 = GpuOps(n)
+    _, out1, info1 = ShardedMerge(n, cfg1, ops1).run(
         torch.as_tensor(d, device="cuda"), torch.as_tensor(u, device="cuda"), rho,
         X[r0:r1].contiguous(), seed=[0, 7])
     T = hb.gen_config5(1024, 4)
-    res = adc_solve_distributed(T, hb.SolverConfig(rank_eps=1e-13), GpuOps(512))
+    ops5 = GpuOps(512)
+    res = adc_solve_distributed(T, hb.SolverConfig(rank_eps=1e-13), ops5)
     # the sample rows went straight into both ranks' Y / Z (CUDA IPC peer stores fused in
     # the split-K reduction), not through a separate all-gather
     assert info.get("sample_gather") == ("peer" if peer == "1" else "nccl"), info.get("sample_gather")
@@ -59,6 +61,9 @@ def _worker(rank, world, port, out_path, peer="1"):
         np.savez(out_path, lam=lam.cpu().numpy(), out=np.concatenate([o[0] for o in outs]),
                  used=info["used_hss"], elam=res.lam, Q=Q,
                  out1=np.concatenate([o[4] for o in outs]), used1=all(o[5] for o in outs))
+    # the CUDA-IPC peer buffers are unmapped in group order before the processes exit
+    for ops in (sm.ops, ops1, ops5):
+        ops.close()
     dist.destroy_process_group()
 
 
