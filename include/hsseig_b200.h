@@ -196,7 +196,7 @@ typedef struct hsseig_tree {
  * drops below (tol ||M||_F)^2 or at max_rank, saturation flag, X = identity on J.
  * Matrix b at M + b*stride_m (leading dimension ldm); X (p x max_rank, ldx) at
  * X + b*stride_x, J[b*max_rank ..], rank / resid / saturated per matrix.  Shared memory
- * per matrix: hsseig_interp_smem_bytes(p, w) <= 227 KB.
+ * per matrix: hsseig_interp_smem_bytes(p, w) <= 227 KB; w <= 128 (the sample widths).
  */
 int64_t hsseig_interp_smem_bytes(int32_t p, int32_t w);
 int hsseig_interp_decomp(const double *M, int64_t ldm, int64_t stride_m, int32_t p, int32_t w,

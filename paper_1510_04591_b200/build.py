@@ -37,6 +37,7 @@ def build(force=False, verbose=False):
     odir = os.path.join(os.path.dirname(PKG), "build", "obj")
     os.makedirs(odir, exist_ok=True)
     cflags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "shared")]
+    cflags += os.environ.get("HSSEIG_NVCC_EXTRA", "").split()   # e.g. -DHSSEIG_ID_TIMING (tools)
 
     def comp(src):
         obj = os.path.join(odir, os.path.basename(src)[:-3] + ".o")

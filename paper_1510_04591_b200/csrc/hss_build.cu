@@ -201,15 +201,6 @@ __global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level, i
   }
 }
 
-// LAPACK dlapy2: sqrt(x^2 + y^2) without destructive under/overflow
-__device__ __forceinline__ double lapy2(double x, double y) {
-  double xa = fabs(x), ya = fabs(y);
-  double wv = fmax(xa, ya), zv = fmin(xa, ya);
-  if (zv == 0.0) return wv;
-  double q = zv / wv;
-  return wv * sqrt(1.0 + q * q);
-}
-
 // Truncation of the factored A = M^T (hss.py:128-148): trailing Frobenius mass of R's
 // rows, rank r = min(first t with tail(t) <= (tol ||M||_F)^2, max_rank, nonzero diagonal),
 // saturation flag, relative residual, then T = R11^{-1} R12 in place (dtrsm L/U/N/N).
@@ -445,6 +436,18 @@ __device__ __forceinline__ void id_finish(const TreeDev& T, int side, int node, 
   }
 }
 
+#ifdef HSSEIG_ID_TIMING
+// per-phase clock64 totals of block 0 / thread 0 (tools/id_timing.cu):
+// [0] warp-0 pivot + reflector, [1] wait at the reflector barrier, [2] own update,
+// [3] wait at the end-of-step barrier, [4] steps, [5] elimination total, [6] finish total
+__device__ unsigned long long g_id_t[8];
+#define ID_T0(v) long long v = 0; if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) v = clock64()
+#define ID_ACC(k, from, to) if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) { to = clock64(); g_id_t[k] += to - from; }
+#else
+#define ID_T0(v)
+#define ID_ACC(k, from, to)
+#endif
+
 // Norms and column-pivoted Householder elimination of A = M^T held in sA (candidate j at
 // sA[j*SW + t]; piv[j] = j on entry).  dgeqp3/dlaqp2 semantics: pivot = first maximum of
 // the downdated norms (idamax), dlarfg reflector, dlaqp2 norm downdate with the sqrt(eps)
@@ -495,6 +498,11 @@ __device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* 
   const int stop_at = min(mn, max(max_rank, 1));
   if (!(nf == 0.0 || p == 0 || w == 0)) {
     for (int i = 0; i < mn; ++i) {
+      ID_T0(ta);
+#ifdef HSSEIG_ID_TIMING
+      long long tb = 0, tc = 0, td = 0, te = 0;
+      if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_id_t[4] += 1;
+#endif
       if (warp == 0) {
         double best = -1.0;
         int bi = i;
@@ -508,39 +516,56 @@ __device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* 
           int oi = __shfl_xor_sync(0xffffffffu, bi, o);
           if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
         }
+        // swap and reflector in one pass: the pivot column and column i come into
+        // registers (w <= 128: four rows per lane), dlarfg runs on the pivot's values, and
+        // position i receives the reflected column while position pvt receives old column i
         const int pvt = bi;
-        if (pvt != i) {
-          for (int t = lane; t < w; t += 32) {
-            double x0 = sA[i * SW + t];
-            sA[i * SW + t] = sA[pvt * SW + t];
-            sA[pvt * SW + t] = x0;
-          }
-          if (lane == 0) {
-            int tp = piv[pvt]; piv[pvt] = piv[i]; piv[i] = tp;
-            vn1[pvt] = vn1[i];
-            vn2[pvt] = vn2[i];
-          }
+        double* ci = sA + i * SW;
+        double* cp = sA + pvt * SW;
+        double pv[4], cv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = lane + 32 * j;
+          pv[j] = t < w ? cp[t] : 0.0;
+          cv[j] = (t < w && pvt != i) ? ci[t] : 0.0;
         }
-        __syncwarp();
-        double* col = sA + i * SW;
         double xs = 0.0;
-        for (int t = i + 1 + lane; t < w; t += 32) xs = fma(col[t], col[t], xs);
-        const double xnorm = sqrt(warp_sum(xs));
-        const double alpha = col[i];
-        double tau = 0.0, beta = alpha;
-        if (xnorm != 0.0) {
-          beta = -copysign(lapy2(alpha, xnorm), alpha);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = lane + 32 * j;
+          if (t > i && t < w) xs = fma(pv[j], pv[j], xs);
+        }
+        xs = warp_sum(xs);
+        double ai = pv[0];
+#pragma unroll
+        for (int j = 1; j < 4; ++j)
+          if (j == (i >> 5)) ai = pv[j];
+        const double alpha = __shfl_sync(0xffffffffu, ai, i & 31);
+        double tau = 0.0, beta = alpha, scal = 1.0;
+        if (xs != 0.0) {
+          // beta = -sign(alpha) ||(alpha, x)|| (dlarfg); entries are far from overflow
+          beta = -copysign(sqrt(fma(alpha, alpha, xs)), alpha);
           tau = (beta - alpha) / beta;
-          const double scal = 1.0 / (alpha - beta);
-          for (int t = i + 1 + lane; t < w; t += 32) col[t] *= scal;
+          scal = 1.0 / (alpha - beta);
         }
-        __syncwarp();
-        if (lane == 0) {
-          col[i] = beta;
-          s_tau = tau;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int t = lane + 32 * j;
+          if (t < w) {
+            ci[t] = t < i ? pv[j] : (t == i ? beta : pv[j] * scal);
+            if (pvt != i) cp[t] = cv[j];
+          }
         }
+        if (pvt != i) {
+          if (lane == 0) { const int tp = piv[pvt]; piv[pvt] = piv[i]; piv[i] = tp; }
+          if (lane == 1) vn1[pvt] = vn1[i];
+          if (lane == 2) vn2[pvt] = vn2[i];
+        }
+        if (lane == 0) s_tau = tau;
       }
+      ID_ACC(0, ta, tb);
       __syncthreads();
+      ID_ACC(1, tb, tc);
       const double tau = s_tau;
       const double* v = sA + i * SW;
       double mine = 0.0;   // downdated norms^2 of this thread's trailing candidates
@@ -588,10 +613,12 @@ __device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* 
         }
         mine = fma(vn1[c], vn1[c], mine);
       }
+      ID_ACC(2, tc, td);
       if (i + 1 >= mn) break;   // full factorisation: trailing mass 0
       mine = warp_sum(mine);
       if (lane == 0) red[8 + warp] = mine;
       __syncthreads();
+      ID_ACC(3, td, te);
       double proxy = 0.0;
       for (int t = 0; t < nwarps; ++t) proxy += red[8 + t];   // same order in every thread
       if (proxy <= 4.0 * cut || i + 1 == stop_at) {
@@ -659,8 +686,14 @@ __global__ void __launch_bounds__(256, 2) id_kernel(TreeDev T, int level, double
   __syncthreads();
   int steps;
   double trail;
+  ID_T0(t0);
+#ifdef HSSEIG_ID_TIMING
+  long long t1 = 0, t2 = 0;
+#endif
   const double nf = id_eliminate(sA, vn1, vn2, red, piv, p, w, SW, tol, w, steps, trail);
+  ID_ACC(5, t0, t1);
   id_finish(T, side, node, leaf, p, nf, steps, trail, tol, om, ldom, st, Mg, sA, tail, red, piv);
+  ID_ACC(6, t1, t2);
 }
 
 
@@ -956,7 +989,8 @@ extern "C" int hsseig_interp_decomp(const double* M, int64_t ldm, int64_t stride
                                     int32_t w, int64_t batch, double tol, int32_t max_rank,
                                     double* X, int64_t ldx, int64_t stride_x, int32_t* J,
                                     int32_t* rank, double* resid, int32_t* saturated, void* stream) {
-  if (p < 0 || w < 0 || batch < 0 || max_rank < 0 || ldm < w || ldx < max_rank) HSS_ARG_FAIL();
+  if (p < 0 || w < 0 || w > 128 || batch < 0 || max_rank < 0 || ldm < w || ldx < max_rank)
+    HSS_ARG_FAIL();
   if (batch == 0) return HSSEIG_OK;
   const int64_t smem = hsseig_interp_smem_bytes(p, w);
   if (smem > 227 * 1024 || !M || !X || !J || !rank || !resid || !saturated) HSS_ARG_FAIL();
@@ -966,3 +1000,16 @@ extern "C" int hsseig_interp_decomp(const double* M, int64_t ldm, int64_t stride
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
+
+#ifdef HSSEIG_ID_TIMING
+extern "C" int hsseig_debug_id_timing(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, hsseig::g_id_t, sizeof(unsigned long long) * 8) != cudaSuccess)
+    return HSSEIG_ERR_CUDA;
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(hsseig::g_id_t, z, sizeof(z));
+  }
+  return HSSEIG_OK;
+}
+#endif
+
