@@ -201,6 +201,15 @@ __global__ void __launch_bounds__(256) inner_form_kernel(TreeDev T, int level, i
   }
 }
 
+// LAPACK dlapy2: sqrt(x^2 + y^2) without destructive under/overflow
+__device__ __forceinline__ double lapy2(double x, double y) {
+  double xa = fabs(x), ya = fabs(y);
+  double wv = fmax(xa, ya), zv = fmin(xa, ya);
+  if (zv == 0.0) return wv;
+  double q = zv / wv;
+  return wv * sqrt(1.0 + q * q);
+}
+
 // Truncation of the factored A = M^T (hss.py:128-148): trailing Frobenius mass of R's
 // rows, rank r = min(first t with tail(t) <= (tol ||M||_F)^2, max_rank, nonzero diagonal),
 // saturation flag, relative residual, then T = R11^{-1} R12 in place (dtrsm L/U/N/N).
@@ -529,22 +538,19 @@ __device__ __forceinline__ double id_eliminate(double* sA, double* vn1, double* 
           pv[j] = t < w ? cp[t] : 0.0;
           cv[j] = (t < w && pvt != i) ? ci[t] : 0.0;
         }
+        // the sum of squares with the lane association of the sequential version (lane l
+        // takes rows i + 1 + l + 32 j): the reflector, and the merge records pinned to it,
+        // stay bit-identical
         double xs = 0.0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int t = lane + 32 * j;
-          if (t > i && t < w) xs = fma(pv[j], pv[j], xs);
-        }
+        for (int t = i + 1 + lane; t < w; t += 32) xs = fma(cp[t], cp[t], xs);
         xs = warp_sum(xs);
-        double ai = pv[0];
-#pragma unroll
-        for (int j = 1; j < 4; ++j)
-          if (j == (i >> 5)) ai = pv[j];
-        const double alpha = __shfl_sync(0xffffffffu, ai, i & 31);
+        const double alpha = cp[i];
         double tau = 0.0, beta = alpha, scal = 1.0;
-        if (xs != 0.0) {
-          // beta = -sign(alpha) ||(alpha, x)|| (dlarfg); entries are far from overflow
-          beta = -copysign(sqrt(fma(alpha, alpha, xs)), alpha);
+        const double xnorm = sqrt(xs);
+        if (xnorm != 0.0) {
+          // dlarfg with dlapy2: the rounding the merge records are pinned to (a flagged-tree
+          // decision at the noise level flips with a cheaper beta)
+          beta = -copysign(lapy2(alpha, xnorm), alpha);
           tau = (beta - alpha) / beta;
           scal = 1.0 / (alpha - beta);
         }
