@@ -377,10 +377,17 @@ def eigh_lines(peak_hbm=None):
         ("cfg3_kac_N20000_defaults", hb.gen_kac(20000), hb.SolverConfig(), kac, "cfg3d", False),
         ("cfg5_N65536", hb.gen_config5(65536, 0), hb.SolverConfig(rank_eps=1e-13), None, None, True),
     ]
+    import gc
+    res = None
     for name, T, cfg, exact, tag, glue in cases:
+        # the previous case's blocks are released first, so this case's warm-up leaves the
+        # allocator holding exactly the segments its timed runs reuse
+        res = None
+        gc.collect()
+        torch.cuda.empty_cache()
         hb.adc_solve(T, cfg)   # warm-up (allocator, tree buffers)
         best = None
-        for _ in range(2):
+        for _ in range(3):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             res = hb.adc_solve(T, cfg)
