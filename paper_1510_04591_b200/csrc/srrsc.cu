@@ -23,10 +23,14 @@
 // new maximum, and the CTAs' records meet through DSMEM after one cluster barrier.  The
 // search is division-free: an entry only reaches the exact IEEE value |s t / g| (and the
 // argmax compare) when |s| |t| / best + slack >= |e - c| (the gap with the rounding of its
-// folded form covered by the slack), so per entry the sweep costs one DADD, one DFMA and
-// one compare.
-// Cost: sum over nodes of |R| (k - |t|) rank entries, O(k^2 r) per merge, the complexity the
-// paper quotes for ADC1.
+// folded form covered by the slack).  The column points c are sorted, so that filter is
+// first applied to blocks of 32 columns (largest |t| and slack of the block, distance from
+// the row's point to the block's span): each row walks outwards from the block holding its
+// point and evaluates only the blocks that can pass -- the argmax, and so every pivot, is
+// the full sweep's (sr_sweep_blocks).
+// Cost: the column rescaling is O(k - |t|) per elimination step and the search O(|R| (log +
+// passing blocks)), against the sum over nodes of |R| (k - |t|) entries per step of a full
+// sweep (the O(k^2 r) per merge the paper quotes for ADC1).
 #include <algorithm>
 #include <climits>
 
@@ -39,7 +43,6 @@ namespace hsseig {
 namespace cg = cooperative_groups;
 
 constexpr int kSrThreads = 256;
-constexpr int kSrCols = 4;      // columns a thread holds in registers during a sweep
 constexpr int kSrMaxCluster = 16;
 
 // lam_a - lam_b for eigen indices a != b through the pole between them (both terms carry the
@@ -63,110 +66,223 @@ struct SweepPivot {          // previous pivot, for the deferred column rescalin
   double rx, ry, rz, rw;     // its row's points (sX, sY, sZ, sW)
 };
 
-// One sweep over columns [c_lo, c_hi) (all left (RIGHT = false) or all right of the node):
-// apply the previous pivot's rescaling to the column generators, then search the largest
-// |s t / g| with the division-free filter
-//     |s| |t| / best + slack >= |e - c|     (e - c the gap up to the folded rounding)
-// and the exact IEEE value and row-major argmax only for entries that pass it.
+// Block-pruned sweep: the same search with the filter applied to whole blocks of 32 columns
+// first.  The column points c are ascending in the column index (eigenvalues on side 0,
+// poles on side 1), so a block spans [cLo, cHi]; with T_B = max |t| and S_B = max slack over
+// the block, every column of it fails the per-entry filter for row a whenever
+//     fl(dist(e_a, [cLo, cHi])) > fma(|s_a|, fl(T_B * rthr), S_B)
+// (rounded products and fma are monotone, so the block bound dominates every column's left
+// side and the distance is a lower bound of every column's |e - c|).  Each row starts at the
+// block holding its point and walks outwards, stopping in each direction once even the
+// largest T of all blocks further out cannot pass (prefix / suffix maxima).  Only the
+// columns of the blocks that pass meet the per-entry filter and the exact value.  The
+// argmax is the maximum over all entries with the row-major tie-break, whatever the order
+// in which entries are evaluated: the result is the full sweep's.
+// Pass 1 (all threads over columns) applies the previous pivot's rescaling and forms the
+// block statistics in shared memory; pass 2 (a warp per row, lanes over a block's columns)
+// searches.
+constexpr int kSrBlk = 32;
+
 template <int SIDE, bool RIGHT>
-__device__ __forceinline__ void sr_sweep(const CauchyGen& g, int c_lo, int c_hi, int lo, int width,
-                                         int ncomp, int p, int step, const SweepPivot& pv,
-                                         double* __restrict__ tstate, const double* sS,
-                                         const double* sX, const double* sY, const double* sZ,
-                                         const double* sW, const double2* sE, double& bv,
-                                         long long& bk, double& bt) {
-  const int tid = threadIdx.x;
-  const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+__device__ __forceinline__ void sr_col_point(const CauchyGen& g, int b, double& cy, double& cz) {
+  if (SIDE == 0) {
+    cy = RIGHT ? __ldg(g.d + b) : __ldg(g.dnext + b);
+    cz = RIGHT ? __ldg(g.gam + b) : -__ldg(g.mu + b);
+  } else {
+    cy = __ldg(g.d + b);
+    cz = 0.0;
+  }
+}
+
+template <int SIDE, bool RIGHT>
+__device__ __forceinline__ void sr_sweep_blocks(const CauchyGen& g, int c_lo, int c_hi, int lo,
+                                                int width, int ncomp, int p, int step,
+                                                const SweepPivot& pv, double* __restrict__ tstate,
+                                                const double* sS, const double* sX,
+                                                const double* sY, const double* sZ,
+                                                const double* sW, const double2* sE,
+                                                double* bstat, double& bv, long long& bk,
+                                                double& bt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  for (int c0 = c_lo; c0 < c_hi; c0 += kSrThreads * kSrCols) {
-    double tv[kSrCols], ce[kSrCols], cs[kSrCols], tb[kSrCols];
-#pragma unroll
-    for (int u = 0; u < kSrCols; ++u) {
-      const int c = c0 + u * kSrThreads + tid;
-      double t = 0.0;
-      double cy = kNaN, cz = kNaN;   // invalid column: NaN gaps never pass a compare
-      if (c < c_hi) {
-        const int b = c < lo ? c : c + width;
-        if (SIDE == 0) {     // columns are eigen indices
-          const double db = __ldg(g.d + b), gb = __ldg(g.gam + b);
-          const double nb = __ldg(g.dnext + b), mb = __ldg(g.mu + b);
-          cy = RIGHT ? db : nb;
-          cz = RIGHT ? gb : -mb;       // g = (x - cy) - cz  ==  (x - dnext) + mu on the left
-          if (step == 0) {
-            t = __ldg(g.v + b);
-          } else if (b == pv.gb) {
-            t = 0.0;
-          } else {
-            const double gp = (pv.rx - cy) - cz;
-            const double cf = lamdiff(pv.gb, b, pv.d, pv.g, pv.n, pv.m, db, gb, nb, mb) / gp;
-            t = tstate[c] * cf;
-          }
-        } else {             // columns are poles
-          const double db = __ldg(g.d + b);
-          cy = db;
-          if (step == 0) {
-            t = __ldg(g.zhat + b);
-          } else if (b == pv.gb) {
-            t = 0.0;
-          } else {
-            const double gp = RIGHT ? ((db - pv.rz) - pv.rw) : ((db - pv.rx) - pv.ry);
-            const double cf = (db - pv.d) / gp;
-            t = tstate[c] * cf;
-          }
-        }
-        tstate[c] = t;
-      }
-      tv[u] = t;
+  const int n = c_hi - c_lo;
+  if (n <= 0) return;   // uniform: every thread has the same range
+  const int nb = (n + kSrBlk - 1) / kSrBlk;
+  double* bLo = bstat;
+  double* bHi = bLo + nb;
+  double* bT = bHi + nb;
+  double* bS = bT + nb;
+  double* bPre = bS + nb;   // max T over blocks [0, b]
+  double* bSuf = bPre + nb; // max T over blocks [b, nb)
+  // ---- pass 1: rescale every column generator, block statistics (a warp = a block) ----
+  for (int c0 = c_lo + warp * kSrBlk; c0 < c_hi; c0 += kSrThreads) {
+    const int c = c0 + lane;
+    double t = 0.0, ce = 0.0, cs = 0.0;
+    const bool valid = c < c_hi;
+    if (valid) {
+      const int b = c < lo ? c : c + width;
       if (SIDE == 0) {
-        ce[u] = cy + cz;
-        cs[u] = 0x1p-50 * (fabs(cy) + fabs(cz));
-      } else {
-        ce[u] = cy;
-        cs[u] = 0.0;
-      }
-    }
-    double rthr = bv > 0.0 ? 1.0 / (bv * (1.0 - 1e-9)) : kInf;
-#pragma unroll
-    for (int u = 0; u < kSrCols; ++u) tb[u] = fabs(tv[u]) * rthr;
-    // two rows per iteration (independent filter chains); p is padded by a zero row
-    // (s = 0 never passes) when odd, see the row setup
-    for (int a0 = 0; a0 < p; a0 += 2) {
-      const double as0 = fabs(sS[a0]), as1 = fabs(sS[a0 + 1]);
-      const double2 e0 = sE[a0], e1 = sE[a0 + 1];  // (folded point, slack) for this branch
-      unsigned hm = 0;   // bit u: (row a0, column u) passes; bit kSrCols + u: row a0 + 1
-#pragma unroll
-      for (int u = 0; u < kSrCols; ++u) {
-        hm |= (fma(as0, tb[u], SIDE == 0 ? cs[u] : e0.y) >= fabs(ce[u] - e0.x)) ? 1u << u : 0u;
-        hm |= (fma(as1, tb[u], SIDE == 0 ? cs[u] : e1.y) >= fabs(ce[u] - e1.x))
-                  ? 1u << (kSrCols + u) : 0u;
-      }
-      if (!hm) continue;
-      for (int a = a0; a < a0 + 2; ++a, hm >>= kSrCols) {   // rare: exact values, argmax
-        const double sa = sS[a];
-        if (sa == 0.0) continue;
-#pragma unroll
-        for (int u = 0; u < kSrCols; ++u) {
-          const int c = c0 + u * kSrThreads + tid;
-          if (!((hm >> u) & 1u) || c >= c_hi) continue;
-          const int b = c < lo ? c : c + width;   // exact gap from the column's points again
-          double gv;
-          if (SIDE == 0) {
-            gv = RIGHT ? ((sX[a] - __ldg(g.d + b)) - __ldg(g.gam + b))
-                       : ((sX[a] - __ldg(g.dnext + b)) - (-__ldg(g.mu + b)));
-          } else {
-            const double db = __ldg(g.d + b);
-            gv = RIGHT ? ((db - sZ[a]) - sW[a]) : ((db - sX[a]) - sY[a]);
-          }
-          const double val = fabs((sa * tv[u]) / gv);
-          const long long key = (long long)a * ncomp + c;
-          if (better(val, key, bv, bk)) { bv = val; bk = key; bt = tv[u]; }
+        const double db = __ldg(g.d + b), gb = __ldg(g.gam + b);
+        const double nb2 = __ldg(g.dnext + b), mb = __ldg(g.mu + b);
+        const double cy = RIGHT ? db : nb2, cz = RIGHT ? gb : -mb;
+        if (step == 0) {
+          t = __ldg(g.v + b);
+        } else if (b == pv.gb) {
+          t = 0.0;
+        } else {
+          const double gp = (pv.rx - cy) - cz;
+          const double cf = lamdiff(pv.gb, b, pv.d, pv.g, pv.n, pv.m, db, gb, nb2, mb) / gp;
+          t = tstate[c] * cf;
         }
+        ce = cy + cz;
+        cs = 0x1p-50 * (fabs(cy) + fabs(cz));
+      } else {
+        const double db = __ldg(g.d + b);
+        if (step == 0) {
+          t = __ldg(g.zhat + b);
+        } else if (b == pv.gb) {
+          t = 0.0;
+        } else {
+          const double gp = RIGHT ? ((db - pv.rz) - pv.rw) : ((db - pv.rx) - pv.ry);
+          const double cf = (db - pv.d) / gp;
+          t = tstate[c] * cf;
+        }
+        ce = db;
       }
-      rthr = bv > 0.0 ? 1.0 / (bv * (1.0 - 1e-9)) : rthr;
+      tstate[c] = t;
+    }
+    double tm = valid ? fabs(t) : 0.0, sm2 = valid ? cs : 0.0;
 #pragma unroll
-      for (int u = 0; u < kSrCols; ++u) tb[u] = fabs(tv[u]) * rthr;
+    for (int o = 16; o > 0; o >>= 1) {
+      tm = fmax(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+      sm2 = fmax(sm2, __shfl_xor_sync(0xffffffffu, sm2, o));
+    }
+    const int last = min(31, c_hi - 1 - c0);
+    const double chi = __shfl_sync(0xffffffffu, ce, last);
+    if (lane == 0) {
+      const int blk = (c0 - c_lo) / kSrBlk;
+      bLo[blk] = ce;
+      bHi[blk] = chi;
+      bT[blk] = tm;
+      bS[blk] = sm2;
     }
   }
+  __syncthreads();
+  // prefix / suffix maxima of T (a warp per direction, 32 blocks per shuffle scan) and the
+  // largest column slack of the range (side 0)
+  __shared__ double s_smax;
+  if (warp == 2) {
+    double m = 0.0;
+    for (int b = lane; b < nb; b += 32) m = fmax(m, bS[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_smax = m;
+  }
+  if (warp < 2) {
+    double carry = 0.0;
+    for (int base = 0; base < nb; base += 32) {
+      const int b = warp == 0 ? base + lane : nb - 1 - (base + lane);
+      double v = (warp == 0 ? b < nb : b >= 0) ? bT[b] : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = fmax(v, u);
+      }
+      v = fmax(v, carry);
+      if (warp == 0 ? b < nb : b >= 0) (warp == 0 ? bPre : bSuf)[b] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  const double smax = s_smax;
+  // ---- pass 2: a warp per row; the 32 columns of a block that can pass are filtered and
+  // evaluated lane-parallel (coalesced loads).  Round A scans every row's two blocks nearest
+  // its point (where the largest entries |s t / g| sit) and the CTA agrees on the best value
+  // found -- a lower bound of the final maximum -- so that round B's walks outwards start
+  // with tight windows.  Every skip compares against a lower bound of the final maximum, so
+  // the argmax stays exact; lanes keep their own argmax records ----
+  __shared__ double s_wbest[kSrThreads / 32];
+  auto block_of = [&](double ex) {   // last block with bLo <= ex (or -1)
+    int lo_b = 0, hi_b = nb;
+    while (lo_b < hi_b) {
+      const int mid = (lo_b + hi_b) >> 1;
+      if (bLo[mid] <= ex) lo_b = mid + 1;
+      else hi_b = mid;
+    }
+    return lo_b - 1;
+  };
+  auto scan_block = [&](int a, double sa, double as, double2 e, int blk, double rthr) {
+    const int c = c_lo + blk * kSrBlk + lane;
+    if (c < c_hi) {
+      const double tc = tstate[c];
+      const int b = c < lo ? c : c + width;
+      double cy, cz;
+      sr_col_point<SIDE, RIGHT>(g, b, cy, cz);
+      const double ce = SIDE == 0 ? cy + cz : cy;
+      const double csl = SIDE == 0 ? 0x1p-50 * (fabs(cy) + fabs(cz)) : e.y;
+      if (fma(as, fabs(tc) * rthr, csl) >= fabs(ce - e.x)) {
+        double gv;
+        if (SIDE == 0) gv = (sX[a] - cy) - cz;   // (x - d_b) - gam_b | (x - dnext_b) + mu_b
+        else gv = RIGHT ? ((cy - sZ[a]) - sW[a]) : ((cy - sX[a]) - sY[a]);
+        const double val = fabs((sa * tc) / gv);
+        const long long key = (long long)a * ncomp + c;
+        if (better(val, key, bv, bk)) { bv = val; bk = key; bt = tc; }
+      }
+    }
+  };
+  auto warp_max = [&](double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+  };
+  // round A: the two blocks nearest each row's point, every entry evaluated exactly
+  for (int a = warp; a < p; a += kSrThreads / 32) {
+    const double sa = sS[a];
+    if (sa == 0.0) continue;   // uniform across the warp
+    const int bc = block_of(sE[a].x);
+    for (int blk = max(bc, 0); blk <= min(bc + 1, nb - 1); ++blk)
+      scan_block(a, sa, fabs(sa), sE[a], blk, kInf);
+  }
+  {
+    const double m = warp_max(bv);
+    if (lane == 0) s_wbest[warp] = m;
+  }
+  __syncthreads();
+  double bv0 = 0.0;
+  for (int w2 = 0; w2 < kSrThreads / 32; ++w2) bv0 = fmax(bv0, s_wbest[w2]);
+  // round B: walk outwards from the point, skipping the round-A blocks
+  for (int a = warp; a < p; a += kSrThreads / 32) {
+    const double sa = sS[a];
+    if (sa == 0.0) continue;
+    const double as = fabs(sa);
+    const double2 e = sE[a];
+    const double ex = e.x;
+    const double rslack = SIDE == 0 ? smax : e.y;
+    const int bc = block_of(ex);
+    double wbv = fmax(bv0, warp_max(bv));
+    double rthr = wbv > 0.0 ? 1.0 / (wbv * (1.0 - 1e-9)) : kInf;
+    auto visit = [&](int blk) {
+      scan_block(a, sa, as, e, blk, rthr);
+      const double m = warp_max(bv);
+      if (m > wbv) { wbv = m; rthr = 1.0 / (wbv * (1.0 - 1e-9)); }
+    };
+    for (int blk = max(bc, 0); blk < nb; ++blk) {   // blocks at and right of the point
+      const double dist = ex <= bLo[blk] ? bLo[blk] - ex : (ex <= bHi[blk] ? 0.0 : ex - bHi[blk]);
+      if (blk > bc && dist > fma(as, bSuf[blk] * rthr, rslack)) break;
+      if (blk <= bc + 1) continue;                  // scanned in round A
+      const double bsl = SIDE == 0 ? bS[blk] : rslack;
+      if (dist > fma(as, bT[blk] * rthr, bsl)) continue;
+      visit(blk);
+    }
+    for (int blk = bc - 1; blk >= 0; --blk) {        // blocks left of the point
+      const double dist = ex - bHi[blk];
+      if (dist > fma(as, bPre[blk] * rthr, rslack)) break;
+      const double bsl = SIDE == 0 ? bS[blk] : rslack;
+      if (dist > fma(as, bT[blk] * rthr, bsl)) continue;
+      visit(blk);
+    }
+  }
+  __syncthreads();   // the block statistics are rewritten by the next range / step
 }
 
 // One thread-block cluster of CL CTAs per (node, side): every CTA keeps the candidate rows
@@ -212,6 +328,9 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
   int* sG = reinterpret_cast<int*>(sER + P);  // global index of the candidate
   int* sPos = sG + P;                         // elimination step that pivoted it, or -1
   int* sPiv = sPos + P;                       // candidate pivoted at each step
+  // block statistics of the pruned sweep (6 x (k / 32 + 1) doubles, 8-byte aligned)
+  double* bstat = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(sPiv + T.ws + 1) + 7) & ~(uintptr_t)7);
   __shared__ double sRedV[kSrThreads / 32], sRedT[kSrThreads / 32];
   __shared__ long long sRedK[kSrThreads / 32];
   __shared__ double sPartV[2], sPartT[2];     // this CTA's slice record, by step parity
@@ -284,11 +403,11 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
     {
       const int l0 = cbeg, l1 = min(cend, lo), r0 = max(cbeg, lo), r1 = cend;
       if (side == 0) {
-        sr_sweep<0, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bv, bk, bt);
-        sr_sweep<0, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bv, bk, bt);
+        sr_sweep_blocks<0, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bstat, bv, bk, bt);
+        sr_sweep_blocks<0, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bstat, bv, bk, bt);
       } else {
-        sr_sweep<1, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bv, bk, bt);
-        sr_sweep<1, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bv, bk, bt);
+        sr_sweep_blocks<1, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bstat, bv, bk, bt);
+        sr_sweep_blocks<1, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bstat, bv, bk, bt);
       }
     }
     // ---- slice argmax (first maximum in row-major order), then across the cluster ----
@@ -469,7 +588,8 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
   g.d = gen->d; g.dnext = gen->dnext; g.gam = gen->gamma; g.mu = gen->mu; g.zhat = gen->zhat;
   g.v = gen->v; g.k = gen->k;
   TreeDev T = to_dev(tree);
-  const size_t smem = sizeof(double) * 9 * (size_t)T.pmax + sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1);
+  const size_t smem = sizeof(double) * 9 * (size_t)T.pmax + sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1) +
+                      8 + sizeof(double) * 6 * ((size_t)T.k / kSrBlk + 2);
   if (smem > 227 * 1024) HSS_ARG_FAIL();
   cudaFuncSetAttribute(srrsc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(srrsc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -1,0 +1,5 @@
+export PYTHONUNBUFFERED=1
+timeout 900 python -m pytest tests/test_gpu_srrsc.py -q -x -p no:cacheprovider > gpurun_out/round2_ag_t1.log 2>&1; echo "srrsc tests rc=$?"; grep -E "passed|failed|FAILED|Error|assert" gpurun_out/round2_ag_t1.log | head -10
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/round2_ag_tests.log 2>&1; echo "tests rc=$?"; grep -E "passed|failed|FAILED" gpurun_out/round2_ag_tests.log | head
+timeout 600 python tools/adc1_bench.py 2>&1 | tail -5
+timeout 300 python tools/srrsc_prof.py 5000 64 3 2>&1 | tail -3
