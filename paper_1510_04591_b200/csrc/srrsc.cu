@@ -27,7 +27,7 @@
 // first applied to blocks of 32 columns (largest |t| and slack of the block, distance from
 // the row's point to the block's span): each row walks outwards from the block holding its
 // point and evaluates only the blocks that can pass -- the argmax, and so every pivot, is
-// the full sweep's (sr_sweep_blocks).
+// the full sweep's (sr_sweep_blocks, used from kSrPruneMin columns off the node).
 // Cost: the column rescaling is O(k - |t|) per elimination step and the search O(|R| (log +
 // passing blocks)), against the sum over nodes of |R| (k - |t|) entries per step of a full
 // sweep (the O(k^2 r) per merge the paper quotes for ADC1).
@@ -44,6 +44,8 @@ namespace cg = cooperative_groups;
 
 constexpr int kSrThreads = 256;
 constexpr int kSrMaxCluster = 16;
+constexpr int kSrCols = 4;          // columns a thread holds in registers in the full sweep
+constexpr int kSrPruneMin = 12288;  // columns off the node from which the pruned search pays
 
 // lam_a - lam_b for eigen indices a != b through the pole between them (both terms carry the
 // sign of the result):  a < b: ((d_{a+1} - d_b) - gam_b) - mu_a;  a > b: mu_b - ((d_{b+1} - d_a) - gam_a)
@@ -65,6 +67,112 @@ struct SweepPivot {          // previous pivot, for the deferred column rescalin
   double d, g, n, m;         // column point data (side 0: d, gam, dnext, mu; side 1: d)
   double rx, ry, rz, rw;     // its row's points (sX, sY, sZ, sW)
 };
+
+// One sweep over columns [c_lo, c_hi) (all left (RIGHT = false) or all right of the node):
+// apply the previous pivot's rescaling to the column generators, then search the largest
+// |s t / g| with the division-free filter
+//     |s| |t| / best + slack >= |e - c|     (e - c the gap up to the folded rounding)
+// and the exact IEEE value and row-major argmax only for entries that pass it.
+template <int SIDE, bool RIGHT>
+__device__ __forceinline__ void sr_sweep(const CauchyGen& g, int c_lo, int c_hi, int lo, int width,
+                                         int ncomp, int p, int step, const SweepPivot& pv,
+                                         double* __restrict__ tstate, const double* sS,
+                                         const double* sX, const double* sY, const double* sZ,
+                                         const double* sW, const double2* sE, double& bv,
+                                         long long& bk, double& bt) {
+  const int tid = threadIdx.x;
+  const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  for (int c0 = c_lo; c0 < c_hi; c0 += kSrThreads * kSrCols) {
+    double tv[kSrCols], ce[kSrCols], cs[kSrCols], tb[kSrCols];
+#pragma unroll
+    for (int u = 0; u < kSrCols; ++u) {
+      const int c = c0 + u * kSrThreads + tid;
+      double t = 0.0;
+      double cy = kNaN, cz = kNaN;   // invalid column: NaN gaps never pass a compare
+      if (c < c_hi) {
+        const int b = c < lo ? c : c + width;
+        if (SIDE == 0) {     // columns are eigen indices
+          const double db = __ldg(g.d + b), gb = __ldg(g.gam + b);
+          const double nb = __ldg(g.dnext + b), mb = __ldg(g.mu + b);
+          cy = RIGHT ? db : nb;
+          cz = RIGHT ? gb : -mb;       // g = (x - cy) - cz  ==  (x - dnext) + mu on the left
+          if (step == 0) {
+            t = __ldg(g.v + b);
+          } else if (b == pv.gb) {
+            t = 0.0;
+          } else {
+            const double gp = (pv.rx - cy) - cz;
+            const double cf = lamdiff(pv.gb, b, pv.d, pv.g, pv.n, pv.m, db, gb, nb, mb) / gp;
+            t = tstate[c] * cf;
+          }
+        } else {             // columns are poles
+          const double db = __ldg(g.d + b);
+          cy = db;
+          if (step == 0) {
+            t = __ldg(g.zhat + b);
+          } else if (b == pv.gb) {
+            t = 0.0;
+          } else {
+            const double gp = RIGHT ? ((db - pv.rz) - pv.rw) : ((db - pv.rx) - pv.ry);
+            const double cf = (db - pv.d) / gp;
+            t = tstate[c] * cf;
+          }
+        }
+        tstate[c] = t;
+      }
+      tv[u] = t;
+      if (SIDE == 0) {
+        ce[u] = cy + cz;
+        cs[u] = 0x1p-50 * (fabs(cy) + fabs(cz));
+      } else {
+        ce[u] = cy;
+        cs[u] = 0.0;
+      }
+    }
+    double rthr = bv > 0.0 ? 1.0 / (bv * (1.0 - 1e-9)) : kInf;
+#pragma unroll
+    for (int u = 0; u < kSrCols; ++u) tb[u] = fabs(tv[u]) * rthr;
+    // two rows per iteration (independent filter chains); p is padded by a zero row
+    // (s = 0 never passes) when odd, see the row setup
+    for (int a0 = 0; a0 < p; a0 += 2) {
+      const double as0 = fabs(sS[a0]), as1 = fabs(sS[a0 + 1]);
+      const double2 e0 = sE[a0], e1 = sE[a0 + 1];  // (folded point, slack) for this branch
+      unsigned hm = 0;   // bit u: (row a0, column u) passes; bit kSrCols + u: row a0 + 1
+#pragma unroll
+      for (int u = 0; u < kSrCols; ++u) {
+        hm |= (fma(as0, tb[u], SIDE == 0 ? cs[u] : e0.y) >= fabs(ce[u] - e0.x)) ? 1u << u : 0u;
+        hm |= (fma(as1, tb[u], SIDE == 0 ? cs[u] : e1.y) >= fabs(ce[u] - e1.x))
+                  ? 1u << (kSrCols + u) : 0u;
+      }
+      if (!hm) continue;
+      for (int a = a0; a < a0 + 2; ++a, hm >>= kSrCols) {   // rare: exact values, argmax
+        const double sa = sS[a];
+        if (sa == 0.0) continue;
+#pragma unroll
+        for (int u = 0; u < kSrCols; ++u) {
+          const int c = c0 + u * kSrThreads + tid;
+          if (!((hm >> u) & 1u) || c >= c_hi) continue;
+          const int b = c < lo ? c : c + width;   // exact gap from the column's points again
+          double gv;
+          if (SIDE == 0) {
+            gv = RIGHT ? ((sX[a] - __ldg(g.d + b)) - __ldg(g.gam + b))
+                       : ((sX[a] - __ldg(g.dnext + b)) - (-__ldg(g.mu + b)));
+          } else {
+            const double db = __ldg(g.d + b);
+            gv = RIGHT ? ((db - sZ[a]) - sW[a]) : ((db - sX[a]) - sY[a]);
+          }
+          const double val = fabs((sa * tv[u]) / gv);
+          const long long key = (long long)a * ncomp + c;
+          if (better(val, key, bv, bk)) { bv = val; bk = key; bt = tv[u]; }
+        }
+      }
+      rthr = bv > 0.0 ? 1.0 / (bv * (1.0 - 1e-9)) : rthr;
+#pragma unroll
+      for (int u = 0; u < kSrCols; ++u) tb[u] = fabs(tv[u]) * rthr;
+    }
+  }
+}
 
 // Block-pruned sweep: the same search with the filter applied to whole blocks of 32 columns
 // first.  The column points c are ascending in the column index (eigenvalues on side 0,
@@ -290,6 +398,7 @@ __device__ __forceinline__ void sr_sweep_blocks(const CauchyGen& g, int c_lo, in
 // elimination step each CTA publishes its slice's (max, key, t at the max) in shared memory
 // (double-buffered by step parity), one cluster barrier, and every CTA reads the CL records
 // through DSMEM and takes the same decision.
+template <bool PRUNED>
 __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev T, int level,
                                                            int j0, double tol, int cap,
                                                            double* __restrict__ work, int64_t ldw,
@@ -402,12 +511,23 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
     long long bk = LLONG_MAX;
     {
       const int l0 = cbeg, l1 = min(cend, lo), r0 = max(cbeg, lo), r1 = cend;
-      if (side == 0) {
-        sr_sweep_blocks<0, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bstat, bv, bk, bt);
-        sr_sweep_blocks<0, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bstat, bv, bk, bt);
+      // the pruned search pays where the rows' point scans are long (config 4: k - |t| ~ 32k
+      // columns); below that the full sweep's streaming filter is faster (config 2).  Two
+      // instantiations, so each keeps its own register budget.
+      if constexpr (PRUNED) {
+        if (side == 0) {
+          sr_sweep_blocks<0, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bstat, bv, bk, bt);
+          sr_sweep_blocks<0, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bstat, bv, bk, bt);
+        } else {
+          sr_sweep_blocks<1, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bstat, bv, bk, bt);
+          sr_sweep_blocks<1, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bstat, bv, bk, bt);
+        }
+      } else if (side == 0) {
+        sr_sweep<0, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bv, bk, bt);
+        sr_sweep<0, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bv, bk, bt);
       } else {
-        sr_sweep_blocks<1, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bstat, bv, bk, bt);
-        sr_sweep_blocks<1, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bstat, bv, bk, bt);
+        sr_sweep<1, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bv, bk, bt);
+        sr_sweep<1, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bv, bk, bt);
       }
     }
     // ---- slice argmax (first maximum in row-major order), then across the cluster ----
@@ -589,14 +709,19 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
   g.v = gen->v; g.k = gen->k;
   TreeDev T = to_dev(tree);
   const size_t smem = sizeof(double) * 9 * (size_t)T.pmax + sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1) +
-                      8 + sizeof(double) * 6 * ((size_t)T.k / kSrBlk + 2);
+                      8 + (T.k >= kSrPruneMin ? sizeof(double) * 6 * ((size_t)T.k / kSrBlk + 2) : 0);
   if (smem > 227 * 1024) HSS_ARG_FAIL();
-  cudaFuncSetAttribute(srrsc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(srrsc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  // pruned search when every node of the tree leaves at least kSrPruneMin columns off it
+  const bool pruned = (int64_t)T.k - (T.k >> 1) - 8 >= kSrPruneMin;
+  const auto kern = pruned ? srrsc_kernel<true> : srrsc_kernel<false>;
+  const size_t smem_k = pruned ? smem : sizeof(double) * 9 * (size_t)T.pmax +
+                                           sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1) + 8;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const int64_t ldw = srrsc_ldw(tree);
   // resident CTAs of the whole GPU: a level is sized to fill them in one wave
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srrsc_kernel, kSrThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSrThreads, smem_k);
   const int slots = std::max(1, per_sm) * sm_count();
   for (int lev = lev_from; lev >= lev_to && lev >= 1; --lev) {
     const int npos = 1 << lev;
@@ -612,7 +737,7 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(cnt * cl, 2);
     lc.blockDim = dim3(kSrThreads);
-    lc.dynamicSmemBytes = smem;
+    lc.dynamicSmemBytes = smem_k;
     lc.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -622,7 +747,7 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
     lc.attrs = at;
     lc.numAttrs = 1;
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (cudaLaunchKernelEx(&lc, srrsc_kernel, g, T, lev, j0, tol, (int)max_rank, work, ldw, st) !=
+    if (cudaLaunchKernelEx(&lc, kern, g, T, lev, j0, tol, (int)max_rank, work, ldw, st) !=
         cudaSuccess)
       return HSSEIG_ERR_CUDA;
   }

@@ -7,6 +7,8 @@ post-deflation rank-one system whose eigenvector block already sits on the GPU.
 """
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 import torch
 
@@ -214,7 +216,7 @@ def _side_streams(n):
     return _SIDE[:n]
 
 
-def update_vectors_hss_many(jobs, cfg, max_streams=8):
+def update_vectors_hss_many(jobs, cfg, max_streams=None):
     """update_vectors_hss (dc.py:141-171) for every HSS merge of one recursion level.
 
     Phase by phase, so the level pays a handful of host waits instead of ~9 per merge
@@ -224,6 +226,8 @@ def update_vectors_hss_many(jobs, cfg, max_streams=8):
     merges overlap on the GPU.  Per job the operations and their inputs are exactly those
     of update_vectors_hss.  The caller's stream waits for all of it before returning.
     """
+    if max_streams is None:
+        max_streams = int(os.environ.get("HSSEIG_HSS_STREAMS", "8"))
     main = torch.cuda.current_stream()
 
     def dense_fallback(j):
