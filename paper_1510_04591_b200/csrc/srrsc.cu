@@ -708,14 +708,15 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
   g.d = gen->d; g.dnext = gen->dnext; g.gam = gen->gamma; g.mu = gen->mu; g.zhat = gen->zhat;
   g.v = gen->v; g.k = gen->k;
   TreeDev T = to_dev(tree);
-  const size_t smem = sizeof(double) * 9 * (size_t)T.pmax + sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1) +
-                      8 + (T.k >= kSrPruneMin ? sizeof(double) * 6 * ((size_t)T.k / kSrBlk + 2) : 0);
-  if (smem > 227 * 1024) HSS_ARG_FAIL();
-  // pruned search when every node of the tree leaves at least kSrPruneMin columns off it
-  const bool pruned = (int64_t)T.k - (T.k >> 1) - 8 >= kSrPruneMin;
+  // pruned search when every node of the tree leaves at least kSrPruneMin columns off it;
+  // HSSEIG_SRRSC_PRUNE=0/1 forces either search (tests compare the two bit for bit)
+  const char* pe = getenv("HSSEIG_SRRSC_PRUNE");
+  const bool pruned = pe && pe[0] ? pe[0] == '1' : (int64_t)T.k - (T.k >> 1) - 8 >= kSrPruneMin;
   const auto kern = pruned ? srrsc_kernel<true> : srrsc_kernel<false>;
-  const size_t smem_k = pruned ? smem : sizeof(double) * 9 * (size_t)T.pmax +
-                                           sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1) + 8;
+  const size_t smem_k = sizeof(double) * 9 * (size_t)T.pmax +
+                        sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1) + 8 +
+                        (pruned ? sizeof(double) * 6 * ((size_t)T.k / kSrBlk + 2) : 0);
+  if (smem_k > 227 * 1024) HSS_ARG_FAIL();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k);
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   const int64_t ldw = srrsc_ldw(tree);

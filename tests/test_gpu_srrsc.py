@@ -42,9 +42,12 @@ def _system(kind, k, seed=0):
     return G, C
 
 
+@pytest.mark.parametrize("prune", ["0", "1"])
 @pytest.mark.parametrize("kind,k,leaf", [("config4", 1024, 64), ("config4", 2048, 128),
                                          ("toeplitz", 1536, 48)])
-def test_srrsc_tree_matches_definition(kind, k, leaf):
+def test_srrsc_tree_matches_definition(monkeypatch, kind, k, leaf, prune):
+    # prune = "1": the block-pruned search (used from 12k columns off a node) forced on
+    monkeypatch.setenv("HSSEIG_SRRSC_PRUNE", prune)
     G, C = _system(kind, k, seed=3)
     part = hb.build_partition(k, leaf, C.d, C.gamma, C.mu)
     ranges = orc.leaf_ranges(k, leaf, G.mu)
@@ -198,3 +201,31 @@ def test_adc1_toeplitz_closed_form_and_dense_dc():
     Qd = np_(dd.Q)
     s = np.sign((Qa * Qd).sum(axis=0))
     assert np.abs(Qa * s - Qd).max() <= 1e-10
+
+
+def test_srrsc_pruned_search_equals_full_sweep_at_size(monkeypatch):
+    # at a size where the pruned search is the default (k - |t| >= 12k columns): the tree is
+    # bit-identical to the full sweep's (every pivot, rank, basis, flag)
+    k = 24576
+    d, u, rho = config4_system(k, 4)
+    s = hb.RankOneSystem(d, u, rho)
+    sol = hb.solve_secular(s)
+    hb.recompute_weights(d, sol, u, rho=rho)
+    C = hb.CauchyEvecMatrix.from_secular(s, sol)
+    part = hb.build_partition(k, 128, C.d, C.gamma, C.mu)
+    cap = hb.srrsc_cap(part)
+    trees = []
+    for prune in ("0", "1"):
+        monkeypatch.setenv("HSSEIG_SRRSC_PRUNE", prune)
+        trees.append(hb.srrsc_hss_construct(C, part, cap, tol=1e-15))
+    A, B = trees
+    assert A.flagged == B.flagged and A.r_used == B.r_used
+    for na, nb in zip(A.nodes, B.nodes):
+        if na.index == A.root:
+            continue
+        np.testing.assert_array_equal(na.rows_sel, nb.rows_sel)
+        np.testing.assert_array_equal(na.cols_sel, nb.cols_sel)
+        np.testing.assert_array_equal(np_(na.U), np_(nb.U))
+        np.testing.assert_array_equal(np_(na.V), np_(nb.V))
+        np.testing.assert_array_equal(np_(na.B), np_(nb.B))
+
