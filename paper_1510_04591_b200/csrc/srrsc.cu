@@ -174,22 +174,52 @@ __device__ __forceinline__ void sr_sweep(const CauchyGen& g, int c_lo, int c_hi,
   }
 }
 
-// Block-pruned sweep: the same search with the filter applied to whole blocks of 32 columns
-// first.  The column points c are ascending in the column index (eigenvalues on side 0,
-// poles on side 1), so a block spans [cLo, cHi]; with T_B = max |t| and S_B = max slack over
-// the block, every column of it fails the per-entry filter for row a whenever
+// Block-pruned sweep with lazily rescaled column generators: the same search as sr_sweep,
+// with the filter applied to whole blocks of 32 columns first.  The column points c are
+// ascending in the column index (eigenvalues on side 0, poles on side 1), so a block spans
+// [cLo, cHi]; with T_B >= max |t| and S_B = max slack over the block, every column of it fails
+// the per-entry filter for row a whenever
 //     fl(dist(e_a, [cLo, cHi])) > fma(|s_a|, fl(T_B * rthr), S_B)
 // (rounded products and fma are monotone, so the block bound dominates every column's left
-// side and the distance is a lower bound of every column's |e - c|).  Each row starts at the
-// block holding its point and walks outwards, stopping in each direction once even the
-// largest T of all blocks further out cannot pass (prefix / suffix maxima).  Only the
-// columns of the blocks that pass meet the per-entry filter and the exact value.  The
-// argmax is the maximum over all entries with the row-major tie-break, whatever the order
-// in which entries are evaluated: the result is the full sweep's.
-// Pass 1 (all threads over columns) applies the previous pivot's rescaling and forms the
-// block statistics in shared memory; pass 2 (a warp per row, lanes over a block's columns)
-// searches.
+// side and the distance is a lower bound of every column's |e - c|).  Every row's point lies
+// beyond the node's side of the range (rows are candidates inside the node, columns outside
+// it), so rows walk outwards from the block next to the node, stopping once even the largest
+// T of all blocks further out cannot pass (prefix / suffix maxima).
+//
+// Lazy rescaling.  A block's generators are only brought up to date ("materialised": the
+// pending pivots' rescalings applied in step order, so every t is bit-identical to the eager
+// update) when the block can pass the filter for some row; otherwise only its bound T_B is
+// advanced by an upper bound of the step's factor over the block.  The factor of a column is
+// a Moebius function of its point (side 0: (lam_q - lam_b) / (d_p - lam_b); side 1:
+// (d_b - d_q) / (d_b - lam_p)), monotone on each side of its pole, so away from the pole its
+// largest modulus over the block sits at an end column (sr_block_factor, with margins for
+// rounding and for the two representations of an eigenvalue).  The argmax is the maximum over
+// all entries with the row-major tie-break, whatever the order in which entries are
+// evaluated: the result is the full sweep's.
 constexpr int kSrBlk = 32;
+
+// blocks of one CTA's two column ranges together (at most k / 32 + 2), rounded up
+__host__ __device__ __forceinline__ int sr_nblocks(int k) { return k / kSrBlk + 4; }
+
+// One CTA's share of a column range [c_lo, c_hi): the range's blocks of 32 columns are dealt
+// to the cluster's CTAs cyclically (block i of this CTA is the range's block i * cl + rank), so
+// every CTA holds blocks near the node, where the search does its work.
+struct SrRange {
+  int c_lo, c_hi, cl, rank;
+  __device__ __forceinline__ int col0(int i) const { return c_lo + (i * cl + rank) * kSrBlk; }
+  __device__ __forceinline__ int nblocks() const {
+    const int nt = (c_hi - c_lo + kSrBlk - 1) / kSrBlk;
+    return nt > rank ? (nt - rank + cl - 1) / cl : 0;
+  }
+};
+
+struct SrBlocks {       // one column range's blocks, kept over the elimination
+  double* lo;           // first / last column point of the block
+  double* hi;
+  double* T;            // >= max |t| over the block (exact when materialised)
+  double* S;            // largest rounding slack of the block's column points (side 0)
+  int* st;              // step the block's generators are materialised at
+};
 
 template <int SIDE, bool RIGHT>
 __device__ __forceinline__ void sr_col_point(const CauchyGen& g, int b, double& cy, double& cz) {
@@ -202,125 +232,175 @@ __device__ __forceinline__ void sr_col_point(const CauchyGen& g, int b, double& 
   }
 }
 
+template <int SIDE>
+__device__ __forceinline__ void sr_load_col(const CauchyGen& g, int b, double& db, double& gb,
+                                            double& nb, double& mb) {
+  db = __ldg(g.d + b);
+  if (SIDE == 0) {
+    gb = __ldg(g.gam + b); nb = __ldg(g.dnext + b); mb = __ldg(g.mu + b);
+  } else {
+    gb = nb = mb = 0.0;
+  }
+}
+
+// rescaling factor of column b for pivot pv (b != pv.gb) and the gap it divides by; the
+// operations of the eager update (sr_sweep), so the lazily applied chain is bit-identical
 template <int SIDE, bool RIGHT>
-__device__ __forceinline__ void sr_sweep_blocks(const CauchyGen& g, int c_lo, int c_hi, int lo,
-                                                int width, int ncomp, int p, int step,
-                                                const SweepPivot& pv, double* __restrict__ tstate,
-                                                const double* sS, const double* sX,
-                                                const double* sY, const double* sZ,
-                                                const double* sW, const double2* sE,
-                                                double* bstat, double& bv, long long& bk,
-                                                double& bt) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ __forceinline__ double sr_col_factor(int b, const SweepPivot& pv, double db, double gb,
+                                                double nb, double mb, double& gp) {
+  if (SIDE == 0) {
+    const double cy = RIGHT ? db : nb, cz = RIGHT ? gb : -mb;
+    gp = (pv.rx - cy) - cz;
+    return lamdiff(pv.gb, b, pv.d, pv.g, pv.n, pv.m, db, gb, nb, mb) / gp;
+  } else {
+    gp = RIGHT ? ((db - pv.rz) - pv.rw) : ((db - pv.rx) - pv.ry);
+    return (db - pv.d) / gp;
+  }
+}
+
+// Upper bound of |factor| over the columns of block blk for pivot pv, or +inf when the
+// factor's pole may lie in (or within a 2^-20 relative margin of) the block's span.  Both end
+// gaps of one sign and above the margin put the pole outside the span; the exact factor is
+// then monotone over the block and its modulus peaks at an end.  Computed factors carry a
+// relative error of a few ulps plus, on side 0, an absolute error of the numerator from the
+// other representation of an eigenvalue (d_b + gam_b vs dnext_b - mu_b, a few ulps of the
+// points): 2^-33 of the point scale over the smallest gap covers both with a wide margin.
+template <int SIDE, bool RIGHT>
+__device__ __forceinline__ double sr_block_factor(const CauchyGen& g, const SrRange& rg, int lo,
+                                                  int width, int blk, const SweepPivot& pv,
+                                                  double eLo, double eHi) {
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
-  const int n = c_hi - c_lo;
-  if (n <= 0) return;   // uniform: every thread has the same range
-  const int nb = (n + kSrBlk - 1) / kSrBlk;
-  double* bLo = bstat;
-  double* bHi = bLo + nb;
-  double* bT = bHi + nb;
-  double* bS = bT + nb;
-  double* bPre = bS + nb;   // max T over blocks [0, b]
-  double* bSuf = bPre + nb; // max T over blocks [b, nb)
-  // ---- pass 1: rescale every column generator, block statistics (a warp = a block) ----
-  for (int c0 = c_lo + warp * kSrBlk; c0 < c_hi; c0 += kSrThreads) {
-    const int c = c0 + lane;
-    double t = 0.0, ce = 0.0, cs = 0.0;
-    const bool valid = c < c_hi;
-    if (valid) {
-      const int b = c < lo ? c : c + width;
-      if (SIDE == 0) {
-        const double db = __ldg(g.d + b), gb = __ldg(g.gam + b);
-        const double nb2 = __ldg(g.dnext + b), mb = __ldg(g.mu + b);
-        const double cy = RIGHT ? db : nb2, cz = RIGHT ? gb : -mb;
-        if (step == 0) {
-          t = __ldg(g.v + b);
-        } else if (b == pv.gb) {
-          t = 0.0;
-        } else {
-          const double gp = (pv.rx - cy) - cz;
-          const double cf = lamdiff(pv.gb, b, pv.d, pv.g, pv.n, pv.m, db, gb, nb2, mb) / gp;
-          t = tstate[c] * cf;
-        }
-        ce = cy + cz;
-        cs = 0x1p-50 * (fabs(cy) + fabs(cz));
+  const int c0 = rg.col0(blk), c1 = min(rg.c_hi, c0 + kSrBlk) - 1;
+  const int b0 = c0 < lo ? c0 : c0 + width, b1 = c1 < lo ? c1 : c1 + width;
+  double db, gb, nb, mb, g0, g1;
+  sr_load_col<SIDE>(g, b0, db, gb, nb, mb);
+  const double f0 = sr_col_factor<SIDE, RIGHT>(b0, pv, db, gb, nb, mb, g0);
+  sr_load_col<SIDE>(g, b1, db, gb, nb, mb);
+  const double f1 = sr_col_factor<SIDE, RIGHT>(b1, pv, db, gb, nb, mb, g1);
+  const double scale = fabs(eLo) + fabs(eHi) + fabs(pv.rx) + fabs(pv.ry) + fabs(pv.rz) +
+                       fabs(pv.rw) + fabs(pv.d);
+  const double gmin = fmin(fabs(g0), fabs(g1));
+  if (!(g0 * g1 > 0.0) || !(gmin > 0x1p-20 * scale)) return kInf;
+  return (fmax(fabs(f0), fabs(f1)) + 0x1p-32 * scale / gmin) * (1.0 + 0x1p-40);
+}
+
+// Bring block blk's generators to `step` (a warp, lane = column): the pending pivots'
+// rescalings in step order, then the exact max |t| of the block.
+template <int SIDE, bool RIGHT>
+__device__ __forceinline__ void sr_materialise(const CauchyGen& g, const SrRange& rg, int lo,
+                                               int width, int blk, int step,
+                                               const SweepPivot* recs,
+                                               double* __restrict__ tstate, SrBlocks bs) {
+  const int lane = threadIdx.x & 31;
+  const int c = rg.col0(blk) + lane;
+  const int from = bs.st[blk];
+  double t = 0.0;
+  if (c < rg.c_hi) {
+    const int b = c < lo ? c : c + width;
+    double db, gb, nb, mb;
+    sr_load_col<SIDE>(g, b, db, gb, nb, mb);
+    t = tstate[c];
+    for (int s = from + 1; s <= step; ++s) {
+      const SweepPivot& pv = recs[s];
+      if (b == pv.gb) {
+        t = 0.0;
       } else {
-        const double db = __ldg(g.d + b);
-        if (step == 0) {
-          t = __ldg(g.zhat + b);
-        } else if (b == pv.gb) {
-          t = 0.0;
-        } else {
-          const double gp = RIGHT ? ((db - pv.rz) - pv.rw) : ((db - pv.rx) - pv.ry);
-          const double cf = (db - pv.d) / gp;
-          t = tstate[c] * cf;
-        }
-        ce = db;
+        double gp;
+        const double cf = sr_col_factor<SIDE, RIGHT>(b, pv, db, gb, nb, mb, gp);
+        t = t * cf;
       }
-      tstate[c] = t;
     }
-    double tm = valid ? fabs(t) : 0.0, sm2 = valid ? cs : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      tm = fmax(tm, __shfl_xor_sync(0xffffffffu, tm, o));
-      sm2 = fmax(sm2, __shfl_xor_sync(0xffffffffu, sm2, o));
-    }
-    const int last = min(31, c_hi - 1 - c0);
-    const double chi = __shfl_sync(0xffffffffu, ce, last);
-    if (lane == 0) {
-      const int blk = (c0 - c_lo) / kSrBlk;
-      bLo[blk] = ce;
-      bHi[blk] = chi;
-      bT[blk] = tm;
-      bS[blk] = sm2;
-    }
+    tstate[c] = t;
   }
-  __syncthreads();
-  // prefix / suffix maxima of T (a warp per direction, 32 blocks per shuffle scan) and the
-  // largest column slack of the range (side 0)
+  double tm = fabs(t);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tm = fmax(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+  if (lane == 0) {
+    bs.T[blk] = tm;
+    bs.st[blk] = step;
+  }
+}
+
+template <int SIDE, bool RIGHT>
+__device__ __forceinline__ void sr_sweep_lazy(const CauchyGen& g, const SrRange rg, int lo,
+                                              int width, int ncomp, int p, int step,
+                                              const SweepPivot* recs, double* __restrict__ tstate,
+                                              const double* sS, const double* sX,
+                                              const double* sY, const double* sZ,
+                                              const double* sW, const double2* sE, SrBlocks bs,
+                                              double* bPre, double* bSuf, int* mlist,
+                                              hsseig_status* st, double& bv, long long& bk,
+                                              double& bt) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = kSrThreads / 32;
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  const int c_hi = rg.c_hi;
+  const int nb = rg.nblocks();
+  if (nb <= 0) return;   // uniform: every thread has the same range
+  double* bLo = bs.lo;
+  double* bHi = bs.hi;
+  double* bT = bs.T;
+  double* bS = bs.S;
+  const int near = RIGHT ? 0 : nb - 1;   // the block next to the node
+  __shared__ int s_nm;
+  __shared__ double s_wbest[kWarps];
   __shared__ double s_smax;
-  if (warp == 2) {
-    double m = 0.0;
-    for (int b = lane; b < nb; b += 32) m = fmax(m, bS[b]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) s_smax = m;
-  }
-  if (warp < 2) {
-    double carry = 0.0;
-    for (int base = 0; base < nb; base += 32) {
-      const int b = warp == 0 ? base + lane : nb - 1 - (base + lane);
-      double v = (warp == 0 ? b < nb : b >= 0) ? bT[b] : 0.0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v = fmax(v, u);
+  if (step == 0) {
+    // ---- every block materialised with the initial generators; points, slack, T ----
+    for (int blk = warp; blk < nb; blk += kWarps) {
+      const int c0 = rg.col0(blk), c = c0 + lane;
+      double t = 0.0, ce = 0.0, cs = 0.0;
+      const bool valid = c < c_hi;
+      if (valid) {
+        const int b = c < lo ? c : c + width;
+        double db, gb, nb2, mb;
+        sr_load_col<SIDE>(g, b, db, gb, nb2, mb);
+        if (SIDE == 0) {
+          const double cy = RIGHT ? db : nb2, cz = RIGHT ? gb : -mb;
+          t = __ldg(g.v + b);
+          ce = cy + cz;
+          cs = 0x1p-50 * (fabs(cy) + fabs(cz));
+        } else {
+          t = __ldg(g.zhat + b);
+          ce = db;
+        }
+        tstate[c] = t;
       }
-      v = fmax(v, carry);
-      if (warp == 0 ? b < nb : b >= 0) (warp == 0 ? bPre : bSuf)[b] = v;
-      carry = __shfl_sync(0xffffffffu, v, 31);
+      double tm = valid ? fabs(t) : 0.0, sm2 = valid ? cs : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        tm = fmax(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+        sm2 = fmax(sm2, __shfl_xor_sync(0xffffffffu, sm2, o));
+      }
+      const int last = min(31, c_hi - 1 - c0);
+      const double chi = __shfl_sync(0xffffffffu, ce, last);
+      if (lane == 0) {
+        bLo[blk] = ce;
+        bHi[blk] = chi;
+        bT[blk] = tm;
+        bS[blk] = sm2;
+        bs.st[blk] = 0;
+      }
     }
+  } else {
+    // ---- bounds advanced by the previous pivot's factor; the block next to the node
+    // (every row's nearest, always searched) materialised ----
+    const SweepPivot& pv = recs[step];
+    for (int blk = tid; blk < nb; blk += kSrThreads) {
+      if (blk == near) continue;
+      const double f = sr_block_factor<SIDE, RIGHT>(g, rg, lo, width, blk, pv, bLo[blk],
+                                                    bHi[blk]);
+      bT[blk] = f == kInf ? kInf : (bT[blk] * f) * (1.0 + 0x1p-50);
+    }
+    if (warp == kWarps - 1)
+      sr_materialise<SIDE, RIGHT>(g, rg, lo, width, near, step, recs, tstate, bs);
   }
+  if (tid == 0) s_nm = 0;
   __syncthreads();
-  const double smax = s_smax;
-  // ---- pass 2: a warp per row; the 32 columns of a block that can pass are filtered and
-  // evaluated lane-parallel (coalesced loads).  Round A scans every row's two blocks nearest
-  // its point (where the largest entries |s t / g| sit) and the CTA agrees on the best value
-  // found -- a lower bound of the final maximum -- so that round B's walks outwards start
-  // with tight windows.  Every skip compares against a lower bound of the final maximum, so
-  // the argmax stays exact; lanes keep their own argmax records ----
-  __shared__ double s_wbest[kSrThreads / 32];
-  auto block_of = [&](double ex) {   // last block with bLo <= ex (or -1)
-    int lo_b = 0, hi_b = nb;
-    while (lo_b < hi_b) {
-      const int mid = (lo_b + hi_b) >> 1;
-      if (bLo[mid] <= ex) lo_b = mid + 1;
-      else hi_b = mid;
-    }
-    return lo_b - 1;
-  };
   auto scan_block = [&](int a, double sa, double as, double2 e, int blk, double rthr) {
-    const int c = c_lo + blk * kSrBlk + lane;
+    const int c = rg.col0(blk) + lane;
+    if (lane == 0 && bs.st[blk] != step)   // never: only materialised blocks can pass
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st->v[7]), 1ull);
     if (c < c_hi) {
       const double tc = tstate[c];
       const int b = c < lo ? c : c + width;
@@ -343,13 +423,12 @@ __device__ __forceinline__ void sr_sweep_blocks(const CauchyGen& g, int c_lo, in
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
   };
-  // round A: the two blocks nearest each row's point, every entry evaluated exactly
-  for (int a = warp; a < p; a += kSrThreads / 32) {
+  // ---- round A: every row against the block next to the node, every entry exact; the CTA
+  // agrees on the best value found, a lower bound of the final maximum ----
+  for (int a = warp; a < p; a += kWarps) {
     const double sa = sS[a];
     if (sa == 0.0) continue;   // uniform across the warp
-    const int bc = block_of(sE[a].x);
-    for (int blk = max(bc, 0); blk <= min(bc + 1, nb - 1); ++blk)
-      scan_block(a, sa, fabs(sa), sE[a], blk, kInf);
+    scan_block(a, sa, fabs(sa), sE[a], near, kInf);
   }
   {
     const double m = warp_max(bv);
@@ -357,16 +436,74 @@ __device__ __forceinline__ void sr_sweep_blocks(const CauchyGen& g, int c_lo, in
   }
   __syncthreads();
   double bv0 = 0.0;
-  for (int w2 = 0; w2 < kSrThreads / 32; ++w2) bv0 = fmax(bv0, s_wbest[w2]);
-  // round B: walk outwards from the point, skipping the round-A blocks
-  for (int a = warp; a < p; a += kSrThreads / 32) {
+  for (int w2 = 0; w2 < kWarps; ++w2) bv0 = fmax(bv0, s_wbest[w2]);
+  if (step > 0) {
+    // ---- blocks that may pass for some row are materialised: the distance to the rows'
+    // nearest point, the largest |s| and slack of all rows and the threshold of round A's
+    // bound dominate every row's block test in round B (monotone rounding) ----
+    double rlo = kInf, rhi = -kInf, mas = 0.0, msl = 0.0;
+    for (int a = lane; a < p; a += 32) {
+      const double sa = sS[a];
+      if (sa == 0.0) continue;
+      const double2 e = sE[a];
+      rlo = fmin(rlo, e.x);
+      rhi = fmax(rhi, e.x);
+      mas = fmax(mas, fabs(sa));
+      msl = fmax(msl, e.y);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      rlo = fmin(rlo, __shfl_xor_sync(0xffffffffu, rlo, o));
+      rhi = fmax(rhi, __shfl_xor_sync(0xffffffffu, rhi, o));
+      mas = fmax(mas, __shfl_xor_sync(0xffffffffu, mas, o));
+      msl = fmax(msl, __shfl_xor_sync(0xffffffffu, msl, o));
+    }
+    const double rthr0 = bv0 > 0.0 ? 1.0 / (bv0 * (1.0 - 1e-9)) : kInf;
+    for (int blk = tid; blk < nb; blk += kSrThreads) {
+      if (bs.st[blk] == step) continue;
+      const double dist = RIGHT ? bLo[blk] - rhi : rlo - bHi[blk];
+      const double bsl = SIDE == 0 ? bS[blk] : msl;
+      if (!(dist > fma(mas, bT[blk] * rthr0, bsl))) mlist[atomicAdd(&s_nm, 1)] = blk;
+    }
+    __syncthreads();
+    const int nm = s_nm;
+    for (int i = warp; i < nm; i += kWarps)
+      sr_materialise<SIDE, RIGHT>(g, rg, lo, width, mlist[i], step, recs, tstate, bs);
+    __syncthreads();
+  }
+  // ---- prefix / suffix maxima of T (a warp per direction, 32 blocks per shuffle scan) and
+  // the largest column slack of the range (side 0) ----
+  if (warp == 2) {
+    double m = 0.0;
+    for (int b = lane; b < nb; b += 32) m = fmax(m, bS[b]);
+    m = warp_max(m);
+    if (lane == 0) s_smax = m;
+  }
+  if (warp < 2) {
+    double carry = 0.0;
+    for (int base = 0; base < nb; base += 32) {
+      const int b = warp == 0 ? base + lane : nb - 1 - (base + lane);
+      double v = (warp == 0 ? b < nb : b >= 0) ? bT[b] : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v = fmax(v, u);
+      }
+      v = fmax(v, carry);
+      if (warp == 0 ? b < nb : b >= 0) (warp == 0 ? bPre : bSuf)[b] = v;
+      carry = __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  __syncthreads();
+  const double smax = s_smax;
+  // ---- round B: a warp per row walks outwards from the node, skipping the near block ----
+  for (int a = warp; a < p; a += kWarps) {
     const double sa = sS[a];
     if (sa == 0.0) continue;
     const double as = fabs(sa);
     const double2 e = sE[a];
     const double ex = e.x;
     const double rslack = SIDE == 0 ? smax : e.y;
-    const int bc = block_of(ex);
     double wbv = fmax(bv0, warp_max(bv));
     double rthr = wbv > 0.0 ? 1.0 / (wbv * (1.0 - 1e-9)) : kInf;
     auto visit = [&](int blk) {
@@ -374,23 +511,33 @@ __device__ __forceinline__ void sr_sweep_blocks(const CauchyGen& g, int c_lo, in
       const double m = warp_max(bv);
       if (m > wbv) { wbv = m; rthr = 1.0 / (wbv * (1.0 - 1e-9)); }
     };
-    for (int blk = max(bc, 0); blk < nb; ++blk) {   // blocks at and right of the point
-      const double dist = ex <= bLo[blk] ? bLo[blk] - ex : (ex <= bHi[blk] ? 0.0 : ex - bHi[blk]);
-      if (blk > bc && dist > fma(as, bSuf[blk] * rthr, rslack)) break;
-      if (blk <= bc + 1) continue;                  // scanned in round A
-      const double bsl = SIDE == 0 ? bS[blk] : rslack;
-      if (dist > fma(as, bT[blk] * rthr, bsl)) continue;
-      visit(blk);
-    }
-    for (int blk = bc - 1; blk >= 0; --blk) {        // blocks left of the point
-      const double dist = ex - bHi[blk];
-      if (dist > fma(as, bPre[blk] * rthr, rslack)) break;
-      const double bsl = SIDE == 0 ? bS[blk] : rslack;
-      if (dist > fma(as, bT[blk] * rthr, bsl)) continue;
-      visit(blk);
+    // 32 blocks per iteration, a lane per block: the suffix (prefix) bound ends the walk at
+    // the first lane where it fails, the passing blocks before it are visited in order of
+    // distance (each visit may raise the best value, so later tests in the chunk are looser
+    // than necessary, never tighter: the argmax stays exact)
+    for (int base = RIGHT ? 1 : nb - 2; RIGHT ? base < nb : base >= 0;
+         base += RIGHT ? 32 : -32) {
+      const int blk = RIGHT ? base + lane : base - lane;
+      const bool in = RIGHT ? blk < nb : blk >= 0;
+      bool brk = true, pass = false;
+      if (in) {
+        const double dist = RIGHT ? bLo[blk] - ex : ex - bHi[blk];
+        brk = dist > fma(as, (RIGHT ? bSuf : bPre)[blk] * rthr, rslack);
+        const double bsl = SIDE == 0 ? bS[blk] : rslack;
+        pass = !brk && !(dist > fma(as, bT[blk] * rthr, bsl));
+      }
+      const unsigned bm = __ballot_sync(0xffffffffu, brk);
+      unsigned pm = __ballot_sync(0xffffffffu, pass);
+      if (bm) pm &= (1u << (__ffs(bm) - 1)) - 1u;
+      while (pm) {
+        const int i = __ffs(pm) - 1;
+        pm &= pm - 1;
+        visit(RIGHT ? base + i : base - i);
+      }
+      if (bm) break;
     }
   }
-  __syncthreads();   // the block statistics are rewritten by the next range / step
+  __syncthreads();   // the block statistics are read by the next range / step
 }
 
 // One thread-block cluster of CL CTAs per (node, side): every CTA keeps the candidate rows
@@ -399,7 +546,7 @@ __device__ __forceinline__ void sr_sweep_blocks(const CauchyGen& g, int c_lo, in
 // (double-buffered by step parity), one cluster barrier, and every CTA reads the CL records
 // through DSMEM and takes the same decision.
 template <bool PRUNED>
-__global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev T, int level,
+__global__ void __launch_bounds__(kSrThreads, PRUNED ? 2 : 0) srrsc_kernel(CauchyGen g, TreeDev T, int level,
                                                            int j0, double tol, int cap,
                                                            double* __restrict__ work, int64_t ldw,
                                                            hsseig_status* st) {
@@ -437,9 +584,20 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
   int* sG = reinterpret_cast<int*>(sER + P);  // global index of the candidate
   int* sPos = sG + P;                         // elimination step that pivoted it, or -1
   int* sPiv = sPos + P;                       // candidate pivoted at each step
-  // block statistics of the pruned sweep (6 x (k / 32 + 1) doubles, 8-byte aligned)
-  double* bstat = reinterpret_cast<double*>(
+  // pruned sweep: the pivots of every step (lazy rescaling) and the block state of the two
+  // column ranges (left blocks from 0, right blocks after them), 8-byte aligned
+  SweepPivot* recs = reinterpret_cast<SweepPivot*>(
       (reinterpret_cast<uintptr_t>(sPiv + T.ws + 1) + 7) & ~(uintptr_t)7);
+  const int NB = sr_nblocks(T.k);
+  double* bD = reinterpret_cast<double*>(recs + T.ws + 2);
+  int* bI = reinterpret_cast<int*>(bD + 6 * NB);
+  const SrRange rgL{0, lo, CL, rank}, rgR{lo, ncomp, CL, rank};
+  const int nbL = rgL.nblocks();
+  const SrBlocks bsL{bD, bD + NB, bD + 2 * NB, bD + 3 * NB, bI};
+  const SrBlocks bsR{bD + nbL, bD + NB + nbL, bD + 2 * NB + nbL, bD + 3 * NB + nbL, bI + nbL};
+  double* bPre = bD + 4 * NB;
+  double* bSuf = bD + 5 * NB;
+  int* mlist = bI + NB;
   __shared__ double sRedV[kSrThreads / 32], sRedT[kSrThreads / 32];
   __shared__ long long sRedK[kSrThreads / 32];
   __shared__ double sPartV[2], sPartT[2];     // this CTA's slice record, by step parity
@@ -516,11 +674,11 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
       // instantiations, so each keeps its own register budget.
       if constexpr (PRUNED) {
         if (side == 0) {
-          sr_sweep_blocks<0, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bstat, bv, bk, bt);
-          sr_sweep_blocks<0, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bstat, bv, bk, bt);
+          sr_sweep_lazy<0, false>(g, rgL, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sEL, bsL, bPre, bSuf, mlist, st, bv, bk, bt);
+          sr_sweep_lazy<0, true>(g, rgR, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sER, bsR, bPre, bSuf, mlist, st, bv, bk, bt);
         } else {
-          sr_sweep_blocks<1, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bstat, bv, bk, bt);
-          sr_sweep_blocks<1, true>(g, r0, r1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sER, bstat, bv, bk, bt);
+          sr_sweep_lazy<1, false>(g, rgL, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sEL, bsL, bPre, bSuf, mlist, st, bv, bk, bt);
+          sr_sweep_lazy<1, true>(g, rgR, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sER, bsR, bPre, bSuf, mlist, st, bv, bk, bt);
         }
       } else if (side == 0) {
         sr_sweep<0, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bv, bk, bt);
@@ -590,6 +748,12 @@ __global__ void __launch_bounds__(kSrThreads) srrsc_kernel(CauchyGen g, TreeDev 
         sTq = tq;
         sPv = (sS[ast] * tq) / gpv;
         sPiv[step] = ast;
+        if (PRUNED) {   // the pivot the next step's rescaling applies (lazy replay)
+          SweepPivot& rc = recs[step + 1];
+          rc.gb = gb; rc.past = ast;
+          rc.d = sPd; rc.g = sPg; rc.n = sPn; rc.m = sPm;
+          rc.rx = sX[ast]; rc.ry = sY[ast]; rc.rz = sZ[ast]; rc.rw = sW[ast];
+        }
       }
       }
     }
@@ -715,7 +879,9 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
   const auto kern = pruned ? srrsc_kernel<true> : srrsc_kernel<false>;
   const size_t smem_k = sizeof(double) * 9 * (size_t)T.pmax +
                         sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1) + 8 +
-                        (pruned ? sizeof(double) * 6 * ((size_t)T.k / kSrBlk + 2) : 0);
+                        (pruned ? sizeof(SweepPivot) * (T.ws + 2) + 8 +
+                                      (6 * sizeof(double) + 2 * sizeof(int)) * sr_nblocks(T.k)
+                                : 0);
   if (smem_k > 227 * 1024) HSS_ARG_FAIL();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k);
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -57,6 +57,7 @@ def test_srrsc_tree_matches_definition(monkeypatch, kind, k, leaf, prune):
     fo, fg = orc.Flops(), FlopCounter()
     ref = so.srrsc_construct(G, ranges, cap, 1e-15, fo)
     H = hb.srrsc_hss_construct(C, part, cap, tol=1e-15, flops=fg)
+    assert H._status.read()[7] == 0     # the lazy search only ever read materialised blocks
     assert H.flagged == ref.flagged
     assert fg.hss_construct == fo.hss_construct
     rres = np_(H._view("rres", torch.float64, H.ct.n_nodes, 0))
@@ -219,6 +220,7 @@ def test_srrsc_pruned_search_equals_full_sweep_at_size(monkeypatch):
         monkeypatch.setenv("HSSEIG_SRRSC_PRUNE", prune)
         trees.append(hb.srrsc_hss_construct(C, part, cap, tol=1e-15))
     A, B = trees
+    assert B._status.read()[7] == 0
     assert A.flagged == B.flagged and A.r_used == B.r_used
     for na, nb in zip(A.nodes, B.nodes):
         if na.index == A.root:
