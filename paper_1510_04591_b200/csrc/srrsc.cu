@@ -328,7 +328,7 @@ __device__ __forceinline__ void sr_sweep_lazy(const CauchyGen& g, const SrRange 
                                               const double* sS, const double* sX,
                                               const double* sY, const double* sZ,
                                               const double* sW, const double2* sE, SrBlocks bs,
-                                              double* bPre, double* bSuf, int* mlist,
+                                              int* mlist,
                                               hsseig_status* st, double& bv, long long& bk,
                                               double& bt) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -344,7 +344,6 @@ __device__ __forceinline__ void sr_sweep_lazy(const CauchyGen& g, const SrRange 
   const int near = RIGHT ? 0 : nb - 1;   // the block next to the node
   __shared__ int s_nm;
   __shared__ double s_wbest[kWarps];
-  __shared__ double s_smax;
   if (step == 0) {
     // ---- every block materialised with the initial generators; points, slack, T ----
     for (int blk = warp; blk < nb; blk += kWarps) {
@@ -397,25 +396,31 @@ __device__ __forceinline__ void sr_sweep_lazy(const CauchyGen& g, const SrRange 
   }
   if (tid == 0) s_nm = 0;
   __syncthreads();
-  auto scan_block = [&](int a, double sa, double as, double2 e, int blk, double rthr) {
-    const int c = rg.col0(blk) + lane;
-    if (lane == 0 && bs.st[blk] != step)   // never: only materialised blocks can pass
+  // A block's columns in a warp's registers (lane = column): generator t, point (cy, cz), the
+  // folded point ce and its slack; entry() is the per-entry filter and exact value of one row.
+  double tc = 0.0, cy = 0.0, cz = 0.0, ce = 0.0, csl = 0.0;
+  int cc = c_hi;
+  auto load_block = [&](int blk) {
+    if (lane == 0 && bs.st[blk] != step)   // never: only materialised blocks are searched
       atomicAdd(reinterpret_cast<unsigned long long*>(&st->v[7]), 1ull);
-    if (c < c_hi) {
-      const double tc = tstate[c];
-      const int b = c < lo ? c : c + width;
-      double cy, cz;
-      sr_col_point<SIDE, RIGHT>(g, b, cy, cz);
-      const double ce = SIDE == 0 ? cy + cz : cy;
-      const double csl = SIDE == 0 ? 0x1p-50 * (fabs(cy) + fabs(cz)) : e.y;
-      if (fma(as, fabs(tc) * rthr, csl) >= fabs(ce - e.x)) {
-        double gv;
-        if (SIDE == 0) gv = (sX[a] - cy) - cz;   // (x - d_b) - gam_b | (x - dnext_b) + mu_b
-        else gv = RIGHT ? ((cy - sZ[a]) - sW[a]) : ((cy - sX[a]) - sY[a]);
-        const double val = fabs((sa * tc) / gv);
-        const long long key = (long long)a * ncomp + c;
-        if (better(val, key, bv, bk)) { bv = val; bk = key; bt = tc; }
-      }
+    cc = rg.col0(blk) + lane;
+    if (cc < c_hi) {
+      tc = tstate[cc];
+      sr_col_point<SIDE, RIGHT>(g, cc < lo ? cc : cc + width, cy, cz);
+      ce = SIDE == 0 ? cy + cz : cy;
+      csl = SIDE == 0 ? 0x1p-50 * (fabs(cy) + fabs(cz)) : 0.0;
+    }
+  };
+  auto entry = [&](int a, double rthr) {
+    const double sa = sS[a];
+    const double2 e = sE[a];
+    if (cc < c_hi && fma(fabs(sa), fabs(tc) * rthr, SIDE == 0 ? csl : e.y) >= fabs(ce - e.x)) {
+      double gv;
+      if (SIDE == 0) gv = (sX[a] - cy) - cz;   // (x - d_b) - gam_b | (x - dnext_b) + mu_b
+      else gv = RIGHT ? ((cy - sZ[a]) - sW[a]) : ((cy - sX[a]) - sY[a]);
+      const double val = fabs((sa * tc) / gv);
+      const long long key = (long long)a * ncomp + cc;
+      if (better(val, key, bv, bk)) { bv = val; bk = key; bt = tc; }
     }
   };
   auto warp_max = [&](double v) {
@@ -423,13 +428,12 @@ __device__ __forceinline__ void sr_sweep_lazy(const CauchyGen& g, const SrRange 
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
   };
-  // ---- round A: every row against the block next to the node, every entry exact; the CTA
-  // agrees on the best value found, a lower bound of the final maximum ----
-  for (int a = warp; a < p; a += kWarps) {
-    const double sa = sS[a];
-    if (sa == 0.0) continue;   // uniform across the warp
-    scan_block(a, sa, fabs(sa), sE[a], near, kInf);
-  }
+  // ---- round A: the block next to the node against every row (rows dealt to the warps),
+  // every entry exact; the CTA agrees on the best value found, a lower bound of the final
+  // maximum ----
+  load_block(near);
+  for (int a = warp; a < p; a += kWarps)
+    if (sS[a] != 0.0) entry(a, kInf);
   {
     const double m = warp_max(bv);
     if (lane == 0) s_wbest[warp] = m;
@@ -437,10 +441,10 @@ __device__ __forceinline__ void sr_sweep_lazy(const CauchyGen& g, const SrRange 
   __syncthreads();
   double bv0 = 0.0;
   for (int w2 = 0; w2 < kWarps; ++w2) bv0 = fmax(bv0, s_wbest[w2]);
-  if (step > 0) {
-    // ---- blocks that may pass for some row are materialised: the distance to the rows'
-    // nearest point, the largest |s| and slack of all rows and the threshold of round A's
-    // bound dominate every row's block test in round B (monotone rounding) ----
+  // ---- candidate blocks: those that can pass for some row -- the distance to the rows'
+  // nearest point, the largest |s| and slack of all rows and round A's threshold dominate
+  // every row's block test (monotone rounding); candidates behind the step are materialised ----
+  {
     double rlo = kInf, rhi = -kInf, mas = 0.0, msl = 0.0;
     for (int a = lane; a < p; a += 32) {
       const double sa = sS[a];
@@ -460,81 +464,47 @@ __device__ __forceinline__ void sr_sweep_lazy(const CauchyGen& g, const SrRange 
     }
     const double rthr0 = bv0 > 0.0 ? 1.0 / (bv0 * (1.0 - 1e-9)) : kInf;
     for (int blk = tid; blk < nb; blk += kSrThreads) {
-      if (bs.st[blk] == step) continue;
+      if (blk == near) continue;
       const double dist = RIGHT ? bLo[blk] - rhi : rlo - bHi[blk];
       const double bsl = SIDE == 0 ? bS[blk] : msl;
       if (!(dist > fma(mas, bT[blk] * rthr0, bsl))) mlist[atomicAdd(&s_nm, 1)] = blk;
     }
-    __syncthreads();
-    const int nm = s_nm;
-    for (int i = warp; i < nm; i += kWarps)
-      sr_materialise<SIDE, RIGHT>(g, rg, lo, width, mlist[i], step, recs, tstate, bs);
-    __syncthreads();
-  }
-  // ---- prefix / suffix maxima of T (a warp per direction, 32 blocks per shuffle scan) and
-  // the largest column slack of the range (side 0) ----
-  if (warp == 2) {
-    double m = 0.0;
-    for (int b = lane; b < nb; b += 32) m = fmax(m, bS[b]);
-    m = warp_max(m);
-    if (lane == 0) s_smax = m;
-  }
-  if (warp < 2) {
-    double carry = 0.0;
-    for (int base = 0; base < nb; base += 32) {
-      const int b = warp == 0 ? base + lane : nb - 1 - (base + lane);
-      double v = (warp == 0 ? b < nb : b >= 0) ? bT[b] : 0.0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v = fmax(v, u);
-      }
-      v = fmax(v, carry);
-      if (warp == 0 ? b < nb : b >= 0) (warp == 0 ? bPre : bSuf)[b] = v;
-      carry = __shfl_sync(0xffffffffu, v, 31);
-    }
   }
   __syncthreads();
-  const double smax = s_smax;
-  // ---- round B: a warp per row walks outwards from the node, skipping the near block ----
-  for (int a = warp; a < p; a += kWarps) {
-    const double sa = sS[a];
-    if (sa == 0.0) continue;
-    const double as = fabs(sa);
-    const double2 e = sE[a];
-    const double ex = e.x;
-    const double rslack = SIDE == 0 ? smax : e.y;
-    double wbv = fmax(bv0, warp_max(bv));
-    double rthr = wbv > 0.0 ? 1.0 / (wbv * (1.0 - 1e-9)) : kInf;
-    auto visit = [&](int blk) {
-      scan_block(a, sa, as, e, blk, rthr);
-      const double m = warp_max(bv);
-      if (m > wbv) { wbv = m; rthr = 1.0 / (wbv * (1.0 - 1e-9)); }
-    };
-    // 32 blocks per iteration, a lane per block: the suffix (prefix) bound ends the walk at
-    // the first lane where it fails, the passing blocks before it are visited in order of
-    // distance (each visit may raise the best value, so later tests in the chunk are looser
-    // than necessary, never tighter: the argmax stays exact)
-    for (int base = RIGHT ? 1 : nb - 2; RIGHT ? base < nb : base >= 0;
-         base += RIGHT ? 32 : -32) {
-      const int blk = RIGHT ? base + lane : base - lane;
-      const bool in = RIGHT ? blk < nb : blk >= 0;
-      bool brk = true, pass = false;
-      if (in) {
-        const double dist = RIGHT ? bLo[blk] - ex : ex - bHi[blk];
-        brk = dist > fma(as, (RIGHT ? bSuf : bPre)[blk] * rthr, rslack);
-        const double bsl = SIDE == 0 ? bS[blk] : rslack;
-        pass = !brk && !(dist > fma(as, bT[blk] * rthr, bsl));
+  const int nm = s_nm;
+  if (step > 0) {
+    for (int i = warp; i < nm; i += kWarps)
+      if (bs.st[mlist[i]] != step)
+        sr_materialise<SIDE, RIGHT>(g, rg, lo, width, mlist[i], step, recs, tstate, bs);
+    __syncthreads();
+  }
+  // ---- round B: a warp per candidate block (its columns in registers); lanes over rows for
+  // the block test against the warp's best so far, lanes over columns for the entries of the
+  // rows that pass ----
+  double wbv = fmax(bv0, warp_max(bv));
+  for (int i = warp; i < nm; i += kWarps) {
+    const int blk = mlist[i];
+    load_block(blk);
+    const double bTb = bT[blk], bLb = bLo[blk], bHb = bHi[blk], bSb = SIDE == 0 ? bS[blk] : 0.0;
+    for (int a0 = 0; a0 < p; a0 += 32) {
+      const double rthr = wbv > 0.0 ? 1.0 / (wbv * (1.0 - 1e-9)) : kInf;
+      const int a = a0 + lane;
+      bool pass = false;
+      if (a < p) {
+        const double sa = sS[a];
+        if (sa != 0.0) {
+          const double2 e = sE[a];
+          const double dist = RIGHT ? bLb - e.x : e.x - bHb;
+          pass = !(dist > fma(fabs(sa), bTb * rthr, SIDE == 0 ? bSb : e.y));
+        }
       }
-      const unsigned bm = __ballot_sync(0xffffffffu, brk);
       unsigned pm = __ballot_sync(0xffffffffu, pass);
-      if (bm) pm &= (1u << (__ffs(bm) - 1)) - 1u;
       while (pm) {
-        const int i = __ffs(pm) - 1;
+        const int r = a0 + __ffs(pm) - 1;
         pm &= pm - 1;
-        visit(RIGHT ? base + i : base - i);
+        entry(r, rthr);
       }
-      if (bm) break;
+      wbv = fmax(wbv, warp_max(bv));
     }
   }
   __syncthreads();   // the block statistics are read by the next range / step
@@ -590,13 +560,11 @@ __global__ void __launch_bounds__(kSrThreads, PRUNED ? 2 : 0) srrsc_kernel(Cauch
       (reinterpret_cast<uintptr_t>(sPiv + T.ws + 1) + 7) & ~(uintptr_t)7);
   const int NB = sr_nblocks(T.k);
   double* bD = reinterpret_cast<double*>(recs + T.ws + 2);
-  int* bI = reinterpret_cast<int*>(bD + 6 * NB);
+  int* bI = reinterpret_cast<int*>(bD + 4 * NB);
   const SrRange rgL{0, lo, CL, rank}, rgR{lo, ncomp, CL, rank};
   const int nbL = rgL.nblocks();
   const SrBlocks bsL{bD, bD + NB, bD + 2 * NB, bD + 3 * NB, bI};
   const SrBlocks bsR{bD + nbL, bD + NB + nbL, bD + 2 * NB + nbL, bD + 3 * NB + nbL, bI + nbL};
-  double* bPre = bD + 4 * NB;
-  double* bSuf = bD + 5 * NB;
   int* mlist = bI + NB;
   __shared__ double sRedV[kSrThreads / 32], sRedT[kSrThreads / 32];
   __shared__ long long sRedK[kSrThreads / 32];
@@ -674,11 +642,11 @@ __global__ void __launch_bounds__(kSrThreads, PRUNED ? 2 : 0) srrsc_kernel(Cauch
       // instantiations, so each keeps its own register budget.
       if constexpr (PRUNED) {
         if (side == 0) {
-          sr_sweep_lazy<0, false>(g, rgL, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sEL, bsL, bPre, bSuf, mlist, st, bv, bk, bt);
-          sr_sweep_lazy<0, true>(g, rgR, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sER, bsR, bPre, bSuf, mlist, st, bv, bk, bt);
+          sr_sweep_lazy<0, false>(g, rgL, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sEL, bsL, mlist, st, bv, bk, bt);
+          sr_sweep_lazy<0, true>(g, rgR, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sER, bsR, mlist, st, bv, bk, bt);
         } else {
-          sr_sweep_lazy<1, false>(g, rgL, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sEL, bsL, bPre, bSuf, mlist, st, bv, bk, bt);
-          sr_sweep_lazy<1, true>(g, rgR, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sER, bsR, bPre, bSuf, mlist, st, bv, bk, bt);
+          sr_sweep_lazy<1, false>(g, rgL, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sEL, bsL, mlist, st, bv, bk, bt);
+          sr_sweep_lazy<1, true>(g, rgR, lo, width, ncomp, p, step, recs, tstate, sS, sX, sY, sZ, sW, sER, bsR, mlist, st, bv, bk, bt);
         }
       } else if (side == 0) {
         sr_sweep<0, false>(g, l0, l1, lo, width, ncomp, p, step, pv, tstate, sS, sX, sY, sZ, sW, sEL, bv, bk, bt);
@@ -880,7 +848,7 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
   const size_t smem_k = sizeof(double) * 9 * (size_t)T.pmax +
                         sizeof(int) * (2 * (size_t)T.pmax + T.ws + 1) + 8 +
                         (pruned ? sizeof(SweepPivot) * (T.ws + 2) + 8 +
-                                      (6 * sizeof(double) + 2 * sizeof(int)) * sr_nblocks(T.k)
+                                      (4 * sizeof(double) + 2 * sizeof(int)) * sr_nblocks(T.k)
                                 : 0);
   if (smem_k > 227 * 1024) HSS_ARG_FAIL();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_k);
