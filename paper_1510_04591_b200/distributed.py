@@ -648,7 +648,7 @@ class GpuOps:
 
     def local_solve(self, a, b, nodes, sub, cfg):
         from .solver import _plan, solve_subtree
-        a_mod, _ = _plan(a, b, cfg.base_size)
+        a_mod = nodes.split_diagonal(a, b)
         return solve_subtree(a_mod, b, nodes, sub, cfg)
 
     def deflate(self, nL, nR, L, zrow, bk):
@@ -718,18 +718,6 @@ def _group(ranks):
     if key not in _GROUPS:
         _GROUPS[key] = dist.new_group(list(ranks))
     return _GROUPS[key]
-
-
-def _split_a(a, b, nodes, max_depth):
-    """Diagonal with the split modifications of the recursion nodes above max_depth."""
-    a = a.copy()
-    for nd in nodes:
-        if not nd["leaf"] and nd["depth"] < max_depth:
-            m = nd["split"]
-            rho = abs(float(b[m - 1]))
-            a[m - 1] -= rho
-            a[m] -= rho
-    return a
 
 
 def _gather_padded(vec, length, group, device):

@@ -233,24 +233,80 @@ def adc_solve_recursive(T, cfg=None):
 # ----------------------------------------------------------------------------------------
 # Level-batched schedule: every merge of one recursion depth runs in one set of launches.
 # ----------------------------------------------------------------------------------------
+class _Tree:
+    """Recursion nodes (dc.py:194-203: split at n // 2, merge ids in postorder) as arrays in
+    postorder, built level by level with NumPy (a Python recursion over the 8191 nodes of
+    config 5 cost 12 ms of host time before the first launch).  A subtree is the contiguous
+    id range [i - size[i] + 1, i].  Indexing or iterating yields per-node dicts with the keys
+    lo, hi, depth, leaf and, for merges, left, right, split, mid."""
+
+    def __init__(self, n, base):
+        lo, hi = np.zeros(1, np.int64), np.full(1, n, np.int64)
+        levels = []
+        while len(lo):
+            inner = (hi - lo) > base
+            m = lo + (hi - lo) // 2
+            levels.append((lo, hi, inner, m))
+            li, hi_i, mi = lo[inner], hi[inner], m[inner]
+            lo = np.stack([li, mi], 1).reshape(-1)
+            hi = np.stack([mi, hi_i], 1).reshape(-1)
+        # subtree sizes bottom-up; the children of a level's j-th merge are nodes 2j, 2j+1 below
+        sizes = [None] * len(levels)
+        for d in range(len(levels) - 1, -1, -1):
+            inner = levels[d][2]
+            sz = np.ones(len(inner), np.int64)
+            if inner.any():
+                c = sizes[d + 1]
+                sz[inner] += c[0::2] + c[1::2]
+            sizes[d] = sz
+        total = int(sizes[0][0])
+        self.lo, self.hi, self.depth, self.split, self.left, self.right, self.size = (
+            np.zeros(total, np.int64) for _ in range(7))
+        self.leaf = np.ones(total, bool)
+        post = np.array([total - 1], np.int64)
+        for d, (lo, hi, inner, m) in enumerate(levels):
+            self.lo[post], self.hi[post], self.depth[post], self.size[post] = lo, hi, d, sizes[d]
+            if not inner.any():
+                break
+            pi = post[inner]
+            right = pi - 1
+            left = right - sizes[d + 1][1::2]
+            self.leaf[pi] = False
+            self.split[pi], self.left[pi], self.right[pi] = m[inner], left, right
+            post = np.stack([left, right], 1).reshape(-1)
+        self.mid = np.cumsum(~self.leaf) - 1
+
+    def __len__(self):
+        return len(self.lo)
+
+    def __getitem__(self, i):
+        i = int(i)
+        nd = {"lo": int(self.lo[i]), "hi": int(self.hi[i]), "depth": int(self.depth[i]),
+              "leaf": bool(self.leaf[i])}
+        if not nd["leaf"]:
+            nd.update(left=int(self.left[i]), right=int(self.right[i]), split=int(self.split[i]),
+                      mid=int(self.mid[i]))
+        return nd
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+    def split_diagonal(self, a, b, max_depth=None):
+        """The diagonal with the split modifications (dc.py:82-102) of every merge (above
+        max_depth): both corner diagonals drop by rho = |b[m-1]|.  Blocks hold >= 2 rows, so
+        no entry is touched by two splits and the update order is immaterial."""
+        a = np.array(a, dtype=np.float64)
+        sel = ~self.leaf if max_depth is None else (~self.leaf & (self.depth < max_depth))
+        m = self.split[sel]
+        rho = np.abs(b[m - 1])
+        a[m - 1] -= rho
+        a[m] -= rho
+        return a
+
+
 def _tree(n, base):
-    """Recursion nodes (dc.py:194-203): split at n // 2, merge ids in postorder."""
-    nodes = []
-    ids = itertools.count()
-
-    def rec(lo, hi, depth):
-        if hi - lo <= base:
-            nodes.append({"lo": lo, "hi": hi, "depth": depth, "leaf": True})
-            return len(nodes) - 1
-        m = lo + (hi - lo) // 2
-        left = rec(lo, m, depth + 1)
-        right = rec(m, hi, depth + 1)
-        nodes.append({"lo": lo, "hi": hi, "depth": depth, "leaf": False, "left": left,
-                      "right": right, "split": m, "mid": next(ids)})
-        return len(nodes) - 1
-
-    root = rec(0, n, 0)
-    return nodes, root
+    nodes = _Tree(n, base)
+    return nodes, len(nodes) - 1
 
 
 def _u64(ptrs):
@@ -282,14 +338,13 @@ def adc_solve(T, cfg=None):
     nat.require_cuda()
     a = np.asarray(T.a, dtype=np.float64)
     b = np.asarray(T.b, dtype=np.float64)
-    a_mod, _ = _plan(a, b, cfg.base_size)
     nodes, root = _tree(T.n, cfg.base_size)
+    a_mod = nodes.split_diagonal(a, b) if cfg.base_size >= 3 else _plan(a, b, cfg.base_size)[0]
     lam, Q, records = solve_subtree(a_mod, b, nodes, root, cfg)
     flops = FlopCounter()
     merges = [records[k] for k in sorted(records)]
-    for r in merges:
-        for p_ in FlopCounter.PHASES:
-            setattr(flops, p_, getattr(flops, p_) + r.flops.get(p_, 0))
+    for p_ in FlopCounter.PHASES:
+        setattr(flops, p_, getattr(flops, p_) + sum(r.flops.get(p_, 0) for r in merges))
     return EigenResult(lam=lam, Q=Q, merges=merges, flops=flops)
 
 
@@ -301,17 +356,13 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
     s = nat.stream_ptr()
     f64 = dict(dtype=torch.float64, device="cuda")
     # nodes are in postorder, so the subtree is the id range [leftmost leaf, sub]
-    first = sub
-    while not nodes[first]["leaf"]:
-        first = nodes[first]["left"]
-    tab = nodes[first:sub + 1]
-    lo_a = np.array([nd["lo"] for nd in tab], dtype=np.int64)
-    hi_a = np.array([nd["hi"] for nd in tab], dtype=np.int64)
-    dep_a = np.array([nd["depth"] for nd in tab], dtype=np.int64)
-    leaf_a = np.array([nd["leaf"] for nd in tab], dtype=bool)
-    split_a = np.array([nd.get("split", 0) for nd in tab], dtype=np.int64)
-    left_a = np.array([nd.get("left", first) for nd in tab], dtype=np.int64) - first
-    right_a = np.array([nd.get("right", first) for nd in tab], dtype=np.int64) - first
+    first = int(sub - nodes.size[sub] + 1)
+    rng = slice(first, sub + 1)
+    lo_a, hi_a, dep_a, leaf_a = nodes.lo[rng], nodes.hi[rng], nodes.depth[rng], nodes.leaf[rng]
+    split_a, mid_a = nodes.split[rng], nodes.mid[rng]
+    left_a = np.where(leaf_a, 0, nodes.left[rng] - first)
+    right_a = np.where(leaf_a, 0, nodes.right[rng] - first)
+    ntab = len(lo_a)
     base_lo = int(lo_a[-1])
     leaf_idx = np.flatnonzero(leaf_a)        # postorder visits the leaves left to right
     lam_all, Qbase, lqoff = _base_cases_flat(a_mod, b, lo_a[leaf_idx], hi_a[leaf_idx], s)
@@ -326,19 +377,19 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         rows_h = Qbase[torch.as_tensor(np.concatenate([first_i, last_i]), device="cuda")].cpu().numpy()
     lrow0 = np.concatenate([[0], np.cumsum(nl)]).astype(np.int64)
     # offsets of every node's first / last row in [leaf rows | the last depth's row gather]
-    first_off = np.zeros(len(tab), dtype=np.int64)
-    last_off = np.zeros(len(tab), dtype=np.int64)
+    first_off = np.zeros(ntab, dtype=np.int64)
+    last_off = np.zeros(ntab, dtype=np.int64)
     first_off[leaf_idx] = lrow0[:-1]
     last_off[leaf_idx] = int(lrow0[-1]) + lrow0[:-1]
-    is_left = np.zeros(len(tab), dtype=bool)
-    has_parent = np.zeros(len(tab), dtype=bool)
-    for j in np.flatnonzero(~leaf_a).tolist():
-        is_left[left_a[j]] = True
-        has_parent[left_a[j]] = has_parent[right_a[j]] = True
+    is_left = np.zeros(ntab, dtype=bool)
+    has_parent = np.zeros(ntab, dtype=bool)
+    inner_j = np.flatnonzero(~leaf_a)
+    is_left[left_a[inner_j]] = True
+    has_parent[left_a[inner_j]] = has_parent[right_a[inner_j]] = True
     pending = None      # (event, pinned rows) of the last depth's early row gather
     pending_records = []
     # per node: device address of its Q block (row-major n x n) and the buffer holding it
-    qptr = np.zeros(len(tab), dtype=np.uint64)
+    qptr = np.zeros(ntab, dtype=np.uint64)
     qptr[leaf_idx] = np.uint64(Qbase.data_ptr()) + (8 * lqoff[:-1]).astype(np.uint64)
     live = {}
     records = {}
@@ -547,10 +598,10 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                     n, k = int(nv[m]), int(kept[m])
                     sl = slice(int(koff[q]), int(koff[q + 1]))
                     C = CauchyEvecMatrix(dk[sl], gam[sl], mu[sl], zh[sl], vv[sl], dnext=dn[sl])
-                    nd = tab[ms[m]]
-                    rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
+                    mid = int(mid_a[ms[m]])
+                    rec_ = records.setdefault(mid, MergeRecord(size=n, kept=k, n_deflated=n - k))
                     Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(ldw[m]))
-                    jobs.append(HssJob(Q=Wm[:, :k], C=C, seed=[cfg.seed, nd["mid"]], flops=FlopCounter(),
+                    jobs.append(HssJob(Q=Wm[:, :k], C=C, seed=[cfg.seed, mid], flops=FlopCounter(),
                                        record=rec_, d=dk_h[sl], gamma=gam_h[sl], mu=mu_h[sl],
                                        out=Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k)))
                 update_vectors_hss_many(jobs, cfg)
@@ -619,19 +670,19 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
     # records and flop counts (reference conventions, dc.py:236-247)
     for ms, segs, nv, kept, rho_eff, seg_iters, hss_m in pending_records:
         for q, m in enumerate(segs.tolist()):
-            nd = tab[ms[m]]
+            mid = int(mid_a[ms[m]])
             n, k = int(nv[m]), int(kept[m])
             sec = secular_flops(k, int(seg_iters[q])) + 14 * k * k
             if q in hss_m:
-                rec_ = records[nd["mid"]]
+                rec_ = records[mid]
                 rec_.flops["secular"] = rec_.flops.get("secular", 0) + sec
             else:
-                rec_ = records.setdefault(nd["mid"], MergeRecord(size=n, kept=k, n_deflated=n - k))
+                rec_ = records.setdefault(mid, MergeRecord(size=n, kept=k, n_deflated=n - k))
                 rec_.flops = {"secular": sec, "update_dense": cauchy_eval_flops(k * k) + gemm_flops(n, k, k),
                               "hss_construct": 0, "hss_mult": 0}
         for m in np.flatnonzero((kept == 0) & (rho_eff != 0.0)).tolist():
             n = int(nv[m])
-            records.setdefault(tab[ms[m]]["mid"], MergeRecord(size=n, kept=0, n_deflated=n)).flops = \
+            records.setdefault(int(mid_a[ms[m]]), MergeRecord(size=n, kept=0, n_deflated=n)).flops = \
                 {p: 0 for p in FlopCounter.PHASES}
     n = int(hi_a[-1] - lo_a[-1])
     if leaf_a[-1]:

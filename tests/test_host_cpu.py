@@ -224,3 +224,46 @@ def test_deflation_tolerance_sums_like_numpy():
                            ctypes.byref(tolo))
     assert tolo.value == ref_tol
     assert k == dk.size and np.array_equal(out[2], perm)
+
+
+def test_recursion_tree_arrays_match_the_recursive_definition():
+    """solver._Tree (level-by-level NumPy build) against the recursion of dc.py:194-203 and its
+    split modifications (dc.py:82-102), including the merge ids in postorder."""
+    import itertools
+    from paper_1510_04591_b200 import solver
+
+    def ref_tree(n, base):
+        nodes, ids = [], itertools.count()
+
+        def rec(lo, hi, depth):
+            if hi - lo <= base:
+                nodes.append({"lo": lo, "hi": hi, "depth": depth, "leaf": True})
+                return len(nodes) - 1
+            m = lo + (hi - lo) // 2
+            left = rec(lo, m, depth + 1)
+            right = rec(m, hi, depth + 1)
+            nodes.append({"lo": lo, "hi": hi, "depth": depth, "leaf": False, "left": left,
+                          "right": right, "split": m, "mid": next(ids)})
+            return len(nodes) - 1
+
+        return nodes, rec(0, n, 0)
+
+    rng = np.random.default_rng(5)
+    for n, base in [(1, 25), (25, 25), (26, 25), (600, 25), (2000, 25), (1023, 3), (4097, 7), (10000, 32)]:
+        want, root = ref_tree(n, base)
+        got, groot = solver._tree(n, base)
+        assert groot == root and len(got) == len(want)
+        assert [got[i] for i in range(len(got))] == want
+        assert list(got) == want
+        for i, nd in enumerate(want):
+            if not nd["leaf"]:
+                assert i - got.size[i] + 1 == min(j for j in range(i + 1) if want[j]["lo"] == nd["lo"])
+        a, b = rng.standard_normal(n), rng.standard_normal(max(n - 1, 0))
+        a_ref, _ = solver._plan(a, b, base)
+        assert np.array_equal(got.split_diagonal(a, b), a_ref)
+        part = a.copy()
+        for nd in want:
+            if not nd["leaf"] and nd["depth"] < 2:
+                part[nd["split"] - 1] -= abs(b[nd["split"] - 1])
+                part[nd["split"]] -= abs(b[nd["split"] - 1])
+        assert np.array_equal(got.split_diagonal(a, b, 2), part)
