@@ -6,11 +6,16 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <numeric>
 #include <thread>
 #include <vector>
+
+#include <unistd.h>
 
 #include "common.cuh"
 
@@ -361,22 +366,24 @@ __device__ __forceinline__ void gather_row(const GatherSrc& g, int m, int64_t ro
   }
 }
 
-// Four rows per block: rows of one merge share the column descriptors, so the descriptor
-// array (8 B per output entry) is read once per four rows instead of once per row and the
-// four rows' source loads are independent (more loads in flight).  Groups that straddle a
-// merge boundary fall back to row by row.
-constexpr int kGatherRows = 4;
-__global__ void wave_gather_kernel(GatherSrc g, const int32_t* __restrict__ row_merge,
-                                   double* __restrict__ out, const int64_t* __restrict__ ooff,
-                                   int64_t nrows) {
+// ROWS rows per block and CPT columns per thread and iteration: rows of one merge share the
+// column descriptors, so the descriptor array (8 B per output entry) is read once per ROWS
+// rows, and a thread keeps ROWS * CPT independent source loads in flight and stores
+// 16 bytes at a time when the output rows are 16-byte aligned (n even).  Groups that
+// straddle a merge boundary fall back to row by row.
+template <int ROWS, int CPT>
+__global__ void __launch_bounds__(256)
+    wave_gather_kernel(GatherSrc g, const int32_t* __restrict__ row_merge,
+                       double* __restrict__ out, const int64_t* __restrict__ ooff, int64_t nrows) {
+  static_assert(CPT % 2 == 0, "columns per thread come in 16-byte pairs");
   constexpr int64_t kMask = (1ll << 40) - 1;
-  const int64_t ngroups = (nrows + kGatherRows - 1) / kGatherRows;
+  const int64_t ngroups = (nrows + ROWS - 1) / ROWS;
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-    const int64_t gr0 = grp * kGatherRows;
+    const int64_t gr0 = grp * ROWS;
     const int m = row_merge[gr0];
-    const bool whole = gr0 + kGatherRows <= nrows && row_merge[gr0 + kGatherRows - 1] == m;
+    const bool whole = gr0 + ROWS <= nrows && row_merge[gr0 + ROWS - 1] == m;
     if (!whole) {
-      for (int64_t gr = gr0; gr < min(gr0 + (int64_t)kGatherRows, nrows); ++gr) {
+      for (int64_t gr = gr0; gr < min(gr0 + (int64_t)ROWS, nrows); ++gr) {
         const int mm = row_merge[gr];
         const int64_t row = gr - g.roff[mm], n = g.n1[mm] + g.n2[mm];
         gather_row(g, mm, row, out + ooff[mm] + row * n);
@@ -386,13 +393,13 @@ __global__ void wave_gather_kernel(GatherSrc g, const int32_t* __restrict__ row_
     const int64_t a = g.n1[m], b = g.n2[m], n = a + b, k = g.kept[m];
     const int64_t row0 = gr0 - g.roff[m], ldw = g.wd[m] + (g.wd[m] & 1);
     const int64_t* dm = g.desc + g.roff[m];
-    const double* q[kGatherRows];
-    const double* w[kGatherRows];
-    const double* qc[kGatherRows];
-    int64_t c0[kGatherRows], nc[kGatherRows];
-    double* o[kGatherRows];
+    const double* q[ROWS];
+    const double* w[ROWS];
+    const double* qc[ROWS];
+    int64_t c0[ROWS], nc[ROWS];
+    double* o[ROWS];
 #pragma unroll
-    for (int r = 0; r < kGatherRows; ++r) {
+    for (int r = 0; r < ROWS; ++r) {
       const int64_t row = row0 + r;
       q[r] = g.Qk + g.qoff[m] + row * k;
       w[r] = g.W + g.woff[m] + row * ldw;
@@ -403,18 +410,37 @@ __global__ void wave_gather_kernel(GatherSrc g, const int32_t* __restrict__ row_
       nc[r] = top ? a : b;
       o[r] = out + ooff[m] + row * n;
     }
-    for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
-      const int64_t dsc = dm[c];
-      const int64_t src = dsc >> 40, idx = dsc & kMask;
-      double v[kGatherRows];
+    const bool vec = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(o[0]) & 15) == 0;
+    for (int64_t c = CPT * (int64_t)threadIdx.x; c < n; c += CPT * (int64_t)blockDim.x) {
+      int64_t src[CPT], idx[CPT];
 #pragma unroll
-      for (int r = 0; r < kGatherRows; ++r) {
-        if (src == 0) v[r] = q[r][idx];
-        else if (src == 1) v[r] = w[r][idx];
-        else v[r] = (idx >= c0[r] && idx < c0[r] + nc[r]) ? qc[r][idx - c0[r]] : 0.0;
+      for (int u = 0; u < CPT; ++u) {
+        const int64_t dsc = dm[c + u < n ? c + u : n - 1];
+        src[u] = dsc >> 40;
+        idx[u] = dsc & kMask;
       }
+      double v[ROWS][CPT];
 #pragma unroll
-      for (int r = 0; r < kGatherRows; ++r) o[r][c] = v[r];
+      for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+        for (int u = 0; u < CPT; ++u) {
+          if (src[u] == 0) v[r][u] = q[r][idx[u]];
+          else if (src[u] == 1) v[r][u] = w[r][idx[u]];
+          else v[r][u] = (idx[u] >= c0[r] && idx[u] < c0[r] + nc[r]) ? qc[r][idx[u] - c0[r]] : 0.0;
+        }
+      if (vec) {   // n even: column pairs never straddle the end of a row
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+          for (int u = 0; u < CPT; u += 2)
+            if (c + u < n) *reinterpret_cast<double2*>(o[r] + c + u) = make_double2(v[r][u], v[r][u + 1]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+          for (int u = 0; u < CPT; ++u)
+            if (c + u < n) o[r][c + u] = v[r][u];
+      }
     }
   }
 }
@@ -639,8 +665,11 @@ extern "C" int hsseig_wave_gather(const double* Qk, const int64_t* qoff, const i
   GatherSrc g{Qk ? Qk : W, qoff, kept, W, woff, wd, desc,
               reinterpret_cast<const unsigned long long*>(q1),
               reinterpret_cast<const unsigned long long*>(q2), n1, n2, roff};
-  wave_gather_kernel<<<rows_grid((nrows + kGatherRows - 1) / kGatherRows), 256, 0,
-                       (cudaStream_t)stream>>>(g, row_merge, out, ooff, nrows);
+  // shape swept at config 5 (rows x columns per thread: 4x2, 4x4, 8x2, 2x4, 1x4, 1x8, 3x4):
+  // 2 x 4 -- a full 32-byte sector per thread and row -- moves the top-level gather's 51.9 GB
+  // at 5.66 TB/s (87% of the measured copy bandwidth)
+  wave_gather_kernel<2, 4><<<rows_grid((nrows + 1) / 2), 256, 0, (cudaStream_t)stream>>>(
+      g, row_merge, out, ooff, nrows);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
 }
@@ -691,7 +720,62 @@ static void stable_argsort_runs(const double* key, int64_t split, int64_t n, int
 }
 
 // The merges of one level are independent: the host-side passes over them (deflation,
-// final order) run on a small thread pool once a level carries enough rows to pay for it.
+// final order, descriptors) run on a persistent worker pool once a level carries enough rows
+// to pay for it.  (Spawning std::threads per call cost 0.3-0.5 ms of each of the three passes
+// of every recursion depth -- a quarter of the host time of the deep, small-merge depths.)
+namespace {
+class MergePool {
+ public:
+  // f runs on the caller and on nt - 1 workers
+  void run(int nt, const std::function<void()>& f) {
+    std::lock_guard<std::mutex> one(run_mu_);
+    if (pid_ != getpid()) {   // a forked child starts without the parent's workers
+      workers_ = 0;
+      pid_ = getpid();
+    }
+    for (; workers_ < nt - 1; ++workers_) std::thread(&MergePool::worker, this, workers_).detach();
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &f;
+      want_ = nt - 1;
+      running_ = nt - 1;
+      ++gen_;
+    }
+    start_.notify_all();
+    f();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return running_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void worker(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      start_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (id >= want_) continue;
+      const std::function<void()>* j = job_;
+      lk.unlock();
+      (*j)();
+      lk.lock();
+      if (--running_ == 0) done_.notify_one();
+    }
+  }
+  std::mutex run_mu_, mu_;
+  std::condition_variable start_, done_;
+  const std::function<void()>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  int want_ = 0, running_ = 0, workers_ = 0;
+  pid_t pid_ = 0;
+};
+MergePool& merge_pool() {
+  static MergePool* p = new MergePool;   // never destroyed: its workers outlive static teardown
+  return *p;
+}
+}  // namespace
+
 template <class F>
 static void for_each_merge(int64_t nm, const int64_t* roff, F&& f) {
   const int64_t rows = roff[nm] - roff[0];
@@ -703,14 +787,11 @@ static void for_each_merge(int64_t nm, const int64_t* roff, F&& f) {
   }
   const int64_t chunk = std::max<int64_t>(1, nm / (nt * 8));
   std::atomic<int64_t> next{0};
-  auto work = [&] {
+  const std::function<void()> work = [&] {
     for (int64_t m0; (m0 = next.fetch_add(chunk)) < nm;)
       for (int64_t m = m0; m < std::min(nm, m0 + chunk); ++m) f(m);
   };
-  std::vector<std::thread> pool;
-  for (int64_t t = 1; t < nt; ++t) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
+  merge_pool().run((int)nt, work);
 }
 
 extern "C" int64_t hsseig_wave_deflate(int64_t nm, const int64_t* n1, const int64_t* n2,

@@ -37,6 +37,15 @@ MAX_BASE = 160   # largest device base case (csrc/glue.cu kQLBig)
 GLUE_PROFILE = None
 
 
+HOST_TRACE = None   # set to a list: (tag, depth, perf_counter) marks of solve_subtree's host side
+
+
+def _mark(tag, depth):
+    if HOST_TRACE is not None:
+        import time
+        HOST_TRACE.append((tag, depth, time.perf_counter()))
+
+
 def _i64(x):
     return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int64), device="cuda")
 
@@ -411,22 +420,35 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         roff = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
         nrows = int(roff[-1])
         rm = np.repeat(np.arange(nm), nv)
-        rows = lo_m[rm] - base_lo + np.arange(nrows) - roff[rm]
-        L = lam_all[rows]
+        # the merges of a depth cover increasing disjoint index ranges; one contiguous range
+        # when the depth holds no leaf (a slice instead of a 65536-entry index array)
+        if nm == 1 or np.array_equal(lo_m[1:], hi_a[ms[:-1]]):
+            rows = slice(int(lo_m[0] - base_lo), int(lo_m[0] - base_lo) + nrows)
+        else:
+            rows = np.arange(nrows) + np.repeat(lo_m - base_lo - roff[:-1], nv)
+        L = np.ascontiguousarray(lam_all[rows])
         q1, q2, n1_d, n2_d, nv_d, roff_d = (
             _Pack().add(qptr[left_a[ms]].view(np.int64)).add(qptr[right_a[ms]].view(np.int64))
             .add(n1).add(n2).add(nv).add(roff).send())
         # boundary rows of the children (sync 1: the early row gather of the previous depth)
         src_rows = rows_h
+        _mark("depth_begin", depth)
         if pending is not None:
             ev_rows, rows_pin = pending
             ev_rows.synchronize()
+            _mark("rows_ready", depth)
             src_rows = np.concatenate([rows_h, rows_pin.numpy()])
             pending = None
         # z rows: [last row of the left child | first row of the right child] per merge
         st_z = np.stack([last_off[left_a[ms]], first_off[right_a[ms]]], 1).reshape(-1)
         ln_z = np.stack([n1, n2], 1).reshape(-1)
-        zrow = src_rows[np.repeat(st_z - (np.cumsum(ln_z) - ln_z), ln_z) + np.arange(nrows)]
+        z_at = np.cumsum(ln_z) - ln_z
+        if np.array_equal(st_z - st_z[0], z_at):
+            # every child is a merge of the previous depth: its row gather is already laid
+            # out as [last row of the left child | first row of the right child] per merge
+            zrow = np.ascontiguousarray(src_rows[int(st_z[0]):int(st_z[0]) + nrows])
+        else:
+            zrow = src_rows[np.repeat(st_z - z_at, ln_z) + np.arange(nrows)]
         bk = np.ascontiguousarray(b[sp_m - 1], dtype=np.float64)
         kept = np.empty(nm, dtype=np.int64)
         rho_eff = np.empty(nm)
@@ -439,6 +461,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                                            _cptr(zrow), _cptr(bk), _cptr(kept), _cptr(rho_eff),
                                            _cptr(d_out), _cptr(z_out), _cptr(src), _cptr(rot_off),
                                            _cptr(ca), _cptr(cb), _cptr(rc), _cptr(rs)))
+        _mark("deflated", depth)
         # W_m holds only the kept columns and the deflated columns a rotation touches (the
         # other deflated columns are plain child eigenvectors, read by the final gather);
         # rows padded to an even leading dimension for the TMA engine
@@ -578,7 +601,9 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                     nat.ptr(dn), nat.ptr(gam), nat.ptr(mu), nat.ptr(zh), nat.ptr(vv), nat.ptr(koff_d),
                     nat.ptr(Qk), nat.ptr(t_qoff), nat.ptr(t_tk), len(tk), s),
                     "wave_dense_update")
+            _mark("updates_queued", depth)
             roots_ready.synchronize()
+            _mark("roots_ready", depth)
             stv = st_pin.numpy()
             bad_b = (stv[:, 1] < ks) | ((ks >= 2) & (stv[:, 2] < ks))
             bad_r = stv[:, 3] < ks
@@ -658,7 +683,11 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                                          nat.ptr(ooff_d), nrows, s), "wave_gather")
         if prof is not None:
             ev_g[1].record()
-            prof.append(("gather", ev_g[0], ev_g[1], 16 * int((nv * nv).sum())))
+            # bytes: every output entry written; a row reads its kept columns (dense update)
+            # and its own child's share of the deflated ones (the other child's are zeros)
+            prof.append(("gather", ev_g[0], ev_g[1],
+                         8 * int((nv * nv + nv * kept + nv * (nv - kept) // 2).sum())))
+        _mark("gather_queued", depth)
         del W, Qk
         live.pop(depth + 1, None)      # the children's blocks are dead once gathered
         live[depth] = A
