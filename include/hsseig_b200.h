@@ -464,6 +464,18 @@ int hsseig_dense_update_ws(const double *Qb, int64_t ldq, int64_t P, const hssei
                            double *out, int64_t ldo, double *work, int64_t work_doubles,
                            void *stream);
 
+/* The dense update of a DC merge (dc.py:132-138 applied to dc.py:215-235's block) without the
+   structural zeros of blockdiag(Q1, Q2): perm (device, k entries) orders the kept columns as
+   [child 1 only | touched by a deflation rotation | child 2 only]; rows [0, n1) of Qb
+   contract over perm[0, ka) and rows [n1, P) over perm[kb, k) -- the terms the full product
+   multiplies by exact zeros are skipped (LAPACK dlaed3's partition), about half the flops.
+   work: hsseig_dense_update_halves_work_doubles(P, k, panel_cols) doubles, 16-byte aligned. */
+int64_t hsseig_dense_update_halves_work_doubles(int64_t P, int64_t k, int64_t panel_cols);
+int hsseig_dense_update_halves(const double *Qb, int64_t ldq, int64_t P, int64_t n1,
+                               const hsseig_gen *gen, const int64_t *perm, int64_t ka,
+                               int64_t kb, double *out, int64_t ldo, double *work,
+                               int64_t work_doubles, void *stream);
+
 /* Plain batched helper used by tests/bench: out = A @ B (P x K)(K x N), FP64 DMMA. */
 int hsseig_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                 int64_t ldc, int64_t M, int64_t N, int64_t K, void *stream);

@@ -4,6 +4,7 @@ Mirror of pkg/src/hsseig/cauchy.py: C[i, j] = zhat[i] v[j] / (d[i] - lam[j]) is
 never stored; blocks, products and the dense update generate tiles on the fly
 in shared memory (csrc/cauchy.cu).
 """
+import numpy as np
 import torch
 
 from . import _native as nat
@@ -153,4 +154,28 @@ class CauchyEvecMatrix:
         nat.check(lib.hsseig_dense_update(nat.ptr(Q), Q.stride(0), Q.shape[0], self._gen,
                                           nat.ptr(out), out.stride(0), nat.stream_ptr()),
                   "dense_update")
+        return out
+
+    def right_multiply_halves_into(self, W, n1, perm, ka, kb, out=None):
+        """out = W @ C for W = the kept columns of a merge's blockdiag(Q1, Q2) block (rows
+        [0, n1) from child 1): perm orders the kept columns [child 1 only | rotated | child 2
+        only], the top rows contract over perm[:ka], the bottom rows over perm[kb:] -- the
+        dense update (dc.py:132-138) without its products with structural zeros."""
+        W = dev_rows(W)
+        P, k = W.shape
+        if k != self.k:
+            raise ValueError("inner dimensions do not match")
+        if W.stride(0) % 2 or W.data_ptr() % 16:
+            raise ValueError("W rows must be 16-byte aligned (even leading dimension)")
+        if out is None:
+            out = torch.empty(P, k, dtype=torch.float64, device="cuda")
+        lib = nat.load()
+        perm_d = torch.as_tensor(np.ascontiguousarray(perm, dtype=np.int64), device="cuda")
+        cols = max(128, DENSE_PANEL_BYTES // (8 * k))
+        work = torch.empty(int(lib.hsseig_dense_update_halves_work_doubles(P, k, cols)),
+                           dtype=torch.float64, device="cuda")
+        nat.check(lib.hsseig_dense_update_halves(nat.ptr(W), W.stride(0), P, int(n1), self._gen,
+                                                 nat.ptr(perm_d), int(ka), int(kb), nat.ptr(out),
+                                                 out.stride(0), nat.ptr(work), work.numel(),
+                                                 nat.stream_ptr()), "dense_update_halves")
         return out

@@ -898,3 +898,111 @@ extern "C" int hsseig_dense_update_ws(const double* Qb, int64_t ldq, int64_t P,
   }
   return HSSEIG_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Dense update of a DC merge without the structural zeros (the dlaed3 observation): the
+// merge's eigenvector block is blockdiag(Q1, Q2) with permuted columns, so a kept column
+// that comes from child 1 and that no deflation rotation touched is zero below row n1, and
+// a child-2 column is zero above it.  perm orders the k kept columns as
+// [child 1 only | rotated (dense) | child 2 only]; the top n1 rows then contract over
+// perm[0, ka) only and the bottom rows over perm[kb, k):
+//   out[0:n1, :]  = W[0:n1, perm[0:ka]]  C[perm[0:ka], :]
+//   out[n1:P, :]  = W[n1:P, perm[kb:k]]  C[perm[kb:k], :]
+// -- about half the flops of out = W C, with exactly the terms that are not products with a
+// structural zero.  The two row blocks of W are compacted once, C's panels are generated
+// with their rows in perm order (entries as gen_panel_kernel<true>, the reference's
+// to_dense values) and both products run on the TMA/DMMA engine.
+// ---------------------------------------------------------------------------
+__global__ void compact_halves_kernel(const double* __restrict__ W, int64_t ldw, int64_t P,
+                                      int64_t n1, const int64_t* __restrict__ perm, int64_t ka,
+                                      int64_t kb, int64_t k, double* __restrict__ top,
+                                      int64_t ldt, double* __restrict__ bot, int64_t ldb) {
+  for (int64_t r = blockIdx.x; r < P; r += gridDim.x) {
+    const double* w = W + r * ldw;
+    if (r < n1) {
+      double* o = top + r * ldt;
+      for (int64_t c = threadIdx.x; c < ka; c += blockDim.x) o[c] = w[__ldg(perm + c)];
+    } else {
+      double* o = bot + (r - n1) * ldb;
+      for (int64_t c = threadIdx.x; c < k - kb; c += blockDim.x) o[c] = w[__ldg(perm + kb + c)];
+    }
+  }
+}
+
+// panel[i][j] = C[perm[i]][j0 + j], i < k, j < nj: the reference's entry, IEEE division
+__global__ void gen_panel_perm_kernel(CauchyGen g, const int64_t* __restrict__ perm, int64_t k,
+                                      int64_t j0, int64_t nj, double* __restrict__ out,
+                                      int64_t ld) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nj) return;
+  const int64_t gj = j0 + j;
+  const double dj = __ldg(g.d + gj), dnj = __ldg(g.dnext + gj), gmj = __ldg(g.gam + gj);
+  const double mj = __ldg(g.mu + gj), vj = __ldg(g.v + gj);
+  for (int64_t i = blockIdx.y; i < k; i += gridDim.y) {
+    const int64_t gi = __ldg(perm + i);
+    const double gap = stable_gap(gi, gj, __ldg(g.d + gi), dj, dnj, gmj, mj);
+    out[i * ld + j] = (__ldg(g.zhat + gi) * vj) / gap;
+  }
+}
+
+static int64_t even64(int64_t x) { return x + (x & 1); }
+
+extern "C" int64_t hsseig_dense_update_halves_work_doubles(int64_t P, int64_t k,
+                                                           int64_t panel_cols) {
+  if (P < 1 || k < 1 || panel_cols < 1) return -1;
+  return P * even64(k) + 64 + hsseig_dense_update_work_doubles(k, panel_cols);
+}
+
+extern "C" int hsseig_dense_update_halves(const double* Qb, int64_t ldq, int64_t P, int64_t n1,
+                                          const hsseig_gen* gen, const int64_t* perm, int64_t ka,
+                                          int64_t kb, double* out, int64_t ldo, double* work,
+                                          int64_t work_doubles, void* stream) {
+  if (!gen || !perm || P < 0 || n1 < 0 || n1 > P || ldq < gen->k || ldo < gen->k || ka < 0 ||
+      kb < 0 || kb > ka || ka > gen->k || !work)
+    HSS_ARG_FAIL();
+  if (P == 0) return HSSEIG_OK;
+  const int64_t k = gen->k, n2 = P - n1, kt = ka, kbn = k - kb;
+  const int64_t ldt = even64(imax64(kt, 1)), ldb = even64(imax64(kbn, 1));
+  const int64_t halves = ((n1 * ldt + n2 * ldb + 31) / 32) * 32;
+  double* top = work;
+  double* bot = work + n1 * ldt;
+  double* rest = work + halves;
+  int64_t kc = (work_doubles - halves - dense_ws_overhead(k)) / (k + 1);
+  kc = imin64(k, kc / 128 * 128);
+  if ((reinterpret_cast<uintptr_t>(work) & 15) || kc < 128) HSS_ARG_FAIL();
+  const int64_t ldp = kc + (kc & 1);
+  double* panel = rest;
+  TJob* jobs = reinterpret_cast<TJob*>(rest + k * ldp);
+  MapSet* dmaps = reinterpret_cast<MapSet*>(
+      (reinterpret_cast<uintptr_t>(jobs + (k + 127) / 128) + 255) & ~(uintptr_t)255);
+  CauchyGen g = to_gen(gen);
+  cudaStream_t s = (cudaStream_t)stream;
+  compact_halves_kernel<<<(unsigned)imin64(P, 1 << 20), 256, 0, s>>>(Qb, ldq, P, n1, perm, ka, kb, k,
+                                                                   top, ldt, bot, ldb);
+  HSS_CHECK_LAUNCH();
+  for (int64_t c0 = 0; c0 < k; c0 += kc) {
+    const int64_t nc = imin64(kc, k - c0);
+    dim3 gr((unsigned)((nc + 255) / 256), (unsigned)imin64(k, 128));
+    gen_panel_perm_kernel<<<gr, 256, 0, s>>>(g, perm, k, c0, nc, panel, ldp);
+    HSS_CHECK_LAUNCH();
+    int rc;
+    if (n1 > 0) {
+      if (kt > 0) {
+        if ((rc = tma_plain_gemm(top, ldt, panel, ldp, out + c0, ldo, n1, nc, kt, jobs, dmaps, s)))
+          return rc;
+      } else if (cudaMemset2DAsync(out + c0, ldo * 8, 0, nc * 8, n1, s) != cudaSuccess) {
+        return HSSEIG_ERR_CUDA;
+      }
+    }
+    if (n2 > 0) {
+      if (kbn > 0) {
+        if ((rc = tma_plain_gemm(bot, ldb, panel + kb * ldp, ldp, out + n1 * ldo + c0, ldo, n2, nc,
+                                 kbn, jobs, dmaps, s)))
+          return rc;
+      } else if (cudaMemset2DAsync(out + n1 * ldo + c0, ldo * 8, 0, nc * 8, n2, s) != cudaSuccess) {
+        return HSSEIG_ERR_CUDA;
+      }
+    }
+  }
+  return HSSEIG_OK;
+}

@@ -488,6 +488,27 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         hss_q = (ks > cfg.hss_threshold) if cfg.method in HSS_METHODS else np.zeros(nseg, bool)
         big_q = ~hss_q & (ks >= DENSE_PANEL_MIN_K)
         small = np.flatnonzero(~hss_q & ~big_q)
+        # K order of every panel update, [child 1 only | rotated | child 2 only] (the rows of
+        # blockdiag(Q1, Q2) above / below the split see only their own child's kept columns
+        # and the ones a deflation rotation mixed: hsseig_dense_update_halves)
+        big = np.flatnonzero(big_q)
+        kperm, ka_b, kb_b = np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64)
+        if len(big):
+            mb, kb_ = segs[big], ks[big]
+            boff = np.concatenate([[0], np.cumsum(kb_)]).astype(np.int64)
+            seg_b = np.repeat(np.arange(len(big)), kb_)
+            pos_b = np.arange(int(boff[-1])) - boff[seg_b]
+            cls = np.where(src[roff[mb][seg_b] + pos_b] < n1[mb][seg_b], 0, 2)
+            nr_b = rot_off[mb + 1] - rot_off[mb]
+            if nr_b.sum():
+                seg_r = np.repeat(np.arange(len(big)), nr_b)
+                ridx = np.repeat(rot_off[mb] - (np.cumsum(nr_b) - nr_b), nr_b) + np.arange(int(nr_b.sum()))
+                for cc in (ca[ridx], cb[ridx]):
+                    ok = cc < kb_[seg_r]
+                    cls[boff[seg_r[ok]] + cc[ok]] = 1
+            kperm = np.lexsort((cls, seg_b)) - boff[seg_b]       # stable within a merge
+            ka_b = np.add.reduceat((cls <= 1).astype(np.int64), boff[:-1])
+            kb_b = np.add.reduceat((cls == 0).astype(np.int64), boff[:-1])
         mt, nt = -(-nvs[small] // bm), -(-ks[small] // bn)
         cnt = mt * nt
         tk = np.empty((int(cnt.sum()), 3), dtype=np.int32)
@@ -512,13 +533,14 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         st0 = np.zeros((nseg, 8), dtype=np.int64)
         st0[:, 1:4] = ks[:, None]
         (woff_d, wd_d, row_merge, csrc_d, coff_d, rot_d1, rot_d2, rot_d3, rot_d4, dk, zk,
-         koff_d, seg_of, rho_d, st, t_woff, t_nv, t_qoff, t_tk, t_ldw, run_t_d, run_off_d) = (
+         koff_d, seg_of, rho_d, st, t_woff, t_nv, t_qoff, t_tk, t_ldw, run_t_d, run_off_d,
+         kperm_d) = (
             _Pack().add(woff).add(wd).add(rm, np.int32).add(csrc[:int(coff[-1])]).add(coff)
             .add(ca[:nrot]).add(cb[:nrot]).add(rc[:nrot], np.float64)
             .add(rs[:nrot], np.float64).add(d_out[kidx], np.float64).add(z_out[kidx], np.float64)
             .add(koff).add(np.repeat(np.arange(nseg), ks), np.int32)
             .add(rho_eff[segs], np.float64).add(st0).add(woff[segs]).add(nvs).add(qoff[segs])
-            .add(tk, np.int32).add(ldw[segs]).add(run_t).add(run_off).send())
+            .add(tk, np.int32).add(ldw[segs]).add(run_t).add(run_off).add(kperm).send())
         W = torch.empty(max(int(woff[-1]), 2), **f64)
         prof = GLUE_PROFILE
         if prof is not None:
@@ -575,26 +597,29 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 mu_pin.copy_(mu, non_blocking=True)
             roots_ready = torch.cuda.Event()
             roots_ready.record()
-            big = np.flatnonzero(big_q)
             if len(big):
                 # materialised-panel updates straight through the C ABI (one generator struct
                 # and one shared workspace; cauchy.py's right_multiply_into per merge costs
                 # ~70 us of host time each at config 5)
-                kmax = int(ks[big].max())
-                pw = torch.empty(int(lib.hsseig_dense_update_work_doubles(
-                    kmax, max(128, DENSE_PANEL_BYTES // (8 * kmax)))), **f64)
+                kmax, kmin, nmax = int(ks[big].max()), int(ks[big].min()), int(nvs[big].max())
+                nw = int(lib.hsseig_dense_update_halves_work_doubles(
+                    nmax, kmax, max(128, DENSE_PANEL_BYTES // (8 * kmin))))
+                pw = torch.empty(nw, **f64)
                 gb = [t.data_ptr() for t in (dk, dn, gam, mu, zh, vv)]
-                Wb, Qb = W.data_ptr(), Qk.data_ptr()
-                for q in big.tolist():
+                Wb, Qb, pb = W.data_ptr(), Qk.data_ptr(), kperm_d.data_ptr()
+                po = 0
+                for q, ka, kb in zip(big.tolist(), ka_b.tolist(), kb_b.tolist()):
                     m = segs[q]
                     n, k, o8 = int(nv[m]), int(kept[m]), 8 * int(koff[q])
                     g = nat.Gen(gb[0] + o8, gb[1] + o8, gb[2] + o8, gb[3] + o8, gb[4] + o8,
                                 gb[5] + o8, k)
-                    nw = int(lib.hsseig_dense_update_work_doubles(k, max(128, DENSE_PANEL_BYTES // (8 * k))))
-                    nat.check(lib.hsseig_dense_update_ws(
-                        ctypes.c_void_p(Wb + 8 * int(woff[m])), int(ldw[m]), n, ctypes.byref(g),
+                    # the shared workspace is sized for the widest merge; a merge may use all of it
+                    nat.check(lib.hsseig_dense_update_halves(
+                        ctypes.c_void_p(Wb + 8 * int(woff[m])), int(ldw[m]), n, int(n1[m]),
+                        ctypes.byref(g), ctypes.c_void_p(pb + 8 * po), ka, kb,
                         ctypes.c_void_p(Qb + 8 * int(qoff[m])), k, nat.ptr(pw), nw, s),
-                        "dense_update")
+                        "dense_update_halves")
+                    po += k
             if len(tk):
                 nat.check(lib.hsseig_wave_dense_update(
                     nat.ptr(W), nat.ptr(t_woff), nat.ptr(t_nv), nat.ptr(t_ldw), nat.ptr(dk),

@@ -173,6 +173,31 @@ def test_dense_update_vs_torch():
     assert float((Qn - ref).abs().max()) <= 1e-13 * float(ref.abs().max())
 
 
+@pytest.mark.parametrize("n1,k1,kr,k2", [(400, 300, 7, 350), (333, 0, 5, 700), (500, 640, 0, 0), (1, 100, 30, 500)])
+def test_dense_update_halves_equals_the_full_product(n1, k1, kr, k2):
+    """hsseig_dense_update_halves (the merge's blockdiag structure: top rows see child-1 and
+    rotated columns only, bottom rows child-2 and rotated) against the full dense update of
+    the same block, whose extra terms are products with exact zeros."""
+    k = k1 + kr + k2
+    P = n1 + 450
+    d, z, rho = config4_system(k, 4)
+    C = hb.merge_update(d, z, rho, np.eye(k)[:2], hb.SolverConfig(method="dense-dc"))[2]
+    rng = np.random.default_rng(8)
+    cls = rng.permutation(np.repeat([0, 1, 2], [k1, kr, k2]))      # interleaved origins
+    W = rng.standard_normal((P, k))
+    W[n1:, cls == 0] = 0.0
+    W[:n1, cls == 2] = 0.0
+    perm = np.argsort(cls, kind="stable")
+    Wd = torch.zeros(P, k + (k & 1), dtype=torch.float64, device="cuda")
+    Wd[:, :k] = torch.as_tensor(W)
+    out = C.right_multiply_halves_into(Wd[:, :k], n1, perm, k1 + kr, k1)
+    full = C.right_multiply_into(Wd[:, :k])
+    ref = torch.as_tensor(W, device="cuda") @ C.to_dense()
+    scale = float(ref.abs().max())
+    assert float((out - full).abs().max()) <= 1e-13 * scale
+    assert float((out - ref).abs().max()) <= 1e-13 * scale
+
+
 def test_plain_gemm_helper():
     rng = np.random.default_rng(5)
     A = rng.standard_normal((517, 300))
