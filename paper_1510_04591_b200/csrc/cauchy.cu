@@ -1006,3 +1006,25 @@ extern "C" int hsseig_dense_update_halves(const double* Qb, int64_t ldq, int64_t
   }
   return HSSEIG_OK;
 }
+
+// Every panel update of one recursion depth in one call (the host loop in C: ~25 us of
+// ctypes overhead per merge otherwise).  rec (host, 9 int64 per merge): W offset, ldw, rows,
+// n1, generator offset, k, ka, kb, out offset; perm holds the merges' K orders back to back.
+extern "C" int hsseig_wave_dense_halves(int64_t nbig, const int64_t* rec, const double* W,
+                                        const double* d, const double* dnext, const double* gamma,
+                                        const double* mu, const double* zhat, const double* v,
+                                        const int64_t* perm, double* out, double* work,
+                                        int64_t work_doubles, void* stream) {
+  if (nbig < 0 || (nbig > 0 && (!rec || !W || !perm || !out || !work))) HSS_ARG_FAIL();
+  int64_t po = 0;
+  for (int64_t q = 0; q < nbig; ++q) {
+    const int64_t* r = rec + 9 * q;
+    const int64_t go = r[4], k = r[5];
+    hsseig_gen g{d + go, dnext + go, gamma + go, mu + go, zhat + go, v + go, k};
+    const int rc = hsseig_dense_update_halves(W + r[0], r[1], r[2], r[3], &g, perm + po, r[6], r[7],
+                                              out + r[8], k, work, work_doubles, stream);
+    if (rc) return rc;
+    po += k;
+  }
+  return HSSEIG_OK;
+}

@@ -605,21 +605,15 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 nw = int(lib.hsseig_dense_update_halves_work_doubles(
                     nmax, kmax, max(128, DENSE_PANEL_BYTES // (8 * kmin))))
                 pw = torch.empty(nw, **f64)
-                gb = [t.data_ptr() for t in (dk, dn, gam, mu, zh, vv)]
-                Wb, Qb, pb = W.data_ptr(), Qk.data_ptr(), kperm_d.data_ptr()
-                po = 0
-                for q, ka, kb in zip(big.tolist(), ka_b.tolist(), kb_b.tolist()):
-                    m = segs[q]
-                    n, k, o8 = int(nv[m]), int(kept[m]), 8 * int(koff[q])
-                    g = nat.Gen(gb[0] + o8, gb[1] + o8, gb[2] + o8, gb[3] + o8, gb[4] + o8,
-                                gb[5] + o8, k)
-                    # the shared workspace is sized for the widest merge; a merge may use all of it
-                    nat.check(lib.hsseig_dense_update_halves(
-                        ctypes.c_void_p(Wb + 8 * int(woff[m])), int(ldw[m]), n, int(n1[m]),
-                        ctypes.byref(g), ctypes.c_void_p(pb + 8 * po), ka, kb,
-                        ctypes.c_void_p(Qb + 8 * int(qoff[m])), k, nat.ptr(pw), nw, s),
-                        "dense_update_halves")
-                    po += k
+                # the shared workspace is sized for the widest merge; a merge may use all of it
+                mb = segs[big]
+                rec9 = np.ascontiguousarray(np.stack(
+                    [woff[mb], ldw[mb], nv[mb], n1[mb], koff[big], kept[mb], ka_b, kb_b, qoff[mb]], 1),
+                    dtype=np.int64)
+                nat.check(lib.hsseig_wave_dense_halves(
+                    len(big), _cptr(rec9), nat.ptr(W), nat.ptr(dk), nat.ptr(dn), nat.ptr(gam),
+                    nat.ptr(mu), nat.ptr(zh), nat.ptr(vv), nat.ptr(kperm_d), nat.ptr(Qk),
+                    nat.ptr(pw), nw, s), "wave_dense_halves")
             if len(tk):
                 nat.check(lib.hsseig_wave_dense_update(
                     nat.ptr(W), nat.ptr(t_woff), nat.ptr(t_nv), nat.ptr(t_ldw), nat.ptr(dk),
