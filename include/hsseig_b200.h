@@ -479,11 +479,15 @@ int hsseig_dense_update_halves(const double *Qb, int64_t ldq, int64_t P, int64_t
 /* hsseig_dense_update_halves for every panel update of one recursion depth (the solver's
    level-batched schedule): rec (host) holds 9 int64 per merge -- W offset, ldw, rows, n1,
    generator offset, k, ka, kb, out offset (offsets in doubles from W / the generator
-   arrays / out); perm (device) holds the merges' K orders back to back. */
+   arrays / out); perm (device) holds the merges' K orders back to back.  The updates are
+   dealt to up to nstreams (<= 8) internal side streams forked from and joined into `stream`,
+   each with work_doubles / nstreams doubles of the workspace (each slice at least
+   hsseig_dense_update_halves_work_doubles of the largest merge). */
 int hsseig_wave_dense_halves(int64_t nbig, const int64_t *rec, const double *W, const double *d,
                              const double *dnext, const double *gamma, const double *mu,
                              const double *zhat, const double *v, const int64_t *perm,
-                             double *out, double *work, int64_t work_doubles, void *stream);
+                             double *out, double *work, int64_t work_doubles, int32_t nstreams,
+                             void *stream);
 
 /* Plain batched helper used by tests/bench: out = A @ B (P x K)(K x N), FP64 DMMA. */
 int hsseig_gemm(const double *A, int64_t lda, const double *B, int64_t ldb, double *C,

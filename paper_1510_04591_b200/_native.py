@@ -108,7 +108,7 @@ _SIGS = {
     "hsseig_dense_update_halves": (ctypes.c_int, [c_vp, c_i64, c_i64, c_i64, ctypes.POINTER(Gen), c_vp,
                                                   c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "hsseig_wave_dense_halves": (ctypes.c_int, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
-                                                c_vp, c_vp, c_vp, c_i64, c_vp]),
+                                                c_vp, c_vp, c_vp, c_i64, ctypes.c_int32, c_vp]),
     "hsseig_set_normal_tables": (ctypes.c_int, [c_vp, c_vp, c_vp]),
     "hsseig_normals_work_bytes": (c_i64, [c_i64]),
     "hsseig_normals_fixup": (c_i64, [c_vp, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp, c_vp]),

@@ -1010,21 +1010,60 @@ extern "C" int hsseig_dense_update_halves(const double* Qb, int64_t ldq, int64_t
 // Every panel update of one recursion depth in one call (the host loop in C: ~25 us of
 // ctypes overhead per merge otherwise).  rec (host, 9 int64 per merge): W offset, ldw, rows,
 // n1, generator offset, k, ka, kb, out offset; perm holds the merges' K orders back to back.
+// The updates of a depth are independent and, below the top depths, each too small to fill
+// the GPU (a 1024 x 600 update has 40 output tiles for 148 SMs): they are dealt round-robin
+// to nstreams side streams (forked from / joined into `stream` by events), each with its own
+// slice of the workspace (work_doubles / nstreams doubles).
+namespace {
+constexpr int kHalvesStreams = 8;
+struct HalvesSide {
+  cudaStream_t s[kHalvesStreams] = {};
+  cudaEvent_t in = nullptr, done[kHalvesStreams] = {};
+  bool ok = false;
+  HalvesSide() {
+    ok = cudaEventCreateWithFlags(&in, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < kHalvesStreams; ++i)
+      ok = cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming) == cudaSuccess;
+  }
+};
+}  // namespace
+
 extern "C" int hsseig_wave_dense_halves(int64_t nbig, const int64_t* rec, const double* W,
                                         const double* d, const double* dnext, const double* gamma,
                                         const double* mu, const double* zhat, const double* v,
                                         const int64_t* perm, double* out, double* work,
-                                        int64_t work_doubles, void* stream) {
-  if (nbig < 0 || (nbig > 0 && (!rec || !W || !perm || !out || !work))) HSS_ARG_FAIL();
+                                        int64_t work_doubles, int32_t nstreams, void* stream) {
+  if (nbig < 0 || nstreams < 1 || (nbig > 0 && (!rec || !W || !perm || !out || !work)))
+    HSS_ARG_FAIL();
+  if (nbig == 0) return HSSEIG_OK;
+  static HalvesSide side;
+  const int ns = (int)imin64(imin64(nstreams, kHalvesStreams), nbig);
+  const int64_t per = (work_doubles / ns) & ~int64_t(31);
+  cudaStream_t main_s = (cudaStream_t)stream;
+  if (ns > 1) {
+    if (!side.ok) return HSSEIG_ERR_CUDA;
+    if (cudaEventRecord(side.in, main_s) != cudaSuccess) return HSSEIG_ERR_CUDA;
+    for (int i = 0; i < ns; ++i)
+      if (cudaStreamWaitEvent(side.s[i], side.in, 0) != cudaSuccess) return HSSEIG_ERR_CUDA;
+  }
   int64_t po = 0;
-  for (int64_t q = 0; q < nbig; ++q) {
+  int rc = HSSEIG_OK;
+  for (int64_t q = 0; q < nbig && rc == HSSEIG_OK; ++q) {
     const int64_t* r = rec + 9 * q;
     const int64_t go = r[4], k = r[5];
     hsseig_gen g{d + go, dnext + go, gamma + go, mu + go, zhat + go, v + go, k};
-    const int rc = hsseig_dense_update_halves(W + r[0], r[1], r[2], r[3], &g, perm + po, r[6], r[7],
-                                              out + r[8], k, work, work_doubles, stream);
-    if (rc) return rc;
+    const int lane = (int)(q % ns);
+    rc = hsseig_dense_update_halves(W + r[0], r[1], r[2], r[3], &g, perm + po, r[6], r[7],
+                                    out + r[8], k, work + lane * per, per,
+                                    ns > 1 ? (void*)side.s[lane] : stream);
     po += k;
   }
-  return HSSEIG_OK;
+  if (ns > 1) {   // join even after a failure so the caller's stream stays ordered
+    for (int i = 0; i < ns; ++i)
+      if (cudaEventRecord(side.done[i], side.s[i]) != cudaSuccess ||
+          cudaStreamWaitEvent(main_s, side.done[i], 0) != cudaSuccess)
+        return HSSEIG_ERR_CUDA;
+  }
+  return rc;
 }

@@ -15,6 +15,7 @@ Eigenvalues are returned on the host (NumPy, as the reference); Q stays on the d
 """
 import ctypes
 import itertools
+import os
 
 import numpy as np
 import torch
@@ -37,6 +38,7 @@ MAX_BASE = 160   # largest device base case (csrc/glue.cu kQLBig)
 GLUE_PROFILE = None
 
 
+DENSE_STREAMS = int(os.environ.get("HSSEIG_DENSE_STREAMS", "4"))   # panel updates of a depth in flight
 HOST_TRACE = None   # set to a list: (tag, depth, perf_counter) marks of solve_subtree's host side
 
 
@@ -602,8 +604,11 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 # and one shared workspace; cauchy.py's right_multiply_into per merge costs
                 # ~70 us of host time each at config 5)
                 kmax, kmin, nmax = int(ks[big].max()), int(ks[big].min()), int(nvs[big].max())
-                nw = int(lib.hsseig_dense_update_halves_work_doubles(
-                    nmax, kmax, max(128, DENSE_PANEL_BYTES // (8 * kmin))))
+                # the depth's updates run on up to DENSE_STREAMS side streams, each with its
+                # own slice of the workspace (sized for the widest merge)
+                nst = min(DENSE_STREAMS, len(big))
+                nw = nst * ((int(lib.hsseig_dense_update_halves_work_doubles(
+                    nmax, kmax, max(128, DENSE_PANEL_BYTES // (8 * kmin)))) + 63) & ~31)
                 pw = torch.empty(nw, **f64)
                 # the shared workspace is sized for the widest merge; a merge may use all of it
                 mb = segs[big]
@@ -613,7 +618,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 nat.check(lib.hsseig_wave_dense_halves(
                     len(big), _cptr(rec9), nat.ptr(W), nat.ptr(dk), nat.ptr(dn), nat.ptr(gam),
                     nat.ptr(mu), nat.ptr(zh), nat.ptr(vv), nat.ptr(kperm_d), nat.ptr(Qk),
-                    nat.ptr(pw), nw, s), "wave_dense_halves")
+                    nat.ptr(pw), nw, nst, s), "wave_dense_halves")
             if len(tk):
                 nat.check(lib.hsseig_wave_dense_update(
                     nat.ptr(W), nat.ptr(t_woff), nat.ptr(t_nv), nat.ptr(t_ldw), nat.ptr(dk),

@@ -35,6 +35,8 @@ by = {}
 for tag, d, t in tr:
     by.setdefault(d, {})[tag] = (t - t0) * 1e3
 print(f"returned {1e3 * (t_ret - t0):.2f} ms, device drained {1e3 * (t_end - t0):.2f} ms")
+if os.environ.get("HSSEIG_TRACE_SUMMARY"):
+    sys.exit(0)
 print("depth  begin  rows_wait  deflate  to_queued  roots_wait  to_gather_queued")
 for d in sorted(by, reverse=True):
     b = by[d]
