@@ -215,6 +215,14 @@ class HssTree:
 
         rec(0, self.partition.n_leaves, 0)
         self.nodes = nodes
+        # topology as arrays (children / sibling = -1 where absent) for the flop counters
+        self._topo = {
+            "leaf": np.array([nd.left < 0 for nd in nodes], dtype=bool),
+            "left": np.array([nd.left for nd in nodes], dtype=np.int64),
+            "right": np.array([nd.right for nd in nodes], dtype=np.int64),
+            "sib": np.array([nd.sibling for nd in nodes], dtype=np.int64),
+            "m": np.array([nd.hi - nd.lo for nd in nodes], dtype=np.int64),
+        }
         self._leaf_pos = {}
         pos = 0
         for nd in nodes:
@@ -335,44 +343,42 @@ def tree_from_factors(partition, factors, w=None):
 
 
 def _construct_flops(tree, k, w):
-    rU, rV = tree.ranks()
+    """hss_construct counter of hss.py:251-287 for the ranks the construction produced (the
+    reference's per-node terms, summed over node arrays: a Python loop over the nodes cost
+    ~10 ms per config-2 / config-3 solve)."""
+    rU, rV = (np.asarray(r, dtype=np.int64) for r in tree.ranks())
+    tp = tree._topo
+    nonroot = np.ones(len(rU), dtype=bool)
+    nonroot[tree.root] = False
     f = 2 * (gemm_flops(k, k, w) + cauchy_eval_flops(k * k))
-    for nd in tree.nodes:
-        if nd.index == tree.root:
-            continue
-        if nd.is_leaf:
-            m = nd.hi - nd.lo
-            f += cauchy_eval_flops(m * m) + 2 * gemm_flops(m, m, w)
-            f += cpqr_flops(w, m, max(int(rU[nd.index]), 1)) + cpqr_flops(w, m, max(int(rV[nd.index]), 1))
-        else:
-            a, b = nd.left, nd.right
-            f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
-            f += 2 * gemm_flops(int(rU[a] + rU[b]), w, max(int(rU[a]), int(rV[b])))
-            f += cpqr_flops(w, int(rU[a] + rU[b]), max(int(rU[nd.index]), 1))
-            f += cpqr_flops(w, int(rV[a] + rV[b]), max(int(rV[nd.index]), 1))
-    rt = tree.nodes[tree.root]
-    a, b = rt.left, rt.right
-    f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
+    lf = tp["leaf"] & nonroot
+    m = tp["m"][lf]
+    f += int((6 * m * m + 2 * 2 * m * m * w + 4 * w * m * np.maximum(rU[lf], 1)
+              + 4 * w * m * np.maximum(rV[lf], 1)).sum())
+    inn = ~tp["leaf"]
+    a, b = tp["left"][inn], tp["right"][inn]
+    cross = 6 * (rU[a] * rV[b] + rU[b] * rV[a])          # B blocks of the children
+    own = (2 * 2 * (rU[a] + rU[b]) * w * np.maximum(rU[a], rV[b])
+           + 4 * w * (rU[a] + rU[b]) * np.maximum(rU[inn], 1)
+           + 4 * w * (rV[a] + rV[b]) * np.maximum(rV[inn], 1))
+    f += int(cross.sum()) + int(own[nonroot[inn]].sum())
     return f
 
 
 def mult_flops(tree, P):
     """hss_mult counter of hss.py:329-357 for P rows."""
-    rU, rV = tree.ranks()
-    f = 0
-    for nd in tree.nodes:
-        i = nd.index
-        if i == tree.root:
-            continue
-        m = nd.hi - nd.lo
-        if nd.is_leaf:
-            f += gemm_flops(P, m, int(rU[i]))
-            f += gemm_flops(P, m, m) + gemm_flops(P, int(rV[i]), m)
-        else:
-            f += gemm_flops(P, int(rU[nd.left] + rU[nd.right]), int(rU[i]))
-            f += gemm_flops(P, int(rV[i]), int(rV[nd.left] + rV[nd.right]))
-        f += gemm_flops(P, int(rU[nd.sibling]), int(rV[i]))
-    return f
+    rU, rV = (np.asarray(r, dtype=np.int64) for r in tree.ranks())
+    tp = tree._topo
+    nonroot = np.ones(len(rU), dtype=bool)
+    nonroot[tree.root] = False
+    lf = tp["leaf"] & nonroot
+    m = tp["m"][lf]
+    f = int((m * rU[lf] + m * m + rV[lf] * m).sum())
+    inn = ~tp["leaf"] & nonroot
+    a, b = tp["left"][inn], tp["right"][inn]
+    f += int(((rU[a] + rU[b]) * rU[inn] + rV[inn] * (rV[a] + rV[b])).sum())
+    f += int((rU[tp["sib"][nonroot]] * rV[nonroot]).sum())
+    return 2 * P * f
 
 
 FLAG_TOL = 1e-12   # hss.py:117

@@ -267,3 +267,82 @@ def test_recursion_tree_arrays_match_the_recursive_definition():
                 part[nd["split"] - 1] -= abs(b[nd["split"] - 1])
                 part[nd["split"]] -= abs(b[nd["split"] - 1])
         assert np.array_equal(got.split_diagonal(a, b, 2), part)
+
+
+def test_tree_flop_counters_equal_the_per_node_definition():
+    """hss._construct_flops / hss.mult_flops (sums over node arrays) against the reference's
+    per-node accumulation (pkg/src/hsseig/hss.py:251-287, 329-357) on random trees."""
+    from paper_1510_04591_b200 import hss
+    from paper_1510_04591_b200.flops import cauchy_eval_flops, cpqr_flops, gemm_flops
+
+    class N:
+        pass
+
+    def loop_construct(tree, k, w):
+        rU, rV = tree.ranks()
+        f = 2 * (gemm_flops(k, k, w) + cauchy_eval_flops(k * k))
+        for nd in tree.nodes:
+            if nd.index == tree.root:
+                continue
+            if nd.left is None:
+                m = nd.hi - nd.lo
+                f += cauchy_eval_flops(m * m) + 2 * gemm_flops(m, m, w)
+                f += cpqr_flops(w, m, max(int(rU[nd.index]), 1)) + cpqr_flops(w, m, max(int(rV[nd.index]), 1))
+            else:
+                a, b = nd.left, nd.right
+                f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
+                f += 2 * gemm_flops(int(rU[a] + rU[b]), w, max(int(rU[a]), int(rV[b])))
+                f += cpqr_flops(w, int(rU[a] + rU[b]), max(int(rU[nd.index]), 1))
+                f += cpqr_flops(w, int(rV[a] + rV[b]), max(int(rV[nd.index]), 1))
+        rt = tree.nodes[tree.root]
+        return f + cauchy_eval_flops(int(rU[rt.left] * rV[rt.right]) + int(rU[rt.right] * rV[rt.left]))
+
+    def loop_mult(tree, P):
+        rU, rV = tree.ranks()
+        f = 0
+        for nd in tree.nodes:
+            i = nd.index
+            if i == tree.root:
+                continue
+            m = nd.hi - nd.lo
+            if nd.left is None:
+                f += gemm_flops(P, m, int(rU[i])) + gemm_flops(P, m, m) + gemm_flops(P, int(rV[i]), m)
+            else:
+                f += gemm_flops(P, int(rU[nd.left] + rU[nd.right]), int(rU[i]))
+                f += gemm_flops(P, int(rV[i]), int(rV[nd.left] + rV[nd.right]))
+            f += gemm_flops(P, int(rU[nd.sibling]), int(rV[i]))
+        return f
+
+    rng = np.random.default_rng(1)
+    for nl in [2, 3, 5, 8, 13, 256]:
+        nodes = []
+        bounds = np.concatenate([[0], np.cumsum(rng.integers(50, 200, nl))])
+
+        def rec(a, b):
+            n = N()
+            if b - a == 1:
+                n.lo, n.hi, n.left, n.right = int(bounds[a]), int(bounds[a + 1]), None, None
+            else:
+                h = (a + b) // 2
+                li, ri = rec(a, h), rec(h, b)
+                n.lo, n.hi, n.left, n.right = nodes[li].lo, nodes[ri].hi, li, ri
+                nodes[li].sibling, nodes[ri].sibling = ri, li
+            n.sibling = None
+            n.index = len(nodes)
+            nodes.append(n)
+            return n.index
+
+        t = N()
+        t.root = rec(0, nl)
+        t.nodes = nodes
+        rU = rng.integers(0, 90, len(nodes)).astype(np.int32)
+        rV = rng.integers(0, 90, len(nodes)).astype(np.int32)
+        t.ranks = lambda: (rU, rV)
+        t._topo = {"leaf": np.array([n.left is None for n in nodes]),
+                   "left": np.array([-1 if n.left is None else n.left for n in nodes]),
+                   "right": np.array([-1 if n.right is None else n.right for n in nodes]),
+                   "sib": np.array([-1 if n.sibling is None else n.sibling for n in nodes]),
+                   "m": np.array([n.hi - n.lo for n in nodes])}
+        k = int(bounds[-1])
+        assert hss._construct_flops(t, k, 88) == loop_construct(t, k, 88)
+        assert hss.mult_flops(t, 32768) == loop_mult(t, 32768)
