@@ -720,6 +720,11 @@ def _group(ranks):
     return _GROUPS[key]
 
 
+def _split_a(a, b, nodes, max_depth):
+    """Diagonal with the split modifications of the recursion nodes above max_depth."""
+    return nodes.split_diagonal(a, b, max_depth)
+
+
 def _gather_padded(vec, length, group, device):
     """All-gather 1-D tensors of up to `length` entries (padded); returns the list."""
     world = dist.get_world_size(group)
