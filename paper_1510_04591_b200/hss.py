@@ -550,25 +550,22 @@ def srrsc_hss_construct(A, partition, cap, tol=DEFAULT_ID_TOL, flops=None, finis
 def _srrsc_flops(tree, k):
     """Construction counter of oracle/srrsc_oracle.py: every elimination sweep evaluates the
     whole candidate block (6 per entry, cauchy.py:55 convention), p r^2 for the bases, and the
-    D / B entries."""
-    rU, rV = tree.ranks()
-    f = 0
-    for nd in tree.nodes:
-        if nd.index == tree.root:
-            a, b = nd.left, nd.right
-            f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
-            continue
-        ncomp = k - (nd.hi - nd.lo)
-        if nd.is_leaf:
-            m = nd.hi - nd.lo
-            f += cauchy_eval_flops(m * m)
-            ps = (m, m)
-        else:
-            a, b = nd.left, nd.right
-            f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
-            ps = (int(rU[a] + rU[b]), int(rV[a] + rV[b]))
-        for pc, r in zip(ps, (int(rU[nd.index]), int(rV[nd.index]))):
-            f += cauchy_eval_flops((r + 1) * pc * ncomp) + pc * r * r
+    D / B entries.  Summed over node arrays (see _construct_flops)."""
+    rU, rV = (np.asarray(r, dtype=np.int64) for r in tree.ranks())
+    tp = tree._topo
+    nonroot = np.ones(len(rU), dtype=bool)
+    nonroot[tree.root] = False
+    inn = ~tp["leaf"]
+    a, b = tp["left"][inn], tp["right"][inn]
+    f = int((6 * (rU[a] * rV[b] + rU[b] * rV[a])).sum())      # B blocks, the root's included
+    lf = tp["leaf"] & nonroot
+    f += int((6 * tp["m"][lf] * tp["m"][lf]).sum())            # D blocks
+    # candidate counts of the two sides: a leaf's own indices, an inner node's children's skeletons
+    pU, pV = tp["m"].copy(), tp["m"].copy()
+    pU[inn], pV[inn] = rU[a] + rU[b], rV[a] + rV[b]
+    ncomp = k - tp["m"]
+    for pc, r in ((pU, rU), (pV, rV)):
+        f += int((6 * (r + 1) * pc * ncomp + pc * r * r)[nonroot].sum())
     return f
 
 

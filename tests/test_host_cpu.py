@@ -313,6 +313,27 @@ def test_tree_flop_counters_equal_the_per_node_definition():
             f += gemm_flops(P, int(rU[nd.sibling]), int(rV[i]))
         return f
 
+    def loop_srrsc(tree, k):
+        rU, rV = tree.ranks()
+        f = 0
+        for nd in tree.nodes:
+            if nd.index == tree.root:
+                a, b = nd.left, nd.right
+                f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
+                continue
+            ncomp = k - (nd.hi - nd.lo)
+            if nd.left is None:
+                m = nd.hi - nd.lo
+                f += cauchy_eval_flops(m * m)
+                ps = (m, m)
+            else:
+                a, b = nd.left, nd.right
+                f += cauchy_eval_flops(int(rU[a] * rV[b]) + int(rU[b] * rV[a]))
+                ps = (int(rU[a] + rU[b]), int(rV[a] + rV[b]))
+            for pc, r in zip(ps, (int(rU[nd.index]), int(rV[nd.index]))):
+                f += cauchy_eval_flops((r + 1) * pc * ncomp) + pc * r * r
+        return f
+
     rng = np.random.default_rng(1)
     for nl in [2, 3, 5, 8, 13, 256]:
         nodes = []
@@ -346,3 +367,4 @@ def test_tree_flop_counters_equal_the_per_node_definition():
         k = int(bounds[-1])
         assert hss._construct_flops(t, k, 88) == loop_construct(t, k, 88)
         assert hss.mult_flops(t, 32768) == loop_mult(t, 32768)
+        assert hss._srrsc_flops(t, k) == loop_srrsc(t, k)
