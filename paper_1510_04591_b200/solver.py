@@ -534,6 +534,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             run_t, run_off, rot_tasks = np.zeros(1, np.int64), np.zeros(nm + 1, np.int64), 0
         st0 = np.zeros((nseg, 8), dtype=np.int64)
         st0[:, 1:4] = ks[:, None]
+        _mark("t_indexed", depth)
         (woff_d, wd_d, row_merge, csrc_d, coff_d, rot_d1, rot_d2, rot_d3, rot_d4, dk, zk,
          koff_d, seg_of, rho_d, st, t_woff, t_nv, t_qoff, t_tk, t_ldw, run_t_d, run_off_d,
          kperm_d) = (
@@ -543,6 +544,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             .add(koff).add(np.repeat(np.arange(nseg), ks), np.int32)
             .add(rho_eff[segs], np.float64).add(st0).add(woff[segs]).add(nvs).add(qoff[segs])
             .add(tk, np.int32).add(ldw[segs]).add(run_t).add(run_off).add(kperm).send())
+        _mark("t_packed", depth)
         W = torch.empty(max(int(woff[-1]), 2), **f64)
         prof = GLUE_PROFILE
         if prof is not None:
@@ -565,6 +567,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         if prof is not None:
             ev_g[1].record()
             prof.append(("assemble", ev_g[0], ev_g[1], gbytes))
+        _mark("t_assembled", depth)
         Qk = torch.empty(max(int(qoff[-1]), 1), **f64)
         hss_m = set(np.flatnonzero(hss_q).tolist())
         seg_iters = np.zeros(nseg, dtype=np.int64)
@@ -588,6 +591,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             # statuses and roots (sync 2) go to pinned host buffers right behind the secular
             # stage; the dense updates are queued before the host waits, so the host-side
             # checks, HSS set-up and final ordering below overlap them on the device
+            _mark("t_secular", depth)
             st_pin = torch.empty((nseg, 8), dtype=torch.int64, pin_memory=True)
             lam_pin = torch.empty(ktot, dtype=torch.float64, pin_memory=True)
             st_pin.copy_(st.view(nseg, 8), non_blocking=True)

@@ -37,6 +37,14 @@ for tag, d, t in tr:
 print(f"returned {1e3 * (t_ret - t0):.2f} ms, device drained {1e3 * (t_end - t0):.2f} ms")
 if os.environ.get("HSSEIG_TRACE_SUMMARY"):
     sys.exit(0)
+if os.environ.get("HSSEIG_TRACE_FINE"):   # every mark of a depth, as deltas (ms) from the previous one
+    seq = {}
+    for tag, d, t in tr:
+        seq.setdefault(d, []).append((tag, t))
+    for d in sorted(seq, reverse=True):
+        ev = seq[d]
+        print(d, " ".join(f"{b[0]}+{(b[1] - a[1]) * 1e3:.2f}" for a, b in zip(ev, ev[1:])))
+    sys.exit(0)
 print("depth  begin  rows_wait  deflate  to_queued  roots_wait  to_gather_queued")
 for d in sorted(by, reverse=True):
     b = by[d]
