@@ -607,15 +607,18 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                 # materialised-panel updates straight through the C ABI (one generator struct
                 # and one shared workspace; cauchy.py's right_multiply_into per merge costs
                 # ~70 us of host time each at config 5)
-                kmax, kmin, nmax = int(ks[big].max()), int(ks[big].min()), int(nvs[big].max())
+                kmax, kmin = int(ks[big].max()), int(ks[big].min())
                 # the depth's updates run on up to DENSE_STREAMS side streams, each with its
                 # own slice of the workspace (sized for the widest merge)
                 nst = min(DENSE_STREAMS, len(big))
-                nw = nst * ((int(lib.hsseig_dense_update_halves_work_doubles(
-                    nmax, kmax, max(128, DENSE_PANEL_BYTES // (8 * kmin)))) + 63) & ~31)
-                pw = torch.empty(nw, **f64)
-                # the shared workspace is sized for the widest merge; a merge may use all of it
                 mb = segs[big]
+                # a slice holds a merge's two compacted row blocks (exact sizes: about half of
+                # rows x k) and the panel workspace of the widest merge
+                kt, kbn = np.maximum(ka_b, 1), np.maximum(kept[mb] - kb_b, 1)
+                halves = int((n1[mb] * (kt + (kt & 1)) + n2[mb] * (kbn + (kbn & 1))).max()) + 64
+                nw = nst * ((halves + int(lib.hsseig_dense_update_work_doubles(
+                    kmax, max(128, DENSE_PANEL_BYTES // (8 * kmin)))) + 63) & ~31)
+                pw = torch.empty(nw, **f64)
                 rec9 = np.ascontiguousarray(np.stack(
                     [woff[mb], ldw[mb], nv[mb], n1[mb], koff[big], kept[mb], ka_b, kb_b, qoff[mb]], 1),
                     dtype=np.int64)
