@@ -101,8 +101,16 @@ class _Pack:
         for p, q in zip(self.parts, offs):
             hv[q:q + p.nbytes] = p.view(np.uint8)
         dev = host.to("cuda", non_blocking=True)
-        return [dev[q:q + max(p.nbytes, p.itemsize)].view(self._T[p.dtype])
-                for p, q in zip(self.parts, offs)]
+        # one reinterpretation of the staging buffer per element type; a part is then a slice
+        typed = {}
+        out = []
+        for p, q in zip(self.parts, offs):
+            t = typed.get(p.dtype)
+            if t is None:
+                t = typed[p.dtype] = dev.view(self._T[p.dtype])
+            e = q // p.itemsize
+            out.append(t[e:e + max(p.size, 1)])
+        return out
 
 
 def _base_cases_flat(a_mod, b, lo, hi, stream):
@@ -421,7 +429,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         nv = n1 + n2
         roff = np.concatenate([[0], np.cumsum(nv)]).astype(np.int64)
         nrows = int(roff[-1])
-        rm = np.repeat(np.arange(nm), nv)
+        rm = np.repeat(np.arange(nm, dtype=np.int32), nv)      # row -> merge (device table)
         # the merges of a depth cover increasing disjoint index ranges; one contiguous range
         # when the depth holds no leaf (a slice instead of a 65536-entry index array)
         if nm == 1 or np.array_equal(lo_m[1:], hi_a[ms[:-1]]):
@@ -541,7 +549,7 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             _Pack().add(woff).add(wd).add(rm, np.int32).add(csrc[:int(coff[-1])]).add(coff)
             .add(ca[:nrot]).add(cb[:nrot]).add(rc[:nrot], np.float64)
             .add(rs[:nrot], np.float64).add(d_out[kidx], np.float64).add(z_out[kidx], np.float64)
-            .add(koff).add(np.repeat(np.arange(nseg), ks), np.int32)
+            .add(koff).add(np.repeat(np.arange(nseg, dtype=np.int32), ks), np.int32)
             .add(rho_eff[segs], np.float64).add(st0).add(woff[segs]).add(nvs).add(qoff[segs])
             .add(tk, np.int32).add(ldw[segs]).add(run_t).add(run_off).add(kperm).send())
         _mark("t_packed", depth)
