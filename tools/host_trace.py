@@ -20,6 +20,8 @@ elif cfg_id == "3":
     T, cfg = hb.gen_kac(n), hb.SolverConfig(rank_eps=1e-13)
 else:
     T, cfg = hb.gen_config5(n, 0), hb.SolverConfig(rank_eps=1e-13)
+if os.environ.get("HSSEIG_METHOD"):
+    cfg.method = os.environ["HSSEIG_METHOD"]
 for _ in range(2):
     hb.adc_solve(T, cfg)
 torch.cuda.synchronize()

@@ -1,0 +1,8 @@
+export PYTHONUNBUFFERED=1 HSSEIG_TRACE_SUMMARY=1
+for st in 8 16 32; do
+echo "== HSS streams $st"
+export HSSEIG_HSS_STREAMS=$st
+HSSEIG_METHOD=adc-srrsc python tools/host_trace.py 2 10000
+HSSEIG_METHOD=adc-rand python tools/host_trace.py 2 10000
+python tools/host_trace.py 3 20000
+done
