@@ -7,6 +7,7 @@ the structured product (Algorithm 3) run in libhsseig_b200.so
 out by hsseig_tree_layout; per-node views are materialised only on request.
 """
 import ctypes
+import functools
 import math
 import os
 from dataclasses import dataclass, field
@@ -164,6 +165,42 @@ class HssNode:
     cols_local = property(lambda self: self._sel("cloc", 1))
 
 
+@functools.lru_cache(maxsize=256)
+def _topology(n_leaves):
+    """Postorder structure of the balanced tree over n_leaves leaves (hss.py:188-214): children,
+    parent, sibling (-1 where absent), level, first / last leaf of every node, position of a
+    leaf among the leaves.  Depends on the leaf count only, so it is built once per count."""
+    left, right, level, first, last = [], [], [], [], []
+
+    def rec(a, b, lv):
+        if b - a == 1:
+            li = ri = -1
+        else:
+            h = (a + b) // 2
+            li, ri = rec(a, h, lv + 1), rec(h, b, lv + 1)
+        left.append(li)
+        right.append(ri)
+        level.append(lv)
+        first.append(a)
+        last.append(b - 1)
+        return len(left) - 1
+
+    rec(0, n_leaves, 0)
+    left, right = np.array(left, dtype=np.int64), np.array(right, dtype=np.int64)
+    n = len(left)
+    parent, sib = np.full(n, -1, dtype=np.int64), np.full(n, -1, dtype=np.int64)
+    inner = np.flatnonzero(left >= 0)
+    parent[left[inner]] = parent[right[inner]] = inner
+    sib[left[inner]], sib[right[inner]] = right[inner], left[inner]
+    leaf = left < 0
+    tp = {"leaf": leaf, "left": left, "right": right, "sib": sib, "parent": parent,
+          "level": np.array(level, dtype=np.int64), "first": np.array(first, dtype=np.int64),
+          "last": np.array(last, dtype=np.int64), "leaf_pos": np.cumsum(leaf) - 1}
+    for v in tp.values():
+        v.setflags(write=False)
+    return tp
+
+
 @dataclass
 class HssTree:
     """Device-resident HSS tree (hss.py:177-185) with reference-compatible node views."""
@@ -196,46 +233,32 @@ class HssTree:
 
     # -- topology (postorder, identical to hss.py:188-214) --
     def _build_nodes(self):
-        nodes = []
-        ranges = self.partition.ranges
+        """Node arrays from the cached structure of a tree with this many leaves; the
+        per-node HssNode views are only materialised on request (`nodes`): the solver's hot
+        path (one tree per HSS merge) needs the arrays alone."""
+        tp = _topology(self.partition.n_leaves)
+        b = np.asarray(self._bounds, dtype=np.int64)
+        lo, hi = b[tp["first"]], b[tp["last"] + 1]
+        self._topo = dict(tp, lo=lo, hi=hi, m=hi - lo)
+        self._leaf_pos = tp["leaf_pos"]
+        self._nodes = None
 
-        def rec(a, b, level):
-            if b - a == 1:
-                nodes.append(HssNode(self, len(nodes), level, *ranges[a]))
-                return len(nodes) - 1
-            h = (a + b) // 2
-            li, ri = rec(a, h, level + 1), rec(h, b, level + 1)
-            nd = HssNode(self, len(nodes), level, nodes[li].lo, nodes[ri].hi)
-            nd.left, nd.right = li, ri
-            nodes.append(nd)
-            me = len(nodes) - 1
-            nodes[li].parent = nodes[ri].parent = me
-            nodes[li].sibling, nodes[ri].sibling = ri, li
-            return me
-
-        rec(0, self.partition.n_leaves, 0)
-        self.nodes = nodes
-        # topology as arrays (children / sibling = -1 where absent) for the flop counters
-        self._topo = {
-            "leaf": np.array([nd.left < 0 for nd in nodes], dtype=bool),
-            "left": np.array([nd.left for nd in nodes], dtype=np.int64),
-            "right": np.array([nd.right for nd in nodes], dtype=np.int64),
-            "sib": np.array([nd.sibling for nd in nodes], dtype=np.int64),
-            "m": np.array([nd.hi - nd.lo for nd in nodes], dtype=np.int64),
-        }
-        self._leaf_pos = {}
-        pos = 0
-        for nd in nodes:
-            if nd.is_leaf:
-                self._leaf_pos[nd.index] = pos
-                pos += 1
+    @property
+    def nodes(self):
+        if self._nodes is None:
+            tp = self._topo
+            nodes = []
+            for i in range(len(tp["left"])):
+                nd = HssNode(self, i, int(tp["level"][i]), int(tp["lo"][i]), int(tp["hi"][i]))
+                nd.left, nd.right = int(tp["left"][i]), int(tp["right"][i])
+                nd.parent, nd.sibling = int(tp["parent"][i]), int(tp["sib"][i])
+                nodes.append(nd)
+            self._nodes = nodes
+        return self._nodes
 
     def levels(self):
-        depth = max(n.level for n in self.nodes)
-        by = [[] for _ in range(depth + 1)]
-        for n in self.nodes:
-            by[n.level].append(n.index)
-        return by
+        lv = self._topo["level"]
+        return [np.flatnonzero(lv == l).tolist() for l in range(int(lv.max()) + 1)]
 
     # -- device views --
     def _view(self, attr, dtype, count, offset_elems):
@@ -273,7 +296,7 @@ class HssTree:
         j = self._leaf_pos[node]
         n = drows * mm
         flat = self._view("D", torch.float64, n, j * n)
-        m = self.nodes[node].hi - self.nodes[node].lo
+        m = int(self._topo["m"][node])
         return flat.view(drows, mm)[1:m + 1, :m].cpu().numpy().copy()
 
 
@@ -611,8 +634,9 @@ def finish_construct(tree, flops=None, pre=None):
     tree._ranks = (blob[24 * nn:28 * nn].view(np.int32).copy(), blob[28 * nn:32 * nn].view(np.int32).copy())
     tree.flags = []
     # the reference appends flags in processing order: deepest level first, postorder within
-    for idx in sorted((n.index for n in tree.nodes if n.index != tree.root),
-                      key=lambda i: -tree.nodes[i].level):
+    flagged = np.flatnonzero(fl.any(axis=1))
+    flagged = flagged[flagged != tree.root]
+    for idx in sorted(flagged.tolist(), key=lambda i: -int(tree._topo["level"][i])):
         if fl[idx, 0]:
             tree.flags.append((idx, "row", float(rr[idx])))
         if fl[idx, 1]:
