@@ -814,6 +814,21 @@ def run_ours(args):
             line["same_n"] = same_n
         if world == 1 and not args.no_eigh:
             line["eigh"] = eigh_lines(peak_hbm())
+            # the metric's HBM half: the full solve's HBM-bound kernel (final column gather of
+            # every recursion depth of config 5) against the measured copy bandwidth
+            gl = (line["eigh"].get("cfg5_N65536") or {}).get("glue_hbm") or {}
+            ga = gl.get("gather")
+            if ga and ga.get("GB_s"):
+                pk = peak_hbm()
+                line["roofline_hbm"] = {
+                    "bound": "hbm", "kernel": "wave_gather_kernel<2, 4> (config 5, all depths)",
+                    "achieved": ga["GB_s"], "peak": pk, "unit": "GB/s",
+                    "frac": ga["GB_s"] / pk if pk else None, "traffic": None,
+                    "algorithmic": "8 B written per output entry + 8 B read per kept entry and per "
+                                   "own-child deflated entry (the other child's are structural zeros) "
+                                   "/ CUDA-event time of the gather launches; ncu DRAM bytes per depth "
+                                   "in profiles/round2_hbm_kernels.txt",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "unavailable"}
         if adc1 is not None:
             line["config4_adc1"] = adc1
         if world > 1 and eigh_d is not None:
