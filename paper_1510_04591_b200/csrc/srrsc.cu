@@ -33,6 +33,7 @@
 // sweep (the O(k^2 r) per merge the paper quotes for ADC1).
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -866,9 +867,18 @@ static int build_srrsc_levels(const hsseig_gen* gen, double tol, int32_t max_ran
       const int rc = launch_genB(g, T, lev, j0, cnt, s);
       if (rc) return rc;
     }
-    // columns of a node split over a cluster so that a level fills about four CTAs per SM
+    // columns of a node split over a cluster so that a level fills about four CTAs per SM,
+    // but never thinner than ~cols_per_cta columns a CTA: a small system (the mid-depth
+    // merges of a full solve: k of a few hundred to a few thousand) gains nothing from 16
+    // CTAs of a few dozen columns each and pays their cluster barrier every elimination step,
+    // and its whole-GPU grids kept the independent merges of a depth (one stream each) from
+    // running side by side
+    static const int cols_per_cta = getenv("HSSEIG_SRRSC_COLS_PER_CTA")
+                                        ? std::max(1, atoi(getenv("HSSEIG_SRRSC_COLS_PER_CTA")))
+                                        : 1024;
     int cl = 1;
-    while (cl < kSrMaxCluster && 2 * cnt * cl * 2 <= slots) cl *= 2;
+    while (cl < kSrMaxCluster && 2 * cnt * cl * 2 <= slots && (int64_t)cl * cols_per_cta < T.k)
+      cl *= 2;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(cnt * cl, 2);
     lc.blockDim = dim3(kSrThreads);

@@ -1,0 +1,5 @@
+export PYTHONUNBUFFERED=1
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/bj.txt 2>&1; tail -2 gpurun_out/bj.txt
+HSSEIG_TRACE_SUMMARY=1 HSSEIG_METHOD=adc-srrsc python tools/host_trace.py 2 10000
+HSSEIG_TRACE_SUMMARY=1 HSSEIG_METHOD=adc-srrsc python tools/host_trace.py 3 20000
+HSSEIG_TRACE_SUMMARY=1 python tools/host_trace.py 3 20000
