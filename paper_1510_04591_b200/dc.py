@@ -12,7 +12,7 @@ import os
 import numpy as np
 import torch
 
-from .cauchy import CauchyEvecMatrix
+from .cauchy import DENSE_PANEL_MIN_K, CauchyEvecMatrix
 from .flops import FlopCounter, cauchy_eval_flops, gemm_flops
 from .hss import (DEFAULT_ID_TOL, MAX_WIDTH, build_partition, draw_omegas, estimate_rank,
                   finish_construct, hss_matmul_right, rand_hss_construct, srrsc_hss_construct)
@@ -205,6 +205,9 @@ class HssJob:
     gamma: np.ndarray
     mu: np.ndarray
     out: object
+    # (n1, perm, ka, kb) when Q is the kept block of blockdiag(Q1, Q2): a dense fallback then
+    # skips the structural zeros (CauchyEvecMatrix.right_multiply_halves_into)
+    halves: object = None
 
 
 _SIDE = []
@@ -233,6 +236,12 @@ def update_vectors_hss_many(jobs, cfg, max_streams=None):
     def dense_fallback(j):
         j.record.used_hss = False
         j.record.fell_back = True
+        if j.halves is not None and j.C.k >= DENSE_PANEL_MIN_K:
+            # same count as update_vectors_dense (the reference's, dc.py:132-138)
+            j.flops.update_dense += cauchy_eval_flops(j.C.k * j.C.k) + gemm_flops(j.Q.shape[0], j.C.k, j.C.k)
+            n1, perm, ka, kb = j.halves
+            j.C.right_multiply_halves_into(j.Q, n1, perm, ka, kb, out=j.out)
+            return
         j.out.copy_(update_vectors_dense(j.Q, j.C, flops=j.flops))
 
     live = []

@@ -502,7 +502,14 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
         # blockdiag(Q1, Q2) above / below the split see only their own child's kept columns
         # and the ones a deflation rotation mixed: hsseig_dense_update_halves)
         big = np.flatnonzero(big_q)
+        # ... also for the HSS merges wide enough for the panel path, whose flagged trees fall
+        # back to the dense update (the classification rides along; the panel loop below
+        # takes the first len(big) entries)
+        hss_p = np.flatnonzero(hss_q & (ks >= DENSE_PANEL_MIN_K))
+        nbig = len(big)
+        big = np.concatenate([big, hss_p])
         kperm, ka_b, kb_b = np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, np.int64)
+        boff = np.zeros(1, np.int64)
         if len(big):
             mb, kb_ = segs[big], ks[big]
             boff = np.concatenate([[0], np.cumsum(kb_)]).astype(np.int64)
@@ -519,6 +526,10 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
             kperm = np.lexsort((cls, seg_b)) - boff[seg_b]       # stable within a merge
             ka_b = np.add.reduceat((cls <= 1).astype(np.int64), boff[:-1])
             kb_b = np.add.reduceat((cls == 0).astype(np.int64), boff[:-1])
+        # K orders of the HSS merges (host side, handed to their jobs), then the panel merges alone
+        hss_halves = {int(q): (kperm[boff[nbig + i]:boff[nbig + i + 1]], int(ka_b[nbig + i]), int(kb_b[nbig + i]))
+                      for i, q in enumerate(hss_p.tolist())}
+        big, kperm, ka_b, kb_b = big[:nbig], kperm[:boff[nbig]], ka_b[:nbig], kb_b[:nbig]
         mt, nt = -(-nvs[small] // bm), -(-ks[small] // bn)
         cnt = mt * nt
         tk = np.empty((int(cnt.sum()), 3), dtype=np.int32)
@@ -667,7 +678,8 @@ def solve_subtree(a_mod, b, nodes, sub, cfg):
                     Wm = W[int(woff[m]):int(woff[m + 1])].view(n, int(ldw[m]))
                     jobs.append(HssJob(Q=Wm[:, :k], C=C, seed=[cfg.seed, mid], flops=FlopCounter(),
                                        record=rec_, d=dk_h[sl], gamma=gam_h[sl], mu=mu_h[sl],
-                                       out=Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k)))
+                                       out=Qk[int(qoff[m]):int(qoff[m + 1])].view(n, k),
+                                       halves=(int(n1[m]),) + hss_halves[q] if q in hss_halves else None))
                 update_vectors_hss_many(jobs, cfg)
                 for j in jobs:
                     j.record.flops = j.flops.as_dict()
