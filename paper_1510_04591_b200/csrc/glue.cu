@@ -366,13 +366,19 @@ __device__ __forceinline__ void gather_row(const GatherSrc& g, int m, int64_t ro
   }
 }
 
+// resident blocks per SM the gather is compiled for: 4 (64 registers, no spills) measured
+// against 5 / 6 / 8 (48 / 40 / 32 registers with 8 / 48 / 80 bytes of spills): config-5
+// gathers 20.2 ms against 21.1 / 25.2 / 30.0 ms
+#ifndef HSSEIG_GATHER_MINB
+#define HSSEIG_GATHER_MINB 4
+#endif
 // ROWS rows per block and CPT columns per thread and iteration: rows of one merge share the
 // column descriptors, so the descriptor array (8 B per output entry) is read once per ROWS
 // rows, and a thread keeps ROWS * CPT independent source loads in flight and stores
 // 16 bytes at a time when the output rows are 16-byte aligned (n even).  Groups that
 // straddle a merge boundary fall back to row by row.
 template <int ROWS, int CPT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, HSSEIG_GATHER_MINB)
     wave_gather_kernel(GatherSrc g, const int32_t* __restrict__ row_merge,
                        double* __restrict__ out, const int64_t* __restrict__ ooff, int64_t nrows) {
   static_assert(CPT % 2 == 0, "columns per thread come in 16-byte pairs");
