@@ -198,6 +198,20 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ part, int nsplit
   out[row * ldo + col] = s;
 }
 
+// The same reduction for rows [r0, r0 + nr) of the partials only (same order of the splits, so
+// the sums are bit-identical): the rows of one panel chunk, reduced as soon as its product is done.
+__global__ void splitk_reduce_rows_kernel(const double* __restrict__ part, int nsplit,
+                                          int64_t split_stride, int64_t r0, int64_t nr, int w,
+                                          int64_t ldp, double* __restrict__ out, int64_t ldo) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nr * w) return;
+  int64_t row = r0 + e / w;
+  int col = (int)(e % w);
+  double s = 0.0;
+  for (int t = 0; t < nsplit; ++t) s += part[(int64_t)t * split_stride + row * ldp + col];
+  out[row * ldo + col] = s;
+}
+
 // out = Qb @ C with B-operand tiles of C generated in shared memory; one BM x BN tile.
 template <class T>
 __device__ __forceinline__ void dense_update_tile(const double* __restrict__ Q, int64_t ldq,
@@ -605,13 +619,15 @@ __global__ void mat_jobs_kernel(TJob* __restrict__ jobs, MatPlan p, int64_t k, i
 // drives one device per process)
 struct PanelSide {
   cudaStream_t s = nullptr;
-  cudaEvent_t in = nullptr, gen[kPanelChunks] = {};
+  cudaEvent_t in = nullptr, gen[kPanelChunks] = {}, ygemm[kPanelChunks] = {}, yred = nullptr;
   bool ok = false;
   PanelSide() {
     ok = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
-         cudaEventCreateWithFlags(&in, cudaEventDisableTiming) == cudaSuccess;
+         cudaEventCreateWithFlags(&in, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&yred, cudaEventDisableTiming) == cudaSuccess;
     for (int c = 0; ok && c < kPanelChunks; ++c)
-      ok = cudaEventCreateWithFlags(&gen[c], cudaEventDisableTiming) == cudaSuccess;
+      ok = cudaEventCreateWithFlags(&gen[c], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&ygemm[c], cudaEventDisableTiming) == cudaSuccess;
   }
 };
 
@@ -633,6 +649,7 @@ static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom,
   const Operand none{nullptr, 0, 0, 0};
   const int njobs = (int)(p.nch * p.sy + p.sz * p.tiles_n);
   int rc;
+  bool y_early = false;
   // Omega^T and the job tables (built on the device)
   dim3 gt((unsigned)((k + 31) / 32), (unsigned)((w + 31) / 32));
   transpose_kernel<<<gt, dim3(32, 8), 0, s>>>(om, ldom, k, w, omt, p.kld);
@@ -672,8 +689,22 @@ static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom,
                                   none, none, none};
       if ((rc = tma_jobs_gemm(0, w, ops, dmaps + c, djobs + c * p.sy, (int)p.sy, r1 - r0, s)))
         return rc;
+      if (!peY) {
+        // this chunk's rows of Y are reduced on the side stream (idle once the panel is
+        // written) under the DMMA-bound Z^T products instead of after them
+        if (cudaEventRecord(side.ygemm[c], s) != cudaSuccess ||
+            cudaStreamWaitEvent(side.s, side.ygemm[c], 0) != cudaSuccess)
+          return HSSEIG_ERR_CUDA;
+        splitk_reduce_rows_kernel<<<(unsigned)(((r1 - r0) * w + 255) / 256), 256, 0, side.s>>>(
+            pY, (int)p.sy, nr * p.ldp, r0, r1 - r0, w, p.ldp, Y, ldy);
+        HSS_CHECK_LAUNCH();
+        y_early = true;
+      }
       if ((rc = z_gemm(c))) return rc;
     }
+    if (y_early && (cudaEventRecord(side.yred, side.s) != cudaSuccess ||
+                    cudaStreamWaitEvent(s, side.yred, 0) != cudaSuccess))
+      return HSSEIG_ERR_CUDA;
   } else {
     gen_panel_rows(g, row0, nr, k, C1, p.kld, s);
     HSS_CHECK_LAUNCH();
@@ -694,8 +725,10 @@ static int launch_sample_mat(const CauchyGen& g, const double* om, int64_t ldom,
     HSS_CHECK_LAUNCH();
     return HSSEIG_OK;
   }
-  splitk_reduce_kernel<<<rb, 256, 0, s>>>(pY, (int)p.sy, nr, w, p.ldp, Y, ldy);
-  HSS_CHECK_LAUNCH();
+  if (!y_early) {
+    splitk_reduce_kernel<<<rb, 256, 0, s>>>(pY, (int)p.sy, nr, w, p.ldp, Y, ldy);
+    HSS_CHECK_LAUNCH();
+  }
   splitk_reduce_t_kernel<<<rb, 256, 0, s>>>(pZ, (int)p.sz, nr, w, p.nld, w * p.nld, Z, ldy);
   HSS_CHECK_LAUNCH();
   return HSSEIG_OK;
